@@ -1,0 +1,363 @@
+// bf16 x bf16 -> fp32 GEMM on the 5th-generation tensor cores (sm_100a).
+//
+// Persistent, warp-specialised kernel, one CTA per SM:
+//   warp 0   : TMA producer (cp.async.bulk.tensor, 128B swizzle) into a STAGES-deep smem ring
+//   warp 1   : TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=256, K=16 per instruction)
+//   warps 2-5: epilogue — tcgen05.ld from a double-buffered TMEM accumulator, fused elementwise op,
+//              vectorised stores. Double buffering lets tile i's epilogue overlap tile i+1's MMAs.
+// Both operands may be K-major or MN-major (UMMA descriptor major bits), so the six FFN GEMMs of the
+// MEFT layer read their operands in place with no transposes.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace meft_dev {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BK = 64;  // one 128-byte swizzle atom of bf16
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;
+constexpr int B_BYTES = BN * BK * 2;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int NUM_THREADS = 192;
+constexpr int TMEM_COLS = 512;  // 2 accumulators x 256 fp32 columns
+constexpr int GROUP_M = 16;     // raster: 16 M-tiles share each resident B panel in L2
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+
+struct KArgs {
+    int M, N, K;
+    int tiles_m, tiles_n, num_kb;
+    int epi;
+    int accumulate;
+    void* c;
+    long long ldc;
+    const uint16_t* mask;
+    long long ldm;
+    const int32_t* row_idx;
+};
+
+__device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int& m_blk, int& n_blk) {
+    const int group_size = GROUP_M * tiles_n;
+    const int g = tile / group_size;
+    const int first_m = g * GROUP_M;
+    const int gm = min(GROUP_M, tiles_m - first_m);
+    const int local = tile - g * group_size;
+    m_blk = first_m + local % gm;
+    n_blk = local / gm;
+}
+
+__device__ __forceinline__ void epilogue_chunk(const KArgs& a, int m, int n, const uint32_t (&r)[32]) {
+    const int cnt = min(32, a.N - n);
+    switch (a.epi) {
+        case EPI_STORE_F32:
+        case EPI_ROWS_ADD_F32: {
+            const long long row = (a.epi == EPI_ROWS_ADD_F32) ? (long long)a.row_idx[m] : (long long)m;
+            const bool acc = a.accumulate || a.epi == EPI_ROWS_ADD_F32;
+            float* c = reinterpret_cast<float*>(a.c) + row * a.ldc + n;
+            if (cnt == 32) {
+                float4* c4 = reinterpret_cast<float4*>(c);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    float4 v = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                           __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+                    if (acc) {
+                        const float4 o = c4[j];
+                        v.x += o.x;
+                        v.y += o.y;
+                        v.z += o.z;
+                        v.w += o.w;
+                    }
+                    c4[j] = v;
+                }
+            } else {
+                for (int j = 0; j < cnt; ++j) c[j] = (acc ? c[j] : 0.0f) + __uint_as_float(r[j]);
+            }
+            break;
+        }
+        case EPI_RELU_BF16: {
+            uint16_t* c = reinterpret_cast<uint16_t*>(a.c) + (long long)m * a.ldc + n;
+            if (cnt == 32) {
+                uint4* c4 = reinterpret_cast<uint4*>(c);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    uint4 v;
+                    v.x = pack_bf16x2(relu_bf16_bits(__uint_as_float(r[8 * j + 0])),
+                                      relu_bf16_bits(__uint_as_float(r[8 * j + 1])));
+                    v.y = pack_bf16x2(relu_bf16_bits(__uint_as_float(r[8 * j + 2])),
+                                      relu_bf16_bits(__uint_as_float(r[8 * j + 3])));
+                    v.z = pack_bf16x2(relu_bf16_bits(__uint_as_float(r[8 * j + 4])),
+                                      relu_bf16_bits(__uint_as_float(r[8 * j + 5])));
+                    v.w = pack_bf16x2(relu_bf16_bits(__uint_as_float(r[8 * j + 6])),
+                                      relu_bf16_bits(__uint_as_float(r[8 * j + 7])));
+                    c4[j] = v;
+                }
+            } else {
+                for (int j = 0; j < cnt; ++j) c[j] = relu_bf16_bits(__uint_as_float(r[j]));
+            }
+            break;
+        }
+        case EPI_MASK_BF16: {
+            uint16_t* c = reinterpret_cast<uint16_t*>(a.c) + (long long)m * a.ldc + n;
+            const uint16_t* mk = a.mask + (long long)m * a.ldm + n;
+            if (cnt == 32) {
+                uint4* c4 = reinterpret_cast<uint4*>(c);
+                const uint4* m4 = reinterpret_cast<const uint4*>(mk);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint4 mm = m4[j];
+                    const uint32_t mw[4] = {mm.x, mm.y, mm.z, mm.w};
+                    uint32_t o[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint16_t lo = (mw[q] & 0xFFFFu) ? f32_to_bf16_bits(__uint_as_float(r[8 * j + 2 * q])) : 0;
+                        const uint16_t hi = (mw[q] >> 16) ? f32_to_bf16_bits(__uint_as_float(r[8 * j + 2 * q + 1])) : 0;
+                        o[q] = pack_bf16x2(lo, hi);
+                    }
+                    c4[j] = make_uint4(o[0], o[1], o[2], o[3]);
+                }
+            } else {
+                for (int j = 0; j < cnt; ++j) c[j] = mk[j] ? f32_to_bf16_bits(__uint_as_float(r[j])) : 0;
+            }
+            break;
+        }
+        default:
+            break;
+    }
+}
+
+template <bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    k_gemm_bf16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const KArgs args) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(tfull + b, 1);
+            mbar_init(tempty + b, 4);  // one arrive per epilogue warp
+        }
+        fence_barrier_init();
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int num_tiles = args.tiles_m * args.tiles_n;
+
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                int mb, nb;
+                tile_coords(tile, args.tiles_m, args.tiles_n, mb, nb);
+                const int m0 = mb * BM, n0 = nb * BN;
+                for (int kb = 0; kb < args.num_kb; ++kb) {
+                    mbar_wait(empty + stage, phase ^ 1);
+                    uint8_t* sa = smem + stage * STAGE_BYTES;
+                    uint8_t* sb = sa + A_BYTES;
+                    mbar_arrive_expect_tx(full + stage, STAGE_BYTES);
+                    const int k0 = kb * BK;
+                    if (!A_MN) {
+                        tma_load_2d(sa, &tmA, full + stage, k0, m0);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < BM / 64; ++j) tma_load_2d(sa + j * 8192, &tmA, full + stage, m0 + 64 * j, k0);
+                    }
+                    if (!B_MN) {
+                        tma_load_2d(sb, &tmB, full + stage, k0, n0);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 8192, &tmB, full + stage, n0 + 64 * j, k0);
+                    }
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, A_MN, B_MN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+                const int acc = it & 1;
+                const uint32_t aphase = (it >> 1) & 1;
+                mbar_wait(tempty + acc, aphase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (int kb = 0; kb < args.num_kb; ++kb) {
+                    mbar_wait(full + stage, phase);
+                    tc_fence_after();
+                    const uint32_t a_addr = smem_u32(smem + stage * STAGE_BYTES);
+                    const uint32_t b_addr = a_addr + A_BYTES;
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k) {
+                        // K-major SW128: a 16-element K step is +32 B inside the swizzle atom, SBO = 8 rows * 128 B.
+                        // MN-major SW128: a 16-row K step is +2048 B; LBO = 8 KB between 64-wide MN chunks.
+                        const uint64_t ad = A_MN ? umma_desc_sw128(a_addr + k * 2048, 8192, 1024)
+                                                 : umma_desc_sw128(a_addr + k * 32, 16, 1024);
+                        const uint64_t bd = B_MN ? umma_desc_sw128(b_addr + k * 2048, 8192, 1024)
+                                                 : umma_desc_sw128(b_addr + k * 32, 16, 1024);
+                        umma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                    }
+                    umma_commit(empty + stage);  // frees this smem stage once the MMAs above retire
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                umma_commit(tfull + acc);  // accumulator ready for the epilogue
+            }
+        }
+    } else {
+        // ------------------------------------------------ epilogue (warps 2..5)
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        int it = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+            int mb, nb;
+            tile_coords(tile, args.tiles_m, args.tiles_n, mb, nb);
+            const int acc = it & 1;
+            const uint32_t aphase = (it >> 1) & 1;
+            mbar_wait(tfull + acc, aphase);
+            tc_fence_after();
+            const int m = mb * BM + q * 32 + lane;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t r[32];
+                tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c * 32, r);
+                tmem_ld_wait();
+                const int n = nb * BN + c * 32;
+                if (m < args.M && n < args.N) epilogue_chunk(args, m, n, r);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty + acc);
+        }
+    }
+
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, TMEM_COLS);
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    if (!fn) throw MeftError(6, "cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+// 2-D bf16 tensor map: `inner` contiguous elements per row, `outer` rows of pitch ld elements.
+CUtensorMap make_map(const void* base, int64_t inner, int64_t outer, int64_t ld, uint32_t box_inner,
+                     uint32_t box_outer) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {cuuint64_t(inner), cuuint64_t(outer)};
+    cuuint64_t strides[1] = {cuuint64_t(ld) * 2};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw MeftError(6, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+    return m;
+}
+
+template <bool A_MN, bool B_MN>
+void launch(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const KArgs& args) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        MEFT_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_bf16<A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             SMEM_BYTES));
+        attr_set = true;
+    }
+    const int tiles = args.tiles_m * args.tiles_n;
+    const int grid = std::min(tiles, num_sms());
+    k_gemm_bf16<A_MN, B_MN><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ta, tb, args);
+    check_launch("k_gemm_bf16");
+}
+
+}  // namespace
+
+void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOperand& A, const GemmOperand& B,
+               const GemmEpilogue& epi) {
+    if (M <= 0 || N <= 0) return;
+    if (K <= 0) throw MeftError(2, "gemm_bf16: K must be positive");
+    if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) throw MeftError(1, "gemm_bf16: dimension too large");
+    auto aligned16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    if (!aligned16(A.ptr) || !aligned16(B.ptr) || (A.ld % 8) || (B.ld % 8))
+        throw MeftError(2, "gemm_bf16: operands need 16-byte aligned base and leading dimension % 8 == 0");
+    if (epi.kind == EPI_STORE_F32 || epi.kind == EPI_ROWS_ADD_F32) {
+        if (!aligned16(epi.c) || (epi.ldc % 4)) throw MeftError(2, "gemm_bf16: f32 output alignment");
+    } else {
+        if (!aligned16(epi.c) || (epi.ldc % 8)) throw MeftError(2, "gemm_bf16: bf16 output alignment");
+    }
+    if (epi.kind == EPI_MASK_BF16 && (!aligned16(epi.mask) || (epi.ldm % 8)))
+        throw MeftError(2, "gemm_bf16: mask alignment");
+
+    const CUtensorMap ta = A.mn_major ? make_map(A.ptr, M, K, A.ld, 64, 64) : make_map(A.ptr, K, M, A.ld, 64, BM);
+    const CUtensorMap tb = B.mn_major ? make_map(B.ptr, N, K, B.ld, 64, 64) : make_map(B.ptr, K, N, B.ld, 64, BN);
+
+    KArgs args;
+    args.M = int(M);
+    args.N = int(N);
+    args.K = int(K);
+    args.tiles_m = int(ceil_div(M, BM));
+    args.tiles_n = int(ceil_div(N, BN));
+    args.num_kb = int(ceil_div(K, BK));
+    args.epi = epi.kind;
+    args.accumulate = epi.accumulate ? 1 : 0;
+    args.c = epi.c;
+    args.ldc = epi.ldc;
+    args.mask = static_cast<const uint16_t*>(epi.mask);
+    args.ldm = epi.ldm;
+    args.row_idx = epi.row_idx;
+
+    if (!A.mn_major && !B.mn_major)
+        launch<false, false>(st, ta, tb, args);
+    else if (!A.mn_major && B.mn_major)
+        launch<false, true>(st, ta, tb, args);
+    else if (A.mn_major && B.mn_major)
+        launch<true, true>(st, ta, tb, args);
+    else
+        launch<true, false>(st, ta, tb, args);
+}
+
+}  // namespace meft_dev

@@ -1,0 +1,60 @@
+// Internal host-side launch API of the sm_100a kernels (not part of the C-ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace meft_dev {
+
+// ---------------------------------------------------------------- bf16 tcgen05 GEMM
+// C[M x N] (epilogue) of  sum_k A(m,k) * B(n,k)  with bf16 operands and fp32 accumulation in TMEM.
+//   K-major operand:  X(i,k) = ptr[i*ld + k]
+//   MN-major operand: X(i,k) = ptr[k*ld + i]
+struct GemmOperand {
+    const void* ptr;
+    int64_t ld;     // elements
+    bool mn_major;
+};
+
+enum GemmEpi : int {
+    EPI_STORE_F32 = 0,     // C f32 [M x ldc] = acc            (or += acc when accumulate)
+    EPI_RELU_BF16 = 1,     // C bf16 = relu(acc), positive never rounds to zero
+    EPI_MASK_BF16 = 2,     // C bf16 = mask(m,n) > 0 ? acc : 0 ; mask bf16 [M x ldm]
+    EPI_ROWS_ADD_F32 = 3,  // C f32: C[row_idx[m]*ldc + n] += acc (row_idx unique -> no atomics)
+};
+
+struct GemmEpilogue {
+    int kind = EPI_STORE_F32;
+    void* c = nullptr;
+    int64_t ldc = 0;
+    const void* mask = nullptr;
+    int64_t ldm = 0;
+    const int32_t* row_idx = nullptr;
+    bool accumulate = false;
+};
+
+void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOperand& A, const GemmOperand& B,
+               const GemmEpilogue& epi);
+
+// ---------------------------------------------------------------- fp64 SIMT GEMM (API-fidelity path)
+// C[M x N] = sum_k A(m,k) * B(k,n) over ascending k (fma chain, reference kernels.cpp:34-41), with
+// arbitrary element strides so transposed views need no copies.
+struct DOperand {
+    const double* ptr;
+    int64_t s0, s1;  // element strides for (row, col) of the logical matrix
+};
+enum DEpi : int {
+    DEPI_STORE = 0,        // C = acc
+    DEPI_ADD = 1,          // C += acc
+    DEPI_RELU_STORE = 2,   // C = relu(acc)   (unused by the shim; kept for symmetry)
+    DEPI_MASK_STORE = 3,   // C = mask(m,n) > 0 ? acc : 0   (mask f64 with strides)
+};
+void dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, const DOperand& A, const DOperand& B, double* C,
+           int64_t ldc, int epi, const DOperand* mask);
+
+// ---------------------------------------------------------------- exact selection (fp64 scores)
+// dtype: 0 = f64 inputs (unfused mul/add, reference's compiled dot()), 2 = bf16 inputs (exact products:
+// fma == unfused).
+void score_rows(cudaStream_t st, int dtype, const void* h, int64_t T, int64_t d, const void* w, int64_t rows,
+                double* scores);  // scores[T x rows] = dot(h_t, w_row)
+}  // namespace meft_dev

@@ -1,0 +1,490 @@
+// Key-Experts selection with reference-exact indices (experts.cpp:47-117, adapter.cpp:42-84).
+//
+// Scores are fp64 dot products accumulated strictly left to right, one chain per (token, row), exactly
+// the reference's dot() (kernels.hpp:37-41). With bf16 inputs every product a_k*b_k is exact in fp64,
+// so fma(a,b,acc) == fl(acc + fl(a*b)) and the fast DFMA path is bit-identical to the reference; with
+// fp64 inputs the kernel uses __dmul_rn/__dadd_rn (no contraction). Rankings use the reference's total
+// order (score desc via operator>/!=, so -0.0 == +0.0; then lower index), and every list is emitted
+// ascending, so selected experts, per-token neurons and the union match the CPU reference bit for bit.
+//
+// Pipeline:
+//   router scores [T x N]  -> warp top-kk per token (tau, ascending) -> bucket (token,slot) by expert
+//   -> grouped key scoring [T x kk*E] (each expert's key rows are read once per 64-token tile)
+//   -> CTA bitonic top-K per token over (score, global index) -> per-token list + union bitmap
+//   -> ordered compaction of the bitmap into the ascending union S.
+#include <algorithm>
+#include <cfloat>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "select.h"
+
+namespace meft_dev {
+namespace {
+
+constexpr int ST = 64;   // score tile: entries
+constexpr int SC = 64;   // score tile: key rows
+constexpr int SK = 16;   // k chunk
+constexpr int STHREADS = 256;
+
+__device__ __forceinline__ double ld_in(const double* p, int64_t i) { return p[i]; }
+__device__ __forceinline__ double ld_in(const uint16_t* p, int64_t i) { return double(bf16_bits_to_f32(p[i])); }
+
+template <bool EXACT_PRODUCTS>
+__device__ __forceinline__ double mac(double acc, double a, double b) {
+    if (EXACT_PRODUCTS) return fma(a, b, acc);  // a*b exact => identical to the unfused form
+    return __dadd_rn(acc, __dmul_rn(a, b));
+}
+
+// The reference's comparator (experts.cpp:36-41): a precedes b.
+__device__ __forceinline__ bool beats(double sa, int ia, double sb, int ib) {
+    if (sa != sb) return sa > sb;
+    return ia < ib;
+}
+
+// Grouped score tile. Group g = blockIdx.z-resolved: W rows [g*ncols, (g+1)*ncols), entry list
+// entries[off[g] .. off[g+1]) (entry e -> token e / ent_div, output row e). entries == nullptr means
+// one group of `n_entries` identity entries.
+template <typename In, bool EXACT>
+__global__ void __launch_bounds__(STHREADS)
+    k_score(const In* __restrict__ h, int d, const In* __restrict__ w, int ncols, const int32_t* __restrict__ entries,
+            const int32_t* __restrict__ off, const int32_t* __restrict__ tile_off, int n_groups, int n_entries,
+            int ent_div, double* __restrict__ out) {
+    __shared__ double sh[SK][ST + 1];
+    __shared__ double sw[SK][SC + 1];
+    __shared__ int s_tok[ST];
+    __shared__ int s_row[ST];
+
+    int g = 0, tile_in_group = blockIdx.x, ebeg = 0, ecount = n_entries;
+    if (entries) {
+        // locate the group owning this tile (tile_off is the exclusive scan of per-group tile counts)
+        int lo = 0, hi = n_groups;  // find last g with tile_off[g] <= blockIdx.x
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (tile_off[mid] <= (int)blockIdx.x) lo = mid; else hi = mid;
+        }
+        g = lo;
+        if ((int)blockIdx.x >= tile_off[n_groups]) return;
+        tile_in_group = blockIdx.x - tile_off[g];
+        ebeg = off[g];
+        ecount = off[g + 1] - off[g];
+    }
+    const int e0 = tile_in_group * ST;
+    if (e0 >= ecount) return;
+    const int c0 = blockIdx.y * SC;
+    if (c0 >= ncols) return;
+    const int tid = threadIdx.x;
+    if (tid < ST) {
+        const int e = e0 + tid;
+        if (e < ecount) {
+            const int ent = entries ? entries[ebeg + e] : e;
+            s_row[tid] = ent;
+            s_tok[tid] = ent / ent_div;
+        } else {
+            s_row[tid] = -1;
+            s_tok[tid] = 0;
+        }
+    }
+    __syncthreads();
+
+    const int tx = tid & 15, ty = tid >> 4;  // 16 x 16 threads, 4 x 4 outputs each
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+
+    const int64_t wrow0 = int64_t(g) * ncols + c0;
+    for (int k0 = 0; k0 < d; k0 += SK) {
+        const int kn = min(SK, d - k0);
+        for (int i = tid; i < ST * SK; i += STHREADS) {
+            const int r = i / SK, kk = i % SK;
+            sh[kk][r] = (kk < kn) ? ld_in(h, int64_t(s_tok[r]) * d + k0 + kk) : 0.0;
+        }
+        for (int i = tid; i < SC * SK; i += STHREADS) {
+            const int c = i / SK, kk = i % SK;
+            sw[kk][c] = (kk < kn && c0 + c < ncols) ? ld_in(w, (wrow0 + c) * d + k0 + kk) : 0.0;
+        }
+        __syncthreads();
+        for (int kk = 0; kk < kn; ++kk) {  // strictly ascending k
+            double a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = sh[kk][ty * 4 + i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = sw[kk][tx * 4 + j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = mac<EXACT>(acc[i][j], a[i], b[j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int r = ty * 4 + i;
+        const int row = s_row[r];
+        if (row < 0) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int c = c0 + tx * 4 + j;
+            if (c < ncols) out[int64_t(row) * ncols + c] = acc[i][j];
+        }
+    }
+}
+
+// Warp per token: top-kk experts of the router scores (experts.cpp:30-45), written ascending.
+__global__ void k_topk_experts(const double* __restrict__ scores, int T, int N, int kk, int32_t* __restrict__ tau,
+                               int32_t* __restrict__ counts) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= T) return;
+    const double* s = scores + int64_t(warp) * N;
+    int32_t* out = tau + int64_t(warp) * kk;
+    double ps = 0.0;
+    int pi = -1;  // previous pick; -1 = none yet
+    for (int r = 0; r < kk; ++r) {
+        double bs = -DBL_MAX;
+        int bi = -1;
+        for (int i = lane; i < N; i += 32) {
+            const double v = s[i];
+            if (pi >= 0 && !beats(ps, pi, v, i)) continue;  // already taken (ranked at or above prev)
+            if (bi < 0 || beats(v, i, bs, bi)) {
+                bs = v;
+                bi = i;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double os = __shfl_xor_sync(0xffffffffu, bs, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (oi >= 0 && (bi < 0 || beats(os, oi, bs, bi))) {
+                bs = os;
+                bi = oi;
+            }
+        }
+        ps = bs;
+        pi = bi;
+        if (lane == 0) out[r] = bi;
+    }
+    __syncwarp();
+    if (lane == 0) {
+        for (int a = 1; a < kk; ++a) {  // insertion sort ascending (kk is small)
+            const int v = out[a];
+            int b = a - 1;
+            while (b >= 0 && out[b] > v) {
+                out[b + 1] = out[b];
+                --b;
+            }
+            out[b + 1] = v;
+        }
+        if (counts)
+            for (int a = 0; a < kk; ++a) atomicAdd(&counts[out[a]], 1);
+    }
+}
+
+// Single CTA: off = exclusive scan(counts), tile_off = exclusive scan(ceil(counts/ST)), cursor = 0.
+__global__ void k_bucket_scan(const int32_t* __restrict__ counts, int N, int32_t* __restrict__ off,
+                              int32_t* __restrict__ tile_off, int32_t* __restrict__ cursor) {
+    __shared__ int s_run, s_trun;
+    if (threadIdx.x == 0) {
+        s_run = 0;
+        s_trun = 0;
+    }
+    __syncthreads();
+    for (int base = 0; base < N; base += blockDim.x) {
+        const int i = base + threadIdx.x;
+        const int c = i < N ? counts[i] : 0;
+        const int tcount = (c + ST - 1) / ST;
+        // block-wide inclusive scan via warp scans
+        int v = c, tv = tcount;
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int x = __shfl_up_sync(0xffffffffu, v, o);
+            const int tx = __shfl_up_sync(0xffffffffu, tv, o);
+            if (lane >= o) {
+                v += x;
+                tv += tx;
+            }
+        }
+        __shared__ int ws[32], wts[32];
+        if (lane == 31) {
+            ws[wid] = v;
+            wts[wid] = tv;
+        }
+        __syncthreads();
+        if (wid == 0) {
+            const int nw = blockDim.x >> 5;
+            int a = lane < nw ? ws[lane] : 0, b = lane < nw ? wts[lane] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int x = __shfl_up_sync(0xffffffffu, a, o);
+                const int y = __shfl_up_sync(0xffffffffu, b, o);
+                if (lane >= o) {
+                    a += x;
+                    b += y;
+                }
+            }
+            ws[lane] = a;
+            wts[lane] = b;
+        }
+        __syncthreads();
+        const int wpre = wid > 0 ? ws[wid - 1] : 0, wtpre = wid > 0 ? wts[wid - 1] : 0;
+        if (i < N) {
+            off[i] = s_run + wpre + v - c;
+            tile_off[i] = s_trun + wtpre + tv - tcount;
+            cursor[i] = 0;
+        }
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) {
+            s_run += wpre + v;
+            s_trun += wtpre + tv;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        off[N] = s_run;
+        tile_off[N] = s_trun;
+    }
+}
+
+__global__ void k_bucket_fill(const int32_t* __restrict__ tau, int T, int kk, const int32_t* __restrict__ off,
+                              int32_t* __restrict__ cursor, int32_t* __restrict__ entries) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= T * kk) return;
+    const int e = tau[i];
+    const int pos = atomicAdd(&cursor[e], 1);
+    entries[off[e] + pos] = i;  // i = t*kk + slot
+}
+
+// CTA per token: bitonic sort of the C candidates by the reference order, keep `take`, emit ascending.
+__global__ void k_topk_neurons(const double* __restrict__ cand, const int32_t* __restrict__ tau, int kk, int E,
+                               int C, int P2, int take, int TP2, int32_t* __restrict__ per_token,
+                               uint8_t* __restrict__ flags) {
+    extern __shared__ uint8_t sm[];
+    double* ks = reinterpret_cast<double*>(sm);
+    int* is = reinterpret_cast<int*>(ks + P2);
+    const int t = blockIdx.x;
+    const double* c = cand + int64_t(t) * C;
+    for (int i = threadIdx.x; i < P2; i += blockDim.x) {
+        if (i < C) {
+            const int slot = i / E, j = i - slot * E;
+            ks[i] = c[i];
+            is[i] = (tau ? tau[int64_t(t) * kk + slot] : 0) * E + j;
+        } else {
+            ks[i] = -DBL_MAX;
+            is[i] = INT32_MAX;
+        }
+    }
+    __syncthreads();
+    for (int k = 2; k <= P2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < P2; i += blockDim.x) {
+                const int p = i ^ j;
+                if (p > i) {
+                    const double a = ks[i], b = ks[p];
+                    const int ia = is[i], ib = is[p];
+                    const bool first = (i & k) == 0;  // this half in "precedes" order
+                    bool sw;
+                    if (ia == INT32_MAX || ib == INT32_MAX)
+                        sw = first ? (ia == INT32_MAX && ib != INT32_MAX) : (ib == INT32_MAX && ia != INT32_MAX);
+                    else
+                        sw = first ? beats(b, ib, a, ia) : beats(a, ia, b, ib);
+                    if (sw) {
+                        ks[i] = b;
+                        ks[p] = a;
+                        is[i] = ib;
+                        is[p] = ia;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // the first `take` entries are the selection; sort their indices ascending (reuse ks storage as ints)
+    int* sel = reinterpret_cast<int*>(ks);
+    for (int i = threadIdx.x; i < TP2; i += blockDim.x) sel[i] = (i < take) ? is[i] : INT32_MAX;
+    __syncthreads();
+    for (int k = 2; k <= TP2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < TP2; i += blockDim.x) {
+                const int p = i ^ j;
+                if (p > i) {
+                    const int a = sel[i], b = sel[p];
+                    const bool up = (i & k) == 0;
+                    if (up ? (a > b) : (a < b)) {
+                        sel[i] = b;
+                        sel[p] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = threadIdx.x; i < take; i += blockDim.x) {
+        const int v = sel[i];
+        per_token[int64_t(t) * take + i] = v;
+        flags[v] = 1;
+    }
+}
+
+// Ordered compaction of the union bitmap (experts.cpp:109-115): pass 1 counts per 1024-block.
+__global__ void k_flag_count(const uint8_t* __restrict__ flags, int M, int32_t* __restrict__ bcount) {
+    const int i = blockIdx.x * 1024 + threadIdx.x;
+    const int f = (i < M) ? (flags[i] != 0) : 0;
+    const int c = __syncthreads_count(f);
+    if (threadIdx.x == 0) bcount[blockIdx.x] = c;
+}
+
+__global__ void k_scan_blocks(int32_t* __restrict__ bcount, int nb, int32_t* __restrict__ total) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        int run = 0;
+        for (int b = 0; b < nb; ++b) {
+            const int c = bcount[b];
+            bcount[b] = run;
+            run += c;
+        }
+        *total = run;
+    }
+}
+
+__global__ void k_flag_write(const uint8_t* __restrict__ flags, int M, const int32_t* __restrict__ boff,
+                             int32_t* __restrict__ out) {
+    __shared__ int wsum[32];
+    const int i = blockIdx.x * 1024 + threadIdx.x;
+    const int f = (i < M) ? (flags[i] != 0) : 0;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) wsum[wid] = __popc(bal);
+    __syncthreads();
+    if (wid == 0) {
+        int v = wsum[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int x = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += x;
+        }
+        wsum[lane] = v - wsum[lane];  // exclusive
+    }
+    __syncthreads();
+    if (f) out[boff[blockIdx.x] + wsum[wid] + __popc(bal & ((1u << lane) - 1u))] = i;
+}
+
+int next_pow2(int x) {
+    int p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+template <typename In, bool EXACT>
+void launch_score(cudaStream_t st, const void* h, int d, const void* w, int ncols, const int32_t* entries,
+                  const int32_t* off, const int32_t* tile_off, int n_groups, int grid_x, int n_entries, int ent_div,
+                  double* out) {
+    dim3 grid(grid_x, (ncols + SC - 1) / SC, 1);
+    k_score<In, EXACT><<<grid, STHREADS, 0, st>>>(static_cast<const In*>(h), d, static_cast<const In*>(w), ncols,
+                                                  entries, off, tile_off, n_groups, n_entries, ent_div, out);
+    check_launch("k_score");
+}
+
+void score_dispatch(cudaStream_t st, int dtype, const void* h, int d, const void* w, int ncols,
+                    const int32_t* entries, const int32_t* off, const int32_t* tile_off, int n_groups, int grid_x,
+                    int n_entries, int ent_div, double* out) {
+    if (dtype == 2)
+        launch_score<uint16_t, true>(st, h, d, w, ncols, entries, off, tile_off, n_groups, grid_x, n_entries, ent_div,
+                                     out);
+    else
+        launch_score<double, false>(st, h, d, w, ncols, entries, off, tile_off, n_groups, grid_x, n_entries, ent_div,
+                                    out);
+}
+
+}  // namespace
+
+void score_rows(cudaStream_t st, int dtype, const void* h, int64_t T, int64_t d, const void* w, int64_t rows,
+                double* scores) {
+    if (T <= 0 || rows <= 0) return;
+    score_dispatch(st, dtype, h, int(d), w, int(rows), nullptr, nullptr, nullptr, 1, int((T + ST - 1) / ST), int(T),
+                   1, scores);
+}
+
+size_t select_workspace_bytes(int64_t T, int64_t M, int64_t N, int64_t kk_eff) {
+    const int64_t E = M / N;
+    size_t b = 0;
+    auto add = [&](size_t x) { b += (x + 255) & ~size_t(255); };
+    add(T * N * 8);             // router scores
+    add(T * kk_eff * 4);        // tau (internal copy)
+    add(T * kk_eff * E * 8);    // candidate scores
+    add(T * kk_eff * 4);        // entries
+    add((N + 1) * 4 * 4);       // counts, off, tile_off, cursor
+    add(M);                     // union flags
+    add(((M + 1023) / 1024 + 1) * 4);  // block offsets
+    return b;
+}
+
+void ke_select_device(cudaStream_t st, int dtype, const void* h, const void* w_g, const void* keys, int64_t T,
+                      int64_t d, int64_t M, int64_t N, int64_t kk_eff, int64_t take, void* ws, size_t ws_bytes,
+                      int32_t* per_token, int32_t* tau_out, int32_t* union_idx, int32_t* union_size) {
+    if (ws_bytes < select_workspace_bytes(T, M, N, kk_eff)) throw MeftError(6, "ke_select: workspace too small");
+    const int64_t E = M / N;
+    const int64_t C = kk_eff * E;
+    uint8_t* p = static_cast<uint8_t*>(ws);
+    auto take_buf = [&](size_t x) {
+        void* r = p;
+        p += (x + 255) & ~size_t(255);
+        return r;
+    };
+    double* rscores = static_cast<double*>(take_buf(T * N * 8));
+    int32_t* tau = static_cast<int32_t*>(take_buf(T * kk_eff * 4));
+    double* cand = static_cast<double*>(take_buf(T * C * 8));
+    int32_t* entries = static_cast<int32_t*>(take_buf(T * kk_eff * 4));
+    int32_t* counts = static_cast<int32_t*>(take_buf((N + 1) * 4 * 4));
+    int32_t* off = counts + (N + 1);
+    int32_t* tile_off = off + (N + 1);
+    int32_t* cursor = tile_off + (N + 1);
+    uint8_t* flags = static_cast<uint8_t*>(take_buf(M));
+    int32_t* boff = static_cast<int32_t*>(take_buf(((M + 1023) / 1024 + 1) * 4));
+
+    const int P2 = next_pow2(int(C));
+    const int TP2 = next_pow2(int(take));
+    const size_t topk_smem = size_t(P2) * 12;
+    if (topk_smem > 200 * 1024) throw MeftError(2, "ke_select: kk*E candidates per token exceed 16384 (unsupported)");
+
+    MEFT_CUDA_CHECK(cudaMemsetAsync(flags, 0, M, st));
+    if (N == 1) {
+        // single expert: every token sees all M keys (topk_select / ke_select with N=1)
+        MEFT_CUDA_CHECK(cudaMemsetAsync(tau, 0, T * 4, st));
+        score_rows(st, dtype, h, T, d, keys, M, cand);
+    } else {
+        score_rows(st, dtype, h, T, d, w_g, N, rscores);
+        MEFT_CUDA_CHECK(cudaMemsetAsync(counts, 0, N * 4, st));
+        k_topk_experts<<<int((T * 32 + 255) / 256), 256, 0, st>>>(rscores, int(T), int(N), int(kk_eff), tau, counts);
+        check_launch("k_topk_experts");
+        k_bucket_scan<<<1, 1024, 0, st>>>(counts, int(N), off, tile_off, cursor);
+        check_launch("k_bucket_scan");
+        k_bucket_fill<<<int((T * kk_eff + 255) / 256), 256, 0, st>>>(tau, int(T), int(kk_eff), off, cursor, entries);
+        check_launch("k_bucket_fill");
+        const int grid_x = int((T * kk_eff + ST - 1) / ST + N);  // >= total tiles over all groups
+        score_dispatch(st, dtype, h, int(d), keys, int(E), entries, off, tile_off, int(N), grid_x, int(T * kk_eff),
+                       int(kk_eff), cand);
+    }
+    static bool attr = false;
+    if (!attr) {
+        MEFT_CUDA_CHECK(cudaFuncSetAttribute(k_topk_neurons, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
+    k_topk_neurons<<<int(T), 512, topk_smem, st>>>(cand, tau, int(kk_eff), int(E), int(C), P2, int(take), TP2,
+                                                   per_token, flags);
+    check_launch("k_topk_neurons");
+    if (tau_out) MEFT_CUDA_CHECK(cudaMemcpyAsync(tau_out, tau, T * kk_eff * 4, cudaMemcpyDeviceToDevice, st));
+    const int nb = int((M + 1023) / 1024);
+    k_flag_count<<<nb, 1024, 0, st>>>(flags, int(M), boff);
+    k_scan_blocks<<<1, 32, 0, st>>>(boff, nb, union_size);
+    k_flag_write<<<nb, 1024, 0, st>>>(flags, int(M), boff, union_idx);
+    check_launch("k_flag_write");
+}
+
+void route_topk_device(cudaStream_t st, const double* scores, int64_t T, int64_t N, int64_t kk, int32_t* tau) {
+    k_topk_experts<<<int((T * 32 + 255) / 256), 256, 0, st>>>(scores, int(T), int(N), int(kk), tau, nullptr);
+    check_launch("k_topk_experts");
+}
+
+}  // namespace meft_dev

@@ -1,0 +1,22 @@
+// Internal selection launch API (see select.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace meft_dev {
+
+size_t select_workspace_bytes(int64_t T, int64_t M, int64_t N, int64_t kk_eff);
+
+// Key-Experts selection for T tokens against N experts of E = M/N keys each.
+// dtype 0: h/w_g/keys are f64; 2: bf16 bits. keys is neuron-major [M x d].
+// per_token [T x take] ascending rows; tau_out [T x kk_eff] (nullable); union_idx [M] ascending with the
+// device-side count in *union_size. N == 1 is the flat topk_select of adapter.cpp:42-84.
+void ke_select_device(cudaStream_t st, int dtype, const void* h, const void* w_g, const void* keys, int64_t T,
+                      int64_t d, int64_t M, int64_t N, int64_t kk_eff, int64_t take, void* ws, size_t ws_bytes,
+                      int32_t* per_token, int32_t* tau_out, int32_t* union_idx, int32_t* union_size);
+
+// select_experts (experts.cpp:30-45) over precomputed router scores [T x N].
+void route_topk_device(cudaStream_t st, const double* scores, int64_t T, int64_t N, int64_t kk, int32_t* tau);
+
+}  // namespace meft_dev
