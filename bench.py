@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""MEFT adapter layer benchmark (BASELINE.json metric: tokens/sec of fwd + bwd + sparse Adam).
+
+Workload (BASELINE.json configs[1]): LLaMA-7B-shape MEFT layer, d=4096, M=65536 key-value pairs, N=256
+experts, K=128 neurons/token, kk=4 experts/token, T=8192 tokens per step, bf16 compute, tables and optimizer
+state resident in HBM. One step = meft_ffn (ke_select -> fetch -> sparse FFN) -> sparse_backward ->
+scatter_grads -> sparse_adam_update (the reference trainer's per-layer sequence).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N>1 (torchrun, one rank per GPU): every rank runs its own layer replica on its own T tokens ("scaling":
+"weak"); the expert-sharded layer is described in DESIGN.md §6. Rank 0 prints one JSON line.
+The reference arm times the UNMODIFIED reference CPU implementation (oracle/_ref, built from
+/root/reference by oracle/Makefile) on the host cores, same config/metric, bounded per-step sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG = dict(workload="llama7b_meft_layer", d=4096, pairs=65536, experts=256, k=128, kk=4, tokens=8192, lr=1e-4)
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return PEAKS_FALLBACK, "fallback"
+
+
+# ----------------------------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """Samples SM clock and clock-event reasons via NVML in a background thread during timed regions."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device_index=0, period=0.01):
+        self.samples, self.reasons, self.period, self.ok = [], set(), period, False
+        self.max_mhz = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                try:
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except AttributeError:
+                    r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def start(self):
+        if self.ok:
+            self._stop.clear()
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+
+    def stop(self):
+        if self._t:
+            self._stop.set()
+            self._t.join()
+            self._t = None
+
+    def summary(self):
+        s = sorted(self.samples)
+        med = s[len(s) // 2] if s else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(s)}
+
+
+# ----------------------------------------------------------------------------------------------- reference arm
+
+def ref_sample_step_tokens():
+    return int(os.environ.get("MEFT_REF_SAMPLE_TOKENS", "64"))
+
+
+def run_reference_sample(steps, warmup, tokens, threads=None):
+    """Times ref_layer_step of the unmodified reference (oracle/_ref) at the cfg2 table shapes on `tokens`
+    tokens per step; returns (tokens/s, seconds per step, phase split, cores)."""
+    import numpy as np
+
+    from oracle import oracle as O
+
+    if not O.ref_available():
+        O.build()
+    R = O.ref()
+    cores = threads or os.cpu_count()
+    R.ref_set_threads(cores)
+    d, M, N = CFG["d"], CFG["pairs"], CFG["experts"]
+    st = O.RefStore(1, d, M, N, seed=1)
+    rng = np.random.default_rng(0x7001)
+    b = 1.0 / math.sqrt(d)
+    st.set(0, "w_b", rng.uniform(-b, b, size=(M, d)))
+    h = rng.uniform(-1, 1, size=(tokens, d))
+    g = rng.uniform(-1, 1, size=(tokens, d))
+    times, phases = [], np.zeros(6)
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        r = st.layer_step(0, h, g, CFG["kk"], CFG["k"], CFG["lr"], want_outputs=False)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            times.append(dt)
+            phases += r["phases"]
+    sec = sum(times) / len(times)
+    return tokens / sec, sec, (phases / max(1, len(times))).tolist(), cores
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return  # rank 0 alone runs the CPU reference; other ranks exit 0 without work
+    tokens = ref_sample_step_tokens()
+    try:
+        tps, sec, phases, cores = run_reference_sample(args.steps, args.warmup, tokens)
+    except Exception as e:  # pragma: no cover - surfaced as unavailable, never as a fake number
+        print(json.dumps({"impl": "reference", "unavailable": f"reference CPU run failed: {e}"}))
+        return
+    sample = (f"reference ref_layer_step (meft_ffn->sparse_backward->scatter_grads->sparse_adam_update) on the "
+              f"cfg2 tables d={CFG['d']} M={CFG['pairs']} N={CFG['experts']} K={CFG['k']} kk={CFG['kk']}, "
+              f"{tokens} tokens per step (bounded sample of the T={CFG['tokens']} step), fp64, OpenMP "
+              f"{cores} threads on {cpu_model()}")
+    line = {
+        "impl": "reference", "metric": "MEFT adapter layer tokens/sec (fwd+bwd+sparse update)", "value": tps,
+        "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": dict(workload=CFG["workload"], d=CFG["d"], pairs=CFG["pairs"], experts=CFG["experts"],
+                       k=CFG["k"], kk=CFG["kk"], tokens_per_step=tokens, global_tokens=CFG["tokens"]),
+        "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "reference", "sample": sample},
+        "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "phase_seconds": dict(zip(["select", "fetch", "forward", "backward", "scatter", "adam"], phases)),
+    }
+    print(json.dumps(line))
+
+
+# ----------------------------------------------------------------------------------------------- our arm
+
+def our_arm(args, rank, world, local_rank):
+    import torch
+
+    from paper_2406_04984_b200 import meft as G
+
+    dist = torch.distributed if world > 1 else None
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    d, M, N, K, kk, T, lr = (CFG[x] for x in ("d", "pairs", "experts", "k", "kk", "tokens", "lr"))
+
+    ctx = G.Context(local_rank)
+    store = G.Store(ctx, 1, d, M, N, G.STORE_MIXED)
+    store.init_reference(seed=1)  # HostStore::init tables (reference RNG streams 0x5000/0x5001)
+    gen = torch.Generator(device=dev).manual_seed(0x7001 + rank)
+    b = 1.0 / math.sqrt(d)
+    w_b = (torch.rand((M, d), generator=gen, device=dev) * 2 - 1) * b  # W_B ~ U(+-1/sqrt d)
+    store.tensor(0, "w_b").copy_(w_b)
+    store.tensor(0, "w_b_compute").copy_(w_b.to(torch.bfloat16))
+    del w_b
+    h = (torch.rand((T, d), generator=gen, device=dev) * 2 - 1).to(torch.bfloat16)
+    g = (torch.rand((T, d), generator=gen, device=dev) * 2 - 1).to(torch.bfloat16)
+    out = torch.empty((T, d), dtype=torch.float32, device=dev)
+    grad_h = torch.empty((T, d), dtype=torch.float32, device=dev)
+
+    def step():
+        return store.layer_step(0, h, g, kk, K, lr, out=out, grad_h=grad_h)
+
+    for _ in range(args.warmup):
+        info = step()
+    torch.cuda.synchronize()
+    ctx.read_timing()  # drop warm-up records
+    ctx.set_timing(True)
+
+    clocks = ClockSampler(local_rank)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev0.record()
+    launches = 0
+    usizes = []
+    for _ in range(args.steps):
+        info = step()
+        launches += info["gpu_launches"]
+        usizes.append(info["union_size"])
+    ev1.record()
+    torch.cuda.synchronize()
+    clocks.stop()
+    if dist:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    phases = ctx.read_timing()
+    ctx.set_timing(False)
+    if dist:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * T / (ms * 1e-3)
+
+    # ---- end to end through the C-ABI host entry point (pinned host buffers, copies inside the timed region)
+    h_host = h.cpu().pin_memory()
+    g_host = g.cpu().pin_memory()
+    out_host = torch.empty((T, d), dtype=torch.float32).pin_memory()
+    gh_host = torch.empty((T, d), dtype=torch.float32).pin_memory()
+    e2e_steps = max(3, min(args.steps, 10))
+    store.layer_step_host(0, h_host, g_host, kk, K, lr, out_host, gh_host)
+    if dist:
+        dist.barrier()
+    clocks.start()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        store.layer_step_host(0, h_host, g_host, kk, K, lr, out_host, gh_host)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    clocks.stop()
+    if dist:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = world * T / e2e_s
+
+    if rank != 0:
+        return
+
+    # ---- roofline of the dominant kernel (tcgen05 GEMM) from live CUDA-event phase timings
+    peaks, peak_src = load_peaks()
+    S = sum(usizes) / len(usizes)
+    gemm_ms = (phases["ffn_forward"][0] + phases["ffn_backward"][0]) / args.steps
+    gemm_launches = (phases["ffn_forward"][1] + phases["ffn_backward"][1]) / args.steps  # 6 per step
+    gemm_flops = 2.0 * T * d * S  # algorithmic flops of one of the six T x d x |S| GEMMs
+    gemm_tflops = gemm_flops / (gemm_ms / gemm_launches * 1e-3) / 1e12
+    tc_peak = peaks.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"])
+    hbm = peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"])
+    adam_bytes = 2 * S * d * 34.0  # read w,m,v,g + write w,m,v,g(=0) fp32 + bf16 copy, key and value rows
+    gather_bytes = 2 * S * d * 2 * 2.0
+    adam_ms = phases["adam"][0] / args.steps
+    gather_ms = phases["gather"][0] / args.steps
+    select_ms = phases["select"][0] / args.steps
+    # composite layer roofline: sum_k max(F_k / TC peak, B_k / HBM peak)
+    key_bytes = (M * d * 2) + T * d * 2
+    roof_ms = (6 * gemm_flops / (tc_peak * 1e12) + adam_bytes / (hbm * 1e9) + key_bytes / (hbm * 1e9)
+               + 2 * T * N * d / (tc_peak * 1e12)) * 1e3
+
+    cpu = None
+    if world == 1 and not args.skip_cpu_baseline:
+        tokens = ref_sample_step_tokens()
+        try:
+            tps, sec, cph, cores = run_reference_sample(1, 0, tokens)
+            cpu = {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "reference",
+                   "sample": f"unmodified reference ref_layer_step, cfg2 tables, {tokens} tokens, one step "
+                             f"({sec:.1f} s, fp64, OpenMP {cores} threads, {cpu_model()})"}
+        except Exception as e:
+            cpu = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"not run: {e}"}
+
+    line = {
+        "metric": "MEFT adapter layer tokens/sec (fwd+bwd+sparse update)",
+        "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (HostStore::init tables, uniform W_B/h/grad_out)",
+        "config": dict(workload=CFG["workload"], d=d, pairs=M, experts=N, k=K, kk=kk, tokens_per_gpu=T,
+                       global_tokens=T * world, parallelism=f"replica{world}", precision="bf16 compute, fp32 "
+                       "master/Adam state", l2="inputs larger than L2 (9.7 GB of tables per layer)",
+                       union_size=S),
+        "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": 2 * T * d * 2,
+                "d2h_bytes_per_step": 2 * T * d * 4, "ms_per_step": e2e_s * 1e3,
+                "path": "meft_layer_step_host (C ABI, pinned host buffers)"},
+        "roofline": {"bound": "tensor", "kernel": "k_gemm_bf16 (tcgen05 FFN GEMM)", "achieved": gemm_tflops,
+                     "peak": tc_peak, "unit": "TFLOP/s", "frac": gemm_tflops / tc_peak, "traffic": None,
+                     "peak_source": f"{peak_src} bf16_tflops_sustained",
+                     "per_launch": {"flops": gemm_flops, "ms": gemm_ms / gemm_launches}},
+        "layer_roofline": {"roofline_ms": roof_ms, "measured_ms": ms, "frac": roof_ms / ms},
+        "phases_ms": {"select": select_ms, "gather": gather_ms, "ffn_forward": phases["ffn_forward"][0] / args.steps,
+                      "ffn_backward": phases["ffn_backward"][0] / args.steps, "adam": adam_ms},
+        "hbm_kernels": {"adam_gbs": adam_bytes / (adam_ms * 1e-3) / 1e9 if adam_ms else None,
+                        "gather_gbs": gather_bytes / (gather_ms * 1e-3) / 1e9 if gather_ms else None,
+                        "peak_gbs": hbm},
+        "cpu_baseline": cpu,
+        "clocks": clocks.summary(),
+        "gpu_launches": launches,
+    }
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--skip-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 0)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+        return
+    if world > 1:
+        import torch
+
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        our_arm(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch
+
+            torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,236 @@
+/* meft_cuda.h — C ABI of libmeft_cuda.so, the B200 (sm_100a) implementation of the MEFT sparse
+ * Key-Experts adapter layer (arXiv 2406.04984).
+ *
+ * This is the thin layer under the drop-in C++ host API (include/meft/*.hpp, the same declarations as
+ * the reference's proj/include/meft/*.hpp). Every entry point names the reference function it replaces
+ * (paths relative to /root/reference/proj). Plain pointers and sizes only — no torch or CUDA types.
+ *
+ * Conventions
+ *  - All array arguments are DEVICE pointers unless a function name ends in _host.
+ *  - Work is enqueued on the context's stream; only calls that must return a host-visible size
+ *    synchronise (documented per function).
+ *  - Key tables are NEURON-MAJOR: row j of `keys` [pairs x d] is column j of the reference's w_a (d x r,
+ *    adapter.hpp:20-26). Values [pairs x d] are the reference's w_b rows unchanged. The *_host store
+ *    transfers convert from/to the reference layouts.
+ *  - Indices on device are int32 (pairs < 2^31); the drop-in shim widens to index_t (int64).
+ *  - Errors map to the reference's exception taxonomy: MEFT_E_SHAPE -> ShapeError,
+ *    MEFT_E_INVALID -> std::invalid_argument, MEFT_E_RANGE -> std::out_of_range (offending index via
+ *    meft_last_error_index), MEFT_E_LOGIC -> std::logic_error, MEFT_E_NONFINITE -> runtime_error("...non-finite...").
+ *  - One host thread per context at a time.
+ */
+#ifndef MEFT_CUDA_H
+#define MEFT_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum meft_status {
+    MEFT_OK = 0,
+    MEFT_E_SHAPE = 1,
+    MEFT_E_INVALID = 2,
+    MEFT_E_RANGE = 3,
+    MEFT_E_LOGIC = 4,
+    MEFT_E_NONFINITE = 5,
+    MEFT_E_CUDA = 6,
+    MEFT_E_NCCL = 7,
+    MEFT_E_OOM = 8
+} meft_status;
+
+typedef enum meft_dtype { MEFT_F64 = 0, MEFT_F32 = 1, MEFT_BF16 = 2 } meft_dtype;
+
+/* Store precision. F64 mirrors the reference HostStore bit for bit (API-fidelity mode); MIXED keeps fp32
+ * master weights / Adam moments / staging plus bf16 compute copies (the performance mode). */
+typedef enum meft_precision { MEFT_STORE_F64 = 0, MEFT_STORE_MIXED = 1 } meft_precision;
+
+/* Per-layer store tensors (HostLayer, memtier.hpp:90-106). Reference layouts for _host transfers:
+ * W_A, M_A, V_A, STAGE_A are d x r; W_B, M_B, V_B, STAGE_B are r x d; W_G is N x d; PAIR_STEP is int64[r];
+ * STAGED is int8[r]. On device every pair tensor is neuron-major [r x d]. *_COMPUTE are the bf16 copies the
+ * kernels read in MIXED mode. */
+typedef enum meft_tensor {
+    MEFT_T_W_A = 0,
+    MEFT_T_W_B = 1,
+    MEFT_T_W_G = 2,
+    MEFT_T_M_A = 3,
+    MEFT_T_V_A = 4,
+    MEFT_T_M_B = 5,
+    MEFT_T_V_B = 6,
+    MEFT_T_STAGE_A = 7,
+    MEFT_T_STAGE_B = 8,
+    MEFT_T_PAIR_STEP = 9,
+    MEFT_T_STAGED = 10,
+    MEFT_T_W_A_COMPUTE = 11,
+    MEFT_T_W_B_COMPUTE = 12,
+    MEFT_T_W_G_COMPUTE = 13
+} meft_tensor;
+
+typedef struct meft_ctx meft_ctx;
+typedef struct meft_store meft_store;
+
+/* ------------------------------------------------------------------ context, errors, memory */
+
+const char* meft_version(void);
+/* device = CUDA ordinal; stream = cudaStream_t or NULL (the context then owns a non-blocking stream). */
+meft_status meft_ctx_create(int device, void* stream, meft_ctx** out);
+void meft_ctx_destroy(meft_ctx* ctx);
+void* meft_ctx_stream(meft_ctx* ctx);
+const char* meft_last_error(const meft_ctx* ctx); /* ctx may be NULL: last error of this thread */
+int64_t meft_last_error_index(const meft_ctx* ctx);
+meft_status meft_synchronize(meft_ctx* ctx);
+
+/* Per-phase device timing of meft_layer_step with CUDA events recorded on the context stream:
+ * phase 0 selection (ke_select), 1 fetch (row gather), 2 FFN forward GEMMs, 3 FFN backward GEMMs (scatter
+ * fused into their epilogues), 4 sparse Adam (staged compaction + update). read_timing synchronises, returns
+ * the accumulated milliseconds and kernel launches per phase since the last read, and resets them. */
+meft_status meft_ctx_set_timing(meft_ctx* ctx, int enable);
+meft_status meft_ctx_read_timing(meft_ctx* ctx, double* ms5, int64_t* launches5);
+
+meft_status meft_device_alloc(meft_ctx* ctx, size_t bytes, void** out);
+meft_status meft_device_free(meft_ctx* ctx, void* ptr);
+meft_status meft_host_alloc(meft_ctx* ctx, size_t bytes, void** out); /* pinned */
+meft_status meft_host_free(meft_ctx* ctx, void* ptr);
+meft_status meft_copy_to_device(meft_ctx* ctx, void* dst, const void* src, size_t bytes); /* stream-ordered */
+meft_status meft_copy_to_host(meft_ctx* ctx, void* dst, const void* src, size_t bytes);   /* synchronises */
+meft_status meft_memset(meft_ctx* ctx, void* dst, int value, size_t bytes);
+meft_status meft_convert(meft_ctx* ctx, void* dst, meft_dtype dst_dt, const void* src, meft_dtype src_dt, int64_t n);
+
+/* ------------------------------------------------------------------ selection */
+
+/* Host-side clamp arithmetic of ke_select (experts.cpp:56-65) / topk_select (adapter.cpp:43-49):
+ * kk_eff = min(kk, N); take = min(k, kk_eff*(M/N)); *warn = 1 when the reference would call warn().
+ * Returns MEFT_E_INVALID for k < 1, kk < 1, N < 1 or N not dividing M (ExpertPartition::make). */
+meft_status meft_selection_shape(int64_t M, int64_t N, int64_t kk, int64_t k, int64_t* take, int64_t* kk_eff,
+                                 int* warn);
+
+/* route_scores (experts.cpp:21-28) for T tokens: scores[T x N] fp64, each a strict left-to-right dot. */
+meft_status meft_route_scores(meft_ctx* ctx, meft_dtype dt, const void* h, const void* w_g, int64_t T, int64_t d,
+                              int64_t N, double* scores);
+
+/* select_experts (experts.cpp:30-45) per row of scores[T x N]: tau[T x min(kk,N)] ascending. */
+meft_status meft_select_experts(meft_ctx* ctx, const double* scores, int64_t T, int64_t N, int64_t kk,
+                                int32_t* tau);
+
+/* ke_select (experts.cpp:47-117). dt in {F64, BF16} for h [T x d], w_g [N x d], keys [M x d].
+ * Outputs: per_token [T x take] (rows ascending), tau [T x kk_eff] (nullable), union_idx [M] ascending with
+ * its length in *union_size_dev (device int32). Bit-exact with the reference on identical inputs. */
+meft_status meft_ke_select(meft_ctx* ctx, meft_dtype dt, const void* h, const void* w_g, const void* keys,
+                           int64_t T, int64_t d, int64_t M, int64_t N, int64_t kk, int64_t k, int32_t* per_token,
+                           int32_t* tau, int32_t* union_idx, int32_t* union_size_dev);
+
+/* topk_select (adapter.cpp:42-84): flat top-K over all M keys; take = min(k, M). */
+meft_status meft_topk_select(meft_ctx* ctx, meft_dtype dt, const void* h, const void* keys, int64_t T, int64_t d,
+                             int64_t M, int64_t k, int32_t* per_token, int32_t* union_idx, int32_t* union_size_dev);
+
+/* ------------------------------------------------------------------ gather */
+
+/* gather_adapter (adapter.cpp:86-110) on neuron-major tables: keys_s[i] = keys[S[i]], values_s[i] =
+ * values[S[i]] (rows of d elements of dt). Validates S (synchronises): out of range -> MEFT_E_RANGE with the
+ * index, not strictly ascending -> MEFT_E_INVALID. */
+meft_status meft_gather_adapter(meft_ctx* ctx, meft_dtype dt, const void* keys, const void* values, int64_t M,
+                                int64_t d, const int32_t* S, int64_t s, void* keys_s, void* values_s);
+
+/* ------------------------------------------------------------------ sparse FFN (adapter half) */
+
+/* sparse_ffn_pa adapter term (adapter.cpp:122-126) for every token against all s selected pairs.
+ *   F64 : h [T x d] f64, keys_s/values_s [s x d] f64; z [T x ld_z] f64 receives h*w_a_k (the cache);
+ *         out [T x d] f64 = (accumulate ? out : 0) + ReLU(z) * w_b_k.
+ *   BF16: h, keys_s, values_s bf16; z receives bf16 ReLU(z) (a positive z never rounds to 0, so act > 0 is
+ *         exactly z > 0); out f32. ld_z % 8 == 0, d % 8 == 0.
+ */
+meft_status meft_ffn_forward(meft_ctx* ctx, meft_dtype dt, const void* h, const void* keys_s, const void* values_s,
+                             int64_t T, int64_t d, int64_t s, int64_t ld_z, void* z, void* out, int accumulate);
+
+/* sparse_backward adapter term (adapter.cpp:166-175), given the forward cache z:
+ *   masked = (grad_out * w_b_k^T) .* 1[z > 0]        (masked_ws [T x ld_z], dt)
+ *   grad_values_s [s x d] = ReLU(z)^T grad_out       (w_b_k layout)
+ *   grad_keys_s   [s x d] = masked^T h               (neuron-major, i.e. transpose of the reference d x s)
+ *   grad_h [T x d] = (accumulate_grad_h ? grad_h : 0) + masked * w_a_k^T
+ * F64: every buffer f64. BF16: grad_out/h/z/keys_s/values_s/masked bf16; grad_* f32. */
+meft_status meft_ffn_backward(meft_ctx* ctx, meft_dtype dt, const void* grad_out, const void* h, const void* z,
+                              const void* keys_s, const void* values_s, int64_t T, int64_t d, int64_t s,
+                              int64_t ld_z, void* masked_ws, void* grad_keys_s, void* grad_values_s, void* grad_h,
+                              int accumulate_grad_h);
+
+/* Frozen base FFN half of sparse_ffn_pa / sparse_backward (adapter.cpp:119-120, 153-164), f64 only.
+ * act: 0 SiLU, 1 ReLU. forward: base_pre [T x n] = h*w_in, out [T x d] = act(base_pre)*w_out.
+ * backward: grad_h [T x d] = ((grad_out*w_out^T) .* act'(base_pre)) * w_in^T. */
+meft_status meft_base_ffn_forward(meft_ctx* ctx, const double* h, const double* w_in, const double* w_out,
+                                  int64_t T, int64_t d, int64_t n, int act, double* base_pre, double* out);
+meft_status meft_base_ffn_backward(meft_ctx* ctx, const double* grad_out, const double* base_pre,
+                                   const double* w_in, const double* w_out, int64_t T, int64_t d, int64_t n, int act,
+                                   double* grad_h);
+
+/* Dense fp64 product C[m x n] = A[m x k] * B[k x n] (row-major), the reference matmul (kernels.cpp:57-76):
+ * ascending-k fma chains that skip zero a-entries, bitwise equal to the compiled reference. Non-finite
+ * results return MEFT_E_NONFINITE like check_finite (kernels.cpp:7-13); synchronises. */
+meft_status meft_matmul_f64(meft_ctx* ctx, const double* A, const double* B, int64_t m, int64_t k, int64_t n,
+                            double* C);
+
+/* ------------------------------------------------------------------ HBM-resident store */
+
+/* HostStore for `layers` layers (memtier.hpp:108-133) resident in HBM. All tensors start at zero; use
+ * meft_store_upload_host (or meft_store_init_reference) to set weights. */
+meft_status meft_store_create(meft_ctx* ctx, int64_t layers, int64_t d, int64_t pairs, int64_t experts,
+                              meft_precision precision, meft_store** out);
+void meft_store_destroy(meft_store* store);
+meft_status meft_store_info(const meft_store* store, int64_t* layers, int64_t* d, int64_t* pairs, int64_t* experts,
+                            meft_precision* precision);
+/* HostStore::init (memtier.cpp:60-96): W_A ~ U(+-1/sqrt(d)) from mix_seed(seed, 0x5000+2l), W_G from
+ * 0x5001+2l, W_B = 0, moments/steps/staging zero. Generated on the host with the reference RNG (rng.hpp),
+ * bit-identical to the reference tables; bf16 compute copies are rounded from them in MIXED mode. */
+meft_status meft_store_init_reference(meft_ctx* ctx, meft_store* store, uint64_t seed);
+/* Host transfers in the reference layouts (see meft_tensor). host_dt F64 (or int64/int8 for counters). */
+meft_status meft_store_upload_host(meft_ctx* ctx, meft_store* store, int64_t layer, meft_tensor t, const void* host,
+                                   int64_t rows, int64_t cols);
+meft_status meft_store_download_host(meft_ctx* ctx, meft_store* store, int64_t layer, meft_tensor t, void* host,
+                                     int64_t rows, int64_t cols); /* synchronises */
+/* Device view of a store tensor in its device layout. */
+meft_status meft_store_tensor(meft_store* store, int64_t layer, meft_tensor t, void** dev, meft_dtype* dt,
+                              int64_t* rows, int64_t* cols);
+
+/* fetch (memtier.cpp:117-126): gather rows S of the layer's compute tables (validated like gather_adapter). */
+meft_status meft_fetch(meft_ctx* ctx, meft_store* store, int64_t layer, const int32_t* S, int64_t s, void* keys_s,
+                       void* values_s);
+/* scatter_grads (memtier.cpp:128-155): stage[S_j] += grad (neuron-major rows, dtype gdt in {F64, F32}),
+ * staged[S_j] = 1; repeated scatters sum. Validates S range (synchronises) -> MEFT_E_RANGE. */
+meft_status meft_scatter_grads(meft_ctx* ctx, meft_store* store, int64_t layer, const int32_t* S, int64_t s,
+                               const void* grad_keys_s, const void* grad_values_s, meft_dtype gdt);
+/* sparse_adam_update (memtier.cpp:187-210): lazy Adam on every staged pair (per-pair step counter), then
+ * clears staging. Untouched pairs stay bit-identical. No host synchronisation. */
+meft_status meft_sparse_adam_update(meft_ctx* ctx, meft_store* store, int64_t layer, double beta1, double beta2,
+                                    double eps, double lr);
+
+/* ------------------------------------------------------------------ whole layer step */
+
+typedef struct meft_step_info {
+    int64_t union_size; /* |S| */
+    int64_t take;       /* per-token K after the clamp */
+    int64_t kk_eff;
+    int warned;         /* the reference would have called warn() */
+    int gpu_launches;   /* kernels this step launched */
+} meft_step_info;
+
+/* One MEFT layer training step in MIXED precision, the trainer's per-layer sequence
+ * (trainer.cpp:220,270,283,525): meft_ffn (ke_select -> fetch -> sparse_ffn_pa) -> sparse_backward ->
+ * scatter_grads -> sparse_adam_update. h and grad_out are bf16 [T x d] on device; out and grad_h are f32
+ * [T x d] (either may be NULL). Optional outputs per_token [T x take] / union_idx [M] (device int32) may be
+ * NULL. Synchronises once (to size the union).
+ */
+meft_status meft_layer_step(meft_ctx* ctx, meft_store* store, int64_t layer, const void* h, const void* grad_out,
+                            int64_t T, int64_t kk, int64_t k, double beta1, double beta2, double eps, double lr,
+                            float* out, float* grad_h, int32_t* per_token, int32_t* union_idx, meft_step_info* info);
+
+/* Same step from HOST buffers (pinned or pageable): copies h/grad_out in and out/grad_h back inside the
+ * call; returns when the results are on the host. */
+meft_status meft_layer_step_host(meft_ctx* ctx, meft_store* store, int64_t layer, const uint16_t* h_host,
+                                 const uint16_t* grad_out_host, int64_t T, int64_t kk, int64_t k, double beta1,
+                                 double beta2, double eps, double lr, float* out_host, float* grad_h_host,
+                                 meft_step_info* info);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MEFT_CUDA_H */

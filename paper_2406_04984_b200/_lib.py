@@ -1,0 +1,111 @@
+"""ctypes binding of the C ABI in include/meft_cuda.h (libmeft_cuda.so, built in-tree).
+
+Loading fails loudly when the library is missing: there is no CPU fallback anywhere in this package.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmeft_cuda.so")
+
+P = C.c_void_p
+I64 = C.c_int64
+I32P = C.POINTER(C.c_int32)
+D = C.c_double
+INT = C.c_int
+
+# name -> (restype, argtypes)
+_SIGS = {
+    "meft_version": (C.c_char_p, []),
+    "meft_ctx_create": (INT, [INT, P, C.POINTER(P)]),
+    "meft_ctx_destroy": (None, [P]),
+    "meft_ctx_stream": (P, [P]),
+    "meft_last_error": (C.c_char_p, [P]),
+    "meft_last_error_index": (I64, [P]),
+    "meft_synchronize": (INT, [P]),
+    "meft_ctx_set_timing": (INT, [P, INT]),
+    "meft_ctx_read_timing": (INT, [P, P, P]),
+    "meft_device_alloc": (INT, [P, C.c_size_t, C.POINTER(P)]),
+    "meft_device_free": (INT, [P, P]),
+    "meft_host_alloc": (INT, [P, C.c_size_t, C.POINTER(P)]),
+    "meft_host_free": (INT, [P, P]),
+    "meft_copy_to_device": (INT, [P, P, P, C.c_size_t]),
+    "meft_copy_to_host": (INT, [P, P, P, C.c_size_t]),
+    "meft_memset": (INT, [P, P, INT, C.c_size_t]),
+    "meft_convert": (INT, [P, P, INT, P, INT, I64]),
+    "meft_selection_shape": (INT, [I64, I64, I64, I64, C.POINTER(I64), C.POINTER(I64), C.POINTER(INT)]),
+    "meft_route_scores": (INT, [P, INT, P, P, I64, I64, I64, P]),
+    "meft_select_experts": (INT, [P, P, I64, I64, I64, P]),
+    "meft_ke_select": (INT, [P, INT, P, P, P, I64, I64, I64, I64, I64, I64, P, P, P, P]),
+    "meft_topk_select": (INT, [P, INT, P, P, I64, I64, I64, I64, P, P, P]),
+    "meft_gather_adapter": (INT, [P, INT, P, P, I64, I64, P, I64, P, P]),
+    "meft_ffn_forward": (INT, [P, INT, P, P, P, I64, I64, I64, I64, P, P, INT]),
+    "meft_ffn_backward": (INT, [P, INT, P, P, P, P, P, I64, I64, I64, I64, P, P, P, P, INT]),
+    "meft_base_ffn_forward": (INT, [P, P, P, P, I64, I64, I64, INT, P, P]),
+    "meft_base_ffn_backward": (INT, [P, P, P, P, P, I64, I64, I64, INT, P]),
+    "meft_matmul_f64": (INT, [P, P, P, I64, I64, I64, P]),
+    "meft_store_create": (INT, [P, I64, I64, I64, I64, INT, C.POINTER(P)]),
+    "meft_store_destroy": (None, [P]),
+    "meft_store_info": (INT, [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64), C.POINTER(I64), C.POINTER(INT)]),
+    "meft_store_init_reference": (INT, [P, P, C.c_uint64]),
+    "meft_store_upload_host": (INT, [P, P, I64, INT, P, I64, I64]),
+    "meft_store_download_host": (INT, [P, P, I64, INT, P, I64, I64]),
+    "meft_store_tensor": (INT, [P, I64, INT, C.POINTER(P), C.POINTER(INT), C.POINTER(I64), C.POINTER(I64)]),
+    "meft_fetch": (INT, [P, P, I64, P, I64, P, P]),
+    "meft_scatter_grads": (INT, [P, P, I64, P, I64, P, P, INT]),
+    "meft_sparse_adam_update": (INT, [P, P, I64, D, D, D, D]),
+    "meft_layer_step": (INT, [P, P, I64, P, P, I64, I64, I64, D, D, D, D, P, P, P, P, P]),
+    "meft_layer_step_host": (INT, [P, P, I64, P, P, I64, I64, I64, D, D, D, D, P, P, P]),
+}
+
+F64, F32, BF16 = 0, 1, 2
+STORE_F64, STORE_MIXED = 0, 1
+
+TENSORS = {"w_a": 0, "w_b": 1, "w_g": 2, "m_a": 3, "v_a": 4, "m_b": 5, "v_b": 6, "stage_a": 7, "stage_b": 8,
+           "pair_step": 9, "staged": 10, "w_a_compute": 11, "w_b_compute": 12, "w_g_compute": 13}
+
+
+class StepInfo(C.Structure):
+    _fields_ = [("union_size", I64), ("take", I64), ("kk_eff", I64), ("warned", INT), ("gpu_launches", INT)]
+
+
+class MeftError(RuntimeError):
+    """Error raised from a meft_status != MEFT_OK; `kind` mirrors the reference exception type."""
+
+    KINDS = {1: "ShapeError", 2: "invalid_argument", 3: "out_of_range", 4: "logic_error", 5: "non-finite",
+             6: "cuda", 7: "nccl", 8: "oom"}
+
+    def __init__(self, code: int, msg: str, index: int = -1):
+        super().__init__(f"{self.KINDS.get(code, code)}: {msg}")
+        self.code = code
+        self.kind = self.KINDS.get(code, str(code))
+        self.index = index
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is not built; run __graft_entry__.build() (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def exported_symbols():
+    return list(_SIGS)
+
+
+def check(status: int, ctx=None):
+    if status != 0:
+        L = lib()
+        raise MeftError(status, L.meft_last_error(ctx).decode(errors="replace"), int(L.meft_last_error_index(ctx)))

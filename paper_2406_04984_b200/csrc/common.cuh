@@ -34,7 +34,11 @@ struct MeftError : std::runtime_error {
                                                              cudaGetErrorString(_e));           \
     } while (0)
 
+// Counts every kernel launch of the library (reported as gpu_launches by the layer step and bench).
+long long& launch_counter();
+
 inline void check_launch(const char* what) {
+    ++launch_counter();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw MeftError(6, std::string(what) + ": " + cudaGetErrorString(e));
 }

@@ -41,7 +41,8 @@ void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOpera
 // arbitrary element strides so transposed views need no copies.
 struct DOperand {
     const double* ptr;
-    int64_t s0, s1;  // element strides for (row, col) of the logical matrix
+    int64_t s0, s1;     // element strides for (row, col) of the logical matrix
+    bool relu = false;  // load max(x, 0) (A operand only: ReLU(z) without materialising it)
 };
 enum DEpi : int {
     DEPI_STORE = 0,        // C = acc

@@ -1,0 +1,1033 @@
+// libmeft_cuda.so — C ABI of the B200 MEFT layer (declarations and reference citations: include/meft_cuda.h).
+// Host orchestration only: every numeric step is a kernel in gemm_sm100.cu / select.cu / stream_ops.cu /
+// dgemm.cu. There is no CPU compute path.
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/meft_cuda.h"
+#include "common.cuh"
+#include "kernels.h"
+#include "select.h"
+#include "stream_ops.h"
+
+using namespace meft_dev;
+
+namespace {
+thread_local std::string t_err;
+thread_local int64_t t_err_index = -1;
+}  // namespace
+
+struct meft_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;  // overlaps host transfers with compute in the _host step
+    bool own_stream = false;
+    cudaEvent_t ev_in = nullptr, ev_fwd = nullptr, ev_out = nullptr;
+    std::string err;
+    int64_t err_index = -1;
+    int32_t* dev_small = nullptr;   // 64 device ints (validation flags, counts)
+    int32_t* host_small = nullptr;  // 64 pinned ints
+    struct Buf {
+        void* p = nullptr;
+        size_t n = 0;
+    };
+    std::unordered_map<std::string, Buf> scratch;
+
+    // phase timing (meft_ctx_set_timing)
+    bool timing = false;
+    struct PhaseRec {
+        int phase;
+        cudaEvent_t a, b;
+        long long launches;
+    };
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    std::vector<PhaseRec> recs;
+
+    cudaEvent_t next_event() {
+        if (ev_used == ev_pool.size()) {
+            cudaEvent_t e;
+            MEFT_CUDA_CHECK(cudaEventCreate(&e));
+            ev_pool.push_back(e);
+        }
+        return ev_pool[ev_used++];
+    }
+
+    void* get(const std::string& name, size_t bytes) {
+        Buf& b = scratch[name];
+        if (b.n < bytes) {
+            if (b.p) MEFT_CUDA_CHECK(cudaFree(b.p));
+            b.p = nullptr;
+            b.n = 0;
+            const size_t want = std::max<size_t>(bytes, 256);
+            cudaError_t e = cudaMalloc(&b.p, want);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                throw MeftError(MEFT_E_OOM, "device allocation of " + std::to_string(want) + " bytes for '" + name +
+                                                "' failed: " + cudaGetErrorString(e));
+            }
+            b.n = want;
+        }
+        return b.p;
+    }
+};
+
+namespace {
+
+struct LayerBufs {
+    void* w_a = nullptr;  // [r x d] master (f64 or f32)
+    void* w_b = nullptr;
+    void* w_g = nullptr;  // [N x d]
+    void* m_a = nullptr;
+    void* v_a = nullptr;
+    void* m_b = nullptr;
+    void* v_b = nullptr;
+    void* st_a = nullptr;
+    void* st_b = nullptr;
+    void* c_a = nullptr;  // compute copies (bf16 in MIXED; alias of the masters in F64)
+    void* c_b = nullptr;
+    void* c_g = nullptr;
+    int32_t* step = nullptr;  // [r]
+    uint8_t* staged = nullptr;
+    void* base = nullptr;
+};
+
+}  // namespace
+
+struct meft_store {
+    int64_t layers = 0, d = 0, pairs = 0, experts = 0;
+    meft_precision prec = MEFT_STORE_MIXED;
+    int device = 0;
+    std::vector<LayerBufs> L;
+};
+
+namespace {
+
+// Records CUDA events on the context stream around one phase of the layer step (when timing is enabled).
+struct PhaseScope {
+    meft_ctx* c;
+    int phase;
+    cudaEvent_t a = nullptr;
+    long long l0 = 0;
+    PhaseScope(meft_ctx* ctx, int p) : c(ctx), phase(p) {
+        if (!c->timing) return;
+        a = c->next_event();
+        MEFT_CUDA_CHECK(cudaEventRecord(a, c->stream));
+        l0 = launch_counter();
+    }
+    ~PhaseScope() {
+        if (!c->timing) return;
+        cudaEvent_t b = c->next_event();
+        cudaEventRecord(b, c->stream);
+        c->recs.push_back({phase, a, b, launch_counter() - l0});
+    }
+};
+
+meft_status fail(meft_ctx* ctx, int code, const std::string& msg, int64_t index = -1) {
+    t_err = msg;
+    t_err_index = index;
+    if (ctx) {
+        ctx->err = msg;
+        ctx->err_index = index;
+    }
+    return static_cast<meft_status>(code);
+}
+
+template <class F>
+meft_status guarded(meft_ctx* ctx, F&& f) {
+    try {
+        if (ctx) MEFT_CUDA_CHECK(cudaSetDevice(ctx->device));
+        f();
+        return MEFT_OK;
+    } catch (const MeftError& e) {
+        return fail(ctx, e.code, e.what(), e.index);
+    } catch (const std::bad_alloc&) {
+        return fail(ctx, MEFT_E_OOM, "host allocation failed");
+    } catch (const std::exception& e) {
+        return fail(ctx, MEFT_E_CUDA, e.what());
+    }
+}
+
+int esize(meft_dtype dt) { return dt == MEFT_F64 ? 8 : dt == MEFT_F32 ? 4 : 2; }
+int dcode(meft_dtype dt) { return int(dt); }
+
+void require(bool ok, int code, const std::string& msg) {
+    if (!ok) throw MeftError(code, msg);
+}
+
+void require_ctx(meft_ctx* ctx) { require(ctx != nullptr, MEFT_E_INVALID, "null context"); }
+
+const LayerBufs& layer_of(const meft_store* s, int64_t layer) {
+    require(s != nullptr, MEFT_E_INVALID, "null store");
+    if (layer < 0 || layer >= s->layers)
+        throw MeftError(MEFT_E_RANGE, "layer " + std::to_string(layer) + " out of range", layer);
+    return s->L[size_t(layer)];
+}
+
+// Reads the device validation flags written by check_sorted_unique (err[0] code, err[1] first bad position).
+void raise_index_error(meft_ctx* ctx, const int32_t* S, const char* who, bool order_matters) {
+    MEFT_CUDA_CHECK(cudaMemcpyAsync(ctx->host_small, ctx->dev_small, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+    MEFT_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    const int code = ctx->host_small[0];
+    if (code == 3) {
+        int32_t bad = 0;
+        MEFT_CUDA_CHECK(cudaMemcpy(&bad, S + ctx->host_small[1], sizeof(int32_t), cudaMemcpyDeviceToHost));
+        throw MeftError(MEFT_E_RANGE, std::string(who) + ": index " + std::to_string(bad) + " out of range", bad);
+    }
+    if (code == 2 && order_matters)
+        throw MeftError(MEFT_E_INVALID, std::string(who) + ": indices not sorted ascending");
+}
+
+int validate_indices(meft_ctx* ctx, const int32_t* S, int64_t s, int64_t limit, const char* who,
+                     bool order_matters) {
+    if (s <= 0) return 0;
+    const int32_t init[2] = {0, INT32_MAX};
+    MEFT_CUDA_CHECK(cudaMemcpyAsync(ctx->dev_small, init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
+    check_sorted_unique(ctx->stream, S, s, limit, ctx->dev_small);
+    raise_index_error(ctx, S, who, order_matters);
+    return ctx->host_small[0];
+}
+
+int64_t selection_take(int64_t M, int64_t N, int64_t kk, int64_t k, int64_t* kk_eff, int* warned) {
+    if (k < 1) throw MeftError(MEFT_E_INVALID, "ke_select: K must be >= 1");
+    if (N < 1 || M < 1) throw MeftError(MEFT_E_INVALID, "ExpertPartition: N and r must be >= 1");
+    if (M % N) throw MeftError(MEFT_E_INVALID, "ExpertPartition: N=" + std::to_string(N) + " does not divide r=" +
+                                                   std::to_string(M));
+    if (kk < 1) throw MeftError(MEFT_E_INVALID, "select_experts: budget must be >= 1");
+    const int64_t ke = std::min(kk, N);
+    const int64_t visible = ke * (M / N);
+    if (kk_eff) *kk_eff = ke;
+    if (warned) *warned = k > visible ? 1 : 0;
+    return std::min(k, visible);
+}
+
+// ---- FFN building blocks (adapter.cpp:122-126, 166-175)
+
+void ffn_forward_impl(meft_ctx* ctx, meft_dtype dt, const void* h, const void* keys_s, const void* values_s,
+                      int64_t T, int64_t d, int64_t s, int64_t ld_z, void* z, void* out, bool accumulate) {
+    cudaStream_t st = ctx->stream;
+    if (dt == MEFT_F64) {
+        double* outd = static_cast<double*>(out);
+        if (!accumulate) MEFT_CUDA_CHECK(cudaMemsetAsync(outd, 0, size_t(T * d) * 8, st));
+        if (s == 0) return;
+        // z = h * w_a_k   (w_a_k(k=c, n=j) = keys_s[j*d + c])
+        dgemm(st, T, s, d, DOperand{static_cast<const double*>(h), d, 1}, DOperand{static_cast<const double*>(keys_s), 1, d},
+              static_cast<double*>(z), ld_z, DEPI_STORE, nullptr);
+        // out += ReLU(z) * w_b_k   (a separate chain added afterwards, like add_inplace)
+        double* tmp = static_cast<double*>(ctx->get("ffn_tmp", size_t(T * d) * 8));
+        DOperand A{static_cast<const double*>(z), ld_z, 1};
+        A.relu = true;
+        dgemm(st, T, d, s, A, DOperand{static_cast<const double*>(values_s), d, 1}, tmp, d, DEPI_STORE, nullptr);
+        add_f64(st, outd, tmp, T * d);
+        return;
+    }
+    require(dt == MEFT_BF16, MEFT_E_INVALID, "ffn_forward: dtype must be F64 or BF16");
+    require(d % 8 == 0 && ld_z % 8 == 0 && ld_z >= s, MEFT_E_INVALID, "ffn_forward(bf16): d and ld_z must be multiples of 8");
+    if (s == 0) {
+        if (!accumulate) MEFT_CUDA_CHECK(cudaMemsetAsync(out, 0, size_t(T * d) * 4, st));
+        return;
+    }
+    GemmEpilogue e1;
+    e1.kind = EPI_RELU_BF16;
+    e1.c = z;
+    e1.ldc = ld_z;
+    gemm_bf16(st, T, s, d, GemmOperand{h, d, false}, GemmOperand{keys_s, d, false}, e1);
+    GemmEpilogue e2;
+    e2.kind = EPI_STORE_F32;
+    e2.c = out;
+    e2.ldc = d;
+    e2.accumulate = accumulate;
+    gemm_bf16(st, T, d, s, GemmOperand{z, ld_z, false}, GemmOperand{values_s, d, true}, e2);
+}
+
+// stage_keys/stage_values non-null => weight grads are row-added into the store staging at S (fused scatter).
+void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* h, const void* z, const void* keys_s,
+                       const void* values_s, int64_t T, int64_t d, int64_t s, int64_t ld_z, void* masked,
+                       void* grad_keys_s, void* grad_values_s, void* grad_h, bool acc_h, const int32_t* S_rows,
+                       void* stage_keys, void* stage_values) {
+    cudaStream_t st = ctx->stream;
+    if (dt == MEFT_F64) {
+        const double* gd = static_cast<const double*>(g);
+        const double* hd = static_cast<const double*>(h);
+        const double* zd = static_cast<const double*>(z);
+        double* md = static_cast<double*>(masked);
+        double* ghd = static_cast<double*>(grad_h);
+        if (!acc_h && ghd) MEFT_CUDA_CHECK(cudaMemsetAsync(ghd, 0, size_t(T * d) * 8, st));
+        if (s == 0) return;
+        // masked = (G * w_b_k^T) .* 1[z>0]
+        DOperand mk{zd, ld_z, 1};
+        dgemm(st, T, s, d, DOperand{gd, d, 1}, DOperand{static_cast<const double*>(values_s), 1, d}, md, ld_z,
+              DEPI_MASK_STORE, &mk);
+        // grad_values = ReLU(z)^T G
+        DOperand rz{zd, 1, ld_z};
+        rz.relu = true;
+        dgemm(st, s, d, T, rz, DOperand{gd, d, 1}, static_cast<double*>(grad_values_s), d, DEPI_STORE, nullptr);
+        // grad_keys (neuron-major) = masked^T h
+        dgemm(st, s, d, T, DOperand{md, 1, ld_z}, DOperand{hd, d, 1}, static_cast<double*>(grad_keys_s), d,
+              DEPI_STORE, nullptr);
+        // grad_h += masked * w_a_k^T, as a separate chain (add_inplace, adapter.cpp:174)
+        if (ghd) {
+            double* tmp = static_cast<double*>(ctx->get("ffn_tmp", size_t(T * d) * 8));
+            dgemm(st, T, d, s, DOperand{md, ld_z, 1}, DOperand{static_cast<const double*>(keys_s), d, 1}, tmp, d,
+                  DEPI_STORE, nullptr);
+            add_f64(st, ghd, tmp, T * d);
+        }
+        return;
+    }
+    require(dt == MEFT_BF16, MEFT_E_INVALID, "ffn_backward: dtype must be F64 or BF16");
+    require(d % 8 == 0 && ld_z % 8 == 0 && ld_z >= s, MEFT_E_INVALID, "ffn_backward(bf16): alignment");
+    if (s == 0) {
+        if (!acc_h && grad_h) MEFT_CUDA_CHECK(cudaMemsetAsync(grad_h, 0, size_t(T * d) * 4, st));
+        return;
+    }
+    GemmEpilogue e3;  // masked = mask(act) .* (G * values_s^T)
+    e3.kind = EPI_MASK_BF16;
+    e3.c = masked;
+    e3.ldc = ld_z;
+    e3.mask = z;
+    e3.ldm = ld_z;
+    gemm_bf16(st, T, s, d, GemmOperand{g, d, false}, GemmOperand{values_s, d, false}, e3);
+    GemmEpilogue e4;  // grad_values = act^T G   (M = s, N = d, K = T)
+    if (S_rows) {
+        e4.kind = EPI_ROWS_ADD_F32;
+        e4.c = stage_values;
+        e4.row_idx = S_rows;
+    } else {
+        e4.kind = EPI_STORE_F32;
+        e4.c = grad_values_s;
+    }
+    e4.ldc = d;
+    gemm_bf16(st, s, d, T, GemmOperand{z, ld_z, true}, GemmOperand{g, d, true}, e4);
+    GemmEpilogue e5 = e4;  // grad_keys = masked^T h
+    e5.c = S_rows ? stage_keys : grad_keys_s;
+    gemm_bf16(st, s, d, T, GemmOperand{masked, ld_z, true}, GemmOperand{h, d, true}, e5);
+    if (grad_h) {
+        GemmEpilogue e6;  // grad_h (+)= masked * keys_s
+        e6.kind = EPI_STORE_F32;
+        e6.c = grad_h;
+        e6.ldc = d;
+        e6.accumulate = acc_h;
+        gemm_bf16(st, T, d, s, GemmOperand{masked, ld_z, false}, GemmOperand{keys_s, d, true}, e6);
+    }
+}
+
+// ---- store helpers
+
+bool is_a_family(meft_tensor t) {
+    return t == MEFT_T_W_A || t == MEFT_T_M_A || t == MEFT_T_V_A || t == MEFT_T_STAGE_A || t == MEFT_T_W_A_COMPUTE;
+}
+
+void* tensor_ptr(const meft_store* s, const LayerBufs& L, meft_tensor t, meft_dtype* dt, int64_t* rows,
+                 int64_t* cols) {
+    const meft_dtype master = s->prec == MEFT_STORE_F64 ? MEFT_F64 : MEFT_F32;
+    const meft_dtype comp = s->prec == MEFT_STORE_F64 ? MEFT_F64 : MEFT_BF16;
+    *rows = s->pairs;
+    *cols = s->d;
+    switch (t) {
+        case MEFT_T_W_A: *dt = master; return L.w_a;
+        case MEFT_T_W_B: *dt = master; return L.w_b;
+        case MEFT_T_W_G: *dt = master; *rows = s->experts; return L.w_g;
+        case MEFT_T_M_A: *dt = master; return L.m_a;
+        case MEFT_T_V_A: *dt = master; return L.v_a;
+        case MEFT_T_M_B: *dt = master; return L.m_b;
+        case MEFT_T_V_B: *dt = master; return L.v_b;
+        case MEFT_T_STAGE_A: *dt = master; return L.st_a;
+        case MEFT_T_STAGE_B: *dt = master; return L.st_b;
+        case MEFT_T_W_A_COMPUTE: *dt = comp; return L.c_a;
+        case MEFT_T_W_B_COMPUTE: *dt = comp; return L.c_b;
+        case MEFT_T_W_G_COMPUTE: *dt = comp; *rows = s->experts; return L.c_g;
+        case MEFT_T_PAIR_STEP: *dt = MEFT_F32; *cols = 1; return L.step;  // int32 storage
+        case MEFT_T_STAGED: *dt = MEFT_BF16; *cols = 1; return L.staged;  // uint8 storage
+        default: throw MeftError(MEFT_E_INVALID, "unknown store tensor");
+    }
+}
+
+// Uploads a float64 host matrix in the reference layout into the device tensor (converting layout/precision),
+// refreshing the bf16 compute copy when a MIXED master weight changes.
+void upload_f64(meft_ctx* ctx, meft_store* s, const LayerBufs& L, meft_tensor t, const double* host) {
+    cudaStream_t st = ctx->stream;
+    meft_dtype dt;
+    int64_t rows, cols;
+    void* dst = tensor_ptr(s, L, t, &dt, &rows, &cols);
+    const int64_t n = rows * cols;
+    double* tmp = static_cast<double*>(ctx->get("upload_a", size_t(n) * 8));
+    MEFT_CUDA_CHECK(cudaMemcpyAsync(tmp, host, size_t(n) * 8, cudaMemcpyHostToDevice, st));
+    const double* src = tmp;
+    if (is_a_family(t)) {  // host d x r -> device r x d
+        double* tr = static_cast<double*>(ctx->get("upload_b", size_t(n) * 8));
+        transpose8(st, tmp, tr, s->d, s->pairs);
+        src = tr;
+    }
+    convert(st, dcode(dt), dst, 0, src, n);
+    if (s->prec == MEFT_STORE_MIXED) {
+        if (t == MEFT_T_W_A) convert(st, 2, L.c_a, 0, src, n);
+        if (t == MEFT_T_W_B) convert(st, 2, L.c_b, 0, src, n);
+        if (t == MEFT_T_W_G) convert(st, 2, L.c_g, 0, src, n);
+    }
+    MEFT_CUDA_CHECK(cudaStreamSynchronize(st));  // the host buffer may be pageable and is released on return
+}
+
+void download_f64(meft_ctx* ctx, meft_store* s, const LayerBufs& L, meft_tensor t, double* host) {
+    cudaStream_t st = ctx->stream;
+    meft_dtype dt;
+    int64_t rows, cols;
+    const void* srcp = tensor_ptr(s, L, t, &dt, &rows, &cols);
+    const int64_t n = rows * cols;
+    double* tmp = static_cast<double*>(ctx->get("upload_a", size_t(n) * 8));
+    convert(st, 0, tmp, dcode(dt), srcp, n);
+    const double* out = tmp;
+    if (is_a_family(t)) {  // device r x d -> host d x r
+        double* tr = static_cast<double*>(ctx->get("upload_b", size_t(n) * 8));
+        transpose8(st, tmp, tr, s->pairs, s->d);
+        out = tr;
+    }
+    MEFT_CUDA_CHECK(cudaMemcpyAsync(host, out, size_t(n) * 8, cudaMemcpyDeviceToHost, st));
+    MEFT_CUDA_CHECK(cudaStreamSynchronize(st));
+}
+
+// HostStore::init streams (memtier.cpp:67-77) with the reference RNG (rng.hpp:13-36, 62-66).
+uint64_t mix_seed(uint64_t seed, uint64_t stream) {
+    uint64_t x = seed ^ (0x9E3779B97F4A7C15ull * (stream + 1));
+    x ^= x >> 30;
+    x *= 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 27;
+    x *= 0x94D049BB133111EBull;
+    x ^= x >> 31;
+    return x;
+}
+
+void uniform_fill(uint64_t seed, double lo, double hi, double* out, int64_t n) {
+    std::mt19937_64 gen(seed);
+    for (int64_t i = 0; i < n; ++i) {
+        const double u = double(gen() >> 11) * 0x1.0p-53;
+        out[i] = std::fma(hi - lo, u, lo);  // the compiled reference contracts lo + (hi-lo)*u
+    }
+}
+
+// ---- sparse Adam over the staged set (memtier.cpp:187-210)
+
+void adam_impl(meft_ctx* ctx, meft_store* s, const LayerBufs& L, double b1, double b2, double eps, double lr) {
+    cudaStream_t st = ctx->stream;
+    int32_t* rows = static_cast<int32_t*>(ctx->get("adam_rows", size_t(s->pairs) * 4));
+    int32_t* bws = static_cast<int32_t*>(ctx->get("adam_bws", size_t((s->pairs + 1023) / 1024 + 1) * 4));
+    int32_t* cnt = ctx->dev_small + 8;
+    compact_flags(st, L.staged, s->pairs, rows, cnt, bws);
+    if (s->prec == MEFT_STORE_MIXED)
+        adam_mixed(st, rows, cnt, 0, s->d, static_cast<float*>(L.w_a), static_cast<float*>(L.m_a),
+                   static_cast<float*>(L.v_a), static_cast<float*>(L.st_a), static_cast<uint16_t*>(L.c_a),
+                   static_cast<float*>(L.w_b), static_cast<float*>(L.m_b), static_cast<float*>(L.v_b),
+                   static_cast<float*>(L.st_b), static_cast<uint16_t*>(L.c_b), L.step, L.staged, b1, b2, eps, lr);
+    else
+        adam_f64(st, rows, cnt, 0, s->d, static_cast<double*>(L.w_a), static_cast<double*>(L.m_a),
+                 static_cast<double*>(L.v_a), static_cast<double*>(L.st_a), static_cast<double*>(L.w_b),
+                 static_cast<double*>(L.m_b), static_cast<double*>(L.v_b), static_cast<double*>(L.st_b), L.step,
+                 L.staged, b1, b2, eps, lr);
+}
+
+}  // namespace
+
+// =========================================================================================== C ABI
+
+extern "C" {
+
+const char* meft_version(void) { return "meft-b200 0.1 (sm_100a)"; }
+
+meft_status meft_ctx_create(int device, void* stream, meft_ctx** out) {
+    if (!out) return fail(nullptr, MEFT_E_INVALID, "null output pointer");
+    std::unique_ptr<meft_ctx> c(new meft_ctx());
+    c->device = device;
+    meft_status st = guarded(c.get(), [&] {
+        if (stream) {
+            c->stream = static_cast<cudaStream_t>(stream);
+        } else {
+            MEFT_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+            c->own_stream = true;
+        }
+        MEFT_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        MEFT_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
+        MEFT_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_fwd, cudaEventDisableTiming));
+        MEFT_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
+        MEFT_CUDA_CHECK(cudaMalloc(&c->dev_small, 64 * sizeof(int32_t)));
+        MEFT_CUDA_CHECK(cudaMallocHost(&c->host_small, 64 * sizeof(int32_t)));
+    });
+    if (st != MEFT_OK) return st;
+    *out = c.release();
+    return MEFT_OK;
+}
+
+void meft_ctx_destroy(meft_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (auto& kv : ctx->scratch)
+        if (kv.second.p) cudaFree(kv.second.p);
+    for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+    if (ctx->dev_small) cudaFree(ctx->dev_small);
+    if (ctx->host_small) cudaFreeHost(ctx->host_small);
+    if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
+    if (ctx->ev_fwd) cudaEventDestroy(ctx->ev_fwd);
+    if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+void* meft_ctx_stream(meft_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+const char* meft_last_error(const meft_ctx* ctx) { return ctx ? ctx->err.c_str() : t_err.c_str(); }
+int64_t meft_last_error_index(const meft_ctx* ctx) { return ctx ? ctx->err_index : t_err_index; }
+
+meft_status meft_synchronize(meft_ctx* ctx) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        MEFT_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+meft_status meft_ctx_set_timing(meft_ctx* ctx, int enable) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        ctx->timing = enable != 0;
+    });
+}
+
+meft_status meft_ctx_read_timing(meft_ctx* ctx, double* ms5, int64_t* launches5) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        MEFT_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        double ms[5] = {0, 0, 0, 0, 0};
+        int64_t ln[5] = {0, 0, 0, 0, 0};
+        for (const auto& r : ctx->recs) {
+            float e = 0.f;
+            MEFT_CUDA_CHECK(cudaEventElapsedTime(&e, r.a, r.b));
+            if (r.phase >= 0 && r.phase < 5) {
+                ms[r.phase] += e;
+                ln[r.phase] += r.launches;
+            }
+        }
+        ctx->recs.clear();
+        ctx->ev_used = 0;
+        for (int i = 0; i < 5; ++i) {
+            if (ms5) ms5[i] = ms[i];
+            if (launches5) launches5[i] = ln[i];
+        }
+    });
+}
+
+meft_status meft_device_alloc(meft_ctx* ctx, size_t bytes, void** out) {
+    return guarded(ctx, [&] {
+        cudaError_t e = cudaMalloc(out, std::max<size_t>(bytes, 1));
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            throw MeftError(MEFT_E_OOM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+        }
+    });
+}
+meft_status meft_device_free(meft_ctx* ctx, void* ptr) {
+    return guarded(ctx, [&] { MEFT_CUDA_CHECK(cudaFree(ptr)); });
+}
+meft_status meft_host_alloc(meft_ctx* ctx, size_t bytes, void** out) {
+    return guarded(ctx, [&] { MEFT_CUDA_CHECK(cudaMallocHost(out, std::max<size_t>(bytes, 1))); });
+}
+meft_status meft_host_free(meft_ctx* ctx, void* ptr) {
+    return guarded(ctx, [&] { MEFT_CUDA_CHECK(cudaFreeHost(ptr)); });
+}
+meft_status meft_copy_to_device(meft_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        if (bytes) MEFT_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    });
+}
+meft_status meft_copy_to_host(meft_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        if (bytes) MEFT_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        MEFT_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+meft_status meft_memset(meft_ctx* ctx, void* dst, int value, size_t bytes) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        if (bytes) MEFT_CUDA_CHECK(cudaMemsetAsync(dst, value, bytes, ctx->stream));
+    });
+}
+meft_status meft_convert(meft_ctx* ctx, void* dst, meft_dtype dst_dt, const void* src, meft_dtype src_dt, int64_t n) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        convert(ctx->stream, dcode(dst_dt), dst, dcode(src_dt), src, n);
+    });
+}
+
+// ------------------------------------------------------------------ selection
+
+meft_status meft_selection_shape(int64_t M, int64_t N, int64_t kk, int64_t k, int64_t* take, int64_t* kk_eff,
+                                 int* warn) {
+    return guarded(nullptr, [&] {
+        const int64_t t = selection_take(M, N, kk, k, kk_eff, warn);
+        if (take) *take = t;
+    });
+}
+
+meft_status meft_route_scores(meft_ctx* ctx, meft_dtype dt, const void* h, const void* w_g, int64_t T, int64_t d,
+                              int64_t N, double* scores) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(dt == MEFT_F64 || dt == MEFT_BF16, MEFT_E_INVALID, "route_scores: dtype must be F64 or BF16");
+        require(T >= 0 && d >= 0 && N >= 0, MEFT_E_SHAPE, "route_scores: negative dimension");
+        score_rows(ctx->stream, dcode(dt), h, T, d, w_g, N, scores);
+    });
+}
+
+meft_status meft_select_experts(meft_ctx* ctx, const double* scores, int64_t T, int64_t N, int64_t kk, int32_t* tau) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        if (kk < 1) throw MeftError(MEFT_E_INVALID, "select_experts: budget must be >= 1");
+        if (T > 0 && N > 0) route_topk_device(ctx->stream, scores, T, N, std::min(kk, N), tau);
+    });
+}
+
+meft_status meft_ke_select(meft_ctx* ctx, meft_dtype dt, const void* h, const void* w_g, const void* keys, int64_t T,
+                           int64_t d, int64_t M, int64_t N, int64_t kk, int64_t k, int32_t* per_token, int32_t* tau,
+                           int32_t* union_idx, int32_t* union_size_dev) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(dt == MEFT_F64 || dt == MEFT_BF16, MEFT_E_INVALID, "ke_select: dtype must be F64 or BF16");
+        int64_t kk_eff = 0;
+        const int64_t take = selection_take(M, N, kk, k, &kk_eff, nullptr);
+        if (T == 0) {
+            MEFT_CUDA_CHECK(cudaMemsetAsync(union_size_dev, 0, 4, ctx->stream));
+            return;
+        }
+        const size_t wsb = select_workspace_bytes(T, M, N, kk_eff);
+        void* ws = ctx->get("select_ws", wsb);
+        ke_select_device(ctx->stream, dcode(dt), h, w_g, keys, T, d, M, N, kk_eff, take, ws, wsb, per_token, tau,
+                         union_idx, union_size_dev);
+    });
+}
+
+meft_status meft_topk_select(meft_ctx* ctx, meft_dtype dt, const void* h, const void* keys, int64_t T, int64_t d,
+                             int64_t M, int64_t k, int32_t* per_token, int32_t* union_idx, int32_t* union_size_dev) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(dt == MEFT_F64 || dt == MEFT_BF16, MEFT_E_INVALID, "topk_select: dtype must be F64 or BF16");
+        if (k < 1) throw MeftError(MEFT_E_INVALID, "topk_select: K must be >= 1");
+        require(M >= 1, MEFT_E_SHAPE, "topk_select: no keys");
+        const int64_t take = std::min(k, M);
+        if (T == 0) {
+            MEFT_CUDA_CHECK(cudaMemsetAsync(union_size_dev, 0, 4, ctx->stream));
+            return;
+        }
+        const size_t wsb = select_workspace_bytes(T, M, 1, 1);
+        void* ws = ctx->get("select_ws", wsb);
+        ke_select_device(ctx->stream, dcode(dt), h, nullptr, keys, T, d, M, 1, 1, take, ws, wsb, per_token, nullptr,
+                         union_idx, union_size_dev);
+    });
+}
+
+// ------------------------------------------------------------------ gather
+
+meft_status meft_gather_adapter(meft_ctx* ctx, meft_dtype dt, const void* keys, const void* values, int64_t M,
+                                int64_t d, const int32_t* S, int64_t s, void* keys_s, void* values_s) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        validate_indices(ctx, S, s, M, "gather_adapter", true);
+        if (s > 0 && d > 0) gather_rows2(ctx->stream, keys, values, d * esize(dt), S, nullptr, s, keys_s, values_s);
+    });
+}
+
+// ------------------------------------------------------------------ FFN
+
+meft_status meft_ffn_forward(meft_ctx* ctx, meft_dtype dt, const void* h, const void* keys_s, const void* values_s,
+                             int64_t T, int64_t d, int64_t s, int64_t ld_z, void* z, void* out, int accumulate) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(T >= 0 && d >= 0 && s >= 0 && ld_z >= s, MEFT_E_SHAPE, "ffn_forward: bad shape");
+        ffn_forward_impl(ctx, dt, h, keys_s, values_s, T, d, s, ld_z, z, out, accumulate != 0);
+    });
+}
+
+meft_status meft_ffn_backward(meft_ctx* ctx, meft_dtype dt, const void* grad_out, const void* h, const void* z,
+                              const void* keys_s, const void* values_s, int64_t T, int64_t d, int64_t s,
+                              int64_t ld_z, void* masked_ws, void* grad_keys_s, void* grad_values_s, void* grad_h,
+                              int accumulate_grad_h) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(T >= 0 && d >= 0 && s >= 0 && ld_z >= s, MEFT_E_SHAPE, "ffn_backward: bad shape");
+        ffn_backward_impl(ctx, dt, grad_out, h, z, keys_s, values_s, T, d, s, ld_z, masked_ws, grad_keys_s,
+                          grad_values_s, grad_h, accumulate_grad_h != 0, nullptr, nullptr, nullptr);
+    });
+}
+
+meft_status meft_base_ffn_forward(meft_ctx* ctx, const double* h, const double* w_in, const double* w_out, int64_t T,
+                                  int64_t d, int64_t n, int act, double* base_pre, double* out) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        cudaStream_t st = ctx->stream;
+        dgemm(st, T, n, d, DOperand{h, d, 1}, DOperand{w_in, n, 1}, base_pre, n, DEPI_STORE, nullptr);
+        double* a = static_cast<double*>(ctx->get("base_act", size_t(std::max<int64_t>(T * n, 1)) * 8));
+        act_forward(st, base_pre, a, T * n, act);
+        dgemm(st, T, d, n, DOperand{a, n, 1}, DOperand{w_out, d, 1}, out, d, DEPI_STORE, nullptr);
+    });
+}
+
+meft_status meft_base_ffn_backward(meft_ctx* ctx, const double* grad_out, const double* base_pre, const double* w_in,
+                                   const double* w_out, int64_t T, int64_t d, int64_t n, int act, double* grad_h) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        cudaStream_t st = ctx->stream;
+        double* da = static_cast<double*>(ctx->get("base_act", size_t(std::max<int64_t>(T * n, 1)) * 8));
+        // d_act = G * w_out^T ; d_pre = d_act .* f'(base_pre) ; grad_h = d_pre * w_in^T
+        dgemm(st, T, n, d, DOperand{grad_out, d, 1}, DOperand{w_out, 1, d}, da, n, DEPI_STORE, nullptr);
+        act_backward(st, da, base_pre, T * n, act);
+        dgemm(st, T, d, n, DOperand{da, n, 1}, DOperand{w_in, 1, n}, grad_h, d, DEPI_STORE, nullptr);
+    });
+}
+
+meft_status meft_matmul_f64(meft_ctx* ctx, const double* A, const double* B, int64_t m, int64_t k, int64_t n,
+                            double* C) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        cudaStream_t st = ctx->stream;
+        dgemm(st, m, n, k, DOperand{A, k, 1}, DOperand{B, n, 1}, C, n, DEPI_STORE, nullptr);
+        MEFT_CUDA_CHECK(cudaMemsetAsync(ctx->dev_small + 16, 0, 4, st));
+        flag_nonfinite(st, C, m * n, ctx->dev_small + 16);
+        MEFT_CUDA_CHECK(cudaMemcpyAsync(ctx->host_small + 16, ctx->dev_small + 16, 4, cudaMemcpyDeviceToHost, st));
+        MEFT_CUDA_CHECK(cudaStreamSynchronize(st));
+        if (ctx->host_small[16]) throw MeftError(MEFT_E_NONFINITE, "matmul: non-finite entry");
+    });
+}
+
+// ------------------------------------------------------------------ store
+
+meft_status meft_store_create(meft_ctx* ctx, int64_t layers, int64_t d, int64_t pairs, int64_t experts,
+                              meft_precision precision, meft_store** out) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(out != nullptr, MEFT_E_INVALID, "null output pointer");
+        require(layers >= 1 && d >= 1 && pairs >= 1 && experts >= 1, MEFT_E_SHAPE, "store_create: non-positive shape");
+        std::unique_ptr<meft_store> s(new meft_store());
+        s->layers = layers;
+        s->d = d;
+        s->pairs = pairs;
+        s->experts = experts;
+        s->prec = precision;
+        s->device = ctx->device;
+        const int mb = precision == MEFT_STORE_F64 ? 8 : 4;
+        const size_t pd = size_t(pairs) * size_t(d), nd = size_t(experts) * size_t(d);
+        auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+        size_t bytes = 8 * al(pd * mb) + al(nd * mb) + al(size_t(pairs) * 4) + al(size_t(pairs));
+        if (precision == MEFT_STORE_MIXED) bytes += 2 * al(pd * 2) + al(nd * 2);
+        for (int64_t l = 0; l < layers; ++l) {
+            LayerBufs L;
+            cudaError_t e = cudaMalloc(&L.base, bytes);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                for (auto& p : s->L) cudaFree(p.base);
+                throw MeftError(MEFT_E_OOM, "store_create: cannot allocate " + std::to_string(bytes) +
+                                                " bytes for layer " + std::to_string(l));
+            }
+            MEFT_CUDA_CHECK(cudaMemsetAsync(L.base, 0, bytes, ctx->stream));
+            uint8_t* p = static_cast<uint8_t*>(L.base);
+            auto take = [&](size_t n) {
+                void* r = p;
+                p += al(n);
+                return r;
+            };
+            L.w_a = take(pd * mb);
+            L.w_b = take(pd * mb);
+            L.m_a = take(pd * mb);
+            L.v_a = take(pd * mb);
+            L.m_b = take(pd * mb);
+            L.v_b = take(pd * mb);
+            L.st_a = take(pd * mb);
+            L.st_b = take(pd * mb);
+            L.w_g = take(nd * mb);
+            L.step = static_cast<int32_t*>(take(size_t(pairs) * 4));
+            L.staged = static_cast<uint8_t*>(take(size_t(pairs)));
+            if (precision == MEFT_STORE_MIXED) {
+                L.c_a = take(pd * 2);
+                L.c_b = take(pd * 2);
+                L.c_g = take(nd * 2);
+            } else {
+                L.c_a = L.w_a;
+                L.c_b = L.w_b;
+                L.c_g = L.w_g;
+            }
+            s->L.push_back(L);
+        }
+        MEFT_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        *out = s.release();
+    });
+}
+
+void meft_store_destroy(meft_store* store) {
+    if (!store) return;
+    cudaSetDevice(store->device);
+    for (auto& L : store->L) cudaFree(L.base);
+    delete store;
+}
+
+meft_status meft_store_info(const meft_store* s, int64_t* layers, int64_t* d, int64_t* pairs, int64_t* experts,
+                            meft_precision* precision) {
+    return guarded(nullptr, [&] {
+        require(s != nullptr, MEFT_E_INVALID, "null store");
+        if (layers) *layers = s->layers;
+        if (d) *d = s->d;
+        if (pairs) *pairs = s->pairs;
+        if (experts) *experts = s->experts;
+        if (precision) *precision = s->prec;
+    });
+}
+
+meft_status meft_store_init_reference(meft_ctx* ctx, meft_store* s, uint64_t seed) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(s != nullptr, MEFT_E_INVALID, "null store");
+        const double bound = 1.0 / std::sqrt(double(s->d));
+        std::vector<double> buf(size_t(s->d * std::max(s->pairs, s->experts)));
+        for (int64_t l = 0; l < s->layers; ++l) {
+            const LayerBufs& L = s->L[size_t(l)];
+            uniform_fill(mix_seed(seed, 0x5000 + 2 * uint64_t(l)), -bound, bound, buf.data(), s->d * s->pairs);
+            upload_f64(ctx, s, L, MEFT_T_W_A, buf.data());
+            uniform_fill(mix_seed(seed, 0x5001 + 2 * uint64_t(l)), -bound, bound, buf.data(), s->experts * s->d);
+            upload_f64(ctx, s, L, MEFT_T_W_G, buf.data());
+        }
+    });
+}
+
+meft_status meft_store_upload_host(meft_ctx* ctx, meft_store* s, int64_t layer, meft_tensor t, const void* host,
+                                   int64_t rows, int64_t cols) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        const LayerBufs& L = layer_of(s, layer);
+        if (t == MEFT_T_PAIR_STEP || t == MEFT_T_STAGED) {
+            require(rows * cols == s->pairs, MEFT_E_SHAPE, "store_upload: counter length");
+            if (t == MEFT_T_PAIR_STEP) {
+                int64_t* tmp = static_cast<int64_t*>(ctx->get("upload_a", size_t(s->pairs) * 8));
+                MEFT_CUDA_CHECK(cudaMemcpyAsync(tmp, host, size_t(s->pairs) * 8, cudaMemcpyHostToDevice, ctx->stream));
+                convert_index(ctx->stream, false, L.step, tmp, s->pairs);
+            } else {
+                MEFT_CUDA_CHECK(cudaMemcpyAsync(L.staged, host, size_t(s->pairs), cudaMemcpyHostToDevice, ctx->stream));
+            }
+            MEFT_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+            return;
+        }
+        require(t != MEFT_T_W_A_COMPUTE && t != MEFT_T_W_B_COMPUTE && t != MEFT_T_W_G_COMPUTE, MEFT_E_INVALID,
+                "store_upload: compute copies are derived from the masters");
+        meft_dtype dt;
+        int64_t dr, dc;
+        tensor_ptr(s, L, t, &dt, &dr, &dc);
+        const int64_t er = is_a_family(t) ? s->d : dr, ec = is_a_family(t) ? s->pairs : dc;
+        if (rows != er || cols != ec)
+            throw MeftError(MEFT_E_SHAPE, "store_upload: expected " + std::to_string(er) + "x" + std::to_string(ec));
+        upload_f64(ctx, s, L, t, static_cast<const double*>(host));
+    });
+}
+
+meft_status meft_store_download_host(meft_ctx* ctx, meft_store* s, int64_t layer, meft_tensor t, void* host,
+                                     int64_t rows, int64_t cols) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        const LayerBufs& L = layer_of(s, layer);
+        if (t == MEFT_T_PAIR_STEP || t == MEFT_T_STAGED) {
+            require(rows * cols == s->pairs, MEFT_E_SHAPE, "store_download: counter length");
+            if (t == MEFT_T_PAIR_STEP) {
+                int64_t* tmp = static_cast<int64_t*>(ctx->get("upload_a", size_t(s->pairs) * 8));
+                convert_index(ctx->stream, true, tmp, L.step, s->pairs);
+                MEFT_CUDA_CHECK(cudaMemcpyAsync(host, tmp, size_t(s->pairs) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+            } else {
+                MEFT_CUDA_CHECK(cudaMemcpyAsync(host, L.staged, size_t(s->pairs), cudaMemcpyDeviceToHost, ctx->stream));
+            }
+            MEFT_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+            return;
+        }
+        meft_dtype dt;
+        int64_t dr, dc;
+        tensor_ptr(s, L, t, &dt, &dr, &dc);
+        const int64_t er = is_a_family(t) ? s->d : dr, ec = is_a_family(t) ? s->pairs : dc;
+        if (rows != er || cols != ec)
+            throw MeftError(MEFT_E_SHAPE, "store_download: expected " + std::to_string(er) + "x" + std::to_string(ec));
+        download_f64(ctx, s, L, t, static_cast<double*>(host));
+    });
+}
+
+meft_status meft_store_tensor(meft_store* s, int64_t layer, meft_tensor t, void** dev, meft_dtype* dt, int64_t* rows,
+                              int64_t* cols) {
+    return guarded(nullptr, [&] {
+        const LayerBufs& L = layer_of(s, layer);
+        meft_dtype d0;
+        int64_t r0, c0;
+        void* p = tensor_ptr(s, L, t, &d0, &r0, &c0);
+        if (dev) *dev = p;
+        if (dt) *dt = d0;
+        if (rows) *rows = r0;
+        if (cols) *cols = c0;
+    });
+}
+
+meft_status meft_fetch(meft_ctx* ctx, meft_store* s, int64_t layer, const int32_t* S, int64_t n, void* keys_s,
+                       void* values_s) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        const LayerBufs& L = layer_of(s, layer);
+        validate_indices(ctx, S, n, s->pairs, "gather_adapter", true);
+        const int es = s->prec == MEFT_STORE_F64 ? 8 : 2;
+        if (n > 0) gather_rows2(ctx->stream, L.c_a, L.c_b, s->d * es, S, nullptr, n, keys_s, values_s);
+    });
+}
+
+meft_status meft_scatter_grads(meft_ctx* ctx, meft_store* s, int64_t layer, const int32_t* S, int64_t n,
+                               const void* gk, const void* gv, meft_dtype gdt) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        const LayerBufs& L = layer_of(s, layer);
+        require(gdt == MEFT_F64 || gdt == MEFT_F32, MEFT_E_INVALID, "scatter_grads: gradient dtype must be F64/F32");
+        if (n <= 0) return;
+        const int code = validate_indices(ctx, S, n, s->pairs, "scatter_grads", false);
+        const int sdt = s->prec == MEFT_STORE_F64 ? 0 : 1;
+        if (code == 0) {  // strictly ascending => unique rows => one CTA per row, no atomics
+            stage_add(ctx->stream, sdt, L.st_a, s->d, S, n, dcode(gdt), gk, L.staged);
+            stage_add(ctx->stream, sdt, L.st_b, s->d, S, n, dcode(gdt), gv, nullptr);
+        } else {  // repeated indices: apply entries in order (memtier.cpp:139-149 sums them in sequence)
+            const int ge = esize(gdt);
+            for (int64_t j = 0; j < n; ++j) {
+                stage_add(ctx->stream, sdt, L.st_a, s->d, S + j, 1, dcode(gdt),
+                          static_cast<const uint8_t*>(gk) + j * s->d * ge, L.staged);
+                stage_add(ctx->stream, sdt, L.st_b, s->d, S + j, 1, dcode(gdt),
+                          static_cast<const uint8_t*>(gv) + j * s->d * ge, nullptr);
+            }
+        }
+    });
+}
+
+meft_status meft_sparse_adam_update(meft_ctx* ctx, meft_store* s, int64_t layer, double beta1, double beta2,
+                                    double eps, double lr) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        adam_impl(ctx, s, layer_of(s, layer), beta1, beta2, eps, lr);
+    });
+}
+
+// ------------------------------------------------------------------ fused layer step
+
+static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const void* h, const void* g, int64_t T,
+                            int64_t kk, int64_t k, double b1, double b2, double eps, double lr, float* out,
+                            float* grad_h, int32_t* per_token_user, int32_t* union_user, meft_step_info* info,
+                            cudaEvent_t g_ready, cudaEvent_t fwd_done) {
+    const long long launches0 = launch_counter();
+    const LayerBufs& L = layer_of(s, layer);
+    require(s->prec == MEFT_STORE_MIXED, MEFT_E_INVALID, "layer_step: requires a MIXED precision store");
+    const int64_t d = s->d, M = s->pairs, N = s->experts;
+    require(d % 8 == 0, MEFT_E_INVALID, "layer_step: d must be a multiple of 8");
+    int64_t kk_eff = 0;
+    int warned = 0;
+    const int64_t take = selection_take(M, N, kk, k, &kk_eff, &warned);
+    cudaStream_t st = ctx->stream;
+
+    int32_t* per_token = per_token_user ? per_token_user
+                                        : static_cast<int32_t*>(ctx->get("per_token", size_t(T * take) * 4));
+    int32_t* uni = union_user ? union_user : static_cast<int32_t*>(ctx->get("union", size_t(M) * 4));
+    int32_t* usize = ctx->dev_small + 4;
+    const size_t wsb = select_workspace_bytes(T, M, N, kk_eff);
+    void* ws = ctx->get("select_ws", wsb);
+
+    // meft_ffn: ke_select (experts.cpp:47-117)
+    {
+        PhaseScope ps(ctx, 0);
+        ke_select_device(st, 2, h, L.c_g, L.c_a, T, d, M, N, kk_eff, take, ws, wsb, per_token, nullptr, uni, usize);
+    }
+    MEFT_CUDA_CHECK(cudaMemcpyAsync(ctx->host_small + 4, usize, 4, cudaMemcpyDeviceToHost, st));
+    MEFT_CUDA_CHECK(cudaStreamSynchronize(st));
+    const int64_t su = ctx->host_small[4];
+    const int64_t ld = round_up(std::max<int64_t>(su, 1), 64);
+
+    // fetch (memtier.cpp:117-126): gather the selected key/value rows of the bf16 compute tables
+    uint16_t* ks = static_cast<uint16_t*>(ctx->get("keys_s", size_t(std::max<int64_t>(su, 1) * d) * 2));
+    uint16_t* vs = static_cast<uint16_t*>(ctx->get("values_s", size_t(std::max<int64_t>(su, 1) * d) * 2));
+    uint16_t* act = static_cast<uint16_t*>(ctx->get("act", size_t(T * ld) * 2));
+    uint16_t* masked = static_cast<uint16_t*>(ctx->get("masked", size_t(T * ld) * 2));
+    float* outb = out ? out : static_cast<float*>(ctx->get("out", size_t(T * d) * 4));
+    float* ghb = grad_h ? grad_h : static_cast<float*>(ctx->get("grad_h", size_t(T * d) * 4));
+    if (su > 0) {
+        PhaseScope ps(ctx, 1);
+        gather_rows2(st, L.c_a, L.c_b, d * 2, uni, nullptr, su, ks, vs);
+    }
+
+    // sparse_ffn_pa adapter term (adapter.cpp:122-126), every token against the whole union
+    {
+        PhaseScope ps(ctx, 2);
+        ffn_forward_impl(ctx, MEFT_BF16, h, ks, vs, T, d, su, ld, act, outb, false);
+    }
+    if (fwd_done) MEFT_CUDA_CHECK(cudaEventRecord(fwd_done, st));
+    if (g_ready) MEFT_CUDA_CHECK(cudaStreamWaitEvent(st, g_ready, 0));
+
+    // sparse_backward + scatter_grads fused: weight-grad GEMM epilogues add straight into stage rows at S
+    {
+        PhaseScope ps(ctx, 3);
+        ffn_backward_impl(ctx, MEFT_BF16, g, h, act, ks, vs, T, d, su, ld, masked, nullptr, nullptr, ghb, false, uni,
+                          L.st_a, L.st_b);
+    }
+
+    // sparse_adam_update (memtier.cpp:187-210) over the staged pairs
+    {
+        PhaseScope ps(ctx, 4);
+        if (su > 0) mark_rows(st, L.staged, uni, nullptr, su);
+        adam_impl(ctx, s, L, b1, b2, eps, lr);
+    }
+
+    if (info) {
+        info->union_size = su;
+        info->take = take;
+        info->kk_eff = kk_eff;
+        info->warned = warned;
+        info->gpu_launches = int(launch_counter() - launches0);
+    }
+}
+
+meft_status meft_layer_step(meft_ctx* ctx, meft_store* s, int64_t layer, const void* h, const void* grad_out,
+                            int64_t T, int64_t kk, int64_t k, double beta1, double beta2, double eps, double lr,
+                            float* out, float* grad_h, int32_t* per_token, int32_t* union_idx, meft_step_info* info) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(T >= 1, MEFT_E_SHAPE, "layer_step: no tokens");
+        layer_step_impl(ctx, s, layer, h, grad_out, T, kk, k, beta1, beta2, eps, lr, out, grad_h, per_token, union_idx,
+                        info, nullptr, nullptr);
+    });
+}
+
+meft_status meft_layer_step_host(meft_ctx* ctx, meft_store* s, int64_t layer, const uint16_t* h_host,
+                                 const uint16_t* g_host, int64_t T, int64_t kk, int64_t k, double beta1, double beta2,
+                                 double eps, double lr, float* out_host, float* grad_h_host, meft_step_info* info) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(T >= 1, MEFT_E_SHAPE, "layer_step: no tokens");
+        require(s != nullptr, MEFT_E_INVALID, "null store");
+        const int64_t d = s->d;
+        const size_t in_bytes = size_t(T * d) * 2, out_bytes = size_t(T * d) * 4;
+        void* hd = ctx->get("h_in", in_bytes);
+        void* gd = ctx->get("g_in", in_bytes);
+        float* od = static_cast<float*>(ctx->get("out_dev", out_bytes));
+        float* ghd = static_cast<float*>(ctx->get("gh_dev", out_bytes));
+        // h on the compute stream; grad_out on the copy stream, overlapping selection + forward
+        MEFT_CUDA_CHECK(cudaMemcpyAsync(hd, h_host, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+        MEFT_CUDA_CHECK(cudaMemcpyAsync(gd, g_host, in_bytes, cudaMemcpyHostToDevice, ctx->copy_stream));
+        MEFT_CUDA_CHECK(cudaEventRecord(ctx->ev_in, ctx->copy_stream));
+        layer_step_impl(ctx, s, layer, hd, gd, T, kk, k, beta1, beta2, eps, lr, od, ghd, nullptr, nullptr, info,
+                        ctx->ev_in, ctx->ev_fwd);
+        // the forward output streams back while the backward runs
+        if (out_host) {
+            MEFT_CUDA_CHECK(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_fwd, 0));
+            MEFT_CUDA_CHECK(cudaMemcpyAsync(out_host, od, out_bytes, cudaMemcpyDeviceToHost, ctx->copy_stream));
+        }
+        if (grad_h_host) MEFT_CUDA_CHECK(cudaMemcpyAsync(grad_h_host, ghd, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        MEFT_CUDA_CHECK(cudaStreamSynchronize(ctx->copy_stream));
+        MEFT_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+}  // extern "C"

@@ -488,3 +488,17 @@ void route_topk_device(cudaStream_t st, const double* scores, int64_t T, int64_t
 }
 
 }  // namespace meft_dev
+
+namespace meft_dev {
+// Ascending list of the set entries of flags[M] (used for the staged set of sparse_adam_update).
+void compact_flags(cudaStream_t st, const uint8_t* flags, int64_t M, int32_t* out_idx, int32_t* count_dev,
+                   int32_t* block_ws) {
+    const int nb = int((M + 1023) / 1024);
+    k_flag_count<<<nb, 1024, 0, st>>>(flags, int(M), block_ws);
+    check_launch("k_flag_count");
+    k_scan_blocks<<<1, 32, 0, st>>>(block_ws, nb, count_dev);
+    check_launch("k_scan_blocks");
+    k_flag_write<<<nb, 1024, 0, st>>>(flags, int(M), block_ws, out_idx);
+    check_launch("k_flag_write");
+}
+}  // namespace meft_dev

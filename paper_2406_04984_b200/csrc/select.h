@@ -20,3 +20,10 @@ void ke_select_device(cudaStream_t st, int dtype, const void* h, const void* w_g
 void route_topk_device(cudaStream_t st, const double* scores, int64_t T, int64_t N, int64_t kk, int32_t* tau);
 
 }  // namespace meft_dev
+
+namespace meft_dev {
+// Ordered compaction: out_idx = ascending indices with flags[i] != 0, *count_dev = their number.
+// block_ws needs ceil(M/1024) int32.
+void compact_flags(cudaStream_t st, const uint8_t* flags, int64_t M, int32_t* out_idx, int32_t* count_dev,
+                   int32_t* block_ws);
+}  // namespace meft_dev

@@ -1,0 +1,390 @@
+// HBM-streaming kernels of the MEFT layer: row gather of the selected key/value rows
+// (adapter.cpp:86-110 / memtier.cpp:117-126), staging of weight gradients (memtier.cpp:128-155),
+// the lazy per-pair sparse Adam (memtier.cpp:176-228) and layout/precision conversions used at the
+// upload/download boundary. All tables are neuron-major ([pairs x d] rows), so every kernel streams
+// whole contiguous rows with 16-byte vector accesses.
+#include "common.cuh"
+#include "stream_ops.h"
+
+namespace meft_dev {
+namespace {
+
+// ---------------------------------------------------------------- gather
+
+// One warp per selected row; both tables in one pass. W is the copy word (uint4 when rows are 16-byte
+// multiples, else uint2 / uint16_t).
+template <typename W>
+__global__ void k_gather2(const W* __restrict__ a, const W* __restrict__ b, int64_t row_words,
+                          const int32_t* __restrict__ idx, const int32_t* __restrict__ count_dev, int count,
+                          W* __restrict__ oa, W* __restrict__ ob) {
+    const int n = count_dev ? *count_dev : count;
+    const int lane = threadIdx.x & 31;
+    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += (gridDim.x * blockDim.x) >> 5) {
+        const W* sa = a + int64_t(idx[r]) * row_words;
+        const W* sb = b + int64_t(idx[r]) * row_words;
+        W* da = oa + int64_t(r) * row_words;
+        W* db = ob + int64_t(r) * row_words;
+        for (int64_t v = lane; v < row_words; v += 64) {
+            const W x0 = __ldg(sa + v);
+            const W y0 = __ldg(sb + v);
+            const bool two = v + 32 < row_words;
+            W x1 = x0, y1 = y0;
+            if (two) {
+                x1 = __ldg(sa + v + 32);
+                y1 = __ldg(sb + v + 32);
+            }
+            da[v] = x0;
+            db[v] = y0;
+            if (two) {
+                da[v + 32] = x1;
+                db[v + 32] = y1;
+            }
+        }
+    }
+}
+
+__global__ void k_check_sorted(const int32_t* __restrict__ idx, int n, int64_t limit, int32_t* __restrict__ err) {
+    // err[0]: 0 ok, 3 out of range (err[1] = first bad index), 2 not strictly ascending
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int v = idx[i];
+    if (v < 0 || v >= limit) {
+        atomicCAS(&err[0], 0, 3);
+        atomicMin(&err[1], i);
+    } else if (i > 0 && v <= idx[i - 1]) {
+        atomicCAS(&err[0], 0, 2);
+    }
+}
+
+// ---------------------------------------------------------------- staging (scatter_grads)
+
+template <typename G, typename S>
+__global__ void k_stage_add(S* __restrict__ stage, int64_t d, const int32_t* __restrict__ idx, int n,
+                            const G* __restrict__ g, uint8_t* __restrict__ staged) {
+    const int r = blockIdx.x;
+    if (r >= n) return;
+    const int64_t row = idx[r];
+    S* s = stage + row * d;
+    const G* gr = g + int64_t(r) * d;
+    for (int64_t i = threadIdx.x; i < d; i += blockDim.x) s[i] += S(gr[i]);
+    if (staged && threadIdx.x == 0) staged[row] = 1;
+}
+
+__global__ void k_mark(uint8_t* __restrict__ staged, const int32_t* __restrict__ idx, const int32_t* count_dev,
+                       int count) {
+    const int n = count_dev ? *count_dev : count;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) staged[idx[i]] = 1;
+}
+
+// ---------------------------------------------------------------- sparse Adam (memtier.cpp:187-228)
+
+// Mixed-precision store: fp32 master/m/v/stage, bf16 compute copy. One CTA per staged pair updates the key
+// row and the value row (the pair shares one step counter, memtier.hpp:87-89), zeroes its staging and flag.
+__global__ void __launch_bounds__(256) k_adam_mixed(const int32_t* __restrict__ rows, const int32_t* count_dev,
+                                                    int count, int64_t d, float* __restrict__ wa, float* __restrict__ ma,
+                                                    float* __restrict__ va, float* __restrict__ sa,
+                                                    uint16_t* __restrict__ ca, float* __restrict__ wb,
+                                                    float* __restrict__ mb, float* __restrict__ vb,
+                                                    float* __restrict__ sb, uint16_t* __restrict__ cb,
+                                                    int32_t* __restrict__ step, uint8_t* __restrict__ staged, float b1,
+                                                    float b2, float eps, float lr) {
+    const int n = count_dev ? *count_dev : count;
+    __shared__ float s_c1, s_c2;
+    for (int r = blockIdx.x; r < n; r += gridDim.x) {
+        const int64_t j = rows[r];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int t = step[j] + 1;
+            step[j] = t;
+            staged[j] = 0;
+            s_c1 = float(1.0 - pow(double(b1), double(t)));
+            s_c2 = float(1.0 - pow(double(b2), double(t)));
+        }
+        __syncthreads();
+        const float c1 = s_c1, inv_c2 = 1.0f / s_c2;
+        const float ob1 = 1.0f - b1, ob2 = 1.0f - b2;
+        const float step_scale = lr / c1;
+#pragma unroll
+        for (int tab = 0; tab < 2; ++tab) {
+            float4* w4 = reinterpret_cast<float4*>((tab ? wb : wa) + j * d);
+            float4* m4 = reinterpret_cast<float4*>((tab ? mb : ma) + j * d);
+            float4* v4 = reinterpret_cast<float4*>((tab ? vb : va) + j * d);
+            float4* g4 = reinterpret_cast<float4*>((tab ? sb : sa) + j * d);
+            uint2* c4 = reinterpret_cast<uint2*>((tab ? cb : ca) + j * d);
+            for (int64_t i = threadIdx.x; i < d / 4; i += blockDim.x) {
+                const float4 g = g4[i];
+                float4 m = m4[i], v = v4[i], w = w4[i];
+                float* mp = &m.x;
+                float* vp = &v.x;
+                float* wp = &w.x;
+                const float* gp = &g.x;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    mp[q] = b1 * mp[q] + ob1 * gp[q];
+                    vp[q] = b2 * vp[q] + ob2 * gp[q] * gp[q];
+                    wp[q] -= step_scale * mp[q] / (sqrtf(vp[q] * inv_c2) + eps);
+                }
+                m4[i] = m;
+                v4[i] = v;
+                w4[i] = w;
+                g4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+                c4[i] = make_uint2(pack_bf16x2(f32_to_bf16_bits(w.x), f32_to_bf16_bits(w.y)),
+                                   pack_bf16x2(f32_to_bf16_bits(w.z), f32_to_bf16_bits(w.w)));
+            }
+        }
+    }
+}
+
+// fp64 store (API-fidelity mode): the reference's adam_entry in double (memtier.cpp:176-185).
+__global__ void __launch_bounds__(256) k_adam_f64(const int32_t* __restrict__ rows, const int32_t* count_dev, int count,
+                                                  int64_t d, double* __restrict__ wa, double* __restrict__ ma,
+                                                  double* __restrict__ va, double* __restrict__ sa,
+                                                  double* __restrict__ wb, double* __restrict__ mb,
+                                                  double* __restrict__ vb, double* __restrict__ sb,
+                                                  int32_t* __restrict__ step, uint8_t* __restrict__ staged, double b1,
+                                                  double b2, double eps, double lr) {
+    const int n = count_dev ? *count_dev : count;
+    __shared__ double s_c1, s_c2;
+    for (int r = blockIdx.x; r < n; r += gridDim.x) {
+        const int64_t j = rows[r];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int t = step[j] + 1;
+            step[j] = t;
+            staged[j] = 0;
+            s_c1 = 1.0 - pow(b1, double(t));
+            s_c2 = 1.0 - pow(b2, double(t));
+        }
+        __syncthreads();
+        const double c1 = s_c1, c2 = s_c2;
+        for (int tab = 0; tab < 2; ++tab) {
+            double* w = (tab ? wb : wa) + j * d;
+            double* m = (tab ? mb : ma) + j * d;
+            double* v = (tab ? vb : va) + j * d;
+            double* g = (tab ? sb : sa) + j * d;
+            for (int64_t i = threadIdx.x; i < d; i += blockDim.x) {
+                const double gi = g[i];
+                const double mi = b1 * m[i] + (1.0 - b1) * gi;
+                const double vi = b2 * v[i] + (1.0 - b2) * gi * gi;
+                m[i] = mi;
+                v[i] = vi;
+                w[i] -= lr * (mi / c1) / (sqrt(vi / c2) + eps);
+                g[i] = 0.0;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- conversions
+
+__global__ void k_f64_to_bf16(const double* __restrict__ s, uint16_t* __restrict__ d, int64_t n) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        d[i] = f32_to_bf16_bits(float(s[i]));  // double->float->bf16: exact for bf16-representable inputs
+}
+__global__ void k_f64_to_f32(const double* __restrict__ s, float* __restrict__ d, int64_t n) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        d[i] = float(s[i]);
+}
+__global__ void k_f32_to_f64(const float* __restrict__ s, double* __restrict__ d, int64_t n) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        d[i] = double(s[i]);
+}
+__global__ void k_f32_to_bf16(const float* __restrict__ s, uint16_t* __restrict__ d, int64_t n) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        d[i] = f32_to_bf16_bits(s[i]);
+}
+__global__ void k_bf16_to_f64(const uint16_t* __restrict__ s, double* __restrict__ d, int64_t n) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        d[i] = double(bf16_bits_to_f32(s[i]));
+}
+__global__ void k_i32_to_i64(const int32_t* __restrict__ s, int64_t* __restrict__ d, int64_t n) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        d[i] = s[i];
+}
+__global__ void k_i64_to_i32(const int64_t* __restrict__ s, int32_t* __restrict__ d, int64_t n) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        d[i] = int32_t(s[i]);
+}
+
+// 32x32 tiled transpose of a rows x cols matrix of 8-byte elements.
+__global__ void k_transpose8(const uint64_t* __restrict__ s, uint64_t* __restrict__ d, int64_t rows, int64_t cols) {
+    __shared__ uint64_t tile[32][33];
+    const int64_t c0 = int64_t(blockIdx.x) * 32, r0 = int64_t(blockIdx.y) * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int64_t r = r0 + i, c = c0 + threadIdx.x;
+        if (r < rows && c < cols) tile[i][threadIdx.x] = s[r * cols + c];
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int64_t c = c0 + i, r = r0 + threadIdx.x;
+        if (r < rows && c < cols) d[c * rows + r] = tile[threadIdx.x][i];
+    }
+}
+
+int grid_for(int64_t n, int per = 256) {
+    int64_t g = (n + per - 1) / per;
+    const int64_t cap = int64_t(num_sms()) * 16;
+    return int(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+}  // namespace
+
+void gather_rows2(cudaStream_t st, const void* a, const void* b, int64_t row_bytes, const int32_t* idx,
+                  const int32_t* count_dev, int64_t count, void* oa, void* ob) {
+    if (count <= 0 && !count_dev) return;
+    const int64_t warps = count > 0 ? count : int64_t(num_sms()) * 64;
+    const int grid = std::max(1, std::min<int>(int((warps * 32 + 255) / 256), num_sms() * 8));
+    auto al = [](const void* p, int n) { return (reinterpret_cast<uintptr_t>(p) % n) == 0; };
+    if (row_bytes % 16 == 0 && al(a, 16) && al(b, 16) && al(oa, 16) && al(ob, 16))
+        k_gather2<uint4><<<grid, 256, 0, st>>>(static_cast<const uint4*>(a), static_cast<const uint4*>(b),
+                                               row_bytes / 16, idx, count_dev, int(count), static_cast<uint4*>(oa),
+                                               static_cast<uint4*>(ob));
+    else if (row_bytes % 8 == 0)
+        k_gather2<uint2><<<grid, 256, 0, st>>>(static_cast<const uint2*>(a), static_cast<const uint2*>(b),
+                                               row_bytes / 8, idx, count_dev, int(count), static_cast<uint2*>(oa),
+                                               static_cast<uint2*>(ob));
+    else
+        k_gather2<uint16_t><<<grid, 256, 0, st>>>(static_cast<const uint16_t*>(a), static_cast<const uint16_t*>(b),
+                                                  row_bytes / 2, idx, count_dev, int(count),
+                                                  static_cast<uint16_t*>(oa), static_cast<uint16_t*>(ob));
+    check_launch("k_gather2");
+}
+
+void check_sorted_unique(cudaStream_t st, const int32_t* idx, int64_t n, int64_t limit, int32_t* err_dev) {
+    if (n <= 0) return;
+    k_check_sorted<<<int((n + 255) / 256), 256, 0, st>>>(idx, int(n), limit, err_dev);
+    check_launch("k_check_sorted");
+}
+
+void stage_add(cudaStream_t st, int stage_dtype, void* stage, int64_t d, const int32_t* idx, int64_t n, int g_dtype,
+               const void* g, uint8_t* staged) {
+    if (n <= 0) return;
+    if (stage_dtype == 0 && g_dtype == 0)
+        k_stage_add<double, double><<<int(n), 256, 0, st>>>(static_cast<double*>(stage), d, idx, int(n),
+                                                            static_cast<const double*>(g), staged);
+    else if (stage_dtype == 1 && g_dtype == 1)
+        k_stage_add<float, float><<<int(n), 256, 0, st>>>(static_cast<float*>(stage), d, idx, int(n),
+                                                          static_cast<const float*>(g), staged);
+    else if (stage_dtype == 1 && g_dtype == 0)
+        k_stage_add<double, float><<<int(n), 256, 0, st>>>(static_cast<float*>(stage), d, idx, int(n),
+                                                           static_cast<const double*>(g), staged);
+    else
+        k_stage_add<float, double><<<int(n), 256, 0, st>>>(static_cast<double*>(stage), d, idx, int(n),
+                                                           static_cast<const float*>(g), staged);
+    check_launch("k_stage_add");
+}
+
+void mark_rows(cudaStream_t st, uint8_t* staged, const int32_t* idx, const int32_t* count_dev, int64_t count) {
+    const int grid = grid_for(count > 0 ? count : 1);
+    k_mark<<<grid, 256, 0, st>>>(staged, idx, count_dev, int(count));
+    check_launch("k_mark");
+}
+
+void adam_mixed(cudaStream_t st, const int32_t* rows, const int32_t* count_dev, int64_t count, int64_t d, float* wa,
+                float* ma, float* va, float* sa, uint16_t* ca, float* wb, float* mb, float* vb, float* sb,
+                uint16_t* cb, int32_t* step, uint8_t* staged, double b1, double b2, double eps, double lr) {
+    if (d % 4) throw MeftError(2, "adam: d must be a multiple of 4 in mixed precision");
+    const int grid = std::max(1, std::min<int>(int(count > 0 ? count : num_sms() * 8), num_sms() * 8));
+    k_adam_mixed<<<grid, 256, 0, st>>>(rows, count_dev, int(count), d, wa, ma, va, sa, ca, wb, mb, vb, sb, cb, step,
+                                       staged, float(b1), float(b2), float(eps), float(lr));
+    check_launch("k_adam_mixed");
+}
+
+void adam_f64(cudaStream_t st, const int32_t* rows, const int32_t* count_dev, int64_t count, int64_t d, double* wa,
+              double* ma, double* va, double* sa, double* wb, double* mb, double* vb, double* sb, int32_t* step,
+              uint8_t* staged, double b1, double b2, double eps, double lr) {
+    const int grid = std::max(1, std::min<int>(int(count > 0 ? count : num_sms() * 8), num_sms() * 8));
+    k_adam_f64<<<grid, 256, 0, st>>>(rows, count_dev, int(count), d, wa, ma, va, sa, wb, mb, vb, sb, step, staged, b1,
+                                     b2, eps, lr);
+    check_launch("k_adam_f64");
+}
+
+void convert(cudaStream_t st, int ddt, void* dst, int sdt, const void* src, int64_t n) {
+    if (n <= 0) return;
+    const int g = grid_for(n);
+    if (sdt == 0 && ddt == 2)
+        k_f64_to_bf16<<<g, 256, 0, st>>>(static_cast<const double*>(src), static_cast<uint16_t*>(dst), n);
+    else if (sdt == 0 && ddt == 1)
+        k_f64_to_f32<<<g, 256, 0, st>>>(static_cast<const double*>(src), static_cast<float*>(dst), n);
+    else if (sdt == 1 && ddt == 0)
+        k_f32_to_f64<<<g, 256, 0, st>>>(static_cast<const float*>(src), static_cast<double*>(dst), n);
+    else if (sdt == 1 && ddt == 2)
+        k_f32_to_bf16<<<g, 256, 0, st>>>(static_cast<const float*>(src), static_cast<uint16_t*>(dst), n);
+    else if (sdt == 2 && ddt == 0)
+        k_bf16_to_f64<<<g, 256, 0, st>>>(static_cast<const uint16_t*>(src), static_cast<double*>(dst), n);
+    else if (sdt == ddt)
+        MEFT_CUDA_CHECK(cudaMemcpyAsync(dst, src, n * (sdt == 0 ? 8 : sdt == 1 ? 4 : 2), cudaMemcpyDeviceToDevice, st));
+    else
+        throw MeftError(2, "convert: unsupported dtype pair");
+    check_launch("convert");
+}
+
+void convert_index(cudaStream_t st, bool to64, void* dst, const void* src, int64_t n) {
+    if (n <= 0) return;
+    const int g = grid_for(n);
+    if (to64)
+        k_i32_to_i64<<<g, 256, 0, st>>>(static_cast<const int32_t*>(src), static_cast<int64_t*>(dst), n);
+    else
+        k_i64_to_i32<<<g, 256, 0, st>>>(static_cast<const int64_t*>(src), static_cast<int32_t*>(dst), n);
+    check_launch("convert_index");
+}
+
+void transpose8(cudaStream_t st, const void* src, void* dst, int64_t rows, int64_t cols) {
+    if (rows <= 0 || cols <= 0) return;
+    dim3 grid(unsigned((cols + 31) / 32), unsigned((rows + 31) / 32));
+    k_transpose8<<<grid, dim3(32, 8), 0, st>>>(static_cast<const uint64_t*>(src), static_cast<uint64_t*>(dst), rows,
+                                                cols);
+    check_launch("k_transpose8");
+}
+
+namespace {
+// kernels.cpp:15-22: sigmoid(x) = 1/(1+exp(-x)); silu = x*sigmoid(x); silu'(x) = s*(1 + x*(1-s)).
+__global__ void k_act_fwd(const double* __restrict__ x, double* __restrict__ y, int64_t n, int act) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const double v = x[i];
+        y[i] = act == 1 ? (v > 0.0 ? v : 0.0) : v * (1.0 / (1.0 + exp(-v)));
+    }
+}
+__global__ void k_act_bwd(double* __restrict__ g, const double* __restrict__ pre, int64_t n, int act) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const double x = pre[i];
+        if (act == 1) {
+            g[i] = x > 0.0 ? g[i] : 0.0;
+        } else {
+            const double s = 1.0 / (1.0 + exp(-x));
+            g[i] = g[i] * (s * (1.0 + x * (1.0 - s)));
+        }
+    }
+}
+__global__ void k_nonfinite(const double* __restrict__ x, int64_t n, int32_t* __restrict__ flag) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        if (!isfinite(x[i])) *flag = 1;
+}
+__global__ void k_add_f64(double* __restrict__ a, const double* __restrict__ b, int64_t n) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        a[i] = a[i] + b[i];
+}
+}  // namespace
+
+void act_forward(cudaStream_t st, const double* x, double* y, int64_t n, int act) {
+    if (n <= 0) return;
+    k_act_fwd<<<grid_for(n), 256, 0, st>>>(x, y, n, act);
+    check_launch("k_act_fwd");
+}
+void act_backward(cudaStream_t st, double* g, const double* pre, int64_t n, int act) {
+    if (n <= 0) return;
+    k_act_bwd<<<grid_for(n), 256, 0, st>>>(g, pre, n, act);
+    check_launch("k_act_bwd");
+}
+void flag_nonfinite(cudaStream_t st, const double* x, int64_t n, int32_t* flag_dev) {
+    if (n <= 0) return;
+    k_nonfinite<<<grid_for(n), 256, 0, st>>>(x, n, flag_dev);
+    check_launch("k_nonfinite");
+}
+void add_f64(cudaStream_t st, double* a, const double* b, int64_t n) {
+    if (n <= 0) return;
+    k_add_f64<<<grid_for(n), 256, 0, st>>>(a, b, n);
+    check_launch("k_add_f64");
+}
+
+}  // namespace meft_dev

@@ -1,0 +1,28 @@
+// Internal launch API of the HBM-streaming kernels (see stream_ops.cu). dtype codes: 0 f64, 1 f32, 2 bf16.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace meft_dev {
+
+void gather_rows2(cudaStream_t st, const void* a, const void* b, int64_t row_bytes, const int32_t* idx,
+                  const int32_t* count_dev, int64_t count, void* oa, void* ob);
+void check_sorted_unique(cudaStream_t st, const int32_t* idx, int64_t n, int64_t limit, int32_t* err_dev);
+void stage_add(cudaStream_t st, int stage_dtype, void* stage, int64_t d, const int32_t* idx, int64_t n, int g_dtype,
+               const void* g, uint8_t* staged);
+void mark_rows(cudaStream_t st, uint8_t* staged, const int32_t* idx, const int32_t* count_dev, int64_t count);
+void adam_mixed(cudaStream_t st, const int32_t* rows, const int32_t* count_dev, int64_t count, int64_t d, float* wa,
+                float* ma, float* va, float* sa, uint16_t* ca, float* wb, float* mb, float* vb, float* sb,
+                uint16_t* cb, int32_t* step, uint8_t* staged, double b1, double b2, double eps, double lr);
+void adam_f64(cudaStream_t st, const int32_t* rows, const int32_t* count_dev, int64_t count, int64_t d, double* wa,
+              double* ma, double* va, double* sa, double* wb, double* mb, double* vb, double* sb, int32_t* step,
+              uint8_t* staged, double b1, double b2, double eps, double lr);
+void convert(cudaStream_t st, int ddt, void* dst, int sdt, const void* src, int64_t n);
+void convert_index(cudaStream_t st, bool to64, void* dst, const void* src, int64_t n);
+void act_forward(cudaStream_t st, const double* x, double* y, int64_t n, int act);   // 0 SiLU, 1 ReLU
+void act_backward(cudaStream_t st, double* g, const double* pre, int64_t n, int act);  // g *= act'(pre)
+void flag_nonfinite(cudaStream_t st, const double* x, int64_t n, int32_t* flag_dev);
+void add_f64(cudaStream_t st, double* a, const double* b, int64_t n);                  // a += b (add_inplace)
+void transpose8(cudaStream_t st, const void* src, void* dst, int64_t rows, int64_t cols);
+
+}  // namespace meft_dev

@@ -5,6 +5,11 @@
 
 namespace meft_dev {
 
+long long& launch_counter() {
+    static thread_local long long n = 0;
+    return n;
+}
+
 int num_sms() {
     static int n = 0;
     static std::once_flag once;

@@ -1,0 +1,120 @@
+"""GPU parity of Key-Experts selection (experts.cpp:47-117, adapter.cpp:42-84): indices must be BIT-EXACT
+against the oracle (pinned to the reference) on identical inputs."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_2406_04984_b200 import meft as G
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(x, bf16):
+    t = torch.from_numpy(np.ascontiguousarray(x))
+    return (t.float().to(torch.bfloat16) if bf16 else t.double()).cuda().contiguous()
+
+
+def gpu_ke(ctx, h, w_g, w_a, kk, k, bf16):
+    sel = G.ke_select(ctx, dev(h, bf16), dev(w_g, bf16), dev(w_a.T, bf16), kk, k)
+    return sel.per_token.cpu().numpy(), sel.tau.cpu().numpy(), sel.unioned.cpu().numpy(), sel
+
+
+def inputs(T, d, r, N, seed, bf16):
+    mk = lambda s, shape: O.uniform(O.mix_seed(seed, s), shape, -1.0, 1.0)  # noqa: E731
+    h, w_a, w_g = mk(1, (T, d)), mk(2, (d, r)), mk(3, (N, d))
+    if bf16:
+        h, w_a, w_g = O.bf16_round(h), O.bf16_round(w_a), O.bf16_round(w_g)
+    return h, w_a, w_g
+
+
+@pytest.mark.parametrize("name", ["cfg1_bf16", "cfg1_f64", "odd_d_f64", "clamp", "full_budget", "one_expert"])
+def test_ke_select_matches_reference_fixture(ctx, golden, name):
+    g = golden("selection.npz")
+    f = lambda k: g[f"{name}__{k}"]  # noqa: E731
+    T, d, r, N, kk, k = (int(f(x)) for x in ("T", "d", "r", "N", "kk", "k"))
+    bf16 = bool(f("bf16"))
+    h, w_a, w_g = inputs(T, d, r, N, int(f("seed")), bf16)
+    per, tau, uni, sel = gpu_ke(ctx, h, w_g, w_a, kk, k, bf16)
+    np.testing.assert_array_equal(per, f("per_token"))
+    np.testing.assert_array_equal(tau, f("tau"))
+    np.testing.assert_array_equal(uni, f("unioned"))
+    assert sel.take == int(f("take"))
+    flat = G.topk_select(ctx, dev(h, bf16), dev(w_a.T, bf16), k)
+    np.testing.assert_array_equal(flat.per_token.cpu().numpy(), f("flat_per_token"))
+    np.testing.assert_array_equal(flat.unioned.cpu().numpy(), f("flat_unioned"))
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_ke_select_random_shapes_vs_oracle(ctx, seed):
+    rs = np.random.RandomState(seed)
+    T, d, N = rs.randint(1, 300), rs.randint(1, 70), rs.randint(1, 20)
+    r = N * rs.randint(1, 40)
+    kk, k = rs.randint(1, N + 3), rs.randint(1, 64)
+    bf16 = seed % 2 == 0
+    h, w_a, w_g = inputs(T, d, r, N, 500 + seed, bf16)
+    want = O.ke_select(h, w_g, w_a, kk, k)
+    per, tau, uni, sel = gpu_ke(ctx, h, w_g, w_a, kk, k, bf16)
+    np.testing.assert_array_equal(per, want["per_token"])
+    np.testing.assert_array_equal(tau, want["tau"])
+    np.testing.assert_array_equal(uni, want["unioned"])
+    assert sel.warned == want["warned"]
+
+
+def test_ties_and_signed_zero_follow_reference_order(ctx):
+    # zero input: every score is +-0.0 and ties break to the lowest index (test_adapter.cpp:93-99)
+    h = np.zeros((2, 3))
+    w_a = np.zeros((3, 6))
+    w_a[0, 1] = -1.0  # score of key 1 becomes -0.0 for h == 0: still equal to +0.0
+    flat = G.topk_select(ctx, dev(h, False), dev(w_a.T, False), 3)
+    assert flat.per_token.cpu().tolist() == [[0, 1, 2], [0, 1, 2]]
+    # exact duplicate keys: the lower global index wins inside and across experts
+    w_a = np.tile(O.uniform(3, (4, 1), -1, 1), (1, 8))
+    w_g = np.ones((4, 4))
+    res = G.ke_select(ctx, dev(O.uniform(4, (5, 4), -1, 1), False), dev(w_g, False), dev(w_a.T, False), 2, 3)
+    assert res.tau.cpu().tolist() == [[0, 1]] * 5
+    assert res.per_token.cpu().tolist() == [[0, 1, 2]] * 5
+
+
+def test_hand_examples(ctx):
+    w_a = np.array([[1.0, 0.0, -1.0, 0.5], [0.0, 1.0, 0.0, 0.5]])  # test_adapter.cpp:101-117
+    res = G.topk_select(ctx, dev(np.array([[1.0, 2.0]]), False), dev(w_a.T, False), 2)
+    assert res.unioned.cpu().tolist() == [1, 3]
+    w_a = np.zeros((2, 4))  # test_experts.cpp:87-110
+    w_a[0, 0], w_a[0, 2], w_a[0, 3] = 100.0, 1.0, 2.0
+    w_g = np.zeros((2, 2))
+    w_g[0, 0], w_g[1, 0] = -1.0, 1.0
+    res = G.ke_select(ctx, dev(np.array([[1.0, 0.0]]), False), dev(w_g, False), dev(w_a.T, False), 1, 1)
+    assert res.unioned.cpu().tolist() == [3]
+
+
+def test_route_scores_and_select_experts(ctx):
+    h = O.bf16_round(O.uniform(7, (33, 64), -1, 1))
+    w_g = O.bf16_round(O.uniform(8, (16, 64), -1, 1))
+    p = G.route_scores(ctx, dev(h, True), dev(w_g, True)).cpu().numpy()
+    for t in range(33):
+        np.testing.assert_array_equal(p[t], O.route_scores(h[t], w_g))  # bitwise: same sequential fp64 chain
+    tau = G.select_experts(ctx, torch.from_numpy(p).cuda(), 3).cpu().numpy()
+    for t in range(33):
+        np.testing.assert_array_equal(tau[t], O.select_experts(p[t], 3))
+
+
+def test_invalid_arguments_raise_reference_kinds(ctx):
+    h = dev(np.zeros((2, 4)), False)
+    with pytest.raises(G.MeftError) as e:
+        G.ke_select(ctx, h, dev(np.zeros((3, 4)), False), dev(np.zeros((8, 4)), False), 1, 2)  # 3 does not divide 8
+    assert e.value.kind == "invalid_argument"
+    with pytest.raises(G.MeftError) as e:
+        G.ke_select(ctx, h, dev(np.zeros((2, 4)), False), dev(np.zeros((8, 4)), False), 1, 0)
+    assert e.value.kind == "invalid_argument"
+    with pytest.raises(G.MeftError) as e:
+        G.ke_select(ctx, h, dev(np.zeros((2, 5)), False), dev(np.zeros((8, 4)), False), 1, 1)
+    assert e.value.kind == "ShapeError"
+
+
+def test_selection_is_deterministic(ctx):
+    h, w_a, w_g = inputs(512, 128, 2048, 32, 77, True)
+    a = gpu_ke(ctx, h, w_g, w_a, 4, 16, True)
+    b = gpu_ke(ctx, h, w_g, w_a, 4, 16, True)
+    for x, y in zip(a[:3], b[:3]):
+        np.testing.assert_array_equal(x, y)

@@ -1,0 +1,98 @@
+"""GPU parity of the HBM store: HostStore::init tables, scatter_grads staging and the lazy sparse Adam
+(memtier.cpp:60-228) against the reference fixture / oracle."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_2406_04984_b200 import meft as G
+
+pytestmark = pytest.mark.gpu
+
+
+def test_init_reference_tables_bit_identical(ctx):
+    st = G.Store(ctx, 2, 48, 96, 8, G.STORE_F64)
+    st.init_reference(seed=7)
+    b = 1.0 / np.sqrt(48)
+    for layer in range(2):
+        np.testing.assert_array_equal(st.download(layer, "w_a"), O.uniform(O.mix_seed(7, 0x5000 + 2 * layer), (48, 96), -b, b))
+        np.testing.assert_array_equal(st.download(layer, "w_g"), O.uniform(O.mix_seed(7, 0x5001 + 2 * layer), (8, 48), -b, b))
+        assert float(np.abs(st.download(layer, "w_b")).max()) == 0.0
+        assert st.download(layer, "pair_step").tolist() == [0] * 96
+    if O.ref_available():
+        ref = O.RefStore(2, 48, 96, 8, seed=7)
+        np.testing.assert_array_equal(st.download(1, "w_a"), ref.get(1, "w_a"))
+
+
+def test_scatter_adam_f64_matches_reference_fixture(ctx, golden):
+    g = golden("adam.npz")
+    d, r = int(g["d"]), int(g["r"])
+    st = G.Store(ctx, 1, d, r, 2, G.STORE_F64)
+    st.upload(0, "w_a", g["w_a0"])
+    st.upload(0, "w_b", g["w_b0"])
+    for i in range(int(g["steps"])):
+        s = lambda k: g[f"s{i}__{k}"]  # noqa: E731
+        S = torch.tensor(s("S"), dtype=torch.int32, device="cuda")
+        st.scatter_grads(0, S, torch.from_numpy(s("ga").T.copy()).cuda(), torch.from_numpy(s("gb")).cuda())
+        st.sparse_adam_update(0, float(s("lr")))
+        for name in ("w_a", "w_b", "m_a", "v_a", "m_b", "v_b"):
+            np.testing.assert_allclose(st.download(0, name), s(name), rtol=1e-14, atol=1e-17, err_msg=name)
+        np.testing.assert_array_equal(st.download(0, "pair_step"), s("pair_step"))
+        assert float(np.abs(st.download(0, "stage_a")).max()) == 0.0  # staging cleared (memtier.cpp:200-205)
+        assert st.download(0, "staged").tolist() == [0] * r
+
+
+def test_untouched_pairs_bit_identical_and_overlapping_scatters_sum(ctx):  # test_memtier.cpp:76-134
+    st = G.Store(ctx, 2, 3, 6, 2, G.STORE_F64)
+    st.init_reference(seed=99)
+    before = {(l, n): st.download(l, n) for l in range(2) for n in ("w_a", "w_b", "m_a", "v_a")}
+    ga = np.zeros((2, 3))
+    ga[0, 0] = 0.7
+    gb = np.zeros((2, 3))
+    gb[1, 2] = -0.3
+    st.scatter_grads(1, torch.tensor([0, 3], dtype=torch.int32, device="cuda"), torch.from_numpy(ga).cuda(),
+                     torch.from_numpy(gb).cuda())
+    st.scatter_grads(1, torch.tensor([3, 3], dtype=torch.int32, device="cuda"), torch.from_numpy(ga).cuda(),
+                     torch.from_numpy(ga).cuda())  # repeated index: both entries add, in order
+    stage_b = st.download(1, "stage_b")
+    np.testing.assert_allclose(stage_b[3], gb[1] + 2 * ga[0])
+    st.sparse_adam_update(1, 1e-3)
+    ps = st.download(1, "pair_step")
+    assert ps.tolist() == [1, 0, 0, 1, 0, 0]
+    for (l, n), v in before.items():
+        after = st.download(l, n)
+        cols = [j for j in range(6) if not (l == 1 and j in (0, 3))]
+        if n in ("w_a", "m_a", "v_a"):
+            np.testing.assert_array_equal(after[:, cols], v[:, cols])
+        else:
+            np.testing.assert_array_equal(after[cols, :], v[cols, :])
+    with pytest.raises(G.MeftError) as e:
+        st.scatter_grads(0, torch.tensor([9], dtype=torch.int32, device="cuda"), torch.zeros((1, 3), dtype=torch.float64,
+                         device="cuda"), torch.zeros((1, 3), dtype=torch.float64, device="cuda"))
+    assert e.value.kind == "out_of_range"
+
+
+def test_mixed_store_adam_tolerance(ctx):
+    """MIXED store (fp32 master/moments): |dw_gpu - dw_ref| <= 1e-2*lr + 1e-6*|w| over 3 steps."""
+    d, r, lr = 64, 32, 1e-3
+    w_a = O.bf16_round(O.uniform(1, (d, r), -0.1, 0.1))
+    w_b = O.bf16_round(O.uniform(2, (r, d), -0.1, 0.1))
+    st = G.Store(ctx, 1, d, r, 4, G.STORE_MIXED)
+    st.upload(0, "w_a", w_a)
+    st.upload(0, "w_b", w_b)
+    orc = O.OracleStore(w_a, w_b)
+    for it, S in enumerate([[0, 5, 9], [5, 6, 31], [0, 1, 2, 3, 4, 5]]):
+        ga = O.uniform(10 + it, (d, len(S)), -1, 1).astype(np.float32).astype(np.float64)
+        gb = O.uniform(20 + it, (len(S), d), -1, 1).astype(np.float32).astype(np.float64)
+        st.scatter_grads(0, torch.tensor(S, dtype=torch.int32, device="cuda"),
+                         torch.from_numpy(ga.T.copy()).float().cuda(), torch.from_numpy(gb).float().cuda())
+        st.sparse_adam_update(0, lr)
+        orc.scatter_grads(S, ga, gb)
+        orc.sparse_adam(lr)
+    for name, want, w0 in (("w_a", orc.w_a, w_a), ("w_b", orc.w_b, w_b)):
+        got = st.download(0, name)
+        assert np.all(np.abs((got - w0) - (want - w0)) <= 1e-2 * lr + 1e-6 * np.abs(want)), name
+    np.testing.assert_array_equal(st.download(0, "pair_step"), orc.pair_step)
+    comp = st.tensor(0, "w_a_compute").float().cpu().numpy()  # bf16 copy tracks the fp32 master
+    master = st.download(0, "w_a").T
+    assert np.all(np.abs(comp - master) <= np.abs(master) * 2.0 ** -8)
