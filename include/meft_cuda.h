@@ -73,7 +73,9 @@ typedef struct meft_store meft_store;
 /* ------------------------------------------------------------------ context, errors, memory */
 
 const char* meft_version(void);
-/* device = CUDA ordinal; stream = cudaStream_t or NULL (the context then owns a non-blocking stream). */
+/* device = CUDA ordinal; stream = a cudaStream_t, NULL for the legacy default stream, or MEFT_OWN_STREAM for a
+ * private non-blocking stream owned by the context. */
+#define MEFT_OWN_STREAM ((void*)(intptr_t)-1)
 meft_status meft_ctx_create(int device, void* stream, meft_ctx** out);
 void meft_ctx_destroy(meft_ctx* ctx);
 void* meft_ctx_stream(meft_ctx* ctx);

@@ -443,11 +443,13 @@ meft_status meft_ctx_create(int device, void* stream, meft_ctx** out) {
     std::unique_ptr<meft_ctx> c(new meft_ctx());
     c->device = device;
     meft_status st = guarded(c.get(), [&] {
-        if (stream) {
-            c->stream = static_cast<cudaStream_t>(stream);
-        } else {
+        // NULL is the legacy default stream (what torch reports for its default stream), so work stays
+        // ordered with the caller's framework; pass MEFT_OWN_STREAM to get a private non-blocking stream.
+        if (stream == MEFT_OWN_STREAM) {
             MEFT_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
             c->own_stream = true;
+        } else {
+            c->stream = static_cast<cudaStream_t>(stream);
         }
         MEFT_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
         MEFT_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
