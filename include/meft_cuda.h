@@ -88,6 +88,13 @@ meft_status meft_synchronize(meft_ctx* ctx);
  * fused into their epilogues), 4 sparse Adam (staged compaction + update). read_timing synchronises, returns
  * the accumulated milliseconds and kernel launches per phase since the last read, and resets them. */
 meft_status meft_ctx_set_timing(meft_ctx* ctx, int enable);
+
+/* Selection algorithm for bf16 inputs. AUTO (default): certified tensor-core scoring with exact fp64 re-scoring
+ * of the ambiguous candidates (select_tc.cuh); EXACT: fp64 SIMT scoring of every candidate. Both return the
+ * reference's indices bit for bit; EXACT exists to cross-validate AUTO at full size. */
+#define MEFT_SELECT_AUTO 0
+#define MEFT_SELECT_EXACT 1
+meft_status meft_ctx_set_selection(meft_ctx* ctx, int mode);
 meft_status meft_ctx_read_timing(meft_ctx* ctx, double* ms5, int64_t* launches5);
 
 meft_status meft_device_alloc(meft_ctx* ctx, size_t bytes, void** out);
@@ -213,6 +220,8 @@ typedef struct meft_step_info {
     int64_t kk_eff;
     int warned;         /* the reference would have called warn() */
     int gpu_launches;   /* kernels this step launched */
+    int rescored;       /* ambiguous candidates re-scored exactly by the certified selection */
+    int fallbacks;      /* of those, exact dots that needed the sequential fp64 chain */
 } meft_step_info;
 
 /* One MEFT layer training step in MIXED precision, the trainer's per-layer sequence

@@ -26,6 +26,7 @@ _SIGS = {
     "meft_last_error_index": (I64, [P]),
     "meft_synchronize": (INT, [P]),
     "meft_ctx_set_timing": (INT, [P, INT]),
+    "meft_ctx_set_selection": (INT, [P, INT]),
     "meft_ctx_read_timing": (INT, [P, P, P]),
     "meft_device_alloc": (INT, [P, C.c_size_t, C.POINTER(P)]),
     "meft_device_free": (INT, [P, P]),
@@ -68,7 +69,8 @@ TENSORS = {"w_a": 0, "w_b": 1, "w_g": 2, "m_a": 3, "v_a": 4, "m_b": 5, "v_b": 6,
 
 
 class StepInfo(C.Structure):
-    _fields_ = [("union_size", I64), ("take", I64), ("kk_eff", I64), ("warned", INT), ("gpu_launches", INT)]
+    _fields_ = [("union_size", I64), ("take", I64), ("kk_eff", I64), ("warned", INT), ("gpu_launches", INT),
+                ("rescored", INT), ("fallbacks", INT)]
 
 
 class MeftError(RuntimeError):

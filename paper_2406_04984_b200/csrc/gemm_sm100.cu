@@ -39,7 +39,46 @@ struct KArgs {
     const uint16_t* mask;
     long long ldm;
     const int32_t* row_idx;
+    // grouped mode: G groups; group g owns A rows [g_row_off[g], g_row_off[g+1]) and B rows
+    // [g*g_brows, (g+1)*g_brows); g_tile_off = exclusive scan of its BM-tiles (device arrays).
+    int grouped;
+    int G, g_ntiles, g_brows;
+    const int32_t* g_row_off;
+    const int32_t* g_tile_off;
 };
+
+struct TileInfo {
+    int a_row0;  // first A row (global)
+    int b_row0;  // first B row (global)
+    int m_lim;   // A rows >= m_lim are not part of this tile's problem
+    int n_col0;  // output column of the tile's first B row
+};
+
+__device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int& m_blk, int& n_blk);
+
+__device__ __forceinline__ TileInfo resolve_tile(const KArgs& a, int tile) {
+    TileInfo t;
+    if (!a.grouped) {
+        int mb, nb;
+        tile_coords(tile, a.tiles_m, a.tiles_n, mb, nb);
+        t.a_row0 = mb * BM;
+        t.b_row0 = nb * BN;
+        t.m_lim = a.M;
+        t.n_col0 = t.b_row0;
+    } else {
+        const int mt_global = tile / a.g_ntiles, nt = tile - mt_global * a.g_ntiles;
+        int lo = 0, hi = a.G;  // last g with g_tile_off[g] <= mt_global
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (a.g_tile_off[mid] <= mt_global) lo = mid; else hi = mid;
+        }
+        t.a_row0 = a.g_row_off[lo] + (mt_global - a.g_tile_off[lo]) * BM;
+        t.m_lim = a.g_row_off[lo + 1];
+        t.n_col0 = nt * BN;
+        t.b_row0 = lo * a.g_brows + t.n_col0;
+    }
+    return t;
+}
 
 __device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int& m_blk, int& n_blk) {
     const int group_size = GROUP_M * tiles_n;
@@ -55,8 +94,9 @@ __device__ __forceinline__ void epilogue_chunk(const KArgs& a, int m, int n, con
     const int cnt = min(32, a.N - n);
     switch (a.epi) {
         case EPI_STORE_F32:
-        case EPI_ROWS_ADD_F32: {
-            const long long row = (a.epi == EPI_ROWS_ADD_F32) ? (long long)a.row_idx[m] : (long long)m;
+        case EPI_ROWS_ADD_F32:
+        case EPI_ROWS_STORE_F32: {
+            const long long row = (a.epi != EPI_STORE_F32) ? (long long)a.row_idx[m] : (long long)m;
             const bool acc = a.accumulate || a.epi == EPI_ROWS_ADD_F32;
             float* c = reinterpret_cast<float*>(a.c) + row * a.ldc + n;
             if (cnt == 32) {
@@ -165,7 +205,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    const int num_tiles = args.tiles_m * args.tiles_n;
+    const int num_tiles = args.grouped ? args.g_tile_off[args.G] * args.g_ntiles : args.tiles_m * args.tiles_n;
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
@@ -173,9 +213,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-                int mb, nb;
-                tile_coords(tile, args.tiles_m, args.tiles_n, mb, nb);
-                const int m0 = mb * BM, n0 = nb * BN;
+                const TileInfo ti = resolve_tile(args, tile);
+                const int m0 = ti.a_row0, n0 = ti.b_row0;
                 for (int kb = 0; kb < args.num_kb; ++kb) {
                     mbar_wait(empty + stage, phase ^ 1);
                     uint8_t* sa = smem + stage * STAGE_BYTES;
@@ -243,20 +282,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int q = warp & 3;  // TMEM lane quarter this warp may access
         int it = 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-            int mb, nb;
-            tile_coords(tile, args.tiles_m, args.tiles_n, mb, nb);
+            const TileInfo ti = resolve_tile(args, tile);
             const int acc = it & 1;
             const uint32_t aphase = (it >> 1) & 1;
             mbar_wait(tfull + acc, aphase);
             tc_fence_after();
-            const int m = mb * BM + q * 32 + lane;
+            const int m = ti.a_row0 + q * 32 + lane;
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
                 uint32_t r[32];
                 tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c * 32, r);
                 tmem_ld_wait();
-                const int n = nb * BN + c * 32;
-                if (m < args.M && n < args.N) epilogue_chunk(args, m, n, r);
+                const int n = ti.n_col0 + c * 32;
+                if (m < ti.m_lim && n < args.N) epilogue_chunk(args, m, n, r);
             }
             tc_fence_before();
             __syncwarp();
@@ -301,41 +339,32 @@ CUtensorMap make_map(const void* base, int64_t inner, int64_t outer, int64_t ld,
 }
 
 template <bool A_MN, bool B_MN>
-void launch(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const KArgs& args) {
+void launch(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const KArgs& args, int tiles_bound) {
     static bool attr_set = false;
     if (!attr_set) {
         MEFT_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_bf16<A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              SMEM_BYTES));
         attr_set = true;
     }
-    const int tiles = args.tiles_m * args.tiles_n;
-    const int grid = std::min(tiles, num_sms());
+    const int grid = std::max(1, std::min(tiles_bound, num_sms()));
     k_gemm_bf16<A_MN, B_MN><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ta, tb, args);
     check_launch("k_gemm_bf16");
 }
 
-}  // namespace
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOperand& A, const GemmOperand& B,
-               const GemmEpilogue& epi) {
-    if (M <= 0 || N <= 0) return;
-    if (K <= 0) throw MeftError(2, "gemm_bf16: K must be positive");
-    if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) throw MeftError(1, "gemm_bf16: dimension too large");
-    auto aligned16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-    if (!aligned16(A.ptr) || !aligned16(B.ptr) || (A.ld % 8) || (B.ld % 8))
-        throw MeftError(2, "gemm_bf16: operands need 16-byte aligned base and leading dimension % 8 == 0");
-    if (epi.kind == EPI_STORE_F32 || epi.kind == EPI_ROWS_ADD_F32) {
+void check_epilogue(const GemmEpilogue& epi) {
+    if (epi.kind == EPI_STORE_F32 || epi.kind == EPI_ROWS_ADD_F32 || epi.kind == EPI_ROWS_STORE_F32) {
         if (!aligned16(epi.c) || (epi.ldc % 4)) throw MeftError(2, "gemm_bf16: f32 output alignment");
     } else {
         if (!aligned16(epi.c) || (epi.ldc % 8)) throw MeftError(2, "gemm_bf16: bf16 output alignment");
     }
     if (epi.kind == EPI_MASK_BF16 && (!aligned16(epi.mask) || (epi.ldm % 8)))
         throw MeftError(2, "gemm_bf16: mask alignment");
+}
 
-    const CUtensorMap ta = A.mn_major ? make_map(A.ptr, M, K, A.ld, 64, 64) : make_map(A.ptr, K, M, A.ld, 64, BM);
-    const CUtensorMap tb = B.mn_major ? make_map(B.ptr, N, K, B.ld, 64, 64) : make_map(B.ptr, K, N, B.ld, 64, BN);
-
-    KArgs args;
+KArgs base_args(int64_t M, int64_t N, int64_t K, const GemmEpilogue& epi) {
+    KArgs args{};
     args.M = int(M);
     args.N = int(N);
     args.K = int(K);
@@ -349,15 +378,57 @@ void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOpera
     args.mask = static_cast<const uint16_t*>(epi.mask);
     args.ldm = epi.ldm;
     args.row_idx = epi.row_idx;
+    args.grouped = 0;
+    return args;
+}
 
-    if (!A.mn_major && !B.mn_major)
-        launch<false, false>(st, ta, tb, args);
-    else if (!A.mn_major && B.mn_major)
-        launch<false, true>(st, ta, tb, args);
-    else if (A.mn_major && B.mn_major)
-        launch<true, true>(st, ta, tb, args);
+void dispatch(cudaStream_t st, bool a_mn, bool b_mn, const CUtensorMap& ta, const CUtensorMap& tb, const KArgs& args,
+              int tiles_bound) {
+    if (!a_mn && !b_mn)
+        launch<false, false>(st, ta, tb, args, tiles_bound);
+    else if (!a_mn && b_mn)
+        launch<false, true>(st, ta, tb, args, tiles_bound);
+    else if (a_mn && b_mn)
+        launch<true, true>(st, ta, tb, args, tiles_bound);
     else
-        launch<true, false>(st, ta, tb, args);
+        launch<true, false>(st, ta, tb, args, tiles_bound);
+}
+
+}  // namespace
+
+void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOperand& A, const GemmOperand& B,
+               const GemmEpilogue& epi) {
+    if (M <= 0 || N <= 0) return;
+    if (K <= 0) throw MeftError(2, "gemm_bf16: K must be positive");
+    if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) throw MeftError(1, "gemm_bf16: dimension too large");
+    if (!aligned16(A.ptr) || !aligned16(B.ptr) || (A.ld % 8) || (B.ld % 8))
+        throw MeftError(2, "gemm_bf16: operands need 16-byte aligned base and leading dimension % 8 == 0");
+    check_epilogue(epi);
+    const CUtensorMap ta = A.mn_major ? make_map(A.ptr, M, K, A.ld, 64, 64) : make_map(A.ptr, K, M, A.ld, 64, BM);
+    const CUtensorMap tb = B.mn_major ? make_map(B.ptr, N, K, B.ld, 64, 64) : make_map(B.ptr, K, N, B.ld, 64, BN);
+    const KArgs args = base_args(M, N, K, epi);
+    dispatch(st, A.mn_major, B.mn_major, ta, tb, args, args.tiles_m * args.tiles_n);
+}
+
+void gemm_bf16_grouped(cudaStream_t st, int G, int64_t N, int64_t K, const GemmOperand& A, int64_t a_rows,
+                       const GemmOperand& B, int64_t b_rows, const int32_t* row_off, const int32_t* tile_off,
+                       const GemmEpilogue& epi) {
+    if (G <= 0 || N <= 0 || a_rows <= 0) return;
+    if (A.mn_major || B.mn_major) throw MeftError(2, "gemm_bf16_grouped: K-major operands only");
+    if (!aligned16(A.ptr) || !aligned16(B.ptr) || (A.ld % 8) || (B.ld % 8))
+        throw MeftError(2, "gemm_bf16_grouped: operand alignment");
+    check_epilogue(epi);
+    const CUtensorMap ta = make_map(A.ptr, K, a_rows, A.ld, 64, BM);
+    const CUtensorMap tb = make_map(B.ptr, K, b_rows, B.ld, 64, BN);
+    KArgs args = base_args(a_rows, N, K, epi);
+    args.grouped = 1;
+    args.G = G;
+    args.g_ntiles = int(ceil_div(N, BN));
+    args.g_brows = int(N);
+    args.g_row_off = row_off;
+    args.g_tile_off = tile_off;
+    const int64_t bound = (ceil_div(a_rows, BM) + G) * args.g_ntiles;  // >= device-side tile count
+    dispatch(st, false, false, ta, tb, args, int(std::min<int64_t>(bound, INT32_MAX)));
 }
 
 }  // namespace meft_dev

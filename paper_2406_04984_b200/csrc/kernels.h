@@ -21,6 +21,7 @@ enum GemmEpi : int {
     EPI_RELU_BF16 = 1,     // C bf16 = relu(acc), positive never rounds to zero
     EPI_MASK_BF16 = 2,     // C bf16 = mask(m,n) > 0 ? acc : 0 ; mask bf16 [M x ldm]
     EPI_ROWS_ADD_F32 = 3,  // C f32: C[row_idx[m]*ldc + n] += acc (row_idx unique -> no atomics)
+    EPI_ROWS_STORE_F32 = 4,  // C f32: C[row_idx[m]*ldc + n] = acc
 };
 
 struct GemmEpilogue {
@@ -35,6 +36,13 @@ struct GemmEpilogue {
 
 void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOperand& A, const GemmOperand& B,
                const GemmEpilogue& epi);
+
+// Grouped variant (K-major operands): group g computes rows [row_off[g], row_off[g+1]) of A against the N rows
+// [g*N, (g+1)*N) of B; tile_off = exclusive scan of ceil(rows_g / 128) (device arrays, no host sync). The
+// epilogue sees the global A row m (use EPI_ROWS_STORE_F32 with row_idx to place it) and column n < N.
+void gemm_bf16_grouped(cudaStream_t st, int G, int64_t N, int64_t K, const GemmOperand& A, int64_t a_rows,
+                       const GemmOperand& B, int64_t b_rows, const int32_t* row_off, const int32_t* tile_off,
+                       const GemmEpilogue& epi);
 
 // ---------------------------------------------------------------- fp64 SIMT GEMM (API-fidelity path)
 // C[M x N] = sum_k A(m,k) * B(k,n) over ascending k (fma chain, reference kernels.cpp:34-41), with

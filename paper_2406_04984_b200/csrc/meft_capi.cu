@@ -38,6 +38,8 @@ struct meft_ctx {
     };
     std::unordered_map<std::string, Buf> scratch;
 
+    int selection_mode = MEFT_SELECT_AUTO;
+
     // phase timing (meft_ctx_set_timing)
     bool timing = false;
     struct PhaseRec {
@@ -498,6 +500,14 @@ meft_status meft_ctx_set_timing(meft_ctx* ctx, int enable) {
     });
 }
 
+meft_status meft_ctx_set_selection(meft_ctx* ctx, int mode) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(mode == MEFT_SELECT_AUTO || mode == MEFT_SELECT_EXACT, MEFT_E_INVALID, "unknown selection mode");
+        ctx->selection_mode = mode;
+    });
+}
+
 meft_status meft_ctx_read_timing(meft_ctx* ctx, double* ms5, int64_t* launches5) {
     return guarded(ctx, [&] {
         require_ctx(ctx);
@@ -605,10 +615,10 @@ meft_status meft_ke_select(meft_ctx* ctx, meft_dtype dt, const void* h, const vo
             MEFT_CUDA_CHECK(cudaMemsetAsync(union_size_dev, 0, 4, ctx->stream));
             return;
         }
-        const size_t wsb = select_workspace_bytes(T, M, N, kk_eff);
+        const size_t wsb = select_workspace_bytes(T, d, M, N, kk_eff);
         void* ws = ctx->get("select_ws", wsb);
         ke_select_device(ctx->stream, dcode(dt), h, w_g, keys, T, d, M, N, kk_eff, take, ws, wsb, per_token, tau,
-                         union_idx, union_size_dev);
+                         union_idx, union_size_dev, nullptr, ctx->selection_mode == MEFT_SELECT_AUTO);
     });
 }
 
@@ -624,10 +634,10 @@ meft_status meft_topk_select(meft_ctx* ctx, meft_dtype dt, const void* h, const 
             MEFT_CUDA_CHECK(cudaMemsetAsync(union_size_dev, 0, 4, ctx->stream));
             return;
         }
-        const size_t wsb = select_workspace_bytes(T, M, 1, 1);
+        const size_t wsb = select_workspace_bytes(T, d, M, 1, 1);
         void* ws = ctx->get("select_ws", wsb);
         ke_select_device(ctx->stream, dcode(dt), h, nullptr, keys, T, d, M, 1, 1, take, ws, wsb, per_token, nullptr,
-                         union_idx, union_size_dev);
+                         union_idx, union_size_dev, nullptr, ctx->selection_mode == MEFT_SELECT_AUTO);
     });
 }
 
@@ -935,15 +945,16 @@ static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
                                         : static_cast<int32_t*>(ctx->get("per_token", size_t(T * take) * 4));
     int32_t* uni = union_user ? union_user : static_cast<int32_t*>(ctx->get("union", size_t(M) * 4));
     int32_t* usize = ctx->dev_small + 4;
-    const size_t wsb = select_workspace_bytes(T, M, N, kk_eff);
+    const size_t wsb = select_workspace_bytes(T, d, M, N, kk_eff);
     void* ws = ctx->get("select_ws", wsb);
 
     // meft_ffn: ke_select (experts.cpp:47-117)
     {
         PhaseScope ps(ctx, 0);
-        ke_select_device(st, 2, h, L.c_g, L.c_a, T, d, M, N, kk_eff, take, ws, wsb, per_token, nullptr, uni, usize);
+        ke_select_device(st, 2, h, L.c_g, L.c_a, T, d, M, N, kk_eff, take, ws, wsb, per_token, nullptr, uni, usize,
+                         ctx->dev_small + 5, ctx->selection_mode == MEFT_SELECT_AUTO);
     }
-    MEFT_CUDA_CHECK(cudaMemcpyAsync(ctx->host_small + 4, usize, 4, cudaMemcpyDeviceToHost, st));
+    MEFT_CUDA_CHECK(cudaMemcpyAsync(ctx->host_small + 4, usize, 12, cudaMemcpyDeviceToHost, st));
     MEFT_CUDA_CHECK(cudaStreamSynchronize(st));
     const int64_t su = ctx->host_small[4];
     const int64_t ld = round_up(std::max<int64_t>(su, 1), 64);
@@ -988,6 +999,8 @@ static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
         info->kk_eff = kk_eff;
         info->warned = warned;
         info->gpu_launches = int(launch_counter() - launches0);
+        info->rescored = ctx->host_small[5];
+        info->fallbacks = ctx->host_small[6];
     }
 }
 

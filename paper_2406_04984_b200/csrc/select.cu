@@ -184,7 +184,7 @@ __global__ void k_topk_experts(const double* __restrict__ scores, int T, int N, 
 
 // Single CTA: off = exclusive scan(counts), tile_off = exclusive scan(ceil(counts/ST)), cursor = 0.
 __global__ void k_bucket_scan(const int32_t* __restrict__ counts, int N, int32_t* __restrict__ off,
-                              int32_t* __restrict__ tile_off, int32_t* __restrict__ cursor) {
+                              int32_t* __restrict__ tile_off, int32_t* __restrict__ cursor, int tile) {
     __shared__ int s_run, s_trun;
     if (threadIdx.x == 0) {
         s_run = 0;
@@ -194,7 +194,7 @@ __global__ void k_bucket_scan(const int32_t* __restrict__ counts, int N, int32_t
     for (int base = 0; base < N; base += blockDim.x) {
         const int i = base + threadIdx.x;
         const int c = i < N ? counts[i] : 0;
-        const int tcount = (c + ST - 1) / ST;
+        const int tcount = (c + tile - 1) / tile;
         // block-wide inclusive scan via warp scans
         int v = c, tv = tcount;
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -399,6 +399,8 @@ void score_dispatch(cudaStream_t st, int dtype, const void* h, int d, const void
 
 }  // namespace
 
+#include "select_tc.cuh"
+
 void score_rows(cudaStream_t st, int dtype, const void* h, int64_t T, int64_t d, const void* w, int64_t rows,
                 double* scores) {
     if (T <= 0 || rows <= 0) return;
@@ -406,7 +408,8 @@ void score_rows(cudaStream_t st, int dtype, const void* h, int64_t T, int64_t d,
                    1, scores);
 }
 
-size_t select_workspace_bytes(int64_t T, int64_t M, int64_t N, int64_t kk_eff) {
+namespace {
+size_t exact_workspace_bytes(int64_t T, int64_t M, int64_t N, int64_t kk_eff) {
     const int64_t E = M / N;
     size_t b = 0;
     auto add = [&](size_t x) { b += (x + 255) & ~size_t(255); };
@@ -420,10 +423,154 @@ size_t select_workspace_bytes(int64_t T, int64_t M, int64_t N, int64_t kk_eff) {
     return b;
 }
 
+size_t cert_workspace_bytes(int64_t T, int64_t d, int64_t M, int64_t N, int64_t kk_eff) {
+    const int64_t E = M / N;
+    size_t b = 0;
+    auto add = [&](size_t x) { b += (x + 255) & ~size_t(255); };
+    add(T * round_up(N, 4) * 4);  // approximate router scores (fp32)
+    add((T + N + M) * 4);         // row norms of h, w_g, keys
+    add(T * kk_eff * 4);          // tau
+    add(T * kk_eff * 4);          // entries
+    add((N + 1) * 4 * 4);         // counts, off, tile_off, cursor
+    add(T * kk_eff * d * 2);      // token rows bucketed by expert (bf16)
+    add(T * kk_eff * E * 4);      // approximate candidate scores (fp32)
+    add(M);                       // union flags
+    add(((M + 1023) / 1024 + 1) * 4);
+    return b;
+}
+
+bool certified_ok(int dtype, int64_t d, int64_t M, int64_t N, int64_t kk_eff) {
+    const int64_t E = M / N;
+    return dtype == 2 && d % 8 == 0 && d <= 32768 && E % 4 == 0 && kk_eff * E <= CERT_MAX_C && N <= 2048 &&
+           kk_eff <= 64;
+}
+
+void ke_select_exact(cudaStream_t st, int dtype, const void* h, const void* w_g, const void* keys, int64_t T,
+                     int64_t d, int64_t M, int64_t N, int64_t kk_eff, int64_t take, void* ws, size_t ws_bytes,
+                     int32_t* per_token, int32_t* tau_out, int32_t* union_idx, int32_t* union_size);
+}  // namespace
+
+size_t select_workspace_bytes(int64_t T, int64_t d, int64_t M, int64_t N, int64_t kk_eff) {
+    return std::max(exact_workspace_bytes(T, M, N, kk_eff), cert_workspace_bytes(T, d, M, N, kk_eff));
+}
+
+// Certified tensor-core selection (select_tc.cuh): bit-exact with the reference, no fp64 GEMM.
+static void ke_select_certified(cudaStream_t st, const void* h_, const void* w_g_, const void* keys_, int64_t T,
+                                int64_t d, int64_t M, int64_t N, int64_t kk_eff, int64_t take, void* ws,
+                                int32_t* per_token, int32_t* tau_out, int32_t* union_idx, int32_t* union_size,
+                                int32_t* stats) {
+    const uint16_t* h = static_cast<const uint16_t*>(h_);
+    const uint16_t* wg = static_cast<const uint16_t*>(w_g_);
+    const uint16_t* keys = static_cast<const uint16_t*>(keys_);
+    const int64_t E = M / N, C = kk_eff * E, ldp = round_up(N, 4);
+    uint8_t* p = static_cast<uint8_t*>(ws);
+    auto take_buf = [&](size_t x) {
+        void* r = p;
+        p += (x + 255) & ~size_t(255);
+        return r;
+    };
+    float* P = static_cast<float*>(take_buf(T * ldp * 4));
+    float* hn = static_cast<float*>(take_buf((T + N + M) * 4));
+    float* gn = hn + T;
+    float* kn = gn + N;
+    int32_t* tau = static_cast<int32_t*>(take_buf(T * kk_eff * 4));
+    int32_t* entries = static_cast<int32_t*>(take_buf(T * kk_eff * 4));
+    int32_t* counts = static_cast<int32_t*>(take_buf((N + 1) * 4 * 4));
+    int32_t* off = counts + (N + 1);
+    int32_t* tile_off = off + (N + 1);
+    int32_t* cursor = tile_off + (N + 1);
+    uint16_t* hs = static_cast<uint16_t*>(take_buf(T * kk_eff * d * 2));
+    float* cand = static_cast<float*>(take_buf(T * C * 4));
+    uint8_t* flags = static_cast<uint8_t*>(take_buf(M));
+    int32_t* boff = static_cast<int32_t*>(take_buf(((M + 1023) / 1024 + 1) * 4));
+    const double cb = cert_bound_coeff(int(d));
+
+    MEFT_CUDA_CHECK(cudaMemsetAsync(flags, 0, M, st));
+    if (stats) MEFT_CUDA_CHECK(cudaMemsetAsync(stats, 0, 2 * sizeof(int32_t), st));
+    k_row_norms<<<int((T * 32 + 255) / 256), 256, 0, st>>>(h, T, int(d), hn);
+    check_launch("k_row_norms");
+    k_row_norms<<<int((M * 32 + 255) / 256), 256, 0, st>>>(keys, M, int(d), kn);
+    check_launch("k_row_norms");
+    if (N == 1) {
+        // flat top-K (adapter.cpp:42-84): one candidate block of all M keys per token
+        MEFT_CUDA_CHECK(cudaMemsetAsync(tau, 0, T * 4, st));
+        GemmEpilogue e;
+        e.kind = EPI_STORE_F32;
+        e.c = cand;
+        e.ldc = M;
+        gemm_bf16(st, T, M, d, GemmOperand{h, d, false}, GemmOperand{keys, d, false}, e);
+    } else {
+        k_row_norms<<<int((N * 32 + 255) / 256), 256, 0, st>>>(wg, N, int(d), gn);
+        check_launch("k_row_norms");
+        GemmEpilogue e;  // approximate router scores on the tensor cores
+        e.kind = EPI_STORE_F32;
+        e.c = P;
+        e.ldc = ldp;
+        gemm_bf16(st, T, N, d, GemmOperand{h, d, false}, GemmOperand{wg, d, false}, e);
+        MEFT_CUDA_CHECK(cudaMemsetAsync(counts, 0, N * 4, st));
+        const int wpb = 4;
+        const size_t rsm = size_t(wpb) * (kk_eff + 2 * N) * 4 + size_t(wpb) * N * 8;
+        static bool rattr = false;
+        if (!rattr) {
+            MEFT_CUDA_CHECK(cudaFuncSetAttribute(k_router_certified, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 200 * 1024));
+            rattr = true;
+        }
+        k_router_certified<<<int((T + wpb - 1) / wpb), wpb * 32, rsm, st>>>(P, int(ldp), hn, gn, cb, h, wg, int(d),
+                                                                          int(T), int(N), int(kk_eff), tau, counts,
+                                                                          stats);
+        check_launch("k_router_certified");
+        k_bucket_scan<<<1, 1024, 0, st>>>(counts, int(N), off, tile_off, cursor, 128);
+        check_launch("k_bucket_scan");
+        k_bucket_fill<<<int((T * kk_eff + 255) / 256), 256, 0, st>>>(tau, int(T), int(kk_eff), off, cursor, entries);
+        check_launch("k_bucket_fill");
+        const int rows = int(T * kk_eff);
+        k_gather_tokens<<<std::max(1, std::min(rows / 8 + 1, num_sms() * 16)), 256, 0, st>>>(h, int(d), entries, rows,
+                                                                                              int(kk_eff), hs);
+        check_launch("k_gather_tokens");
+        GemmEpilogue eg;  // grouped by expert: cand[entry][j] = h_token . key_{g*E + j}
+        eg.kind = EPI_ROWS_STORE_F32;
+        eg.c = cand;
+        eg.ldc = E;
+        eg.row_idx = entries;
+        gemm_bf16_grouped(st, int(N), E, d, GemmOperand{hs, d, false}, rows, GemmOperand{keys, d, false}, M, off,
+                          tile_off, eg);
+    }
+    const int P2 = next_pow2(int(C)), TP2 = next_pow2(int(take));
+    const size_t tsm = size_t(P2) * 20 + size_t(TP2) * 4 + size_t(d) * 2 + 16;
+    static bool tattr = false;
+    if (!tattr) {
+        MEFT_CUDA_CHECK(cudaFuncSetAttribute(k_topk_certified, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        tattr = true;
+    }
+    if (tsm > 220 * 1024) throw MeftError(2, "ke_select: candidate set too large for the certified path");
+    k_topk_certified<<<int(T), 256, tsm, st>>>(cand, tau, int(kk_eff), int(E), int(C), P2, int(take), TP2, hn, kn, cb,
+                                               h, keys, int(d), per_token, flags, stats);
+    check_launch("k_topk_certified");
+    if (tau_out) MEFT_CUDA_CHECK(cudaMemcpyAsync(tau_out, tau, T * kk_eff * 4, cudaMemcpyDeviceToDevice, st));
+    compact_flags(st, flags, M, union_idx, union_size, boff);
+}
+
 void ke_select_device(cudaStream_t st, int dtype, const void* h, const void* w_g, const void* keys, int64_t T,
                       int64_t d, int64_t M, int64_t N, int64_t kk_eff, int64_t take, void* ws, size_t ws_bytes,
-                      int32_t* per_token, int32_t* tau_out, int32_t* union_idx, int32_t* union_size) {
-    if (ws_bytes < select_workspace_bytes(T, M, N, kk_eff)) throw MeftError(6, "ke_select: workspace too small");
+                      int32_t* per_token, int32_t* tau_out, int32_t* union_idx, int32_t* union_size,
+                      int32_t* stats, bool allow_certified) {
+    if (ws_bytes < select_workspace_bytes(T, d, M, N, kk_eff)) throw MeftError(6, "ke_select: workspace too small");
+    if (allow_certified && certified_ok(dtype, d, M, N, kk_eff)) {
+        ke_select_certified(st, h, w_g, keys, T, d, M, N, kk_eff, take, ws, per_token, tau_out, union_idx, union_size,
+                            stats);
+        return;
+    }
+    if (stats) MEFT_CUDA_CHECK(cudaMemsetAsync(stats, 0, 2 * sizeof(int32_t), st));
+    ke_select_exact(st, dtype, h, w_g, keys, T, d, M, N, kk_eff, take, ws, ws_bytes, per_token, tau_out, union_idx,
+                    union_size);
+}
+
+namespace {
+void ke_select_exact(cudaStream_t st, int dtype, const void* h, const void* w_g, const void* keys, int64_t T,
+                     int64_t d, int64_t M, int64_t N, int64_t kk_eff, int64_t take, void* ws, size_t ws_bytes,
+                     int32_t* per_token, int32_t* tau_out, int32_t* union_idx, int32_t* union_size) {
+    (void)ws_bytes;
     const int64_t E = M / N;
     const int64_t C = kk_eff * E;
     uint8_t* p = static_cast<uint8_t*>(ws);
@@ -458,7 +605,7 @@ void ke_select_device(cudaStream_t st, int dtype, const void* h, const void* w_g
         MEFT_CUDA_CHECK(cudaMemsetAsync(counts, 0, N * 4, st));
         k_topk_experts<<<int((T * 32 + 255) / 256), 256, 0, st>>>(rscores, int(T), int(N), int(kk_eff), tau, counts);
         check_launch("k_topk_experts");
-        k_bucket_scan<<<1, 1024, 0, st>>>(counts, int(N), off, tile_off, cursor);
+        k_bucket_scan<<<1, 1024, 0, st>>>(counts, int(N), off, tile_off, cursor, ST);
         check_launch("k_bucket_scan");
         k_bucket_fill<<<int((T * kk_eff + 255) / 256), 256, 0, st>>>(tau, int(T), int(kk_eff), off, cursor, entries);
         check_launch("k_bucket_fill");
@@ -481,6 +628,7 @@ void ke_select_device(cudaStream_t st, int dtype, const void* h, const void* w_g
     k_flag_write<<<nb, 1024, 0, st>>>(flags, int(M), boff, union_idx);
     check_launch("k_flag_write");
 }
+}  // namespace
 
 void route_topk_device(cudaStream_t st, const double* scores, int64_t T, int64_t N, int64_t kk, int32_t* tau) {
     k_topk_experts<<<int((T * 32 + 255) / 256), 256, 0, st>>>(scores, int(T), int(N), int(kk), tau, nullptr);

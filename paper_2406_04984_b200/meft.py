@@ -76,6 +76,10 @@ class Context:
 
     PHASES = ("select", "gather", "ffn_forward", "ffn_backward", "adam")
 
+    def set_selection(self, exact: bool):
+        """exact=True forces fp64 SIMT scoring of every candidate (cross-validation of the certified path)."""
+        self.check(lib().meft_ctx_set_selection(self.h, 1 if exact else 0))
+
     def set_timing(self, on: bool):
         self.check(lib().meft_ctx_set_timing(self.h, int(on)))
 
@@ -305,7 +309,7 @@ class Store:
         self.ctx.check(lib().meft_layer_step(self.ctx.h, self.h, layer, _p(h), _p(grad_out), T, kk, k, beta1, beta2,
                                              eps, lr, _p(out), _p(grad_h), _p(per), _p(uni), C.byref(info)))
         res = dict(union_size=info.union_size, take=info.take, kk_eff=info.kk_eff, warned=bool(info.warned),
-                   gpu_launches=info.gpu_launches)
+                   gpu_launches=info.gpu_launches, rescored=info.rescored, fallbacks=info.fallbacks)
         if want_selection:
             res["per_token"] = per
             res["unioned"] = uni[: info.union_size]

@@ -118,3 +118,69 @@ def test_selection_is_deterministic(ctx):
     b = gpu_ke(ctx, h, w_g, w_a, 4, 16, True)
     for x, y in zip(a[:3], b[:3]):
         np.testing.assert_array_equal(x, y)
+
+
+# ---------------------------------------------------------------- certified tensor-core selection
+
+def _rand_bf16(gen, shape, scale):
+    return ((torch.rand(shape, generator=gen, device="cuda") * 2 - 1) * scale).to(torch.bfloat16).contiguous()
+
+
+def _both_paths(ctx, h, w_g, keys, kk, k):
+    a = G.ke_select(ctx, h, w_g, keys, kk, k)
+    ctx.set_selection(exact=True)
+    try:
+        b = G.ke_select(ctx, h, w_g, keys, kk, k)
+    finally:
+        ctx.set_selection(exact=False)
+    return a, b
+
+
+@pytest.mark.slow
+def test_certified_equals_exact_at_baseline_cfg2(ctx):
+    """All 8192 tokens of the LLaMA-shape layer: certified tensor-core selection == fp64 SIMT selection."""
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    d, M, N, K, kk, T = 4096, 65536, 256, 128, 4, 8192
+    h = _rand_bf16(gen, (T, d), 1.0)
+    keys = _rand_bf16(gen, (M, d), 1 / 64)
+    w_g = _rand_bf16(gen, (N, d), 1 / 64)
+    a, b = _both_paths(ctx, h, w_g, keys, kk, K)
+    assert torch.equal(a.tau, b.tau)
+    assert torch.equal(a.per_token, b.per_token)
+    assert torch.equal(a.unioned, b.unioned)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_certified_resolves_forced_near_ties(ctx, seed):
+    """Duplicate and 1-ulp-apart keys/experts force every boundary decision through exact re-scoring;
+    a few tokens mix huge and tiny coordinates so the exactness certificate fails and the sequential fp64
+    chain is used. The result must still equal the oracle bit for bit."""
+    rs = np.random.RandomState(seed)
+    T, d, N, E, kk, k = 96, 64, 8, 32, 3, 20
+    M = N * E
+    w_a = O.bf16_round(rs.uniform(-1, 1, (d, M)) / 8)
+    w_a[:, 1::2] = w_a[:, 0::2]                      # exact duplicate keys inside each expert
+    w_a[0, 2::4] = O.bf16_round(w_a[0, 2::4] * (1 + 2.0 ** -7))  # neighbours one bf16 ulp apart
+    w_g = O.bf16_round(rs.uniform(-1, 1, (N, d)) / 8)
+    w_g[1] = w_g[0]                                   # duplicate experts: router ties
+    h = O.bf16_round(rs.uniform(-1, 1, (T, d)))
+    h[:8, 0] = 1.0
+    h[:8, 1:] = O.bf16_round(h[:8, 1:] * 2.0 ** -70)  # products 2^70 apart: certificate fails
+    want = O.ke_select(h, w_g, w_a, kk, k)
+    for exact in (False, True):
+        ctx.set_selection(exact=exact)
+        try:
+            per, tau, uni, _ = gpu_ke(ctx, h, w_g, w_a, kk, k, True)
+        finally:
+            ctx.set_selection(exact=False)
+        np.testing.assert_array_equal(tau, want["tau"])
+        np.testing.assert_array_equal(per, want["per_token"])
+        np.testing.assert_array_equal(uni, want["unioned"])
+
+
+def test_certified_flat_topk(ctx):
+    h, w_a, _ = inputs(200, 256, 4096, 1, 91, True)
+    want = O.topk_select(h, w_a, 48)
+    flat = G.topk_select(ctx, dev(h, True), dev(w_a.T, True), 48)
+    np.testing.assert_array_equal(flat.per_token.cpu().numpy(), want["per_token"])
+    np.testing.assert_array_equal(flat.unioned.cpu().numpy(), want["unioned"])
