@@ -216,10 +216,13 @@ def our_arm(args, rank, world, local_rank):
     ev0.record()
     launches = 0
     usizes = []
+    rescored = fallbacks = 0
     for _ in range(args.steps):
         info = step()
         launches += info["gpu_launches"]
         usizes.append(info["union_size"])
+        rescored += info["rescored"]
+        fallbacks += info["fallbacks"]
     ev1.record()
     torch.cuda.synchronize()
     clocks.stop()
@@ -311,6 +314,9 @@ def our_arm(args, rank, world, local_rank):
         "hbm_kernels": {"adam_gbs": adam_bytes / (adam_ms * 1e-3) / 1e9 if adam_ms else None,
                         "gather_gbs": gather_bytes / (gather_ms * 1e-3) / 1e9 if gather_ms else None,
                         "peak_gbs": hbm},
+        "selection": {"algorithm": "certified tcgen05 scoring + exact fp64 re-scoring (bit-exact indices)",
+                      "rescored_per_token": rescored / (args.steps * T),
+                      "sequential_fallbacks_per_step": fallbacks / args.steps},
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
         "gpu_launches": launches,

@@ -68,6 +68,24 @@ __device__ __forceinline__ uint16_t relu_bf16_bits(float z) {
 
 __device__ __forceinline__ uint32_t pack_bf16x2(uint16_t lo, uint16_t hi) { return uint32_t(lo) | (uint32_t(hi) << 16); }
 
+// One lazy-Adam entry update (memtier.cpp:176-185) in fp32 with every rounding spelled out, so the standalone
+// Adam kernel and the Adam-fused GEMM epilogue produce bit-identical weights and moments.
+//   scale = lr / (1 - b1^t),  inv_c2 = 1 / (1 - b2^t)
+struct AdamCoef {
+    float scale, inv_c2;
+};
+__device__ __forceinline__ AdamCoef adam_coef(float b1, float b2, float lr, int t) {
+    const float c1 = float(1.0 - pow(double(b1), double(t)));
+    const float c2 = float(1.0 - pow(double(b2), double(t)));
+    return AdamCoef{__fdiv_rn(lr, c1), __fdiv_rn(1.0f, c2)};
+}
+__device__ __forceinline__ void adam_update(float& w, float& m, float& v, float g, float b1, float b2, float eps,
+                                            AdamCoef k) {
+    m = __fadd_rn(__fmul_rn(b1, m), __fmul_rn(__fsub_rn(1.0f, b1), g));
+    v = __fadd_rn(__fmul_rn(b2, v), __fmul_rn(__fmul_rn(__fsub_rn(1.0f, b2), g), g));
+    w = __fsub_rn(w, __fdiv_rn(__fmul_rn(k.scale, m), __fadd_rn(__fsqrt_rn(__fmul_rn(v, k.inv_c2)), eps)));
+}
+
 // ------------------------------------------------------------------ shared-memory / mbarrier PTX
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

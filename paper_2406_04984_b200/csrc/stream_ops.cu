@@ -79,7 +79,9 @@ __global__ void k_mark(uint8_t* __restrict__ staged, const int32_t* __restrict__
 // ---------------------------------------------------------------- sparse Adam (memtier.cpp:187-228)
 
 // Mixed-precision store: fp32 master/m/v/stage, bf16 compute copy. One CTA per staged pair updates the key
-// row and the value row (the pair shares one step counter, memtier.hpp:87-89), zeroes its staging and flag.
+// row and/or the value row (`tables`: bit 0 keys, bit 1 values) with the pair's shared step counter
+// (memtier.hpp:87-89), zeroes their staging; with `bump` it also advances the counter and clears the flag
+// (the layer step updates the value rows first without bump, the key rows afterwards with it).
 __global__ void __launch_bounds__(256) k_adam_mixed(const int32_t* __restrict__ rows, const int32_t* count_dev,
                                                     int count, int64_t d, float* __restrict__ wa, float* __restrict__ ma,
                                                     float* __restrict__ va, float* __restrict__ sa,
@@ -87,25 +89,25 @@ __global__ void __launch_bounds__(256) k_adam_mixed(const int32_t* __restrict__ 
                                                     float* __restrict__ mb, float* __restrict__ vb,
                                                     float* __restrict__ sb, uint16_t* __restrict__ cb,
                                                     int32_t* __restrict__ step, uint8_t* __restrict__ staged, float b1,
-                                                    float b2, float eps, float lr) {
+                                                    float b2, float eps, float lr, int tables, int bump) {
     const int n = count_dev ? *count_dev : count;
-    __shared__ float s_c1, s_c2;
+    __shared__ AdamCoef s_k;
     for (int r = blockIdx.x; r < n; r += gridDim.x) {
         const int64_t j = rows[r];
         __syncthreads();
         if (threadIdx.x == 0) {
             const int t = step[j] + 1;
-            step[j] = t;
-            staged[j] = 0;
-            s_c1 = float(1.0 - pow(double(b1), double(t)));
-            s_c2 = float(1.0 - pow(double(b2), double(t)));
+            if (bump) {
+                step[j] = t;
+                staged[j] = 0;
+            }
+            s_k = adam_coef(b1, b2, lr, t);
         }
         __syncthreads();
-        const float c1 = s_c1, inv_c2 = 1.0f / s_c2;
-        const float ob1 = 1.0f - b1, ob2 = 1.0f - b2;
-        const float step_scale = lr / c1;
+        const AdamCoef k = s_k;
 #pragma unroll
         for (int tab = 0; tab < 2; ++tab) {
+            if (!(tables & (1 << tab))) continue;
             float4* w4 = reinterpret_cast<float4*>((tab ? wb : wa) + j * d);
             float4* m4 = reinterpret_cast<float4*>((tab ? mb : ma) + j * d);
             float4* v4 = reinterpret_cast<float4*>((tab ? vb : va) + j * d);
@@ -119,11 +121,7 @@ __global__ void __launch_bounds__(256) k_adam_mixed(const int32_t* __restrict__ 
                 float* wp = &w.x;
                 const float* gp = &g.x;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    mp[q] = b1 * mp[q] + ob1 * gp[q];
-                    vp[q] = b2 * vp[q] + ob2 * gp[q] * gp[q];
-                    wp[q] -= step_scale * mp[q] / (sqrtf(vp[q] * inv_c2) + eps);
-                }
+                for (int q = 0; q < 4; ++q) adam_update(wp[q], mp[q], vp[q], gp[q], b1, b2, eps, k);
                 m4[i] = m;
                 v4[i] = v;
                 w4[i] = w;
@@ -282,11 +280,12 @@ void mark_rows(cudaStream_t st, uint8_t* staged, const int32_t* idx, const int32
 
 void adam_mixed(cudaStream_t st, const int32_t* rows, const int32_t* count_dev, int64_t count, int64_t d, float* wa,
                 float* ma, float* va, float* sa, uint16_t* ca, float* wb, float* mb, float* vb, float* sb,
-                uint16_t* cb, int32_t* step, uint8_t* staged, double b1, double b2, double eps, double lr) {
+                uint16_t* cb, int32_t* step, uint8_t* staged, double b1, double b2, double eps, double lr, int tables,
+                bool bump) {
     if (d % 4) throw MeftError(2, "adam: d must be a multiple of 4 in mixed precision");
     const int grid = std::max(1, std::min<int>(int(count > 0 ? count : num_sms() * 8), num_sms() * 8));
     k_adam_mixed<<<grid, 256, 0, st>>>(rows, count_dev, int(count), d, wa, ma, va, sa, ca, wb, mb, vb, sb, cb, step,
-                                       staged, float(b1), float(b2), float(eps), float(lr));
+                                       staged, float(b1), float(b2), float(eps), float(lr), tables, bump ? 1 : 0);
     check_launch("k_adam_mixed");
 }
 

@@ -91,6 +91,24 @@ def test_layer_step_host_buffers_match_device_path(ctx):
         np.testing.assert_array_equal(a, b)  # same kernels, same order: bitwise deterministic
 
 
+def test_pending_zero_staging_is_neutral(ctx):
+    """Two layer steps with and without pre-uploaded (zero) staging must agree bit for bit: the weight-gradient
+    epilogues add into staging and the lazy Adam consumes it (stage = 0 + g)."""
+    w_a, w_g, w_b, h, gr = cfg1_inputs(T=128)
+    res = []
+    for dirty in (False, True):
+        st = make_store(ctx, w_a, w_g, w_b, 64)
+        if dirty:
+            st.upload(0, "stage_b", np.zeros((4096, 512)))  # marks the staging as pending
+        for _ in range(2):
+            st.layer_step(0, bf16_dev(h), bf16_dev(gr), 4, 32, 1e-3)
+        torch.cuda.synchronize()
+        res.append({n: st.download(0, n) for n in ("w_a", "w_b", "m_a", "v_b", "pair_step")})
+        res[-1]["c_a"] = st.tensor(0, "w_a_compute").float().cpu().numpy()
+    for n in res[0]:
+        np.testing.assert_array_equal(res[0][n], res[1][n], err_msg=n)
+
+
 @pytest.mark.slow
 def test_layer_step_cfg2_properties(ctx):
     """BASELINE cfg2 (d=4096, M=65536, N=256, K=128, T=8192): exact indices on a token sample against the
