@@ -178,6 +178,18 @@ meft_status meft_base_ffn_backward(meft_ctx* ctx, const double* grad_out, const 
 meft_status meft_matmul_f64(meft_ctx* ctx, const double* A, const double* B, int64_t m, int64_t k, int64_t n,
                             double* C);
 
+/* Layout/elementwise helpers of the fp64 API path: dst[cols x rows] = src[rows x cols]ᵀ (kernels.cpp:94-101);
+ * y = act(x) with act 0 SiLU (x*sigmoid(x), kernels.cpp:15-17), 1 ReLU (kernels.cpp:78-84). */
+meft_status meft_transpose_f64(meft_ctx* ctx, const double* src, double* dst, int64_t rows, int64_t cols);
+meft_status meft_activation_f64(meft_ctx* ctx, int act, const double* x, double* y, int64_t n);
+
+/* Lazy Adam over arbitrary fp64 row tables (the router rows of sparse_adam_update, memtier.cpp:211-227):
+ * for each row r in rows[0..n): t = ++step[r]; Adam on w/m/v[r,:] with gradient stage[r,:]; stage[r,:] = 0;
+ * staged[r] = 0. step is int64 [table rows]; staged uint8. */
+meft_status meft_adam_rows_f64(meft_ctx* ctx, double* w, double* m, double* v, double* stage, int64_t* step,
+                               uint8_t* staged, const int32_t* rows, int64_t n, int64_t d, double beta1, double beta2,
+                               double eps, double lr);
+
 /* ------------------------------------------------------------------ HBM-resident store */
 
 /* HostStore for `layers` layers (memtier.hpp:108-133) resident in HBM. All tensors start at zero; use

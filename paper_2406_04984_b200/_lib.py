@@ -47,6 +47,9 @@ _SIGS = {
     "meft_base_ffn_forward": (INT, [P, P, P, P, I64, I64, I64, INT, P, P]),
     "meft_base_ffn_backward": (INT, [P, P, P, P, P, I64, I64, I64, INT, P]),
     "meft_matmul_f64": (INT, [P, P, P, I64, I64, I64, P]),
+    "meft_transpose_f64": (INT, [P, P, P, I64, I64]),
+    "meft_activation_f64": (INT, [P, INT, P, P, I64]),
+    "meft_adam_rows_f64": (INT, [P, P, P, P, P, P, P, P, I64, I64, D, D, D, D]),
     "meft_store_create": (INT, [P, I64, I64, I64, I64, INT, C.POINTER(P)]),
     "meft_store_destroy": (None, [P]),
     "meft_store_info": (INT, [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64), C.POINTER(I64), C.POINTER(INT)]),

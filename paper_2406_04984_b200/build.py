@@ -65,5 +65,57 @@ def build(verbose: bool = False, force: bool = False) -> str:
     return LIB
 
 
+DROPIN_SRC = os.path.join(PKG, "dropin")
+
+
+def build_dropin(verbose: bool = False, force: bool = False) -> str:
+    """libmeft_dropin.so: the reference's C++ API (include/meft/*.hpp) implemented over the C ABI."""
+    build()
+    srcs = sorted(os.path.join(DROPIN_SRC, f) for f in os.listdir(DROPIN_SRC) if f.endswith(".cpp"))
+    hdrs = [os.path.join(DROPIN_SRC, f) for f in os.listdir(DROPIN_SRC) if f.endswith(".hpp")]
+    hdrs += [os.path.join(ROOT, "include", "meft", f) for f in os.listdir(os.path.join(ROOT, "include", "meft"))]
+    hdrs.append(os.path.join(ROOT, "include", "meft_cuda.h"))
+    if force or _needs(DROPIN_LIB, srcs + hdrs + [LIB]):
+        cmd = [HOST_CXX, "-O2", "-std=c++17", "-fPIC", "-shared", "-Wall", "-Wno-unused-function",
+               "-I" + os.path.join(ROOT, "include"), "-o", DROPIN_LIB] + srcs + \
+              ["-L" + PKG, "-lmeft_cuda", "-Wl,-rpath,$ORIGIN"]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"g++ failed:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    return DROPIN_LIB
+
+
+REF_TESTS = ("test_numerics", "test_adapter", "test_experts", "test_memtier")
+DROPIN_TEST_BIN = os.path.join(ROOT, "build", "dropin_tests")
+
+
+def build_reference_tests(ref_proj: str = "/root/reference/proj", verbose: bool = False) -> list:
+    """Compile the reference's own unit tests, UNMODIFIED, against the drop-in shim (test infrastructure).
+    Needs the reference sources (this container); the binaries travel with the snapshot to the GPU box."""
+    if not os.path.isdir(os.path.join(ref_proj, "tests")):
+        return []
+    lib = build_dropin(verbose)
+    os.makedirs(DROPIN_TEST_BIN, exist_ok=True)
+    out = []
+    for t in REF_TESTS:
+        src = os.path.join(ref_proj, "tests", t + ".cpp")
+        exe = os.path.join(DROPIN_TEST_BIN, t)
+        if _needs(exe, [src, lib]):
+            cmd = [HOST_CXX, "-O1", "-std=c++20", "-w", "-I" + os.path.join(ROOT, "tests", "dropin"),
+                   "-I" + os.path.join(ROOT, "include"), "-o", exe, src, "-L" + PKG, "-lmeft_dropin", "-lmeft_cuda",
+                   "-Wl,-rpath," + PKG + ",-rpath,$ORIGIN/../../paper_2406_04984_b200"]
+            if verbose:
+                print(" ".join(cmd), file=sys.stderr)
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            if r.returncode != 0:
+                raise RuntimeError(f"g++ failed:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+        out.append(exe)
+    return out
+
+
 if __name__ == "__main__":
     print(build(verbose=True, force="--force" in sys.argv))
+    print(build_dropin(verbose=True, force="--force" in sys.argv))
+    print(build_reference_tests(verbose=True))

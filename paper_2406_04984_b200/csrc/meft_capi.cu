@@ -714,6 +714,30 @@ meft_status meft_matmul_f64(meft_ctx* ctx, const double* A, const double* B, int
     });
 }
 
+meft_status meft_transpose_f64(meft_ctx* ctx, const double* src, double* dst, int64_t rows, int64_t cols) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        transpose8(ctx->stream, src, dst, rows, cols);
+    });
+}
+
+meft_status meft_activation_f64(meft_ctx* ctx, int act, const double* x, double* y, int64_t n) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(act == 0 || act == 1, MEFT_E_INVALID, "activation: 0 SiLU or 1 ReLU");
+        act_forward(ctx->stream, x, y, n, act);
+    });
+}
+
+meft_status meft_adam_rows_f64(meft_ctx* ctx, double* w, double* m, double* v, double* stage, int64_t* step,
+                               uint8_t* staged, const int32_t* rows, int64_t n, int64_t d, double beta1, double beta2,
+                               double eps, double lr) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        adam_rows_f64(ctx->stream, w, m, v, stage, step, staged, rows, n, d, beta1, beta2, eps, lr);
+    });
+}
+
 // ------------------------------------------------------------------ store
 
 meft_status meft_store_create(meft_ctx* ctx, int64_t layers, int64_t d, int64_t pairs, int64_t experts,

@@ -173,6 +173,37 @@ __global__ void __launch_bounds__(256) k_adam_f64(const int32_t* __restrict__ ro
     }
 }
 
+// Lazy Adam over one fp64 row table with int64 per-row steps (router rows, memtier.cpp:211-227).
+__global__ void __launch_bounds__(256) k_adam_rows_f64(double* __restrict__ w, double* __restrict__ m,
+                                                       double* __restrict__ v, double* __restrict__ stage,
+                                                       int64_t* __restrict__ step, uint8_t* __restrict__ staged,
+                                                       const int32_t* __restrict__ rows, int n, int64_t d, double b1,
+                                                       double b2, double eps, double lr) {
+    __shared__ double s_c1, s_c2;
+    for (int r = blockIdx.x; r < n; r += gridDim.x) {
+        const int64_t j = rows[r];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int64_t t = ++step[j];
+            staged[j] = 0;
+            s_c1 = 1.0 - pow(b1, double(t));
+            s_c2 = 1.0 - pow(b2, double(t));
+        }
+        __syncthreads();
+        const double c1 = s_c1, c2 = s_c2;
+        for (int64_t i = threadIdx.x; i < d; i += blockDim.x) {
+            const int64_t q = j * d + i;
+            const double gi = stage[q];
+            const double mi = b1 * m[q] + (1.0 - b1) * gi;
+            const double vi = b2 * v[q] + (1.0 - b2) * gi * gi;
+            m[q] = mi;
+            v[q] = vi;
+            w[q] -= lr * (mi / c1) / (sqrt(vi / c2) + eps);
+            stage[q] = 0.0;
+        }
+    }
+}
+
 // ---------------------------------------------------------------- conversions
 
 __global__ void k_f64_to_bf16(const double* __restrict__ s, uint16_t* __restrict__ d, int64_t n) {
@@ -296,6 +327,14 @@ void adam_f64(cudaStream_t st, const int32_t* rows, const int32_t* count_dev, in
     k_adam_f64<<<grid, 256, 0, st>>>(rows, count_dev, int(count), d, wa, ma, va, sa, wb, mb, vb, sb, step, staged, b1,
                                      b2, eps, lr);
     check_launch("k_adam_f64");
+}
+
+void adam_rows_f64(cudaStream_t st, double* w, double* m, double* v, double* stage, int64_t* step, uint8_t* staged,
+                   const int32_t* rows, int64_t n, int64_t d, double b1, double b2, double eps, double lr) {
+    if (n <= 0) return;
+    const int grid = std::max(1, std::min<int>(int(n), num_sms() * 8));
+    k_adam_rows_f64<<<grid, 256, 0, st>>>(w, m, v, stage, step, staged, rows, int(n), d, b1, b2, eps, lr);
+    check_launch("k_adam_rows_f64");
 }
 
 void convert(cudaStream_t st, int ddt, void* dst, int sdt, const void* src, int64_t n) {

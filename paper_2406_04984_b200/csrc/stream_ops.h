@@ -18,6 +18,8 @@ void adam_mixed(cudaStream_t st, const int32_t* rows, const int32_t* count_dev, 
 void adam_f64(cudaStream_t st, const int32_t* rows, const int32_t* count_dev, int64_t count, int64_t d, double* wa,
               double* ma, double* va, double* sa, double* wb, double* mb, double* vb, double* sb, int32_t* step,
               uint8_t* staged, double b1, double b2, double eps, double lr);
+void adam_rows_f64(cudaStream_t st, double* w, double* m, double* v, double* stage, int64_t* step, uint8_t* staged,
+                   const int32_t* rows, int64_t n, int64_t d, double b1, double b2, double eps, double lr);
 void convert(cudaStream_t st, int ddt, void* dst, int sdt, const void* src, int64_t n);
 void convert_index(cudaStream_t st, bool to64, void* dst, const void* src, int64_t n);
 void act_forward(cudaStream_t st, const double* x, double* y, int64_t n, int act);   // 0 SiLU, 1 ReLU

@@ -1,0 +1,99 @@
+// Drop-in shim plumbing (see device.hpp).
+#include "device.hpp"
+
+#include <cmath>
+#include <stdexcept>
+
+namespace meft::dropin {
+
+std::recursive_mutex& api_mutex() {
+    static std::recursive_mutex m;
+    return m;
+}
+
+meft_ctx* ctx() {
+    static meft_ctx* c = [] {
+        meft_ctx* p = nullptr;
+        const meft_status st = meft_ctx_create(0, MEFT_OWN_STREAM, &p);
+        if (st != MEFT_OK) throw std::runtime_error(std::string("meft: cannot create device context: ") +
+                                                    meft_last_error(nullptr));
+        return p;
+    }();
+    return c;
+}
+
+void check(meft_status st) {
+    if (st == MEFT_OK) return;
+    const std::string msg = meft_last_error(ctx());
+    switch (st) {
+        case MEFT_E_SHAPE: throw ShapeError(msg);
+        case MEFT_E_INVALID: throw std::invalid_argument(msg);
+        case MEFT_E_RANGE: throw std::out_of_range(msg);
+        case MEFT_E_LOGIC: throw std::logic_error(msg);
+        case MEFT_E_NONFINITE: throw std::runtime_error(msg);
+        default: throw std::runtime_error("meft device error: " + msg);
+    }
+}
+
+DevBuf::DevBuf(size_t bytes) : n_(bytes) {
+    if (bytes) check(meft_device_alloc(ctx(), bytes, &p_));
+}
+
+DevBuf::~DevBuf() {
+    if (p_) meft_device_free(ctx(), p_);
+}
+
+DevBuf& DevBuf::operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+        if (p_) meft_device_free(ctx(), p_);
+        p_ = o.p_;
+        n_ = o.n_;
+        o.p_ = nullptr;
+        o.n_ = 0;
+    }
+    return *this;
+}
+
+DevBuf upload(const double* host, size_t count) {
+    DevBuf b(count * sizeof(double));
+    if (count) check(meft_copy_to_device(ctx(), b.get(), host, count * sizeof(double)));
+    return b;
+}
+
+DevBuf upload(const Matrix& m) { return upload(m.data.data(), m.data.size()); }
+
+DevBuf upload_indices(const std::vector<index_t>& idx) {
+    std::vector<int32_t> tmp(idx.begin(), idx.end());
+    DevBuf b(tmp.size() * sizeof(int32_t));
+    if (!tmp.empty()) check(meft_copy_to_device(ctx(), b.get(), tmp.data(), tmp.size() * sizeof(int32_t)));
+    check(meft_synchronize(ctx()));  // tmp is released on return
+    return b;
+}
+
+void download(double* host, const DevBuf& b, size_t count) {
+    if (count) check(meft_copy_to_host(ctx(), host, b.get(), count * sizeof(double)));
+}
+
+Matrix download_matrix(const DevBuf& b, index_t rows, index_t cols) {
+    Matrix m(rows, cols);
+    download(m.data.data(), b, m.data.size());
+    return m;
+}
+
+void download_i32(std::vector<int32_t>& host, const DevBuf& b, size_t count) {
+    host.resize(count);
+    if (count) check(meft_copy_to_host(ctx(), host.data(), b.get(), count * sizeof(int32_t)));
+}
+
+DevBuf transposed(const DevBuf& src, index_t rows, index_t cols) {
+    DevBuf out(size_t(rows * cols) * sizeof(double));
+    if (rows * cols > 0) check(meft_transpose_f64(ctx(), src.as<double>(), out.as<double>(), rows, cols));
+    return out;
+}
+
+void require_finite(const Matrix& m, const char* where) {
+    for (double x : m.data)
+        if (!std::isfinite(x)) throw std::runtime_error(std::string(where) + ": non-finite entry");
+}
+
+}  // namespace meft::dropin
