@@ -429,6 +429,7 @@ size_t cert_workspace_bytes(int64_t T, int64_t d, int64_t M, int64_t N, int64_t 
     auto add = [&](size_t x) { b += (x + 255) & ~size_t(255); };
     add(T * round_up(N, 4) * 4);  // approximate router scores (fp32)
     add((T + N + M) * 4);         // row norms of h, w_g, keys
+    add((T + N + M) * 4);         // their minimum LSB exponents
     add(T * kk_eff * 4);          // tau
     add(T * kk_eff * 4);          // entries
     add((N + 1) * 4 * 4);         // counts, off, tile_off, cursor
@@ -436,6 +437,12 @@ size_t cert_workspace_bytes(int64_t T, int64_t d, int64_t M, int64_t N, int64_t 
     add(T * kk_eff * E * 4);      // approximate candidate scores (fp32)
     add(M);                       // union flags
     add(((M + 1023) / 1024 + 1) * 4);
+    const int64_t C = kk_eff * E, take_max = C;
+    add(T * take_max * 4 + T * 4);  // certain members + counts
+    add(T * C * 4 + T * 4);         // ambiguous candidates + counts
+    add(T * C * 8);                 // their exact scores
+    add(2 * T * C * 4);             // (token, position) pairs grouped by expert
+    add((N + 1) * 4 * 4);           // per-expert ambiguous counts, offsets, tiles, cursor
     return b;
 }
 
@@ -473,6 +480,9 @@ static void ke_select_certified(cudaStream_t st, const void* h_, const void* w_g
     float* hn = static_cast<float*>(take_buf((T + N + M) * 4));
     float* gn = hn + T;
     float* kn = gn + N;
+    int32_t* hl = static_cast<int32_t*>(take_buf((T + N + M) * 4));  // per-row minimum LSB exponents
+    int32_t* gl = hl + T;
+    int32_t* kl = gl + N;
     int32_t* tau = static_cast<int32_t*>(take_buf(T * kk_eff * 4));
     int32_t* entries = static_cast<int32_t*>(take_buf(T * kk_eff * 4));
     int32_t* counts = static_cast<int32_t*>(take_buf((N + 1) * 4 * 4));
@@ -487,9 +497,9 @@ static void ke_select_certified(cudaStream_t st, const void* h_, const void* w_g
 
     MEFT_CUDA_CHECK(cudaMemsetAsync(flags, 0, M, st));
     if (stats) MEFT_CUDA_CHECK(cudaMemsetAsync(stats, 0, 2 * sizeof(int32_t), st));
-    k_row_norms<<<int((T * 32 + 255) / 256), 256, 0, st>>>(h, T, int(d), hn);
+    k_row_norms<<<int((T * 32 + 255) / 256), 256, 0, st>>>(h, T, int(d), hn, hl);
     check_launch("k_row_norms");
-    k_row_norms<<<int((M * 32 + 255) / 256), 256, 0, st>>>(keys, M, int(d), kn);
+    k_row_norms<<<int((M * 32 + 255) / 256), 256, 0, st>>>(keys, M, int(d), kn, kl);
     check_launch("k_row_norms");
     if (N == 1) {
         // flat top-K (adapter.cpp:42-84): one candidate block of all M keys per token
@@ -500,7 +510,7 @@ static void ke_select_certified(cudaStream_t st, const void* h_, const void* w_g
         e.ldc = M;
         gemm_bf16(st, T, M, d, GemmOperand{h, d, false}, GemmOperand{keys, d, false}, e);
     } else {
-        k_row_norms<<<int((N * 32 + 255) / 256), 256, 0, st>>>(wg, N, int(d), gn);
+        k_row_norms<<<int((N * 32 + 255) / 256), 256, 0, st>>>(wg, N, int(d), gn, gl);
         check_launch("k_row_norms");
         GemmEpilogue e;  // approximate router scores on the tensor cores
         e.kind = EPI_STORE_F32;
@@ -516,7 +526,8 @@ static void ke_select_certified(cudaStream_t st, const void* h_, const void* w_g
                                                  200 * 1024));
             rattr = true;
         }
-        k_router_certified<<<int((T + wpb - 1) / wpb), wpb * 32, rsm, st>>>(P, int(ldp), hn, gn, cb, h, wg, int(d),
+        k_router_certified<<<int((T + wpb - 1) / wpb), wpb * 32, rsm, st>>>(P, int(ldp), hn, gn, hl, gl, cb, h, wg,
+                                                                          int(d),
                                                                           int(T), int(N), int(kk_eff), tau, counts,
                                                                           stats);
         check_launch("k_router_certified");
@@ -536,17 +547,40 @@ static void ke_select_certified(cudaStream_t st, const void* h_, const void* w_g
         gemm_bf16_grouped(st, int(N), E, d, GemmOperand{hs, d, false}, rows, GemmOperand{keys, d, false}, M, off,
                           tile_off, eg);
     }
+    // certified top-K: classify -> exact re-scoring grouped by expert -> finalize
+    int32_t* sure = static_cast<int32_t*>(take_buf(T * C * 4 + T * 4));
+    int32_t* n_sure = sure + T * C;
+    int32_t* amb = static_cast<int32_t*>(take_buf(T * C * 4 + T * 4));
+    int32_t* n_amb = amb + T * C;
+    double* xs = static_cast<double*>(take_buf(T * C * 8));
+    int32_t* pair_t = static_cast<int32_t*>(take_buf(2 * T * C * 4));
+    int32_t* pair_a = pair_t + T * C;
+    int32_t* acount = static_cast<int32_t*>(take_buf((N + 1) * 4 * 4));
+    int32_t* aoff = acount + (N + 1);
+    int32_t* atile = aoff + (N + 1);
+    int32_t* acur = atile + (N + 1);
     const int P2 = next_pow2(int(C)), TP2 = next_pow2(int(take));
-    const size_t tsm = size_t(P2) * 20 + size_t(TP2) * 4 + size_t(d) * 2 + 16;
-    static bool tattr = false;
-    if (!tattr) {
-        MEFT_CUDA_CHECK(cudaFuncSetAttribute(k_topk_certified, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        tattr = true;
+    const size_t csm = size_t(C) * 5 + 16;  // classify: u32 keys + u8 membership
+    if (csm > 200 * 1024) throw MeftError(2, "ke_select: candidate set too large for the certified path");
+    static bool cattr = false;
+    if (!cattr) {
+        MEFT_CUDA_CHECK(cudaFuncSetAttribute(k_topk_classify, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        cattr = true;
     }
-    if (tsm > 220 * 1024) throw MeftError(2, "ke_select: candidate set too large for the certified path");
-    k_topk_certified<<<int(T), 256, tsm, st>>>(cand, tau, int(kk_eff), int(E), int(C), P2, int(take), TP2, hn, kn, cb,
-                                               h, keys, int(d), per_token, flags, stats);
-    check_launch("k_topk_certified");
+    MEFT_CUDA_CHECK(cudaMemsetAsync(acount, 0, N * 4, st));
+    k_topk_classify<<<int(T), 256, csm, st>>>(cand, tau, int(kk_eff), int(E), int(C), P2, int(take), hn, kn, cb, sure,
+                                              n_sure, amb, n_amb, acount);
+    check_launch("k_topk_classify");
+    k_bucket_scan<<<1, 1024, 0, st>>>(acount, int(N), aoff, atile, acur, 1);
+    check_launch("k_bucket_scan");
+    k_amb_fill<<<int(T), 128, 0, st>>>(amb, n_amb, int(C), int(E), aoff, acur, pair_t, pair_a);
+    check_launch("k_amb_fill");
+    k_rescore_pairs<<<num_sms() * 8, 256, 0, st>>>(pair_t, pair_a, aoff + N, amb, int(C), h, keys, int(d), hn, kn, hl,
+                                                    kl, xs, stats);
+    check_launch("k_rescore_pairs");
+    k_topk_finalize<<<int(T), 128, size_t(TP2) * 4, st>>>(sure, n_sure, amb, n_amb, xs, int(C), int(take), TP2,
+                                                           per_token, flags);
+    check_launch("k_topk_finalize");
     if (tau_out) MEFT_CUDA_CHECK(cudaMemcpyAsync(tau_out, tau, T * kk_eff * 4, cudaMemcpyDeviceToDevice, st));
     compact_flags(st, flags, M, union_idx, union_size, boff);
 }

@@ -81,24 +81,65 @@ __device__ double exact_dot_warp(const uint16_t* __restrict__ a, const uint16_t*
 }
 
 // ||row||_2 of bf16 rows (fp64 sum of squares, rounded up), one warp per row.
-__global__ void k_row_norms(const uint16_t* __restrict__ x, int64_t rows, int d, float* __restrict__ out) {
+// Also the row's minimum LSB exponent over its nonzero entries (INT32_MAX for an all-zero row): with
+// lsb(h_t) + lsb(w_j) and ||h_t|| ||w_j|| the exactness certificate of a dot can be decided per row pair.
+__global__ void k_row_norms(const uint16_t* __restrict__ x, int64_t rows, int d, float* __restrict__ out,
+                            int32_t* __restrict__ minlsb) {
     const int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (r >= rows) return;
     const uint16_t* p = x + r * d;
     double s = 0.0;
+    int lsb = INT32_MAX;
     for (int k = lane; k < d; k += 32) {
-        const double v = bfd(p[k]);
+        const uint16_t b = p[k];
+        const double v = bfd(b);
         s = fma(v, v, s);
+        if (b & 0x7FFF) lsb = min(lsb, bf16_lsb_exp(b));
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) out[r] = __double2float_ru(sqrt(s) * (1.0 + 0x1p-20));
+    for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        lsb = min(lsb, __shfl_xor_sync(0xffffffffu, lsb, o));
+    }
+    if (lane == 0) {
+        out[r] = __double2float_ru(sqrt(s) * (1.0 + 0x1p-20));
+        if (minlsb) minlsb[r] = lsb;
+    }
+}
+
+// exact_dot_warp with a row-level certificate: when every product is a multiple of 2^(lsb_a + lsb_b) and
+// ||a|| ||b|| (>= sum|p|) < 2^(lsb_a + lsb_b + 53), all partial sums in any order are exact, so a plain warp
+// fma reduction equals the reference's sequential chain. Otherwise the per-product path decides.
+__device__ __forceinline__ double exact_dot_rows(const uint16_t* __restrict__ a, const uint16_t* __restrict__ b, int d,
+                                                 int lane, int lsb_a, int lsb_b, float na, float nb, int* fallbacks) {
+    if (lsb_a == INT32_MAX || lsb_b == INT32_MAX) return 0.0;  // an all-zero row: every product is +-0
+    const int lsb = lsb_a + lsb_b;
+    if (lsb + 53 < 1000 && double(na) * double(nb) * (1.0 + 0x1p-30) < ldexp(1.0, lsb + 53) &&
+        (d % 8 == 0) && ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) % 16 == 0)) {
+        const uint4* a4 = reinterpret_cast<const uint4*>(a);
+        const uint4* b4 = reinterpret_cast<const uint4*>(b);
+        double s = 0.0;
+        for (int v = lane; v < d / 8; v += 32) {
+            const uint4 x = a4[v], y = __ldg(b4 + v);
+            const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                s = fma(double(__uint_as_float(xs[q] << 16)), double(__uint_as_float(ys[q] << 16)), s);
+                s = fma(double(__uint_as_float(xs[q] & 0xFFFF0000u)), double(__uint_as_float(ys[q] & 0xFFFF0000u)), s);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        return s;
+    }
+    return exact_dot_warp(a, b, d, lane, fallbacks);
 }
 
 // Warp per token: certified top-kk experts of the approximate router scores P [T x ldp].
 __global__ void k_router_certified(const float* __restrict__ P, int ldp, const float* __restrict__ hn,
-                                   const float* __restrict__ gn, double cb, const uint16_t* __restrict__ h,
+                                   const float* __restrict__ gn, const int32_t* __restrict__ hl,
+                                   const int32_t* __restrict__ gl, double cb, const uint16_t* __restrict__ h,
                                    const uint16_t* __restrict__ wg, int d, int T, int N, int kk,
                                    int32_t* __restrict__ tau, int32_t* __restrict__ counts, int* __restrict__ stats) {
     extern __shared__ uint8_t sm_raw[];
@@ -181,8 +222,9 @@ __global__ void k_router_certified(const float* __restrict__ P, int ldp, const f
         if (lane == 0)
             for (int r = 0; r < kk; ++r) out[r] = top[r];
     } else {
-        for (int a = 0; a < na; ++a) ax[a] = exact_dot_warp(h + int64_t(t) * d, wg + int64_t(aidx[a]) * d, d, lane,
-                                                            stats ? stats + 1 : nullptr);
+        for (int a = 0; a < na; ++a)
+            ax[a] = exact_dot_rows(h + int64_t(t) * d, wg + int64_t(aidx[a]) * d, d, lane, hl[t], gl[aidx[a]], hn[t],
+                                   gn[aidx[a]], stats ? stats + 1 : nullptr);
         __syncwarp();
         if (lane == 0) {
             if (stats) atomicAdd(stats, na);
@@ -230,67 +272,110 @@ __global__ void k_gather_tokens(const uint16_t* __restrict__ h, int d, const int
     }
 }
 
-// CTA per token: certified top-`take` of the C = kk*E approximate candidate scores.
-// smem: ks f32[P2] | is i32[P2] | alist i32[P2] | ax f64[P2] | sel i32[TP2] | hrow bf16[d]
+// ---- certified per-token top-K, in three kernels so the exact re-scoring can be grouped by expert (key rows
+// stay hot in L2) — and, in the expert-sharded layer, executed on the rank that owns the keys.
+
+// orderable uint32 of a float: larger float <=> larger key
+__device__ __forceinline__ uint32_t float_key(float f) {
+    const uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// K1, CTA per token: radix-select the approximate top-`take` (order: score desc, then candidate position asc —
+// positions ascend with the global index because tau is ascending), derive L_in / U_out, and split the
+// candidates into certain members (sure[t][0..n_sure)) and ambiguous ones (amb[t][0..n_amb), global indices).
+// amb_count[idx / E] counts ambiguous pairs per expert for the grouping.
+// smem: key u32[C] | in_top u8[C]
 __global__ void __launch_bounds__(256)
-    k_topk_certified(const float* __restrict__ cand, const int32_t* __restrict__ tau, int kk, int E, int C, int P2,
-                     int take, int TP2, const float* __restrict__ hn, const float* __restrict__ kn, double cb,
-                     const uint16_t* __restrict__ h, const uint16_t* __restrict__ keys, int d,
-                     int32_t* __restrict__ per_token, uint8_t* __restrict__ flags, int* __restrict__ stats) {
+    k_topk_classify(const float* __restrict__ cand, const int32_t* __restrict__ tau, int kk, int E, int C, int P2,
+                    int take, const float* __restrict__ hn, const float* __restrict__ kn, double cb,
+                    int32_t* __restrict__ sure, int32_t* __restrict__ n_sure, int32_t* __restrict__ amb,
+                    int32_t* __restrict__ n_amb, int32_t* __restrict__ amb_count) {
     extern __shared__ __align__(16) uint8_t sm[];
-    double* ax = reinterpret_cast<double*>(sm);
-    float* ks = reinterpret_cast<float*>(ax + P2);
-    int* is = reinterpret_cast<int*>(ks + P2);
-    int* alist = is + P2;
-    int* sel = alist + P2;
-    uint16_t* hrow = reinterpret_cast<uint16_t*>(sel + TP2);
+    uint32_t* key = reinterpret_cast<uint32_t*>(sm);
+    uint8_t* in_top = reinterpret_cast<uint8_t*>(key + C);
     __shared__ double w_lin[32], w_uout[32];
-    __shared__ int s_na, s_nsel, s_nsure;
+    __shared__ int hist[256], w_cnt[32];
+    __shared__ uint32_t s_prefix;
+    __shared__ int s_remaining, s_na, s_ns;
     const int t = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     const float* c = cand + int64_t(t) * C;
-    for (int i = tid; i < P2; i += blockDim.x) {
-        if (i < C) {
-            const int slot = i / E, j = i - slot * E;
-            ks[i] = c[i];
-            is[i] = tau[int64_t(t) * kk + slot] * E + j;
-        } else {
-            ks[i] = -FLT_MAX;
-            is[i] = INT32_MAX;
-        }
-    }
+    for (int i = tid; i < C; i += blockDim.x) key[i] = float_key(c[i]);
     if (tid == 0) {
         s_na = 0;
-        s_nsel = 0;
-        s_nsure = 0;
+        s_ns = 0;
+        s_prefix = 0;
+        s_remaining = take;
     }
     __syncthreads();
-    // bitonic sort into the reference order on the approximate scores (padding sorts last)
-    for (int k = 2; k <= P2; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = tid; i < P2; i += blockDim.x) {
-                const int p = i ^ j;
-                if (p > i) {
-                    const float a = ks[i], b = ks[p];
-                    const int ia = is[i], ib = is[p];
-                    const bool b_first = (b > a) || (b == a && ib < ia);
-                    if (((i & k) == 0) ? b_first : !b_first) {
-                        ks[i] = b;
-                        ks[p] = a;
-                        is[i] = ib;
-                        is[p] = ia;
+    // radix select of the take-th largest key, 8 bits at a time from the top
+    uint32_t mask = 0;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (int b = tid; b < 256; b += blockDim.x) hist[b] = 0;
+        __syncthreads();
+        const uint32_t prefix = s_prefix;
+        for (int i = tid; i < C; i += blockDim.x)
+            if ((key[i] & mask) == prefix) atomicAdd(&hist[(key[i] >> shift) & 255], 1);
+        __syncthreads();
+        if (warp == 0) {  // digits descending: lane l owns digits 255-8l .. 248-8l
+            int part = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) part += hist[255 - 8 * lane - q];
+            int incl = part;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int x = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += x;
+            }
+            const int rem = s_remaining;
+            const int excl = incl - part;
+            if (excl < rem && rem <= incl) {  // exactly one lane
+                int cum = excl;
+                for (int q = 0; q < 8; ++q) {
+                    const int dgt = 255 - 8 * lane - q;
+                    if (cum + hist[dgt] >= rem) {
+                        s_prefix = prefix | (uint32_t(dgt) << shift);
+                        s_remaining = rem - cum;
+                        break;
                     }
+                    cum += hist[dgt];
                 }
             }
-            __syncthreads();
         }
+        mask |= 255u << shift;
+        __syncthreads();
     }
-    // L_in = min over Top (s - e), U_out = max over the rest (s + e)
+    const uint32_t kth = s_prefix;
+    const int need_eq = s_remaining;  // how many candidates equal to the take-th key belong to Top
+    // rank among equals by position: block exclusive scan of the equality flags over contiguous chunks
+    const int chunk = (C + blockDim.x - 1) / blockDim.x, c0 = tid * chunk, c1 = min(C, c0 + chunk);
+    int eq = 0;
+    for (int i = c0; i < c1; ++i) eq += key[i] == kth;
+    int incl = eq;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int x = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += x;
+    }
+    if (lane == 31) w_cnt[warp] = incl;
+    __syncthreads();
+    int before = incl - eq;
+    for (int w = 0; w < warp; ++w) before += w_cnt[w];
+    for (int i = c0; i < c1; ++i) {
+        const bool e_ = key[i] == kth;
+        in_top[i] = key[i] > kth || (e_ && before < need_eq);
+        before += e_;
+    }
+    __syncthreads();
     const double he = cb * double(hn[t]);
+    const int32_t* my_tau = tau + int64_t(t) * kk;
     double lin = DBL_MAX, uout = -DBL_MAX;
     for (int i = tid; i < C; i += blockDim.x) {
-        const double e = he * double(kn[is[i]]);
-        if (i < take) lin = fmin(lin, double(ks[i]) - e);
-        else uout = fmax(uout, double(ks[i]) + e);
+        const int slot = i / E;
+        const int gi = my_tau[slot] * E + (i - slot * E);
+        const double e = he * double(kn[gi]);
+        if (in_top[i]) lin = fmin(lin, double(c[i]) - e);
+        else uout = fmax(uout, double(c[i]) + e);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -308,41 +393,88 @@ __global__ void __launch_bounds__(256)
         lin = fmin(lin, w_lin[w]);
         uout = fmax(uout, w_uout[w]);
     }
-    // classify: certain members go straight to sel; ambiguous ones to alist
+    int32_t* my_sure = sure + int64_t(t) * take;
+    int32_t* my_amb = amb + int64_t(t) * C;
     for (int i = tid; i < C; i += blockDim.x) {
-        const double e = he * double(kn[is[i]]);
-        if (i < take) {
-            if (double(ks[i]) - e <= uout) alist[atomicAdd(&s_na, 1)] = is[i];
-            else {
-                sel[atomicAdd(&s_nsel, 1)] = is[i];
-                atomicAdd(&s_nsure, 1);
-            }
-        } else if (double(ks[i]) + e >= lin) {
-            alist[atomicAdd(&s_na, 1)] = is[i];
+        const int slot = i / E;
+        const int gi = my_tau[slot] * E + (i - slot * E);
+        const double e = he * double(kn[gi]);
+        const bool top = in_top[i];
+        const bool ambiguous = top ? (double(c[i]) - e <= uout) : (double(c[i]) + e >= lin);
+        if (ambiguous) {
+            my_amb[atomicAdd(&s_na, 1)] = gi;
+            atomicAdd(&amb_count[gi / E], 1);
+        } else if (top) {
+            my_sure[atomicAdd(&s_ns, 1)] = gi;
         }
     }
     __syncthreads();
-    const int na = s_na;
-    if (na > 0) {
-        for (int k = tid; k < d; k += blockDim.x) hrow[k] = h[int64_t(t) * d + k];
-        __syncthreads();
-        for (int a = warp; a < na; a += nwarps)
-            ax[a] = exact_dot_warp(hrow, keys + int64_t(alist[a]) * d, d, lane, stats ? stats + 1 : nullptr);
-        __syncthreads();
-        const int need = take - s_nsure;
-        for (int a = tid; a < na; a += blockDim.x) {  // rank within A by the exact reference order
-            const double xa = ax[a];
-            const int ia = alist[a];
-            int rank = 0;
-            for (int b = 0; b < na; ++b) rank += (ax[b] > xa) || (ax[b] == xa && alist[b] < ia);
-            if (rank < need) sel[atomicAdd(&s_nsel, 1)] = ia;
-        }
-        if (tid == 0 && stats) atomicAdd(stats, na);
+    if (tid == 0) {
+        n_amb[t] = s_na;
+        n_sure[t] = s_ns;
+    }
+}
+
+// K2a, CTA per token: bucket the token's ambiguous pairs by expert (pair_t / pair_a = token, position in amb[t]).
+__global__ void k_amb_fill(const int32_t* __restrict__ amb, const int32_t* __restrict__ n_amb, int C, int E,
+                           const int32_t* __restrict__ off, int32_t* __restrict__ cursor, int32_t* __restrict__ pair_t,
+                           int32_t* __restrict__ pair_a) {
+    const int t = blockIdx.x;
+    const int n = n_amb[t];
+    for (int a = threadIdx.x; a < n; a += blockDim.x) {
+        const int e = amb[int64_t(t) * C + a] / E;
+        const int pos = off[e] + atomicAdd(&cursor[e], 1);
+        pair_t[pos] = t;
+        pair_a[pos] = a;
+    }
+}
+
+// K2b, warp per ambiguous pair, pairs in expert order: the reference's exact fp64 score.
+__global__ void k_rescore_pairs(const int32_t* __restrict__ pair_t, const int32_t* __restrict__ pair_a,
+                                const int32_t* __restrict__ total, const int32_t* __restrict__ amb, int C,
+                                const uint16_t* __restrict__ h, const uint16_t* __restrict__ keys, int d,
+                                const float* __restrict__ hn, const float* __restrict__ kn,
+                                const int32_t* __restrict__ hl, const int32_t* __restrict__ kl,
+                                double* __restrict__ x, int* __restrict__ stats) {
+    const int lane = threadIdx.x & 31;
+    const int n = *total;
+    for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < n; p += (gridDim.x * blockDim.x) >> 5) {
+        const int t = pair_t[p], a = pair_a[p];
+        const int idx = amb[int64_t(t) * C + a];
+        const double v = exact_dot_rows(h + int64_t(t) * d, keys + int64_t(idx) * d, d, lane, hl[t], kl[idx], hn[t],
+                                        kn[idx], stats ? stats + 1 : nullptr);
+        if (lane == 0) x[int64_t(t) * C + a] = v;
+    }
+    if (stats && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(stats, n);
+}
+
+// K3, CTA per token: sure members + the best (take - n_sure) ambiguous ones by the exact reference order,
+// emitted ascending (experts.cpp:94-105) into per_token, and marked in the union bitmap.
+__global__ void __launch_bounds__(128)
+    k_topk_finalize(const int32_t* __restrict__ sure, const int32_t* __restrict__ n_sure,
+                    const int32_t* __restrict__ amb, const int32_t* __restrict__ n_amb, const double* __restrict__ x,
+                    int C, int take, int TP2, int32_t* __restrict__ per_token, uint8_t* __restrict__ flags) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    int* sel = reinterpret_cast<int*>(sm);
+    __shared__ int s_n;
+    const int t = blockIdx.x, tid = threadIdx.x;
+    const int ns = n_sure[t], na = n_amb[t], need = take - ns;
+    const int32_t* my_amb = amb + int64_t(t) * C;
+    const double* my_x = x + int64_t(t) * C;
+    for (int i = tid; i < ns; i += blockDim.x) sel[i] = sure[int64_t(t) * take + i];
+    if (tid == 0) s_n = ns;
+    __syncthreads();
+    for (int a = tid; a < na; a += blockDim.x) {
+        const double xa = my_x[a];
+        const int ia = my_amb[a];
+        int rank = 0;
+        for (int b = 0; b < na; ++b) rank += (my_x[b] > xa) || (my_x[b] == xa && my_amb[b] < ia);
+        if (rank < need) sel[atomicAdd(&s_n, 1)] = ia;
     }
     __syncthreads();
     for (int i = take + tid; i < TP2; i += blockDim.x) sel[i] = INT32_MAX;
     __syncthreads();
-    for (int k = 2; k <= TP2; k <<= 1) {  // ascending output (experts.cpp:104)
+    for (int k = 2; k <= TP2; k <<= 1) {
         for (int j = k >> 1; j > 0; j >>= 1) {
             for (int i = tid; i < TP2; i += blockDim.x) {
                 const int p = i ^ j;
