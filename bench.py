@@ -8,8 +8,10 @@ scatter_grads -> sparse_adam_update (the reference trainer's per-layer sequence)
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N>1 (torchrun, one rank per GPU): every rank runs its own layer replica on its own T tokens ("scaling":
-"weak"); the expert-sharded layer is described in DESIGN.md §6. Rank 0 prints one JSON line.
+N>1 (torchrun, one rank per GPU): the expert-sharded layer (paper_2406_04984_b200/sharded.py) —
+each rank owns N/P experts and M/P pairs and brings T tokens, so the step covers N*T tokens ("scaling": "weak");
+tokens, candidate scores and partial outputs move over NCCL. --sharded runs that path on one GPU too.
+Rank 0 prints one JSON line.
 The reference arm times the UNMODIFIED reference CPU implementation (oracle/_ref, built from
 /root/reference by oracle/Makefile) on the host cores, same config/metric, bounded per-step sample.
 """
@@ -179,27 +181,46 @@ def our_arm(args, rank, world, local_rank):
 
     from paper_2406_04984_b200 import meft as G
 
-    dist = torch.distributed if world > 1 else None
+    dist = torch.distributed if world > 1 else None  # barriers / max-over-ranks only with several ranks
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     d, M, N, K, kk, T, lr = (CFG[x] for x in ("d", "pairs", "experts", "k", "kk", "tokens", "lr"))
 
     ctx = G.Context(local_rank)
-    store = G.Store(ctx, 1, d, M, N, G.STORE_MIXED)
-    store.init_reference(seed=1)  # HostStore::init tables (reference RNG streams 0x5000/0x5001)
-    gen = torch.Generator(device=dev).manual_seed(0x7001 + rank)
-    b = 1.0 / math.sqrt(d)
-    w_b = (torch.rand((M, d), generator=gen, device=dev) * 2 - 1) * b  # W_B ~ U(+-1/sqrt d)
-    store.tensor(0, "w_b").copy_(w_b)
-    store.tensor(0, "w_b_compute").copy_(w_b.to(torch.bfloat16))
-    del w_b
+    gen = torch.Generator(device=dev).manual_seed(0x7002 + rank)
     h = (torch.rand((T, d), generator=gen, device=dev) * 2 - 1).to(torch.bfloat16)
     g = (torch.rand((T, d), generator=gen, device=dev) * 2 - 1).to(torch.bfloat16)
     out = torch.empty((T, d), dtype=torch.float32, device=dev)
     grad_h = torch.empty((T, d), dtype=torch.float32, device=dev)
+    sharded = world > 1 or args.sharded
+    if not sharded:
+        store = G.Store(ctx, 1, d, M, N, G.STORE_MIXED)
+        store.init_reference(seed=1)  # HostStore::init tables (reference RNG streams 0x5000/0x5001)
+        wgen = torch.Generator(device=dev).manual_seed(0x7001)
+        b = 1.0 / math.sqrt(d)
+        w_b = (torch.rand((M, d), generator=wgen, device=dev) * 2 - 1) * b  # W_B ~ U(+-1/sqrt d)
+        store.tensor(0, "w_b").copy_(w_b)
+        store.tensor(0, "w_b_compute").copy_(w_b.to(torch.bfloat16))
+        del w_b
 
-    def step():
-        return store.layer_step(0, h, g, kk, K, lr, out=out, grad_h=grad_h)
+        def step():
+            return store.layer_step(0, h, g, kk, K, lr, out=out, grad_h=grad_h)
+    else:
+        # expert-sharded layer: this rank owns N/P experts and M/P pairs; tokens are exchanged over NCCL
+        from paper_2406_04984_b200 import sharded as SH
+
+        eng, store = SH.make_device_layer(ctx, d, M, N, seed=1)
+        layer = SH.ShardedLayer(eng, d, M, N)
+
+        def step():
+            l0 = G.kernel_launches()
+            res = layer.step(h, g, kk, K, lr)
+            out.copy_(res["out"])
+            grad_h.copy_(res["grad_h"])
+            info = dict(layer.last)
+            info["gpu_launches"] = G.kernel_launches() - l0
+            info["fallbacks"] = 0
+            return info
 
     for _ in range(args.warmup):
         info = step()
@@ -243,13 +264,25 @@ def our_arm(args, rank, world, local_rank):
     out_host = torch.empty((T, d), dtype=torch.float32).pin_memory()
     gh_host = torch.empty((T, d), dtype=torch.float32).pin_memory()
     e2e_steps = max(3, min(args.steps, 10))
-    store.layer_step_host(0, h_host, g_host, kk, K, lr, out_host, gh_host)
+
+    def e2e_step():
+        if not sharded:  # one C-ABI call: copies overlapped with the step inside meft_layer_step_host
+            store.layer_step_host(0, h_host, g_host, kk, K, lr, out_host, gh_host)
+        else:
+            h.copy_(h_host, non_blocking=True)
+            g.copy_(g_host, non_blocking=True)
+            step()
+            out_host.copy_(out, non_blocking=True)
+            gh_host.copy_(grad_h, non_blocking=True)
+            torch.cuda.synchronize()
+
+    e2e_step()
     if dist:
         dist.barrier()
     clocks.start()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        store.layer_step_host(0, h_host, g_host, kk, K, lr, out_host, gh_host)
+        e2e_step()
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     clocks.stop()
     if dist:
@@ -298,12 +331,15 @@ def our_arm(args, rank, world, local_rank):
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (HostStore::init tables, uniform W_B/h/grad_out)",
         "config": dict(workload=CFG["workload"], d=d, pairs=M, experts=N, k=K, kk=kk, tokens_per_gpu=T,
-                       global_tokens=T * world, parallelism=f"replica{world}", precision="bf16 compute, fp32 "
+                       global_tokens=T * world,
+                       parallelism="single GPU" if not sharded else f"expert-sharded ep{world} (NCCL all-to-all)",
+                       precision="bf16 compute, fp32 "
                        "master/Adam state", l2="inputs larger than L2 (9.7 GB of tables per layer)",
                        union_size=S),
         "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": 2 * T * d * 2,
                 "d2h_bytes_per_step": 2 * T * d * 4, "ms_per_step": e2e_s * 1e3,
-                "path": "meft_layer_step_host (C ABI, pinned host buffers)"},
+                "path": "meft_layer_step_host (C ABI, pinned host buffers)" if not sharded else
+                        "sharded layer step with pinned host copies in and out"},
         "roofline": {"bound": "tensor", "kernel": "k_gemm_bf16 (tcgen05 FFN GEMM)", "achieved": gemm_tflops,
                      "peak": tc_peak, "unit": "TFLOP/s", "frac": gemm_tflops / tc_peak, "traffic": None,
                      "peak_source": f"{peak_src} bf16_tflops_sustained",
@@ -331,6 +367,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--skip-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true", help="run the expert-sharded layer even on one GPU")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -339,15 +376,20 @@ def main():
     if args.impl == "reference":
         reference_arm(args, rank, world)
         return
-    if world > 1:
+    distributed = world > 1 or args.sharded
+    if distributed:
         import torch
 
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29511")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         torch.cuda.set_device(local_rank)
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         our_arm(args, rank, world, local_rank)
     finally:
-        if world > 1:
+        if distributed:
             import torch
 
             torch.distributed.destroy_process_group()

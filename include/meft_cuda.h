@@ -82,6 +82,8 @@ void* meft_ctx_stream(meft_ctx* ctx);
 const char* meft_last_error(const meft_ctx* ctx); /* ctx may be NULL: last error of this thread */
 int64_t meft_last_error_index(const meft_ctx* ctx);
 meft_status meft_synchronize(meft_ctx* ctx);
+/* Number of kernels this library has launched from the calling thread (for launch accounting). */
+int64_t meft_kernel_launches(void);
 
 /* Per-phase device timing of meft_layer_step with CUDA events recorded on the context stream:
  * phase 0 selection (ke_select), 1 fetch (row gather), 2 FFN forward GEMMs, 3 FFN backward GEMMs (scatter
@@ -223,6 +225,43 @@ meft_status meft_scatter_grads(meft_ctx* ctx, meft_store* store, int64_t layer, 
  * clears staging. Untouched pairs stay bit-identical. No host synchronisation. */
 meft_status meft_sparse_adam_update(meft_ctx* ctx, meft_store* store, int64_t layer, double beta1, double beta2,
                                     double eps, double lr);
+
+/* ------------------------------------------------------------------ expert-sharded layer
+ * Rank r owns experts [r*N/P, (r+1)*N/P) and their pairs; its store holds only those (pairs = M/P, experts = N/P).
+ * The orchestration (paper_2406_04984_b200/sharded.py) moves rows between ranks with NCCL; these calls are the
+ * per-rank compute. All selection pieces are the certified path of meft_ke_select split at the rank boundary, so
+ * the sharded layer selects exactly the reference's indices. */
+
+/* home rank: certified top-kk experts per token against the replicated router (experts.cpp:21-45). */
+meft_status meft_route_select(meft_ctx* ctx, const uint16_t* h, const uint16_t* w_g, int64_t T, int64_t d, int64_t N,
+                              int64_t kk, int32_t* tau);
+/* norms (rounded up) and minimum LSB exponents of bf16 rows (inputs of the error bounds / exactness certificate). */
+meft_status meft_row_stats(meft_ctx* ctx, const uint16_t* rows, int64_t n, int64_t d, float* norms, int32_t* minlsb);
+/* owner rank: the same statistics for the layer's local keys (cached until the next update of the keys). */
+meft_status meft_store_key_stats(meft_ctx* ctx, meft_store* store, int64_t layer, float* norms, int32_t* minlsb);
+/* owner rank: approximate tcgen05 scores of R dispatched token rows against all E keys of their local expert
+ * (expert_local[r] in [0, N/P)): cand [R x E] fp32. */
+meft_status meft_score_candidates(meft_ctx* ctx, meft_store* store, int64_t layer, const uint16_t* rows,
+                                  const int32_t* expert_local, int64_t R, float* cand);
+/* owner rank: the reference's exact fp64 scores dot(rows[pair_row[q]], key[pair_key[q]]) of Q pairs. */
+meft_status meft_exact_scores(meft_ctx* ctx, meft_store* store, int64_t layer, const uint16_t* rows, int64_t R,
+                              const int32_t* pair_row, const int32_t* pair_key, int64_t Q, double* out);
+/* home rank: certified classification of each token's C = kk*E approximate candidates (cand [T x C], slot order =
+ * tau order; kn = norms of ALL M keys): certain members -> sure [T x take] / n_sure, ambiguous global indices ->
+ * amb [T x C] / n_amb. Then, with the owners' exact scores x [T x C] (x[t][a] for amb[t][a]), finalize writes the
+ * ascending per-token selection and marks union_flags [M]. */
+meft_status meft_topk_classify(meft_ctx* ctx, const float* cand, const int32_t* tau, int64_t T, int64_t kk, int64_t E,
+                               int64_t take, int64_t d, const float* hn, const float* kn, int32_t* sure,
+                               int32_t* n_sure, int32_t* amb, int32_t* n_amb);
+meft_status meft_topk_finalize(meft_ctx* ctx, const int32_t* sure, const int32_t* n_sure, const int32_t* amb,
+                               const int32_t* n_amb, const double* x, int64_t T, int64_t C, int64_t take,
+                               int32_t* per_token, uint8_t* union_flags);
+/* owner rank: the FFN of ALL T (all-gathered) tokens against its local part of the union (S_local: ascending local
+ * pair ids), the fused scatter, and the lazy Adam of those pairs. out/grad_h are this shard's partial sums
+ * [T x d] fp32 (to be reduce-scattered). */
+meft_status meft_layer_ffn_local(meft_ctx* ctx, meft_store* store, int64_t layer, const uint16_t* h_all,
+                                 const uint16_t* g_all, int64_t T, const int32_t* S_local, int64_t s, double beta1,
+                                 double beta2, double eps, double lr, float* out_partial, float* grad_h_partial);
 
 /* ------------------------------------------------------------------ whole layer step */
 

@@ -25,6 +25,15 @@ _SIGS = {
     "meft_last_error": (C.c_char_p, [P]),
     "meft_last_error_index": (I64, [P]),
     "meft_synchronize": (INT, [P]),
+    "meft_kernel_launches": (I64, []),
+    "meft_route_select": (INT, [P, P, P, I64, I64, I64, I64, P]),
+    "meft_row_stats": (INT, [P, P, I64, I64, P, P]),
+    "meft_store_key_stats": (INT, [P, P, I64, P, P]),
+    "meft_score_candidates": (INT, [P, P, I64, P, P, I64, P]),
+    "meft_exact_scores": (INT, [P, P, I64, P, I64, P, P, I64, P]),
+    "meft_topk_classify": (INT, [P, P, P, I64, I64, I64, I64, I64, P, P, P, P, P, P]),
+    "meft_topk_finalize": (INT, [P, P, P, P, P, P, I64, I64, I64, P, P]),
+    "meft_layer_ffn_local": (INT, [P, P, I64, P, P, I64, P, I64, D, D, D, D, P, P]),
     "meft_ctx_set_timing": (INT, [P, INT]),
     "meft_ctx_set_selection": (INT, [P, INT]),
     "meft_ctx_read_timing": (INT, [P, P, P]),

@@ -96,6 +96,8 @@ struct LayerBufs {
     void* c_g = nullptr;
     int32_t* step = nullptr;  // [r]
     uint8_t* staged = nullptr;
+    float* kn = nullptr;      // MIXED: cached norms of the bf16 compute keys
+    int32_t* kl = nullptr;    // MIXED: cached minimum LSB exponents of the bf16 compute keys
     void* base = nullptr;
 };
 
@@ -106,6 +108,7 @@ struct meft_store {
     meft_precision prec = MEFT_STORE_MIXED;
     int device = 0;
     std::vector<LayerBufs> L;
+    std::vector<char> key_stats_valid;  // per layer: kn/kl match the current compute keys
 };
 
 namespace {
@@ -367,6 +370,10 @@ void upload_f64(meft_ctx* ctx, meft_store* s, const LayerBufs& L, meft_tensor t,
         src = tr;
     }
     convert(st, dcode(dt), dst, 0, src, n);
+    if (t == MEFT_T_W_A) {
+        for (size_t l = 0; l < s->L.size(); ++l)
+            if (&s->L[l] == &L) s->key_stats_valid[l] = 0;
+    }
     if (s->prec == MEFT_STORE_MIXED) {
         if (t == MEFT_T_W_A) convert(st, 2, L.c_a, 0, src, n);
         if (t == MEFT_T_W_B) convert(st, 2, L.c_b, 0, src, n);
@@ -492,6 +499,8 @@ meft_status meft_synchronize(meft_ctx* ctx) {
         MEFT_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     });
 }
+
+int64_t meft_kernel_launches(void) { return launch_counter(); }
 
 meft_status meft_ctx_set_timing(meft_ctx* ctx, int enable) {
     return guarded(ctx, [&] {
@@ -757,7 +766,7 @@ meft_status meft_store_create(meft_ctx* ctx, int64_t layers, int64_t d, int64_t 
         const size_t pd = size_t(pairs) * size_t(d), nd = size_t(experts) * size_t(d);
         auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
         size_t bytes = 8 * al(pd * mb) + al(nd * mb) + al(size_t(pairs) * 4) + al(size_t(pairs));
-        if (precision == MEFT_STORE_MIXED) bytes += 2 * al(pd * 2) + al(nd * 2);
+        if (precision == MEFT_STORE_MIXED) bytes += 2 * al(pd * 2) + al(nd * 2) + 2 * al(size_t(pairs) * 4);
         for (int64_t l = 0; l < layers; ++l) {
             LayerBufs L;
             cudaError_t e = cudaMalloc(&L.base, bytes);
@@ -789,12 +798,15 @@ meft_status meft_store_create(meft_ctx* ctx, int64_t layers, int64_t d, int64_t 
                 L.c_a = take(pd * 2);
                 L.c_b = take(pd * 2);
                 L.c_g = take(nd * 2);
+                L.kn = static_cast<float*>(take(size_t(pairs) * 4));
+                L.kl = static_cast<int32_t*>(take(size_t(pairs) * 4));
             } else {
                 L.c_a = L.w_a;
                 L.c_b = L.w_b;
                 L.c_g = L.w_g;
             }
             s->L.push_back(L);
+            s->key_stats_valid.push_back(0);
         }
         MEFT_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
         *out = s.release();
@@ -946,10 +958,15 @@ meft_status meft_sparse_adam_update(meft_ctx* ctx, meft_store* s, int64_t layer,
     return guarded(ctx, [&] {
         require_ctx(ctx);
         adam_impl(ctx, s, layer_of(s, layer), beta1, beta2, eps, lr);
+        s->key_stats_valid[size_t(layer)] = 0;
     });
 }
 
 // ------------------------------------------------------------------ fused layer step
+
+static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const void* h, const void* g, int64_t T,
+                            const int32_t* uni, int64_t su, double b1, double b2, double eps, double lr, float* out,
+                            float* grad_h, cudaEvent_t g_ready, cudaEvent_t fwd_done);
 
 static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const void* h, const void* g, int64_t T,
                             int64_t kk, int64_t k, double b1, double b2, double eps, double lr, float* out,
@@ -981,6 +998,27 @@ static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
     MEFT_CUDA_CHECK(cudaMemcpyAsync(ctx->host_small + 4, usize, 12, cudaMemcpyDeviceToHost, st));
     MEFT_CUDA_CHECK(cudaStreamSynchronize(st));
     const int64_t su = ctx->host_small[4];
+    ffn_update_impl(ctx, s, layer, h, g, T, uni, su, b1, b2, eps, lr, out, grad_h, g_ready, fwd_done);
+
+    if (info) {
+        info->union_size = su;
+        info->take = take;
+        info->kk_eff = kk_eff;
+        info->warned = warned;
+        info->gpu_launches = int(launch_counter() - launches0);
+        info->rescored = ctx->host_small[5];
+        info->fallbacks = ctx->host_small[6];
+    }
+}
+
+// fetch -> sparse_ffn_pa -> sparse_backward -> scatter_grads -> sparse_adam_update for T tokens against the union S
+// (uni: ascending store-local pair ids, su of them), on a MIXED store.
+static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const void* h, const void* g, int64_t T,
+                            const int32_t* uni, int64_t su, double b1, double b2, double eps, double lr, float* out,
+                            float* grad_h, cudaEvent_t g_ready, cudaEvent_t fwd_done) {
+    const LayerBufs& L = layer_of(s, layer);
+    const int64_t d = s->d;
+    cudaStream_t st = ctx->stream;
     const int64_t ld = round_up(std::max<int64_t>(su, 1), 64);
 
     // fetch (memtier.cpp:117-126): gather the selected key/value rows of the bf16 compute tables
@@ -1016,16 +1054,107 @@ static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
         if (su > 0) mark_rows(st, L.staged, uni, nullptr, su);
         adam_impl(ctx, s, L, b1, b2, eps, lr);
     }
+    s->key_stats_valid[size_t(layer)] = 0;
+}
 
-    if (info) {
-        info->union_size = su;
-        info->take = take;
-        info->kk_eff = kk_eff;
-        info->warned = warned;
-        info->gpu_launches = int(launch_counter() - launches0);
-        info->rescored = ctx->host_small[5];
-        info->fallbacks = ctx->host_small[6];
-    }
+// Cached norms / minimum LSB exponents of a layer's bf16 compute keys (the certified selection's inputs).
+static void ensure_key_stats(meft_ctx* ctx, meft_store* s, int64_t layer) {
+    const LayerBufs& L = layer_of(s, layer);
+    require(s->prec == MEFT_STORE_MIXED, MEFT_E_INVALID, "key stats: requires a MIXED precision store");
+    if (s->key_stats_valid[size_t(layer)]) return;
+    row_stats(ctx->stream, static_cast<const uint16_t*>(L.c_a), s->pairs, s->d, L.kn, L.kl);
+    s->key_stats_valid[size_t(layer)] = 1;
+}
+
+// ------------------------------------------------------------------ expert-sharded layer building blocks
+
+meft_status meft_route_select(meft_ctx* ctx, const uint16_t* h, const uint16_t* w_g, int64_t T, int64_t d, int64_t N,
+                              int64_t kk, int32_t* tau) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        if (kk < 1) throw MeftError(MEFT_E_INVALID, "select_experts: budget must be >= 1");
+        require(N >= 1 && d % 8 == 0, MEFT_E_INVALID, "route_select: N >= 1 and d % 8 == 0 required");
+        void* ws = ctx->get("route_ws", route_workspace_bytes(T, d, N));
+        route_certified(ctx->stream, h, w_g, T, d, N, std::min(kk, N), ws, tau, nullptr);
+    });
+}
+
+meft_status meft_row_stats(meft_ctx* ctx, const uint16_t* rows, int64_t n, int64_t d, float* norms, int32_t* minlsb) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        row_stats(ctx->stream, rows, n, d, norms, minlsb);
+    });
+}
+
+meft_status meft_store_key_stats(meft_ctx* ctx, meft_store* s, int64_t layer, float* norms, int32_t* minlsb) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        const LayerBufs& L = layer_of(s, layer);
+        ensure_key_stats(ctx, s, layer);
+        if (norms)
+            MEFT_CUDA_CHECK(cudaMemcpyAsync(norms, L.kn, size_t(s->pairs) * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+        if (minlsb)
+            MEFT_CUDA_CHECK(cudaMemcpyAsync(minlsb, L.kl, size_t(s->pairs) * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+    });
+}
+
+meft_status meft_score_candidates(meft_ctx* ctx, meft_store* s, int64_t layer, const uint16_t* rows,
+                                  const int32_t* expert_local, int64_t R, float* cand) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        const LayerBufs& L = layer_of(s, layer);
+        require(s->prec == MEFT_STORE_MIXED && s->d % 8 == 0, MEFT_E_INVALID, "score_candidates: MIXED store, d % 8");
+        const int64_t E = s->pairs / s->experts;
+        require(E % 4 == 0, MEFT_E_INVALID, "score_candidates: expert size must be a multiple of 4");
+        void* ws = ctx->get("score_ws", score_workspace_bytes(R, s->d, s->experts));
+        score_candidates(ctx->stream, rows, expert_local, R, s->d, static_cast<const uint16_t*>(L.c_a), s->experts, E,
+                         ws, cand);
+    });
+}
+
+meft_status meft_exact_scores(meft_ctx* ctx, meft_store* s, int64_t layer, const uint16_t* rows, int64_t R,
+                              const int32_t* pair_row, const int32_t* pair_key, int64_t Q, double* out) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        const LayerBufs& L = layer_of(s, layer);
+        ensure_key_stats(ctx, s, layer);
+        float* rn = static_cast<float*>(ctx->get("rows_norm", size_t(std::max<int64_t>(R, 1)) * 4));
+        int32_t* rl = static_cast<int32_t*>(ctx->get("rows_lsb", size_t(std::max<int64_t>(R, 1)) * 4));
+        row_stats(ctx->stream, rows, R, s->d, rn, rl);
+        exact_pair_scores(ctx->stream, rows, rn, rl, static_cast<const uint16_t*>(L.c_a), L.kn, L.kl, pair_row,
+                          pair_key, Q, s->d, out, nullptr);
+    });
+}
+
+meft_status meft_topk_classify(meft_ctx* ctx, const float* cand, const int32_t* tau, int64_t T, int64_t kk, int64_t E,
+                               int64_t take, int64_t d, const float* hn, const float* kn, int32_t* sure,
+                               int32_t* n_sure, int32_t* amb, int32_t* n_amb) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(take >= 1 && take <= kk * E, MEFT_E_INVALID, "topk_classify: 1 <= take <= kk*E");
+        topk_classify(ctx->stream, cand, tau, T, kk, E, take, d, hn, kn, sure, n_sure, amb, n_amb, nullptr);
+    });
+}
+
+meft_status meft_topk_finalize(meft_ctx* ctx, const int32_t* sure, const int32_t* n_sure, const int32_t* amb,
+                               const int32_t* n_amb, const double* x, int64_t T, int64_t C, int64_t take,
+                               int32_t* per_token, uint8_t* union_flags) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        topk_finalize(ctx->stream, sure, n_sure, amb, n_amb, x, T, C, take, per_token, union_flags);
+    });
+}
+
+meft_status meft_layer_ffn_local(meft_ctx* ctx, meft_store* s, int64_t layer, const uint16_t* h_all,
+                                 const uint16_t* g_all, int64_t T, const int32_t* S_local, int64_t su, double beta1,
+                                 double beta2, double eps, double lr, float* out_partial, float* grad_h_partial) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        layer_of(s, layer);
+        require(s->prec == MEFT_STORE_MIXED && s->d % 8 == 0, MEFT_E_INVALID, "layer_ffn_local: MIXED store, d % 8");
+        ffn_update_impl(ctx, s, layer, h_all, g_all, T, S_local, su, beta1, beta2, eps, lr, out_partial,
+                        grad_h_partial, nullptr, nullptr);
+    });
 }
 
 meft_status meft_layer_step(meft_ctx* ctx, meft_store* s, int64_t layer, const void* h, const void* grad_out,

@@ -684,3 +684,159 @@ void compact_flags(cudaStream_t st, const uint8_t* flags, int64_t M, int32_t* ou
     check_launch("k_flag_write");
 }
 }  // namespace meft_dev
+
+// ------------------------------------------------------------------ sharded-selection building blocks
+namespace meft_dev {
+namespace {
+__global__ void k_count_experts(const int32_t* __restrict__ expert, int R, int32_t* __restrict__ counts) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < R) atomicAdd(&counts[expert[r]], 1);
+}
+
+__global__ void k_exact_pairs(const uint16_t* __restrict__ rows, const float* __restrict__ rn,
+                              const int32_t* __restrict__ rl, const uint16_t* __restrict__ keys,
+                              const float* __restrict__ kn, const int32_t* __restrict__ kl,
+                              const int32_t* __restrict__ pair_row, const int32_t* __restrict__ pair_key, int Q, int d,
+                              double* __restrict__ out, int* __restrict__ stats) {
+    const int lane = threadIdx.x & 31;
+    for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < Q; p += (gridDim.x * blockDim.x) >> 5) {
+        const int r = pair_row[p], k = pair_key[p];
+        const double v = exact_dot_rows(rows + int64_t(r) * d, keys + int64_t(k) * d, d, lane, rl[r], kl[k], rn[r],
+                                        kn[k], stats ? stats + 1 : nullptr);
+        if (lane == 0) out[p] = v;
+    }
+}
+}  // namespace
+
+void row_stats(cudaStream_t st, const uint16_t* x, int64_t rows, int64_t d, float* norms, int32_t* minlsb) {
+    if (rows <= 0) return;
+    k_row_norms<<<int((rows * 32 + 255) / 256), 256, 0, st>>>(x, rows, int(d), norms, minlsb);
+    check_launch("k_row_norms");
+}
+
+size_t route_workspace_bytes(int64_t T, int64_t d, int64_t N) {
+    (void)d;
+    size_t b = 0;
+    auto add = [&](size_t x) { b += (x + 255) & ~size_t(255); };
+    add(T * round_up(N, 4) * 4);
+    add((T + N) * 4);
+    add((T + N) * 4);
+    add((N + 1) * 4);
+    return b;
+}
+
+void route_certified(cudaStream_t st, const uint16_t* h, const uint16_t* w_g, int64_t T, int64_t d, int64_t N,
+                     int64_t kk_eff, void* ws, int32_t* tau, int32_t* stats) {
+    if (T <= 0) return;
+    const int64_t ldp = round_up(N, 4);
+    uint8_t* p = static_cast<uint8_t*>(ws);
+    auto take_buf = [&](size_t x) {
+        void* r = p;
+        p += (x + 255) & ~size_t(255);
+        return r;
+    };
+    float* P = static_cast<float*>(take_buf(T * ldp * 4));
+    float* hn = static_cast<float*>(take_buf((T + N) * 4));
+    float* gn = hn + T;
+    int32_t* hl = static_cast<int32_t*>(take_buf((T + N) * 4));
+    int32_t* gl = hl + T;
+    int32_t* counts = static_cast<int32_t*>(take_buf((N + 1) * 4));
+    row_stats(st, h, T, d, hn, hl);
+    row_stats(st, w_g, N, d, gn, gl);
+    GemmEpilogue e;
+    e.kind = EPI_STORE_F32;
+    e.c = P;
+    e.ldc = ldp;
+    gemm_bf16(st, T, N, d, GemmOperand{h, d, false}, GemmOperand{w_g, d, false}, e);
+    MEFT_CUDA_CHECK(cudaMemsetAsync(counts, 0, N * 4, st));
+    const int wpb = 4;
+    const size_t rsm = size_t(wpb) * (kk_eff + 2 * N) * 4 + size_t(wpb) * N * 8;
+    static bool rattr = false;
+    if (!rattr) {
+        MEFT_CUDA_CHECK(cudaFuncSetAttribute(k_router_certified, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        rattr = true;
+    }
+    k_router_certified<<<int((T + wpb - 1) / wpb), wpb * 32, rsm, st>>>(P, int(ldp), hn, gn, hl, gl,
+                                                                      cert_bound_coeff(int(d)), h, w_g, int(d), int(T),
+                                                                      int(N), int(kk_eff), tau, counts, stats);
+    check_launch("k_router_certified");
+}
+
+size_t score_workspace_bytes(int64_t R, int64_t d, int64_t n_experts) {
+    size_t b = 0;
+    auto add = [&](size_t x) { b += (x + 255) & ~size_t(255); };
+    add((n_experts + 1) * 4 * 4);
+    add(R * 4);
+    add(R * d * 2);
+    return b;
+}
+
+void score_candidates(cudaStream_t st, const uint16_t* rows, const int32_t* expert, int64_t R, int64_t d,
+                      const uint16_t* keys, int64_t n_experts, int64_t E, void* ws, float* cand) {
+    if (R <= 0) return;
+    uint8_t* p = static_cast<uint8_t*>(ws);
+    auto take_buf = [&](size_t x) {
+        void* r = p;
+        p += (x + 255) & ~size_t(255);
+        return r;
+    };
+    int32_t* counts = static_cast<int32_t*>(take_buf((n_experts + 1) * 4 * 4));
+    int32_t* off = counts + (n_experts + 1);
+    int32_t* tile_off = off + (n_experts + 1);
+    int32_t* cursor = tile_off + (n_experts + 1);
+    int32_t* entries = static_cast<int32_t*>(take_buf(R * 4));
+    uint16_t* hs = static_cast<uint16_t*>(take_buf(R * d * 2));
+    MEFT_CUDA_CHECK(cudaMemsetAsync(counts, 0, n_experts * 4, st));
+    k_count_experts<<<int((R + 255) / 256), 256, 0, st>>>(expert, int(R), counts);
+    check_launch("k_count_experts");
+    k_bucket_scan<<<1, 1024, 0, st>>>(counts, int(n_experts), off, tile_off, cursor, 128);
+    check_launch("k_bucket_scan");
+    k_bucket_fill<<<int((R + 255) / 256), 256, 0, st>>>(expert, int(R), 1, off, cursor, entries);
+    check_launch("k_bucket_fill");
+    k_gather_tokens<<<std::max(1, std::min(int(R / 8 + 1), num_sms() * 16)), 256, 0, st>>>(rows, int(d), entries,
+                                                                                           int(R), 1, hs);
+    check_launch("k_gather_tokens");
+    GemmEpilogue eg;
+    eg.kind = EPI_ROWS_STORE_F32;
+    eg.c = cand;
+    eg.ldc = E;
+    eg.row_idx = entries;
+    gemm_bf16_grouped(st, int(n_experts), E, d, GemmOperand{hs, d, false}, R, GemmOperand{keys, d, false},
+                      n_experts * E, off, tile_off, eg);
+}
+
+void exact_pair_scores(cudaStream_t st, const uint16_t* rows, const float* rn, const int32_t* rl,
+                       const uint16_t* keys, const float* kn, const int32_t* kl, const int32_t* pair_row,
+                       const int32_t* pair_key, int64_t Q, int64_t d, double* out, int32_t* stats) {
+    if (Q <= 0) return;
+    const int grid = std::max(1, std::min<int>(int((Q * 32 + 255) / 256), num_sms() * 8));
+    k_exact_pairs<<<grid, 256, 0, st>>>(rows, rn, rl, keys, kn, kl, pair_row, pair_key, int(Q), int(d), out, stats);
+    check_launch("k_exact_pairs");
+}
+
+void topk_classify(cudaStream_t st, const float* cand, const int32_t* tau, int64_t T, int64_t kk, int64_t E,
+                   int64_t take, int64_t d, const float* hn, const float* kn, int32_t* sure, int32_t* n_sure,
+                   int32_t* amb, int32_t* n_amb, int32_t* amb_count_per_expert) {
+    if (T <= 0) return;
+    const int64_t C = kk * E;
+    const size_t csm = size_t(C) * 5 + 16;
+    static bool cattr = false;
+    if (!cattr) {
+        MEFT_CUDA_CHECK(cudaFuncSetAttribute(k_topk_classify, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        cattr = true;
+    }
+    k_topk_classify<<<int(T), 256, csm, st>>>(cand, tau, int(kk), int(E), int(C), next_pow2(int(C)), int(take), hn, kn,
+                                              cert_bound_coeff(int(d)), sure, n_sure, amb, n_amb, amb_count_per_expert);
+    check_launch("k_topk_classify");
+}
+
+void topk_finalize(cudaStream_t st, const int32_t* sure, const int32_t* n_sure, const int32_t* amb,
+                   const int32_t* n_amb, const double* x, int64_t T, int64_t C, int64_t take, int32_t* per_token,
+                   uint8_t* flags) {
+    if (T <= 0) return;
+    const int TP2 = next_pow2(int(take));
+    k_topk_finalize<<<int(T), 128, size_t(TP2) * 4, st>>>(sure, n_sure, amb, n_amb, x, int(C), int(take), TP2,
+                                                           per_token, flags);
+    check_launch("k_topk_finalize");
+}
+}  // namespace meft_dev

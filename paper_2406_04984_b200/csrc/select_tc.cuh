@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(256)
         const bool ambiguous = top ? (double(c[i]) - e <= uout) : (double(c[i]) + e >= lin);
         if (ambiguous) {
             my_amb[atomicAdd(&s_na, 1)] = gi;
-            atomicAdd(&amb_count[gi / E], 1);
+            if (amb_count) atomicAdd(&amb_count[gi / E], 1);
         } else if (top) {
             my_sure[atomicAdd(&s_ns, 1)] = gi;
         }

@@ -91,6 +91,11 @@ class Context:
         return {p: (ms[i], ln[i]) for i, p in enumerate(self.PHASES)}
 
 
+def kernel_launches() -> int:
+    """Kernels libmeft_cuda.so has launched from this thread so far."""
+    return int(lib().meft_kernel_launches())
+
+
 def selection_shape(M, N, kk, k):
     take, kk_eff, warn = I64(), I64(), C.c_int()
     check(lib().meft_selection_shape(M, N, kk, k, C.byref(take), C.byref(kk_eff), C.byref(warn)))

@@ -1,0 +1,265 @@
+"""Expert-sharded MEFT layer step over P ranks (one per GPU), DESIGN.md §6.
+
+Rank r owns experts [r*N/P, (r+1)*N/P) and their M/P key/value pairs (+ Adam state); the router W_g is
+replicated. Each rank brings its own T tokens (weak scaling: the layer step is over all P*T tokens, with the
+reference's batch-union semantics). Per step:
+
+  1. route the local tokens (certified, exact tau) ............................ home rank
+  2. all-to-all: dispatch each (token, expert) row to the expert's owner ........ NCCL
+  3. approximate candidate scores against the owner's keys (tcgen05) ............ owner rank
+  4. all-to-all: candidate scores back; all-gather key norms .................... NCCL
+  5. certified top-K classification (sure / ambiguous) .......................... home rank
+  6. all-to-all: ambiguous (row, key) requests -> owners' exact fp64 scores -> back  NCCL + owner
+  7. finalize the per-token selection; all-reduce(MAX) of the M-byte union bitmap .. home + NCCL
+  8. all-gather h and grad_out; FFN + fused scatter + lazy Adam on the local part of the union .. owner
+  9. reduce-scatter the partial out / grad_h back to the token homes ............. NCCL
+
+Selection is the single-GPU certified algorithm split at the rank boundary, so indices are the reference's,
+bit for bit. The compute is behind an engine interface: ``DeviceEngine`` calls libmeft_cuda.so; the CPU test
+suite drives the same orchestration with an fp64 oracle engine over gloo (tests/test_sharded.py).
+torch is used for buffers, index bookkeeping (argsort/bincount of routing decisions) and torch.distributed.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from ._lib import lib
+
+
+def cert_bound_coeff(d: int) -> float:
+    """CB(d) of select_tc.cuh: |approx - reference| <= CB(d) * ||h|| * ||w||."""
+    return 32.0 * 2.0 ** -24 * ((d + 15) // 16 + 1) + d * 2.0 ** -52
+
+
+def _p(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+class DeviceEngine:
+    """Per-rank compute on one B200 through the C ABI (the store holds this rank's expert shard)."""
+
+    def __init__(self, ctx, store, w_g):
+        self.ctx, self.store, self.w_g = ctx, store, w_g  # w_g: full replicated router, bf16 [N x d] on device
+        self.dev = w_g.device
+
+    def _check(self, st):
+        self.ctx.check(st)
+
+    def route(self, h, kk):
+        T, d = h.shape
+        N = self.w_g.shape[0]
+        tau = torch.empty((T, min(kk, N)), dtype=torch.int32, device=self.dev)
+        self._check(lib().meft_route_select(self.ctx.h, _p(h), _p(self.w_g), T, d, N, kk, _p(tau)))
+        return tau
+
+    def row_stats(self, rows):
+        n, d = rows.shape
+        norms = torch.empty(n, dtype=torch.float32, device=self.dev)
+        lsb = torch.empty(n, dtype=torch.int32, device=self.dev)
+        self._check(lib().meft_row_stats(self.ctx.h, _p(rows), n, d, _p(norms), _p(lsb)))
+        return norms, lsb
+
+    def key_stats(self):
+        n = self.store.pairs
+        norms = torch.empty(n, dtype=torch.float32, device=self.dev)
+        lsb = torch.empty(n, dtype=torch.int32, device=self.dev)
+        self._check(lib().meft_store_key_stats(self.ctx.h, self.store.h, 0, _p(norms), _p(lsb)))
+        return norms, lsb
+
+    def score(self, rows, expert_local):
+        R = rows.shape[0]
+        E = self.store.pairs // self.store.experts
+        cand = torch.empty((R, E), dtype=torch.float32, device=self.dev)
+        if R:
+            self._check(lib().meft_score_candidates(self.ctx.h, self.store.h, 0, _p(rows), _p(expert_local), R,
+                                                    _p(cand)))
+        return cand
+
+    def exact(self, rows, pair_row, pair_key):
+        Q = pair_row.numel()
+        out = torch.empty(Q, dtype=torch.float64, device=self.dev)
+        if Q:
+            self._check(lib().meft_exact_scores(self.ctx.h, self.store.h, 0, _p(rows), rows.shape[0], _p(pair_row),
+                                                _p(pair_key), Q, _p(out)))
+        return out
+
+    def classify(self, cand, tau, hn, kn, take, d):
+        T, Cc = cand.shape
+        kk = tau.shape[1]
+        E = Cc // kk
+        sure = torch.empty((T, take), dtype=torch.int32, device=self.dev)
+        n_sure = torch.empty(T, dtype=torch.int32, device=self.dev)
+        amb = torch.empty((T, Cc), dtype=torch.int32, device=self.dev)
+        n_amb = torch.empty(T, dtype=torch.int32, device=self.dev)
+        self._check(lib().meft_topk_classify(self.ctx.h, _p(cand), _p(tau), T, kk, E, take, d, _p(hn), _p(kn),
+                                             _p(sure), _p(n_sure), _p(amb), _p(n_amb)))
+        return sure, n_sure, amb, n_amb
+
+    def finalize(self, sure, n_sure, amb, n_amb, x, take, M):
+        T, Cc = amb.shape
+        per = torch.empty((T, take), dtype=torch.int32, device=self.dev)
+        flags = torch.zeros(M, dtype=torch.uint8, device=self.dev)
+        self._check(lib().meft_topk_finalize(self.ctx.h, _p(sure), _p(n_sure), _p(amb), _p(n_amb), _p(x), T, Cc, take,
+                                             _p(per), _p(flags)))
+        return per, flags
+
+    def ffn_local(self, h_all, g_all, S_local, lr, betas=(0.9, 0.999), eps=1e-8):
+        T, d = h_all.shape
+        out = torch.empty((T, d), dtype=torch.float32, device=self.dev)
+        gh = torch.empty((T, d), dtype=torch.float32, device=self.dev)
+        self._check(lib().meft_layer_ffn_local(self.ctx.h, self.store.h, 0, _p(h_all), _p(g_all), T, _p(S_local),
+                                               S_local.numel(), betas[0], betas[1], eps, lr, _p(out), _p(gh)))
+        return out, gh
+
+
+def _a2a(tensor, send_counts, recv_counts, group):
+    """all_to_all_single over dim 0 with per-rank row counts (lists of ints)."""
+    out = torch.empty((sum(recv_counts),) + tuple(tensor.shape[1:]), dtype=tensor.dtype, device=tensor.device)
+    dist.all_to_all_single(out, tensor.contiguous(), recv_counts, send_counts, group=group)
+    return out
+
+
+def _exchange_counts(counts, group):
+    send = torch.tensor(counts, dtype=torch.int64, device=_comm_device(group))
+    recv = torch.empty_like(send)
+    dist.all_to_all_single(recv, send, group=group)
+    return recv.tolist()
+
+
+def _comm_device(group):
+    return torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else torch.device("cpu")
+
+
+def _all_gather_rows(t, group, world):
+    parts = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(parts, t.contiguous(), group=group)
+    return torch.cat(parts, 0)
+
+
+def _reduce_scatter_rows(t, group, world, rank):
+    if dist.get_backend(group) == "nccl":
+        out = torch.empty((t.shape[0] // world,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        dist.reduce_scatter_tensor(out, t.contiguous(), group=group)
+        return out
+    buf = t.clone()  # gloo: all-reduce then keep this rank's rows
+    dist.all_reduce(buf, group=group)
+    n = t.shape[0] // world
+    return buf[rank * n:(rank + 1) * n].clone()
+
+
+class ShardedLayer:
+    """One expert-sharded MEFT layer; ``engine`` does this rank's compute (DeviceEngine on a B200)."""
+
+    def __init__(self, engine, d, M, N, group=None):
+        self.eng, self.d, self.M, self.N = engine, d, M, N
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if N % self.world or M % N:
+            raise ValueError("N must be divisible by the world size and M by N")
+        self.E, self.N_loc, self.M_loc = M // N, N // self.world, M // self.world
+        self.last = {}
+
+    def step(self, h, g, kk, k, lr):
+        P, r, E = self.world, self.rank, self.E
+        eng, grp = self.eng, self.group
+        T, d = h.shape
+        kk_eff = min(kk, self.N)
+        take = min(k, kk_eff * E)
+        # 1. route (exact tau, ascending per token)
+        tau = eng.route(h, kk)
+        # 2. dispatch (token, slot) rows to their expert owners
+        flat_e = tau.reshape(-1).long()
+        owner = flat_e // self.N_loc
+        order = torch.argsort(owner, stable=True)
+        send_counts = torch.bincount(owner, minlength=P).tolist()
+        recv_counts = _exchange_counts(send_counts, grp)
+        send_rows = h[order // kk_eff]
+        send_exp = (flat_e[order] - owner[order] * self.N_loc).to(torch.int32)
+        recv_rows = _a2a(send_rows, send_counts, recv_counts, grp)
+        recv_exp = _a2a(send_exp, send_counts, recv_counts, grp)
+        # 3-4. owners score; candidate blocks come back in dispatch order
+        cand_recv = eng.score(recv_rows, recv_exp)
+        cand_back = _a2a(cand_recv, recv_counts, send_counts, grp)
+        cand = torch.empty((T * kk_eff, E), dtype=torch.float32, device=h.device)
+        cand[order] = cand_back
+        cand = cand.view(T, kk_eff * E)
+        hn, _ = eng.row_stats(h)
+        kn_loc, _ = eng.key_stats()
+        kn = _all_gather_rows(kn_loc, grp, P)
+        # 5. certified classification at the token home
+        sure, n_sure, amb, n_amb = eng.classify(cand, tau, hn, kn, take, d)
+        # 6. exact re-scoring of the ambiguous candidates by their owners
+        Ccand = kk_eff * E
+        na = n_amb.long()
+        tok = torch.repeat_interleave(torch.arange(T, device=h.device), na)
+        pos = torch.arange(int(na.sum().item()), device=h.device) - torch.repeat_interleave(torch.cumsum(na, 0) - na, na)
+        gidx = amb[tok, pos].long()
+        e_glob = gidx // E
+        slot = (tau[tok].long() == e_glob[:, None]).int().argmax(1)  # position of the expert in tau
+        q = torch.empty_like(order)
+        q[order] = torch.arange(order.numel(), device=h.device)
+        dispatch_pos = q[tok * kk_eff + slot]                      # position in the send order
+        a_owner = gidx // self.M_loc
+        send_off = torch.cumsum(torch.tensor([0] + send_counts[:-1], device=h.device), 0)
+        req_row = (dispatch_pos - send_off[a_owner]).to(torch.int32)  # row index in the owner's recv buffer
+        req_key = (gidx - a_owner * self.M_loc).to(torch.int32)
+        rorder = torch.argsort(a_owner, stable=True)
+        rsend = torch.bincount(a_owner, minlength=P).tolist()
+        rrecv = _exchange_counts(rsend, grp)
+        in_row = _a2a(req_row[rorder], rsend, rrecv, grp)
+        in_key = _a2a(req_key[rorder], rsend, rrecv, grp)
+        # requests arrive grouped by source rank; their rows sit after the rows the earlier sources dispatched
+        src = torch.repeat_interleave(torch.arange(P, device=h.device), torch.tensor(rrecv, device=h.device))
+        recv_off = torch.cumsum(torch.tensor([0] + recv_counts[:-1], device=h.device), 0)
+        in_row = (in_row.long() + recv_off[src]).to(torch.int32)
+        x_out = eng.exact(recv_rows, in_row, in_key)
+        x_back = _a2a(x_out, rrecv, rsend, grp)
+        xs = torch.zeros((T, Ccand), dtype=torch.float64, device=h.device)
+        x_sorted = torch.empty_like(x_back)
+        x_sorted[rorder] = x_back
+        xs[tok, pos] = x_sorted
+        # 7. final per-token selection and the global union
+        per_token, flags = eng.finalize(sure, n_sure, amb, n_amb, xs, take, self.M)
+        union = flags.to(torch.int32)
+        dist.all_reduce(union, op=dist.ReduceOp.MAX, group=grp)
+        S = torch.nonzero(union).flatten()
+        S_loc = S[(S >= r * self.M_loc) & (S < (r + 1) * self.M_loc)] - r * self.M_loc
+        # 8-9. FFN over all tokens on the local part of the union, partial sums back to the homes
+        h_all = _all_gather_rows(h, grp, P)
+        g_all = _all_gather_rows(g, grp, P)
+        out_p, gh_p = eng.ffn_local(h_all, g_all, S_loc.to(torch.int32).contiguous(), lr)
+        out = _reduce_scatter_rows(out_p, grp, P, r)
+        grad_h = _reduce_scatter_rows(gh_p, grp, P, r)
+        self.last = dict(union_size=int(S.numel()), local_union=int(S_loc.numel()), rescored=int(na.sum().item()))
+        return dict(per_token=per_token, tau=tau, unioned=S, out=out, grad_h=grad_h)
+
+
+def make_device_layer(ctx, d, M, N, group=None, seed=1, w_b_seed=0x7001):
+    """This rank's shard as a MIXED HBM store: keys from HostStore::init(seed) restricted to the shard (the global
+    table is generated once per rank with the reference RNG, then sliced), W_B ~ U(+-1/sqrt d) (torch RNG,
+    identical on every rank), router replicated."""
+    from . import meft as G
+
+    P = dist.get_world_size(group)
+    r = dist.get_rank(group)
+    M_loc, N_loc = M // P, N // P
+    full = G.Store(ctx, 1, d, M, N, G.STORE_MIXED)
+    full.init_reference(seed)
+    store = G.Store(ctx, 1, d, M_loc, N_loc, G.STORE_MIXED)
+    for name in ("w_a", "w_a_compute"):
+        store.tensor(0, name).copy_(full.tensor(0, name)[r * M_loc:(r + 1) * M_loc])
+    gen = torch.Generator(device=store.tensor(0, "w_b").device).manual_seed(w_b_seed)
+    b = 1.0 / math.sqrt(d)
+    w_b = (torch.rand((M, d), generator=gen, device=gen.device) * 2 - 1) * b
+    store.tensor(0, "w_b").copy_(w_b[r * M_loc:(r + 1) * M_loc])
+    store.tensor(0, "w_b_compute").copy_(w_b[r * M_loc:(r + 1) * M_loc].to(torch.bfloat16))
+    w_g = full.tensor(0, "w_g_compute").clone()
+    full.close()
+    del w_b
+    return DeviceEngine(ctx, store, w_g), store
