@@ -18,6 +18,7 @@ pytestmark = pytest.mark.gpu
 
 @pytest.fixture(scope="module")
 def nccl_world1():
+    created = False
     if not dist.is_initialized():
         with socket.socket() as s:
             s.bind(("127.0.0.1", 0))
@@ -25,7 +26,10 @@ def nccl_world1():
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+        created = True
     yield dist.group.WORLD
+    if created:
+        dist.destroy_process_group()
 
 
 def test_sharded_world1_equals_layer_step(ctx, nccl_world1):
