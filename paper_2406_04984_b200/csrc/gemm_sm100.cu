@@ -309,6 +309,176 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
 }
 
+// ==================================================================================================== CTA pair
+// 2-CTA variant (cta_group::2, cluster of 2 on one TPC): the pair computes a 256 x 256 tile with one
+// tcgen05.mma M=256 per K=16 step, issued by the leader CTA. Each CTA stages its own 128 A rows and its own
+// 128 B rows (half of the tile's N), so per-SM shared-memory operand traffic drops by a third versus the 1-CTA
+// 128x256 tile, and each CTA's TMEM accumulates its 128 rows x all 256 columns.
+//   warp 0 (both CTAs): TMA into the local ring, completion counted on the leader's full barrier
+//   warp 1 (leader)   : MMA issue; commits multicast to both CTAs' empty / tmem-full barriers
+//   warps 2-5 (both)  : epilogue of the local 128 rows; release the accumulator on the leader's tmem-empty
+constexpr int P_STAGES = 6;
+constexpr int P_A_BYTES = 128 * BK * 2;
+constexpr int P_B_BYTES = 128 * BK * 2;
+constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
+constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + 1024 + 256;
+constexpr int P_TILE_M = 256;
+
+__device__ __forceinline__ void tile_coords_pair(int tile, int tiles_m, int tiles_n, int& m_blk, int& n_blk) {
+    const int group = 8;  // 8 pair-tiles of M share each B panel while resident
+    const int group_size = group * tiles_n;
+    const int g = tile / group_size;
+    const int first_m = g * group;
+    const int gm = min(group, tiles_m - first_m);
+    const int local = tile - g * group_size;
+    m_blk = first_m + local % gm;
+    n_blk = local / gm;
+}
+
+template <bool A_MN, bool B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    k_gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const KArgs args) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + P_STAGES * P_STAGE_BYTES);
+    uint64_t* empty = full + P_STAGES;
+    uint64_t* tfull = empty + P_STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < P_STAGES; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(tfull + b, 1);
+            mbar_init(tempty + b, 8);  // 4 epilogue warps in each of the two CTAs
+        }
+        fence_barrier_init();
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+    }
+    if (warp == 1) tmem_alloc_pair(tmem_slot, TMEM_COLS);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int num_tiles = args.tiles_m * args.tiles_n;
+
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer (both CTAs)
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = pair; tile < num_tiles; tile += npairs) {
+                int mb, nb;
+                tile_coords_pair(tile, args.tiles_m, args.tiles_n, mb, nb);
+                const int m0 = mb * P_TILE_M + int(rank) * 128;  // this CTA's A rows
+                const int n0 = nb * BN + int(rank) * 128;        // this CTA's half of the B rows
+                for (int kb = 0; kb < args.num_kb; ++kb) {
+                    mbar_wait(empty + stage, phase ^ 1);
+                    uint8_t* sa = smem + stage * P_STAGE_BYTES;
+                    uint8_t* sb = sa + P_A_BYTES;
+                    if (leader) mbar_arrive_expect_tx(full + stage, 2 * P_STAGE_BYTES);
+                    const int k0 = kb * BK;
+                    if (!A_MN) {
+                        tma_load_2d_pair(sa, &tmA, full + stage, k0, m0);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 2; ++j) tma_load_2d_pair(sa + j * 8192, &tmA, full + stage, m0 + 64 * j, k0);
+                    }
+                    if (!B_MN) {
+                        tma_load_2d_pair(sb, &tmB, full + stage, k0, n0);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 2; ++j) tma_load_2d_pair(sb + j * 8192, &tmB, full + stage, n0 + 64 * j, k0);
+                    }
+                    if (++stage == P_STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer (leader CTA)
+        if (leader && lane == 0) {
+            constexpr uint32_t idesc = umma_idesc_bf16(P_TILE_M, BN, A_MN, B_MN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int tile = pair; tile < num_tiles; tile += npairs, ++it) {
+                const int acc = it & 1;
+                const uint32_t aphase = (it >> 1) & 1;
+                mbar_wait_cluster(tempty + acc, aphase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (int kb = 0; kb < args.num_kb; ++kb) {
+                    mbar_wait(full + stage, phase);
+                    tc_fence_after();
+                    const uint32_t a_addr = smem_u32(smem + stage * P_STAGE_BYTES);
+                    const uint32_t b_addr = a_addr + P_A_BYTES;
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k) {
+                        const uint64_t ad = A_MN ? umma_desc_sw128(a_addr + k * 2048, 8192, 1024)
+                                                 : umma_desc_sw128(a_addr + k * 32, 16, 1024);
+                        const uint64_t bd = B_MN ? umma_desc_sw128(b_addr + k * 2048, 8192, 1024)
+                                                 : umma_desc_sw128(b_addr + k * 32, 16, 1024);
+                        umma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                    }
+                    umma_commit_pair(empty + stage);  // frees this stage in both CTAs
+                    if (++stage == P_STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                umma_commit_pair(tfull + acc);  // both CTAs' accumulators ready
+            }
+        }
+    } else {
+        // ------------------------------------------------ epilogue (warps 2..5, both CTAs)
+        const int q = warp & 3;
+        int it = 0;
+        for (int tile = pair; tile < num_tiles; tile += npairs, ++it) {
+            int mb, nb;
+            tile_coords_pair(tile, args.tiles_m, args.tiles_n, mb, nb);
+            const int acc = it & 1;
+            const uint32_t aphase = (it >> 1) & 1;
+            mbar_wait(tfull + acc, aphase);
+            tc_fence_after();
+            const int m = mb * P_TILE_M + int(rank) * 128 + q * 32 + lane;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t r[32];
+                tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c * 32, r);
+                tmem_ld_wait();
+                const int n = nb * BN + c * 32;
+                if (m < args.M && n < args.N) epilogue_chunk(args, m, n, r);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(tempty + acc, 0);
+        }
+    }
+
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_pair(tmem_base, TMEM_COLS);
+    }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     static std::once_flag once;
@@ -394,6 +564,40 @@ void dispatch(cudaStream_t st, bool a_mn, bool b_mn, const CUtensorMap& ta, cons
         launch<true, false>(st, ta, tb, args, tiles_bound);
 }
 
+template <bool A_MN, bool B_MN>
+void launch_pair(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const KArgs& args, int pair_tiles) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        MEFT_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_bf16_pair<A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             P_SMEM_BYTES));
+        attr_set = true;
+    }
+    const int pairs = std::max(1, std::min(pair_tiles, num_sms() / 2));
+    k_gemm_bf16_pair<A_MN, B_MN><<<2 * pairs, NUM_THREADS, P_SMEM_BYTES, st>>>(ta, tb, args);
+    check_launch("k_gemm_bf16_pair");
+}
+
+void launch_pair_dispatch(cudaStream_t st, bool a_mn, bool b_mn, const CUtensorMap& ta, const CUtensorMap& tb,
+                          const KArgs& args, int pair_tiles) {
+    if (!a_mn && !b_mn)
+        launch_pair<false, false>(st, ta, tb, args, pair_tiles);
+    else if (!a_mn && b_mn)
+        launch_pair<false, true>(st, ta, tb, args, pair_tiles);
+    else if (a_mn && b_mn)
+        launch_pair<true, true>(st, ta, tb, args, pair_tiles);
+    else
+        launch_pair<true, false>(st, ta, tb, args, pair_tiles);
+}
+
+// MEFT_GEMM_PAIR=0 forces the 1-CTA kernel (A/B comparisons in tools/gemm_check).
+bool pair_mode_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("MEFT_GEMM_PAIR");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
+
 }  // namespace
 
 void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOperand& A, const GemmOperand& B,
@@ -404,9 +608,17 @@ void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOpera
     if (!aligned16(A.ptr) || !aligned16(B.ptr) || (A.ld % 8) || (B.ld % 8))
         throw MeftError(2, "gemm_bf16: operands need 16-byte aligned base and leading dimension % 8 == 0");
     check_epilogue(epi);
+    KArgs args = base_args(M, N, K, epi);
     const CUtensorMap ta = A.mn_major ? make_map(A.ptr, M, K, A.ld, 64, 64) : make_map(A.ptr, K, M, A.ld, 64, BM);
+    // large problems: 256x256 tiles on CTA pairs (enough pair-tiles to fill the machine at least once)
+    const int64_t pair_tiles = ceil_div(M, P_TILE_M) * ceil_div(N, BN);
+    if (pair_tiles >= num_sms() / 2 && pair_mode_enabled()) {
+        const CUtensorMap tb = B.mn_major ? make_map(B.ptr, N, K, B.ld, 64, 64) : make_map(B.ptr, K, N, B.ld, 64, 128);
+        args.tiles_m = int(ceil_div(M, P_TILE_M));
+        launch_pair_dispatch(st, A.mn_major, B.mn_major, ta, tb, args, int(pair_tiles));
+        return;
+    }
     const CUtensorMap tb = B.mn_major ? make_map(B.ptr, N, K, B.ld, 64, 64) : make_map(B.ptr, K, N, B.ld, 64, BN);
-    const KArgs args = base_args(M, N, K, epi);
     dispatch(st, A.mn_major, B.mn_major, ta, tb, args, args.tiles_m * args.tiles_n);
 }
 

@@ -203,6 +203,14 @@ int main(int argc, char** argv) {
             fails += check_case(384, 512, 256, false, false, epi);
             fails += check_case(300, 260, 200, true, true, epi);
         }
+        // shapes large enough for the CTA-pair (256x256) kernel, incl. ragged M/N/K edges
+        const int pshapes[][3] = {{2304, 2304, 320}, {2200, 2500, 200}, {4096, 2048, 1024}};
+        for (auto& s : pshapes)
+            for (auto& mj : majors) fails += check_case(s[0], s[1], s[2], mj[0], mj[1], EPI_STORE_F32);
+        for (int epi : {EPI_RELU_BF16, EPI_MASK_BF16, EPI_ROWS_ADD_F32}) {
+            fails += check_case(2304, 2304, 256, false, false, epi);
+            fails += check_case(2200, 2500, 130, true, true, epi);
+        }
         std::printf("gemm_check: %d failures\n", fails);
         return fails ? 1 : 0;
     }
