@@ -303,7 +303,7 @@ def our_arm(args, rank, world, local_rank):
     gemm_tflops = gemm_flops / (gemm_ms / gemm_launches * 1e-3) / 1e12
     tc_peak = peaks.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"])
     hbm = peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"])
-    adam_bytes = 2 * S * d * 34.0  # read w,m,v,g + write w,m,v,g(=0) fp32 + bf16 copy, key and value rows
+    adam_bytes = 2 * S * d * 30.0  # read w,m,v,g + write w,m,v fp32 + bf16 copy, key and value rows (§8d)
     gather_bytes = 2 * S * d * 2 * 2.0
     adam_ms = phases["adam"][0] / args.steps
     gather_ms = phases["gather"][0] / args.steps
@@ -312,6 +312,13 @@ def our_arm(args, rank, world, local_rank):
     key_bytes = (M * d * 2) + T * d * 2
     roof_ms = (6 * gemm_flops / (tc_peak * 1e12) + adam_bytes / (hbm * 1e9) + key_bytes / (hbm * 1e9)
                + 2 * T * N * d / (tc_peak * 1e12)) * 1e3
+
+    # DRAM traffic per GEMM launch from the committed ncu --set full capture of one step's six GEMMs
+    traffic = None
+    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "gemm_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get("mean_dram_bytes_per_launch")
 
     cpu = None
     if world == 1 and not args.skip_cpu_baseline:
@@ -334,14 +341,15 @@ def our_arm(args, rank, world, local_rank):
                        global_tokens=T * world,
                        parallelism="single GPU" if not sharded else f"expert-sharded ep{world} (NCCL all-to-all)",
                        precision="bf16 compute, fp32 "
-                       "master/Adam state", l2="inputs larger than L2 (9.7 GB of tables per layer)",
+                       "master/Adam state", l2="inputs larger than L2 (7.5 GB of tables per layer)",
                        union_size=S),
         "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": 2 * T * d * 2,
                 "d2h_bytes_per_step": 2 * T * d * 4, "ms_per_step": e2e_s * 1e3,
                 "path": "meft_layer_step_host (C ABI, pinned host buffers)" if not sharded else
                         "sharded layer step with pinned host copies in and out"},
         "roofline": {"bound": "tensor", "kernel": "k_gemm_bf16 (tcgen05 FFN GEMM)", "achieved": gemm_tflops,
-                     "peak": tc_peak, "unit": "TFLOP/s", "frac": gemm_tflops / tc_peak, "traffic": None,
+                     "peak": tc_peak, "unit": "TFLOP/s", "frac": gemm_tflops / tc_peak, "traffic": traffic,
+                     "traffic_unit": "bytes per launch (ncu dram read+write, profiles/gemm_traffic.json)",
                      "peak_source": f"{peak_src} bf16_tflops_sustained",
                      "per_launch": {"flops": gemm_flops, "ms": gemm_ms / gemm_launches}},
         "layer_roofline": {"roofline_ms": roof_ms, "measured_ms": ms, "frac": roof_ms / ms},

@@ -45,7 +45,16 @@ struct KArgs {
     int G, g_ntiles, g_brows;
     const int32_t* g_row_off;
     const int32_t* g_tile_off;
+    // pair-kernel raster: m-tiles per group (tiles_m = sweep all of M first); n_fast = sweep N first
+    int raster_group, raster_n_fast;
+    // K split: tile index = split * base_tiles + base tile; split s runs k-blocks [s*kb_split, (s+1)*kb_split)
+    int ksplit, kb_split;
+    long long split_stride;
 };
+
+__device__ __forceinline__ int base_tile_count(const KArgs& a) {
+    return a.grouped ? a.g_tile_off[a.G] * a.g_ntiles : a.tiles_m * a.tiles_n;
+}
 
 struct TileInfo {
     int a_row0;  // first A row (global)
@@ -90,7 +99,8 @@ __device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, 
     n_blk = local / gm;
 }
 
-__device__ __forceinline__ void epilogue_chunk(const KArgs& a, int m, int n, const uint32_t (&r)[32]) {
+__device__ __forceinline__ void epilogue_chunk(const KArgs& a, int m, int n, const uint32_t (&r)[32],
+                                               long long c_off = 0) {
     const int cnt = min(32, a.N - n);
     switch (a.epi) {
         case EPI_STORE_F32:
@@ -98,7 +108,7 @@ __device__ __forceinline__ void epilogue_chunk(const KArgs& a, int m, int n, con
         case EPI_ROWS_STORE_F32: {
             const long long row = (a.epi != EPI_STORE_F32) ? (long long)a.row_idx[m] : (long long)m;
             const bool acc = a.accumulate || a.epi == EPI_ROWS_ADD_F32;
-            float* c = reinterpret_cast<float*>(a.c) + row * a.ldc + n;
+            float* c = reinterpret_cast<float*>(a.c) + c_off + row * a.ldc + n;
             if (cnt == 32) {
                 float4* c4 = reinterpret_cast<float4*>(c);
 #pragma unroll
@@ -205,7 +215,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    const int num_tiles = args.grouped ? args.g_tile_off[args.G] * args.g_ntiles : args.tiles_m * args.tiles_n;
+    const int base_tiles = base_tile_count(args);
+    const int num_tiles = base_tiles * args.ksplit;
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
@@ -213,9 +224,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-                const TileInfo ti = resolve_tile(args, tile);
+                const int sp = tile / base_tiles;
+                const TileInfo ti = resolve_tile(args, tile - sp * base_tiles);
                 const int m0 = ti.a_row0, n0 = ti.b_row0;
-                for (int kb = 0; kb < args.num_kb; ++kb) {
+                const int kb0 = sp * args.kb_split, kb1 = min(args.num_kb, kb0 + args.kb_split);
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(empty + stage, phase ^ 1);
                     uint8_t* sa = smem + stage * STAGE_BYTES;
                     uint8_t* sb = sa + A_BYTES;
@@ -253,7 +266,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 mbar_wait(tempty + acc, aphase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
-                for (int kb = 0; kb < args.num_kb; ++kb) {
+                const int kb0 = (tile / base_tiles) * args.kb_split, kb1 = min(args.num_kb, kb0 + args.kb_split);
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(full + stage, phase);
                     tc_fence_after();
                     const uint32_t a_addr = smem_u32(smem + stage * STAGE_BYTES);
@@ -266,7 +280,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                                  : umma_desc_sw128(a_addr + k * 32, 16, 1024);
                         const uint64_t bd = B_MN ? umma_desc_sw128(b_addr + k * 2048, 8192, 1024)
                                                  : umma_desc_sw128(b_addr + k * 32, 16, 1024);
-                        umma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                        umma_bf16(d_tmem, ad, bd, idesc, (kb != kb0 || k != 0));
                     }
                     umma_commit(empty + stage);  // frees this smem stage once the MMAs above retire
                     if (++stage == STAGES) {
@@ -282,7 +296,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int q = warp & 3;  // TMEM lane quarter this warp may access
         int it = 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-            const TileInfo ti = resolve_tile(args, tile);
+            const int sp = tile / base_tiles;
+            const TileInfo ti = resolve_tile(args, tile - sp * base_tiles);
+            const long long c_off = sp * args.split_stride;
             const int acc = it & 1;
             const uint32_t aphase = (it >> 1) & 1;
             mbar_wait(tfull + acc, aphase);
@@ -294,7 +310,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c * 32, r);
                 tmem_ld_wait();
                 const int n = ti.n_col0 + c * 32;
-                if (m < ti.m_lim && n < args.N) epilogue_chunk(args, m, n, r);
+                if (m < ti.m_lim && n < args.N) epilogue_chunk(args, m, n, r, c_off);
             }
             tc_fence_before();
             __syncwarp();
@@ -324,8 +340,14 @@ constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
 constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + 1024 + 256;
 constexpr int P_TILE_M = 256;
 
-__device__ __forceinline__ void tile_coords_pair(int tile, int tiles_m, int tiles_n, int& m_blk, int& n_blk) {
-    const int group = 8;  // 8 pair-tiles of M share each B panel while resident
+__device__ __forceinline__ void tile_coords_pair(int tile, const KArgs& args, int& m_blk, int& n_blk) {
+    const int tiles_m = args.tiles_m, tiles_n = args.tiles_n;
+    if (args.raster_n_fast) {  // B resident in L2, A streamed once
+        m_blk = tile / tiles_n;
+        n_blk = tile % tiles_n;
+        return;
+    }
+    const int group = args.raster_group;  // pair-tiles of M that share each B panel while resident
     const int group_size = group * tiles_n;
     const int g = tile / group_size;
     const int first_m = g * group;
@@ -382,7 +404,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             uint32_t phase = 0;
             for (int tile = pair; tile < num_tiles; tile += npairs) {
                 int mb, nb;
-                tile_coords_pair(tile, args.tiles_m, args.tiles_n, mb, nb);
+                tile_coords_pair(tile, args, mb, nb);
                 const int m0 = mb * P_TILE_M + int(rank) * 128;  // this CTA's A rows
                 const int n0 = nb * BN + int(rank) * 128;        // this CTA's half of the B rows
                 for (int kb = 0; kb < args.num_kb; ++kb) {
@@ -451,7 +473,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         int it = 0;
         for (int tile = pair; tile < num_tiles; tile += npairs, ++it) {
             int mb, nb;
-            tile_coords_pair(tile, args.tiles_m, args.tiles_n, mb, nb);
+            tile_coords_pair(tile, args, mb, nb);
             const int acc = it & 1;
             const uint32_t aphase = (it >> 1) & 1;
             mbar_wait(tfull + acc, aphase);
@@ -549,6 +571,16 @@ KArgs base_args(int64_t M, int64_t N, int64_t K, const GemmEpilogue& epi) {
     args.ldm = epi.ldm;
     args.row_idx = epi.row_idx;
     args.grouped = 0;
+    args.ksplit = 1;
+    args.kb_split = args.num_kb;
+    args.split_stride = 0;
+    if (epi.ksplit > 1) {
+        if (!(epi.kind == EPI_STORE_F32 || epi.kind == EPI_ROWS_STORE_F32) || epi.accumulate)
+            throw MeftError(2, "gemm_bf16: K split needs a plain f32 store epilogue");
+        args.kb_split = int(ceil_div(args.num_kb, epi.ksplit));
+        args.ksplit = int(ceil_div(args.num_kb, args.kb_split));  // no empty splits
+        args.split_stride = epi.split_stride;
+    }
     return args;
 }
 
@@ -612,14 +644,22 @@ void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOpera
     const CUtensorMap ta = A.mn_major ? make_map(A.ptr, M, K, A.ld, 64, 64) : make_map(A.ptr, K, M, A.ld, 64, BM);
     // large problems: 256x256 tiles on CTA pairs (enough pair-tiles to fill the machine at least once)
     const int64_t pair_tiles = ceil_div(M, P_TILE_M) * ceil_div(N, BN);
-    if (pair_tiles >= num_sms() / 2 && pair_mode_enabled()) {
+    if (pair_tiles >= num_sms() / 2 && pair_mode_enabled() && args.ksplit == 1) {
         const CUtensorMap tb = B.mn_major ? make_map(B.ptr, N, K, B.ld, 64, 64) : make_map(B.ptr, K, N, B.ld, 64, 128);
         args.tiles_m = int(ceil_div(M, P_TILE_M));
+        // G pair-tiles of M share each streamed B panel.  Measured (ncu dram bytes + time, tools/gemm_check):
+        // K-major x K-major (z, dA: K = d) likes 16 (dA 3.31 -> 3.08 ms); the long-K / MN-major GEMMs 8.
+        // Sweeping all of M first doubles DRAM reads: a 64 MB 'resident' operand does not survive per-die L2.
+        static const int forced = [] {
+            const char* v = std::getenv("MEFT_PAIR_GROUP");  // A/B experiments
+            return v ? std::max(1, std::atoi(v)) : 0;
+        }();
+        args.raster_group = forced ? forced : (!A.mn_major && !B.mn_major ? 16 : 8);
         launch_pair_dispatch(st, A.mn_major, B.mn_major, ta, tb, args, int(pair_tiles));
         return;
     }
     const CUtensorMap tb = B.mn_major ? make_map(B.ptr, N, K, B.ld, 64, 64) : make_map(B.ptr, K, N, B.ld, 64, BN);
-    dispatch(st, A.mn_major, B.mn_major, ta, tb, args, args.tiles_m * args.tiles_n);
+    dispatch(st, A.mn_major, B.mn_major, ta, tb, args, args.tiles_m * args.tiles_n * args.ksplit);
 }
 
 void gemm_bf16_grouped(cudaStream_t st, int G, int64_t N, int64_t K, const GemmOperand& A, int64_t a_rows,
@@ -639,7 +679,7 @@ void gemm_bf16_grouped(cudaStream_t st, int G, int64_t N, int64_t K, const GemmO
     args.g_brows = int(N);
     args.g_row_off = row_off;
     args.g_tile_off = tile_off;
-    const int64_t bound = (ceil_div(a_rows, BM) + G) * args.g_ntiles;  // >= device-side tile count
+    const int64_t bound = (ceil_div(a_rows, BM) + G) * args.g_ntiles * args.ksplit;  // >= device tile count
     dispatch(st, false, false, ta, tb, args, int(std::min<int64_t>(bound, INT32_MAX)));
 }
 

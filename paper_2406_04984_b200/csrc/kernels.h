@@ -32,6 +32,10 @@ struct GemmEpilogue {
     int64_t ldm = 0;
     const int32_t* row_idx = nullptr;
     bool accumulate = false;
+    // K split (f32 store epilogues, 1-CTA kernel): split s of `ksplit` multiplies K-chunk s only and writes its
+    // partial product to c + s * split_stride (elements); the caller sums the partials.
+    int ksplit = 1;
+    int64_t split_stride = 0;
 };
 
 void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOperand& A, const GemmOperand& B,

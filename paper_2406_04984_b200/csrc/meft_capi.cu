@@ -99,6 +99,7 @@ struct LayerBufs {
     float* kn = nullptr;      // MIXED: cached norms of the bf16 compute keys
     int32_t* kl = nullptr;    // MIXED: cached minimum LSB exponents of the bf16 compute keys
     void* base = nullptr;
+    void* stage_base = nullptr;  // staging tables, allocated on first use (scatter_grads / staging access)
 };
 
 }  // namespace
@@ -109,6 +110,9 @@ struct meft_store {
     int device = 0;
     std::vector<LayerBufs> L;
     std::vector<char> key_stats_valid;  // per layer: kn/kl match the current compute keys
+    // per layer: staging may hold gradients (scatter_grads / caller access) that the next Adam must consume.
+    // While clear, staging is all zero and the fused layer step bypasses it entirely.
+    std::vector<char> pending;
 };
 
 namespace {
@@ -419,9 +423,38 @@ void uniform_fill(uint64_t seed, double lo, double hi, double* out, int64_t n) {
     }
 }
 
+// Staging tables (the reference's stage_a/stage_b, memtier.hpp:110-113) are allocated zeroed on first use: the
+// fused layer step never needs them, which keeps 2 x pairs x d fp32 per layer out of HBM.
+void ensure_staging(meft_store* s, int64_t layer) {
+    LayerBufs& L = s->L[size_t(layer)];
+    if (L.stage_base) return;
+    const size_t mb = s->prec == MEFT_STORE_F64 ? 8 : 4;
+    const size_t one = (size_t(s->pairs) * size_t(s->d) * mb + 255) & ~size_t(255);
+    int prev = 0;
+    MEFT_CUDA_CHECK(cudaGetDevice(&prev));
+    MEFT_CUDA_CHECK(cudaSetDevice(s->device));
+    cudaError_t e = cudaMalloc(&L.stage_base, 2 * one);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        L.stage_base = nullptr;
+        cudaSetDevice(prev);
+        throw MeftError(MEFT_E_OOM, "staging: cannot allocate " + std::to_string(2 * one) + " bytes for layer " +
+                                        std::to_string(layer));
+    }
+    MEFT_CUDA_CHECK(cudaMemset(L.stage_base, 0, 2 * one));
+    L.st_a = L.stage_base;
+    L.st_b = static_cast<uint8_t*>(L.stage_base) + one;
+    MEFT_CUDA_CHECK(cudaSetDevice(prev));
+}
+
+bool is_staging(meft_tensor t) { return t == MEFT_T_STAGE_A || t == MEFT_T_STAGE_B || t == MEFT_T_STAGED; }
+
 // ---- sparse Adam over the staged set (memtier.cpp:187-210)
 
-void adam_impl(meft_ctx* ctx, meft_store* s, const LayerBufs& L, double b1, double b2, double eps, double lr) {
+void adam_impl(meft_ctx* ctx, meft_store* s, int64_t layer, double b1, double b2, double eps, double lr) {
+    const LayerBufs& L = s->L[size_t(layer)];
+    s->pending[size_t(layer)] = 0;
+    if (!L.stage_base) return;  // staging never touched: nothing is staged (flags are only set with it)
     cudaStream_t st = ctx->stream;
     int32_t* rows = static_cast<int32_t*>(ctx->get("adam_rows", size_t(s->pairs) * 4));
     int32_t* bws = static_cast<int32_t*>(ctx->get("adam_bws", size_t((s->pairs + 1023) / 1024 + 1) * 4));
@@ -765,7 +798,7 @@ meft_status meft_store_create(meft_ctx* ctx, int64_t layers, int64_t d, int64_t 
         const int mb = precision == MEFT_STORE_F64 ? 8 : 4;
         const size_t pd = size_t(pairs) * size_t(d), nd = size_t(experts) * size_t(d);
         auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-        size_t bytes = 8 * al(pd * mb) + al(nd * mb) + al(size_t(pairs) * 4) + al(size_t(pairs));
+        size_t bytes = 6 * al(pd * mb) + al(nd * mb) + al(size_t(pairs) * 4) + al(size_t(pairs));
         if (precision == MEFT_STORE_MIXED) bytes += 2 * al(pd * 2) + al(nd * 2) + 2 * al(size_t(pairs) * 4);
         for (int64_t l = 0; l < layers; ++l) {
             LayerBufs L;
@@ -789,8 +822,6 @@ meft_status meft_store_create(meft_ctx* ctx, int64_t layers, int64_t d, int64_t 
             L.v_a = take(pd * mb);
             L.m_b = take(pd * mb);
             L.v_b = take(pd * mb);
-            L.st_a = take(pd * mb);
-            L.st_b = take(pd * mb);
             L.w_g = take(nd * mb);
             L.step = static_cast<int32_t*>(take(size_t(pairs) * 4));
             L.staged = static_cast<uint8_t*>(take(size_t(pairs)));
@@ -807,6 +838,7 @@ meft_status meft_store_create(meft_ctx* ctx, int64_t layers, int64_t d, int64_t 
             }
             s->L.push_back(L);
             s->key_stats_valid.push_back(0);
+            s->pending.push_back(0);
         }
         MEFT_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
         *out = s.release();
@@ -816,7 +848,10 @@ meft_status meft_store_create(meft_ctx* ctx, int64_t layers, int64_t d, int64_t 
 void meft_store_destroy(meft_store* store) {
     if (!store) return;
     cudaSetDevice(store->device);
-    for (auto& L : store->L) cudaFree(L.base);
+    for (auto& L : store->L) {
+        cudaFree(L.base);
+        if (L.stage_base) cudaFree(L.stage_base);
+    }
     delete store;
 }
 
@@ -853,6 +888,10 @@ meft_status meft_store_upload_host(meft_ctx* ctx, meft_store* s, int64_t layer, 
     return guarded(ctx, [&] {
         require_ctx(ctx);
         const LayerBufs& L = layer_of(s, layer);
+        if (is_staging(t)) {
+            ensure_staging(s, layer);
+            s->pending[size_t(layer)] = 1;
+        }
         if (t == MEFT_T_PAIR_STEP || t == MEFT_T_STAGED) {
             require(rows * cols == s->pairs, MEFT_E_SHAPE, "store_upload: counter length");
             if (t == MEFT_T_PAIR_STEP) {
@@ -882,6 +921,7 @@ meft_status meft_store_download_host(meft_ctx* ctx, meft_store* s, int64_t layer
     return guarded(ctx, [&] {
         require_ctx(ctx);
         const LayerBufs& L = layer_of(s, layer);
+        if (is_staging(t)) ensure_staging(s, layer);
         if (t == MEFT_T_PAIR_STEP || t == MEFT_T_STAGED) {
             require(rows * cols == s->pairs, MEFT_E_SHAPE, "store_download: counter length");
             if (t == MEFT_T_PAIR_STEP) {
@@ -908,6 +948,10 @@ meft_status meft_store_tensor(meft_store* s, int64_t layer, meft_tensor t, void*
                               int64_t* cols) {
     return guarded(nullptr, [&] {
         const LayerBufs& L = layer_of(s, layer);
+        if (is_staging(t)) {  // the caller may write through the view: the next Adam must consume staging
+            ensure_staging(s, layer);
+            s->pending[size_t(layer)] = 1;
+        }
         meft_dtype d0;
         int64_t r0, c0;
         void* p = tensor_ptr(s, L, t, &d0, &r0, &c0);
@@ -937,6 +981,8 @@ meft_status meft_scatter_grads(meft_ctx* ctx, meft_store* s, int64_t layer, cons
         require(gdt == MEFT_F64 || gdt == MEFT_F32, MEFT_E_INVALID, "scatter_grads: gradient dtype must be F64/F32");
         if (n <= 0) return;
         const int code = validate_indices(ctx, S, n, s->pairs, "scatter_grads", false);
+        ensure_staging(s, layer);
+        s->pending[size_t(layer)] = 1;
         const int sdt = s->prec == MEFT_STORE_F64 ? 0 : 1;
         if (code == 0) {  // strictly ascending => unique rows => one CTA per row, no atomics
             stage_add(ctx->stream, sdt, L.st_a, s->d, S, n, dcode(gdt), gk, L.staged);
@@ -957,7 +1003,8 @@ meft_status meft_sparse_adam_update(meft_ctx* ctx, meft_store* s, int64_t layer,
                                     double eps, double lr) {
     return guarded(ctx, [&] {
         require_ctx(ctx);
-        adam_impl(ctx, s, layer_of(s, layer), beta1, beta2, eps, lr);
+        layer_of(s, layer);
+        adam_impl(ctx, s, layer, beta1, beta2, eps, lr);
         s->key_stats_valid[size_t(layer)] = 0;
     });
 }
@@ -1041,18 +1088,34 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
     if (fwd_done) MEFT_CUDA_CHECK(cudaEventRecord(fwd_done, st));
     if (g_ready) MEFT_CUDA_CHECK(cudaStreamWaitEvent(st, g_ready, 0));
 
-    // sparse_backward + scatter_grads fused: weight-grad GEMM epilogues add straight into stage rows at S
-    {
-        PhaseScope ps(ctx, 3);
-        ffn_backward_impl(ctx, MEFT_BF16, g, h, act, ks, vs, T, d, su, ld, masked, nullptr, nullptr, ghb, false, uni,
-                          L.st_a, L.st_b);
-    }
-
-    // sparse_adam_update (memtier.cpp:187-210) over the staged pairs
-    {
+    if (s->pending[size_t(layer)]) {
+        // earlier scatter_grads are pending: sparse_backward + scatter_grads fused, the weight-grad GEMM epilogues
+        // add straight into the stage rows at S, then Adam consumes every staged pair (memtier.cpp:187-210)
+        ensure_staging(s, layer);
+        {
+            PhaseScope ps(ctx, 3);
+            ffn_backward_impl(ctx, MEFT_BF16, g, h, act, ks, vs, T, d, su, ld, masked, nullptr, nullptr, ghb, false,
+                              uni, L.st_a, L.st_b);
+        }
         PhaseScope ps(ctx, 4);
         if (su > 0) mark_rows(st, L.staged, uni, nullptr, su);
-        adam_impl(ctx, s, L, b1, b2, eps, lr);
+        adam_impl(ctx, s, layer, b1, b2, eps, lr);
+    } else {
+        // staging is all zero, so staged == S exactly: the weight grads go to a dense [|S| x d] step block that
+        // Adam reads in place of the staging rows (same values, no staging traffic, nothing to zero)
+        float* gka = static_cast<float*>(ctx->get("step_gka", size_t(std::max<int64_t>(su, 1) * d) * 4));
+        float* gvb = static_cast<float*>(ctx->get("step_gvb", size_t(std::max<int64_t>(su, 1) * d) * 4));
+        {
+            PhaseScope ps(ctx, 3);
+            ffn_backward_impl(ctx, MEFT_BF16, g, h, act, ks, vs, T, d, su, ld, masked, gka, gvb, ghb, false, nullptr,
+                              nullptr, nullptr);
+        }
+        PhaseScope ps(ctx, 4);
+        if (su > 0)
+            adam_mixed(st, uni, nullptr, su, d, static_cast<float*>(L.w_a), static_cast<float*>(L.m_a),
+                       static_cast<float*>(L.v_a), gka, static_cast<uint16_t*>(L.c_a), static_cast<float*>(L.w_b),
+                       static_cast<float*>(L.m_b), static_cast<float*>(L.v_b), gvb, static_cast<uint16_t*>(L.c_b),
+                       L.step, nullptr, b1, b2, eps, lr, 3, true, true);
     }
     s->key_stats_valid[size_t(layer)] = 0;
 }

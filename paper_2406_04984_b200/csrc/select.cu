@@ -423,6 +423,10 @@ size_t exact_workspace_bytes(int64_t T, int64_t M, int64_t N, int64_t kk_eff) {
     return b;
 }
 
+// K-chunks of the candidate-scoring GEMM: 512-wide chunks tighten the certified bound ~d/512-fold, which cuts the
+// exact fp64 re-scoring proportionally (profiles/: 27 -> ~4 ambiguous candidates per token at d = 4096).
+int cert_ksplit(int64_t d) { return int(std::max<int64_t>(1, std::min<int64_t>(8, d / 512))); }
+
 size_t cert_workspace_bytes(int64_t T, int64_t d, int64_t M, int64_t N, int64_t kk_eff) {
     const int64_t E = M / N;
     size_t b = 0;
@@ -434,7 +438,7 @@ size_t cert_workspace_bytes(int64_t T, int64_t d, int64_t M, int64_t N, int64_t 
     add(T * kk_eff * 4);          // entries
     add((N + 1) * 4 * 4);         // counts, off, tile_off, cursor
     add(T * kk_eff * d * 2);      // token rows bucketed by expert (bf16)
-    add(T * kk_eff * E * 4);      // approximate candidate scores (fp32)
+    add(T * kk_eff * E * 4 * cert_ksplit(d));  // approximate candidate scores (fp32 partials per K-chunk)
     add(M);                       // union flags
     add(((M + 1023) / 1024 + 1) * 4);
     const int64_t C = kk_eff * E, take_max = C;
@@ -490,7 +494,8 @@ static void ke_select_certified(cudaStream_t st, const void* h_, const void* w_g
     int32_t* tile_off = off + (N + 1);
     int32_t* cursor = tile_off + (N + 1);
     uint16_t* hs = static_cast<uint16_t*>(take_buf(T * kk_eff * d * 2));
-    float* cand = static_cast<float*>(take_buf(T * C * 4));
+    const int ksplit = N == 1 ? 1 : cert_ksplit(d);
+    float* cand = static_cast<float*>(take_buf(T * C * 4 * ksplit));
     uint8_t* flags = static_cast<uint8_t*>(take_buf(M));
     int32_t* boff = static_cast<int32_t*>(take_buf(((M + 1023) / 1024 + 1) * 4));
     const double cb = cert_bound_coeff(int(d));
@@ -544,6 +549,8 @@ static void ke_select_certified(cudaStream_t st, const void* h_, const void* w_g
         eg.c = cand;
         eg.ldc = E;
         eg.row_idx = entries;
+        eg.ksplit = ksplit;
+        eg.split_stride = T * C;
         gemm_bf16_grouped(st, int(N), E, d, GemmOperand{hs, d, false}, rows, GemmOperand{keys, d, false}, M, off,
                           tile_off, eg);
     }
@@ -560,16 +567,19 @@ static void ke_select_certified(cudaStream_t st, const void* h_, const void* w_g
     int32_t* atile = aoff + (N + 1);
     int32_t* acur = atile + (N + 1);
     const int P2 = next_pow2(int(C)), TP2 = next_pow2(int(take));
-    const size_t csm = size_t(C) * 5 + 16;  // classify: u32 keys + u8 membership
+    const size_t csm = size_t(C) * 9 + 16;  // classify: u32 keys + f32 scores + u8 membership
     if (csm > 200 * 1024) throw MeftError(2, "ke_select: candidate set too large for the certified path");
+    // the split GEMM really used kb_split*64-wide chunks (no empty splits): recompute them exactly like base_args
+    const int64_t nkb = (d + 63) / 64, kbs = (nkb + ksplit - 1) / ksplit, ks_eff = (nkb + kbs - 1) / kbs;
+    const double cbk = ksplit > 1 ? cert_bound_coeff_split(int(d), int(kbs * 64), int(ks_eff)) : cb;
     static bool cattr = false;
     if (!cattr) {
         MEFT_CUDA_CHECK(cudaFuncSetAttribute(k_topk_classify, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         cattr = true;
     }
     MEFT_CUDA_CHECK(cudaMemsetAsync(acount, 0, N * 4, st));
-    k_topk_classify<<<int(T), 256, csm, st>>>(cand, tau, int(kk_eff), int(E), int(C), P2, int(take), hn, kn, cb, sure,
-                                              n_sure, amb, n_amb, acount);
+    k_topk_classify<<<int(T), 256, csm, st>>>(cand, tau, int(kk_eff), int(E), int(C), P2, int(take), hn, kn, cbk,
+                                              sure, n_sure, amb, n_amb, acount, ks_eff, (long long)(T * C));
     check_launch("k_topk_classify");
     k_bucket_scan<<<1, 1024, 0, st>>>(acount, int(N), aoff, atile, acur, 1);
     check_launch("k_bucket_scan");
@@ -819,14 +829,15 @@ void topk_classify(cudaStream_t st, const float* cand, const int32_t* tau, int64
                    int32_t* amb, int32_t* n_amb, int32_t* amb_count_per_expert) {
     if (T <= 0) return;
     const int64_t C = kk * E;
-    const size_t csm = size_t(C) * 5 + 16;
+    const size_t csm = size_t(C) * 9 + 16;
     static bool cattr = false;
     if (!cattr) {
         MEFT_CUDA_CHECK(cudaFuncSetAttribute(k_topk_classify, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         cattr = true;
     }
     k_topk_classify<<<int(T), 256, csm, st>>>(cand, tau, int(kk), int(E), int(C), next_pow2(int(C)), int(take), hn, kn,
-                                              cert_bound_coeff(int(d)), sure, n_sure, amb, n_amb, amb_count_per_expert);
+                                              cert_bound_coeff(int(d)), sure, n_sure, amb, n_amb, amb_count_per_expert,
+                                              1, 0);
     check_launch("k_topk_classify");
 }
 

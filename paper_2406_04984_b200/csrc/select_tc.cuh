@@ -23,6 +23,15 @@ __host__ __device__ inline double cert_bound_coeff(int d) {
     return 32.0 * 0x1p-24 * double((d + 15) / 16 + 1) + double(d) * 0x1p-52;
 }
 
+// Same bound when the tensor-core score is the fp64 sum of `ksplit` partial products over K-chunks of at most
+// `chunk` elements, rounded to fp32: per-chunk accumulation error sum_c CB(chunk)*|h_c||k_c| <= CB(chunk)*|h||k|
+// (Cauchy-Schwarz), plus the reference's own fp64 rounding over all d terms, the fp64 sum of the partials and
+// the final fp32 rounding.
+__host__ __device__ inline double cert_bound_coeff_split(int d, int chunk, int ksplit) {
+    return 32.0 * 0x1p-24 * double((chunk + 15) / 16 + 1) + double(d) * 0x1p-52 + double(ksplit) * 0x1p-52 +
+           0x1p-23;
+}
+
 // exponent of the least significant mantissa bit of a bf16 value (subnormals: 2^-133)
 __device__ __forceinline__ int bf16_lsb_exp(uint16_t b) {
     const int e = (b >> 7) & 0xFF;
@@ -290,17 +299,28 @@ __global__ void __launch_bounds__(256)
     k_topk_classify(const float* __restrict__ cand, const int32_t* __restrict__ tau, int kk, int E, int C, int P2,
                     int take, const float* __restrict__ hn, const float* __restrict__ kn, double cb,
                     int32_t* __restrict__ sure, int32_t* __restrict__ n_sure, int32_t* __restrict__ amb,
-                    int32_t* __restrict__ n_amb, int32_t* __restrict__ amb_count) {
+                    int32_t* __restrict__ n_amb, int32_t* __restrict__ amb_count, int ksplit,
+                    long long split_stride) {
     extern __shared__ __align__(16) uint8_t sm[];
     uint32_t* key = reinterpret_cast<uint32_t*>(sm);
-    uint8_t* in_top = reinterpret_cast<uint8_t*>(key + C);
+    float* val = reinterpret_cast<float*>(key + C);  // approximate scores (sum of the K-split partials)
+    uint8_t* in_top = reinterpret_cast<uint8_t*>(val + C);
     __shared__ double w_lin[32], w_uout[32];
     __shared__ int hist[256], w_cnt[32];
     __shared__ uint32_t s_prefix;
     __shared__ int s_remaining, s_na, s_ns;
     const int t = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     const float* c = cand + int64_t(t) * C;
-    for (int i = tid; i < C; i += blockDim.x) key[i] = float_key(c[i]);
+    for (int i = tid; i < C; i += blockDim.x) {
+        float v = c[i];
+        if (ksplit > 1) {
+            double sum = double(v);
+            for (int sp = 1; sp < ksplit; ++sp) sum += double(c[sp * split_stride + i]);
+            v = float(sum);
+        }
+        val[i] = v;
+        key[i] = float_key(v);
+    }
     if (tid == 0) {
         s_na = 0;
         s_ns = 0;
@@ -374,8 +394,8 @@ __global__ void __launch_bounds__(256)
         const int slot = i / E;
         const int gi = my_tau[slot] * E + (i - slot * E);
         const double e = he * double(kn[gi]);
-        if (in_top[i]) lin = fmin(lin, double(c[i]) - e);
-        else uout = fmax(uout, double(c[i]) + e);
+        if (in_top[i]) lin = fmin(lin, double(val[i]) - e);
+        else uout = fmax(uout, double(val[i]) + e);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -400,7 +420,7 @@ __global__ void __launch_bounds__(256)
         const int gi = my_tau[slot] * E + (i - slot * E);
         const double e = he * double(kn[gi]);
         const bool top = in_top[i];
-        const bool ambiguous = top ? (double(c[i]) - e <= uout) : (double(c[i]) + e >= lin);
+        const bool ambiguous = top ? (double(val[i]) - e <= uout) : (double(val[i]) + e >= lin);
         if (ambiguous) {
             my_amb[atomicAdd(&s_na, 1)] = gi;
             if (amb_count) atomicAdd(&amb_count[gi / E], 1);

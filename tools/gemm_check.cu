@@ -191,6 +191,49 @@ static void perf_case(const char* name, int M, int N, int K, bool amn, bool bmn,
     if (mask) cudaFree(mask);
 }
 
+// K split: partials of `ks` K-chunks written to C + s*stride, summed here and compared with the reference.
+static int check_split(int M, int N, int K, int ks) {
+    const int64_t lda = (K + 7) / 8 * 8 + 8, ldb = lda;
+    uint16_t* A = alloc_fill(M * lda, 7 + M, 1.0f);
+    uint16_t* B = alloc_fill(N * ldb, 3 + N, 1.0f);
+    float* R;
+    CK(cudaMalloc(&R, (int64_t)M * N * 4));
+    k_ref<<<dim3((N + 127) / 128, M), 128>>>(M, N, K, A, lda, false, B, ldb, false, R);
+    CK(cudaGetLastError());
+    std::vector<float> ref((size_t)M * N);
+    CK(cudaMemcpy(ref.data(), R, ref.size() * 4, cudaMemcpyDeviceToHost));
+    const int64_t ldc = (N + 7) / 8 * 8, stride = (int64_t)M * ldc;
+    float* C;
+    CK(cudaMalloc(&C, ks * stride * 4));
+    CK(cudaMemset(C, 0, ks * stride * 4));
+    GemmEpilogue e;
+    e.kind = EPI_STORE_F32;
+    e.c = C;
+    e.ldc = ldc;
+    e.ksplit = ks;
+    e.split_stride = stride;
+    gemm_bf16(0, M, N, K, GemmOperand{A, lda, false}, GemmOperand{B, ldb, false}, e);
+    CK(cudaDeviceSynchronize());
+    std::vector<float> hc(ks * stride);
+    CK(cudaMemcpy(hc.data(), C, hc.size() * 4, cudaMemcpyDeviceToHost));
+    double max_err = 0, max_ref = 0;
+    for (int m = 0; m < M; ++m)
+        for (int n = 0; n < N; ++n) {
+            double got = 0;
+            for (int s = 0; s < ks; ++s) got += hc[s * stride + (size_t)m * ldc + n];
+            max_err = std::fmax(max_err, std::fabs(got - ref[(size_t)m * N + n]));
+            max_ref = std::fmax(max_ref, std::fabs(ref[(size_t)m * N + n]));
+        }
+    const double rel = max_err / (max_ref > 0 ? max_ref : 1);
+    const bool ok = rel < 1e-4;
+    std::printf("split M=%5d N=%5d K=%5d ks=%d  max_rel_err=%.3e  %s\n", M, N, K, ks, rel, ok ? "OK" : "FAIL");
+    cudaFree(A);
+    cudaFree(B);
+    cudaFree(C);
+    cudaFree(R);
+    return ok ? 0 : 1;
+}
+
 int main(int argc, char** argv) {
     const bool perf = argc > 1 && std::strcmp(argv[1], "perf") == 0;
     int fails = 0;
@@ -211,6 +254,9 @@ int main(int argc, char** argv) {
             fails += check_case(2304, 2304, 256, false, false, epi);
             fails += check_case(2200, 2500, 130, true, true, epi);
         }
+        fails += check_split(300, 260, 1024, 8);
+        fails += check_split(512, 256, 4096, 8);
+        fails += check_split(200, 300, 650, 3);
         std::printf("gemm_check: %d failures\n", fails);
         return fails ? 1 : 0;
     }

@@ -2,6 +2,9 @@
 
   python tools/summarize_ncu.py launches <launches.csv>     per-kernel share of device time (launch list)
   python tools/summarize_ncu.py full <report.ncu-rep>       key metrics of a --set full capture
+  python tools/summarize_ncu.py traffic <report.ncu-rep> <out.json>
+                                                            mean per-launch DRAM bytes of the captured kernels
+                                                            (bench.py reports it as roofline.traffic)
 """
 import collections
 import csv
@@ -51,5 +54,26 @@ def full(path):
                 print(f"  {k} = {v[i]} {u[i]}")
 
 
+def traffic(path, out_json):
+    import json
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h, u = rows[0], rows[1]
+    unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    per = []
+    for v in rows[2:]:
+        b = 0.0
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = h.index(k)
+            b += float(v[i].replace(",", "")) * unit[u[i]]
+        per.append({"kernel": v[h.index("Kernel Name")].split("(")[0].split("::")[-1], "dram_bytes": b,
+                    "ms": float(v[h.index("gpu__time_duration.sum")].replace(",", "")) *
+                    {"ms": 1, "msecond": 1, "us": 1e-3, "usecond": 1e-3}[u[h.index("gpu__time_duration.sum")]]})
+    res = {"source": path.split("/")[-1], "launches": per,
+           "mean_dram_bytes_per_launch": sum(p["dram_bytes"] for p in per) / len(per)}
+    json.dump(res, open(out_json, "w"), indent=1)
+    print(json.dumps(res, indent=1))
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
+    {"launches": launches, "full": full, "traffic": traffic}[sys.argv[1]](*sys.argv[2:])
