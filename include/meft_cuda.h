@@ -97,6 +97,16 @@ meft_status meft_ctx_set_timing(meft_ctx* ctx, int enable);
 #define MEFT_SELECT_AUTO 0
 #define MEFT_SELECT_EXACT 1
 meft_status meft_ctx_set_selection(meft_ctx* ctx, int mode);
+
+/* How the fused layer step's FFN GEMMs read the selected key/value rows (the reference's fetch,
+ * memtier.cpp:117-126): KERNEL materialises them with a gather kernel; TMA has the GEMM producers load them
+ * straight from the tables (contiguous runs of the union as plain TMA boxes, the rest with tile::gather4);
+ * AUTO (default; environment MEFT_GATHER=kernel|tma overrides) takes TMA when the union is nearly one run.
+ * Both give bit-identical results. */
+#define MEFT_GATHER_AUTO 0
+#define MEFT_GATHER_KERNEL 1
+#define MEFT_GATHER_TMA 2
+meft_status meft_ctx_set_gather(meft_ctx* ctx, int mode);
 meft_status meft_ctx_read_timing(meft_ctx* ctx, double* ms5, int64_t* launches5);
 
 meft_status meft_device_alloc(meft_ctx* ctx, size_t bytes, void** out);

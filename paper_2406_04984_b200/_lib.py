@@ -36,6 +36,7 @@ _SIGS = {
     "meft_layer_ffn_local": (INT, [P, P, I64, P, P, I64, P, I64, D, D, D, D, P, P]),
     "meft_ctx_set_timing": (INT, [P, INT]),
     "meft_ctx_set_selection": (INT, [P, INT]),
+    "meft_ctx_set_gather": (INT, [P, INT]),
     "meft_ctx_read_timing": (INT, [P, P, P]),
     "meft_device_alloc": (INT, [P, C.c_size_t, C.POINTER(P)]),
     "meft_device_free": (INT, [P, P]),

@@ -50,7 +50,78 @@ struct KArgs {
     // K split: tile index = split * base_tiles + base tile; split s runs k-blocks [s*kb_split, (s+1)*kb_split)
     int ksplit, kb_split;
     long long split_stride;
+    // gathered B: logical B row p < b_idx_n is table row b_idx[p]; rows past it read as zeros (OOB index)
+    const int32_t* b_idx;
+    int b_idx_n, b_oob_row;
+    const int32_t* kb_run;  // MN-major gathered B: per k-block first table row of a contiguous run, or -1
 };
+
+__device__ __forceinline__ int gather_row(const KArgs& a, int p) {
+    return p < a.b_idx_n ? __ldg(a.b_idx + p) : a.b_oob_row;
+}
+
+// Gathered-B indices in the producer warp. A piece of B rows whose table rows form one contiguous run (the
+// common case for a dense union) is loaded as ONE plain 2-D box at the run's first table row; only broken
+// pieces fall back to tile::gather4 (~4x more TMA issue per stage). Indices are fetched with one coalesced warp
+// load per piece, one piece ahead, so the producer never waits on them.
+// MN-major B (gathered along K): the 64 k-rows of a k-block, lane l holds rows 2l and 2l+1.
+struct KRows {
+    int v0, v1;
+};
+__device__ __forceinline__ KRows load_krows(const KArgs& a, int k0, int lane) {
+    return KRows{gather_row(a, k0 + 2 * lane), gather_row(a, k0 + 2 * lane + 1)};
+}
+__device__ __forceinline__ void krows_four(const KRows& x, int r, int& i0, int& i1, int& i2, int& i3) {
+    const int l = r >> 1;  // rows r..r+3 (r % 4 == 0) live in lanes r/2 and r/2 + 1
+    i0 = __shfl_sync(0xffffffffu, x.v0, l);
+    i1 = __shfl_sync(0xffffffffu, x.v1, l);
+    i2 = __shfl_sync(0xffffffffu, x.v0, l + 1);
+    i3 = __shfl_sync(0xffffffffu, x.v1, l + 1);
+}
+// Per-k-block run table (identical for every tile): k_kb_runs builds it before the GEMM; the producer reads it
+// 32 k-blocks per warp load, one aligned batch ahead, so the latency of the read never reaches the TMA issue.
+struct RunBatch {
+    int cur = 0, cur_base = -1 << 30, nxt = 0, nxt_base = -1 << 30;
+    __device__ __forceinline__ int fetch(const KArgs& a, int base, int lane) const {
+        const int kb = base + lane;
+        return (kb >= 0 && kb < a.num_kb) ? __ldg(a.kb_run + kb) : -1;
+    }
+    // run of k-block kb (warp-uniform); next_start = first k-block of the following tile (prefetch target)
+    __device__ __forceinline__ int get(const KArgs& a, int kb, int kb_end, int next_start, int lane) {
+        if (kb < cur_base || kb >= cur_base + 32) {
+            const int base = kb & ~31;
+            if (base == nxt_base) {
+                cur = nxt;
+            } else {
+                cur = fetch(a, base, lane);
+            }
+            cur_base = base;
+            const int nb = (base + 32 < kb_end) ? base + 32 : (next_start & ~31);
+            nxt = fetch(a, nb, lane);
+            nxt_base = nb;
+        }
+        return __shfl_sync(0xffffffffu, cur, kb - cur_base);
+    }
+};
+
+__global__ void k_kb_runs(const int32_t* __restrict__ idx, int n, int num_kb, int32_t* __restrict__ out) {
+    const int kb = blockIdx.x * blockDim.x + threadIdx.x;
+    if (kb >= num_kb) return;
+    const int p = kb * BK;
+    out[kb] = (p + BK <= n && idx[p + BK - 1] - idx[p] == BK - 1) ? idx[p] : -1;
+}
+
+// K-major B (gathered along N): the tile's R = 32 * 4 * H rows, lane l holds rows h*128 + 4l + j.
+template <int H>
+__device__ __forceinline__ void load_nrows(const KArgs& a, int n0, int lane, int (&g)[4 * H]) {
+#pragma unroll
+    for (int j = 0; j < 4 * H; ++j) g[j] = gather_row(a, n0 + (j >> 2) * 128 + 4 * lane + (j & 3));
+}
+template <int H>
+__device__ __forceinline__ int nrows_run(const KArgs& a, const int (&g)[4 * H], int n0) {  // warp-uniform
+    const int first = __shfl_sync(0xffffffffu, g[0], 0), last = __shfl_sync(0xffffffffu, g[4 * H - 1], 31);
+    return (n0 + 128 * H <= a.b_idx_n && last - first == 128 * H - 1) ? first : -1;
+}
 
 __device__ __forceinline__ int base_tile_count(const KArgs& a) {
     return a.grouped ? a.g_tile_off[a.G] * a.g_ntiles : a.tiles_m * a.tiles_n;
@@ -182,7 +253,8 @@ __device__ __forceinline__ void epilogue_chunk(const KArgs& a, int m, int n, con
 
 template <bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-    k_gemm_bf16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const KArgs args) {
+    k_gemm_bf16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmG, const KArgs args) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -208,6 +280,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
+        tma_prefetch_desc(&tmG);
     }
     if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
     tc_fence_before();
@@ -219,37 +292,79 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int num_tiles = base_tiles * args.ksplit;
 
     if (warp == 0) {
-        // ------------------------------------------------ TMA producer
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-                const int sp = tile / base_tiles;
-                const TileInfo ti = resolve_tile(args, tile - sp * base_tiles);
-                const int m0 = ti.a_row0, n0 = ti.b_row0;
-                const int kb0 = sp * args.kb_split, kb1 = min(args.num_kb, kb0 + args.kb_split);
-                for (int kb = kb0; kb < kb1; ++kb) {
+        // ------------------------------------------------ TMA producer (lane 0; all lanes for gathered B rows)
+        const bool gather = args.b_idx != nullptr;
+        int stage = 0;
+        uint32_t phase = 0;
+        int gn[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // K-major gathered B: the NEXT tile's rows (prefetched)
+        RunBatch rb;                            // MN-major gathered B: k-block run table reader
+        auto tile_n0 = [&](int t) {
+            const int sp_ = t / base_tiles;
+            return resolve_tile(args, t - sp_ * base_tiles).b_row0;
+        };
+        if (gather && !B_MN && blockIdx.x < num_tiles) load_nrows<2>(args, tile_n0(blockIdx.x), lane, gn);
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            const int sp = tile / base_tiles;
+            const TileInfo ti = resolve_tile(args, tile - sp * base_tiles);
+            const int m0 = ti.a_row0, n0 = ti.b_row0;
+            const int kb0 = sp * args.kb_split, kb1 = min(args.num_kb, kb0 + args.kb_split);
+            const int next = tile + int(gridDim.x);
+            int gi[8];
+            int run = -1;
+            if (gather && !B_MN) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) gi[j] = gn[j];
+                run = nrows_run<2>(args, gi, n0);
+                if (next < num_tiles) load_nrows<2>(args, tile_n0(next), lane, gn);
+            }
+            for (int kb = kb0; kb < kb1; ++kb) {
+                uint8_t* sa = smem + stage * STAGE_BYTES;
+                uint8_t* sb = sa + A_BYTES;
+                const int k0 = kb * BK;
+                if (gather && B_MN)
+                    run = rb.get(args, kb, kb1, next < num_tiles ? (next / base_tiles) * args.kb_split : 0, lane);
+                if (lane == 0) {
                     mbar_wait(empty + stage, phase ^ 1);
-                    uint8_t* sa = smem + stage * STAGE_BYTES;
-                    uint8_t* sb = sa + A_BYTES;
                     mbar_arrive_expect_tx(full + stage, STAGE_BYTES);
-                    const int k0 = kb * BK;
                     if (!A_MN) {
                         tma_load_2d(sa, &tmA, full + stage, k0, m0);
                     } else {
 #pragma unroll
-                        for (int j = 0; j < BM / 64; ++j) tma_load_2d(sa + j * 8192, &tmA, full + stage, m0 + 64 * j, k0);
+                        for (int j = 0; j < BM / 64; ++j)
+                            tma_load_2d(sa + j * 8192, &tmA, full + stage, m0 + 64 * j, k0);
                     }
-                    if (!B_MN) {
-                        tma_load_2d(sb, &tmB, full + stage, k0, n0);
-                    } else {
+                    if (!gather || run >= 0) {  // plain box (gathered B: at the run's table row)
+                        const int brow = gather ? run : (B_MN ? k0 : n0);
+                        if (!B_MN) {
+                            tma_load_2d(sb, &tmB, full + stage, k0, brow);
+                        } else {
 #pragma unroll
-                        for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 8192, &tmB, full + stage, n0 + 64 * j, k0);
+                            for (int j = 0; j < BN / 64; ++j)
+                                tma_load_2d(sb + j * 8192, &tmB, full + stage, n0 + 64 * j, brow);
+                        }
                     }
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
+                }
+                if (gather && run < 0) {
+                    __syncwarp();  // the stage is free (lane 0 waited on it)
+                    if (!B_MN) {   // 256 B rows x 64 k: lane owns rows 4l..4l+3 and 128+4l..
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+                            tma_gather4(sb + (h * 128 + 4 * lane) * 128, &tmG, full + stage, k0, gi[4 * h],
+                                        gi[4 * h + 1], gi[4 * h + 2], gi[4 * h + 3]);
+                    } else {  // 4 chunks of 64 n x 64 k-rows: lane owns k-rows 4(l%16).. of chunks l/16, l/16+2
+                        const int r = (lane & 15) * 4;
+                        int i0, i1, i2, i3;
+                        krows_four(load_krows(args, k0, lane), r, i0, i1, i2, i3);  // broken k-block: rare
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int ch = (lane >> 4) + 2 * h;
+                            tma_gather4(sb + ch * 8192 + r * 128, &tmG, full + stage, n0 + 64 * ch, i0, i1, i2, i3);
+                        }
                     }
+                }
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
                 }
             }
         }
@@ -360,7 +475,7 @@ __device__ __forceinline__ void tile_coords_pair(int tile, const KArgs& args, in
 template <bool A_MN, bool B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     k_gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const KArgs args) {
+                     const __grid_constant__ CUtensorMap tmG, const KArgs args) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + P_STAGES * P_STAGE_BYTES);
@@ -389,6 +504,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
+        tma_prefetch_desc(&tmG);
     }
     if (warp == 1) tmem_alloc_pair(tmem_slot, TMEM_COLS);
     tc_fence_before();
@@ -398,37 +514,72 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     const int num_tiles = args.tiles_m * args.tiles_n;
 
     if (warp == 0) {
-        // ------------------------------------------------ TMA producer (both CTAs)
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int tile = pair; tile < num_tiles; tile += npairs) {
-                int mb, nb;
-                tile_coords_pair(tile, args, mb, nb);
-                const int m0 = mb * P_TILE_M + int(rank) * 128;  // this CTA's A rows
-                const int n0 = nb * BN + int(rank) * 128;        // this CTA's half of the B rows
-                for (int kb = 0; kb < args.num_kb; ++kb) {
+        // ------------------------------------------------ TMA producer (both CTAs; all lanes for gathered B rows)
+        const bool gather = args.b_idx != nullptr;
+        int stage = 0;
+        uint32_t phase = 0;
+        int gn[4] = {0, 0, 0, 0};  // K-major gathered B: the NEXT tile's rows of this CTA's half (prefetched)
+        RunBatch rb;               // MN-major gathered B: k-block run table reader
+        auto tile_n0 = [&](int t) {
+            int mb_, nb_;
+            tile_coords_pair(t, args, mb_, nb_);
+            return nb_ * BN + int(rank) * 128;
+        };
+        if (gather && !B_MN && pair < num_tiles) load_nrows<1>(args, tile_n0(pair), lane, gn);
+        for (int tile = pair; tile < num_tiles; tile += npairs) {
+            int mb, nb;
+            tile_coords_pair(tile, args, mb, nb);
+            const int m0 = mb * P_TILE_M + int(rank) * 128;  // this CTA's A rows
+            const int n0 = nb * BN + int(rank) * 128;        // this CTA's half of the B rows
+            const int next = tile + npairs;
+            int gi[4];
+            int run = -1;
+            if (gather && !B_MN) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) gi[j] = gn[j];
+                run = nrows_run<1>(args, gi, n0);
+                if (next < num_tiles) load_nrows<1>(args, tile_n0(next), lane, gn);
+            }
+            for (int kb = 0; kb < args.num_kb; ++kb) {
+                uint8_t* sa = smem + stage * P_STAGE_BYTES;
+                uint8_t* sb = sa + P_A_BYTES;
+                const int k0 = kb * BK;
+                if (gather && B_MN) run = rb.get(args, kb, args.num_kb, 0, lane);
+                if (lane == 0) {
                     mbar_wait(empty + stage, phase ^ 1);
-                    uint8_t* sa = smem + stage * P_STAGE_BYTES;
-                    uint8_t* sb = sa + P_A_BYTES;
                     if (leader) mbar_arrive_expect_tx(full + stage, 2 * P_STAGE_BYTES);
-                    const int k0 = kb * BK;
                     if (!A_MN) {
                         tma_load_2d_pair(sa, &tmA, full + stage, k0, m0);
                     } else {
 #pragma unroll
-                        for (int j = 0; j < 2; ++j) tma_load_2d_pair(sa + j * 8192, &tmA, full + stage, m0 + 64 * j, k0);
+                        for (int j = 0; j < 2; ++j)
+                            tma_load_2d_pair(sa + j * 8192, &tmA, full + stage, m0 + 64 * j, k0);
                     }
-                    if (!B_MN) {
-                        tma_load_2d_pair(sb, &tmB, full + stage, k0, n0);
-                    } else {
+                    if (!gather || run >= 0) {  // plain box (gathered B: at the run's table row)
+                        const int brow = gather ? run : (B_MN ? k0 : n0);
+                        if (!B_MN) {
+                            tma_load_2d_pair(sb, &tmB, full + stage, k0, brow);
+                        } else {
 #pragma unroll
-                        for (int j = 0; j < 2; ++j) tma_load_2d_pair(sb + j * 8192, &tmB, full + stage, n0 + 64 * j, k0);
+                            for (int j = 0; j < 2; ++j)
+                                tma_load_2d_pair(sb + j * 8192, &tmB, full + stage, n0 + 64 * j, brow);
+                        }
                     }
-                    if (++stage == P_STAGES) {
-                        stage = 0;
-                        phase ^= 1;
+                }
+                if (gather && run < 0) {
+                    __syncwarp();  // the stage is free (lane 0 waited on it)
+                    if (!B_MN) {   // 128 B rows x 64 k: lane owns rows 4l..4l+3
+                        tma_gather4_pair(sb + 4 * lane * 128, &tmG, full + stage, k0, gi[0], gi[1], gi[2], gi[3]);
+                    } else {  // 2 chunks of 64 n x 64 k-rows: lane owns k-rows 4(l%16).. of chunk l/16
+                        const int r = (lane & 15) * 4, ch = lane >> 4;
+                        int i0, i1, i2, i3;
+                        krows_four(load_krows(args, k0, lane), r, i0, i1, i2, i3);  // broken k-block: rare
+                        tma_gather4_pair(sb + ch * 8192 + r * 128, &tmG, full + stage, n0 + 64 * ch, i0, i1, i2, i3);
                     }
+                }
+                if (++stage == P_STAGES) {
+                    stage = 0;
+                    phase ^= 1;
                 }
             }
         }
@@ -531,7 +682,8 @@ CUtensorMap make_map(const void* base, int64_t inner, int64_t outer, int64_t ld,
 }
 
 template <bool A_MN, bool B_MN>
-void launch(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const KArgs& args, int tiles_bound) {
+void launch(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tg, const KArgs& args,
+            int tiles_bound) {
     static bool attr_set = false;
     if (!attr_set) {
         MEFT_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_bf16<A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -539,7 +691,7 @@ void launch(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const
         attr_set = true;
     }
     const int grid = std::max(1, std::min(tiles_bound, num_sms()));
-    k_gemm_bf16<A_MN, B_MN><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ta, tb, args);
+    k_gemm_bf16<A_MN, B_MN><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ta, tb, tg, args);
     check_launch("k_gemm_bf16");
 }
 
@@ -571,6 +723,10 @@ KArgs base_args(int64_t M, int64_t N, int64_t K, const GemmEpilogue& epi) {
     args.ldm = epi.ldm;
     args.row_idx = epi.row_idx;
     args.grouped = 0;
+    args.b_idx = nullptr;
+    args.kb_run = nullptr;
+    args.b_idx_n = 0;
+    args.b_oob_row = 0;
     args.ksplit = 1;
     args.kb_split = args.num_kb;
     args.split_stride = 0;
@@ -584,20 +740,22 @@ KArgs base_args(int64_t M, int64_t N, int64_t K, const GemmEpilogue& epi) {
     return args;
 }
 
-void dispatch(cudaStream_t st, bool a_mn, bool b_mn, const CUtensorMap& ta, const CUtensorMap& tb, const KArgs& args,
+void dispatch(cudaStream_t st, bool a_mn, bool b_mn, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tg,
+              const KArgs& args,
               int tiles_bound) {
     if (!a_mn && !b_mn)
-        launch<false, false>(st, ta, tb, args, tiles_bound);
+        launch<false, false>(st, ta, tb, tg, args, tiles_bound);
     else if (!a_mn && b_mn)
-        launch<false, true>(st, ta, tb, args, tiles_bound);
+        launch<false, true>(st, ta, tb, tg, args, tiles_bound);
     else if (a_mn && b_mn)
-        launch<true, true>(st, ta, tb, args, tiles_bound);
+        launch<true, true>(st, ta, tb, tg, args, tiles_bound);
     else
-        launch<true, false>(st, ta, tb, args, tiles_bound);
+        launch<true, false>(st, ta, tb, tg, args, tiles_bound);
 }
 
 template <bool A_MN, bool B_MN>
-void launch_pair(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const KArgs& args, int pair_tiles) {
+void launch_pair(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tg, const KArgs& args,
+                 int pair_tiles) {
     static bool attr_set = false;
     if (!attr_set) {
         MEFT_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_bf16_pair<A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -605,20 +763,21 @@ void launch_pair(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, 
         attr_set = true;
     }
     const int pairs = std::max(1, std::min(pair_tiles, num_sms() / 2));
-    k_gemm_bf16_pair<A_MN, B_MN><<<2 * pairs, NUM_THREADS, P_SMEM_BYTES, st>>>(ta, tb, args);
+    k_gemm_bf16_pair<A_MN, B_MN><<<2 * pairs, NUM_THREADS, P_SMEM_BYTES, st>>>(ta, tb, tg, args);
     check_launch("k_gemm_bf16_pair");
 }
 
 void launch_pair_dispatch(cudaStream_t st, bool a_mn, bool b_mn, const CUtensorMap& ta, const CUtensorMap& tb,
+                          const CUtensorMap& tg,
                           const KArgs& args, int pair_tiles) {
     if (!a_mn && !b_mn)
-        launch_pair<false, false>(st, ta, tb, args, pair_tiles);
+        launch_pair<false, false>(st, ta, tb, tg, args, pair_tiles);
     else if (!a_mn && b_mn)
-        launch_pair<false, true>(st, ta, tb, args, pair_tiles);
+        launch_pair<false, true>(st, ta, tb, tg, args, pair_tiles);
     else if (a_mn && b_mn)
-        launch_pair<true, true>(st, ta, tb, args, pair_tiles);
+        launch_pair<true, true>(st, ta, tb, tg, args, pair_tiles);
     else
-        launch_pair<true, false>(st, ta, tb, args, pair_tiles);
+        launch_pair<true, false>(st, ta, tb, tg, args, pair_tiles);
 }
 
 // MEFT_GEMM_PAIR=0 forces the 1-CTA kernel (A/B comparisons in tools/gemm_check).
@@ -642,10 +801,25 @@ void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOpera
     check_epilogue(epi);
     KArgs args = base_args(M, N, K, epi);
     const CUtensorMap ta = A.mn_major ? make_map(A.ptr, M, K, A.ld, 64, 64) : make_map(A.ptr, K, M, A.ld, 64, BM);
+    CUtensorMap tg;
+    if (B.rows) {  // gathered B rows: a {64 x 1} box over the whole table, rows fetched by tile::gather4
+        if (B.table_rows <= 0 || B.table_rows >= INT32_MAX) throw MeftError(2, "gemm_bf16: gather table rows");
+        tg = make_map(B.ptr, B.mn_major ? N : K, B.table_rows, B.ld, 64, 1);
+        args.b_idx = B.rows;
+        args.b_idx_n = int(B.mn_major ? K : N);
+        args.b_oob_row = int(B.table_rows);
+        if (B.mn_major) {
+            if (!B.run_ws) throw MeftError(2, "gemm_bf16: MN-major gathered B needs run_ws");
+            k_kb_runs<<<int((args.num_kb + 255) / 256), 256, 0, st>>>(B.rows, args.b_idx_n, args.num_kb, B.run_ws);
+            check_launch("k_kb_runs");
+            args.kb_run = B.run_ws;
+        }
+    }
     // large problems: 256x256 tiles on CTA pairs (enough pair-tiles to fill the machine at least once)
     const int64_t pair_tiles = ceil_div(M, P_TILE_M) * ceil_div(N, BN);
     if (pair_tiles >= num_sms() / 2 && pair_mode_enabled() && args.ksplit == 1) {
-        const CUtensorMap tb = B.mn_major ? make_map(B.ptr, N, K, B.ld, 64, 64) : make_map(B.ptr, K, N, B.ld, 64, 128);
+        const CUtensorMap tb = B.mn_major ? make_map(B.ptr, N, B.rows ? B.table_rows : K, B.ld, 64, 64)
+                                          : make_map(B.ptr, K, B.rows ? B.table_rows : N, B.ld, 64, 128);
         args.tiles_m = int(ceil_div(M, P_TILE_M));
         // G pair-tiles of M share each streamed B panel.  Measured (ncu dram bytes + time, tools/gemm_check):
         // K-major x K-major (z, dA: K = d) likes 16 (dA 3.31 -> 3.08 ms); the long-K / MN-major GEMMs 8.
@@ -655,11 +829,12 @@ void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOpera
             return v ? std::max(1, std::atoi(v)) : 0;
         }();
         args.raster_group = forced ? forced : (!A.mn_major && !B.mn_major ? 16 : 8);
-        launch_pair_dispatch(st, A.mn_major, B.mn_major, ta, tb, args, int(pair_tiles));
+        launch_pair_dispatch(st, A.mn_major, B.mn_major, ta, tb, B.rows ? tg : tb, args, int(pair_tiles));
         return;
     }
-    const CUtensorMap tb = B.mn_major ? make_map(B.ptr, N, K, B.ld, 64, 64) : make_map(B.ptr, K, N, B.ld, 64, BN);
-    dispatch(st, A.mn_major, B.mn_major, ta, tb, args, args.tiles_m * args.tiles_n * args.ksplit);
+    const CUtensorMap tb = B.mn_major ? make_map(B.ptr, N, B.rows ? B.table_rows : K, B.ld, 64, 64)
+                                      : make_map(B.ptr, K, B.rows ? B.table_rows : N, B.ld, 64, BN);
+    dispatch(st, A.mn_major, B.mn_major, ta, tb, B.rows ? tg : tb, args, args.tiles_m * args.tiles_n * args.ksplit);
 }
 
 void gemm_bf16_grouped(cudaStream_t st, int G, int64_t N, int64_t K, const GemmOperand& A, int64_t a_rows,
@@ -667,6 +842,7 @@ void gemm_bf16_grouped(cudaStream_t st, int G, int64_t N, int64_t K, const GemmO
                        const GemmEpilogue& epi) {
     if (G <= 0 || N <= 0 || a_rows <= 0) return;
     if (A.mn_major || B.mn_major) throw MeftError(2, "gemm_bf16_grouped: K-major operands only");
+    if (B.rows) throw MeftError(2, "gemm_bf16_grouped: gathered B is not supported");
     if (!aligned16(A.ptr) || !aligned16(B.ptr) || (A.ld % 8) || (B.ld % 8))
         throw MeftError(2, "gemm_bf16_grouped: operand alignment");
     check_epilogue(epi);
@@ -680,7 +856,7 @@ void gemm_bf16_grouped(cudaStream_t st, int G, int64_t N, int64_t K, const GemmO
     args.g_row_off = row_off;
     args.g_tile_off = tile_off;
     const int64_t bound = (ceil_div(a_rows, BM) + G) * args.g_ntiles * args.ksplit;  // >= device tile count
-    dispatch(st, false, false, ta, tb, args, int(std::min<int64_t>(bound, INT32_MAX)));
+    dispatch(st, false, false, ta, tb, tb, args, int(std::min<int64_t>(bound, INT32_MAX)));
 }
 
 }  // namespace meft_dev

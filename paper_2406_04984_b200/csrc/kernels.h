@@ -14,6 +14,11 @@ struct GemmOperand {
     const void* ptr;
     int64_t ld;     // elements
     bool mn_major;
+    // B only: row gather. Row p of the logical B (p < N when K-major, p < K when MN-major) is row rows[p] of the
+    // table at ptr ([table_rows x ld]); loaded with TMA tile::gather4 straight into the operand tile.
+    const int32_t* rows = nullptr;
+    int64_t table_rows = 0;
+    int32_t* run_ws = nullptr;  // MN-major gathered B: scratch of ceil(K / 64) ints (per-k-block run table)
 };
 
 enum GemmEpi : int {

@@ -39,6 +39,7 @@ struct meft_ctx {
     std::unordered_map<std::string, Buf> scratch;
 
     int selection_mode = MEFT_SELECT_AUTO;
+    int gather_mode = -1;  // MEFT_GATHER_*; -1 = not set (environment MEFT_GATHER, else AUTO)
 
     // phase timing (meft_ctx_set_timing)
     bool timing = false;
@@ -218,8 +219,27 @@ int64_t selection_take(int64_t M, int64_t N, int64_t kk, int64_t k, int64_t* kk_
 
 // ---- FFN building blocks (adapter.cpp:122-126, 166-175)
 
+// Selected key/value rows either materialised ([s x d], rows == nullptr) or gathered by the GEMMs themselves:
+// keys_s/values_s are then the whole [table_rows x d] compute tables and rows[0..s) the selected row ids
+// (TMA tile::gather4 / contiguous-run boxes into the operand tiles; the fetch kernel disappears).
+struct RowGather {
+    const int32_t* rows = nullptr;
+    int64_t table_rows = 0;
+};
+
+GemmOperand kv_operand(meft_ctx* ctx, const void* p, int64_t d, bool mn_major, const RowGather& rg, int64_t s) {
+    GemmOperand op{p, d, mn_major};
+    if (rg.rows) {
+        op.rows = rg.rows;
+        op.table_rows = rg.table_rows;
+        if (mn_major) op.run_ws = static_cast<int32_t*>(ctx->get("kb_run", size_t(s / 64 + 2) * 4));
+    }
+    return op;
+}
+
 void ffn_forward_impl(meft_ctx* ctx, meft_dtype dt, const void* h, const void* keys_s, const void* values_s,
-                      int64_t T, int64_t d, int64_t s, int64_t ld_z, void* z, void* out, bool accumulate) {
+                      int64_t T, int64_t d, int64_t s, int64_t ld_z, void* z, void* out, bool accumulate,
+                      const RowGather& rg = RowGather()) {
     cudaStream_t st = ctx->stream;
     if (dt == MEFT_F64) {
         double* outd = static_cast<double*>(out);
@@ -246,20 +266,20 @@ void ffn_forward_impl(meft_ctx* ctx, meft_dtype dt, const void* h, const void* k
     e1.kind = EPI_RELU_BF16;
     e1.c = z;
     e1.ldc = ld_z;
-    gemm_bf16(st, T, s, d, GemmOperand{h, d, false}, GemmOperand{keys_s, d, false}, e1);
+    gemm_bf16(st, T, s, d, GemmOperand{h, d, false}, kv_operand(ctx, keys_s, d, false, rg, s), e1);
     GemmEpilogue e2;
     e2.kind = EPI_STORE_F32;
     e2.c = out;
     e2.ldc = d;
     e2.accumulate = accumulate;
-    gemm_bf16(st, T, d, s, GemmOperand{z, ld_z, false}, GemmOperand{values_s, d, true}, e2);
+    gemm_bf16(st, T, d, s, GemmOperand{z, ld_z, false}, kv_operand(ctx, values_s, d, true, rg, s), e2);
 }
 
 // stage_keys/stage_values non-null => weight grads are row-added into the store staging at S (fused scatter).
 void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* h, const void* z, const void* keys_s,
                        const void* values_s, int64_t T, int64_t d, int64_t s, int64_t ld_z, void* masked,
                        void* grad_keys_s, void* grad_values_s, void* grad_h, bool acc_h, const int32_t* S_rows,
-                       void* stage_keys, void* stage_values) {
+                       void* stage_keys, void* stage_values, const RowGather& rg = RowGather()) {
     cudaStream_t st = ctx->stream;
     if (dt == MEFT_F64) {
         const double* gd = static_cast<const double*>(g);
@@ -301,7 +321,7 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
     e3.ldc = ld_z;
     e3.mask = z;
     e3.ldm = ld_z;
-    gemm_bf16(st, T, s, d, GemmOperand{g, d, false}, GemmOperand{values_s, d, false}, e3);
+    gemm_bf16(st, T, s, d, GemmOperand{g, d, false}, kv_operand(ctx, values_s, d, false, rg, s), e3);
     GemmEpilogue e4;  // grad_values = act^T G   (M = s, N = d, K = T)
     if (S_rows) {
         e4.kind = EPI_ROWS_ADD_F32;
@@ -322,7 +342,7 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
         e6.c = grad_h;
         e6.ldc = d;
         e6.accumulate = acc_h;
-        gemm_bf16(st, T, d, s, GemmOperand{masked, ld_z, false}, GemmOperand{keys_s, d, true}, e6);
+        gemm_bf16(st, T, d, s, GemmOperand{masked, ld_z, false}, kv_operand(ctx, keys_s, d, true, rg, s), e6);
     }
 }
 
@@ -547,6 +567,15 @@ meft_status meft_ctx_set_selection(meft_ctx* ctx, int mode) {
         require_ctx(ctx);
         require(mode == MEFT_SELECT_AUTO || mode == MEFT_SELECT_EXACT, MEFT_E_INVALID, "unknown selection mode");
         ctx->selection_mode = mode;
+    });
+}
+
+meft_status meft_ctx_set_gather(meft_ctx* ctx, int mode) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(mode == MEFT_GATHER_AUTO || mode == MEFT_GATHER_KERNEL || mode == MEFT_GATHER_TMA, MEFT_E_INVALID,
+                "unknown gather mode");
+        ctx->gather_mode = mode;
     });
 }
 
@@ -1012,8 +1041,8 @@ meft_status meft_sparse_adam_update(meft_ctx* ctx, meft_store* s, int64_t layer,
 // ------------------------------------------------------------------ fused layer step
 
 static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const void* h, const void* g, int64_t T,
-                            const int32_t* uni, int64_t su, double b1, double b2, double eps, double lr, float* out,
-                            float* grad_h, cudaEvent_t g_ready, cudaEvent_t fwd_done);
+                            const int32_t* uni, int64_t su, int64_t holes, double b1, double b2, double eps,
+                            double lr, float* out, float* grad_h, cudaEvent_t g_ready, cudaEvent_t fwd_done);
 
 static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const void* h, const void* g, int64_t T,
                             int64_t kk, int64_t k, double b1, double b2, double eps, double lr, float* out,
@@ -1042,10 +1071,12 @@ static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
         ke_select_device(st, 2, h, L.c_g, L.c_a, T, d, M, N, kk_eff, take, ws, wsb, per_token, nullptr, uni, usize,
                          ctx->dev_small + 5, ctx->selection_mode == MEFT_SELECT_AUTO);
     }
-    MEFT_CUDA_CHECK(cudaMemcpyAsync(ctx->host_small + 4, usize, 12, cudaMemcpyDeviceToHost, st));
+    union_holes(st, uni, usize, usize + 3);
+    MEFT_CUDA_CHECK(cudaMemcpyAsync(ctx->host_small + 4, usize, 16, cudaMemcpyDeviceToHost, st));
     MEFT_CUDA_CHECK(cudaStreamSynchronize(st));
     const int64_t su = ctx->host_small[4];
-    ffn_update_impl(ctx, s, layer, h, g, T, uni, su, b1, b2, eps, lr, out, grad_h, g_ready, fwd_done);
+    ffn_update_impl(ctx, s, layer, h, g, T, uni, su, ctx->host_small[7], b1, b2, eps, lr, out, grad_h, g_ready,
+                    fwd_done);
 
     if (info) {
         info->union_size = su;
@@ -1060,30 +1091,64 @@ static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
 
 // fetch -> sparse_ffn_pa -> sparse_backward -> scatter_grads -> sparse_adam_update for T tokens against the union S
 // (uni: ascending store-local pair ids, su of them), on a MIXED store.
+// How the FFN GEMMs get the selected key/value rows (meft_ctx_set_gather; default from MEFT_GATHER=kernel|tma).
+// TMA lets the GEMM producers fetch them (contiguous runs as plain boxes, the rest by tile::gather4) -- bitwise
+// the same operand tiles as the materialised copy; AUTO picks it when the union is nearly one run (a broken
+// 128-row piece costs ~4x its TMA issue), i.e. at most one hole per 12800 selected rows.
+static bool use_tma_gather(const meft_ctx* ctx, int64_t su, int64_t holes) {
+    static const int env_mode = [] {
+        const char* v = std::getenv("MEFT_GATHER");
+        if (!v) return int(MEFT_GATHER_AUTO);
+        return std::strcmp(v, "kernel") == 0 ? int(MEFT_GATHER_KERNEL)
+                                             : std::strcmp(v, "tma") == 0 ? int(MEFT_GATHER_TMA) : int(MEFT_GATHER_AUTO);
+    }();
+    const int mode = ctx->gather_mode >= 0 ? ctx->gather_mode : env_mode;
+    if (mode == MEFT_GATHER_KERNEL || su <= 0) return false;
+    if (mode == MEFT_GATHER_TMA) return true;
+    return holes >= 0 && holes * 12800 <= su;
+}
+
 static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const void* h, const void* g, int64_t T,
-                            const int32_t* uni, int64_t su, double b1, double b2, double eps, double lr, float* out,
-                            float* grad_h, cudaEvent_t g_ready, cudaEvent_t fwd_done) {
+                            const int32_t* uni, int64_t su, int64_t holes, double b1, double b2, double eps,
+                            double lr, float* out, float* grad_h, cudaEvent_t g_ready, cudaEvent_t fwd_done) {
     const LayerBufs& L = layer_of(s, layer);
     const int64_t d = s->d;
     cudaStream_t st = ctx->stream;
     const int64_t ld = round_up(std::max<int64_t>(su, 1), 64);
+    if (holes < 0 && su > 0 && use_tma_gather(ctx, su, 0)) {  // caller does not know: measure (one read-back)
+        union_holes_n(st, uni, su, ctx->dev_small + 12);
+        MEFT_CUDA_CHECK(cudaMemcpyAsync(ctx->host_small + 12, ctx->dev_small + 12, 4, cudaMemcpyDeviceToHost, st));
+        MEFT_CUDA_CHECK(cudaStreamSynchronize(st));
+        holes = ctx->host_small[12];
+    }
 
-    // fetch (memtier.cpp:117-126): gather the selected key/value rows of the bf16 compute tables
-    uint16_t* ks = static_cast<uint16_t*>(ctx->get("keys_s", size_t(std::max<int64_t>(su, 1) * d) * 2));
-    uint16_t* vs = static_cast<uint16_t*>(ctx->get("values_s", size_t(std::max<int64_t>(su, 1) * d) * 2));
     uint16_t* act = static_cast<uint16_t*>(ctx->get("act", size_t(T * ld) * 2));
     uint16_t* masked = static_cast<uint16_t*>(ctx->get("masked", size_t(T * ld) * 2));
     float* outb = out ? out : static_cast<float*>(ctx->get("out", size_t(T * d) * 4));
     float* ghb = grad_h ? grad_h : static_cast<float*>(ctx->get("grad_h", size_t(T * d) * 4));
-    if (su > 0) {
-        PhaseScope ps(ctx, 1);
-        gather_rows2(st, L.c_a, L.c_b, d * 2, uni, nullptr, su, ks, vs);
+    // fetch (memtier.cpp:117-126): the selected key/value rows of the bf16 compute tables, either gathered inside
+    // the GEMM operand loads (rg) or materialised by the gather kernel
+    RowGather rg;
+    const void* ks = L.c_a;
+    const void* vs = L.c_b;
+    if (use_tma_gather(ctx, su, holes)) {
+        rg.rows = uni;
+        rg.table_rows = s->pairs;
+    } else {
+        uint16_t* ksb = static_cast<uint16_t*>(ctx->get("keys_s", size_t(std::max<int64_t>(su, 1) * d) * 2));
+        uint16_t* vsb = static_cast<uint16_t*>(ctx->get("values_s", size_t(std::max<int64_t>(su, 1) * d) * 2));
+        if (su > 0) {
+            PhaseScope ps(ctx, 1);
+            gather_rows2(st, L.c_a, L.c_b, d * 2, uni, nullptr, su, ksb, vsb);
+        }
+        ks = ksb;
+        vs = vsb;
     }
 
     // sparse_ffn_pa adapter term (adapter.cpp:122-126), every token against the whole union
     {
         PhaseScope ps(ctx, 2);
-        ffn_forward_impl(ctx, MEFT_BF16, h, ks, vs, T, d, su, ld, act, outb, false);
+        ffn_forward_impl(ctx, MEFT_BF16, h, ks, vs, T, d, su, ld, act, outb, false, rg);
     }
     if (fwd_done) MEFT_CUDA_CHECK(cudaEventRecord(fwd_done, st));
     if (g_ready) MEFT_CUDA_CHECK(cudaStreamWaitEvent(st, g_ready, 0));
@@ -1095,7 +1160,7 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
         {
             PhaseScope ps(ctx, 3);
             ffn_backward_impl(ctx, MEFT_BF16, g, h, act, ks, vs, T, d, su, ld, masked, nullptr, nullptr, ghb, false,
-                              uni, L.st_a, L.st_b);
+                              uni, L.st_a, L.st_b, rg);
         }
         PhaseScope ps(ctx, 4);
         if (su > 0) mark_rows(st, L.staged, uni, nullptr, su);
@@ -1108,7 +1173,7 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
         {
             PhaseScope ps(ctx, 3);
             ffn_backward_impl(ctx, MEFT_BF16, g, h, act, ks, vs, T, d, su, ld, masked, gka, gvb, ghb, false, nullptr,
-                              nullptr, nullptr);
+                              nullptr, nullptr, rg);
         }
         PhaseScope ps(ctx, 4);
         if (su > 0)
@@ -1215,7 +1280,7 @@ meft_status meft_layer_ffn_local(meft_ctx* ctx, meft_store* s, int64_t layer, co
         require_ctx(ctx);
         layer_of(s, layer);
         require(s->prec == MEFT_STORE_MIXED && s->d % 8 == 0, MEFT_E_INVALID, "layer_ffn_local: MIXED store, d % 8");
-        ffn_update_impl(ctx, s, layer, h_all, g_all, T, S_local, su, beta1, beta2, eps, lr, out_partial,
+        ffn_update_impl(ctx, s, layer, h_all, g_all, T, S_local, su, -1, beta1, beta2, eps, lr, out_partial,
                         grad_h_partial, nullptr, nullptr);
     });
 }

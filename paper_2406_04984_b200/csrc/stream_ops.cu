@@ -305,6 +305,27 @@ void stage_add(cudaStream_t st, int stage_dtype, void* stage, int64_t d, const i
     check_launch("k_stage_add");
 }
 
+// holes of an ascending index list: (last - first + 1) - n, i.e. how far it is from one contiguous run
+__global__ void k_union_holes(const int32_t* __restrict__ idx, const int32_t* __restrict__ n_dev,
+                              int32_t* __restrict__ out) {
+    const int n = *n_dev;
+    *out = n > 0 ? idx[n - 1] - idx[0] + 1 - n : 0;
+}
+
+__global__ void k_union_holes_n(const int32_t* __restrict__ idx, int n, int32_t* __restrict__ out) {
+    *out = n > 0 ? idx[n - 1] - idx[0] + 1 - n : 0;
+}
+
+void union_holes(cudaStream_t st, const int32_t* idx, const int32_t* n_dev, int32_t* out) {
+    k_union_holes<<<1, 1, 0, st>>>(idx, n_dev, out);
+    check_launch("k_union_holes");
+}
+
+void union_holes_n(cudaStream_t st, const int32_t* idx, int64_t n, int32_t* out) {
+    k_union_holes_n<<<1, 1, 0, st>>>(idx, int(n), out);
+    check_launch("k_union_holes");
+}
+
 void mark_rows(cudaStream_t st, uint8_t* staged, const int32_t* idx, const int32_t* count_dev, int64_t count) {
     const int grid = grid_for(count > 0 ? count : 1);
     k_mark<<<grid, 256, 0, st>>>(staged, idx, count_dev, int(count));

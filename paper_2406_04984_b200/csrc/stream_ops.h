@@ -11,6 +11,8 @@ void check_sorted_unique(cudaStream_t st, const int32_t* idx, int64_t n, int64_t
 void stage_add(cudaStream_t st, int stage_dtype, void* stage, int64_t d, const int32_t* idx, int64_t n, int g_dtype,
                const void* g, uint8_t* staged);
 void mark_rows(cudaStream_t st, uint8_t* staged, const int32_t* idx, const int32_t* count_dev, int64_t count);
+void union_holes(cudaStream_t st, const int32_t* idx, const int32_t* n_dev, int32_t* out);
+void union_holes_n(cudaStream_t st, const int32_t* idx, int64_t n, int32_t* out);
 void adam_mixed(cudaStream_t st, const int32_t* rows, const int32_t* count_dev, int64_t count, int64_t d, float* wa,
                 float* ma, float* va, float* sa, uint16_t* ca, float* wb, float* mb, float* vb, float* sb,
                 uint16_t* cb, int32_t* step, uint8_t* staged, double b1, double b2, double eps, double lr,

@@ -80,6 +80,10 @@ class Context:
         """exact=True forces fp64 SIMT scoring of every candidate (cross-validation of the certified path)."""
         self.check(lib().meft_ctx_set_selection(self.h, 1 if exact else 0))
 
+    def set_gather(self, mode: str):
+        """How the fused step's GEMMs read the selected key/value rows: "auto", "kernel" or "tma"."""
+        self.check(lib().meft_ctx_set_gather(self.h, {"auto": 0, "kernel": 1, "tma": 2}[mode]))
+
     def set_timing(self, on: bool):
         self.check(lib().meft_ctx_set_timing(self.h, int(on)))
 

@@ -145,3 +145,24 @@ def test_layer_step_cfg2_properties(ctx):
     if len(untouched):
         ut = torch.from_numpy(untouched).cuda()
         assert torch.equal(st.tensor(0, "w_a_compute")[ut], keys_before[ut])
+
+
+@pytest.mark.parametrize("T", [128, 2048])  # sparse union (gather4 pieces) / dense union (contiguous-run boxes)
+def test_tma_gather_matches_gather_kernel_bitwise(ctx, T):
+    """The FFN GEMMs fetching the selected key/value rows themselves (TMA runs + tile::gather4) build the very
+    operand tiles the gather kernel materialises: two layer steps must agree bit for bit."""
+    w_a, w_g, w_b, h, gr = cfg1_inputs(T=T)
+    res = []
+    for mode in ("kernel", "tma"):
+        ctx.set_gather(mode)
+        st = make_store(ctx, w_a, w_g, w_b, 64)
+        o = torch.empty((T, 512), dtype=torch.float32, device="cuda")
+        gh = torch.empty_like(o)
+        for _ in range(2):
+            info = st.layer_step(0, bf16_dev(h), bf16_dev(gr), 4, 32, 1e-3, out=o, grad_h=gh)
+        torch.cuda.synchronize()
+        res.append({"out": o.cpu().numpy(), "grad_h": gh.cpu().numpy(), "w_a": st.download(0, "w_a"),
+                    "w_b": st.download(0, "w_b")})
+    ctx.set_gather("auto")
+    for n in res[0]:
+        np.testing.assert_array_equal(res[0][n], res[1][n], err_msg=n)

@@ -234,8 +234,120 @@ static int check_split(int M, int N, int K, int ks) {
     return ok ? 0 : 1;
 }
 
+// Gathered B (TMA tile::gather4): logical row p of B = table row idx[p]; compared with a materialised gather.
+static int check_gather(int M, int N, int K, bool bmn, int table_rows) {
+    const int64_t lda = (K + 7) / 8 * 8 + 8;
+    const int cols = bmn ? N : K, nidx = bmn ? K : N;
+    const int64_t ldt = (cols + 7) / 8 * 8 + 8;
+    uint16_t* A = alloc_fill((int64_t)M * lda, 11 + M, 1.0f);
+    uint16_t* tab = alloc_fill((int64_t)table_rows * ldt, 29 + N, 1.0f);
+    std::vector<int32_t> idx(nidx);
+    uint32_t x = 12345;
+    for (int p = 0; p < nidx; ++p) {  // ascending with random gaps, like a union
+        x = x * 1664525u + 1013904223u;
+        idx[p] = (p == 0 ? 0 : idx[p - 1] + 1) + int((x >> 24) % 3);
+    }
+    if (idx[nidx - 1] >= table_rows) { std::printf("gather: table too small\n"); return 1; }
+    int32_t* didx;
+    CK(cudaMalloc(&didx, nidx * 4));
+    CK(cudaMemcpy(didx, idx.data(), nidx * 4, cudaMemcpyHostToDevice));
+    // materialise logical B
+    std::vector<uint16_t> ht((size_t)table_rows * ldt), hb((size_t)nidx * ldt);
+    CK(cudaMemcpy(ht.data(), tab, ht.size() * 2, cudaMemcpyDeviceToHost));
+    for (int p = 0; p < nidx; ++p) std::memcpy(&hb[(size_t)p * ldt], &ht[(size_t)idx[p] * ldt], ldt * 2);
+    uint16_t* Bm;
+    CK(cudaMalloc(&Bm, hb.size() * 2));
+    CK(cudaMemcpy(Bm, hb.data(), hb.size() * 2, cudaMemcpyHostToDevice));
+    float* R;
+    CK(cudaMalloc(&R, (int64_t)M * N * 4));
+    k_ref<<<dim3((N + 127) / 128, M), 128>>>(M, N, K, A, lda, false, Bm, ldt, bmn, R);
+    CK(cudaGetLastError());
+    std::vector<float> ref((size_t)M * N), got((size_t)M * N);
+    CK(cudaMemcpy(ref.data(), R, ref.size() * 4, cudaMemcpyDeviceToHost));
+    float* C;
+    CK(cudaMalloc(&C, (int64_t)M * N * 4));
+    GemmEpilogue e;
+    e.kind = EPI_STORE_F32;
+    e.c = C;
+    e.ldc = N;
+    GemmOperand b{tab, ldt, bmn};
+    b.rows = didx;
+    b.table_rows = table_rows;
+    CK(cudaMalloc(&b.run_ws, (K / 64 + 2) * 4));
+    gemm_bf16(0, M, N, K, GemmOperand{A, lda, false}, b, e);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(got.data(), C, got.size() * 4, cudaMemcpyDeviceToHost));
+    double max_err = 0, max_ref = 0;
+    for (size_t i = 0; i < got.size(); ++i) {
+        max_err = std::fmax(max_err, std::fabs(double(got[i]) - ref[i]));
+        max_ref = std::fmax(max_ref, std::fabs(double(ref[i])));
+    }
+    const double rel = max_err / (max_ref > 0 ? max_ref : 1);
+    const bool ok = rel < 1e-4;
+    std::printf("gather M=%5d N=%5d K=%5d bmn=%d table=%d  max_rel_err=%.3e  %s\n", M, N, K, bmn, table_rows, rel,
+                ok ? "OK" : "FAIL");
+    cudaFree(A);
+    cudaFree(tab);
+    cudaFree(didx);
+    cudaFree(Bm);
+    cudaFree(R);
+    cudaFree(C);
+    return ok ? 0 : 1;
+}
+
+static void perf_gather(const char* name, int M, int N, int K, bool bmn, int epi, bool hole = true) {
+    const int cols = bmn ? N : K, nidx = bmn ? K : N, table = nidx + 1;
+    uint16_t* A = alloc_fill((int64_t)M * K, 3);
+    uint16_t* tab = alloc_fill((int64_t)table * cols, 4);
+    std::vector<int32_t> idx(nidx);
+    for (int p = 0; p < nidx; ++p) idx[p] = p + (hole && p >= nidx / 2);  // the union minus one row
+    int32_t* didx;
+    CK(cudaMalloc(&didx, nidx * 4));
+    CK(cudaMemcpy(didx, idx.data(), nidx * 4, cudaMemcpyHostToDevice));
+    void* C;
+    CK(cudaMalloc(&C, (int64_t)M * N * 4));
+    GemmEpilogue e;
+    e.kind = epi;
+    e.c = C;
+    e.ldc = N;
+    GemmOperand b{tab, cols, bmn};
+    b.rows = didx;
+    b.table_rows = table;
+    CK(cudaMalloc(&b.run_ws, (K / 64 + 2) * 4));
+    for (int i = 0; i < 2; ++i) gemm_bf16(0, M, N, K, GemmOperand{A, K, false}, b, e);
+    cudaEvent_t t0, t1;
+    cudaEventCreate(&t0);
+    cudaEventCreate(&t1);
+    const int reps = 5;
+    cudaEventRecord(t0);
+    for (int i = 0; i < reps; ++i) gemm_bf16(0, M, N, K, GemmOperand{A, K, false}, b, e);
+    cudaEventRecord(t1);
+    CK(cudaEventSynchronize(t1));
+    float ms;
+    cudaEventElapsedTime(&ms, t0, t1);
+    ms /= reps;
+    std::printf("perf %-28s M=%5d N=%6d K=%5d  %8.3f ms  %7.1f TFLOP/s\n", name, M, N, K, ms,
+                2.0 * M * N * K / (ms * 1e-3) / 1e12);
+    cudaFree(A);
+    cudaFree(tab);
+    cudaFree(didx);
+    cudaFree(C);
+}
+
 int main(int argc, char** argv) {
     const bool perf = argc > 1 && std::strcmp(argv[1], "perf") == 0;
+    if (argc > 1 && std::strcmp(argv[1], "perfg") == 0) {
+        const int T = 8192, S = 65536, D = 4096;
+        perf_case("z dense", T, S, D, false, false, EPI_RELU_BF16);
+        perf_gather("z gathered, no hole", T, S, D, false, EPI_RELU_BF16, false);
+        perf_gather("z gathered, one hole", T, S, D, false, EPI_RELU_BF16, true);
+        perf_case("z dense", T, S, D, false, false, EPI_RELU_BF16);
+        perf_case("out dense", T, D, S, false, true, EPI_STORE_F32);
+        perf_gather("out gathered, no hole", T, D, S, true, EPI_STORE_F32, false);
+        perf_gather("out gathered, one hole", T, D, S, true, EPI_STORE_F32, true);
+        perf_case("out dense", T, D, S, false, true, EPI_STORE_F32);
+        return 0;
+    }
     int fails = 0;
     if (!perf) {
         const int shapes[][3] = {{128, 256, 64}, {256, 512, 256}, {200, 300, 130}, {1000, 700, 520}, {64, 48, 40}};
@@ -254,6 +366,11 @@ int main(int argc, char** argv) {
             fails += check_case(2304, 2304, 256, false, false, epi);
             fails += check_case(2200, 2500, 130, true, true, epi);
         }
+        for (bool bmn : {false, true}) {
+            fails += check_gather(300, 260, 200, bmn, 1200);    // 1-CTA, ragged
+            fails += check_gather(2304, 2304, 320, bmn, 9000);  // CTA pair
+            fails += check_gather(2200, 2500, 136, bmn, 9000);  // CTA pair, ragged
+        }
         fails += check_split(300, 260, 1024, 8);
         fails += check_split(512, 256, 4096, 8);
         fails += check_split(200, 300, 650, 3);
@@ -265,5 +382,7 @@ int main(int argc, char** argv) {
     perf_case("out=act.values (K,MN)", T, D, S, false, true, EPI_STORE_F32);
     perf_case("dA=g.values^T mask (K,K)", T, S, D, false, false, EPI_MASK_BF16);
     perf_case("gW=act^T.g (MN,MN)", S, D, T, true, true, EPI_STORE_F32);
+    perf_gather("z gathered keys (K,K)", T, S, D, false, EPI_RELU_BF16);
+    perf_gather("out gathered values (K,MN)", T, D, S, true, EPI_STORE_F32);
     return 0;
 }
