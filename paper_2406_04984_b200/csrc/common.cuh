@@ -52,6 +52,12 @@ int num_sms();  // cached cudaDevAttrMultiProcessorCount of the current device
 
 __device__ __forceinline__ float bf16_bits_to_f32(uint16_t b) { return __uint_as_float(uint32_t(b) << 16); }
 
+// exponent of the least significant mantissa bit of a bf16 value (subnormals: 2^-133)
+__device__ __forceinline__ int bf16_lsb_exp(uint16_t b) {
+    const int e = (b >> 7) & 0xFF;
+    return e == 0 ? -133 : e - 134;
+}
+
 // Round-to-nearest-even fp32 -> bf16 bits (finite inputs).
 __device__ __forceinline__ uint16_t f32_to_bf16_bits(float f) {
     return __bfloat16_as_ushort(__float2bfloat16_rn(f));

@@ -1044,6 +1044,8 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
                             const int32_t* uni, int64_t su, int64_t holes, double b1, double b2, double eps,
                             double lr, float* out, float* grad_h, cudaEvent_t g_ready, cudaEvent_t fwd_done);
 
+static void ensure_key_stats(meft_ctx* ctx, meft_store* s, int64_t layer);
+
 static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const void* h, const void* g, int64_t T,
                             int64_t kk, int64_t k, double b1, double b2, double eps, double lr, float* out,
                             float* grad_h, int32_t* per_token_user, int32_t* union_user, meft_step_info* info,
@@ -1068,8 +1070,9 @@ static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
     // meft_ffn: ke_select (experts.cpp:47-117)
     {
         PhaseScope ps(ctx, 0);
+        ensure_key_stats(ctx, s, layer);  // cached across steps: the fused Adam refreshes the rows it updates
         ke_select_device(st, 2, h, L.c_g, L.c_a, T, d, M, N, kk_eff, take, ws, wsb, per_token, nullptr, uni, usize,
-                         ctx->dev_small + 5, ctx->selection_mode == MEFT_SELECT_AUTO);
+                         ctx->dev_small + 5, ctx->selection_mode == MEFT_SELECT_AUTO, L.kn, L.kl);
     }
     union_holes(st, uni, usize, usize + 3);
     MEFT_CUDA_CHECK(cudaMemcpyAsync(ctx->host_small + 4, usize, 16, cudaMemcpyDeviceToHost, st));
@@ -1153,6 +1156,7 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
     if (fwd_done) MEFT_CUDA_CHECK(cudaEventRecord(fwd_done, st));
     if (g_ready) MEFT_CUDA_CHECK(cudaStreamWaitEvent(st, g_ready, 0));
 
+    const bool stats_valid = s->key_stats_valid[size_t(layer)] != 0;
     if (s->pending[size_t(layer)]) {
         // earlier scatter_grads are pending: sparse_backward + scatter_grads fused, the weight-grad GEMM epilogues
         // add straight into the stage rows at S, then Adam consumes every staged pair (memtier.cpp:187-210)
@@ -1180,7 +1184,9 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
             adam_mixed(st, uni, nullptr, su, d, static_cast<float*>(L.w_a), static_cast<float*>(L.m_a),
                        static_cast<float*>(L.v_a), gka, static_cast<uint16_t*>(L.c_a), static_cast<float*>(L.w_b),
                        static_cast<float*>(L.m_b), static_cast<float*>(L.v_b), gvb, static_cast<uint16_t*>(L.c_b),
-                       L.step, nullptr, b1, b2, eps, lr, 3, true, true);
+                       L.step, nullptr, b1, b2, eps, lr, 3, true, true, stats_valid ? L.kn : nullptr,
+                       stats_valid ? L.kl : nullptr);
+        return;  // key statistics stay valid (refreshed for exactly the rows that changed)
     }
     s->key_stats_valid[size_t(layer)] = 0;
 }

@@ -14,6 +14,7 @@
 //   -> ordered compaction of the bitmap into the ascending union S.
 #include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -425,7 +426,14 @@ size_t exact_workspace_bytes(int64_t T, int64_t M, int64_t N, int64_t kk_eff) {
 
 // K-chunks of the candidate-scoring GEMM: 512-wide chunks tighten the certified bound ~d/512-fold, which cuts the
 // exact fp64 re-scoring proportionally (profiles/: 27 -> ~4 ambiguous candidates per token at d = 4096).
-int cert_ksplit(int64_t d) { return int(std::max<int64_t>(1, std::min<int64_t>(8, d / 512))); }
+int cert_ksplit(int64_t d) {
+    static const int forced = [] {  // MEFT_CERT_KSPLIT: developer override for tuning sweeps
+        const char* v = std::getenv("MEFT_CERT_KSPLIT");
+        return v ? std::max(1, std::min(16, std::atoi(v))) : 0;
+    }();
+    if (forced) return int(std::min<int64_t>(forced, std::max<int64_t>(1, d / 64)));
+    return int(std::max<int64_t>(1, std::min<int64_t>(4, d / 1024)));  // 1024-wide chunks: measured best
+}
 
 size_t cert_workspace_bytes(int64_t T, int64_t d, int64_t M, int64_t N, int64_t kk_eff) {
     const int64_t E = M / N;
@@ -469,7 +477,8 @@ size_t select_workspace_bytes(int64_t T, int64_t d, int64_t M, int64_t N, int64_
 static void ke_select_certified(cudaStream_t st, const void* h_, const void* w_g_, const void* keys_, int64_t T,
                                 int64_t d, int64_t M, int64_t N, int64_t kk_eff, int64_t take, void* ws,
                                 int32_t* per_token, int32_t* tau_out, int32_t* union_idx, int32_t* union_size,
-                                int32_t* stats) {
+                                int32_t* stats,
+                                const float* key_norms, const int32_t* key_lsb) {
     const uint16_t* h = static_cast<const uint16_t*>(h_);
     const uint16_t* wg = static_cast<const uint16_t*>(w_g_);
     const uint16_t* keys = static_cast<const uint16_t*>(keys_);
@@ -504,8 +513,13 @@ static void ke_select_certified(cudaStream_t st, const void* h_, const void* w_g
     if (stats) MEFT_CUDA_CHECK(cudaMemsetAsync(stats, 0, 2 * sizeof(int32_t), st));
     k_row_norms<<<int((T * 32 + 255) / 256), 256, 0, st>>>(h, T, int(d), hn, hl);
     check_launch("k_row_norms");
-    k_row_norms<<<int((M * 32 + 255) / 256), 256, 0, st>>>(keys, M, int(d), kn, kl);
-    check_launch("k_row_norms");
+    if (key_norms && key_lsb) {  // the store's cached key statistics (kept current by the fused Adam)
+        kn = const_cast<float*>(key_norms);
+        kl = const_cast<int32_t*>(key_lsb);
+    } else {
+        k_row_norms<<<int((M * 32 + 255) / 256), 256, 0, st>>>(keys, M, int(d), kn, kl);
+        check_launch("k_row_norms");
+    }
     if (N == 1) {
         // flat top-K (adapter.cpp:42-84): one candidate block of all M keys per token
         MEFT_CUDA_CHECK(cudaMemsetAsync(tau, 0, T * 4, st));
@@ -598,11 +612,12 @@ static void ke_select_certified(cudaStream_t st, const void* h_, const void* w_g
 void ke_select_device(cudaStream_t st, int dtype, const void* h, const void* w_g, const void* keys, int64_t T,
                       int64_t d, int64_t M, int64_t N, int64_t kk_eff, int64_t take, void* ws, size_t ws_bytes,
                       int32_t* per_token, int32_t* tau_out, int32_t* union_idx, int32_t* union_size,
-                      int32_t* stats, bool allow_certified) {
+                      int32_t* stats, bool allow_certified,
+                      const float* key_norms, const int32_t* key_lsb) {
     if (ws_bytes < select_workspace_bytes(T, d, M, N, kk_eff)) throw MeftError(6, "ke_select: workspace too small");
     if (allow_certified && certified_ok(dtype, d, M, N, kk_eff)) {
         ke_select_certified(st, h, w_g, keys, T, d, M, N, kk_eff, take, ws, per_token, tau_out, union_idx, union_size,
-                            stats);
+                            stats, key_norms, key_lsb);
         return;
     }
     if (stats) MEFT_CUDA_CHECK(cudaMemsetAsync(stats, 0, 2 * sizeof(int32_t), st));

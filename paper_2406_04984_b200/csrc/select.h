@@ -17,7 +17,8 @@ size_t select_workspace_bytes(int64_t T, int64_t d, int64_t M, int64_t N, int64_
 void ke_select_device(cudaStream_t st, int dtype, const void* h, const void* w_g, const void* keys, int64_t T,
                       int64_t d, int64_t M, int64_t N, int64_t kk_eff, int64_t take, void* ws, size_t ws_bytes,
                       int32_t* per_token, int32_t* tau_out, int32_t* union_idx, int32_t* union_size,
-                      int32_t* stats = nullptr, bool allow_certified = true);
+                      int32_t* stats = nullptr, bool allow_certified = true,
+                      const float* key_norms = nullptr, const int32_t* key_lsb = nullptr);  // cached key stats
 
 // select_experts (experts.cpp:30-45) over precomputed router scores [T x N].
 void route_topk_device(cudaStream_t st, const double* scores, int64_t T, int64_t N, int64_t kk, int32_t* tau);

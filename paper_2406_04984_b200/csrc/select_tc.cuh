@@ -32,11 +32,6 @@ __host__ __device__ inline double cert_bound_coeff_split(int d, int chunk, int k
            0x1p-23;
 }
 
-// exponent of the least significant mantissa bit of a bf16 value (subnormals: 2^-133)
-__device__ __forceinline__ int bf16_lsb_exp(uint16_t b) {
-    const int e = (b >> 7) & 0xFF;
-    return e == 0 ? -133 : e - 134;
-}
 
 __device__ __forceinline__ double bfd(uint16_t b) { return double(bf16_bits_to_f32(b)); }
 

@@ -91,9 +91,12 @@ __global__ void __launch_bounds__(256) k_adam_mixed(const int32_t* __restrict__ 
                                                     float* __restrict__ mb, float* __restrict__ vb,
                                                     float* __restrict__ sb, uint16_t* __restrict__ cb,
                                                     int32_t* __restrict__ step, uint8_t* __restrict__ staged, float b1,
-                                                    float b2, float eps, float lr, int tables, int bump, int gpos) {
+                                                    float b2, float eps, float lr, int tables, int bump, int gpos,
+                                                    float* __restrict__ kn, int32_t* __restrict__ kl) {
     const int n = count_dev ? *count_dev : count;
     __shared__ AdamCoef s_k;
+    __shared__ double s_red[8];
+    __shared__ int s_lsb[8];
     for (int r = blockIdx.x; r < n; r += gridDim.x) {
         const int64_t j = rows[r];
         __syncthreads();
@@ -115,6 +118,9 @@ __global__ void __launch_bounds__(256) k_adam_mixed(const int32_t* __restrict__ 
             float4* v4 = reinterpret_cast<float4*>((tab ? vb : va) + j * d);
             float4* g4 = reinterpret_cast<float4*>((tab ? sb : sa) + (gpos ? int64_t(r) : j) * d);
             uint2* c4 = reinterpret_cast<uint2*>((tab ? cb : ca) + j * d);
+            const bool stats = tab == 0 && kn != nullptr;  // refresh the key row's selection statistics
+            double ss = 0.0;
+            int lsb = INT32_MAX;
             for (int64_t i = threadIdx.x; i < d / 4; i += blockDim.x) {
                 const float4 g = g4[i];
                 float4 m = m4[i], v = v4[i], w = w4[i];
@@ -128,8 +134,39 @@ __global__ void __launch_bounds__(256) k_adam_mixed(const int32_t* __restrict__ 
                 v4[i] = v;
                 w4[i] = w;
                 if (!gpos) g4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-                c4[i] = make_uint2(pack_bf16x2(f32_to_bf16_bits(w.x), f32_to_bf16_bits(w.y)),
-                                   pack_bf16x2(f32_to_bf16_bits(w.z), f32_to_bf16_bits(w.w)));
+                const uint16_t cb4[4] = {f32_to_bf16_bits(w.x), f32_to_bf16_bits(w.y), f32_to_bf16_bits(w.z),
+                                         f32_to_bf16_bits(w.w)};
+                c4[i] = make_uint2(pack_bf16x2(cb4[0], cb4[1]), pack_bf16x2(cb4[2], cb4[3]));
+                if (stats) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const double v = double(bf16_bits_to_f32(cb4[q]));
+                        ss = fma(v, v, ss);
+                        if (cb4[q] & 0x7FFF) lsb = min(lsb, bf16_lsb_exp(cb4[q]));
+                    }
+                }
+            }
+            if (stats) {  // same bound as k_row_norms: sqrt of the fp64 sum of squares, rounded up (x(1+2^-20))
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+                    lsb = min(lsb, __shfl_xor_sync(0xffffffffu, lsb, o));
+                }
+                if ((threadIdx.x & 31) == 0) {
+                    s_red[threadIdx.x >> 5] = ss;
+                    s_lsb[threadIdx.x >> 5] = lsb;
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    double t = 0.0;
+                    int l = INT32_MAX;
+                    for (int w_ = 0; w_ < int(blockDim.x >> 5); ++w_) {
+                        t += s_red[w_];
+                        l = min(l, s_lsb[w_]);
+                    }
+                    kn[j] = __double2float_ru(sqrt(t) * (1.0 + 0x1p-20));
+                    kl[j] = l;
+                }
             }
         }
     }
@@ -335,12 +372,12 @@ void mark_rows(cudaStream_t st, uint8_t* staged, const int32_t* idx, const int32
 void adam_mixed(cudaStream_t st, const int32_t* rows, const int32_t* count_dev, int64_t count, int64_t d, float* wa,
                 float* ma, float* va, float* sa, uint16_t* ca, float* wb, float* mb, float* vb, float* sb,
                 uint16_t* cb, int32_t* step, uint8_t* staged, double b1, double b2, double eps, double lr, int tables,
-                bool bump, bool grads_by_position) {
+                bool bump, bool grads_by_position, float* key_norms, int32_t* key_lsb) {
     if (d % 4) throw MeftError(2, "adam: d must be a multiple of 4 in mixed precision");
     const int grid = std::max(1, std::min<int>(int(count > 0 ? count : num_sms() * 8), num_sms() * 8));
     k_adam_mixed<<<grid, 256, 0, st>>>(rows, count_dev, int(count), d, wa, ma, va, sa, ca, wb, mb, vb, sb, cb, step,
                                        staged, float(b1), float(b2), float(eps), float(lr), tables, bump ? 1 : 0,
-                                       grads_by_position ? 1 : 0);
+                                       grads_by_position ? 1 : 0, key_norms, key_lsb);
     check_launch("k_adam_mixed");
 }
 

@@ -17,7 +17,8 @@ void adam_mixed(cudaStream_t st, const int32_t* rows, const int32_t* count_dev, 
                 float* ma, float* va, float* sa, uint16_t* ca, float* wb, float* mb, float* vb, float* sb,
                 uint16_t* cb, int32_t* step, uint8_t* staged, double b1, double b2, double eps, double lr,
                 int tables = 3, bool bump = true,  // tables: bit 0 keys, bit 1 values
-                bool grads_by_position = false);   // sa/sb = [count x d] gradients of rows[0..count), kept as is
+                bool grads_by_position = false,    // sa/sb = [count x d] gradients of rows[0..count), kept as is
+                float* key_norms = nullptr, int32_t* key_lsb = nullptr);  // refresh updated keys' select stats
 void adam_f64(cudaStream_t st, const int32_t* rows, const int32_t* count_dev, int64_t count, int64_t d, double* wa,
               double* ma, double* va, double* sa, double* wb, double* mb, double* vb, double* sb, int32_t* step,
               uint8_t* staged, double b1, double b2, double eps, double lr);

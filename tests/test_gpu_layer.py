@@ -166,3 +166,23 @@ def test_tma_gather_matches_gather_kernel_bitwise(ctx, T):
     ctx.set_gather("auto")
     for n in res[0]:
         np.testing.assert_array_equal(res[0][n], res[1][n], err_msg=n)
+
+
+def test_fused_adam_keeps_key_statistics_current(ctx):
+    """The certified selection reads cached key norms / min-LSB exponents; the fused Adam refreshes them for the
+    rows it rewrites. After two steps they must still certify the current keys: identical LSB exponents and a
+    norm that upper-bounds the exact one by at most the stated 2^-20 margin."""
+    from paper_2406_04984_b200 import sharded as SH
+    w_a, w_g, w_b, h, gr = cfg1_inputs(T=512)
+    st = make_store(ctx, w_a, w_g, w_b, 64)
+    for _ in range(2):
+        st.layer_step(0, bf16_dev(h), bf16_dev(gr), 4, 32, 1e-2)
+    eng = SH.DeviceEngine(ctx, st, st.tensor(0, "w_g_compute"))
+    kn, kl = eng.key_stats()
+    keys = st.tensor(0, "w_a_compute").contiguous()
+    fn, fl = eng.row_stats(keys)
+    torch.cuda.synchronize()
+    assert torch.equal(kl, fl)
+    exact = keys.double().norm(dim=1)
+    assert bool((kn.double() >= exact).all())
+    assert float((kn.double() / fn.double() - 1).abs().max()) < 1e-6
