@@ -298,7 +298,7 @@ def our_arm(args, rank, world, local_rank):
     peaks, peak_src = load_peaks()
     S = sum(usizes) / len(usizes)
     gemm_ms = (phases["ffn_forward"][0] + phases["ffn_backward"][0]) / args.steps
-    gemm_launches = (phases["ffn_forward"][1] + phases["ffn_backward"][1]) / args.steps  # 6 per step
+    gemm_launches = 6  # z, out | dA, gW_B, gW_A, grad_h per step (the phases also hold two ~us run-table kernels)
     gemm_flops = 2.0 * T * d * S  # algorithmic flops of one of the six T x d x |S| GEMMs
     gemm_tflops = gemm_flops / (gemm_ms / gemm_launches * 1e-3) / 1e12
     tc_peak = peaks.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"])
@@ -347,7 +347,7 @@ def our_arm(args, rank, world, local_rank):
                 "d2h_bytes_per_step": 2 * T * d * 4, "ms_per_step": e2e_s * 1e3,
                 "path": "meft_layer_step_host (C ABI, pinned host buffers)" if not sharded else
                         "sharded layer step with pinned host copies in and out"},
-        "roofline": {"bound": "tensor", "kernel": "k_gemm_bf16 (tcgen05 FFN GEMM)", "achieved": gemm_tflops,
+        "roofline": {"bound": "tensor", "kernel": "k_gemm_bf16_pair (tcgen05 cta_group::2 FFN GEMM, 6 per step)", "achieved": gemm_tflops,
                      "peak": tc_peak, "unit": "TFLOP/s", "frac": gemm_tflops / tc_peak, "traffic": traffic,
                      "traffic_unit": "bytes per launch (ncu dram read+write, profiles/gemm_traffic.json)",
                      "peak_source": f"{peak_src} bf16_tflops_sustained",
