@@ -279,7 +279,8 @@ void ffn_forward_impl(meft_ctx* ctx, meft_dtype dt, const void* h, const void* k
 void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* h, const void* z, const void* keys_s,
                        const void* values_s, int64_t T, int64_t d, int64_t s, int64_t ld_z, void* masked,
                        void* grad_keys_s, void* grad_values_s, void* grad_h, bool acc_h, const int32_t* S_rows,
-                       void* stage_keys, void* stage_values, const RowGather& rg = RowGather()) {
+                       void* stage_keys, void* stage_values, const RowGather& rg = RowGather(),
+                       cudaEvent_t grad_h_done = nullptr) {
     cudaStream_t st = ctx->stream;
     if (dt == MEFT_F64) {
         const double* gd = static_cast<const double*>(g);
@@ -322,6 +323,15 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
     e3.mask = z;
     e3.ldm = ld_z;
     gemm_bf16(st, T, s, d, GemmOperand{g, d, false}, kv_operand(ctx, values_s, d, false, rg, s), e3);
+    if (grad_h) {  // first after masked, so grad_h can stream back while the weight-gradient GEMMs run
+        GemmEpilogue e6;  // grad_h (+)= masked * keys_s
+        e6.kind = EPI_STORE_F32;
+        e6.c = grad_h;
+        e6.ldc = d;
+        e6.accumulate = acc_h;
+        gemm_bf16(st, T, d, s, GemmOperand{masked, ld_z, false}, kv_operand(ctx, keys_s, d, true, rg, s), e6);
+    }
+    if (grad_h_done) MEFT_CUDA_CHECK(cudaEventRecord(grad_h_done, st));
     GemmEpilogue e4;  // grad_values = act^T G   (M = s, N = d, K = T)
     if (S_rows) {
         e4.kind = EPI_ROWS_ADD_F32;
@@ -336,14 +346,6 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
     GemmEpilogue e5 = e4;  // grad_keys = masked^T h
     e5.c = S_rows ? stage_keys : grad_keys_s;
     gemm_bf16(st, s, d, T, GemmOperand{masked, ld_z, true}, GemmOperand{h, d, true}, e5);
-    if (grad_h) {
-        GemmEpilogue e6;  // grad_h (+)= masked * keys_s
-        e6.kind = EPI_STORE_F32;
-        e6.c = grad_h;
-        e6.ldc = d;
-        e6.accumulate = acc_h;
-        gemm_bf16(st, T, d, s, GemmOperand{masked, ld_z, false}, kv_operand(ctx, keys_s, d, true, rg, s), e6);
-    }
 }
 
 // ---- store helpers
@@ -517,6 +519,7 @@ meft_status meft_ctx_create(int device, void* stream, meft_ctx** out) {
         MEFT_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
         MEFT_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_fwd, cudaEventDisableTiming));
         MEFT_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
+        MEFT_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
         MEFT_CUDA_CHECK(cudaMalloc(&c->dev_small, 64 * sizeof(int32_t)));
         MEFT_CUDA_CHECK(cudaMallocHost(&c->host_small, 64 * sizeof(int32_t)));
     });
@@ -536,6 +539,7 @@ void meft_ctx_destroy(meft_ctx* ctx) {
     if (ctx->host_small) cudaFreeHost(ctx->host_small);
     if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
     if (ctx->ev_fwd) cudaEventDestroy(ctx->ev_fwd);
+    if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
     if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -1042,14 +1046,15 @@ meft_status meft_sparse_adam_update(meft_ctx* ctx, meft_store* s, int64_t layer,
 
 static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const void* h, const void* g, int64_t T,
                             const int32_t* uni, int64_t su, int64_t holes, double b1, double b2, double eps,
-                            double lr, float* out, float* grad_h, cudaEvent_t g_ready, cudaEvent_t fwd_done);
+                            double lr, float* out, float* grad_h, cudaEvent_t g_ready, cudaEvent_t fwd_done,
+                            cudaEvent_t gh_done = nullptr);
 
 static void ensure_key_stats(meft_ctx* ctx, meft_store* s, int64_t layer);
 
 static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const void* h, const void* g, int64_t T,
                             int64_t kk, int64_t k, double b1, double b2, double eps, double lr, float* out,
                             float* grad_h, int32_t* per_token_user, int32_t* union_user, meft_step_info* info,
-                            cudaEvent_t g_ready, cudaEvent_t fwd_done) {
+                            cudaEvent_t g_ready, cudaEvent_t fwd_done, cudaEvent_t gh_done = nullptr) {
     const long long launches0 = launch_counter();
     const LayerBufs& L = layer_of(s, layer);
     require(s->prec == MEFT_STORE_MIXED, MEFT_E_INVALID, "layer_step: requires a MIXED precision store");
@@ -1079,7 +1084,7 @@ static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
     MEFT_CUDA_CHECK(cudaStreamSynchronize(st));
     const int64_t su = ctx->host_small[4];
     ffn_update_impl(ctx, s, layer, h, g, T, uni, su, ctx->host_small[7], b1, b2, eps, lr, out, grad_h, g_ready,
-                    fwd_done);
+                    fwd_done, gh_done);
 
     if (info) {
         info->union_size = su;
@@ -1113,7 +1118,8 @@ static bool use_tma_gather(const meft_ctx* ctx, int64_t su, int64_t holes) {
 
 static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const void* h, const void* g, int64_t T,
                             const int32_t* uni, int64_t su, int64_t holes, double b1, double b2, double eps,
-                            double lr, float* out, float* grad_h, cudaEvent_t g_ready, cudaEvent_t fwd_done) {
+                            double lr, float* out, float* grad_h, cudaEvent_t g_ready, cudaEvent_t fwd_done,
+                            cudaEvent_t gh_done) {
     const LayerBufs& L = layer_of(s, layer);
     const int64_t d = s->d;
     cudaStream_t st = ctx->stream;
@@ -1164,7 +1170,7 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
         {
             PhaseScope ps(ctx, 3);
             ffn_backward_impl(ctx, MEFT_BF16, g, h, act, ks, vs, T, d, su, ld, masked, nullptr, nullptr, ghb, false,
-                              uni, L.st_a, L.st_b, rg);
+                              uni, L.st_a, L.st_b, rg, gh_done);
         }
         PhaseScope ps(ctx, 4);
         if (su > 0) mark_rows(st, L.staged, uni, nullptr, su);
@@ -1177,7 +1183,7 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
         {
             PhaseScope ps(ctx, 3);
             ffn_backward_impl(ctx, MEFT_BF16, g, h, act, ks, vs, T, d, su, ld, masked, gka, gvb, ghb, false, nullptr,
-                              nullptr, nullptr, rg);
+                              nullptr, nullptr, rg, gh_done);
         }
         PhaseScope ps(ctx, 4);
         if (su > 0)
@@ -1319,14 +1325,19 @@ meft_status meft_layer_step_host(meft_ctx* ctx, meft_store* s, int64_t layer, co
         MEFT_CUDA_CHECK(cudaMemcpyAsync(hd, h_host, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
         MEFT_CUDA_CHECK(cudaMemcpyAsync(gd, g_host, in_bytes, cudaMemcpyHostToDevice, ctx->copy_stream));
         MEFT_CUDA_CHECK(cudaEventRecord(ctx->ev_in, ctx->copy_stream));
+        // The copy stream carries both results back while compute continues: out after the forward, grad_h as soon
+        // as its GEMM (scheduled right after `masked`) is done -- overlapping the weight-gradient GEMMs and Adam.
+        // The copies are enqueued after the step is (the events are recorded inside it).
         layer_step_impl(ctx, s, layer, hd, gd, T, kk, k, beta1, beta2, eps, lr, od, ghd, nullptr, nullptr, info,
-                        ctx->ev_in, ctx->ev_fwd);
-        // the forward output streams back while the backward runs
+                        ctx->ev_in, ctx->ev_fwd, ctx->ev_out);
         if (out_host) {
             MEFT_CUDA_CHECK(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_fwd, 0));
             MEFT_CUDA_CHECK(cudaMemcpyAsync(out_host, od, out_bytes, cudaMemcpyDeviceToHost, ctx->copy_stream));
         }
-        if (grad_h_host) MEFT_CUDA_CHECK(cudaMemcpyAsync(grad_h_host, ghd, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        if (grad_h_host) {
+            MEFT_CUDA_CHECK(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_out, 0));
+            MEFT_CUDA_CHECK(cudaMemcpyAsync(grad_h_host, ghd, out_bytes, cudaMemcpyDeviceToHost, ctx->copy_stream));
+        }
         MEFT_CUDA_CHECK(cudaStreamSynchronize(ctx->copy_stream));
         MEFT_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     });
