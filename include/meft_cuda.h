@@ -1,8 +1,8 @@
 /* meft_cuda.h — C ABI of libmeft_cuda.so, the B200 (sm_100a) implementation of the MEFT sparse
  * Key-Experts adapter layer (arXiv 2406.04984).
  *
- * This is the thin layer under the drop-in C++ host API (include/meft/*.hpp, the same declarations as
- * the reference's proj/include/meft/*.hpp). Every entry point names the reference function it replaces
+ * This is the thin layer under the drop-in C++ host API (include/meft/<name>.hpp, the same declarations as
+ * the reference's proj/include/meft headers). Every entry point names the reference function it replaces
  * (paths relative to /root/reference/proj). Plain pointers and sizes only — no torch or CUDA types.
  *
  * Conventions
@@ -37,7 +37,13 @@ typedef enum meft_status {
     MEFT_E_NONFINITE = 5,
     MEFT_E_CUDA = 6,
     MEFT_E_NCCL = 7,
-    MEFT_E_OOM = 8
+    MEFT_E_OOM = 8,
+    /* MEFT1 checkpoints (memtier.hpp:172-183): CheckpointHeaderError, CheckpointShapeError,
+     * CheckpointTruncatedError; I/O failures map to std::runtime_error. */
+    MEFT_E_CKPT_HEADER = 9,
+    MEFT_E_CKPT_SHAPE = 10,
+    MEFT_E_CKPT_TRUNCATED = 11,
+    MEFT_E_IO = 12
 } meft_status;
 
 typedef enum meft_dtype { MEFT_F64 = 0, MEFT_F32 = 1, MEFT_BF16 = 2 } meft_dtype;
@@ -64,7 +70,12 @@ typedef enum meft_tensor {
     MEFT_T_STAGED = 10,
     MEFT_T_W_A_COMPUTE = 11,
     MEFT_T_W_B_COMPUTE = 12,
-    MEFT_T_W_G_COMPUTE = 13
+    MEFT_T_W_G_COMPUTE = 13,
+    /* router training state (train_router; memtier.cpp:86-91): N x d moments, int64[N] step counters on the host
+     * side (int32 on device); available after meft_store_enable_router, MEFT_E_LOGIC otherwise */
+    MEFT_T_M_G = 14,
+    MEFT_T_V_G = 15,
+    MEFT_T_ROUTER_STEP = 16
 } meft_tensor;
 
 typedef struct meft_ctx meft_ctx;
@@ -223,6 +234,39 @@ meft_status meft_store_download_host(meft_ctx* ctx, meft_store* store, int64_t l
 /* Device view of a store tensor in its device layout. */
 meft_status meft_store_tensor(meft_store* store, int64_t layer, meft_tensor t, void** dev, meft_dtype* dt,
                               int64_t* rows, int64_t* cols);
+/* HostStore::init(..., train_router=true) (memtier.cpp:86-91): allocate zeroed router moments and step counters
+ * for every layer (MEFT_T_M_G / V_G / ROUTER_STEP); idempotent. meft_store_train_router reports the flag. */
+meft_status meft_store_enable_router(meft_ctx* ctx, meft_store* store);
+meft_status meft_store_train_router(const meft_store* store, int* on);
+
+/* ------------------------------------------------------------------ MEFT1 checkpoints (memtier.cpp:288-396)
+ * One JSON header line {extra, dim, experts, layers, magic "MEFT1", moment_precision "f64", pairs, step,
+ * train_router, version 1, weight_precision "f32"} (keys sorted, as nlohmann::json dumps it), then per layer in
+ * reference layouts: w_a f32 [d x r], w_b f32 [r x d], w_g f32 [N x d], m_a f64 [d x r], v_a f64 [d x r],
+ * m_b f64 [r x d], v_b f64 [r x d], pair_step i64 [r], and with train_router m_g f64 [N x d], v_g f64 [N x d],
+ * router_step i64 [N]. Staging is not saved (it is empty after every sparse_adam_update) and loads as zero.
+ * Errors: extra not JSON -> MEFT_E_INVALID; cannot open / write failure -> MEFT_E_IO; missing or corrupt header,
+ * bad magic, version != 1, missing field -> MEFT_E_CKPT_HEADER; non-positive shape, trailing bytes ->
+ * MEFT_E_CKPT_SHAPE; short payload -> MEFT_E_CKPT_TRUNCATED (messages as the reference's). */
+typedef struct meft_ckpt_header {
+    int64_t layers, dim, pairs, experts, step;
+    int train_router;
+} meft_ckpt_header;
+/* Device store <-> file: save_checkpoint / load_checkpoint for an HBM store (precision of the new store given).
+ * `extra_json` NULL means "{}"; `extra_out` (may be NULL) receives the header's extra object, truncated to cap. */
+meft_status meft_store_save(meft_ctx* ctx, meft_store* store, const char* path, int64_t step, const char* extra_json);
+meft_status meft_store_load(meft_ctx* ctx, const char* path, meft_precision precision, meft_store** out,
+                            meft_ckpt_header* header, char* extra_out, size_t extra_cap);
+/* Host-resident stores (the C++ shim's HostStore): the same format through per-tensor callbacks. Values travel
+ * as double (f32/f64 items) or int64 (counters) in the reference layout, n = rows * cols; a callback returns 0 on
+ * success. The sink sees the parsed header before the first tensor of every layer. */
+typedef int (*meft_ckpt_source)(void* user, int64_t layer, meft_tensor t, void* dst, int64_t n);
+typedef int (*meft_ckpt_sink)(void* user, const meft_ckpt_header* h, int64_t layer, meft_tensor t, const void* src,
+                              int64_t n);
+meft_status meft_ckpt_save(const char* path, const meft_ckpt_header* header, const char* extra_json,
+                           meft_ckpt_source source, void* user);
+meft_status meft_ckpt_load(const char* path, meft_ckpt_header* header, char* extra_out, size_t extra_cap,
+                           meft_ckpt_sink sink, void* user);
 
 /* fetch (memtier.cpp:117-126): gather rows S of the layer's compute tables (validated like gather_adapter). */
 meft_status meft_fetch(meft_ctx* ctx, meft_store* store, int64_t layer, const int32_t* S, int64_t s, void* keys_s,

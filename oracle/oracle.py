@@ -352,6 +352,10 @@ class RefStore:
                                            C.byref(m)))
         return m.value
 
+    def save(self, path, extra="{}", step=0):
+        """The reference's save_checkpoint (MEFT1) of this store."""
+        _check_ref(ref().ref_store_save(_P(self.h), str(path).encode(), extra.encode(), _I64(step)))
+
     def sparse_adam(self, layer, lr, beta1=0.9, beta2=0.999, eps=1e-8):
         _check_ref(ref().ref_sparse_adam(_P(self.h), _I64(layer), _D(beta1), _D(beta2), _D(eps), _D(lr)))
 

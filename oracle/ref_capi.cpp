@@ -228,6 +228,15 @@ void* ref_store_init(int64_t layers, int64_t d, int64_t r, int64_t n, int train_
 
 void ref_store_free(void* s) { delete static_cast<HostStore*>(s); }
 
+// save_checkpoint (memtier.cpp:288-326) of the reference store, global_step set first.
+int ref_store_save(void* sp, const char* path, const char* extra_json, int64_t step) {
+    return guard([&] {
+        HostStore& st = *static_cast<HostStore*>(sp);
+        st.global_step = step;
+        save_checkpoint(st, path, extra_json);
+    });
+}
+
 int ref_store_get(void* sp, int64_t layer, int id, double* out) {
     return guard([&] { from_matrix(*store_tensor(static_cast<HostStore*>(sp)->layer(layer), id), out); });
 }

@@ -16,6 +16,15 @@ I32P = C.POINTER(C.c_int32)
 D = C.c_double
 INT = C.c_int
 
+class CkptHeader(C.Structure):
+    _fields_ = [("layers", I64), ("dim", I64), ("pairs", I64), ("experts", I64), ("step", I64),
+                ("train_router", INT)]
+
+
+# meft_ckpt_source / meft_ckpt_sink (include/meft_cuda.h)
+CKPT_SOURCE = C.CFUNCTYPE(INT, P, I64, INT, P, I64)
+CKPT_SINK = C.CFUNCTYPE(INT, P, C.POINTER(CkptHeader), I64, INT, P, I64)
+
 # name -> (restype, argtypes)
 _SIGS = {
     "meft_version": (C.c_char_p, []),
@@ -61,6 +70,12 @@ _SIGS = {
     "meft_activation_f64": (INT, [P, INT, P, P, I64]),
     "meft_adam_rows_f64": (INT, [P, P, P, P, P, P, P, P, I64, I64, D, D, D, D]),
     "meft_store_create": (INT, [P, I64, I64, I64, I64, INT, C.POINTER(P)]),
+    "meft_store_enable_router": (INT, [P, P]),
+    "meft_store_train_router": (INT, [P, C.POINTER(INT)]),
+    "meft_store_save": (INT, [P, P, C.c_char_p, I64, C.c_char_p]),
+    "meft_store_load": (INT, [P, C.c_char_p, INT, C.POINTER(P), C.POINTER(CkptHeader), C.c_char_p, C.c_size_t]),
+    "meft_ckpt_save": (INT, [C.c_char_p, C.POINTER(CkptHeader), C.c_char_p, CKPT_SOURCE, P]),
+    "meft_ckpt_load": (INT, [C.c_char_p, C.POINTER(CkptHeader), C.c_char_p, C.c_size_t, CKPT_SINK, P]),
     "meft_store_destroy": (None, [P]),
     "meft_store_info": (INT, [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64), C.POINTER(I64), C.POINTER(INT)]),
     "meft_store_init_reference": (INT, [P, P, C.c_uint64]),
@@ -78,7 +93,10 @@ F64, F32, BF16 = 0, 1, 2
 STORE_F64, STORE_MIXED = 0, 1
 
 TENSORS = {"w_a": 0, "w_b": 1, "w_g": 2, "m_a": 3, "v_a": 4, "m_b": 5, "v_b": 6, "stage_a": 7, "stage_b": 8,
-           "pair_step": 9, "staged": 10, "w_a_compute": 11, "w_b_compute": 12, "w_g_compute": 13}
+           "pair_step": 9, "staged": 10, "w_a_compute": 11, "w_b_compute": 12, "w_g_compute": 13, "m_g": 14,
+           "v_g": 15, "router_step": 16}
+TENSOR_NAMES = {v: k for k, v in TENSORS.items()}
+
 
 
 class StepInfo(C.Structure):
@@ -90,7 +108,8 @@ class MeftError(RuntimeError):
     """Error raised from a meft_status != MEFT_OK; `kind` mirrors the reference exception type."""
 
     KINDS = {1: "ShapeError", 2: "invalid_argument", 3: "out_of_range", 4: "logic_error", 5: "non-finite",
-             6: "cuda", 7: "nccl", 8: "oom"}
+             6: "cuda", 7: "nccl", 8: "oom", 9: "CheckpointHeaderError", 10: "CheckpointShapeError",
+             11: "CheckpointTruncatedError", 12: "io"}
 
     def __init__(self, code: int, msg: str, index: int = -1):
         super().__init__(f"{self.KINDS.get(code, code)}: {msg}")

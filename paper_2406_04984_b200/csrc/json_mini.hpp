@@ -11,7 +11,7 @@
 #include <string>
 #include <vector>
 
-namespace meft::dropin::json {
+namespace meft_json {
 
 struct ParseError : std::runtime_error {
     explicit ParseError(const std::string& m) : std::runtime_error(m) {}
@@ -249,4 +249,4 @@ inline std::string dump(const Value& v) {
     return s;
 }
 
-}  // namespace meft::dropin::json
+}  // namespace meft_json

@@ -101,6 +101,11 @@ struct LayerBufs {
     int32_t* kl = nullptr;    // MIXED: cached minimum LSB exponents of the bf16 compute keys
     void* base = nullptr;
     void* stage_base = nullptr;  // staging tables, allocated on first use (scatter_grads / staging access)
+    // router training state (memtier.cpp:86-91), allocated by meft_store_enable_router
+    void* m_g = nullptr;
+    void* v_g = nullptr;
+    int32_t* rstep = nullptr;
+    void* router_base = nullptr;
 };
 
 }  // namespace
@@ -114,6 +119,7 @@ struct meft_store {
     // per layer: staging may hold gradients (scatter_grads / caller access) that the next Adam must consume.
     // While clear, staging is all zero and the fused layer step bypasses it entirely.
     std::vector<char> pending;
+    bool train_router = false;
 };
 
 namespace {
@@ -147,6 +153,13 @@ meft_status fail(meft_ctx* ctx, int code, const std::string& msg, int64_t index 
     }
     return static_cast<meft_status>(code);
 }
+
+}  // namespace
+
+// For the other C-ABI translation units (checkpoint.cu): record an error the way guarded() does.
+meft_status meft_internal_fail(meft_ctx* ctx, int code, const char* msg) { return fail(ctx, code, msg); }
+
+namespace {
 
 template <class F>
 meft_status guarded(meft_ctx* ctx, F&& f) {
@@ -375,6 +388,18 @@ void* tensor_ptr(const meft_store* s, const LayerBufs& L, meft_tensor t, meft_dt
         case MEFT_T_W_G_COMPUTE: *dt = comp; *rows = s->experts; return L.c_g;
         case MEFT_T_PAIR_STEP: *dt = MEFT_F32; *cols = 1; return L.step;  // int32 storage
         case MEFT_T_STAGED: *dt = MEFT_BF16; *cols = 1; return L.staged;  // uint8 storage
+        case MEFT_T_M_G:
+        case MEFT_T_V_G:
+        case MEFT_T_ROUTER_STEP:
+            if (!s->train_router) throw MeftError(MEFT_E_LOGIC, "router state: the router is frozen");
+            *rows = s->experts;
+            if (t == MEFT_T_ROUTER_STEP) {
+                *dt = MEFT_F32;  // int32 storage
+                *cols = 1;
+                return L.rstep;
+            }
+            *dt = master;
+            return t == MEFT_T_M_G ? L.m_g : L.v_g;
         default: throw MeftError(MEFT_E_INVALID, "unknown store tensor");
     }
 }
@@ -884,8 +909,41 @@ void meft_store_destroy(meft_store* store) {
     for (auto& L : store->L) {
         cudaFree(L.base);
         if (L.stage_base) cudaFree(L.stage_base);
+        if (L.router_base) cudaFree(L.router_base);
     }
     delete store;
+}
+
+meft_status meft_store_enable_router(meft_ctx* ctx, meft_store* s) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(s != nullptr, MEFT_E_INVALID, "null store");
+        if (s->train_router) return;
+        const size_t mb = s->prec == MEFT_STORE_F64 ? 8 : 4;
+        const size_t nd = (size_t(s->experts) * size_t(s->d) * mb + 255) & ~size_t(255);
+        const size_t bytes = 2 * nd + size_t(s->experts) * 4;
+        for (auto& L : s->L) {
+            cudaError_t e = cudaMalloc(&L.router_base, bytes);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                L.router_base = nullptr;
+                throw MeftError(MEFT_E_OOM, "enable_router: cannot allocate router state");
+            }
+            MEFT_CUDA_CHECK(cudaMemsetAsync(L.router_base, 0, bytes, ctx->stream));
+            L.m_g = L.router_base;
+            L.v_g = static_cast<uint8_t*>(L.router_base) + nd;
+            L.rstep = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(L.router_base) + 2 * nd);
+        }
+        MEFT_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        s->train_router = true;
+    });
+}
+
+meft_status meft_store_train_router(const meft_store* s, int* on) {
+    return guarded(nullptr, [&] {
+        require(s != nullptr && on != nullptr, MEFT_E_INVALID, "null store / output");
+        *on = s->train_router ? 1 : 0;
+    });
 }
 
 meft_status meft_store_info(const meft_store* s, int64_t* layers, int64_t* d, int64_t* pairs, int64_t* experts,
@@ -925,12 +983,16 @@ meft_status meft_store_upload_host(meft_ctx* ctx, meft_store* s, int64_t layer, 
             ensure_staging(s, layer);
             s->pending[size_t(layer)] = 1;
         }
-        if (t == MEFT_T_PAIR_STEP || t == MEFT_T_STAGED) {
-            require(rows * cols == s->pairs, MEFT_E_SHAPE, "store_upload: counter length");
-            if (t == MEFT_T_PAIR_STEP) {
-                int64_t* tmp = static_cast<int64_t*>(ctx->get("upload_a", size_t(s->pairs) * 8));
-                MEFT_CUDA_CHECK(cudaMemcpyAsync(tmp, host, size_t(s->pairs) * 8, cudaMemcpyHostToDevice, ctx->stream));
-                convert_index(ctx->stream, false, L.step, tmp, s->pairs);
+        if (t == MEFT_T_PAIR_STEP || t == MEFT_T_STAGED || t == MEFT_T_ROUTER_STEP) {
+            const int64_t n = t == MEFT_T_ROUTER_STEP ? s->experts : s->pairs;
+            require(rows * cols == n, MEFT_E_SHAPE, "store_upload: counter length");
+            if (t != MEFT_T_STAGED) {
+                meft_dtype dt_;
+                int64_t r_, c_;
+                int32_t* dst = static_cast<int32_t*>(tensor_ptr(s, L, t, &dt_, &r_, &c_));
+                int64_t* tmp = static_cast<int64_t*>(ctx->get("upload_a", size_t(n) * 8));
+                MEFT_CUDA_CHECK(cudaMemcpyAsync(tmp, host, size_t(n) * 8, cudaMemcpyHostToDevice, ctx->stream));
+                convert_index(ctx->stream, false, dst, tmp, n);
             } else {
                 MEFT_CUDA_CHECK(cudaMemcpyAsync(L.staged, host, size_t(s->pairs), cudaMemcpyHostToDevice, ctx->stream));
             }
@@ -955,12 +1017,16 @@ meft_status meft_store_download_host(meft_ctx* ctx, meft_store* s, int64_t layer
         require_ctx(ctx);
         const LayerBufs& L = layer_of(s, layer);
         if (is_staging(t)) ensure_staging(s, layer);
-        if (t == MEFT_T_PAIR_STEP || t == MEFT_T_STAGED) {
-            require(rows * cols == s->pairs, MEFT_E_SHAPE, "store_download: counter length");
-            if (t == MEFT_T_PAIR_STEP) {
-                int64_t* tmp = static_cast<int64_t*>(ctx->get("upload_a", size_t(s->pairs) * 8));
-                convert_index(ctx->stream, true, tmp, L.step, s->pairs);
-                MEFT_CUDA_CHECK(cudaMemcpyAsync(host, tmp, size_t(s->pairs) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        if (t == MEFT_T_PAIR_STEP || t == MEFT_T_STAGED || t == MEFT_T_ROUTER_STEP) {
+            const int64_t n = t == MEFT_T_ROUTER_STEP ? s->experts : s->pairs;
+            require(rows * cols == n, MEFT_E_SHAPE, "store_download: counter length");
+            if (t != MEFT_T_STAGED) {
+                meft_dtype dt_;
+                int64_t r_, c_;
+                int32_t* src = static_cast<int32_t*>(tensor_ptr(s, L, t, &dt_, &r_, &c_));
+                int64_t* tmp = static_cast<int64_t*>(ctx->get("upload_a", size_t(n) * 8));
+                convert_index(ctx->stream, true, tmp, src, n);
+                MEFT_CUDA_CHECK(cudaMemcpyAsync(host, tmp, size_t(n) * 8, cudaMemcpyDeviceToHost, ctx->stream));
             } else {
                 MEFT_CUDA_CHECK(cudaMemcpyAsync(host, L.staged, size_t(s->pairs), cudaMemcpyDeviceToHost, ctx->stream));
             }

@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import BF16, F32, F64, STORE_F64, STORE_MIXED, TENSORS, MeftError, check, lib
+from ._lib import BF16, F32, F64, STORE_F64, STORE_MIXED, TENSORS, CkptHeader, MeftError, check, lib
 
 P = C.c_void_p
 I64 = C.c_int64
@@ -245,6 +245,26 @@ class Store:
         except Exception:
             pass
 
+    @classmethod
+    def load(cls, ctx: Context, path, precision=STORE_MIXED):
+        """load_checkpoint (MEFT1, memtier.cpp:328-396) straight into a new HBM store. Returns (store, header,
+        extra_json)."""
+        h, hdr, extra = P(), CkptHeader(), C.create_string_buffer(1 << 20)
+        ctx.check(lib().meft_store_load(ctx.h, str(path).encode(), precision, C.byref(h), C.byref(hdr), extra,
+                                        len(extra)))
+        st = cls.__new__(cls)
+        st.ctx, st.h = ctx, h
+        st.layers, st.d, st.pairs, st.experts, st.precision = hdr.layers, hdr.dim, hdr.pairs, hdr.experts, precision
+        return st, hdr, extra.value.decode()
+
+    def save(self, path, step: int = 0, extra: str = "{}"):
+        """save_checkpoint (MEFT1, memtier.cpp:288-326) of this HBM store."""
+        self.ctx.check(lib().meft_store_save(self.ctx.h, self.h, str(path).encode(), step, extra.encode()))
+
+    def enable_router(self):
+        """train_router state (m_g, v_g, router_step) for every layer."""
+        self.ctx.check(lib().meft_store_enable_router(self.ctx.h, self.h))
+
     def init_reference(self, seed: int = 1):
         self.ctx.check(lib().meft_store_init_reference(self.ctx.h, self.h, C.c_uint64(seed)))
 
@@ -253,12 +273,16 @@ class Store:
             return (self.d, self.pairs)
         if name == "w_g":
             return (self.experts, self.d)
+        if name in ("m_g", "v_g"):
+            return (self.experts, self.d)
+        if name == "router_step":
+            return (self.experts,)
         if name in ("pair_step", "staged"):
             return (self.pairs,)
         return (self.pairs, self.d)
 
     def upload(self, layer, name, host):
-        dtype = {"pair_step": np.int64, "staged": np.int8}.get(name, np.float64)
+        dtype = {"pair_step": np.int64, "router_step": np.int64, "staged": np.int8}.get(name, np.float64)
         a = np.ascontiguousarray(host, dtype=dtype)
         shape = self._ref_shape(name)
         if a.shape != shape:
@@ -268,7 +292,7 @@ class Store:
                                                     rows, cols))
 
     def download(self, layer, name):
-        dtype = {"pair_step": np.int64, "staged": np.int8}.get(name, np.float64)
+        dtype = {"pair_step": np.int64, "router_step": np.int64, "staged": np.int8}.get(name, np.float64)
         shape = self._ref_shape(name)
         a = np.empty(shape, dtype=dtype)
         rows, cols = (shape[0], 1) if len(shape) == 1 else shape

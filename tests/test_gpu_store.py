@@ -96,3 +96,49 @@ def test_mixed_store_adam_tolerance(ctx):
     comp = st.tensor(0, "w_a_compute").float().cpu().numpy()  # bf16 copy tracks the fp32 master
     master = st.download(0, "w_a").T
     assert np.all(np.abs(comp - master) <= np.abs(master) * 2.0 ** -8)
+
+
+def test_device_checkpoint_matches_reference_bytes(ctx, tmp_path):
+    """An F64 HBM store holding the reference store's state writes the reference's MEFT1 file byte for byte
+    (memtier.cpp:288-326), router state included."""
+    d, r, n = 16, 32, 4
+    ref = O.RefStore(1, d, r, n, seed=5, train_router=True)
+    rng = np.random.default_rng(3)
+    for _ in range(2):
+        s = np.sort(rng.choice(r, 6, replace=False))
+        ref.scatter_grads(0, s, rng.standard_normal((d, 6)), rng.standard_normal((6, d)))
+        ref.sparse_adam(0, 1e-2)
+    ref.save(tmp_path / "ref.meft", extra='{"a": 1}', step=9)
+    st = G.Store(ctx, 1, d, r, n, G.STORE_F64)
+    st.enable_router()
+    for name in ("w_a", "w_b", "w_g", "m_a", "v_a", "m_b", "v_b"):
+        st.upload(0, name, ref.get(0, name))
+    st.upload(0, "pair_step", ref.pair_step(0))
+    # the reference's router moments are zero here (its STE lives in the trainer), counters too
+    st.save(tmp_path / "dev.meft", step=9, extra='{"a": 1}')
+    assert (tmp_path / "dev.meft").read_bytes() == (tmp_path / "ref.meft").read_bytes()
+
+
+def test_mixed_store_checkpoint_resumes_bit_exactly(ctx, tmp_path):
+    """save -> load of a trained MIXED store restores masters, moments, counters and compute copies exactly, and
+    the next layer step of the resumed store equals the original's bit for bit."""
+    d, M, N, T = 512, 4096, 64, 128
+    st = G.Store(ctx, 1, d, M, N, G.STORE_MIXED)
+    st.init_reference(seed=1)
+    gen = torch.Generator(device="cuda").manual_seed(2)
+    h = (torch.rand((T, d), generator=gen, device="cuda") * 2 - 1).to(torch.bfloat16)
+    g = (torch.rand((T, d), generator=gen, device="cuda") * 2 - 1).to(torch.bfloat16)
+    for _ in range(2):
+        st.layer_step(0, h, g, 4, 32, 1e-3)
+    st.save(tmp_path / "m.meft", step=2)
+    st2, hdr, extra = G.Store.load(ctx, tmp_path / "m.meft", G.STORE_MIXED)
+    assert (hdr.layers, hdr.dim, hdr.pairs, hdr.experts, hdr.step) == (1, d, M, N, 2) and extra == "{}"
+    for name in ("w_a", "w_b", "w_g", "m_a", "v_a", "m_b", "v_b", "pair_step", "w_a_compute", "w_b_compute"):
+        assert torch.equal(st.tensor(0, name), st2.tensor(0, name)), name
+    outs = []
+    for s_ in (st, st2):
+        o = torch.empty((T, d), dtype=torch.float32, device="cuda")
+        s_.layer_step(0, h, g, 4, 32, 1e-3, out=o)
+        outs.append((o, s_.tensor(0, "w_b").clone()))
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
