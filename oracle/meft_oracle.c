@@ -365,3 +365,34 @@ void or_sparse_adam(int64_t d, int64_t r, double* w_a, double* w_b, double* m_a,
         staged[j] = 0;
     }
 }
+
+/* Straight-through router gradient, restating trainer.cpp:140-181 (stage_router_ste; private to the reference's
+ * trainer and not covered by its tests, so this restatement is its oracle). For every token t and each of its
+ * routed experts e (tau row t, kk entries): y = sum over union positions c of expert e (s[c] / esz == e) with
+ * z[t][c] > 0 of z[t][c] * w_b_k[c]; skipped when no such c; dldp = dot(grad_out[t], y) (kernels.hpp:37-41);
+ * grad_g[e] += dldp * h[t] (accumulated in token order); touched[e] = 1. grad_g [n_experts x d] must be zeroed. */
+void or_router_ste(const double* h, const double* z, const double* w_b_k, const int64_t* s, int64_t n_s,
+                   const int64_t* tau, int64_t kk, const double* grad_out, int64_t tokens, int64_t d, int64_t esz,
+                   double* grad_g, int8_t* touched) {
+    double* y = (double*)malloc((size_t)d * sizeof(double));
+    for (int64_t t = 0; t < tokens; ++t) {
+        for (int64_t q = 0; q < kk; ++q) {
+            const int64_t e = tau[t * kk + q];
+            for (int64_t x = 0; x < d; ++x) y[x] = 0.0;
+            int any = 0;
+            for (int64_t c = 0; c < n_s; ++c) {
+                if (s[c] / esz != e) continue;
+                const double a = z[t * n_s + c];
+                if (a <= 0.0) continue;
+                const double* brow = w_b_k + c * d;
+                for (int64_t x = 0; x < d; ++x) y[x] += a * brow[x];
+                any = 1;
+            }
+            if (!any) continue;
+            const double dldp = or_dot(grad_out + t * d, y, d);
+            for (int64_t x = 0; x < d; ++x) grad_g[e * d + x] += dldp * h[t * d + x];
+            touched[e] = 1;
+        }
+    }
+    free(y);
+}

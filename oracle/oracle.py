@@ -206,6 +206,18 @@ def ffn_forward(h, w_a_k, w_b_k, w_in=None, w_out=None, act=0):
     return out, z, pre
 
 
+def router_ste(h, z, w_b_k, s, tau, grad_out, esz, n_experts):
+    """trainer.cpp:140-181 stage_router_ste -> (grad_g [N x d], touched [N] bool)."""
+    h, z, w_b_k, grad_out = map(_f64, (h, z, w_b_k, grad_out))
+    s, tau = _i64(s), _i64(tau)
+    T, d = h.shape
+    gg = np.zeros((n_experts, d))
+    touched = np.zeros(n_experts, np.int8)
+    lib().or_router_ste(_ptr(h), _ptr(z), _ptr(w_b_k), _ptr(s), _I64(len(s)), _ptr(tau), _I64(tau.shape[1]),
+                        _ptr(grad_out), _I64(T), _I64(d), _I64(esz), _ptr(gg), _ptr(touched))
+    return gg, touched.astype(bool)
+
+
 def ffn_backward(grad_out, h, z, base_pre, w_a_k, w_b_k, w_in=None, w_out=None, act=0):
     grad_out, h, z, w_a_k, w_b_k = map(_f64, (grad_out, h, z, w_a_k, w_b_k))
     T, d = h.shape
@@ -355,6 +367,18 @@ class RefStore:
     def save(self, path, extra="{}", step=0):
         """The reference's save_checkpoint (MEFT1) of this store."""
         _check_ref(ref().ref_store_save(_P(self.h), str(path).encode(), extra.encode(), _I64(step)))
+
+    def stage_router_grads(self, layer, rows, grad_rows):
+        rows, grad_rows = _i64(rows), _f64(grad_rows)
+        _check_ref(ref().ref_stage_router_grads(_P(self.h), _I64(layer), _ptr(rows), _I64(len(rows)),
+                                                _ptr(grad_rows)))
+
+    def router(self, layer):
+        """(w_g, m_g, v_g, router_step) of the layer."""
+        w, m, v = (np.empty((self.n, self.d)) for _ in range(3))
+        st = np.empty(self.n, np.int64)
+        _check_ref(ref().ref_store_router(_P(self.h), _I64(layer), _ptr(w), _ptr(m), _ptr(v), _ptr(st)))
+        return w, m, v, st
 
     def sparse_adam(self, layer, lr, beta1=0.9, beta2=0.999, eps=1e-8):
         _check_ref(ref().ref_sparse_adam(_P(self.h), _I64(layer), _D(beta1), _D(beta2), _D(eps), _D(lr)))

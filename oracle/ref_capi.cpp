@@ -228,6 +228,26 @@ void* ref_store_init(int64_t layers, int64_t d, int64_t r, int64_t n, int train_
 
 void ref_store_free(void* s) { delete static_cast<HostStore*>(s); }
 
+// stage_router_grads (memtier.cpp:157-172): stage_g[rows[j]] += grad_rows[j], staged_g = 1.
+int ref_stage_router_grads(void* sp, int64_t layer, const int64_t* rows, int64_t n, const double* grad_rows) {
+    return guard([&] {
+        HostStore& st = *static_cast<HostStore*>(sp);
+        stage_router_grads(st, layer, std::vector<index_t>(rows, rows + n), to_matrix(grad_rows, n, st.dim()));
+    });
+}
+
+// router rows of the layer (memtier.cpp:211-227 state): w_g, m_g, v_g [N x d] and router_step [N]
+int ref_store_router(void* sp, int64_t layer, double* w_g, double* m_g, double* v_g, int64_t* step) {
+    return guard([&] {
+        const HostLayer& hl = static_cast<HostStore*>(sp)->layer(layer);
+        if (w_g) from_matrix(hl.router.w_g, w_g);
+        if (m_g) from_matrix(hl.m_g, m_g);
+        if (v_g) from_matrix(hl.v_g, v_g);
+        if (step)
+            for (size_t i = 0; i < hl.router_step.size(); ++i) step[i] = hl.router_step[i];
+    });
+}
+
 // save_checkpoint (memtier.cpp:288-326) of the reference store, global_step set first.
 int ref_store_save(void* sp, const char* path, const char* extra_json, int64_t step) {
     return guard([&] {

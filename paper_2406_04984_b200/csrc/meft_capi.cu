@@ -1113,7 +1113,7 @@ meft_status meft_sparse_adam_update(meft_ctx* ctx, meft_store* s, int64_t layer,
 static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const void* h, const void* g, int64_t T,
                             const int32_t* uni, int64_t su, int64_t holes, double b1, double b2, double eps,
                             double lr, float* out, float* grad_h, cudaEvent_t g_ready, cudaEvent_t fwd_done,
-                            cudaEvent_t gh_done = nullptr);
+                            cudaEvent_t gh_done = nullptr, const int32_t* tau = nullptr, int64_t kk_eff = 0);
 
 static void ensure_key_stats(meft_ctx* ctx, meft_store* s, int64_t layer);
 
@@ -1135,6 +1135,8 @@ static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
                                         : static_cast<int32_t*>(ctx->get("per_token", size_t(T * take) * 4));
     int32_t* uni = union_user ? union_user : static_cast<int32_t*>(ctx->get("union", size_t(M) * 4));
     int32_t* usize = ctx->dev_small + 4;
+    // the routed experts are kept only when the router trains (its straight-through gradient needs them)
+    int32_t* tau = s->train_router ? static_cast<int32_t*>(ctx->get("tau_step", size_t(T * kk_eff) * 4)) : nullptr;
     const size_t wsb = select_workspace_bytes(T, d, M, N, kk_eff);
     void* ws = ctx->get("select_ws", wsb);
 
@@ -1142,7 +1144,7 @@ static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
     {
         PhaseScope ps(ctx, 0);
         ensure_key_stats(ctx, s, layer);  // cached across steps: the fused Adam refreshes the rows it updates
-        ke_select_device(st, 2, h, L.c_g, L.c_a, T, d, M, N, kk_eff, take, ws, wsb, per_token, nullptr, uni, usize,
+        ke_select_device(st, 2, h, L.c_g, L.c_a, T, d, M, N, kk_eff, take, ws, wsb, per_token, tau, uni, usize,
                          ctx->dev_small + 5, ctx->selection_mode == MEFT_SELECT_AUTO, L.kn, L.kl);
     }
     union_holes(st, uni, usize, usize + 3);
@@ -1150,7 +1152,7 @@ static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
     MEFT_CUDA_CHECK(cudaStreamSynchronize(st));
     const int64_t su = ctx->host_small[4];
     ffn_update_impl(ctx, s, layer, h, g, T, uni, su, ctx->host_small[7], b1, b2, eps, lr, out, grad_h, g_ready,
-                    fwd_done, gh_done);
+                    fwd_done, gh_done, tau, kk_eff);
 
     if (info) {
         info->union_size = su;
@@ -1182,10 +1184,35 @@ static bool use_tma_gather(const meft_ctx* ctx, int64_t su, int64_t holes) {
     return holes >= 0 && holes * 12800 <= su;
 }
 
+// Trainable router (train_router): straight-through gradient (trainer.cpp:140-181, router.cu) staged for the
+// touched experts and applied by the router rows' lazy Adam with their own step counters (memtier.cpp:157-172,
+// 211-227); the bf16 router copy the next selection reads is refreshed by the same kernel.
+static void router_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const uint16_t* h, const uint16_t* act,
+                               const uint16_t* masked, int64_t ld, const int32_t* uni, int64_t su, const int32_t* tau,
+                               int64_t T, int64_t kk, double b1, double b2, double eps, double lr) {
+    const LayerBufs& L = layer_of(s, layer);
+    cudaStream_t st = ctx->stream;
+    const int64_t N = s->experts, d = s->d, E = s->pairs / s->experts;
+    if (su <= 0) return;  // no union: every y_e is empty, nothing is touched
+    PhaseScope ps(ctx, 4);
+    int32_t* lo = static_cast<int32_t*>(ctx->get("rt_lo", size_t(N + 1) * 4));
+    float* dldp = static_cast<float*>(ctx->get("rt_dldp", size_t(T * kk) * 4));
+    uint8_t* live = static_cast<uint8_t*>(ctx->get("rt_live", size_t(T * kk)));
+    float* gg = static_cast<float*>(ctx->get("rt_grad", size_t(N * d) * 4));
+    uint8_t* touched = static_cast<uint8_t*>(ctx->get("rt_touched", size_t(N)));
+    int32_t* rows = static_cast<int32_t*>(ctx->get("rt_rows", size_t(N) * 4));
+    int32_t* bws = static_cast<int32_t*>(ctx->get("rt_bws", size_t((N + 1023) / 1024 + 1) * 4));
+    router_ste_grads(st, uni, su, E, N, act, masked, ld, tau, T, kk, h, d, lo, dldp, live, gg, touched);
+    compact_flags(st, touched, N, rows, ctx->dev_small + 9, bws);
+    adam_mixed(st, rows, ctx->dev_small + 9, 0, d, static_cast<float*>(L.w_g), static_cast<float*>(L.m_g),
+               static_cast<float*>(L.v_g), gg, static_cast<uint16_t*>(L.c_g), nullptr, nullptr, nullptr, nullptr,
+               nullptr, L.rstep, nullptr, b1, b2, eps, lr, 1, true, false);
+}
+
 static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const void* h, const void* g, int64_t T,
                             const int32_t* uni, int64_t su, int64_t holes, double b1, double b2, double eps,
                             double lr, float* out, float* grad_h, cudaEvent_t g_ready, cudaEvent_t fwd_done,
-                            cudaEvent_t gh_done) {
+                            cudaEvent_t gh_done, const int32_t* tau, int64_t kk_eff) {
     const LayerBufs& L = layer_of(s, layer);
     const int64_t d = s->d;
     cudaStream_t st = ctx->stream;
@@ -1229,6 +1256,12 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
     if (g_ready) MEFT_CUDA_CHECK(cudaStreamWaitEvent(st, g_ready, 0));
 
     const bool stats_valid = s->key_stats_valid[size_t(layer)] != 0;
+    require(!s->train_router || tau != nullptr, MEFT_E_LOGIC, "router training runs on the single-GPU layer step");
+    auto train_router = [&] {  // after the backward: it reads act and masked
+        if (s->train_router)
+            router_update_impl(ctx, s, layer, static_cast<const uint16_t*>(h), act, masked, ld, uni, su, tau, T,
+                               kk_eff, b1, b2, eps, lr);
+    };
     if (s->pending[size_t(layer)]) {
         // earlier scatter_grads are pending: sparse_backward + scatter_grads fused, the weight-grad GEMM epilogues
         // add straight into the stage rows at S, then Adam consumes every staged pair (memtier.cpp:187-210)
@@ -1238,6 +1271,7 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
             ffn_backward_impl(ctx, MEFT_BF16, g, h, act, ks, vs, T, d, su, ld, masked, nullptr, nullptr, ghb, false,
                               uni, L.st_a, L.st_b, rg, gh_done);
         }
+        train_router();
         PhaseScope ps(ctx, 4);
         if (su > 0) mark_rows(st, L.staged, uni, nullptr, su);
         adam_impl(ctx, s, layer, b1, b2, eps, lr);
@@ -1251,6 +1285,7 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
             ffn_backward_impl(ctx, MEFT_BF16, g, h, act, ks, vs, T, d, su, ld, masked, gka, gvb, ghb, false, nullptr,
                               nullptr, nullptr, rg, gh_done);
         }
+        train_router();
         PhaseScope ps(ctx, 4);
         if (su > 0)
             adam_mixed(st, uni, nullptr, su, d, static_cast<float*>(L.w_a), static_cast<float*>(L.m_a),
