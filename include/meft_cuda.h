@@ -237,6 +237,11 @@ meft_status meft_store_tensor(meft_store* store, int64_t layer, meft_tensor t, v
 /* HostStore::init(..., train_router=true) (memtier.cpp:86-91): allocate zeroed router moments and step counters
  * for every layer (MEFT_T_M_G / V_G / ROUTER_STEP); idempotent. meft_store_train_router reports the flag. */
 meft_status meft_store_enable_router(meft_ctx* ctx, meft_store* store);
+/* The trainer's expert histogram (trainer.cpp:240): per layer, how often each expert was routed to (one count
+ * per token and selected expert), accumulated on the device by every fused layer step. host_out: int64[N];
+ * reset != 0 clears it after the read. Synchronises. */
+meft_status meft_store_expert_histogram(meft_ctx* ctx, meft_store* store, int64_t layer, int64_t* host_out,
+                                        int reset);
 meft_status meft_store_train_router(const meft_store* store, int* on);
 
 /* ------------------------------------------------------------------ MEFT1 checkpoints (memtier.cpp:288-396)
@@ -327,6 +332,12 @@ typedef struct meft_step_info {
     int gpu_launches;   /* kernels this step launched */
     int rescored;       /* ambiguous candidates re-scored exactly by the certified selection */
     int fallbacks;      /* of those, exact dots that needed the sequential fp64 chain */
+    /* the reference's per-step bookkeeping for this layer, from the step's own selection (no extra sync):
+     * CommMeter (memtier.cpp:56-58, 117-155): fetch 2*d*|S| host->device, scatter 2*d*|S| device->host,
+     * push_hidden T*d; measure_beta (memtier.cpp:14-21) with batch*seq = T; cpu_flops (experts.cpp:119-129). */
+    int64_t meter_h2d, meter_d2h, meter_hidden;
+    double beta_paper, dedup_ratio, activated_fraction;
+    int64_t router_flops, expert_scoring_flops;
 } meft_step_info;
 
 /* One MEFT layer training step in MIXED precision, the trainer's per-layer sequence

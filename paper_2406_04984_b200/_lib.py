@@ -71,6 +71,7 @@ _SIGS = {
     "meft_adam_rows_f64": (INT, [P, P, P, P, P, P, P, P, I64, I64, D, D, D, D]),
     "meft_store_create": (INT, [P, I64, I64, I64, I64, INT, C.POINTER(P)]),
     "meft_store_enable_router": (INT, [P, P]),
+    "meft_store_expert_histogram": (INT, [P, P, I64, P, INT]),
     "meft_store_train_router": (INT, [P, C.POINTER(INT)]),
     "meft_store_save": (INT, [P, P, C.c_char_p, I64, C.c_char_p]),
     "meft_store_load": (INT, [P, C.c_char_p, INT, C.POINTER(P), C.POINTER(CkptHeader), C.c_char_p, C.c_size_t]),
@@ -101,7 +102,9 @@ TENSOR_NAMES = {v: k for k, v in TENSORS.items()}
 
 class StepInfo(C.Structure):
     _fields_ = [("union_size", I64), ("take", I64), ("kk_eff", I64), ("warned", INT), ("gpu_launches", INT),
-                ("rescored", INT), ("fallbacks", INT)]
+                ("rescored", INT), ("fallbacks", INT), ("meter_h2d", I64), ("meter_d2h", I64),
+                ("meter_hidden", I64), ("beta_paper", D), ("dedup_ratio", D), ("activated_fraction", D),
+                ("router_flops", I64), ("expert_scoring_flops", I64)]
 
 
 class MeftError(RuntimeError):

@@ -106,6 +106,7 @@ struct LayerBufs {
     void* v_g = nullptr;
     int32_t* rstep = nullptr;
     void* router_base = nullptr;
+    int64_t* ehist = nullptr;  // [N] routed-token counts per expert (trainer.cpp:240), accumulated by the step
 };
 
 }  // namespace
@@ -858,6 +859,7 @@ meft_status meft_store_create(meft_ctx* ctx, int64_t layers, int64_t d, int64_t 
         auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
         size_t bytes = 6 * al(pd * mb) + al(nd * mb) + al(size_t(pairs) * 4) + al(size_t(pairs));
         if (precision == MEFT_STORE_MIXED) bytes += 2 * al(pd * 2) + al(nd * 2) + 2 * al(size_t(pairs) * 4);
+        bytes += al(size_t(experts) * 8);
         for (int64_t l = 0; l < layers; ++l) {
             LayerBufs L;
             cudaError_t e = cudaMalloc(&L.base, bytes);
@@ -883,6 +885,7 @@ meft_status meft_store_create(meft_ctx* ctx, int64_t layers, int64_t d, int64_t 
             L.w_g = take(nd * mb);
             L.step = static_cast<int32_t*>(take(size_t(pairs) * 4));
             L.staged = static_cast<uint8_t*>(take(size_t(pairs)));
+            L.ehist = static_cast<int64_t*>(take(size_t(experts) * 8));
             if (precision == MEFT_STORE_MIXED) {
                 L.c_a = take(pd * 2);
                 L.c_b = take(pd * 2);
@@ -936,6 +939,18 @@ meft_status meft_store_enable_router(meft_ctx* ctx, meft_store* s) {
         }
         MEFT_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
         s->train_router = true;
+    });
+}
+
+meft_status meft_store_expert_histogram(meft_ctx* ctx, meft_store* s, int64_t layer, int64_t* host_out, int reset) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        const LayerBufs& L = layer_of(s, layer);
+        if (host_out)
+            MEFT_CUDA_CHECK(cudaMemcpyAsync(host_out, L.ehist, size_t(s->experts) * 8, cudaMemcpyDeviceToHost,
+                                            ctx->stream));
+        if (reset) MEFT_CUDA_CHECK(cudaMemsetAsync(L.ehist, 0, size_t(s->experts) * 8, ctx->stream));
+        MEFT_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     });
 }
 
@@ -1135,8 +1150,8 @@ static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
                                         : static_cast<int32_t*>(ctx->get("per_token", size_t(T * take) * 4));
     int32_t* uni = union_user ? union_user : static_cast<int32_t*>(ctx->get("union", size_t(M) * 4));
     int32_t* usize = ctx->dev_small + 4;
-    // the routed experts are kept only when the router trains (its straight-through gradient needs them)
-    int32_t* tau = s->train_router ? static_cast<int32_t*>(ctx->get("tau_step", size_t(T * kk_eff) * 4)) : nullptr;
+    // the routed experts: expert histogram, and the router's straight-through gradient when it trains
+    int32_t* tau = static_cast<int32_t*>(ctx->get("tau_step", size_t(T * kk_eff) * 4));
     const size_t wsb = select_workspace_bytes(T, d, M, N, kk_eff);
     void* ws = ctx->get("select_ws", wsb);
 
@@ -1147,12 +1162,13 @@ static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
         ke_select_device(st, 2, h, L.c_g, L.c_a, T, d, M, N, kk_eff, take, ws, wsb, per_token, tau, uni, usize,
                          ctx->dev_small + 5, ctx->selection_mode == MEFT_SELECT_AUTO, L.kn, L.kl);
     }
+    histogram_add(st, tau, T * kk_eff, L.ehist);
     union_holes(st, uni, usize, usize + 3);
     MEFT_CUDA_CHECK(cudaMemcpyAsync(ctx->host_small + 4, usize, 16, cudaMemcpyDeviceToHost, st));
     MEFT_CUDA_CHECK(cudaStreamSynchronize(st));
     const int64_t su = ctx->host_small[4];
     ffn_update_impl(ctx, s, layer, h, g, T, uni, su, ctx->host_small[7], b1, b2, eps, lr, out, grad_h, g_ready,
-                    fwd_done, gh_done, tau, kk_eff);
+                    fwd_done, gh_done, s->train_router ? tau : nullptr, kk_eff);
 
     if (info) {
         info->union_size = su;
@@ -1162,6 +1178,14 @@ static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
         info->gpu_launches = int(launch_counter() - launches0);
         info->rescored = ctx->host_small[5];
         info->fallbacks = ctx->host_small[6];
+        info->meter_h2d = 2 * d * su;
+        info->meter_d2h = 2 * d * su;
+        info->meter_hidden = T * d;
+        info->beta_paper = double(su) / double(k);
+        info->dedup_ratio = double(su) / double(T * k);
+        info->activated_fraction = double(su) / double(M);
+        info->router_flops = T * N * d;
+        info->expert_scoring_flops = T * kk * (M / N) * d;
     }
 }
 

@@ -353,6 +353,18 @@ __global__ void k_union_holes_n(const int32_t* __restrict__ idx, int n, int32_t*
     *out = n > 0 ? idx[n - 1] - idx[0] + 1 - n : 0;
 }
 
+__global__ void k_hist_add(const int32_t* __restrict__ idx, int n, unsigned long long* __restrict__ hist) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        atomicAdd(hist + idx[i], 1ull);
+}
+
+void histogram_add(cudaStream_t st, const int32_t* idx, int64_t n, int64_t* hist) {
+    if (n <= 0) return;
+    k_hist_add<<<int(std::min<int64_t>((n + 255) / 256, 1184)), 256, 0, st>>>(
+        idx, int(n), reinterpret_cast<unsigned long long*>(hist));
+    check_launch("k_hist_add");
+}
+
 void union_holes(cudaStream_t st, const int32_t* idx, const int32_t* n_dev, int32_t* out) {
     k_union_holes<<<1, 1, 0, st>>>(idx, n_dev, out);
     check_launch("k_union_holes");

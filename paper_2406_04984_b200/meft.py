@@ -261,6 +261,13 @@ class Store:
         """save_checkpoint (MEFT1, memtier.cpp:288-326) of this HBM store."""
         self.ctx.check(lib().meft_store_save(self.ctx.h, self.h, str(path).encode(), step, extra.encode()))
 
+    def expert_histogram(self, layer, reset=False):
+        """Routed-token counts per expert accumulated by the fused steps (trainer.cpp:240)."""
+        out = np.empty(self.experts, np.int64)
+        self.ctx.check(lib().meft_store_expert_histogram(self.ctx.h, self.h, layer, out.ctypes.data_as(P),
+                                                         int(reset)))
+        return out
+
     def enable_router(self):
         """train_router state (m_g, v_g, router_step) for every layer."""
         self.ctx.check(lib().meft_store_enable_router(self.ctx.h, self.h))
@@ -341,8 +348,8 @@ class Store:
         info = _lib.StepInfo()
         self.ctx.check(lib().meft_layer_step(self.ctx.h, self.h, layer, _p(h), _p(grad_out), T, kk, k, beta1, beta2,
                                              eps, lr, _p(out), _p(grad_h), _p(per), _p(uni), C.byref(info)))
-        res = dict(union_size=info.union_size, take=info.take, kk_eff=info.kk_eff, warned=bool(info.warned),
-                   gpu_launches=info.gpu_launches, rescored=info.rescored, fallbacks=info.fallbacks)
+        res = {name: getattr(info, name) for name, _ in _lib.StepInfo._fields_}
+        res["warned"] = bool(info.warned)
         if want_selection:
             res["per_token"] = per
             res["unioned"] = uni[: info.union_size]

@@ -186,3 +186,22 @@ def test_fused_adam_keeps_key_statistics_current(ctx):
     exact = keys.double().norm(dim=1)
     assert bool((kn.double() >= exact).all())
     assert float((kn.double() / fn.double() - 1).abs().max()) < 1e-6
+
+
+def test_step_bookkeeping_and_expert_histogram(ctx):
+    """The reference trainer's per-step bookkeeping from the fused step: expert histogram (trainer.cpp:240) equal to
+    the oracle's routing counts, accumulated across steps; measure_beta / CommMeter / cpu_flops formulas."""
+    d, M, N, K, T, kk = 512, 4096, 64, 32, 256, 4
+    w_a, w_g, w_b, h, gr = cfg1_inputs(d, M, N, T)
+    st = make_store(ctx, w_a, w_g, w_b, N)
+    sel = O.ke_select(h, w_g, w_a, kk, K)
+    info = st.layer_step(0, bf16_dev(h), bf16_dev(gr), kk, K, 0.0)  # lr 0: the selection repeats exactly
+    st.layer_step(0, bf16_dev(h), bf16_dev(gr), kk, K, 0.0)
+    want = np.bincount(sel["tau"].ravel(), minlength=N)
+    np.testing.assert_array_equal(st.expert_histogram(0, reset=True), 2 * want)
+    np.testing.assert_array_equal(st.expert_histogram(0), np.zeros(N, np.int64))
+    s = len(sel["unioned"])
+    assert info["union_size"] == s
+    assert (info["meter_h2d"], info["meter_d2h"], info["meter_hidden"]) == (2 * d * s, 2 * d * s, T * d)
+    assert info["beta_paper"] == s / K and info["dedup_ratio"] == s / (T * K) and info["activated_fraction"] == s / M
+    assert (info["router_flops"], info["expert_scoring_flops"]) == (T * N * d, T * kk * (M // N) * d)
