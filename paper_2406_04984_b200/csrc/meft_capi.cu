@@ -2,6 +2,8 @@
 // Host orchestration only: every numeric step is a kernel in gemm_sm100.cu / select.cu / stream_ops.cu /
 // dgemm.cu. There is no CPU compute path.
 #include <cmath>
+#include <functional>
+#include <optional>
 #include <cstring>
 #include <memory>
 #include <random>
@@ -294,7 +296,7 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
                        const void* values_s, int64_t T, int64_t d, int64_t s, int64_t ld_z, void* masked,
                        void* grad_keys_s, void* grad_values_s, void* grad_h, bool acc_h, const int32_t* S_rows,
                        void* stage_keys, void* stage_values, const RowGather& rg = RowGather(),
-                       cudaEvent_t grad_h_done = nullptr) {
+                       cudaEvent_t grad_h_done = nullptr, const std::function<void()>* between = nullptr) {
     cudaStream_t st = ctx->stream;
     if (dt == MEFT_F64) {
         const double* gd = static_cast<const double*>(g);
@@ -357,6 +359,7 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
     }
     e4.ldc = d;
     gemm_bf16(st, s, d, T, GemmOperand{z, ld_z, true}, GemmOperand{g, d, true}, e4);
+    if (between) (*between)();  // e.g. consume grad_values before grad_keys reuses its buffer
     GemmEpilogue e5 = e4;  // grad_keys = masked^T h
     e5.c = S_rows ? stage_keys : grad_keys_s;
     gemm_bf16(st, s, d, T, GemmOperand{masked, ld_z, true}, GemmOperand{h, d, true}, e5);
@@ -1301,22 +1304,31 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
         adam_impl(ctx, s, layer, b1, b2, eps, lr);
     } else {
         // staging is all zero, so staged == S exactly: the weight grads go to a dense [|S| x d] step block that
-        // Adam reads in place of the staging rows (same values, no staging traffic, nothing to zero)
-        float* gka = static_cast<float*>(ctx->get("step_gka", size_t(std::max<int64_t>(su, 1) * d) * 4));
-        float* gvb = static_cast<float*>(ctx->get("step_gvb", size_t(std::max<int64_t>(su, 1) * d) * 4));
-        {
-            PhaseScope ps(ctx, 3);
-            ffn_backward_impl(ctx, MEFT_BF16, g, h, act, ks, vs, T, d, su, ld, masked, gka, gvb, ghb, false, nullptr,
-                              nullptr, nullptr, rg, gh_done);
-        }
-        train_router();
-        PhaseScope ps(ctx, 4);
-        if (su > 0)
+        // Adam reads in place of the staging rows (same values, no staging traffic, nothing to zero). ONE block
+        // serves both tables: the value rows are updated right after their gradient GEMM (no counter bump), then
+        // the key gradient overwrites the block and the key rows are updated with the shared step counter.
+        float* gblk = static_cast<float*>(ctx->get("step_grad", size_t(std::max<int64_t>(su, 1) * d) * 4));
+        auto adam_table = [&](int table) {
+            PhaseScope p4(ctx, 4);
+            const bool keys = table == 1;
             adam_mixed(st, uni, nullptr, su, d, static_cast<float*>(L.w_a), static_cast<float*>(L.m_a),
-                       static_cast<float*>(L.v_a), gka, static_cast<uint16_t*>(L.c_a), static_cast<float*>(L.w_b),
-                       static_cast<float*>(L.m_b), static_cast<float*>(L.v_b), gvb, static_cast<uint16_t*>(L.c_b),
-                       L.step, nullptr, b1, b2, eps, lr, 3, true, true, stats_valid ? L.kn : nullptr,
-                       stats_valid ? L.kl : nullptr);
+                       static_cast<float*>(L.v_a), gblk, static_cast<uint16_t*>(L.c_a), static_cast<float*>(L.w_b),
+                       static_cast<float*>(L.m_b), static_cast<float*>(L.v_b), gblk, static_cast<uint16_t*>(L.c_b),
+                       L.step, nullptr, b1, b2, eps, lr, table, keys, true, keys && stats_valid ? L.kn : nullptr,
+                       keys && stats_valid ? L.kl : nullptr);
+        };
+        std::optional<PhaseScope> p3;
+        p3.emplace(ctx, 3);
+        const std::function<void()> values_step = [&] {
+            p3.reset();
+            if (su > 0) adam_table(2);
+            p3.emplace(ctx, 3);
+        };
+        ffn_backward_impl(ctx, MEFT_BF16, g, h, act, ks, vs, T, d, su, ld, masked, gblk, gblk, ghb, false, nullptr,
+                          nullptr, nullptr, rg, gh_done, &values_step);
+        p3.reset();
+        train_router();
+        if (su > 0) adam_table(1);
         return;  // key statistics stay valid (refreshed for exactly the rows that changed)
     }
     s->key_stats_valid[size_t(layer)] = 0;
