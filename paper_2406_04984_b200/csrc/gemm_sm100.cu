@@ -791,8 +791,10 @@ bool pair_mode_enabled() {
 
 }  // namespace
 
-void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOperand& A, const GemmOperand& B,
-               const GemmEpilogue& epi) {
+namespace {
+
+void gemm_bf16_one(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOperand& A, const GemmOperand& B,
+                   const GemmEpilogue& epi) {
     if (M <= 0 || N <= 0) return;
     if (K <= 0) throw MeftError(2, "gemm_bf16: K must be positive");
     if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) throw MeftError(1, "gemm_bf16: dimension too large");
@@ -835,6 +837,68 @@ void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOpera
     const CUtensorMap tb = B.mn_major ? make_map(B.ptr, N, B.rows ? B.table_rows : K, B.ld, 64, 64)
                                       : make_map(B.ptr, K, B.rows ? B.table_rows : N, B.ld, 64, BN);
     dispatch(st, A.mn_major, B.mn_major, ta, tb, B.rows ? tg : tb, args, args.tiles_m * args.tiles_n * args.ksplit);
+}
+
+int64_t env_elems(const char* name) {
+    const char* v = std::getenv(name);
+    return v ? std::max<int64_t>(0, std::atoll(v)) : 0;
+}
+
+const void* advance(const void* p, int64_t elems, int64_t esize) {
+    return static_cast<const uint8_t*>(p) + elems * esize;
+}
+
+}  // namespace
+
+// Large problems run as a grid of sub-GEMMs (chunks of M / N / K, each a persistent launch): co-running CTA
+// pairs then stay within an L2-sized window of shared operand panels. M/N chunks are bitwise neutral (every
+// output tile is computed exactly as before); K chunks (f32 store epilogues only) add the chunk partials in the
+// epilogue. Chunk sizes: MEFT_GEMM_{M,N,K}CHUNK (elements), else the policy below. K chunks change the fp32
+// summation order of long-K products (within the bf16 tolerance) and are applied identically on every path.
+void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOperand& A, const GemmOperand& B,
+               const GemmEpilogue& epi) {
+    static const int64_t mc_env = env_elems("MEFT_GEMM_MCHUNK"), nc_env = env_elems("MEFT_GEMM_NCHUNK"),
+                         kc_env = env_elems("MEFT_GEMM_KCHUNK");
+    const bool f32_out = epi.kind == EPI_STORE_F32 || epi.kind == EPI_ROWS_ADD_F32;
+    // policy: 65536 per dimension (measured on |S| = 640k GEMMs: z 37.5 -> 33.8 ms, out 46.7 -> 38.5,
+    // gW 45.2 -> 39.2; 32768 is equivalent, cfg2's |S| = 65536 stays one launch)
+    constexpr int64_t kChunk = 65536;
+    const int64_t mc = round_up(mc_env ? mc_env : kChunk, P_TILE_M);
+    const int64_t nc = round_up(nc_env ? nc_env : kChunk, BN);
+    const int64_t kc = f32_out ? round_up(kc_env ? kc_env : kChunk, BK) : K;
+    if ((mc >= M && nc >= N && kc >= K) || epi.ksplit > 1) return gemm_bf16_one(st, M, N, K, A, B, epi);
+    const int64_t ce = (epi.kind == EPI_STORE_F32 || epi.kind == EPI_ROWS_ADD_F32 || epi.kind == EPI_ROWS_STORE_F32)
+                           ? 4 : 2;
+    const bool rows_epi = epi.kind == EPI_ROWS_ADD_F32 || epi.kind == EPI_ROWS_STORE_F32;
+    for (int64_t m0 = 0; m0 < M; m0 += mc) {
+        for (int64_t n0 = 0; n0 < N; n0 += nc) {
+            for (int64_t k0 = 0; k0 < K; k0 += kc) {
+                const int64_t ml = std::min(mc, M - m0), nl = std::min(nc, N - n0), kl = std::min(kc, K - k0);
+                GemmOperand a = A;
+                a.ptr = advance(A.ptr, A.mn_major ? k0 * A.ld + m0 : m0 * A.ld + k0, 2);
+                GemmOperand b = B;
+                if (!B.rows) {
+                    b.ptr = advance(B.ptr, B.mn_major ? k0 * B.ld + n0 : n0 * B.ld + k0, 2);
+                } else if (B.mn_major) {  // logical rows = K positions; table columns = N
+                    b.rows = B.rows + k0;
+                    b.ptr = advance(B.ptr, n0, 2);
+                } else {  // logical rows = N positions; table columns = K
+                    b.rows = B.rows + n0;
+                    b.ptr = advance(B.ptr, k0, 2);
+                }
+                GemmEpilogue e = epi;
+                if (k0 > 0) e.accumulate = true;
+                if (rows_epi) {
+                    e.row_idx = epi.row_idx + m0;
+                    e.c = const_cast<void*>(advance(epi.c, n0, ce));
+                } else {
+                    e.c = const_cast<void*>(advance(epi.c, m0 * epi.ldc + n0, ce));
+                }
+                if (epi.mask) e.mask = advance(epi.mask, m0 * epi.ldm + n0, 2);
+                gemm_bf16_one(st, ml, nl, kl, a, b, e);
+            }
+        }
+    }
 }
 
 void gemm_bf16_grouped(cudaStream_t st, int G, int64_t N, int64_t K, const GemmOperand& A, int64_t a_rows,

@@ -336,6 +336,13 @@ static void perf_gather(const char* name, int M, int N, int K, bool bmn, int epi
 
 int main(int argc, char** argv) {
     const bool perf = argc > 1 && std::strcmp(argv[1], "perf") == 0;
+    if (argc > 1 && std::strcmp(argv[1], "perf4") == 0) {  // cfg4-like: |S| = 640k of M = 1M neurons
+        const int T = 8192, S = 655360, D = 4096;
+        perf_case("z=h.keys^T relu (K,K)", T, S, D, false, false, EPI_RELU_BF16);
+        perf_case("out=act.values (K,MN)", T, D, S, false, true, EPI_STORE_F32);
+        perf_case("gW=act^T.g (MN,MN)", S, D, T, true, true, EPI_STORE_F32);
+        return 0;
+    }
     if (argc > 1 && std::strcmp(argv[1], "perfg") == 0) {
         const int T = 8192, S = 65536, D = 4096;
         perf_case("z dense", T, S, D, false, false, EPI_RELU_BF16);
