@@ -154,7 +154,7 @@ def reference_arm(args, rank, world):
     try:
         tps, sec, phases, cores = run_reference_sample(args.steps, args.warmup, tokens)
     except Exception as e:  # pragma: no cover - surfaced as unavailable, never as a fake number
-        print(json.dumps({"impl": "reference", "unavailable": f"reference CPU run failed: {e}"}))
+        emit({"impl": "reference", "unavailable": f"reference CPU run failed: {e}"})
         return
     sample = (f"reference ref_layer_step (meft_ffn->sparse_backward->scatter_grads->sparse_adam_update) on the "
               f"cfg2 tables d={CFG['d']} M={CFG['pairs']} N={CFG['experts']} K={CFG['k']} kk={CFG['kk']}, "
@@ -171,7 +171,7 @@ def reference_arm(args, rank, world):
         "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "phase_seconds": dict(zip(["select", "fetch", "forward", "backward", "scatter", "adam"], phases)),
     }
-    print(json.dumps(line))
+    emit(line)
 
 
 # ----------------------------------------------------------------------------------------------- our arm
@@ -365,10 +365,30 @@ def our_arm(args, rank, world, local_rank):
         "clocks": clocks.summary(),
         "gpu_launches": launches,
     }
-    print(json.dumps(line))
+    emit(line)
+
+
+# The JSON line is the only thing on stdout: everything else written to fd 1 (NCCL's version banner, library
+# prints) is redirected to stderr, and the line goes to a saved copy of the original stdout.
+_JSON_OUT = None
+
+
+def _claim_stdout():
+    global _JSON_OUT
+    if _JSON_OUT is None:
+        sys.stdout.flush()
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(line):
+    _claim_stdout()
+    _JSON_OUT.write(json.dumps(line) + "\n")
+    _JSON_OUT.flush()
 
 
 def main():
+    _claim_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)

@@ -299,7 +299,8 @@ meft_status meft_row_stats(meft_ctx* ctx, const uint16_t* rows, int64_t n, int64
 /* owner rank: the same statistics for the layer's local keys (cached until the next update of the keys). */
 meft_status meft_store_key_stats(meft_ctx* ctx, meft_store* store, int64_t layer, float* norms, int32_t* minlsb);
 /* owner rank: approximate tcgen05 scores of R dispatched token rows against all E keys of their local expert
- * (expert_local[r] in [0, N/P)): cand [R x E] fp32. */
+ * (expert_local[r] in [0, N/P)): cand [R x E] fp32 = float(fp64 sum of the K-chunk partial products) -- the
+ * same approximation the fused selection classifies, and the one meft_topk_classify's bound is stated for. */
 meft_status meft_score_candidates(meft_ctx* ctx, meft_store* store, int64_t layer, const uint16_t* rows,
                                   const int32_t* expert_local, int64_t R, float* cand);
 /* owner rank: the reference's exact fp64 scores dot(rows[pair_row[q]], key[pair_key[q]]) of Q pairs. */

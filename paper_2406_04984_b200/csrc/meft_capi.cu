@@ -1383,7 +1383,7 @@ meft_status meft_score_candidates(meft_ctx* ctx, meft_store* s, int64_t layer, c
         require(s->prec == MEFT_STORE_MIXED && s->d % 8 == 0, MEFT_E_INVALID, "score_candidates: MIXED store, d % 8");
         const int64_t E = s->pairs / s->experts;
         require(E % 4 == 0, MEFT_E_INVALID, "score_candidates: expert size must be a multiple of 4");
-        void* ws = ctx->get("score_ws", score_workspace_bytes(R, s->d, s->experts));
+        void* ws = ctx->get("score_ws", score_workspace_bytes(R, s->d, s->experts, E));
         score_candidates(ctx->stream, rows, expert_local, R, s->d, static_cast<const uint16_t*>(L.c_a), s->experts, E,
                          ws, cand);
     });

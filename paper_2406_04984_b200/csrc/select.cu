@@ -435,6 +435,22 @@ int cert_ksplit(int64_t d) {
     return int(std::max<int64_t>(1, std::min<int64_t>(4, d / 1024)));  // 1024-wide chunks: measured best
 }
 
+// K-chunking of the candidate-scoring GEMM and the certified bound that goes with it, shared by the fused
+// selection (partials summed inside the classifier) and the sharded protocol (partials summed by the owner):
+// both compare float(fp64 sum of the chunk partials) against the same bound.
+struct CertSplit {
+    int ks;       // chunks actually launched (no empty ones)
+    int64_t kbs;  // k-blocks per chunk
+    double cb;    // bound coefficient for float(sum of partials)
+};
+CertSplit cert_split(int64_t d, bool allow) {
+    const int req = allow ? cert_ksplit(d) : 1;
+    const int64_t nkb = (d + 63) / 64, kbs = (nkb + req - 1) / req;
+    const int ks = int((nkb + kbs - 1) / kbs);
+    const double cb = ks > 1 ? cert_bound_coeff_split(int(d), int(kbs * 64), ks) : cert_bound_coeff(int(d));
+    return CertSplit{ks, kbs, cb};
+}
+
 size_t cert_workspace_bytes(int64_t T, int64_t d, int64_t M, int64_t N, int64_t kk_eff) {
     const int64_t E = M / N;
     size_t b = 0;
@@ -583,9 +599,10 @@ static void ke_select_certified(cudaStream_t st, const void* h_, const void* w_g
     const int P2 = next_pow2(int(C)), TP2 = next_pow2(int(take));
     const size_t csm = size_t(C) * 9 + 16;  // classify: u32 keys + f32 scores + u8 membership
     if (csm > 200 * 1024) throw MeftError(2, "ke_select: candidate set too large for the certified path");
-    // the split GEMM really used kb_split*64-wide chunks (no empty splits): recompute them exactly like base_args
-    const int64_t nkb = (d + 63) / 64, kbs = (nkb + ksplit - 1) / ksplit, ks_eff = (nkb + kbs - 1) / kbs;
-    const double cbk = ksplit > 1 ? cert_bound_coeff_split(int(d), int(kbs * 64), int(ks_eff)) : cb;
+    // the split GEMM really used kb_split*64-wide chunks (no empty splits): the same arithmetic as base_args
+    const CertSplit cs = cert_split(d, ksplit > 1);
+    const int ks_eff = cs.ks;
+    const double cbk = cs.cb;
     static bool cattr = false;
     if (!cattr) {
         MEFT_CUDA_CHECK(cudaFuncSetAttribute(k_topk_classify, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -787,13 +804,22 @@ void route_certified(cudaStream_t st, const uint16_t* h, const uint16_t* w_g, in
     check_launch("k_router_certified");
 }
 
-size_t score_workspace_bytes(int64_t R, int64_t d, int64_t n_experts) {
+size_t score_workspace_bytes(int64_t R, int64_t d, int64_t n_experts, int64_t E) {
     size_t b = 0;
     auto add = [&](size_t x) { b += (x + 255) & ~size_t(255); };
     add((n_experts + 1) * 4 * 4);
     add(R * 4);
     add(R * d * 2);
+    add(R * E * 4 * cert_split(d, true).ks);  // K-split partial scores
     return b;
+}
+
+__global__ void k_sum_partials(const float* __restrict__ part, int ks, int64_t n, float* __restrict__ out) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        double s = 0.0;
+        for (int p = 0; p < ks; ++p) s += double(part[p * n + i]);
+        out[i] = float(s);
+    }
 }
 
 void score_candidates(cudaStream_t st, const uint16_t* rows, const int32_t* expert, int64_t R, int64_t d,
@@ -821,13 +847,24 @@ void score_candidates(cudaStream_t st, const uint16_t* rows, const int32_t* expe
     k_gather_tokens<<<std::max(1, std::min(int(R / 8 + 1), num_sms() * 16)), 256, 0, st>>>(rows, int(d), entries,
                                                                                            int(R), 1, hs);
     check_launch("k_gather_tokens");
+    // K-split exactly like the fused selection; the owner returns float(fp64 sum of the partials), which the home
+    // classifies against cert_split(d).cb (topk_classify)
+    const CertSplit cs = cert_split(d, true);
+    float* part = cs.ks > 1 ? static_cast<float*>(take_buf(R * E * 4 * cs.ks)) : cand;
     GemmEpilogue eg;
     eg.kind = EPI_ROWS_STORE_F32;
-    eg.c = cand;
+    eg.c = part;
     eg.ldc = E;
     eg.row_idx = entries;
+    eg.ksplit = cs.ks;
+    eg.split_stride = R * E;
     gemm_bf16_grouped(st, int(n_experts), E, d, GemmOperand{hs, d, false}, R, GemmOperand{keys, d, false},
                       n_experts * E, off, tile_off, eg);
+    if (cs.ks > 1) {
+        k_sum_partials<<<int(std::min<int64_t>((R * E + 255) / 256, num_sms() * 8)), 256, 0, st>>>(part, cs.ks, R * E,
+                                                                                                  cand);
+        check_launch("k_sum_partials");
+    }
 }
 
 void exact_pair_scores(cudaStream_t st, const uint16_t* rows, const float* rn, const int32_t* rl,
@@ -851,7 +888,7 @@ void topk_classify(cudaStream_t st, const float* cand, const int32_t* tau, int64
         cattr = true;
     }
     k_topk_classify<<<int(T), 256, csm, st>>>(cand, tau, int(kk), int(E), int(C), next_pow2(int(C)), int(take), hn, kn,
-                                              cert_bound_coeff(int(d)), sure, n_sure, amb, n_amb, amb_count_per_expert,
+                                              cert_split(d, true).cb, sure, n_sure, amb, n_amb, amb_count_per_expert,
                                               1, 0);
     check_launch("k_topk_classify");
 }

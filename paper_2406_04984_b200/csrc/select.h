@@ -39,7 +39,7 @@ size_t route_workspace_bytes(int64_t T, int64_t d, int64_t N);
 void route_certified(cudaStream_t st, const uint16_t* h, const uint16_t* w_g, int64_t T, int64_t d, int64_t N,
                      int64_t kk_eff, void* ws, int32_t* tau, int32_t* stats);
 // approximate scores of R token rows against the E keys of their (local) expert: cand [R x E] fp32.
-size_t score_workspace_bytes(int64_t R, int64_t d, int64_t n_experts);
+size_t score_workspace_bytes(int64_t R, int64_t d, int64_t n_experts, int64_t E);
 void score_candidates(cudaStream_t st, const uint16_t* rows, const int32_t* expert, int64_t R, int64_t d,
                       const uint16_t* keys, int64_t n_experts, int64_t E, void* ws, float* cand);
 // exact reference scores of Q (row, key) pairs
