@@ -264,16 +264,27 @@ def our_arm(args, rank, world, local_rank):
     out_host = torch.empty((T, d), dtype=torch.float32).pin_memory()
     gh_host = torch.empty((T, d), dtype=torch.float32).pin_memory()
     e2e_steps = max(3, min(args.steps, 10))
+    copy_stream = torch.cuda.Stream(device=dev)
+    g_ev = torch.cuda.Event()
 
     def e2e_step():
         if not sharded:  # one C-ABI call: copies overlapped with the step inside meft_layer_step_host
             store.layer_step_host(0, h_host, g_host, kk, K, lr, out_host, gh_host)
-        else:
+        else:  # h first; g, out and grad_h move on a copy stream while the step computes
             h.copy_(h_host, non_blocking=True)
-            g.copy_(g_host, non_blocking=True)
-            step()
-            out_host.copy_(out, non_blocking=True)
-            gh_host.copy_(grad_h, non_blocking=True)
+            with torch.cuda.stream(copy_stream):
+                g.copy_(g_host, non_blocking=True)
+                g_ev.record(copy_stream)
+            res = layer.step(h, g, kk, K, lr, g_ready=g_ev)
+            ready = [res.get("out_ready"), res.get("grad_h_ready")]
+            for dst, src, ev in ((out_host, res["out"], ready[0]), (gh_host, res["grad_h"], ready[1])):
+                if ev is not None:
+                    copy_stream.wait_event(ev)
+                else:
+                    copy_stream.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(copy_stream):
+                    dst.copy_(src, non_blocking=True)
+                src.record_stream(copy_stream)
             torch.cuda.synchronize()
 
     e2e_step()

@@ -118,6 +118,9 @@ meft_status meft_ctx_set_selection(meft_ctx* ctx, int mode);
 #define MEFT_GATHER_KERNEL 1
 #define MEFT_GATHER_TMA 2
 meft_status meft_ctx_set_gather(meft_ctx* ctx, int mode);
+/* Keep `sms` SMs free of the persistent tcgen05 GEMMs (process-wide; 0 = all SMs). The expert-sharded step sets it
+ * while collectives are meant to overlap its FFN: NCCL's kernels need SMs of their own to make progress. */
+meft_status meft_set_gemm_sm_reserve(int sms);
 meft_status meft_ctx_read_timing(meft_ctx* ctx, double* ms5, int64_t* launches5);
 
 meft_status meft_device_alloc(meft_ctx* ctx, size_t bytes, void** out);
@@ -318,10 +321,14 @@ meft_status meft_topk_finalize(meft_ctx* ctx, const int32_t* sure, const int32_t
                                int32_t* per_token, uint8_t* union_flags);
 /* owner rank: the FFN of ALL T (all-gathered) tokens against its local part of the union (S_local: ascending local
  * pair ids), the fused scatter, and the lazy Adam of those pairs. out/grad_h are this shard's partial sums
- * [T x d] fp32 (to be reduce-scattered). */
+ * [T x d] fp32 (to be reduce-scattered).
+ * Overlap hooks (cudaEvent_t, each may be NULL): the backward waits for g_ready (e.g. the grad_out all-gather
+ * on a communication stream); fwd_done is recorded once out_partial is final, grad_h_done once grad_h_partial
+ * is, so their reduce-scatters can run while the rest of the step computes. */
 meft_status meft_layer_ffn_local(meft_ctx* ctx, meft_store* store, int64_t layer, const uint16_t* h_all,
                                  const uint16_t* g_all, int64_t T, const int32_t* S_local, int64_t s, double beta1,
-                                 double beta2, double eps, double lr, float* out_partial, float* grad_h_partial);
+                                 double beta2, double eps, double lr, float* out_partial, float* grad_h_partial,
+                                 void* g_ready, void* fwd_done, void* grad_h_done);
 
 /* ------------------------------------------------------------------ whole layer step */
 

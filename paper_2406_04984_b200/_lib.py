@@ -42,10 +42,11 @@ _SIGS = {
     "meft_exact_scores": (INT, [P, P, I64, P, I64, P, P, I64, P]),
     "meft_topk_classify": (INT, [P, P, P, I64, I64, I64, I64, I64, P, P, P, P, P, P]),
     "meft_topk_finalize": (INT, [P, P, P, P, P, P, I64, I64, I64, P, P]),
-    "meft_layer_ffn_local": (INT, [P, P, I64, P, P, I64, P, I64, D, D, D, D, P, P]),
+    "meft_layer_ffn_local": (INT, [P, P, I64, P, P, I64, P, I64, D, D, D, D, P, P, P, P, P]),
     "meft_ctx_set_timing": (INT, [P, INT]),
     "meft_ctx_set_selection": (INT, [P, INT]),
     "meft_ctx_set_gather": (INT, [P, INT]),
+    "meft_set_gemm_sm_reserve": (INT, [INT]),
     "meft_ctx_read_timing": (INT, [P, P, P]),
     "meft_device_alloc": (INT, [P, C.c_size_t, C.POINTER(P)]),
     "meft_device_free": (INT, [P, P]),

@@ -9,6 +9,7 @@
 // MEFT layer read their operands in place with no transposes.
 #include <cudaTypedefs.h>
 
+#include <atomic>
 #include <mutex>
 
 #include "common.cuh"
@@ -681,6 +682,11 @@ CUtensorMap make_map(const void* base, int64_t inner, int64_t outer, int64_t ld,
     return m;
 }
 
+// SMs the persistent GEMMs may occupy. A communication-overlapped caller reserves a few for concurrently running
+// NCCL kernels, which otherwise only get an SM once a whole chain of persistent GEMMs has drained.
+std::atomic<int> g_reserved_sms{0};
+int gemm_sms() { return std::max(2, num_sms() - g_reserved_sms.load(std::memory_order_relaxed)); }
+
 template <bool A_MN, bool B_MN>
 void launch(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tg, const KArgs& args,
             int tiles_bound) {
@@ -690,7 +696,7 @@ void launch(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const
                                              SMEM_BYTES));
         attr_set = true;
     }
-    const int grid = std::max(1, std::min(tiles_bound, num_sms()));
+    const int grid = std::max(1, std::min(tiles_bound, gemm_sms()));
     k_gemm_bf16<A_MN, B_MN><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ta, tb, tg, args);
     check_launch("k_gemm_bf16");
 }
@@ -762,7 +768,7 @@ void launch_pair(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, 
                                              P_SMEM_BYTES));
         attr_set = true;
     }
-    const int pairs = std::max(1, std::min(pair_tiles, num_sms() / 2));
+    const int pairs = std::max(1, std::min(pair_tiles, gemm_sms() / 2));
     k_gemm_bf16_pair<A_MN, B_MN><<<2 * pairs, NUM_THREADS, P_SMEM_BYTES, st>>>(ta, tb, tg, args);
     check_launch("k_gemm_bf16_pair");
 }
@@ -922,5 +928,7 @@ void gemm_bf16_grouped(cudaStream_t st, int G, int64_t N, int64_t K, const GemmO
     const int64_t bound = (ceil_div(a_rows, BM) + G) * args.g_ntiles * args.ksplit;  // >= device tile count
     dispatch(st, false, false, ta, tb, tb, args, int(std::min<int64_t>(bound, INT32_MAX)));
 }
+
+void gemm_reserve_sms(int n) { g_reserved_sms.store(std::max(0, n), std::memory_order_relaxed); }
 
 }  // namespace meft_dev

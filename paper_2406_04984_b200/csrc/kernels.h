@@ -46,6 +46,9 @@ struct GemmEpilogue {
 void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOperand& A, const GemmOperand& B,
                const GemmEpilogue& epi);
 
+// Leave n SMs free of persistent GEMM CTAs (for overlapped NCCL kernels); 0 restores the full machine.
+void gemm_reserve_sms(int n);
+
 // Grouped variant (K-major operands): group g computes rows [row_off[g], row_off[g+1]) of A against the N rows
 // [g*N, (g+1)*N) of B; tile_off = exclusive scan of ceil(rows_g / 128) (device arrays, no host sync). The
 // epilogue sees the global A row m (use EPI_ROWS_STORE_F32 with row_idx to place it) and column n < N.

@@ -603,6 +603,13 @@ meft_status meft_ctx_set_selection(meft_ctx* ctx, int mode) {
     });
 }
 
+meft_status meft_set_gemm_sm_reserve(int sms) {
+    return guarded(nullptr, [&] {
+        require(sms >= 0 && sms <= 64, MEFT_E_INVALID, "gemm SM reserve must be in [0, 64]");
+        gemm_reserve_sms(sms);
+    });
+}
+
 meft_status meft_ctx_set_gather(meft_ctx* ctx, int mode) {
     return guarded(ctx, [&] {
         require_ctx(ctx);
@@ -1424,13 +1431,15 @@ meft_status meft_topk_finalize(meft_ctx* ctx, const int32_t* sure, const int32_t
 
 meft_status meft_layer_ffn_local(meft_ctx* ctx, meft_store* s, int64_t layer, const uint16_t* h_all,
                                  const uint16_t* g_all, int64_t T, const int32_t* S_local, int64_t su, double beta1,
-                                 double beta2, double eps, double lr, float* out_partial, float* grad_h_partial) {
+                                 double beta2, double eps, double lr, float* out_partial, float* grad_h_partial,
+                                 void* g_ready, void* fwd_done, void* grad_h_done) {
     return guarded(ctx, [&] {
         require_ctx(ctx);
         layer_of(s, layer);
         require(s->prec == MEFT_STORE_MIXED && s->d % 8 == 0, MEFT_E_INVALID, "layer_ffn_local: MIXED store, d % 8");
         ffn_update_impl(ctx, s, layer, h_all, g_all, T, S_local, su, -1, beta1, beta2, eps, lr, out_partial,
-                        grad_h_partial, nullptr, nullptr);
+                        grad_h_partial, static_cast<cudaEvent_t>(g_ready), static_cast<cudaEvent_t>(fwd_done),
+                        static_cast<cudaEvent_t>(grad_h_done));
     });
 }
 

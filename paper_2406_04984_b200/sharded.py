@@ -23,12 +23,13 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 
 import torch
 import torch.distributed as dist
 
 from . import _lib
-from ._lib import lib
+from ._lib import check, lib
 
 
 def cert_bound_coeff(d: int) -> float:
@@ -108,12 +109,16 @@ class DeviceEngine:
                                              _p(per), _p(flags)))
         return per, flags
 
-    def ffn_local(self, h_all, g_all, S_local, lr, betas=(0.9, 0.999), eps=1e-8):
+    def ffn_local(self, h_all, g_all, S_local, lr, betas=(0.9, 0.999), eps=1e-8, g_ready=None, fwd_done=None,
+                  gh_done=None):
+        """Events (torch.cuda.Event, optional): the backward waits for g_ready; fwd_done / gh_done are recorded
+        when out / grad_h are final, for reduce-scatters overlapped with the rest of the step."""
         T, d = h_all.shape
         out = torch.empty((T, d), dtype=torch.float32, device=self.dev)
         gh = torch.empty((T, d), dtype=torch.float32, device=self.dev)
+        ev = [C.c_void_p(e.cuda_event) if e is not None else None for e in (g_ready, fwd_done, gh_done)]
         self._check(lib().meft_layer_ffn_local(self.ctx.h, self.store.h, 0, _p(h_all), _p(g_all), T, _p(S_local),
-                                               S_local.numel(), betas[0], betas[1], eps, lr, _p(out), _p(gh)))
+                                               S_local.numel(), betas[0], betas[1], eps, lr, _p(out), _p(gh), *ev))
         return out, gh
 
 
@@ -164,13 +169,41 @@ class ShardedLayer:
             raise ValueError("N must be divisible by the world size and M by N")
         self.E, self.N_loc, self.M_loc = M // N, N // self.world, M // self.world
         self.last = {}
+        # Overlap (device engine over NCCL): the bulk all-gathers / reduce-scatters run on their own stream and
+        # communicator, so they proceed while the selection exchanges and the FFN compute.
+        self.overlap = isinstance(engine, DeviceEngine) and dist.get_backend(group) == "nccl"
+        if self.overlap:
+            ranks = list(range(self.world)) if group is None else dist.get_process_group_ranks(group)
+            self.bulk_group = dist.new_group(ranks=ranks, backend="nccl")
+            self.comm_stream = torch.cuda.Stream(device=engine.dev)
+            # SMs kept free of the persistent FFN GEMMs so the reduce-scatters can run beside them (P > 1):
+            # ~5% of the GEMM throughput for exchanges that otherwise queue behind the whole backward
+            self.reserve_sms = int(os.environ.get("MEFT_SHARDED_RESERVE_SMS", "8")) if self.world > 1 else 0
 
-    def step(self, h, g, kk, k, lr):
+    def step(self, h, g, kk, k, lr, g_ready=None):
+        """One layer step of this rank's T tokens. g_ready (torch.cuda.Event, optional): g is only final once
+        it fires (e.g. an overlapped host->device copy). With the overlapped NCCL path the result carries
+        out_ready / grad_h_ready events for copies that should not wait for the whole step."""
         P, r, E = self.world, self.rank, self.E
         eng, grp = self.eng, self.group
         T, d = h.shape
         kk_eff = min(kk, self.N)
         take = min(k, kk_eff * E)
+        if self.overlap:  # 8a. all-gather h and g now, behind the whole selection exchange
+            cur, cs = torch.cuda.current_stream(), self.comm_stream
+            ev_in = torch.cuda.Event()
+            ev_in.record(cur)
+            ev_h, ev_g = torch.cuda.Event(), torch.cuda.Event()
+            with torch.cuda.stream(cs):
+                cs.wait_event(ev_in)
+                h_all = _all_gather_rows(h, self.bulk_group, P) if P > 1 else h
+                ev_h.record(cs)
+                if g_ready is not None:
+                    cs.wait_event(g_ready)
+                g_all = _all_gather_rows(g, self.bulk_group, P) if P > 1 else g
+                ev_g.record(cs)
+            h.record_stream(cs)
+            g.record_stream(cs)
         # 1. route (exact tau, ascending per token)
         tau = eng.route(h, kk)
         # 2. dispatch (token, slot) rows to their expert owners
@@ -198,7 +231,8 @@ class ShardedLayer:
         Ccand = kk_eff * E
         na = n_amb.long()
         tok = torch.repeat_interleave(torch.arange(T, device=h.device), na)
-        pos = torch.arange(int(na.sum().item()), device=h.device) - torch.repeat_interleave(torch.cumsum(na, 0) - na, na)
+        n_resc = int(na.sum().item())  # (host sync of the selection phase; never after the FFN is enqueued)
+        pos = torch.arange(n_resc, device=h.device) - torch.repeat_interleave(torch.cumsum(na, 0) - na, na)
         gidx = amb[tok, pos].long()
         e_glob = gidx // E
         slot = (tau[tok].long() == e_glob[:, None]).int().argmax(1)  # position of the expert in tau
@@ -231,13 +265,53 @@ class ShardedLayer:
         S = torch.nonzero(union).flatten()
         S_loc = S[(S >= r * self.M_loc) & (S < (r + 1) * self.M_loc)] - r * self.M_loc
         # 8-9. FFN over all tokens on the local part of the union, partial sums back to the homes
-        h_all = _all_gather_rows(h, grp, P)
-        g_all = _all_gather_rows(g, grp, P)
-        out_p, gh_p = eng.ffn_local(h_all, g_all, S_loc.to(torch.int32).contiguous(), lr)
-        out = _reduce_scatter_rows(out_p, grp, P, r)
-        grad_h = _reduce_scatter_rows(gh_p, grp, P, r)
-        self.last = dict(union_size=int(S.numel()), local_union=int(S_loc.numel()), rescored=int(na.sum().item()))
-        return dict(per_token=per_token, tau=tau, unioned=S, out=out, grad_h=grad_h)
+        S_loc = S_loc.to(torch.int32).contiguous()
+        if self.overlap:
+            cur.wait_event(ev_h)  # the forward needs h_all; the backward waits for g_all inside the step
+            h_all.record_stream(cur)
+            g_all.record_stream(cur)
+            timing = bool(os.environ.get("MEFT_SHARDED_EVENT_TIMING"))  # developer probe
+            fwd_done, gh_done = torch.cuda.Event(enable_timing=timing), torch.cuda.Event(enable_timing=timing)
+            fwd_done.record(cur)  # materialise the CUDA events; the library re-records them
+            gh_done.record(cur)
+            if self.reserve_sms:
+                check(lib().meft_set_gemm_sm_reserve(self.reserve_sms))
+            try:
+                out_p, gh_p = eng.ffn_local(h_all, g_all, S_loc, lr, g_ready=ev_g, fwd_done=fwd_done,
+                                            gh_done=gh_done)
+            finally:
+                if self.reserve_sms:
+                    check(lib().meft_set_gemm_sm_reserve(0))
+            if P == 1:  # the partial sums are the results: no collective, the library's events mark them final
+                out, grad_h, ev_o, ev_out = out_p, gh_p, fwd_done, gh_done
+            else:
+                ev_o, ev_out = torch.cuda.Event(), torch.cuda.Event()
+                with torch.cuda.stream(cs):  # reduce-scatters overlap the backward / weight-gradient GEMMs
+                    cs.wait_event(fwd_done)
+                    out = _reduce_scatter_rows(out_p, self.bulk_group, P, r)
+                    ev_o.record(cs)
+                    cs.wait_event(gh_done)
+                    grad_h = _reduce_scatter_rows(gh_p, self.bulk_group, P, r)
+                    ev_out.record(cs)
+                out_p.record_stream(cs)
+                gh_p.record_stream(cs)
+                cur.wait_event(ev_out)
+                out.record_stream(cur)
+                grad_h.record_stream(cur)
+        else:
+            if g_ready is not None:
+                torch.cuda.current_stream().wait_event(g_ready)
+            h_all = _all_gather_rows(h, grp, P)
+            g_all = _all_gather_rows(g, grp, P)
+            out_p, gh_p = eng.ffn_local(h_all, g_all, S_loc, lr)
+            out = _reduce_scatter_rows(out_p, grp, P, r)
+            grad_h = _reduce_scatter_rows(gh_p, grp, P, r)
+        self.last = dict(union_size=int(S.numel()), local_union=int(S_loc.numel()), rescored=n_resc)
+        res = dict(per_token=per_token, tau=tau, unioned=S, out=out, grad_h=grad_h)
+        if self.overlap:
+            res["out_ready"], res["grad_h_ready"] = ev_o, ev_out
+            res["fwd_done"], res["gh_done"] = fwd_done, gh_done
+        return res
 
 
 def make_device_layer(ctx, d, M, N, group=None, seed=1, w_b_seed=0x7001):
