@@ -205,3 +205,22 @@ def test_step_bookkeeping_and_expert_histogram(ctx):
     assert (info["meter_h2d"], info["meter_d2h"], info["meter_hidden"]) == (2 * d * s, 2 * d * s, T * d)
     assert info["beta_paper"] == s / K and info["dedup_ratio"] == s / (T * K) and info["activated_fraction"] == s / M
     assert (info["router_flops"], info["expert_scoring_flops"]) == (T * N * d, T * kk * (M // N) * d)
+
+
+def test_gemm_sm_reserve_is_bitwise_neutral(ctx):
+    """Reserving SMs for overlapped collectives shrinks the persistent GEMM grids only: same tiles, same bits."""
+    from paper_2406_04984_b200 import _lib
+    w_a, w_g, w_b, h, gr = cfg1_inputs(T=2048)
+    outs = []
+    for reserve in (0, 16):
+        _lib.check(_lib.lib().meft_set_gemm_sm_reserve(reserve))
+        try:
+            st = make_store(ctx, w_a, w_g, w_b, 64)
+            o = torch.empty((2048, 512), dtype=torch.float32, device="cuda")
+            st.layer_step(0, bf16_dev(h), bf16_dev(gr), 4, 32, 1e-3, out=o)
+            torch.cuda.synchronize()
+            outs.append((o.cpu().numpy(), st.download(0, "w_a")))
+        finally:
+            _lib.check(_lib.lib().meft_set_gemm_sm_reserve(0))
+    for a, b in zip(*outs):
+        np.testing.assert_array_equal(a, b)
