@@ -1,0 +1,55 @@
+"""BASELINE config 3 on ONE B200: a stack of L MEFT adapter layers (d=4096, M=65,536, 256 experts, K=128) with
+all tables and Adam state resident in HBM, T tokens per step (16,384 in the config). One step = the fused layer
+step of every layer in turn. 32 layers need ~240 GB of tables (two or more GPUs, expert-sharded); this measures
+the L that fit one GPU and reports the per-layer time and the projected 32-layer step.
+
+  python tools/stack_bench.py [layers=20] [tokens=16384] [steps=3]
+"""
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2406_04984_b200 import meft as G  # noqa: E402
+
+
+def main():
+    L = int(sys.argv[1]) if len(sys.argv) > 1 else 20
+    T = int(sys.argv[2]) if len(sys.argv) > 2 else 16384
+    steps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+    d, M, N, K, kk = 4096, 65536, 256, 128, 4
+    ctx = G.Context(0)
+    st = G.Store(ctx, L, d, M, N, G.STORE_MIXED)
+    b = 1.0 / d ** 0.5
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    with torch.no_grad():
+        for layer in range(L):
+            for name in ("w_a", "w_b", "w_g"):
+                w = st.tensor(layer, name)
+                w.uniform_(-b, b, generator=gen)
+                st.tensor(layer, name + "_compute").copy_(w.to(torch.bfloat16))
+    h = (torch.rand((T, d), generator=gen, device="cuda") * 2 - 1).to(torch.bfloat16)
+    g = (torch.rand((T, d), generator=gen, device="cuda") * 2 - 1).to(torch.bfloat16)
+    for layer in range(L):  # warm-up: every layer once
+        st.layer_step(layer, h, g, kk, K, 1e-4)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        for layer in range(L):
+            st.layer_step(layer, h, g, kk, K, 1e-4)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    per_layer = ms / L
+    free, total = torch.cuda.mem_get_info()
+    print(json.dumps({"layers_resident": L, "tokens_per_step": T, "ms_per_step": ms, "ms_per_layer": per_layer,
+                      "tokens_per_s": T / ms * 1e3, "layer_tokens_per_s": T * L / ms * 1e3,
+                      "projected_32_layer_ms": 32 * per_layer, "projected_32_layer_tokens_per_s": T / (32 * per_layer) * 1e3,
+                      "hbm_used_gb": (total - free) / 1e9}))
+
+
+if __name__ == "__main__":
+    main()
