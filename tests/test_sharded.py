@@ -60,9 +60,9 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("T,kk,k", [(12, 3, 5), (20, 2, 9)])
-def test_sharded_layer_world2_matches_unsharded_reference(T, kk, k):
-    world, lr = 2, 1e-3
+@pytest.mark.parametrize("world,T,kk,k", [(2, 12, 3, 5), (2, 20, 2, 9), (4, 10, 3, 7)])
+def test_sharded_layer_matches_unsharded_reference(world, T, kk, k):
+    lr = 1e-3
     with tempfile.TemporaryDirectory() as outdir:
         mp.start_processes(_worker, args=(world, _free_port(), outdir, T, kk, k, lr), nprocs=world, join=True,
                            start_method="spawn")
