@@ -35,13 +35,72 @@ __host__ __device__ inline double cert_bound_coeff_split(int d, int chunk, int k
 
 __device__ __forceinline__ double bfd(uint16_t b) { return double(bf16_bits_to_f32(b)); }
 
+// Per-product exactness certificate, fp32 flavour: every bf16 x bf16 product is formed exactly in fp32 (the caller
+// guarantees no underflow below 2^-149 and no overflow), its LSB is bounded below by (fp32 exponent field) - 142
+// (an exact product has <= 16 significant bits; subnormals: 2^-149), sum|p| is accumulated in fp32 and inflated by
+// 2^-10 (its rounding error over <= 2^16 terms per lane and the warp sum is far smaller); the value in fp64.
+// ~6 instructions per product and loads 4 deep (the generic path below is ~15 and latency-bound).
+__device__ __forceinline__ bool exact_dot_warp_f32(const uint4* __restrict__ a4, const uint4* __restrict__ b4, int d8,
+                                                   int lane, double& value) {
+    constexpr int U = 4;
+    double s = 0.0;
+    float sa = 0.0f;
+    uint32_t emin = 0x7F800000u;  // min fp32 exponent field (in place) over nonzero products
+    for (int v0 = lane; v0 < d8; v0 += 32 * U) {
+        uint4 x[U], y[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int v = v0 + 32 * u;
+            if (v < d8) {
+                x[u] = a4[v];
+                y[u] = __ldg(b4 + v);
+            } else {
+                x[u] = make_uint4(0, 0, 0, 0);
+                y[u] = x[u];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t xs[4] = {x[u].x, x[u].y, x[u].z, x[u].w}, ys[4] = {y[u].x, y[u].y, y[u].z, y[u].w};
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const uint32_t xw = xs[q >> 1], yw = ys[q >> 1];
+                const float xf = __uint_as_float((q & 1) ? (xw & 0xFFFF0000u) : (xw << 16));
+                const float yf = __uint_as_float((q & 1) ? (yw & 0xFFFF0000u) : (yw << 16));
+                const float p = __fmul_rn(xf, yf);  // exact
+                const uint32_t pb = __float_as_uint(p) & 0x7FFFFFFFu;
+                emin = min(emin, pb == 0 ? 0x7F800000u : (pb & 0x7F800000u));
+                sa += fabsf(p);
+                s += double(p);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        sa += __shfl_xor_sync(0xffffffffu, sa, o);
+        emin = min(emin, __shfl_xor_sync(0xffffffffu, emin, o));
+    }
+    value = s;
+    if (emin == 0x7F800000u) return true;  // every product is +-0
+    const int e = int(emin >> 23);
+    const int lsb = e == 0 ? -149 : e - 142;
+    return double(sa) * (1.0 + 0x1p-10) < ldexp(1.0, lsb + 53);
+}
+
 // The reference's fp64 score dot(a, b) for bf16 rows, computed by a whole warp; all lanes return it.
 __device__ double exact_dot_warp(const uint16_t* __restrict__ a, const uint16_t* __restrict__ b, int d, int lane,
-                                 int* fallbacks) {
+                                 int* fallbacks, bool f32_products = false) {
     double s = 0.0, sa = 0.0;
     int lsb = INT32_MAX;
     const bool vec = (d % 8 == 0) && ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) % 16 == 0);
-    if (vec) {
+    if (vec && f32_products) {
+        double v;
+        if (exact_dot_warp_f32(reinterpret_cast<const uint4*>(a), reinterpret_cast<const uint4*>(b), d / 8, lane, v))
+            return v;
+        lsb = 0;  // certificate failed: go straight to the sequential chain below
+        sa = INFINITY;
+    } else if (vec) {
         const uint4* a4 = reinterpret_cast<const uint4*>(a);
         const uint4* b4 = reinterpret_cast<const uint4*>(b);
         for (int v = lane; v < d / 8; v += 32) {
@@ -76,12 +135,22 @@ __device__ double exact_dot_warp(const uint16_t* __restrict__ a, const uint16_t*
     }
     // every partial sum (in ANY order) is a multiple of 2^lsb bounded by sum|p|: representable iff < 2^(lsb+53)
     if (lsb == INT32_MAX || sa * (1.0 + 0x1p-30) < ldexp(1.0, lsb + 53)) return s;
-    double acc = 0.0;  // certificate failed: run the reference's sequential chain (products exact => fma)
-    if (lane == 0) {
-        for (int k = 0; k < d; ++k) acc = fma(bfd(a[k]), bfd(b[k]), acc);
-        if (fallbacks) atomicAdd(fallbacks, 1);
+    // Certificate failed: the reference's sequential chain acc = fl(acc + a_k b_k), k ascending (products exact, so
+    // this equals its fma chain). The warp loads and multiplies 32 terms at a time; every lane then runs the same
+    // dependent add chain over the broadcast products -- only the fp64 adds are serial.
+    double acc = 0.0;
+    for (int base = 0; base < d; base += 32) {
+        const int k = base + lane;
+        const double p = k < d ? bfd(a[k]) * bfd(b[k]) : 0.0;
+        const int n = min(32, d - base);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const double pj = __shfl_sync(0xffffffffu, p, j);
+            if (j < n) acc += pj;
+        }
     }
-    return __shfl_sync(0xffffffffu, acc, 0);
+    if (lane == 0 && fallbacks) atomicAdd(fallbacks, 1);
+    return acc;
 }
 
 // ||row||_2 of bf16 rows (fp64 sum of squares, rounded up), one warp per row.
@@ -123,21 +192,51 @@ __device__ __forceinline__ double exact_dot_rows(const uint16_t* __restrict__ a,
         (d % 8 == 0) && ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) % 16 == 0)) {
         const uint4* a4 = reinterpret_cast<const uint4*>(a);
         const uint4* b4 = reinterpret_cast<const uint4*>(b);
-        double s = 0.0;
-        for (int v = lane; v < d / 8; v += 32) {
-            const uint4 x = a4[v], y = __ldg(b4 + v);
-            const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+        // Every partial sum is exact, so any order and several accumulators give the reference's value. Loads are
+        // issued 4 deep (latency-bound otherwise, ncu). With -149 <= lsb <= 74 each bf16 x bf16 product is exact
+        // in fp32 too (a multiple of 2^-149 below 2^127 with <= 16 significant bits): one fp32 multiply and one
+        // widening per product instead of two widenings and a DFMA.
+        const bool f32_products = lsb >= -149 && lsb <= 74;
+        constexpr int U = 4;
+        double s0 = 0.0, s1 = 0.0;
+        for (int v0 = lane; v0 < d / 8; v0 += 32 * U) {
+            uint4 x[U], y[U];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                s = fma(double(__uint_as_float(xs[q] << 16)), double(__uint_as_float(ys[q] << 16)), s);
-                s = fma(double(__uint_as_float(xs[q] & 0xFFFF0000u)), double(__uint_as_float(ys[q] & 0xFFFF0000u)), s);
+            for (int u = 0; u < U; ++u) {
+                const int v = v0 + 32 * u;
+                if (v < d / 8) {
+                    x[u] = a4[v];
+                    y[u] = __ldg(b4 + v);
+                } else {
+                    x[u] = make_uint4(0, 0, 0, 0);
+                    y[u] = x[u];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t xs[4] = {x[u].x, x[u].y, x[u].z, x[u].w}, ys[4] = {y[u].x, y[u].y, y[u].z, y[u].w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float xl = __uint_as_float(xs[q] << 16), yl = __uint_as_float(ys[q] << 16);
+                    const float xh = __uint_as_float(xs[q] & 0xFFFF0000u), yh = __uint_as_float(ys[q] & 0xFFFF0000u);
+                    if (f32_products) {
+                        s0 += double(__fmul_rn(xl, yl));
+                        s1 += double(__fmul_rn(xh, yh));
+                    } else {
+                        s0 = fma(double(xl), double(yl), s0);
+                        s1 = fma(double(xh), double(yh), s1);
+                    }
+                }
             }
         }
+        double s = s0 + s1;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         return s;
     }
-    return exact_dot_warp(a, b, d, lane, fallbacks);
+    // fp32-exact products need every product inside fp32's range: all LSBs >= 2^-149 and |p| <= ||a|| ||b|| < 2^127
+    const bool f32ok = lsb >= -149 && double(na) * double(nb) < 0x1p126;
+    return exact_dot_warp(a, b, d, lane, fallbacks, f32ok);
 }
 
 // Warp per token: certified top-kk experts of the approximate router scores P [T x ldp].
