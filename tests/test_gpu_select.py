@@ -184,3 +184,24 @@ def test_certified_flat_topk(ctx):
     flat = G.topk_select(ctx, dev(h, True), dev(w_a.T, True), 48)
     np.testing.assert_array_equal(flat.per_token.cpu().numpy(), want["per_token"])
     np.testing.assert_array_equal(flat.unioned.cpu().numpy(), want["unioned"])
+
+
+@pytest.mark.parametrize("scale_h,scale_k", [(2.0 ** -60, 2.0 ** -75), (2.0 ** 55, 2.0 ** 60), (2.0 ** -130, 1.0),
+                                             (1.0, 2.0 ** 62)])
+def test_certified_at_extreme_magnitudes(ctx, scale_h, scale_k):
+    """Operand scales that push bf16 products to fp32's subnormal range (LSB near 2^-149 and below) or close to
+    its overflow: the fp32-product fast paths must step aside exactly when they cannot be exact, and the indices
+    must equal the oracle bit for bit. Duplicate keys keep exact re-scoring busy."""
+    rs = np.random.RandomState(11)
+    T, d, N, E, kk, k = 64, 128, 8, 32, 3, 24
+    M = N * E
+    w_a = O.bf16_round(rs.uniform(-1, 1, (d, M)) * scale_k)
+    w_a[:, 1::2] = w_a[:, 0::2]
+    w_g = O.bf16_round(rs.uniform(-1, 1, (N, d)))
+    h = O.bf16_round(rs.uniform(-1, 1, (T, d)) * scale_h)
+    h[:4, 3:] = O.bf16_round(h[:4, 3:] * 2.0 ** -40)  # wide dynamic range inside a few rows
+    want = O.ke_select(h, w_g, w_a, kk, k)
+    per, tau, uni, _ = gpu_ke(ctx, h, w_g, w_a, kk, k, True)
+    np.testing.assert_array_equal(tau, want["tau"])
+    np.testing.assert_array_equal(per, want["per_token"])
+    np.testing.assert_array_equal(uni, want["unioned"])
