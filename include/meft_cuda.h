@@ -319,6 +319,24 @@ meft_status meft_topk_classify(meft_ctx* ctx, const float* cand, const int32_t* 
 meft_status meft_topk_finalize(meft_ctx* ctx, const int32_t* sure, const int32_t* n_sure, const int32_t* amb,
                                const int32_t* n_amb, const double* x, int64_t T, int64_t C, int64_t take,
                                int32_t* per_token, uint8_t* union_flags);
+/* Fused reduce-scatter over NVLink peer memory: with `peer` set, the out and grad_h GEMM epilogues store each
+ * output row straight into its home rank's receive buffer, slot `rank`: row g of [world*rows x d] goes to
+ * out_recv[g / rows][(rank * rows + g % rows) * d ...] (grad_h_recv likewise). Buffers are
+ * [world x rows x d] fp32 on every home, mapped into this process (meft_ipc_*); out_partial / grad_h_partial are
+ * then unused. Once every rank's stores are complete (a cross-rank barrier), each home folds its slots with
+ * meft_peer_reduce -- the same data movement as a reduce-scatter, overlapped tile by tile with the GEMMs. */
+typedef struct meft_peer_out {
+    int world, rank;         /* world <= 8 */
+    int64_t rows;            /* tokens per home rank */
+    float* out_recv[8];      /* per home rank: its receive buffer for out */
+    float* grad_h_recv[8];   /* per home rank: its receive buffer for grad_h */
+} meft_peer_out;
+/* out[i] = sum over slots s = 0..world-1 (in that order) of recv[s * rows * d + i], i < rows * d. */
+meft_status meft_peer_reduce(meft_ctx* ctx, const float* recv, int world, int64_t rows, int64_t d, float* out);
+/* CUDA IPC for the receive buffers (allocate them with meft_device_alloc): 64-byte handle out / mapped pointer. */
+meft_status meft_ipc_handle(meft_ctx* ctx, void* dev_ptr, void* handle64);
+meft_status meft_ipc_open(meft_ctx* ctx, const void* handle64, void** dev_ptr);
+meft_status meft_ipc_close(meft_ctx* ctx, void* dev_ptr);
 /* owner rank: the FFN of ALL T (all-gathered) tokens against its local part of the union (S_local: ascending local
  * pair ids), the fused scatter, and the lazy Adam of those pairs. out/grad_h are this shard's partial sums
  * [T x d] fp32 (to be reduce-scattered).
@@ -328,7 +346,8 @@ meft_status meft_topk_finalize(meft_ctx* ctx, const int32_t* sure, const int32_t
 meft_status meft_layer_ffn_local(meft_ctx* ctx, meft_store* store, int64_t layer, const uint16_t* h_all,
                                  const uint16_t* g_all, int64_t T, const int32_t* S_local, int64_t s, double beta1,
                                  double beta2, double eps, double lr, float* out_partial, float* grad_h_partial,
-                                 void* g_ready, void* fwd_done, void* grad_h_done);
+                                 void* g_ready, void* fwd_done, void* grad_h_done,
+                                 const struct meft_peer_out* peer);
 
 /* ------------------------------------------------------------------ whole layer step */
 

@@ -16,6 +16,11 @@ I32P = C.POINTER(C.c_int32)
 D = C.c_double
 INT = C.c_int
 
+class PeerOut(C.Structure):
+    """meft_peer_out (include/meft_cuda.h)."""
+    _fields_ = [("world", INT), ("rank", INT), ("rows", I64), ("out_recv", P * 8), ("grad_h_recv", P * 8)]
+
+
 class CkptHeader(C.Structure):
     _fields_ = [("layers", I64), ("dim", I64), ("pairs", I64), ("experts", I64), ("step", I64),
                 ("train_router", INT)]
@@ -42,7 +47,11 @@ _SIGS = {
     "meft_exact_scores": (INT, [P, P, I64, P, I64, P, P, I64, P]),
     "meft_topk_classify": (INT, [P, P, P, I64, I64, I64, I64, I64, P, P, P, P, P, P]),
     "meft_topk_finalize": (INT, [P, P, P, P, P, P, I64, I64, I64, P, P]),
-    "meft_layer_ffn_local": (INT, [P, P, I64, P, P, I64, P, I64, D, D, D, D, P, P, P, P, P]),
+    "meft_layer_ffn_local": (INT, [P, P, I64, P, P, I64, P, I64, D, D, D, D, P, P, P, P, P, P]),
+    "meft_peer_reduce": (INT, [P, P, INT, I64, I64, P]),
+    "meft_ipc_handle": (INT, [P, P, P]),
+    "meft_ipc_open": (INT, [P, P, C.POINTER(P)]),
+    "meft_ipc_close": (INT, [P, P]),
     "meft_ctx_set_timing": (INT, [P, INT]),
     "meft_ctx_set_selection": (INT, [P, INT]),
     "meft_ctx_set_gather": (INT, [P, INT]),

@@ -55,6 +55,10 @@ struct KArgs {
     const int32_t* b_idx;
     int b_idx_n, b_oob_row;
     const int32_t* kb_run;  // MN-major gathered B: per k-block first table row of a contiguous run, or -1
+    // EPI_PEER_F32 (see kernels.h)
+    float* peer[kMaxPeers];
+    long long peer_rows, row0, col0;
+    int peer_slot;
 };
 
 __device__ __forceinline__ int gather_row(const KArgs& a, int p) {
@@ -177,10 +181,18 @@ __device__ __forceinline__ void epilogue_chunk(const KArgs& a, int m, int n, con
     switch (a.epi) {
         case EPI_STORE_F32:
         case EPI_ROWS_ADD_F32:
-        case EPI_ROWS_STORE_F32: {
-            const long long row = (a.epi != EPI_STORE_F32) ? (long long)a.row_idx[m] : (long long)m;
+        case EPI_ROWS_STORE_F32:
+        case EPI_PEER_F32: {
             const bool acc = a.accumulate || a.epi == EPI_ROWS_ADD_F32;
-            float* c = reinterpret_cast<float*>(a.c) + c_off + row * a.ldc + n;
+            float* c;
+            if (a.epi == EPI_PEER_F32) {  // this row's home rank and the slot reserved for us in its buffer
+                const long long g = a.row0 + m;
+                const long long home = g / a.peer_rows;
+                c = a.peer[home] + (a.peer_slot * a.peer_rows + (g - home * a.peer_rows)) * a.ldc + a.col0 + n;
+            } else {
+                const long long row = (a.epi != EPI_STORE_F32) ? (long long)a.row_idx[m] : (long long)m;
+                c = reinterpret_cast<float*>(a.c) + c_off + row * a.ldc + n;
+            }
             if (cnt == 32) {
                 float4* c4 = reinterpret_cast<float4*>(c);
 #pragma unroll
@@ -704,6 +716,14 @@ void launch(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 void check_epilogue(const GemmEpilogue& epi) {
+    if (epi.kind == EPI_PEER_F32) {
+        if (epi.peer_count < 1 || epi.peer_count > kMaxPeers || epi.peer_rows < 1 || epi.ldc % 4 || epi.col0 % 4 ||
+            epi.peer_slot < 0 || epi.peer_slot >= epi.peer_count)
+            throw MeftError(2, "gemm_bf16: peer epilogue arguments");
+        for (int i = 0; i < epi.peer_count; ++i)
+            if (!aligned16(epi.peer[i])) throw MeftError(2, "gemm_bf16: peer buffers must be 16-byte aligned");
+        return;
+    }
     if (epi.kind == EPI_STORE_F32 || epi.kind == EPI_ROWS_ADD_F32 || epi.kind == EPI_ROWS_STORE_F32) {
         if (!aligned16(epi.c) || (epi.ldc % 4)) throw MeftError(2, "gemm_bf16: f32 output alignment");
     } else {
@@ -731,6 +751,11 @@ KArgs base_args(int64_t M, int64_t N, int64_t K, const GemmEpilogue& epi) {
     args.grouped = 0;
     args.b_idx = nullptr;
     args.kb_run = nullptr;
+    for (int i = 0; i < kMaxPeers; ++i) args.peer[i] = i < epi.peer_count ? epi.peer[i] : nullptr;
+    args.peer_rows = epi.peer_rows;
+    args.row0 = epi.row0;
+    args.col0 = epi.col0;
+    args.peer_slot = epi.peer_slot;
     args.b_idx_n = 0;
     args.b_oob_row = 0;
     args.ksplit = 1;
@@ -865,7 +890,7 @@ void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOpera
                const GemmEpilogue& epi) {
     static const int64_t mc_env = env_elems("MEFT_GEMM_MCHUNK"), nc_env = env_elems("MEFT_GEMM_NCHUNK"),
                          kc_env = env_elems("MEFT_GEMM_KCHUNK");
-    const bool f32_out = epi.kind == EPI_STORE_F32 || epi.kind == EPI_ROWS_ADD_F32;
+    const bool f32_out = epi.kind == EPI_STORE_F32 || epi.kind == EPI_ROWS_ADD_F32 || epi.kind == EPI_PEER_F32;
     // policy: 65536 per dimension (measured on |S| = 640k GEMMs: z 37.5 -> 33.8 ms, out 46.7 -> 38.5,
     // gW 45.2 -> 39.2; 32768 is equivalent, cfg2's |S| = 65536 stays one launch)
     constexpr int64_t kChunk = 65536;
@@ -894,7 +919,10 @@ void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOpera
                 }
                 GemmEpilogue e = epi;
                 if (k0 > 0) e.accumulate = true;
-                if (rows_epi) {
+                if (epi.kind == EPI_PEER_F32) {  // logical offsets: the addresses are resolved per row
+                    e.row0 = epi.row0 + m0;
+                    e.col0 = epi.col0 + n0;
+                } else if (rows_epi) {
                     e.row_idx = epi.row_idx + m0;
                     e.c = const_cast<void*>(advance(epi.c, n0, ce));
                 } else {

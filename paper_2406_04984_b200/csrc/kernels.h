@@ -27,7 +27,12 @@ enum GemmEpi : int {
     EPI_MASK_BF16 = 2,     // C bf16 = mask(m,n) > 0 ? acc : 0 ; mask bf16 [M x ldm]
     EPI_ROWS_ADD_F32 = 3,  // C f32: C[row_idx[m]*ldc + n] += acc (row_idx unique -> no atomics)
     EPI_ROWS_STORE_F32 = 4,  // C f32: C[row_idx[m]*ldc + n] = acc
+    // Push to peers: global row g = row0 + m belongs to home h = g / peer_rows; the f32 row is stored into that
+    // home's receive buffer peer[h] (device pointer, NVLink peer-mapped for h != this rank) at slot peer_slot:
+    // peer[h][(peer_slot * peer_rows + g % peer_rows) * ldc + col0 + n]. A reduce-scatter fused into the epilogue.
+    EPI_PEER_F32 = 5,
 };
+constexpr int kMaxPeers = 8;
 
 struct GemmEpilogue {
     int kind = EPI_STORE_F32;
@@ -41,6 +46,12 @@ struct GemmEpilogue {
     // partial product to c + s * split_stride (elements); the caller sums the partials.
     int ksplit = 1;
     int64_t split_stride = 0;
+    // EPI_PEER_F32
+    float* peer[kMaxPeers] = {};
+    int peer_count = 0;
+    int peer_slot = 0;
+    int64_t peer_rows = 0;
+    int64_t row0 = 0, col0 = 0;
 };
 
 void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOperand& A, const GemmOperand& B,

@@ -253,9 +253,23 @@ GemmOperand kv_operand(meft_ctx* ctx, const void* p, int64_t d, bool mn_major, c
     return op;
 }
 
+// The out / grad_h GEMMs' epilogue when their rows are pushed to the token homes (meft_peer_out).
+GemmEpilogue peer_epilogue(const meft_peer_out& po, bool grad_h, int64_t d) {
+    require(po.world >= 1 && po.world <= kMaxPeers && po.rank >= 0 && po.rank < po.world && po.rows >= 1,
+            MEFT_E_INVALID, "peer_out: world in [1, 8], rank < world, rows >= 1");
+    GemmEpilogue e;
+    e.kind = EPI_PEER_F32;
+    e.ldc = d;
+    e.peer_count = po.world;
+    e.peer_slot = po.rank;
+    e.peer_rows = po.rows;
+    for (int i = 0; i < po.world; ++i) e.peer[i] = grad_h ? po.grad_h_recv[i] : po.out_recv[i];
+    return e;
+}
+
 void ffn_forward_impl(meft_ctx* ctx, meft_dtype dt, const void* h, const void* keys_s, const void* values_s,
                       int64_t T, int64_t d, int64_t s, int64_t ld_z, void* z, void* out, bool accumulate,
-                      const RowGather& rg = RowGather()) {
+                      const RowGather& rg = RowGather(), const meft_peer_out* peer = nullptr) {
     cudaStream_t st = ctx->stream;
     if (dt == MEFT_F64) {
         double* outd = static_cast<double*>(out);
@@ -284,10 +298,14 @@ void ffn_forward_impl(meft_ctx* ctx, meft_dtype dt, const void* h, const void* k
     e1.ldc = ld_z;
     gemm_bf16(st, T, s, d, GemmOperand{h, d, false}, kv_operand(ctx, keys_s, d, false, rg, s), e1);
     GemmEpilogue e2;
-    e2.kind = EPI_STORE_F32;
-    e2.c = out;
-    e2.ldc = d;
-    e2.accumulate = accumulate;
+    if (peer) {
+        e2 = peer_epilogue(*peer, false, d);
+    } else {
+        e2.kind = EPI_STORE_F32;
+        e2.c = out;
+        e2.ldc = d;
+        e2.accumulate = accumulate;
+    }
     gemm_bf16(st, T, d, s, GemmOperand{z, ld_z, false}, kv_operand(ctx, values_s, d, true, rg, s), e2);
 }
 
@@ -296,7 +314,8 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
                        const void* values_s, int64_t T, int64_t d, int64_t s, int64_t ld_z, void* masked,
                        void* grad_keys_s, void* grad_values_s, void* grad_h, bool acc_h, const int32_t* S_rows,
                        void* stage_keys, void* stage_values, const RowGather& rg = RowGather(),
-                       cudaEvent_t grad_h_done = nullptr, const std::function<void()>* between = nullptr) {
+                       cudaEvent_t grad_h_done = nullptr, const std::function<void()>* between = nullptr,
+                       const meft_peer_out* peer = nullptr) {
     cudaStream_t st = ctx->stream;
     if (dt == MEFT_F64) {
         const double* gd = static_cast<const double*>(g);
@@ -339,12 +358,16 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
     e3.mask = z;
     e3.ldm = ld_z;
     gemm_bf16(st, T, s, d, GemmOperand{g, d, false}, kv_operand(ctx, values_s, d, false, rg, s), e3);
-    if (grad_h) {  // first after masked, so grad_h can stream back while the weight-gradient GEMMs run
+    if (grad_h || peer) {  // first after masked, so grad_h can stream back while the weight-gradient GEMMs run
         GemmEpilogue e6;  // grad_h (+)= masked * keys_s
-        e6.kind = EPI_STORE_F32;
-        e6.c = grad_h;
-        e6.ldc = d;
-        e6.accumulate = acc_h;
+        if (peer) {
+            e6 = peer_epilogue(*peer, true, d);
+        } else {
+            e6.kind = EPI_STORE_F32;
+            e6.c = grad_h;
+            e6.ldc = d;
+            e6.accumulate = acc_h;
+        }
         gemm_bf16(st, T, d, s, GemmOperand{masked, ld_z, false}, kv_operand(ctx, keys_s, d, true, rg, s), e6);
     }
     if (grad_h_done) MEFT_CUDA_CHECK(cudaEventRecord(grad_h_done, st));
@@ -548,7 +571,6 @@ meft_status meft_ctx_create(int device, void* stream, meft_ctx** out) {
         MEFT_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
         MEFT_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_fwd, cudaEventDisableTiming));
         MEFT_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
-        MEFT_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
         MEFT_CUDA_CHECK(cudaMalloc(&c->dev_small, 64 * sizeof(int32_t)));
         MEFT_CUDA_CHECK(cudaMallocHost(&c->host_small, 64 * sizeof(int32_t)));
     });
@@ -568,7 +590,6 @@ void meft_ctx_destroy(meft_ctx* ctx) {
     if (ctx->host_small) cudaFreeHost(ctx->host_small);
     if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
     if (ctx->ev_fwd) cudaEventDestroy(ctx->ev_fwd);
-    if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
     if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -1138,7 +1159,8 @@ meft_status meft_sparse_adam_update(meft_ctx* ctx, meft_store* s, int64_t layer,
 static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const void* h, const void* g, int64_t T,
                             const int32_t* uni, int64_t su, int64_t holes, double b1, double b2, double eps,
                             double lr, float* out, float* grad_h, cudaEvent_t g_ready, cudaEvent_t fwd_done,
-                            cudaEvent_t gh_done = nullptr, const int32_t* tau = nullptr, int64_t kk_eff = 0);
+                            cudaEvent_t gh_done = nullptr, const int32_t* tau = nullptr, int64_t kk_eff = 0,
+                            const meft_peer_out* peer = nullptr);
 
 static void ensure_key_stats(meft_ctx* ctx, meft_store* s, int64_t layer);
 
@@ -1246,7 +1268,7 @@ static void router_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, cons
 static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const void* h, const void* g, int64_t T,
                             const int32_t* uni, int64_t su, int64_t holes, double b1, double b2, double eps,
                             double lr, float* out, float* grad_h, cudaEvent_t g_ready, cudaEvent_t fwd_done,
-                            cudaEvent_t gh_done, const int32_t* tau, int64_t kk_eff) {
+                            cudaEvent_t gh_done, const int32_t* tau, int64_t kk_eff, const meft_peer_out* peer) {
     const LayerBufs& L = layer_of(s, layer);
     const int64_t d = s->d;
     cudaStream_t st = ctx->stream;
@@ -1284,7 +1306,7 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
     // sparse_ffn_pa adapter term (adapter.cpp:122-126), every token against the whole union
     {
         PhaseScope ps(ctx, 2);
-        ffn_forward_impl(ctx, MEFT_BF16, h, ks, vs, T, d, su, ld, act, outb, false, rg);
+        ffn_forward_impl(ctx, MEFT_BF16, h, ks, vs, T, d, su, ld, act, outb, false, rg, peer);
     }
     if (fwd_done) MEFT_CUDA_CHECK(cudaEventRecord(fwd_done, st));
     if (g_ready) MEFT_CUDA_CHECK(cudaStreamWaitEvent(st, g_ready, 0));
@@ -1303,7 +1325,7 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
         {
             PhaseScope ps(ctx, 3);
             ffn_backward_impl(ctx, MEFT_BF16, g, h, act, ks, vs, T, d, su, ld, masked, nullptr, nullptr, ghb, false,
-                              uni, L.st_a, L.st_b, rg, gh_done);
+                              uni, L.st_a, L.st_b, rg, gh_done, nullptr, peer);
         }
         train_router();
         PhaseScope ps(ctx, 4);
@@ -1332,7 +1354,7 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
             p3.emplace(ctx, 3);
         };
         ffn_backward_impl(ctx, MEFT_BF16, g, h, act, ks, vs, T, d, su, ld, masked, gblk, gblk, ghb, false, nullptr,
-                          nullptr, nullptr, rg, gh_done, &values_step);
+                          nullptr, nullptr, rg, gh_done, &values_step, peer);
         p3.reset();
         train_router();
         if (su > 0) adam_table(1);
@@ -1432,14 +1454,50 @@ meft_status meft_topk_finalize(meft_ctx* ctx, const int32_t* sure, const int32_t
 meft_status meft_layer_ffn_local(meft_ctx* ctx, meft_store* s, int64_t layer, const uint16_t* h_all,
                                  const uint16_t* g_all, int64_t T, const int32_t* S_local, int64_t su, double beta1,
                                  double beta2, double eps, double lr, float* out_partial, float* grad_h_partial,
-                                 void* g_ready, void* fwd_done, void* grad_h_done) {
+                                 void* g_ready, void* fwd_done, void* grad_h_done, const meft_peer_out* peer) {
     return guarded(ctx, [&] {
         require_ctx(ctx);
         layer_of(s, layer);
         require(s->prec == MEFT_STORE_MIXED && s->d % 8 == 0, MEFT_E_INVALID, "layer_ffn_local: MIXED store, d % 8");
+        if (peer)
+            require(peer->rows * peer->world == T, MEFT_E_SHAPE, "layer_ffn_local: peer rows * world must equal T");
         ffn_update_impl(ctx, s, layer, h_all, g_all, T, S_local, su, -1, beta1, beta2, eps, lr, out_partial,
                         grad_h_partial, static_cast<cudaEvent_t>(g_ready), static_cast<cudaEvent_t>(fwd_done),
-                        static_cast<cudaEvent_t>(grad_h_done));
+                        static_cast<cudaEvent_t>(grad_h_done), nullptr, 0, peer);
+    });
+}
+
+meft_status meft_peer_reduce(meft_ctx* ctx, const float* recv, int world, int64_t rows, int64_t d, float* out) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(world >= 1 && world <= kMaxPeers && rows >= 0 && d >= 0, MEFT_E_INVALID, "peer_reduce: arguments");
+        slot_sum(ctx->stream, recv, world, rows * d, out);
+    });
+}
+
+meft_status meft_ipc_handle(meft_ctx* ctx, void* dev_ptr, void* handle64) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");
+        cudaIpcMemHandle_t hnd;
+        MEFT_CUDA_CHECK(cudaIpcGetMemHandle(&hnd, dev_ptr));
+        std::memcpy(handle64, &hnd, sizeof(hnd));
+    });
+}
+
+meft_status meft_ipc_open(meft_ctx* ctx, const void* handle64, void** dev_ptr) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        cudaIpcMemHandle_t hnd;
+        std::memcpy(&hnd, handle64, sizeof(hnd));
+        MEFT_CUDA_CHECK(cudaIpcOpenMemHandle(dev_ptr, hnd, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+
+meft_status meft_ipc_close(meft_ctx* ctx, void* dev_ptr) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        MEFT_CUDA_CHECK(cudaIpcCloseMemHandle(dev_ptr));
     });
 }
 

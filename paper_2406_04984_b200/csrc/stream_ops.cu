@@ -365,6 +365,31 @@ void histogram_add(cudaStream_t st, const int32_t* idx, int64_t n, int64_t* hist
     check_launch("k_hist_add");
 }
 
+// out[i] = recv[0][i] + recv[1][i] + ... in slot order (the home's side of the peer-memory reduce-scatter).
+__global__ void k_slot_sum(const float4* __restrict__ recv, int world, int64_t n4, float4* __restrict__ out) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4; i += int64_t(gridDim.x) * blockDim.x) {
+        float4 a = recv[i];
+        for (int s = 1; s < world; ++s) {
+            const float4 b = recv[s * n4 + i];
+            a.x += b.x;
+            a.y += b.y;
+            a.z += b.z;
+            a.w += b.w;
+        }
+        out[i] = a;
+    }
+}
+
+void slot_sum(cudaStream_t st, const float* recv, int world, int64_t n, float* out) {
+    if (n <= 0) return;
+    if (n % 4 || (reinterpret_cast<uintptr_t>(recv) | reinterpret_cast<uintptr_t>(out)) % 16)
+        throw MeftError(2, "peer_reduce: rows * d must be a multiple of 4 and buffers 16-byte aligned");
+    const int64_t n4 = n / 4;
+    k_slot_sum<<<int(std::min<int64_t>((n4 + 255) / 256, num_sms() * 8)), 256, 0, st>>>(
+        reinterpret_cast<const float4*>(recv), world, n4, reinterpret_cast<float4*>(out));
+    check_launch("k_slot_sum");
+}
+
 void union_holes(cudaStream_t st, const int32_t* idx, const int32_t* n_dev, int32_t* out) {
     k_union_holes<<<1, 1, 0, st>>>(idx, n_dev, out);
     check_launch("k_union_holes");

@@ -12,6 +12,7 @@ void stage_add(cudaStream_t st, int stage_dtype, void* stage, int64_t d, const i
                const void* g, uint8_t* staged);
 void mark_rows(cudaStream_t st, uint8_t* staged, const int32_t* idx, const int32_t* count_dev, int64_t count);
 void union_holes(cudaStream_t st, const int32_t* idx, const int32_t* n_dev, int32_t* out);
+void slot_sum(cudaStream_t st, const float* recv, int world, int64_t n, float* out);  // sum of `world` slots of n
 void histogram_add(cudaStream_t st, const int32_t* idx, int64_t n, int64_t* hist);  // hist[idx[i]] += 1
 // router.cu: straight-through router gradient of the fused step (trainer.cpp:140-181). grad_g [N x d] fp32 is
 // fully written; touched[e] = some token routed to e had a positive activation in e's union columns.

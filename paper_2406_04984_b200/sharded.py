@@ -110,16 +110,87 @@ class DeviceEngine:
         return per, flags
 
     def ffn_local(self, h_all, g_all, S_local, lr, betas=(0.9, 0.999), eps=1e-8, g_ready=None, fwd_done=None,
-                  gh_done=None):
+                  gh_done=None, peer=None):
         """Events (torch.cuda.Event, optional): the backward waits for g_ready; fwd_done / gh_done are recorded
-        when out / grad_h are final, for reduce-scatters overlapped with the rest of the step."""
+        when out / grad_h are final, for reduce-scatters overlapped with the rest of the step. With `peer`
+        (PeerExchange) the out / grad_h rows are pushed into the token homes' receive buffers instead and
+        (None, None) is returned."""
         T, d = h_all.shape
+        ev = [C.c_void_p(e.cuda_event) if e is not None else None for e in (g_ready, fwd_done, gh_done)]
+        if peer is not None:
+            self._check(lib().meft_layer_ffn_local(self.ctx.h, self.store.h, 0, _p(h_all), _p(g_all), T,
+                                                   _p(S_local), S_local.numel(), betas[0], betas[1], eps, lr, None,
+                                                   None, *ev, C.byref(peer.desc)))
+            return None, None
         out = torch.empty((T, d), dtype=torch.float32, device=self.dev)
         gh = torch.empty((T, d), dtype=torch.float32, device=self.dev)
-        ev = [C.c_void_p(e.cuda_event) if e is not None else None for e in (g_ready, fwd_done, gh_done)]
         self._check(lib().meft_layer_ffn_local(self.ctx.h, self.store.h, 0, _p(h_all), _p(g_all), T, _p(S_local),
-                                               S_local.numel(), betas[0], betas[1], eps, lr, _p(out), _p(gh), *ev))
+                                               S_local.numel(), betas[0], betas[1], eps, lr, _p(out), _p(gh), *ev,
+                                               None))
         return out, gh
+
+
+class PeerExchange:
+    """Receive buffers of the fused peer-memory reduce-scatter (meft_peer_out): out and grad_h, each
+    [world x rows x d] fp32 per home rank, allocated with cudaMalloc and mapped into every rank of `group` through
+    CUDA IPC (handles all-gathered over the group). ``desc`` is the meft_peer_out for this rank; ``reduce`` folds
+    this home's slots in slot order. ``peers`` lets a single process stand in for several ranks (tests)."""
+
+    def __init__(self, ctx, rows, d, group=None, world=None, rank=None, local=None):
+        self.ctx, self.rows, self.d = ctx, rows, d
+        self.world = world if world is not None else dist.get_world_size(group)
+        self.rank = rank if rank is not None else dist.get_rank(group)
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+        nbytes = self.world * rows * d * 4
+        self._own, self._opened = [], []
+        if local is not None:  # single-process emulation: `local` = [(out_ptr, gh_ptr)] of every emulated rank
+            bases = local
+        else:
+            mine = []
+            for _ in range(2):
+                p = C.c_void_p()
+                check(lib().meft_device_alloc(ctx.h, nbytes, C.byref(p)), ctx.h)
+                self._own.append(p.value)
+                mine.append(p.value)
+            handles = []
+            for p in mine:
+                hb = (C.c_char * 64)()
+                check(lib().meft_ipc_handle(ctx.h, C.c_void_p(p), hb), ctx.h)
+                handles.append(bytes(hb))
+            every = [None] * self.world
+            dist.all_gather_object(every, handles, group=group)
+            bases = []
+            for r, hs in enumerate(every):
+                if r == self.rank:
+                    bases.append(tuple(mine))
+                    continue
+                ptrs = []
+                for hbytes in hs:
+                    p = C.c_void_p()
+                    check(lib().meft_ipc_open(ctx.h, (C.c_char * 64).from_buffer_copy(hbytes), C.byref(p)), ctx.h)
+                    self._opened.append(p.value)
+                    ptrs.append(p.value)
+                bases.append(tuple(ptrs))
+        self.desc = _lib.PeerOut()
+        self.desc.world, self.desc.rank, self.desc.rows = self.world, self.rank, rows
+        for r, (po, pg) in enumerate(bases):
+            self.desc.out_recv[r] = po
+            self.desc.grad_h_recv[r] = pg
+        self.recv = bases[self.rank]  # this home's (out, grad_h) receive buffers
+
+    def reduce(self, ctx, which):
+        """Sum this home's slots (which: 0 = out, 1 = grad_h) into a new [rows x d] fp32 tensor on ctx's stream."""
+        out = torch.empty((self.rows, self.d), dtype=torch.float32, device=self.dev)
+        check(lib().meft_peer_reduce(ctx.h, C.c_void_p(self.recv[which]), self.world, self.rows, self.d, _p(out)),
+              ctx.h)
+        return out
+
+    def close(self):
+        for p in self._opened:
+            lib().meft_ipc_close(self.ctx.h, C.c_void_p(p))
+        for p in self._own:
+            lib().meft_device_free(self.ctx.h, C.c_void_p(p))
+        self._opened, self._own = [], []
 
 
 def _a2a(tensor, send_counts, recv_counts, group):
@@ -176,9 +247,45 @@ class ShardedLayer:
             ranks = list(range(self.world)) if group is None else dist.get_process_group_ranks(group)
             self.bulk_group = dist.new_group(ranks=ranks, backend="nccl")
             self.comm_stream = torch.cuda.Stream(device=engine.dev)
-            # SMs kept free of the persistent FFN GEMMs so the reduce-scatters can run beside them (P > 1):
-            # ~5% of the GEMM throughput for exchanges that otherwise queue behind the whole backward
-            self.reserve_sms = int(os.environ.get("MEFT_SHARDED_RESERVE_SMS", "8")) if self.world > 1 else 0
+            # Reduce-scatters of out / grad_h: by default FUSED into the GEMM epilogues over NVLink peer memory
+            # (PeerExchange; P > 1 or MEFT_SHARDED_PEER=1), else NCCL on the comm stream with SMs kept free of the
+            # persistent FFN GEMMs so its kernels can run beside them (~5% of GEMM throughput).
+            env = os.environ.get("MEFT_SHARDED_PEER")
+            self.peer_mode = (env == "1") or (env is None and self.world > 1)
+            self.peer = None
+            self.comm_ctx = None
+            self.reserve_sms = 0 if (self.peer_mode or self.world == 1) else int(
+                os.environ.get("MEFT_SHARDED_RESERVE_SMS", "8"))
+
+    def _peer_exchange(self, T, d):
+        """(Re)build the peer receive buffers for T tokens per rank; every rank agrees on success or falls back."""
+        if self.peer is not None and self.peer.rows == T:
+            return self.peer
+        if self.peer is not None:
+            self.peer.close()
+            self.peer = None
+        ok, px = 1, None
+        try:
+            from .meft import Context
+            if self.comm_ctx is None:
+                self.comm_ctx = Context(torch.cuda.current_device(), stream=self.comm_stream)
+            px = PeerExchange(self.eng.ctx, T, d, group=self.bulk_group)
+        except Exception:  # e.g. no CUDA IPC / peer access between these devices
+            ok = 0
+        flag = torch.tensor([ok], dtype=torch.int32, device=self.eng.dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.bulk_group)
+        if int(flag.item()) == 0:
+            if px is not None:
+                px.close()
+            self.peer_mode = False
+            self.reserve_sms = 0 if self.world == 1 else int(os.environ.get("MEFT_SHARDED_RESERVE_SMS", "8"))
+            return None
+        self.peer = px
+        return px
+
+    def _barrier(self):  # on the current (comm) stream: every rank's pushed rows have landed
+        t = torch.zeros(1, dtype=torch.int32, device=self.eng.dev)
+        dist.all_reduce(t, group=self.bulk_group)
 
     def step(self, h, g, kk, k, lr, g_ready=None):
         """One layer step of this rank's T tokens. g_ready (torch.cuda.Event, optional): g is only final once
@@ -274,15 +381,30 @@ class ShardedLayer:
             fwd_done, gh_done = torch.cuda.Event(enable_timing=timing), torch.cuda.Event(enable_timing=timing)
             fwd_done.record(cur)  # materialise the CUDA events; the library re-records them
             gh_done.record(cur)
+            px = self._peer_exchange(T, d) if self.peer_mode else None
             if self.reserve_sms:
                 check(lib().meft_set_gemm_sm_reserve(self.reserve_sms))
             try:
                 out_p, gh_p = eng.ffn_local(h_all, g_all, S_loc, lr, g_ready=ev_g, fwd_done=fwd_done,
-                                            gh_done=gh_done)
+                                            gh_done=gh_done, peer=px)
             finally:
                 if self.reserve_sms:
                     check(lib().meft_set_gemm_sm_reserve(0))
-            if P == 1:  # the partial sums are the results: no collective, the library's events mark them final
+            if px is not None:  # rows were pushed into the homes' buffers by the GEMM epilogues: fold our slots
+                ev_o, ev_out = torch.cuda.Event(), torch.cuda.Event()
+                with torch.cuda.stream(cs):
+                    cs.wait_event(fwd_done)
+                    self._barrier()
+                    out = px.reduce(self.comm_ctx, 0)
+                    ev_o.record(cs)
+                    cs.wait_event(gh_done)
+                    self._barrier()
+                    grad_h = px.reduce(self.comm_ctx, 1)
+                    ev_out.record(cs)
+                cur.wait_event(ev_out)
+                out.record_stream(cur)
+                grad_h.record_stream(cur)
+            elif P == 1:  # the partial sums are the results: no collective, the library's events mark them final
                 out, grad_h, ev_o, ev_out = out_p, gh_p, fwd_done, gh_done
             else:
                 ev_o, ev_out = torch.cuda.Event(), torch.cuda.Event()

@@ -63,3 +63,30 @@ def test_sharded_world1_equals_layer_step(ctx, nccl_world1):
     res2 = layer.step(h, g, kk, K, lr)
     want2 = O.ke_select(hs, w_g, keys.T, kk, K)
     np.testing.assert_array_equal(res2["per_token"].cpu().numpy(), want2["per_token"])
+
+
+def test_sharded_world1_peer_path_equals_layer_step(ctx, nccl_world1, monkeypatch):
+    """The fused peer-memory reduce-scatter route (forced at world 1: rows pushed into this rank's own receive
+    buffer, one barrier, slot fold) must leave the step bitwise equal to meft_layer_step."""
+    monkeypatch.setenv("MEFT_SHARDED_PEER", "1")
+    d, M, N, K, kk, T, lr = 512, 4096, 64, 32, 4, 256, 1e-3
+    eng, store = SH.make_device_layer(ctx, d, M, N, seed=1)
+    ref = G.Store(ctx, 1, d, M, N, G.STORE_MIXED)
+    ref.init_reference(1)
+    ref.tensor(0, "w_b").copy_(store.tensor(0, "w_b"))
+    ref.tensor(0, "w_b_compute").copy_(store.tensor(0, "w_b_compute"))
+    gen = torch.Generator(device="cuda").manual_seed(12)
+    h = ((torch.rand((T, d), generator=gen, device="cuda") * 2 - 1)).to(torch.bfloat16)
+    g = ((torch.rand((T, d), generator=gen, device="cuda") * 2 - 1)).to(torch.bfloat16)
+    layer = SH.ShardedLayer(eng, d, M, N)
+    assert layer.peer_mode
+    for _ in range(2):
+        res = layer.step(h, g, kk, K, lr)
+        out = torch.empty((T, d), dtype=torch.float32, device="cuda")
+        gh = torch.empty_like(out)
+        ref.layer_step(0, h, g, kk, K, lr, out=out, grad_h=gh)
+        torch.cuda.synchronize()
+        assert layer.peer is not None  # the peer route really ran
+        assert torch.equal(res["out"], out)
+        assert torch.equal(res["grad_h"], gh)
+    layer.peer.close()
