@@ -102,8 +102,13 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------------------------- reference arm
 
-def ref_sample_step_tokens():
-    return int(os.environ.get("MEFT_REF_SAMPLE_TOKENS", "64"))
+def ref_sample_step_tokens(steps=1):
+    """Tokens per timed reference step: 64 (~13 s of 16-core fp64 work at cfg2), 32 for runs of more than 10
+    steps, so `--steps K --warmup W` stays within a few minutes. MEFT_REF_SAMPLE_TOKENS overrides."""
+    env = os.environ.get("MEFT_REF_SAMPLE_TOKENS")
+    if env:
+        return int(env)
+    return 64 if steps <= 10 else 32
 
 
 def run_reference_sample(steps, warmup, tokens, threads=None):
@@ -128,7 +133,8 @@ def run_reference_sample(steps, warmup, tokens, threads=None):
     times, phases = [], np.zeros(6)
     for i in range(warmup + steps):
         t0 = time.perf_counter()
-        r = st.layer_step(0, h, g, CFG["kk"], CFG["k"], CFG["lr"], want_outputs=False)
+        hw, gw = (h, g) if i >= warmup else (h[:8], g[:8])  # warm-up steps: small samples, untimed
+        r = st.layer_step(0, hw, gw, CFG["kk"], CFG["k"], CFG["lr"], want_outputs=False)
         dt = time.perf_counter() - t0
         if i >= warmup:
             times.append(dt)
@@ -150,7 +156,7 @@ def cpu_model():
 def reference_arm(args, rank, world):
     if rank != 0:
         return  # rank 0 alone runs the CPU reference; other ranks exit 0 without work
-    tokens = ref_sample_step_tokens()
+    tokens = ref_sample_step_tokens(args.steps)
     try:
         tps, sec, phases, cores = run_reference_sample(args.steps, args.warmup, tokens)
     except Exception as e:  # pragma: no cover - surfaced as unavailable, never as a fake number
