@@ -28,7 +28,10 @@ constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int NUM_THREADS = 192;
 constexpr int TMEM_COLS = 512;  // 2 accumulators x 256 fp32 columns
 constexpr int GROUP_M = 16;     // raster: 16 M-tiles share each resident B panel in L2
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+// grouped mode: the group offset tables (tile and row offsets, G + 1 each) are staged in shared memory
+constexpr int MAX_SMEM_GROUPS = 2048;
+constexpr int GROUP_TABLE_BYTES = 2 * (MAX_SMEM_GROUPS + 1) * 4;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + GROUP_TABLE_BYTES;
 
 struct KArgs {
     int M, N, K;
@@ -141,7 +144,9 @@ struct TileInfo {
 
 __device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int& m_blk, int& n_blk);
 
-__device__ __forceinline__ TileInfo resolve_tile(const KArgs& a, int tile) {
+// s_toff / s_roff: the group tables in shared memory (grouped mode; nullptr = read them from global memory).
+__device__ __forceinline__ TileInfo resolve_tile(const KArgs& a, int tile, const int* s_toff = nullptr,
+                                                 const int* s_roff = nullptr) {
     TileInfo t;
     if (!a.grouped) {
         int mb, nb;
@@ -152,13 +157,15 @@ __device__ __forceinline__ TileInfo resolve_tile(const KArgs& a, int tile) {
         t.n_col0 = t.b_row0;
     } else {
         const int mt_global = tile / a.g_ntiles, nt = tile - mt_global * a.g_ntiles;
-        int lo = 0, hi = a.G;  // last g with g_tile_off[g] <= mt_global
+        const int* toff = s_toff ? s_toff : a.g_tile_off;
+        const int* roff = s_roff ? s_roff : a.g_row_off;
+        int lo = 0, hi = a.G;  // last g with g_tile_off[g] <= mt_global (a dependent chain: keep it on-chip)
         while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
-            if (a.g_tile_off[mid] <= mt_global) lo = mid; else hi = mid;
+            if (toff[mid] <= mt_global) lo = mid; else hi = mid;
         }
-        t.a_row0 = a.g_row_off[lo] + (mt_global - a.g_tile_off[lo]) * BM;
-        t.m_lim = a.g_row_off[lo + 1];
+        t.a_row0 = roff[lo] + (mt_global - toff[lo]) * BM;
+        t.m_lim = roff[lo + 1];
         t.n_col0 = nt * BN;
         t.b_row0 = lo * a.g_brows + t.n_col0;
     }
@@ -275,6 +282,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    int* s_toff = reinterpret_cast<int*>(smem + STAGES * STAGE_BYTES + 256);
+    int* s_roff = s_toff + (MAX_SMEM_GROUPS + 1);
+    const bool tables = args.grouped && args.G <= MAX_SMEM_GROUPS;
+    if (tables) {
+        for (int i = threadIdx.x; i <= args.G; i += blockDim.x) {
+            s_toff[i] = args.g_tile_off[i];
+            s_roff[i] = args.g_row_off[i];
+        }
+    } else {
+        s_toff = s_roff = nullptr;
+    }
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -313,12 +331,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         RunBatch rb;                            // MN-major gathered B: k-block run table reader
         auto tile_n0 = [&](int t) {
             const int sp_ = t / base_tiles;
-            return resolve_tile(args, t - sp_ * base_tiles).b_row0;
+            return resolve_tile(args, t - sp_ * base_tiles, s_toff, s_roff).b_row0;
         };
         if (gather && !B_MN && blockIdx.x < num_tiles) load_nrows<2>(args, tile_n0(blockIdx.x), lane, gn);
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
             const int sp = tile / base_tiles;
-            const TileInfo ti = resolve_tile(args, tile - sp * base_tiles);
+            const TileInfo ti = resolve_tile(args, tile - sp * base_tiles, s_toff, s_roff);
             const int m0 = ti.a_row0, n0 = ti.b_row0;
             const int kb0 = sp * args.kb_split, kb1 = min(args.num_kb, kb0 + args.kb_split);
             const int next = tile + int(gridDim.x);
@@ -425,7 +443,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         int it = 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
             const int sp = tile / base_tiles;
-            const TileInfo ti = resolve_tile(args, tile - sp * base_tiles);
+            const TileInfo ti = resolve_tile(args, tile - sp * base_tiles, s_toff, s_roff);
             const long long c_off = sp * args.split_stride;
             const int acc = it & 1;
             const uint32_t aphase = (it >> 1) & 1;

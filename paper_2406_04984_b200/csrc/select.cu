@@ -451,11 +451,46 @@ CertSplit cert_split(int64_t d, bool allow) {
     return CertSplit{ks, kbs, cb};
 }
 
+// float(fp64 sum of the ks partial products) of every element
+__global__ void k_sum_partials(const float* __restrict__ part, int ks, int64_t n, float* __restrict__ out) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        double s = 0.0;
+        for (int p = 0; p < ks; ++p) s += double(part[p * n + i]);
+        out[i] = float(s);
+    }
+}
+
+// Approximate router scores P [T x ldp] = float(fp64 sum of the K-chunk partials of H W_g^T): the split launches
+// 4x the tiles of an N = 256 router GEMM (which alone fills under half the SMs) and the certified router bound
+// shrinks like the candidate scores'. Returns the bound coefficient for P. `part` holds ks * T * ldp floats.
+double router_scores(cudaStream_t st, const uint16_t* h, const uint16_t* wg, int64_t T, int64_t N, int64_t d,
+                     int64_t ldp, float* P, float* part) {
+    const CertSplit cs = cert_split(d, true);
+    GemmEpilogue e;
+    e.kind = EPI_STORE_F32;
+    e.ldc = ldp;
+    if (cs.ks > 1) {
+        e.c = part;
+        e.ksplit = cs.ks;
+        e.split_stride = T * ldp;
+    } else {
+        e.c = P;
+    }
+    gemm_bf16(st, T, N, d, GemmOperand{h, d, false}, GemmOperand{wg, d, false}, e);
+    if (cs.ks > 1) {
+        k_sum_partials<<<int(std::min<int64_t>((T * ldp + 255) / 256, num_sms() * 8)), 256, 0, st>>>(part, cs.ks, T * ldp,
+                                                                                                     P);
+        check_launch("k_sum_partials");
+    }
+    return cs.cb;
+}
+
 size_t cert_workspace_bytes(int64_t T, int64_t d, int64_t M, int64_t N, int64_t kk_eff) {
     const int64_t E = M / N;
     size_t b = 0;
     auto add = [&](size_t x) { b += (x + 255) & ~size_t(255); };
     add(T * round_up(N, 4) * 4);  // approximate router scores (fp32)
+    add(T * round_up(N, 4) * 4 * cert_split(d, true).ks);  // their K-chunk partials
     add((T + N + M) * 4);         // row norms of h, w_g, keys
     add((T + N + M) * 4);         // their minimum LSB exponents
     add(T * kk_eff * 4);          // tau
@@ -506,6 +541,7 @@ static void ke_select_certified(cudaStream_t st, const void* h_, const void* w_g
         return r;
     };
     float* P = static_cast<float*>(take_buf(T * ldp * 4));
+    float* Ppart = static_cast<float*>(take_buf(T * ldp * 4 * cert_split(d, true).ks));
     float* hn = static_cast<float*>(take_buf((T + N + M) * 4));
     float* gn = hn + T;
     float* kn = gn + N;
@@ -547,11 +583,7 @@ static void ke_select_certified(cudaStream_t st, const void* h_, const void* w_g
     } else {
         k_row_norms<<<int((N * 32 + 255) / 256), 256, 0, st>>>(wg, N, int(d), gn, gl);
         check_launch("k_row_norms");
-        GemmEpilogue e;  // approximate router scores on the tensor cores
-        e.kind = EPI_STORE_F32;
-        e.c = P;
-        e.ldc = ldp;
-        gemm_bf16(st, T, N, d, GemmOperand{h, d, false}, GemmOperand{wg, d, false}, e);
+        const double cbr = router_scores(st, h, wg, T, N, d, ldp, P, Ppart);  // approximate, on the tensor cores
         MEFT_CUDA_CHECK(cudaMemsetAsync(counts, 0, N * 4, st));
         const int wpb = 4;
         const size_t rsm = size_t(wpb) * (kk_eff + 2 * N) * 4 + size_t(wpb) * N * 8;
@@ -561,7 +593,7 @@ static void ke_select_certified(cudaStream_t st, const void* h_, const void* w_g
                                                  200 * 1024));
             rattr = true;
         }
-        k_router_certified<<<int((T + wpb - 1) / wpb), wpb * 32, rsm, st>>>(P, int(ldp), hn, gn, hl, gl, cb, h, wg,
+        k_router_certified<<<int((T + wpb - 1) / wpb), wpb * 32, rsm, st>>>(P, int(ldp), hn, gn, hl, gl, cbr, h, wg,
                                                                           int(d),
                                                                           int(T), int(N), int(kk_eff), tau, counts,
                                                                           stats);
@@ -757,10 +789,10 @@ void row_stats(cudaStream_t st, const uint16_t* x, int64_t rows, int64_t d, floa
 }
 
 size_t route_workspace_bytes(int64_t T, int64_t d, int64_t N) {
-    (void)d;
     size_t b = 0;
     auto add = [&](size_t x) { b += (x + 255) & ~size_t(255); };
     add(T * round_up(N, 4) * 4);
+    add(T * round_up(N, 4) * 4 * cert_split(d, true).ks);
     add((T + N) * 4);
     add((T + N) * 4);
     add((N + 1) * 4);
@@ -778,6 +810,7 @@ void route_certified(cudaStream_t st, const uint16_t* h, const uint16_t* w_g, in
         return r;
     };
     float* P = static_cast<float*>(take_buf(T * ldp * 4));
+    float* Ppart = static_cast<float*>(take_buf(T * ldp * 4 * cert_split(d, true).ks));
     float* hn = static_cast<float*>(take_buf((T + N) * 4));
     float* gn = hn + T;
     int32_t* hl = static_cast<int32_t*>(take_buf((T + N) * 4));
@@ -785,11 +818,7 @@ void route_certified(cudaStream_t st, const uint16_t* h, const uint16_t* w_g, in
     int32_t* counts = static_cast<int32_t*>(take_buf((N + 1) * 4));
     row_stats(st, h, T, d, hn, hl);
     row_stats(st, w_g, N, d, gn, gl);
-    GemmEpilogue e;
-    e.kind = EPI_STORE_F32;
-    e.c = P;
-    e.ldc = ldp;
-    gemm_bf16(st, T, N, d, GemmOperand{h, d, false}, GemmOperand{w_g, d, false}, e);
+    const double cbr = router_scores(st, h, w_g, T, N, d, ldp, P, Ppart);
     MEFT_CUDA_CHECK(cudaMemsetAsync(counts, 0, N * 4, st));
     const int wpb = 4;
     const size_t rsm = size_t(wpb) * (kk_eff + 2 * N) * 4 + size_t(wpb) * N * 8;
@@ -799,7 +828,7 @@ void route_certified(cudaStream_t st, const uint16_t* h, const uint16_t* w_g, in
         rattr = true;
     }
     k_router_certified<<<int((T + wpb - 1) / wpb), wpb * 32, rsm, st>>>(P, int(ldp), hn, gn, hl, gl,
-                                                                      cert_bound_coeff(int(d)), h, w_g, int(d), int(T),
+                                                                      cbr, h, w_g, int(d), int(T),
                                                                       int(N), int(kk_eff), tau, counts, stats);
     check_launch("k_router_certified");
 }
@@ -814,13 +843,6 @@ size_t score_workspace_bytes(int64_t R, int64_t d, int64_t n_experts, int64_t E)
     return b;
 }
 
-__global__ void k_sum_partials(const float* __restrict__ part, int ks, int64_t n, float* __restrict__ out) {
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        double s = 0.0;
-        for (int p = 0; p < ks; ++p) s += double(part[p * n + i]);
-        out[i] = float(s);
-    }
-}
 
 void score_candidates(cudaStream_t st, const uint16_t* rows, const int32_t* expert, int64_t R, int64_t d,
                       const uint16_t* keys, int64_t n_experts, int64_t E, void* ws, float* cand) {
