@@ -224,3 +224,32 @@ def test_gemm_sm_reserve_is_bitwise_neutral(ctx):
             _lib.check(_lib.lib().meft_set_gemm_sm_reserve(0))
     for a, b in zip(*outs):
         np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("T,kk,K", [(300, 4, 32), (77, 2, 48)])
+def test_layer_step_ragged_vs_live_reference(ctx, T, kk, K):
+    """A ragged token count against the compiled reference's own layer step (oracle/_ref ref_layer_step:
+    meft_ffn -> sparse_backward -> scatter_grads -> sparse_adam_update, fp64) run live on the same inputs."""
+    d, M, N, lr = 512, 4096, 64, 1e-3
+    w_a, w_g, w_b, h, gr = cfg1_inputs(d, M, N, T)
+    ref = O.RefStore(1, d, M, N, seed=1)
+    ref.set(0, "w_a", w_a)
+    ref.set(0, "w_g", w_g)
+    ref.set(0, "w_b", w_b)
+    want = ref.layer_step(0, h, gr, kk, K, lr)
+    sel = O.ke_select(h, w_g, w_a, kk, K)
+    st = make_store(ctx, w_a, w_g, w_b, N)
+    out = torch.empty((T, d), dtype=torch.float32, device="cuda")
+    gh = torch.empty_like(out)
+    res = st.layer_step(0, bf16_dev(h), bf16_dev(gr), kk, K, lr, out=out, grad_h=gh, want_selection=True)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(res["per_token"].cpu().numpy(), sel["per_token"])
+    assert res["union_size"] == want["union_size"] == len(sel["unioned"])
+    assert rel(out.cpu().numpy(), want["out"]) < BF16_TOL
+    assert rel(gh.cpu().numpy(), want["grad_h"]) < BF16_TOL
+    np.testing.assert_array_equal(st.download(0, "pair_step"), ref.pair_step(0))
+    for name, w0 in (("w_a", w_a), ("w_b", w_b)):
+        got, exp = st.download(0, name), ref.get(0, name)
+        err = np.abs((got - w0) - (exp - w0))
+        assert np.all(err <= 2 * lr + 1e-6)
+        assert (err <= 1e-2 * lr + 1e-6 * np.abs(exp)).mean() > 0.99
