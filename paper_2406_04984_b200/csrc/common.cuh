@@ -48,6 +48,18 @@ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 
 int num_sms();  // cached cudaDevAttrMultiProcessorCount of the current device
 
+// Blocks of `kernel` that are co-resident on the whole GPU (SMs x occupancy): the grid for grid-stride loops, so
+// there is never a partial second wave (it doubled the tail of the exact re-scoring kernel: 1.33 waves).
+template <class K>
+int resident_grid(K kernel, int block, size_t smem = 0) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem) != cudaSuccess || per_sm < 1) {
+        cudaGetLastError();
+        per_sm = 1;
+    }
+    return num_sms() * per_sm;
+}
+
 // ------------------------------------------------------------------ bf16 helpers
 
 __device__ __forceinline__ float bf16_bits_to_f32(uint16_t b) { return __uint_as_float(uint32_t(b) << 16); }

@@ -648,7 +648,8 @@ static void ke_select_certified(cudaStream_t st, const void* h_, const void* w_g
     check_launch("k_bucket_scan");
     k_amb_fill<<<int(T), 128, 0, st>>>(amb, n_amb, int(C), int(E), aoff, acur, pair_t, pair_a);
     check_launch("k_amb_fill");
-    k_rescore_pairs<<<num_sms() * 8, 256, 0, st>>>(pair_t, pair_a, aoff + N, amb, int(C), h, keys, int(d), hn, kn, hl,
+    static const int rescore_grid = resident_grid(k_rescore_pairs, 256);
+    k_rescore_pairs<<<rescore_grid, 256, 0, st>>>(pair_t, pair_a, aoff + N, amb, int(C), h, keys, int(d), hn, kn, hl,
                                                     kl, xs, stats);
     check_launch("k_rescore_pairs");
     k_topk_finalize<<<int(T), 128, size_t(TP2) * 4, st>>>(sure, n_sure, amb, n_amb, xs, int(C), int(take), TP2,
@@ -893,7 +894,8 @@ void exact_pair_scores(cudaStream_t st, const uint16_t* rows, const float* rn, c
                        const uint16_t* keys, const float* kn, const int32_t* kl, const int32_t* pair_row,
                        const int32_t* pair_key, int64_t Q, int64_t d, double* out, int32_t* stats) {
     if (Q <= 0) return;
-    const int grid = std::max(1, std::min<int>(int((Q * 32 + 255) / 256), num_sms() * 8));
+    static const int resident = resident_grid(k_exact_pairs, 256);
+    const int grid = std::max(1, std::min<int>(int((Q * 32 + 255) / 256), resident));
     k_exact_pairs<<<grid, 256, 0, st>>>(rows, rn, rl, keys, kn, kl, pair_row, pair_key, int(Q), int(d), out, stats);
     check_launch("k_exact_pairs");
 }
