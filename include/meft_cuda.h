@@ -367,6 +367,15 @@ typedef struct meft_step_info {
     int64_t router_flops, expert_scoring_flops;
 } meft_step_info;
 
+/* The frozen base FFN of the layer (BaseFfn, adapter.hpp:11-16) in bf16 on the device, reference layouts:
+ * w_in [d x n], w_out [n x d] (row-major, n % 8 == 0); act 0 = SiLU (the default), 1 = ReLU. */
+typedef struct meft_base_ffn {
+    const uint16_t* w_in;
+    const uint16_t* w_out;
+    int64_t n;
+    int act;
+} meft_base_ffn;
+
 /* One MEFT layer training step in MIXED precision, the trainer's per-layer sequence
  * (trainer.cpp:220,270,283,525): meft_ffn (ke_select -> fetch -> sparse_ffn_pa) -> sparse_backward ->
  * scatter_grads -> sparse_adam_update. h and grad_out are bf16 [T x d] on device; out and grad_h are f32
@@ -379,6 +388,13 @@ meft_status meft_layer_step(meft_ctx* ctx, meft_store* store, int64_t layer, con
 
 /* Same step from HOST buffers (pinned or pageable): copies h/grad_out in and out/grad_h back inside the
  * call; returns when the results are on the host. */
+/* meft_layer_step with the frozen base FFN (sparse_ffn_pa / sparse_backward with a real BaseFfn,
+ * adapter.cpp:118-120, 153-164): out = act(h w_in) w_out + adapter; grad_h = ((G w_out^T) .* act'(pre)) w_in^T +
+ * adapter part. The base weights receive no gradient (frozen). base == NULL or base->n == 0: meft_layer_step. */
+meft_status meft_layer_step_base(meft_ctx* ctx, meft_store* store, int64_t layer, const void* h, const void* grad_out,
+                                 int64_t T, int64_t kk, int64_t k, double beta1, double beta2, double eps, double lr,
+                                 float* out, float* grad_h, int32_t* per_token, int32_t* union_idx,
+                                 meft_step_info* info, const meft_base_ffn* base);
 meft_status meft_layer_step_host(meft_ctx* ctx, meft_store* store, int64_t layer, const uint16_t* h_host,
                                  const uint16_t* grad_out_host, int64_t T, int64_t kk, int64_t k, double beta1,
                                  double beta2, double eps, double lr, float* out_host, float* grad_h_host,

@@ -16,6 +16,11 @@ I32P = C.POINTER(C.c_int32)
 D = C.c_double
 INT = C.c_int
 
+class BaseFfn(C.Structure):
+    """meft_base_ffn (include/meft_cuda.h): frozen base FFN, bf16 device w_in [d x n], w_out [n x d]."""
+    _fields_ = [("w_in", P), ("w_out", P), ("n", I64), ("act", INT)]
+
+
 class PeerOut(C.Structure):
     """meft_peer_out (include/meft_cuda.h)."""
     _fields_ = [("world", INT), ("rank", INT), ("rows", I64), ("out_recv", P * 8), ("grad_h_recv", P * 8)]
@@ -97,6 +102,7 @@ _SIGS = {
     "meft_scatter_grads": (INT, [P, P, I64, P, I64, P, P, INT]),
     "meft_sparse_adam_update": (INT, [P, P, I64, D, D, D, D]),
     "meft_layer_step": (INT, [P, P, I64, P, P, I64, I64, I64, D, D, D, D, P, P, P, P, P]),
+    "meft_layer_step_base": (INT, [P, P, I64, P, P, I64, I64, I64, D, D, D, D, P, P, P, P, P, P]),
     "meft_layer_step_host": (INT, [P, P, I64, P, P, I64, I64, I64, D, D, D, D, P, P, P]),
 }
 

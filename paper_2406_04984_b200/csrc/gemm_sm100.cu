@@ -58,6 +58,10 @@ struct KArgs {
     const int32_t* b_idx;
     int b_idx_n, b_oob_row;
     const int32_t* kb_run;  // MN-major gathered B: per k-block first table row of a contiguous run, or -1
+    // EPI_ACT_BF16 / EPI_DACT_BF16
+    uint16_t* aux;
+    long long ldaux;
+    int act;
     // EPI_PEER_F32 (see kernels.h)
     float* peer[kMaxPeers];
     long long peer_rows, row0, col0;
@@ -263,6 +267,31 @@ __device__ __forceinline__ void epilogue_chunk(const KArgs& a, int m, int n, con
                 }
             } else {
                 for (int j = 0; j < cnt; ++j) c[j] = mk[j] ? f32_to_bf16_bits(__uint_as_float(r[j])) : 0;
+            }
+            break;
+        }
+        case EPI_ACT_BF16:
+        case EPI_DACT_BF16: {  // frozen base FFN: activation forward / its derivative times the incoming gradient
+            uint16_t* c = reinterpret_cast<uint16_t*>(a.c) + (long long)m * a.ldc + n;
+            uint16_t* x = a.aux + (long long)m * a.ldaux + n;
+            for (int j = 0; j < cnt; ++j) {
+                const float v = __uint_as_float(r[j]);
+                if (a.epi == EPI_ACT_BF16) {
+                    const uint16_t pre = f32_to_bf16_bits(v);
+                    x[j] = pre;
+                    const float p = v;
+                    c[j] = f32_to_bf16_bits(a.act == 1 ? (p > 0.f ? p : 0.f) : p / (1.f + __expf(-p)));
+                } else {
+                    const float p = bf16_bits_to_f32(x[j]);
+                    float dv;
+                    if (a.act == 1) {
+                        dv = p > 0.f ? v : 0.f;
+                    } else {
+                        const float sg = 1.f / (1.f + __expf(-p));
+                        dv = v * (sg * (1.f + p * (1.f - sg)));
+                    }
+                    c[j] = f32_to_bf16_bits(dv);
+                }
             }
             break;
         }
@@ -749,6 +778,9 @@ void check_epilogue(const GemmEpilogue& epi) {
     }
     if (epi.kind == EPI_MASK_BF16 && (!aligned16(epi.mask) || (epi.ldm % 8)))
         throw MeftError(2, "gemm_bf16: mask alignment");
+    if ((epi.kind == EPI_ACT_BF16 || epi.kind == EPI_DACT_BF16) && (!epi.aux || epi.ldaux < 1 || epi.act < 0 ||
+                                                                   epi.act > 1))
+        throw MeftError(2, "gemm_bf16: activation epilogue needs aux [M x ldaux] and act in {0: SiLU, 1: ReLU}");
 }
 
 KArgs base_args(int64_t M, int64_t N, int64_t K, const GemmEpilogue& epi) {
@@ -770,6 +802,9 @@ KArgs base_args(int64_t M, int64_t N, int64_t K, const GemmEpilogue& epi) {
     args.b_idx = nullptr;
     args.kb_run = nullptr;
     for (int i = 0; i < kMaxPeers; ++i) args.peer[i] = i < epi.peer_count ? epi.peer[i] : nullptr;
+    args.aux = static_cast<uint16_t*>(epi.aux);
+    args.ldaux = epi.ldaux;
+    args.act = epi.act;
     args.peer_rows = epi.peer_rows;
     args.row0 = epi.row0;
     args.col0 = epi.col0;
@@ -947,6 +982,7 @@ void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOpera
                     e.c = const_cast<void*>(advance(epi.c, m0 * epi.ldc + n0, ce));
                 }
                 if (epi.mask) e.mask = advance(epi.mask, m0 * epi.ldm + n0, 2);
+                if (epi.aux) e.aux = const_cast<void*>(advance(epi.aux, m0 * epi.ldaux + n0, 2));
                 gemm_bf16_one(st, ml, nl, kl, a, b, e);
             }
         }

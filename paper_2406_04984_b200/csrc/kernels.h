@@ -31,6 +31,9 @@ enum GemmEpi : int {
     // home's receive buffer peer[h] (device pointer, NVLink peer-mapped for h != this rank) at slot peer_slot:
     // peer[h][(peer_slot * peer_rows + g % peer_rows) * ldc + col0 + n]. A reduce-scatter fused into the epilogue.
     EPI_PEER_F32 = 5,
+    // Frozen base FFN (adapter.cpp:118-120, 153-164): act = 0 SiLU, 1 ReLU.
+    EPI_ACT_BF16 = 6,   // C bf16 = act(acc); aux bf16 [M x ldaux] = acc (the pre-activation, kept for backward)
+    EPI_DACT_BF16 = 7,  // C bf16 = acc * act'(aux)   (aux: the stored pre-activation)
 };
 constexpr int kMaxPeers = 8;
 
@@ -46,6 +49,10 @@ struct GemmEpilogue {
     // partial product to c + s * split_stride (elements); the caller sums the partials.
     int ksplit = 1;
     int64_t split_stride = 0;
+    // EPI_ACT_BF16 / EPI_DACT_BF16
+    void* aux = nullptr;
+    int64_t ldaux = 0;
+    int act = 0;
     // EPI_PEER_F32
     float* peer[kMaxPeers] = {};
     int peer_count = 0;

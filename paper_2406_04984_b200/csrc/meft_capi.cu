@@ -1160,14 +1160,15 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
                             const int32_t* uni, int64_t su, int64_t holes, double b1, double b2, double eps,
                             double lr, float* out, float* grad_h, cudaEvent_t g_ready, cudaEvent_t fwd_done,
                             cudaEvent_t gh_done = nullptr, const int32_t* tau = nullptr, int64_t kk_eff = 0,
-                            const meft_peer_out* peer = nullptr);
+                            const meft_peer_out* peer = nullptr, const meft_base_ffn* base = nullptr);
 
 static void ensure_key_stats(meft_ctx* ctx, meft_store* s, int64_t layer);
 
 static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const void* h, const void* g, int64_t T,
                             int64_t kk, int64_t k, double b1, double b2, double eps, double lr, float* out,
                             float* grad_h, int32_t* per_token_user, int32_t* union_user, meft_step_info* info,
-                            cudaEvent_t g_ready, cudaEvent_t fwd_done, cudaEvent_t gh_done = nullptr) {
+                            cudaEvent_t g_ready, cudaEvent_t fwd_done, cudaEvent_t gh_done = nullptr,
+                            const meft_base_ffn* base = nullptr) {
     const long long launches0 = launch_counter();
     const LayerBufs& L = layer_of(s, layer);
     require(s->prec == MEFT_STORE_MIXED, MEFT_E_INVALID, "layer_step: requires a MIXED precision store");
@@ -1200,7 +1201,7 @@ static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
     MEFT_CUDA_CHECK(cudaStreamSynchronize(st));
     const int64_t su = ctx->host_small[4];
     ffn_update_impl(ctx, s, layer, h, g, T, uni, su, ctx->host_small[7], b1, b2, eps, lr, out, grad_h, g_ready,
-                    fwd_done, gh_done, s->train_router ? tau : nullptr, kk_eff);
+                    fwd_done, gh_done, s->train_router ? tau : nullptr, kk_eff, nullptr, base);
 
     if (info) {
         info->union_size = su;
@@ -1268,7 +1269,8 @@ static void router_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, cons
 static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const void* h, const void* g, int64_t T,
                             const int32_t* uni, int64_t su, int64_t holes, double b1, double b2, double eps,
                             double lr, float* out, float* grad_h, cudaEvent_t g_ready, cudaEvent_t fwd_done,
-                            cudaEvent_t gh_done, const int32_t* tau, int64_t kk_eff, const meft_peer_out* peer) {
+                            cudaEvent_t gh_done, const int32_t* tau, int64_t kk_eff, const meft_peer_out* peer,
+                            const meft_base_ffn* base) {
     const LayerBufs& L = layer_of(s, layer);
     const int64_t d = s->d;
     cudaStream_t st = ctx->stream;
@@ -1303,16 +1305,56 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
         vs = vsb;
     }
 
-    // sparse_ffn_pa adapter term (adapter.cpp:122-126), every token against the whole union
+    // sparse_ffn_pa: the frozen base FFN first (adapter.cpp:118-120), then the adapter term (122-126) added onto
+    // it; every token against the whole union
+    if (base && base->n == 0) base = nullptr;
+    require(!(base && peer), MEFT_E_INVALID, "layer step: the base FFN runs on the token home, not with peer outputs");
+    const int64_t ldn = base ? round_up(base->n, 8) : 0;
+    uint16_t* base_pre = base ? static_cast<uint16_t*>(ctx->get("base_pre", size_t(T * ldn) * 2)) : nullptr;
     {
         PhaseScope ps(ctx, 2);
-        ffn_forward_impl(ctx, MEFT_BF16, h, ks, vs, T, d, su, ld, act, outb, false, rg, peer);
+        if (base) {
+            require(base->w_in && base->w_out && base->n % 8 == 0 && (base->act == 0 || base->act == 1),
+                    MEFT_E_INVALID, "base FFN: w_in / w_out, n % 8 == 0, act 0 (SiLU) or 1 (ReLU)");
+            uint16_t* base_act = static_cast<uint16_t*>(ctx->get("base_act", size_t(T * ldn) * 2));
+            GemmEpilogue e1;  // pre = h w_in (kept for the backward), act(pre)
+            e1.kind = EPI_ACT_BF16;
+            e1.c = base_act;
+            e1.ldc = ldn;
+            e1.aux = base_pre;
+            e1.ldaux = ldn;
+            e1.act = base->act;
+            gemm_bf16(st, T, base->n, d, GemmOperand{h, d, false}, GemmOperand{base->w_in, base->n, true}, e1);
+            GemmEpilogue e2;  // out = act(pre) w_out
+            e2.kind = EPI_STORE_F32;
+            e2.c = outb;
+            e2.ldc = d;
+            gemm_bf16(st, T, d, base->n, GemmOperand{base_act, ldn, false}, GemmOperand{base->w_out, d, true}, e2);
+        }
+        ffn_forward_impl(ctx, MEFT_BF16, h, ks, vs, T, d, su, ld, act, outb, base != nullptr, rg, peer);
     }
     if (fwd_done) MEFT_CUDA_CHECK(cudaEventRecord(fwd_done, st));
     if (g_ready) MEFT_CUDA_CHECK(cudaStreamWaitEvent(st, g_ready, 0));
 
     const bool stats_valid = s->key_stats_valid[size_t(layer)] != 0;
     require(!s->train_router || tau != nullptr, MEFT_E_LOGIC, "router training runs on the single-GPU layer step");
+    if (base) {  // frozen-base backward (adapter.cpp:153-164): grad_h = ((G w_out^T) .* act'(pre)) w_in^T, first
+        PhaseScope ps(ctx, 3);
+        uint16_t* dpre = static_cast<uint16_t*>(ctx->get("base_dpre", size_t(T * ldn) * 2));
+        GemmEpilogue e1;
+        e1.kind = EPI_DACT_BF16;
+        e1.c = dpre;
+        e1.ldc = ldn;
+        e1.aux = base_pre;
+        e1.ldaux = ldn;
+        e1.act = base->act;
+        gemm_bf16(st, T, base->n, d, GemmOperand{g, d, false}, GemmOperand{base->w_out, d, false}, e1);
+        GemmEpilogue e2;
+        e2.kind = EPI_STORE_F32;
+        e2.c = ghb;
+        e2.ldc = d;
+        gemm_bf16(st, T, d, base->n, GemmOperand{dpre, ldn, false}, GemmOperand{base->w_in, base->n, false}, e2);
+    }
     auto train_router = [&] {  // after the backward: it reads act and masked
         if (s->train_router)
             router_update_impl(ctx, s, layer, static_cast<const uint16_t*>(h), act, masked, ld, uni, su, tau, T,
@@ -1324,8 +1366,8 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
         ensure_staging(s, layer);
         {
             PhaseScope ps(ctx, 3);
-            ffn_backward_impl(ctx, MEFT_BF16, g, h, act, ks, vs, T, d, su, ld, masked, nullptr, nullptr, ghb, false,
-                              uni, L.st_a, L.st_b, rg, gh_done, nullptr, peer);
+            ffn_backward_impl(ctx, MEFT_BF16, g, h, act, ks, vs, T, d, su, ld, masked, nullptr, nullptr, ghb,
+                              base != nullptr, uni, L.st_a, L.st_b, rg, gh_done, nullptr, peer);
         }
         train_router();
         PhaseScope ps(ctx, 4);
@@ -1353,8 +1395,8 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
             if (su > 0) adam_table(2);
             p3.emplace(ctx, 3);
         };
-        ffn_backward_impl(ctx, MEFT_BF16, g, h, act, ks, vs, T, d, su, ld, masked, gblk, gblk, ghb, false, nullptr,
-                          nullptr, nullptr, rg, gh_done, &values_step, peer);
+        ffn_backward_impl(ctx, MEFT_BF16, g, h, act, ks, vs, T, d, su, ld, masked, gblk, gblk, ghb, base != nullptr,
+                          nullptr, nullptr, nullptr, rg, gh_done, &values_step, peer);
         p3.reset();
         train_router();
         if (su > 0) adam_table(1);
@@ -1509,6 +1551,18 @@ meft_status meft_layer_step(meft_ctx* ctx, meft_store* s, int64_t layer, const v
         require(T >= 1, MEFT_E_SHAPE, "layer_step: no tokens");
         layer_step_impl(ctx, s, layer, h, grad_out, T, kk, k, beta1, beta2, eps, lr, out, grad_h, per_token, union_idx,
                         info, nullptr, nullptr);
+    });
+}
+
+meft_status meft_layer_step_base(meft_ctx* ctx, meft_store* s, int64_t layer, const void* h, const void* grad_out,
+                                 int64_t T, int64_t kk, int64_t k, double beta1, double beta2, double eps, double lr,
+                                 float* out, float* grad_h, int32_t* per_token, int32_t* union_idx,
+                                 meft_step_info* info, const meft_base_ffn* base) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(T >= 1, MEFT_E_SHAPE, "layer_step: no tokens");
+        layer_step_impl(ctx, s, layer, h, grad_out, T, kk, k, beta1, beta2, eps, lr, out, grad_h, per_token, union_idx,
+                        info, nullptr, nullptr, nullptr, base);
     });
 }
 

@@ -338,16 +338,26 @@ class Store:
         self.ctx.check(lib().meft_sparse_adam_update(self.ctx.h, self.h, layer, beta1, beta2, eps, lr))
 
     def layer_step(self, layer, h, grad_out, kk, k, lr, beta1=0.9, beta2=0.999, eps=1e-8, out=None, grad_h=None,
-                   want_selection=False):
-        """meft_ffn -> sparse_backward -> scatter_grads -> sparse_adam_update on device buffers (bf16 in)."""
+                   want_selection=False, base=None):
+        """meft_ffn -> sparse_backward -> scatter_grads -> sparse_adam_update on device buffers (bf16 in).
+        base = (w_in bf16 [d x n], w_out bf16 [n x d], act 0 SiLU / 1 ReLU): the frozen base FFN as well."""
         _contig(h, grad_out)
         T, d = h.shape
         take, _, _ = selection_shape(self.pairs, self.experts, kk, k)
         per = torch.empty((T, take), dtype=torch.int32, device=h.device) if want_selection else None
         uni = torch.empty(self.pairs, dtype=torch.int32, device=h.device) if want_selection else None
         info = _lib.StepInfo()
-        self.ctx.check(lib().meft_layer_step(self.ctx.h, self.h, layer, _p(h), _p(grad_out), T, kk, k, beta1, beta2,
-                                             eps, lr, _p(out), _p(grad_h), _p(per), _p(uni), C.byref(info)))
+        if base is None:
+            self.ctx.check(lib().meft_layer_step(self.ctx.h, self.h, layer, _p(h), _p(grad_out), T, kk, k, beta1,
+                                                 beta2, eps, lr, _p(out), _p(grad_h), _p(per), _p(uni),
+                                                 C.byref(info)))
+        else:
+            w_in, w_out, act = base
+            _contig(w_in, w_out)
+            bf = _lib.BaseFfn(w_in.data_ptr(), w_out.data_ptr(), w_in.shape[1], act)
+            self.ctx.check(lib().meft_layer_step_base(self.ctx.h, self.h, layer, _p(h), _p(grad_out), T, kk, k, beta1,
+                                                      beta2, eps, lr, _p(out), _p(grad_h), _p(per), _p(uni),
+                                                      C.byref(info), C.byref(bf)))
         res = {name: getattr(info, name) for name, _ in _lib.StepInfo._fields_}
         res["warned"] = bool(info.warned)
         if want_selection:

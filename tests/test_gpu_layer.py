@@ -253,3 +253,27 @@ def test_layer_step_ragged_vs_live_reference(ctx, T, kk, K):
         err = np.abs((got - w0) - (exp - w0))
         assert np.all(err <= 2 * lr + 1e-6)
         assert (err <= 1e-2 * lr + 1e-6 * np.abs(exp)).mean() > 0.99
+
+
+@pytest.mark.parametrize("act", [0, 1])  # SiLU (the reference default), ReLU
+def test_layer_step_with_frozen_base_ffn(ctx, act):
+    """sparse_ffn_pa / sparse_backward with a real BaseFfn (adapter.cpp:118-120, 153-164) on the fused step:
+    out = act(h w_in) w_out + adapter, grad_h = base part + adapter part, against the fp64 oracle."""
+    d, M, N, K, kk, T, n = 512, 4096, 64, 32, 4, 256, 1024
+    w_a, w_g, w_b, h, gr = cfg1_inputs(d, M, N, T)
+    rs = np.random.RandomState(3)
+    w_in = O.bf16_round(rs.uniform(-1, 1, (d, n)) / np.sqrt(d))
+    w_out = O.bf16_round(rs.uniform(-1, 1, (n, d)) / np.sqrt(n))
+    sel = O.ke_select(h, w_g, w_a, kk, K)
+    wak, wbk = O.gather_adapter(w_a, w_b, sel["unioned"])
+    want_out, z, pre = O.ffn_forward(h, wak, wbk, w_in, w_out, act)
+    _, _, want_gh = O.ffn_backward(gr, h, z, pre, wak, wbk, w_in, w_out, act)
+    st = make_store(ctx, w_a, w_g, w_b, N)
+    out = torch.empty((T, d), dtype=torch.float32, device="cuda")
+    gh = torch.empty_like(out)
+    res = st.layer_step(0, bf16_dev(h), bf16_dev(gr), kk, K, 1e-3, out=out, grad_h=gh, want_selection=True,
+                        base=(bf16_dev(w_in), bf16_dev(w_out), act))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(res["per_token"].cpu().numpy(), sel["per_token"])
+    assert rel(out.cpu().numpy(), want_out) < BF16_TOL
+    assert rel(gh.cpu().numpy(), want_gh) < BF16_TOL
