@@ -209,8 +209,16 @@ def our_arm(args, rank, world, local_rank):
         store.tensor(0, "w_b_compute").copy_(w_b.to(torch.bfloat16))
         del w_b
 
+        base = None
+        if args.base_ffn:  # the frozen base FFN of the layer too (optional n = 11008 run)
+            bgen = torch.Generator(device=dev).manual_seed(0x7004)
+            w_in = ((torch.rand((d, args.base_ffn), generator=bgen, device=dev) * 2 - 1) / math.sqrt(d)).to(torch.bfloat16)
+            w_out = ((torch.rand((args.base_ffn, d), generator=bgen, device=dev) * 2 - 1)
+                     / math.sqrt(args.base_ffn)).to(torch.bfloat16)
+            base = (w_in, w_out, 0)
+
         def step():
-            return store.layer_step(0, h, g, kk, K, lr, out=out, grad_h=grad_h)
+            return store.layer_step(0, h, g, kk, K, lr, out=out, grad_h=grad_h, base=base)
     else:
         # expert-sharded layer: this rank owns N/P experts and M/P pairs; tokens are exchanged over NCCL
         from paper_2406_04984_b200 import sharded as SH
@@ -357,6 +365,7 @@ def our_arm(args, rank, world, local_rank):
         "config": dict(workload=CFG["workload"], d=d, pairs=M, experts=N, k=K, kk=kk, tokens_per_gpu=T,
                        global_tokens=T * world,
                        parallelism="single GPU" if not sharded else f"expert-sharded ep{world} (NCCL all-to-all)",
+                       base_ffn=args.base_ffn,
                        precision="bf16 compute, fp32 "
                        "master/Adam state", l2="inputs larger than L2 (7.5 GB of tables per layer)",
                        union_size=S),
@@ -413,6 +422,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--skip-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="run the expert-sharded layer even on one GPU")
+    ap.add_argument("--base-ffn", type=int, default=0,
+                    help="also run the frozen base FFN of width n (SiLU), e.g. 11008 for LLaMA-7B (single GPU)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
     world = int(os.environ.get("WORLD_SIZE", "1"))

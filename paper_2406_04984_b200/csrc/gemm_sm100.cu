@@ -274,23 +274,44 @@ __device__ __forceinline__ void epilogue_chunk(const KArgs& a, int m, int n, con
         case EPI_DACT_BF16: {  // frozen base FFN: activation forward / its derivative times the incoming gradient
             uint16_t* c = reinterpret_cast<uint16_t*>(a.c) + (long long)m * a.ldc + n;
             uint16_t* x = a.aux + (long long)m * a.ldaux + n;
-            for (int j = 0; j < cnt; ++j) {
-                const float v = __uint_as_float(r[j]);
-                if (a.epi == EPI_ACT_BF16) {
-                    const uint16_t pre = f32_to_bf16_bits(v);
-                    x[j] = pre;
-                    const float p = v;
-                    c[j] = f32_to_bf16_bits(a.act == 1 ? (p > 0.f ? p : 0.f) : p / (1.f + __expf(-p)));
-                } else {
-                    const float p = bf16_bits_to_f32(x[j]);
-                    float dv;
-                    if (a.act == 1) {
-                        dv = p > 0.f ? v : 0.f;
-                    } else {
-                        const float sg = 1.f / (1.f + __expf(-p));
-                        dv = v * (sg * (1.f + p * (1.f - sg)));
+            auto act_f = [&](float p) { return a.act == 1 ? (p > 0.f ? p : 0.f) : p / (1.f + __expf(-p)); };
+            auto dact_f = [&](float v, float p) {
+                if (a.act == 1) return p > 0.f ? v : 0.f;
+                const float sg = 1.f / (1.f + __expf(-p));
+                return v * (sg * (1.f + p * (1.f - sg)));
+            };
+            const bool vec = cnt == 32 && ((reinterpret_cast<uintptr_t>(c) | reinterpret_cast<uintptr_t>(x)) % 16 == 0);
+            if (vec) {  // 4 x 16-byte accesses of 8 bf16 per row chunk
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    uint32_t cw[4], xw[4];
+                    if (a.epi == EPI_DACT_BF16) {
+                        const uint4 xv = reinterpret_cast<const uint4*>(x)[q];
+                        xw[0] = xv.x, xw[1] = xv.y, xw[2] = xv.z, xw[3] = xv.w;
                     }
-                    c[j] = f32_to_bf16_bits(dv);
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) {
+                        const float v0 = __uint_as_float(r[8 * q + 2 * w]), v1 = __uint_as_float(r[8 * q + 2 * w + 1]);
+                        if (a.epi == EPI_ACT_BF16) {
+                            xw[w] = pack_bf16x2(f32_to_bf16_bits(v0), f32_to_bf16_bits(v1));
+                            cw[w] = pack_bf16x2(f32_to_bf16_bits(act_f(v0)), f32_to_bf16_bits(act_f(v1)));
+                        } else {
+                            const float p0 = bf16_bits_to_f32(uint16_t(xw[w])), p1 = bf16_bits_to_f32(uint16_t(xw[w] >> 16));
+                            cw[w] = pack_bf16x2(f32_to_bf16_bits(dact_f(v0, p0)), f32_to_bf16_bits(dact_f(v1, p1)));
+                        }
+                    }
+                    reinterpret_cast<uint4*>(c)[q] = make_uint4(cw[0], cw[1], cw[2], cw[3]);
+                    if (a.epi == EPI_ACT_BF16) reinterpret_cast<uint4*>(x)[q] = make_uint4(xw[0], xw[1], xw[2], xw[3]);
+                }
+            } else {
+                for (int j = 0; j < cnt; ++j) {
+                    const float v = __uint_as_float(r[j]);
+                    if (a.epi == EPI_ACT_BF16) {
+                        x[j] = f32_to_bf16_bits(v);
+                        c[j] = f32_to_bf16_bits(act_f(v));
+                    } else {
+                        c[j] = f32_to_bf16_bits(dact_f(v, bf16_bits_to_f32(x[j])));
+                    }
                 }
             }
             break;
