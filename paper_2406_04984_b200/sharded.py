@@ -193,8 +193,78 @@ class PeerExchange:
         self._opened, self._own = [], []
 
 
+class ThreadGroup:
+    """In-process stand-in for a process group: P threads of ONE process, one per emulated rank, exchange
+    finished device tensors at host-side rendezvous (a barrier), so no kernel ever waits on another rank's
+    kernel -- the way to run the multi-rank device path with fewer GPUs than ranks. Each thread calls
+    ``bind(rank)`` first; the layer's collectives then route here instead of torch.distributed."""
+
+    def __init__(self, world):
+        import threading
+        self.world = world
+        self._barrier = threading.Barrier(world)
+        self._slots = [None] * world
+        self._local = threading.local()
+
+    def bind(self, rank):
+        self._local.rank = rank
+
+    def rank(self):
+        return self._local.rank
+
+    def _publish(self, value):
+        torch.cuda.synchronize()  # the payload is final before any peer reads it
+        self._slots[self.rank()] = value
+        self._barrier.wait()
+        every = list(self._slots)
+        self._barrier.wait()  # everyone has read the slots before they are reused
+        return every
+
+    def all_to_all(self, tensor, send_counts, recv_counts):
+        chunks = list(torch.split(tensor.contiguous(), list(send_counts), 0))
+        every = self._publish(chunks)
+        r = self.rank()
+        return torch.cat([every[src][r].to(tensor.device) for src in range(self.world)], 0)
+
+    def all_gather(self, tensor):
+        return torch.cat([t.to(tensor.device) for t in self._publish(tensor.contiguous().clone())], 0)
+
+    def all_reduce(self, tensor, op="sum"):
+        every = self._publish(tensor.clone())
+        out = every[0].clone()
+        for t in every[1:]:
+            out = torch.maximum(out, t) if op == "max" else (torch.minimum(out, t) if op == "min" else out + t)
+        tensor.copy_(out)
+
+    def reduce_scatter(self, tensor):
+        every = self._publish(tensor.contiguous().clone())
+        n = tensor.shape[0] // self.world
+        r = self.rank()
+        out = every[0][r * n:(r + 1) * n].clone()
+        for t in every[1:]:
+            out += t[r * n:(r + 1) * n]  # slot (source rank) order, like the fused peer fold
+        return out
+
+
+def _world(group):
+    return group.world if isinstance(group, ThreadGroup) else dist.get_world_size(group)
+
+
+def _rank(group):
+    return group.rank() if isinstance(group, ThreadGroup) else dist.get_rank(group)
+
+
+def _all_reduce(tensor, group, op="sum"):
+    if isinstance(group, ThreadGroup):
+        return group.all_reduce(tensor, op)
+    dop = {"sum": dist.ReduceOp.SUM, "max": dist.ReduceOp.MAX, "min": dist.ReduceOp.MIN}[op]
+    dist.all_reduce(tensor, op=dop, group=group)
+
+
 def _a2a(tensor, send_counts, recv_counts, group):
     """all_to_all_single over dim 0 with per-rank row counts (lists of ints)."""
+    if isinstance(group, ThreadGroup):
+        return group.all_to_all(tensor, send_counts, recv_counts)
     out = torch.empty((sum(recv_counts),) + tuple(tensor.shape[1:]), dtype=tensor.dtype, device=tensor.device)
     dist.all_to_all_single(out, tensor.contiguous(), recv_counts, send_counts, group=group)
     return out
@@ -202,22 +272,30 @@ def _a2a(tensor, send_counts, recv_counts, group):
 
 def _exchange_counts(counts, group):
     send = torch.tensor(counts, dtype=torch.int64, device=_comm_device(group))
+    if isinstance(group, ThreadGroup):
+        return group.all_to_all(send, [1] * group.world, [1] * group.world).tolist()
     recv = torch.empty_like(send)
     dist.all_to_all_single(recv, send, group=group)
     return recv.tolist()
 
 
 def _comm_device(group):
-    return torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    if isinstance(group, ThreadGroup) or dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
 
 
 def _all_gather_rows(t, group, world):
+    if isinstance(group, ThreadGroup):
+        return group.all_gather(t)
     parts = [torch.empty_like(t) for _ in range(world)]
     dist.all_gather(parts, t.contiguous(), group=group)
     return torch.cat(parts, 0)
 
 
 def _reduce_scatter_rows(t, group, world, rank):
+    if isinstance(group, ThreadGroup):
+        return group.reduce_scatter(t)
     if dist.get_backend(group) == "nccl":
         out = torch.empty((t.shape[0] // world,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
         dist.reduce_scatter_tensor(out, t.contiguous(), group=group)
@@ -234,15 +312,16 @@ class ShardedLayer:
     def __init__(self, engine, d, M, N, group=None):
         self.eng, self.d, self.M, self.N = engine, d, M, N
         self.group = group
-        self.world = dist.get_world_size(group)
-        self.rank = dist.get_rank(group)
+        self.world = _world(group)
+        self.rank = _rank(group)
         if N % self.world or M % N:
             raise ValueError("N must be divisible by the world size and M by N")
         self.E, self.N_loc, self.M_loc = M // N, N // self.world, M // self.world
         self.last = {}
         # Overlap (device engine over NCCL): the bulk all-gathers / reduce-scatters run on their own stream and
         # communicator, so they proceed while the selection exchanges and the FFN compute.
-        self.overlap = isinstance(engine, DeviceEngine) and dist.get_backend(group) == "nccl"
+        self.overlap = (isinstance(engine, DeviceEngine) and not isinstance(group, ThreadGroup)
+                        and dist.get_backend(group) == "nccl")
         if self.overlap:
             ranks = list(range(self.world)) if group is None else dist.get_process_group_ranks(group)
             self.bulk_group = dist.new_group(ranks=ranks, backend="nccl")
@@ -368,7 +447,7 @@ class ShardedLayer:
         # 7. final per-token selection and the global union
         per_token, flags = eng.finalize(sure, n_sure, amb, n_amb, xs, take, self.M)
         union = flags.to(torch.int32)
-        dist.all_reduce(union, op=dist.ReduceOp.MAX, group=grp)
+        _all_reduce(union, grp, "max")
         S = torch.nonzero(union).flatten()
         S_loc = S[(S >= r * self.M_loc) & (S < (r + 1) * self.M_loc)] - r * self.M_loc
         # 8-9. FFN over all tokens on the local part of the union, partial sums back to the homes
@@ -442,8 +521,8 @@ def make_device_layer(ctx, d, M, N, group=None, seed=1, w_b_seed=0x7001):
     identical on every rank), router replicated."""
     from . import meft as G
 
-    P = dist.get_world_size(group)
-    r = dist.get_rank(group)
+    P = _world(group)
+    r = _rank(group)
     M_loc, N_loc = M // P, N // P
     full = G.Store(ctx, 1, d, M, N, G.STORE_MIXED)
     full.init_reference(seed)

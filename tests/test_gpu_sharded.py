@@ -90,3 +90,63 @@ def test_sharded_world1_peer_path_equals_layer_step(ctx, nccl_world1, monkeypatc
         assert torch.equal(res["out"], out)
         assert torch.equal(res["grad_h"], gh)
     layer.peer.close()
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_sharded_device_path_multirank_emulated(ctx, P):
+    """The expert-sharded step with the DEVICE engine at P ranks, emulated in one process (ThreadGroup: one thread
+    and one context per rank, collectives as host-side exchanges of finished tensors -- no kernel waits on another
+    rank). Against the single-GPU fused step on the same P*T tokens: selection bit for bit, the shards' updated
+    tables bit for bit (each weight-gradient row contracts the same tokens in the same order), out / grad_h to
+    fp32 round-off (partial sums are added per rank)."""
+    import threading
+
+    d, M, N, K, kk, T, lr = 512, 4096, 64, 32, 4, 128, 1e-3
+    gen = torch.Generator(device="cuda").manual_seed(21)
+    h = ((torch.rand((P * T, d), generator=gen, device="cuda") * 2 - 1)).to(torch.bfloat16)
+    g = ((torch.rand((P * T, d), generator=gen, device="cuda") * 2 - 1)).to(torch.bfloat16)
+    # single-GPU reference with the same tables as make_device_layer builds
+    ref = G.Store(ctx, 1, d, M, N, G.STORE_MIXED)
+    ref.init_reference(1)
+    wgen = torch.Generator(device="cuda").manual_seed(0x7001)
+    w_b = (torch.rand((M, d), generator=wgen, device="cuda") * 2 - 1) * (1.0 / d ** 0.5)
+    ref.tensor(0, "w_b").copy_(w_b)
+    ref.tensor(0, "w_b_compute").copy_(w_b.to(torch.bfloat16))
+    out = torch.empty((P * T, d), dtype=torch.float32, device="cuda")
+    gh = torch.empty_like(out)
+    want = ref.layer_step(0, h, g, kk, K, lr, out=out, grad_h=gh, want_selection=True)
+    torch.cuda.synchronize()
+
+    tg = SH.ThreadGroup(P)
+    results, errors = [None] * P, []
+
+    def rank_main(r):
+        try:
+            tg.bind(r)
+            rctx = G.Context(0)
+            eng, store = SH.make_device_layer(rctx, d, M, N, group=tg, seed=1)
+            layer = SH.ShardedLayer(eng, d, M, N, group=tg)
+            res = layer.step(h[r * T:(r + 1) * T].contiguous(), g[r * T:(r + 1) * T].contiguous(), kk, K, lr)
+            torch.cuda.synchronize()
+            results[r] = (res, {n: store.tensor(0, n).clone() for n in ("w_a", "w_b", "m_a", "v_b", "pair_step")},
+                          rctx, store)
+        except Exception as e:  # surfaced below
+            errors.append((r, repr(e)))
+            tg._barrier.abort()
+
+    threads = [threading.Thread(target=rank_main, args=(r,)) for r in range(P)]
+    for t_ in threads:
+        t_.start()
+    for t_ in threads:
+        t_.join(timeout=300)
+    assert not errors, errors
+    M_loc = M // P
+    for r in range(P):
+        res, tabs, _, _ = results[r]
+        assert torch.equal(res["per_token"], want["per_token"][r * T:(r + 1) * T])
+        assert torch.equal(res["unioned"].to(torch.int32), want["unioned"])
+        rows = slice(r * T, (r + 1) * T)
+        assert float((res["out"] - out[rows]).norm() / out[rows].norm()) < 1e-5
+        assert float((res["grad_h"] - gh[rows]).norm() / gh[rows].norm()) < 1e-5
+        for n_, t_ in tabs.items():
+            assert torch.equal(t_, ref.tensor(0, n_)[r * M_loc:(r + 1) * M_loc]), (r, n_)
