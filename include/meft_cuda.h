@@ -118,6 +118,11 @@ meft_status meft_ctx_set_selection(meft_ctx* ctx, int mode);
 #define MEFT_GATHER_KERNEL 1
 #define MEFT_GATHER_TMA 2
 meft_status meft_ctx_set_gather(meft_ctx* ctx, int mode);
+/* The reference runs check_finite on every matmul output and the trainer turns the runtime_error into
+ * DivergenceError (kernels.cpp:7-13, trainer.cpp:504-518). With enable != 0 the fused layer steps scan out and
+ * grad_h once the step is done (one extra sync) and return MEFT_E_NONFINITE ("... non-finite ...") on NaN / Inf.
+ * Default off: the scan costs a sync per step. */
+meft_status meft_ctx_set_check_finite(meft_ctx* ctx, int enable);
 /* Keep `sms` SMs free of the persistent tcgen05 GEMMs (process-wide; 0 = all SMs). The expert-sharded step sets it
  * while collectives are meant to overlap its FFN: NCCL's kernels need SMs of their own to make progress. */
 meft_status meft_set_gemm_sm_reserve(int sms);

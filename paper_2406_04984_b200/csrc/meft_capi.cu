@@ -42,6 +42,7 @@ struct meft_ctx {
 
     int selection_mode = MEFT_SELECT_AUTO;
     int gather_mode = -1;  // MEFT_GATHER_*; -1 = not set (environment MEFT_GATHER, else AUTO)
+    bool check_finite = false;  // fused step: raise MEFT_E_NONFINITE like check_finite (kernels.cpp:7-13)
 
     // phase timing (meft_ctx_set_timing)
     bool timing = false;
@@ -624,6 +625,13 @@ meft_status meft_ctx_set_selection(meft_ctx* ctx, int mode) {
     });
 }
 
+meft_status meft_ctx_set_check_finite(meft_ctx* ctx, int enable) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        ctx->check_finite = enable != 0;
+    });
+}
+
 meft_status meft_set_gemm_sm_reserve(int sms) {
     return guarded(nullptr, [&] {
         require(sms >= 0 && sms <= 64, MEFT_E_INVALID, "gemm SM reserve must be in [0, 64]");
@@ -1202,6 +1210,15 @@ static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
     const int64_t su = ctx->host_small[4];
     ffn_update_impl(ctx, s, layer, h, g, T, uni, su, ctx->host_small[7], b1, b2, eps, lr, out, grad_h, g_ready,
                     fwd_done, gh_done, s->train_router ? tau : nullptr, kk_eff, nullptr, base);
+    if (ctx->check_finite) {  // the reference's check_finite on its matmul outputs (kernels.cpp:7-13)
+        int32_t* flag = ctx->dev_small + 20;
+        MEFT_CUDA_CHECK(cudaMemsetAsync(flag, 0, 4, st));
+        if (out) flag_nonfinite_f32(st, out, T * d, flag);
+        if (grad_h) flag_nonfinite_f32(st, grad_h, T * d, flag);
+        MEFT_CUDA_CHECK(cudaMemcpyAsync(ctx->host_small + 20, flag, 4, cudaMemcpyDeviceToHost, st));
+        MEFT_CUDA_CHECK(cudaStreamSynchronize(st));
+        if (ctx->host_small[20]) throw MeftError(MEFT_E_NONFINITE, "layer_step: non-finite entry in out / grad_h");
+    }
 
     if (info) {
         info->union_size = su;

@@ -496,6 +496,14 @@ __global__ void k_nonfinite(const double* __restrict__ x, int64_t n, int32_t* __
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
         if (!isfinite(x[i])) *flag = 1;
 }
+__global__ void k_nonfinite_f32(const float4* __restrict__ x, int64_t n4, int32_t* __restrict__ flag) {
+    bool bad = false;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4; i += int64_t(gridDim.x) * blockDim.x) {
+        const float4 v = x[i];
+        bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *flag = 1;
+}
 __global__ void k_add_f64(double* __restrict__ a, const double* __restrict__ b, int64_t n) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
         a[i] = a[i] + b[i];
@@ -515,6 +523,13 @@ void act_backward(cudaStream_t st, double* g, const double* pre, int64_t n, int 
 void flag_nonfinite(cudaStream_t st, const double* x, int64_t n, int32_t* flag_dev) {
     if (n <= 0) return;
     k_nonfinite<<<grid_for(n), 256, 0, st>>>(x, n, flag_dev);
+    check_launch("k_nonfinite");
+}
+void flag_nonfinite_f32(cudaStream_t st, const float* x, int64_t n, int32_t* flag_dev) {
+    if (n <= 0) return;
+    if (n % 4 || reinterpret_cast<uintptr_t>(x) % 16) throw MeftError(2, "check_finite: f32 rows must be float4 aligned");
+    k_nonfinite_f32<<<int(std::min<int64_t>((n / 4 + 255) / 256, num_sms() * 8)), 256, 0, st>>>(
+        reinterpret_cast<const float4*>(x), n / 4, flag_dev);
     check_launch("k_nonfinite");
 }
 void add_f64(cudaStream_t st, double* a, const double* b, int64_t n) {

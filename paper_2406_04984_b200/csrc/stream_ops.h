@@ -37,6 +37,7 @@ void convert_index(cudaStream_t st, bool to64, void* dst, const void* src, int64
 void act_forward(cudaStream_t st, const double* x, double* y, int64_t n, int act);   // 0 SiLU, 1 ReLU
 void act_backward(cudaStream_t st, double* g, const double* pre, int64_t n, int act);  // g *= act'(pre)
 void flag_nonfinite(cudaStream_t st, const double* x, int64_t n, int32_t* flag_dev);
+void flag_nonfinite_f32(cudaStream_t st, const float* x, int64_t n, int32_t* flag_dev);
 void add_f64(cudaStream_t st, double* a, const double* b, int64_t n);                  // a += b (add_inplace)
 void transpose8(cudaStream_t st, const void* src, void* dst, int64_t rows, int64_t cols);
 

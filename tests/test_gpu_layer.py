@@ -277,3 +277,20 @@ def test_layer_step_with_frozen_base_ffn(ctx, act):
     np.testing.assert_array_equal(res["per_token"].cpu().numpy(), sel["per_token"])
     assert rel(out.cpu().numpy(), want_out) < BF16_TOL
     assert rel(gh.cpu().numpy(), want_gh) < BF16_TOL
+
+
+def test_check_finite_raises_reference_kind(ctx):
+    """check_finite (kernels.cpp:7-13) on the fused step: NaN input -> MEFT_E_NONFINITE with 'non-finite'."""
+    w_a, w_g, w_b, h, gr = cfg1_inputs(T=128)
+    st = make_store(ctx, w_a, w_g, w_b, 64)
+    g_bad = bf16_dev(gr)
+    g_bad[3, 7] = float("nan")
+    ctx.set_check_finite(True)
+    try:
+        st.layer_step(0, bf16_dev(h), bf16_dev(gr), 4, 32, 1e-3)  # clean inputs pass
+        with pytest.raises(G.MeftError) as e:
+            st.layer_step(0, bf16_dev(h), g_bad, 4, 32, 1e-3, out=torch.empty((128, 512), device="cuda"),
+                          grad_h=torch.empty((128, 512), device="cuda"))
+        assert e.value.kind == "non-finite" and "non-finite" in str(e.value)
+    finally:
+        ctx.set_check_finite(False)
