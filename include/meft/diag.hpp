@@ -1,12 +1,12 @@
-// Drop-in declaration of the reference's warning channel (proj/include/meft/diag.hpp:1-11):
-// one stderr line per warning, counted so callers can assert a clamp warned exactly once.
+// meft/diag.hpp for the B200 drop-in library (the reference's proj/include/meft/diag.hpp): warnings go to stderr,
+// one line each, and are counted so a caller can assert that a clamp warned exactly once.
 #pragma once
 
 #include <string>
 
 namespace meft {
 
-void warn(const std::string& msg);
+void warn(const std::string& message);
 long warn_count();
 
 }  // namespace meft
