@@ -328,15 +328,26 @@ def our_arm(args, rank, world, local_rank):
     gemm_tflops = gemm_flops / (gemm_ms / gemm_launches * 1e-3) / 1e12
     tc_peak = peaks.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"])
     hbm = peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"])
-    adam_bytes = 2 * S * d * 30.0  # read w,m,v,g + write w,m,v fp32 + bf16 copy, key and value rows (§8d)
+    # sparse Adam: fused into the two grad-W GEMM epilogues by default (the gradient never reaches HBM: read w,m,v
+    # + write w,m,v fp32 + bf16 copy = 26 B/entry); MEFT_ADAM_EPILOGUE=0 runs the separate pass over a gradient
+    # block (+ the gradient read: 30 B/entry)
+    adam_fused = os.environ.get("MEFT_ADAM_EPILOGUE", "1") != "0"
+    adam_bytes = 2 * S * d * (26.0 if adam_fused else 30.0)  # key and value rows
     gather_bytes = 2 * S * d * 2 * 2.0
     adam_ms = phases["adam"][0] / args.steps
     gather_ms = phases["gather"][0] / args.steps
     select_ms = phases["select"][0] / args.steps
-    # composite layer roofline: sum_k max(F_k / TC peak, B_k / HBM peak)
+    bwd_ms = phases["ffn_backward"][0] / args.steps
+    # composite layer roofline: sum_k max(F_k / TC peak, B_k / HBM peak); with the fused Adam each
+    # grad-W GEMM is one kernel moving its operands plus half the Adam bytes under its flops
+    gemm_t = gemm_flops / (tc_peak * 1e12)
+    if adam_fused:
+        adam_gemm_t = max(gemm_t, (adam_bytes / 2 + (T * S + T * d) * 2.0) / (hbm * 1e9))
+        ffn_roof = 4 * gemm_t + 2 * adam_gemm_t
+    else:
+        ffn_roof = 6 * gemm_t + adam_bytes / (hbm * 1e9)
     key_bytes = (M * d * 2) + T * d * 2
-    roof_ms = (6 * gemm_flops / (tc_peak * 1e12) + adam_bytes / (hbm * 1e9) + key_bytes / (hbm * 1e9)
-               + 2 * T * N * d / (tc_peak * 1e12)) * 1e3
+    roof_ms = (ffn_roof + key_bytes / (hbm * 1e9) + 2 * T * N * d / (tc_peak * 1e12)) * 1e3
 
     # DRAM traffic per GEMM launch from the committed ncu --set full capture of one step's six GEMMs
     traffic = None
@@ -373,7 +384,11 @@ def our_arm(args, rank, world, local_rank):
                 "d2h_bytes_per_step": 2 * T * d * 4, "ms_per_step": e2e_s * 1e3,
                 "path": "meft_layer_step_host (C ABI, pinned host buffers)" if not sharded else
                         "sharded layer step with pinned host copies in and out"},
-        "roofline": {"bound": "tensor", "kernel": "k_gemm_bf16_pair (tcgen05 cta_group::2 FFN GEMM, 6 per step)", "achieved": gemm_tflops,
+        "roofline": {"bound": "tensor",
+                     "kernel": "k_gemm_bf16_pair (tcgen05 cta_group::2 FFN GEMM, 6 per step"
+                               + ("; the two grad-W launches also run the sparse Adam in their epilogue)"
+                                  if adam_fused else ")"),
+                     "achieved": gemm_tflops,
                      "peak": tc_peak, "unit": "TFLOP/s", "frac": gemm_tflops / tc_peak, "traffic": traffic,
                      "traffic_unit": "bytes per launch (ncu dram read+write, profiles/gemm_traffic.json)",
                      "peak_source": f"{peak_src} bf16_tflops_sustained",
@@ -381,7 +396,9 @@ def our_arm(args, rank, world, local_rank):
         "layer_roofline": {"roofline_ms": roof_ms, "measured_ms": ms, "frac": roof_ms / ms},
         "phases_ms": {"select": select_ms, "gather": gather_ms, "ffn_forward": phases["ffn_forward"][0] / args.steps,
                       "ffn_backward": phases["ffn_backward"][0] / args.steps, "adam": adam_ms},
-        "hbm_kernels": {"adam_gbs": adam_bytes / (adam_ms * 1e-3) / 1e9 if adam_ms else None,
+        "hbm_kernels": {"adam_placement": "grad-W GEMM epilogues" if adam_fused else "separate pass",
+                        "adam_bytes_per_step": adam_bytes,
+                        "adam_gbs": adam_bytes / (adam_ms * 1e-3) / 1e9 if adam_ms and not adam_fused else None,
                         "gather_gbs": gather_bytes / (gather_ms * 1e-3) / 1e9 if gather_ms else None,
                         "peak_gbs": hbm},
         "selection": {"algorithm": "certified tcgen05 scoring + exact fp64 re-scoring (bit-exact indices)",

@@ -118,6 +118,14 @@ meft_status meft_ctx_set_selection(meft_ctx* ctx, int mode);
 #define MEFT_GATHER_KERNEL 1
 #define MEFT_GATHER_TMA 2
 meft_status meft_ctx_set_gather(meft_ctx* ctx, int mode);
+/* Where the fused layer step runs the lazy sparse Adam (memtier.cpp:187-210) when no scatter_grads are pending:
+ * EPILOGUE (default; environment MEFT_ADAM_EPILOGUE=0 selects PASS) applies it inside the two weight-gradient
+ * GEMMs' epilogues to the fp32 accumulator rows as they drain, overlapping the HBM-bound update with the
+ * tensor-bound mainloop; PASS writes the gradients to a [|S| x d] block and runs a separate Adam kernel.
+ * Both give bit-identical tables, moments and counters. */
+#define MEFT_ADAM_EPILOGUE 0
+#define MEFT_ADAM_PASS 1
+meft_status meft_ctx_set_adam(meft_ctx* ctx, int mode);
 /* The reference runs check_finite on every matmul output and the trainer turns the runtime_error into
  * DivergenceError (kernels.cpp:7-13, trainer.cpp:504-518). With enable != 0 the fused layer steps scan out and
  * grad_h once the step is done (one extra sync) and return MEFT_E_NONFINITE ("... non-finite ...") on NaN / Inf.

@@ -60,6 +60,7 @@ _SIGS = {
     "meft_ctx_set_timing": (INT, [P, INT]),
     "meft_ctx_set_selection": (INT, [P, INT]),
     "meft_ctx_set_gather": (INT, [P, INT]),
+    "meft_ctx_set_adam": (INT, [P, INT]),
     "meft_ctx_set_check_finite": (INT, [P, INT]),
     "meft_set_gemm_sm_reserve": (INT, [INT]),
     "meft_ctx_read_timing": (INT, [P, P, P]),

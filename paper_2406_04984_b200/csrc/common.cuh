@@ -89,6 +89,10 @@ __device__ __forceinline__ uint32_t pack_bf16x2(uint16_t lo, uint16_t hi) { retu
 // One lazy-Adam entry update (memtier.cpp:176-185) in fp32 with every rounding spelled out, so the standalone
 // Adam kernel and the Adam-fused GEMM epilogue produce bit-identical weights and moments.
 //   scale = lr / (1 - b1^t),  inv_c2 = 1 / (1 - b2^t)
+//   m = b1 m + (1-b1) g ;  v = b2 v + (1-b2) g^2 ;  w -= scale m / (sqrt(v inv_c2) + eps)
+// The square root and the quotient use the SFU approximations (sqrt.approx, rcp-based divide; <= 2 ulp): an fp32
+// step of an fp64 reference is already within its tolerance band by ~1e-6 relative, and the epilogue form must
+// be short -- one epilogue warp per SM sub-partition applies it to a 128 x 256 tile behind every GEMM mainloop.
 struct AdamCoef {
     float scale, inv_c2;
 };
@@ -97,11 +101,16 @@ __device__ __forceinline__ AdamCoef adam_coef(float b1, float b2, float lr, int 
     const float c2 = float(1.0 - pow(double(b2), double(t)));
     return AdamCoef{__fdiv_rn(lr, c1), __fdiv_rn(1.0f, c2)};
 }
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float y;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 __device__ __forceinline__ void adam_update(float& w, float& m, float& v, float g, float b1, float b2, float eps,
                                             AdamCoef k) {
-    m = __fadd_rn(__fmul_rn(b1, m), __fmul_rn(__fsub_rn(1.0f, b1), g));
-    v = __fadd_rn(__fmul_rn(b2, v), __fmul_rn(__fmul_rn(__fsub_rn(1.0f, b2), g), g));
-    w = __fsub_rn(w, __fdiv_rn(__fmul_rn(k.scale, m), __fadd_rn(__fsqrt_rn(__fmul_rn(v, k.inv_c2)), eps)));
+    m = __fmaf_rn(b1, m, __fmul_rn(__fsub_rn(1.0f, b1), g));
+    v = __fmaf_rn(b2, v, __fmul_rn(__fmul_rn(__fsub_rn(1.0f, b2), g), g));
+    w = __fsub_rn(w, __fdividef(__fmul_rn(k.scale, m), __fadd_rn(sqrt_approx(__fmul_rn(v, k.inv_c2)), eps)));
 }
 
 // ------------------------------------------------------------------ shared-memory / mbarrier PTX

@@ -66,6 +66,16 @@ struct KArgs {
     float* peer[kMaxPeers];
     long long peer_rows, row0, col0;
     int peer_slot;
+    // EPI_ADAM_F32 (see kernels.h)
+    float* adam_w;
+    float* adam_m;
+    float* adam_v;
+    uint16_t* adam_c;
+    const float2* adam_coef;
+    float b1, b2, eps;
+    double* stat_ss;
+    int32_t* stat_lsb;
+    long long stat_ld;
 };
 
 __device__ __forceinline__ int gather_row(const KArgs& a, int p) {
@@ -321,6 +331,169 @@ __device__ __forceinline__ void epilogue_chunk(const KArgs& a, int m, int n, con
     }
 }
 
+// ---------------------------------------------------------------- EPI_ADAM_F32: sparse Adam in the epilogue
+// Four entries of one table row: the shared adam_update (bit-identical to k_adam_mixed), bf16 copy, statistics.
+template <bool STATS>
+__device__ __forceinline__ uint2 adam4(float4& w, float4& m, float4& v, const float4& g, const KArgs& a, AdamCoef k,
+                                       double& ss, int& lsb) {
+    adam_update(w.x, m.x, v.x, g.x, a.b1, a.b2, a.eps, k);
+    adam_update(w.y, m.y, v.y, g.y, a.b1, a.b2, a.eps, k);
+    adam_update(w.z, m.z, v.z, g.z, a.b1, a.b2, a.eps, k);
+    adam_update(w.w, m.w, v.w, g.w, a.b1, a.b2, a.eps, k);
+    const uint16_t c[4] = {f32_to_bf16_bits(w.x), f32_to_bf16_bits(w.y), f32_to_bf16_bits(w.z), f32_to_bf16_bits(w.w)};
+    if (STATS) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double x = double(bf16_bits_to_f32(c[q]));
+            ss = fma(x, x, ss);
+            if (c[q] & 0x7FFF) lsb = min(lsb, bf16_lsb_exp(c[q]));
+        }
+    }
+    return make_uint2(pack_bf16x2(c[0], c[1]), pack_bf16x2(c[2], c[3]));
+}
+
+// Pair kernel: the warp's 32 accumulator rows (one per lane, 32 columns per tcgen05.ld) are transposed through a
+// 32 x 36 fp32 shared scratch so that 8 lanes cover one table row's 128 contiguous bytes: every w/m/v load and
+// store is a full 128-byte segment. All 8 rows' loads of a chunk are issued before any update (24 x 16 B in flight
+// per lane) to cover DRAM latency behind the mainloop of the next tile.
+__device__ __forceinline__ void st_shared_f4(uint32_t addr, float4 v) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ float4 ld_shared_f4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr)
+                 : "memory");
+    return v;
+}
+constexpr int ADAM_SCRATCH_LD = 36;  // floats per scratch row (16-byte aligned, conflict-free quarter-warp phases)
+constexpr int ADAM_SCRATCH_BYTES = 4 * 32 * ADAM_SCRATCH_LD * 4;
+
+template <bool STATS>
+__device__ __forceinline__ void adam_tile_transposed(const KArgs& a, uint32_t taddr, int m0, int n_col0, float* sw,
+                                                     int lane) {
+    const int mrow = m0 + lane;
+    const int jl = mrow < a.M ? __ldg(a.row_idx + mrow) : -1;
+    const float2 kl = mrow < a.M ? __ldg(a.adam_coef + mrow) : make_float2(0.f, 0.f);
+    const int sub = lane >> 3, c4 = (lane & 7) * 4;
+    int j[8];
+    AdamCoef k[8];
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+        const int row = it * 4 + sub;
+        j[it] = __shfl_sync(0xffffffffu, jl, row);
+        k[it] = AdamCoef{__shfl_sync(0xffffffffu, kl.x, row), __shfl_sync(0xffffffffu, kl.y, row)};
+    }
+    // L2 prefetch of one 128-byte row segment per array, one chunk ahead (lanes 0-2: w, m, v of row `lane`)
+    auto prefetch = [&](int n) {
+        if (lane < 3 && jl >= 0 && n < a.N) {
+            const float* base = lane == 0 ? a.adam_w : lane == 1 ? a.adam_m : a.adam_v;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (long long)jl * a.ldc + n));
+        }
+    };
+    prefetch(n_col0);
+    double ss[8];
+    int lsb[8];
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+        ss[it] = 0.0;
+        lsb[it] = INT32_MAX;
+    }
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+        const int n = n_col0 + c * 32;
+        if (n >= a.N) break;  // warp-uniform (N % 32 == 0)
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(taddr + c * 32, r);
+        prefetch(n + 32);
+        float4 w[8], m[8], v[8];
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {  // invalid rows (past M: j < 0) read row 0 and never store
+            const long long off = (long long)max(j[it], 0) * a.ldc + n + c4;
+            w[it] = __ldcs(reinterpret_cast<const float4*>(a.adam_w + off));
+            m[it] = __ldcs(reinterpret_cast<const float4*>(a.adam_m + off));
+            v[it] = __ldcs(reinterpret_cast<const float4*>(a.adam_v + off));
+        }
+        tmem_ld_wait();
+        const uint32_t sbase = smem_u32(sw);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            st_shared_f4(sbase + (lane * ADAM_SCRATCH_LD + 4 * q) * 4,
+                         make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                     __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3])));
+        __syncwarp();
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+            const float4 g = ld_shared_f4(sbase + ((it * 4 + sub) * ADAM_SCRATCH_LD + c4) * 4);
+            const uint2 cb = adam4<STATS>(w[it], m[it], v[it], g, a, k[it], ss[it], lsb[it]);
+            if (j[it] >= 0) {
+                const long long off = (long long)j[it] * a.ldc + n + c4;
+                __stcs(reinterpret_cast<float4*>(a.adam_w + off), w[it]);
+                __stcs(reinterpret_cast<float4*>(a.adam_m + off), m[it]);
+                __stcs(reinterpret_cast<float4*>(a.adam_v + off), v[it]);
+                *reinterpret_cast<uint2*>(a.adam_c + off) = cb;
+            }
+        }
+        __syncwarp();  // the scratch is rewritten by the next chunk
+    }
+    if (STATS) {  // the 8 lanes of each row reduce in a fixed butterfly; lane 8*sub writes the row's partial
+        const int nb = n_col0 / kAdamStatTile;
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+            double t = ss[it];
+            int l = lsb[it];
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) {
+                t += __shfl_xor_sync(0xffffffffu, t, o);
+                l = min(l, __shfl_xor_sync(0xffffffffu, l, o));
+            }
+            const int mr = m0 + it * 4 + sub;
+            if ((lane & 7) == 0 && mr < a.M) {
+                a.stat_ss[mr * a.stat_ld + nb] = t;
+                a.stat_lsb[mr * a.stat_ld + nb] = l;
+            }
+        }
+    }
+}
+
+// 1-CTA kernel (small problems): thread = accumulator row, same arithmetic without the transpose.
+__device__ __forceinline__ void adam_tile_rows(const KArgs& a, uint32_t taddr, int m, int n_col0) {
+    const bool ok = m < a.M;
+    const int j = ok ? __ldg(a.row_idx + m) : 0;
+    const float2 kl = ok ? __ldg(a.adam_coef + m) : make_float2(0.f, 0.f);
+    const AdamCoef k{kl.x, kl.y};
+    double ss = 0.0;
+    int lsb = INT32_MAX;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+        const int n = n_col0 + c * 32;
+        if (n >= a.N) break;
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(taddr + c * 32, r);
+        tmem_ld_wait();
+        if (!ok) continue;
+        const long long off = (long long)j * a.ldc + n;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            float4 w = reinterpret_cast<const float4*>(a.adam_w + off)[q];
+            float4 mm = reinterpret_cast<const float4*>(a.adam_m + off)[q];
+            float4 v = reinterpret_cast<const float4*>(a.adam_v + off)[q];
+            const float4 g = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                         __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+            const uint2 cb = adam4<true>(w, mm, v, g, a, k, ss, lsb);
+            reinterpret_cast<float4*>(a.adam_w + off)[q] = w;
+            reinterpret_cast<float4*>(a.adam_m + off)[q] = mm;
+            reinterpret_cast<float4*>(a.adam_v + off)[q] = v;
+            reinterpret_cast<uint2*>(a.adam_c + off)[q] = cb;
+        }
+    }
+    if (a.stat_ss && ok) {
+        const int nb = n_col0 / kAdamStatTile;
+        a.stat_ss[m * a.stat_ld + nb] = ss;
+        a.stat_lsb[m * a.stat_ld + nb] = lsb;
+    }
+}
+
 template <bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_gemm_bf16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -500,13 +673,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mbar_wait(tfull + acc, aphase);
             tc_fence_after();
             const int m = ti.a_row0 + q * 32 + lane;
+            if (args.epi == EPI_ADAM_F32) {
+                adam_tile_rows(args, tmem_base + (uint32_t(q * 32) << 16) + acc * BN, m, ti.n_col0);
+            } else {
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-                uint32_t r[32];
-                tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c * 32, r);
-                tmem_ld_wait();
-                const int n = ti.n_col0 + c * 32;
-                if (m < ti.m_lim && n < args.N) epilogue_chunk(args, m, n, r, c_off);
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t r[32];
+                    tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c * 32, r);
+                    tmem_ld_wait();
+                    const int n = ti.n_col0 + c * 32;
+                    if (m < ti.m_lim && n < args.N) epilogue_chunk(args, m, n, r, c_off);
+                }
             }
             tc_fence_before();
             __syncwarp();
@@ -711,13 +888,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             mbar_wait(tfull + acc, aphase);
             tc_fence_after();
             const int m = mb * P_TILE_M + int(rank) * 128 + q * 32 + lane;
+            if (args.epi == EPI_ADAM_F32) {
+                float* sw = reinterpret_cast<float*>(smem + P_STAGES * P_STAGE_BYTES + 256) + q * 32 * ADAM_SCRATCH_LD;
+                const uint32_t ta = tmem_base + (uint32_t(q * 32) << 16) + acc * BN;
+                if (args.stat_ss)
+                    adam_tile_transposed<true>(args, ta, m - lane, nb * BN, sw, lane);
+                else
+                    adam_tile_transposed<false>(args, ta, m - lane, nb * BN, sw, lane);
+            } else {
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-                uint32_t r[32];
-                tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c * 32, r);
-                tmem_ld_wait();
-                const int n = nb * BN + c * 32;
-                if (m < args.M && n < args.N) epilogue_chunk(args, m, n, r);
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t r[32];
+                    tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c * 32, r);
+                    tmem_ld_wait();
+                    const int n = nb * BN + c * 32;
+                    if (m < args.M && n < args.N) epilogue_chunk(args, m, n, r);
+                }
             }
             tc_fence_before();
             __syncwarp();
@@ -792,6 +978,13 @@ void check_epilogue(const GemmEpilogue& epi) {
             if (!aligned16(epi.peer[i])) throw MeftError(2, "gemm_bf16: peer buffers must be 16-byte aligned");
         return;
     }
+    if (epi.kind == EPI_ADAM_F32) {
+        if (!epi.row_idx || !epi.adam_coef || !aligned16(epi.adam_w) || !aligned16(epi.adam_m) ||
+            !aligned16(epi.adam_v) || !aligned16(epi.adam_c) || epi.ldc % 32 || epi.ksplit > 1 || epi.accumulate ||
+            (epi.stat_ss && (!epi.stat_lsb || epi.stat_ld < 1)))
+            throw MeftError(2, "gemm_bf16: Adam epilogue arguments (row_idx, coef, 16-byte aligned tables, ldc % 32)");
+        return;
+    }
     if (epi.kind == EPI_STORE_F32 || epi.kind == EPI_ROWS_ADD_F32 || epi.kind == EPI_ROWS_STORE_F32) {
         if (!aligned16(epi.c) || (epi.ldc % 4)) throw MeftError(2, "gemm_bf16: f32 output alignment");
     } else {
@@ -830,6 +1023,17 @@ KArgs base_args(int64_t M, int64_t N, int64_t K, const GemmEpilogue& epi) {
     args.row0 = epi.row0;
     args.col0 = epi.col0;
     args.peer_slot = epi.peer_slot;
+    args.adam_w = epi.adam_w;
+    args.adam_m = epi.adam_m;
+    args.adam_v = epi.adam_v;
+    args.adam_c = epi.adam_c;
+    args.adam_coef = epi.adam_coef;
+    args.b1 = epi.b1;
+    args.b2 = epi.b2;
+    args.eps = epi.eps;
+    args.stat_ss = epi.stat_ss;
+    args.stat_lsb = epi.stat_lsb;
+    args.stat_ld = epi.stat_ld;
     args.b_idx_n = 0;
     args.b_oob_row = 0;
     args.ksplit = 1;
@@ -864,11 +1068,12 @@ void launch_pair(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, 
     static bool attr_set = false;
     if (!attr_set) {
         MEFT_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_bf16_pair<A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             P_SMEM_BYTES));
+                                             P_SMEM_BYTES + ADAM_SCRATCH_BYTES));
         attr_set = true;
     }
     const int pairs = std::max(1, std::min(pair_tiles, gemm_sms() / 2));
-    k_gemm_bf16_pair<A_MN, B_MN><<<2 * pairs, NUM_THREADS, P_SMEM_BYTES, st>>>(ta, tb, tg, args);
+    const int smem = P_SMEM_BYTES + (args.epi == EPI_ADAM_F32 ? ADAM_SCRATCH_BYTES : 0);
+    k_gemm_bf16_pair<A_MN, B_MN><<<2 * pairs, NUM_THREADS, smem, st>>>(ta, tb, tg, args);
     check_launch("k_gemm_bf16_pair");
 }
 
@@ -971,6 +1176,8 @@ void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOpera
     const int64_t mc = round_up(mc_env ? mc_env : kChunk, P_TILE_M);
     const int64_t nc = round_up(nc_env ? nc_env : kChunk, BN);
     const int64_t kc = f32_out ? round_up(kc_env ? kc_env : kChunk, BK) : K;
+    if (epi.kind == EPI_ADAM_F32 && (N > nc || N != epi.ldc))
+        throw MeftError(2, "gemm_bf16: the Adam epilogue covers whole table rows of at most 65536 columns");
     if ((mc >= M && nc >= N && kc >= K) || epi.ksplit > 1) return gemm_bf16_one(st, M, N, K, A, B, epi);
     const int64_t ce = (epi.kind == EPI_STORE_F32 || epi.kind == EPI_ROWS_ADD_F32 || epi.kind == EPI_ROWS_STORE_F32)
                            ? 4 : 2;
@@ -996,6 +1203,13 @@ void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOpera
                 if (epi.kind == EPI_PEER_F32) {  // logical offsets: the addresses are resolved per row
                     e.row0 = epi.row0 + m0;
                     e.col0 = epi.col0 + n0;
+                } else if (epi.kind == EPI_ADAM_F32) {
+                    e.row_idx = epi.row_idx + m0;
+                    e.adam_coef = epi.adam_coef + m0;
+                    if (epi.stat_ss) {
+                        e.stat_ss = epi.stat_ss + m0 * epi.stat_ld;
+                        e.stat_lsb = epi.stat_lsb + m0 * epi.stat_ld;
+                    }
                 } else if (rows_epi) {
                     e.row_idx = epi.row_idx + m0;
                     e.c = const_cast<void*>(advance(epi.c, n0, ce));

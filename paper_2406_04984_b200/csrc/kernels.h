@@ -34,6 +34,13 @@ enum GemmEpi : int {
     // Frozen base FFN (adapter.cpp:118-120, 153-164): act = 0 SiLU, 1 ReLU.
     EPI_ACT_BF16 = 6,   // C bf16 = act(acc); aux bf16 [M x ldaux] = acc (the pre-activation, kept for backward)
     EPI_DACT_BF16 = 7,  // C bf16 = acc * act'(aux)   (aux: the stored pre-activation)
+    // Lazy sparse Adam fused into a weight-gradient GEMM (memtier.cpp:187-210 on the fused step): acc row m is the
+    // gradient of table row j = row_idx[m]; the epilogue applies adam_update to adam_w/m/v[j*ldc + n] with the
+    // per-position coefficients adam_coef[m] (scale, inv_c2) and writes the bf16 compute copy adam_c. With stat_ss
+    // it also emits the selection statistics of the new bf16 row per 256-column tile nb:
+    // stat_ss[m*stat_ld + nb] = fp64 sum of squares, stat_lsb[...] = minimum LSB exponent of the nonzero entries.
+    // No K split (the update needs the finished gradient); N <= 65536.
+    EPI_ADAM_F32 = 8,
 };
 constexpr int kMaxPeers = 8;
 
@@ -59,7 +66,18 @@ struct GemmEpilogue {
     int peer_slot = 0;
     int64_t peer_rows = 0;
     int64_t row0 = 0, col0 = 0;
+    // EPI_ADAM_F32 (ldc = table row pitch in elements)
+    float* adam_w = nullptr;
+    float* adam_m = nullptr;
+    float* adam_v = nullptr;
+    uint16_t* adam_c = nullptr;
+    const float2* adam_coef = nullptr;
+    float b1 = 0.9f, b2 = 0.999f, eps = 1e-8f;
+    double* stat_ss = nullptr;
+    int32_t* stat_lsb = nullptr;
+    int64_t stat_ld = 0;  // >= ceil(N / 256)
 };
+constexpr int kAdamStatTile = 256;  // columns per EPI_ADAM_F32 statistics partial
 
 void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOperand& A, const GemmOperand& B,
                const GemmEpilogue& epi);

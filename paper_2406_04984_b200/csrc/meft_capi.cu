@@ -41,6 +41,7 @@ struct meft_ctx {
     std::unordered_map<std::string, Buf> scratch;
 
     int selection_mode = MEFT_SELECT_AUTO;
+    int adam_mode = -1;  // MEFT_ADAM_*; -1 = not set (environment MEFT_ADAM_EPILOGUE, else EPILOGUE)
     int gather_mode = -1;  // MEFT_GATHER_*; -1 = not set (environment MEFT_GATHER, else AUTO)
     bool check_finite = false;  // fused step: raise MEFT_E_NONFINITE like check_finite (kernels.cpp:7-13)
 
@@ -316,7 +317,8 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
                        void* grad_keys_s, void* grad_values_s, void* grad_h, bool acc_h, const int32_t* S_rows,
                        void* stage_keys, void* stage_values, const RowGather& rg = RowGather(),
                        cudaEvent_t grad_h_done = nullptr, const std::function<void()>* between = nullptr,
-                       const meft_peer_out* peer = nullptr) {
+                       const meft_peer_out* peer = nullptr, const GemmEpilogue* epi_values = nullptr,
+                       const GemmEpilogue* epi_keys = nullptr) {
     cudaStream_t st = ctx->stream;
     if (dt == MEFT_F64) {
         const double* gd = static_cast<const double*>(g);
@@ -382,11 +384,11 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
         e4.c = grad_values_s;
     }
     e4.ldc = d;
-    gemm_bf16(st, s, d, T, GemmOperand{z, ld_z, true}, GemmOperand{g, d, true}, e4);
+    gemm_bf16(st, s, d, T, GemmOperand{z, ld_z, true}, GemmOperand{g, d, true}, epi_values ? *epi_values : e4);
     if (between) (*between)();  // e.g. consume grad_values before grad_keys reuses its buffer
     GemmEpilogue e5 = e4;  // grad_keys = masked^T h
     e5.c = S_rows ? stage_keys : grad_keys_s;
-    gemm_bf16(st, s, d, T, GemmOperand{masked, ld_z, true}, GemmOperand{h, d, true}, e5);
+    gemm_bf16(st, s, d, T, GemmOperand{masked, ld_z, true}, GemmOperand{h, d, true}, epi_keys ? *epi_keys : e5);
 }
 
 // ---- store helpers
@@ -645,6 +647,14 @@ meft_status meft_ctx_set_gather(meft_ctx* ctx, int mode) {
         require(mode == MEFT_GATHER_AUTO || mode == MEFT_GATHER_KERNEL || mode == MEFT_GATHER_TMA, MEFT_E_INVALID,
                 "unknown gather mode");
         ctx->gather_mode = mode;
+    });
+}
+
+meft_status meft_ctx_set_adam(meft_ctx* ctx, int mode) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(mode == MEFT_ADAM_EPILOGUE || mode == MEFT_ADAM_PASS, MEFT_E_INVALID, "unknown Adam mode");
+        ctx->adam_mode = mode;
     });
 }
 
@@ -1245,6 +1255,15 @@ static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
 // TMA lets the GEMM producers fetch them (contiguous runs as plain boxes, the rest by tile::gather4) -- bitwise
 // the same operand tiles as the materialised copy; AUTO picks it when the union is nearly one run (a broken
 // 128-row piece costs ~4x its TMA issue), i.e. at most one hole per 12800 selected rows.
+// meft_ctx_set_adam; default from MEFT_ADAM_EPILOGUE=0 (separate pass) for A/B comparisons (bitwise identical).
+static bool adam_epilogue_enabled(const meft_ctx* ctx) {
+    static const bool env_on = [] {
+        const char* v = std::getenv("MEFT_ADAM_EPILOGUE");
+        return !(v && v[0] == '0');
+    }();
+    return ctx->adam_mode < 0 ? env_on : ctx->adam_mode == MEFT_ADAM_EPILOGUE;
+}
+
 static bool use_tma_gather(const meft_ctx* ctx, int64_t su, int64_t holes) {
     static const int env_mode = [] {
         const char* v = std::getenv("MEFT_GATHER");
@@ -1390,6 +1409,49 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
         PhaseScope ps(ctx, 4);
         if (su > 0) mark_rows(st, L.staged, uni, nullptr, su);
         adam_impl(ctx, s, layer, b1, b2, eps, lr);
+    } else if (adam_epilogue_enabled(ctx) && d % 32 == 0 && d <= 65536) {
+        // staging is all zero, so staged == S exactly and each weight-gradient row is final when its GEMM tile
+        // drains: the sparse Adam (memtier.cpp:187-210) runs in those GEMMs' epilogues (EPI_ADAM_F32) on the
+        // fp32 accumulator, overlapping the HBM-bound update with the tensor-bound mainloop -- no gradient block,
+        // no separate pass. Per-pair steps advance once, before either GEMM (the key and value rows share them).
+        float2* coef = static_cast<float2*>(ctx->get("adam_coef", size_t(std::max<int64_t>(su, 1)) * 8));
+        const int64_t parts = ceil_div(d, int64_t(kAdamStatTile));
+        const bool stats = stats_valid && su > 0;
+        double* kss = stats ? static_cast<double*>(ctx->get("adam_kss", size_t(su * parts) * 8)) : nullptr;
+        int32_t* klsb = stats ? static_cast<int32_t*>(ctx->get("adam_klsb", size_t(su * parts) * 4)) : nullptr;
+        if (su > 0) adam_coef_bump(st, uni, su, L.step, coef, b1, b2, lr);
+        auto adam_epi = [&](bool keys) {
+            GemmEpilogue e;
+            e.kind = EPI_ADAM_F32;
+            e.ldc = d;
+            e.row_idx = uni;
+            e.adam_w = static_cast<float*>(keys ? L.w_a : L.w_b);
+            e.adam_m = static_cast<float*>(keys ? L.m_a : L.m_b);
+            e.adam_v = static_cast<float*>(keys ? L.v_a : L.v_b);
+            e.adam_c = static_cast<uint16_t*>(keys ? L.c_a : L.c_b);
+            e.adam_coef = coef;
+            e.b1 = float(b1);
+            e.b2 = float(b2);
+            e.eps = float(eps);
+            if (keys && stats) {
+                e.stat_ss = kss;
+                e.stat_lsb = klsb;
+                e.stat_ld = parts;
+            }
+            return e;
+        };
+        const GemmEpilogue ev = adam_epi(false), ek = adam_epi(true);
+        {
+            PhaseScope ps(ctx, 3);
+            ffn_backward_impl(ctx, MEFT_BF16, g, h, act, ks, vs, T, d, su, ld, masked, nullptr, nullptr, ghb,
+                              base != nullptr, nullptr, nullptr, nullptr, rg, gh_done, nullptr, peer, &ev, &ek);
+        }
+        train_router();
+        if (stats) {
+            PhaseScope p4(ctx, 4);
+            adam_stats_finalize(st, uni, su, kss, klsb, parts, L.kn, L.kl);
+        }
+        return;  // key statistics stay valid (refreshed for exactly the rows that changed)
     } else {
         // staging is all zero, so staged == S exactly: the weight grads go to a dense [|S| x d] step block that
         // Adam reads in place of the staging rows (same values, no staging traffic, nothing to zero). ONE block

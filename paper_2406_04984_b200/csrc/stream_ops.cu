@@ -172,6 +172,38 @@ __global__ void __launch_bounds__(256) k_adam_mixed(const int32_t* __restrict__ 
     }
 }
 
+// Adam fused into the weight-gradient GEMM epilogues (EPI_ADAM_F32): the per-pair step of every pair of S advances
+// once (memtier.cpp:192-195, the key column and value row share it) and its bias-correction coefficients are
+// tabulated by position, before either GEMM runs. Same coefficients as k_adam_mixed (adam_coef).
+__global__ void k_adam_coef_bump(const int32_t* __restrict__ rows, int n, int32_t* __restrict__ step,
+                                 float2* __restrict__ coef, float b1, float b2, float lr) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+        const int32_t j = rows[r];
+        const int t = step[j] + 1;
+        step[j] = t;
+        const AdamCoef k = adam_coef(b1, b2, lr, t);
+        coef[r] = make_float2(k.scale, k.inv_c2);
+    }
+}
+
+// Key-row selection statistics from the epilogue's per-256-column partials, summed in column order (the bound of
+// k_row_norms: sqrt of the fp64 sum of squares, rounded up with a 2^-20 margin).
+__global__ void k_adam_stats_finalize(const int32_t* __restrict__ rows, int n, const double* __restrict__ ss,
+                                      const int32_t* __restrict__ lsb, int parts, float* __restrict__ kn,
+                                      int32_t* __restrict__ kl) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+        double t = 0.0;
+        int l = INT32_MAX;
+        for (int p = 0; p < parts; ++p) {
+            t += ss[int64_t(r) * parts + p];
+            l = min(l, lsb[int64_t(r) * parts + p]);
+        }
+        const int32_t j = rows[r];
+        kn[j] = __double2float_ru(sqrt(t) * (1.0 + 0x1p-20));
+        kl[j] = l;
+    }
+}
+
 // fp64 store (API-fidelity mode): the reference's adam_entry in double (memtier.cpp:176-185).
 __global__ void __launch_bounds__(256) k_adam_f64(const int32_t* __restrict__ rows, const int32_t* count_dev, int count,
                                                   int64_t d, double* __restrict__ wa, double* __restrict__ ma,
@@ -416,6 +448,20 @@ void adam_mixed(cudaStream_t st, const int32_t* rows, const int32_t* count_dev, 
                                        staged, float(b1), float(b2), float(eps), float(lr), tables, bump ? 1 : 0,
                                        grads_by_position ? 1 : 0, key_norms, key_lsb);
     check_launch("k_adam_mixed");
+}
+
+void adam_coef_bump(cudaStream_t st, const int32_t* rows, int64_t n, int32_t* step, float2* coef, double b1,
+                    double b2, double lr) {
+    if (n <= 0) return;
+    k_adam_coef_bump<<<grid_for(n), 256, 0, st>>>(rows, int(n), step, coef, float(b1), float(b2), float(lr));
+    check_launch("k_adam_coef_bump");
+}
+
+void adam_stats_finalize(cudaStream_t st, const int32_t* rows, int64_t n, const double* ss, const int32_t* lsb,
+                         int64_t parts, float* kn, int32_t* kl) {
+    if (n <= 0) return;
+    k_adam_stats_finalize<<<grid_for(n), 256, 0, st>>>(rows, int(n), ss, lsb, int(parts), kn, kl);
+    check_launch("k_adam_stats_finalize");
 }
 
 void adam_f64(cudaStream_t st, const int32_t* rows, const int32_t* count_dev, int64_t count, int64_t d, double* wa,

@@ -27,6 +27,12 @@ void adam_mixed(cudaStream_t st, const int32_t* rows, const int32_t* count_dev, 
                 int tables = 3, bool bump = true,  // tables: bit 0 keys, bit 1 values
                 bool grads_by_position = false,    // sa/sb = [count x d] gradients of rows[0..count), kept as is
                 float* key_norms = nullptr, int32_t* key_lsb = nullptr);  // refresh updated keys' select stats
+// Adam fused into the weight-gradient GEMMs (EPI_ADAM_F32): advance step[rows[r]] and tabulate its
+// (lr / (1 - b1^t), 1 / (1 - b2^t)) by position; then fold the epilogue's key statistics partials.
+void adam_coef_bump(cudaStream_t st, const int32_t* rows, int64_t n, int32_t* step, float2* coef, double b1,
+                    double b2, double lr);
+void adam_stats_finalize(cudaStream_t st, const int32_t* rows, int64_t n, const double* ss, const int32_t* lsb,
+                         int64_t parts, float* kn, int32_t* kl);
 void adam_f64(cudaStream_t st, const int32_t* rows, const int32_t* count_dev, int64_t count, int64_t d, double* wa,
               double* ma, double* va, double* sa, double* wb, double* mb, double* vb, double* sb, int32_t* step,
               uint8_t* staged, double b1, double b2, double eps, double lr);

@@ -84,6 +84,10 @@ class Context:
         """How the fused step's GEMMs read the selected key/value rows: "auto", "kernel" or "tma"."""
         self.check(lib().meft_ctx_set_gather(self.h, {"auto": 0, "kernel": 1, "tma": 2}[mode]))
 
+    def set_adam(self, mode: str):
+        """Fused layer step's sparse Adam: "epilogue" (in the weight-gradient GEMMs) or "pass" (separate kernel)."""
+        self.check(lib().meft_ctx_set_adam(self.h, {"epilogue": 0, "pass": 1}[mode]))
+
     def set_check_finite(self, on: bool):
         """Fused layer steps raise the reference's 'non-finite' error on NaN / Inf in out or grad_h."""
         self.check(lib().meft_ctx_set_check_finite(self.h, int(on)))

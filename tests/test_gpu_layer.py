@@ -294,3 +294,44 @@ def test_check_finite_raises_reference_kind(ctx):
         assert e.value.kind == "non-finite" and "non-finite" in str(e.value)
     finally:
         ctx.set_check_finite(False)
+
+
+@pytest.mark.parametrize("shape", [(512, 4096, 64, 32, 256),     # 1-CTA GEMMs (row-wise Adam epilogue)
+                                   (1024, 16384, 64, 64, 512)])  # CTA-pair GEMMs (transposed Adam epilogue)
+def test_adam_epilogue_matches_adam_pass_bitwise(ctx, shape):
+    """Sparse Adam inside the weight-gradient GEMM epilogues (EPI_ADAM_F32) applies the same per-entry update to
+    the same fp32 accumulator values as the separate Adam kernel over the gradient block: after three steps
+    (per-pair counters 1..3, intermittent pairs) every table, moment, counter and output is bit-identical, and the
+    cached key statistics still certify the keys."""
+    from paper_2406_04984_b200 import sharded as SH
+    d, M, N, K, T = shape
+    w_a, w_g, w_b, h, gr = cfg1_inputs(d, M, N, T)
+    hs = [bf16_dev(h), bf16_dev(gr), bf16_dev(-h), bf16_dev(gr[::-1].copy())]  # step 2 selects other pairs
+    res = []
+    for mode in ("pass", "epilogue"):
+        ctx.set_adam(mode)
+        st = make_store(ctx, w_a, w_g, w_b, N)
+        o = torch.empty((T, d), dtype=torch.float32, device="cuda")
+        gh = torch.empty_like(o)
+        for i in range(3):
+            x, gx = (hs[0], hs[1]) if i != 1 else (hs[2], hs[3])
+            st.layer_step(0, x, gx, 4, K, 1e-2, out=o, grad_h=gh)
+        torch.cuda.synchronize()
+        r = {"out": o.cpu().numpy(), "grad_h": gh.cpu().numpy()}
+        for name in ("w_a", "w_b", "m_a", "v_a", "m_b", "v_b", "pair_step"):
+            r[name] = st.download(0, name)
+        for name in ("w_a_compute", "w_b_compute"):
+            r[name] = st.tensor(0, name).cpu().view(torch.int16).numpy()
+        eng = SH.DeviceEngine(ctx, st, st.tensor(0, "w_g_compute"))
+        kn, kl = eng.key_stats()
+        keys = st.tensor(0, "w_a_compute").contiguous()
+        fn, fl = eng.row_stats(keys)
+        torch.cuda.synchronize()
+        assert torch.equal(kl, fl), mode
+        assert bool((kn.double() >= keys.double().norm(dim=1)).all()), mode
+        assert float((kn.double() / fn.double() - 1).abs().max()) < 1e-6, mode
+        res.append(r)
+    ctx.set_adam("epilogue")
+    assert res[0]["pair_step"].max() == 3
+    for n in res[0]:
+        np.testing.assert_array_equal(res[0][n], res[1][n], err_msg=n)
