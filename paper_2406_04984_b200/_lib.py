@@ -8,7 +8,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmeft_cuda.so")
+# MEFT_LIB: an alternative build of the same library (developer A/B variants, e.g. tools/ab_variants.sh)
+LIB_PATH = os.environ.get("MEFT_LIB") or os.path.join(HERE, "libmeft_cuda.so")
 
 P = C.c_void_p
 I64 = C.c_int64

@@ -333,9 +333,16 @@ __device__ __forceinline__ void epilogue_chunk(const KArgs& a, int m, int n, con
 
 // ---------------------------------------------------------------- EPI_ADAM_F32: sparse Adam in the epilogue
 // Four entries of one table row: the shared adam_update (bit-identical to k_adam_mixed), bf16 copy, statistics.
+// Key statistics (sum of squares of the new bf16 row) as an fp32 UPPER bound: every bf16 square is exact in fp32
+// and every addition rounds toward +inf, so the bound holds with no fp64 work in the epilogue (measured: the fp64
+// form made the key-table GEMM 0.5 ms slower and doubled its operand re-reads).
+using stat_t = float;
+__device__ __forceinline__ float stat_sq_add(float x, float s) { return __fmaf_ru(x, x, s); }
+__device__ __forceinline__ float stat_add(float a, float b) { return __fadd_ru(a, b); }
+
 template <bool STATS>
 __device__ __forceinline__ uint2 adam4(float4& w, float4& m, float4& v, const float4& g, const KArgs& a, AdamCoef k,
-                                       double& ss, int& lsb) {
+                                       stat_t& ss, int& lsb) {
     adam_update(w.x, m.x, v.x, g.x, a.b1, a.b2, a.eps, k);
     adam_update(w.y, m.y, v.y, g.y, a.b1, a.b2, a.eps, k);
     adam_update(w.z, m.z, v.z, g.z, a.b1, a.b2, a.eps, k);
@@ -344,8 +351,7 @@ __device__ __forceinline__ uint2 adam4(float4& w, float4& m, float4& v, const fl
     if (STATS) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const double x = double(bf16_bits_to_f32(c[q]));
-            ss = fma(x, x, ss);
+            ss = stat_sq_add(bf16_bits_to_f32(c[q]), ss);
             if (c[q] & 0x7FFF) lsb = min(lsb, bf16_lsb_exp(c[q]));
         }
     }
@@ -355,7 +361,8 @@ __device__ __forceinline__ uint2 adam4(float4& w, float4& m, float4& v, const fl
 // Pair kernel: the warp's 32 accumulator rows (one per lane, 32 columns per tcgen05.ld) are transposed through a
 // 32 x 36 fp32 shared scratch so that 8 lanes cover one table row's 128 contiguous bytes: every w/m/v load and
 // store is a full 128-byte segment. All 8 rows' loads of a chunk are issued before any update (24 x 16 B in flight
-// per lane) to cover DRAM latency behind the mainloop of the next tile.
+// per lane) to cover DRAM latency behind the mainloop of the next tile (an L2 prefetch one chunk ahead measured
+// neutral).
 __device__ __forceinline__ void st_shared_f4(uint32_t addr, float4 v) {
     asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                  : "memory");
@@ -384,19 +391,11 @@ __device__ __forceinline__ void adam_tile_transposed(const KArgs& a, uint32_t ta
         j[it] = __shfl_sync(0xffffffffu, jl, row);
         k[it] = AdamCoef{__shfl_sync(0xffffffffu, kl.x, row), __shfl_sync(0xffffffffu, kl.y, row)};
     }
-    // L2 prefetch of one 128-byte row segment per array, one chunk ahead (lanes 0-2: w, m, v of row `lane`)
-    auto prefetch = [&](int n) {
-        if (lane < 3 && jl >= 0 && n < a.N) {
-            const float* base = lane == 0 ? a.adam_w : lane == 1 ? a.adam_m : a.adam_v;
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (long long)jl * a.ldc + n));
-        }
-    };
-    prefetch(n_col0);
-    double ss[8];
+    stat_t ss[8];
     int lsb[8];
 #pragma unroll
     for (int it = 0; it < 8; ++it) {
-        ss[it] = 0.0;
+        ss[it] = 0;
         lsb[it] = INT32_MAX;
     }
 #pragma unroll 1
@@ -405,7 +404,6 @@ __device__ __forceinline__ void adam_tile_transposed(const KArgs& a, uint32_t ta
         if (n >= a.N) break;  // warp-uniform (N % 32 == 0)
         uint32_t r[32];
         tmem_ld_32x32b_x32(taddr + c * 32, r);
-        prefetch(n + 32);
         float4 w[8], m[8], v[8];
 #pragma unroll
         for (int it = 0; it < 8; ++it) {  // invalid rows (past M: j < 0) read row 0 and never store
@@ -440,11 +438,11 @@ __device__ __forceinline__ void adam_tile_transposed(const KArgs& a, uint32_t ta
         const int nb = n_col0 / kAdamStatTile;
 #pragma unroll
         for (int it = 0; it < 8; ++it) {
-            double t = ss[it];
+            stat_t t = ss[it];
             int l = lsb[it];
 #pragma unroll
             for (int o = 1; o < 8; o <<= 1) {
-                t += __shfl_xor_sync(0xffffffffu, t, o);
+                t = stat_add(t, __shfl_xor_sync(0xffffffffu, t, o));
                 l = min(l, __shfl_xor_sync(0xffffffffu, l, o));
             }
             const int mr = m0 + it * 4 + sub;
@@ -462,7 +460,7 @@ __device__ __forceinline__ void adam_tile_rows(const KArgs& a, uint32_t taddr, i
     const int j = ok ? __ldg(a.row_idx + m) : 0;
     const float2 kl = ok ? __ldg(a.adam_coef + m) : make_float2(0.f, 0.f);
     const AdamCoef k{kl.x, kl.y};
-    double ss = 0.0;
+    stat_t ss = 0;
     int lsb = INT32_MAX;
 #pragma unroll 1
     for (int c = 0; c < BN / 32; ++c) {

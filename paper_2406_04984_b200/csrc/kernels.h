@@ -38,7 +38,8 @@ enum GemmEpi : int {
     // gradient of table row j = row_idx[m]; the epilogue applies adam_update to adam_w/m/v[j*ldc + n] with the
     // per-position coefficients adam_coef[m] (scale, inv_c2) and writes the bf16 compute copy adam_c. With stat_ss
     // it also emits the selection statistics of the new bf16 row per 256-column tile nb:
-    // stat_ss[m*stat_ld + nb] = fp64 sum of squares, stat_lsb[...] = minimum LSB exponent of the nonzero entries.
+    // stat_ss[m*stat_ld + nb] = an upper bound of the sum of squares (fp32 sums rounded up, stored as double),
+    // stat_lsb[...] = minimum LSB exponent of the nonzero entries.
     // No K split (the update needs the finished gradient); N <= 65536.
     EPI_ADAM_F32 = 8,
 };

@@ -186,8 +186,9 @@ __global__ void k_adam_coef_bump(const int32_t* __restrict__ rows, int n, int32_
     }
 }
 
-// Key-row selection statistics from the epilogue's per-256-column partials, summed in column order (the bound of
-// k_row_norms: sqrt of the fp64 sum of squares, rounded up with a 2^-20 margin).
+// Key-row selection statistics from the epilogue's per-256-column partials (fp32 upper bounds of the partial sums
+// of squares), summed in column order; same bound form as k_row_norms: sqrt of the sum, rounded up with a 2^-20
+// margin (which also covers the fp64 rounding of this 16-term sum).
 __global__ void k_adam_stats_finalize(const int32_t* __restrict__ rows, int n, const double* __restrict__ ss,
                                       const int32_t* __restrict__ lsb, int parts, float* __restrict__ kn,
                                       int32_t* __restrict__ kl) {
