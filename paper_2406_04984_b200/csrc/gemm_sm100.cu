@@ -1147,7 +1147,12 @@ void gemm_bf16_one(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmO
             const char* v = std::getenv("MEFT_PAIR_GROUP");  // A/B experiments
             return v ? std::max(1, std::atoi(v)) : 0;
         }();
+        static const int forced_amn = [] {
+            const char* v = std::getenv("MEFT_PAIR_GROUP_AMN");  // A/B experiments (grad-W GEMMs)
+            return v ? std::max(1, std::atoi(v)) : 0;
+        }();
         args.raster_group = forced ? forced : (!A.mn_major && !B.mn_major ? 16 : 8);
+        if (A.mn_major && forced_amn) args.raster_group = forced_amn;
         // L2 residency (K-major x K-major, i.e. z / masked: h against the key or value table): the small operand
         // every output tile re-reads is loaded evict_last, the streamed table evict_first (measured: masked GEMM
         // 3.33 -> 3.18 ms, DRAM reads 6.3 -> 5.4 GB; step -1.5%). Hinting the MN-major grad-W GEMMs the same way

@@ -70,6 +70,36 @@ __global__ void k_stage_add(S* __restrict__ stage, int64_t d, const int32_t* __r
     if (staged && threadIdx.x == 0) staged[row] = 1;
 }
 
+// fp32 staging, fp32 gradients (the mixed store's scatter_grads): 16-byte vectors, 4 in flight per thread.
+__global__ void __launch_bounds__(256) k_stage_add_f32x4(float* __restrict__ stage, int64_t d,
+                                                         const int32_t* __restrict__ idx, int n,
+                                                         const float* __restrict__ g, uint8_t* __restrict__ staged) {
+    const int r = blockIdx.x;
+    if (r >= n) return;
+    const int64_t row = idx[r];
+    float4* s = reinterpret_cast<float4*>(stage + row * d);
+    const float4* gr = reinterpret_cast<const float4*>(g + int64_t(r) * d);
+    const int d4 = int(d / 4);
+    constexpr int U = 4;
+    for (int i0 = threadIdx.x; i0 < d4; i0 += blockDim.x * U) {
+        float4 a[U], b[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = i0 + u * blockDim.x;
+            if (i < d4) {
+                a[u] = s[i];
+                b[u] = __ldcs(gr + i);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = i0 + u * blockDim.x;
+            if (i < d4) s[i] = make_float4(a[u].x + b[u].x, a[u].y + b[u].y, a[u].z + b[u].z, a[u].w + b[u].w);
+        }
+    }
+    if (staged && threadIdx.x == 0) staged[row] = 1;
+}
+
 __global__ void k_mark(uint8_t* __restrict__ staged, const int32_t* __restrict__ idx, const int32_t* count_dev,
                        int count) {
     const int n = count_dev ? *count_dev : count;
@@ -363,6 +393,9 @@ void stage_add(cudaStream_t st, int stage_dtype, void* stage, int64_t d, const i
     if (stage_dtype == 0 && g_dtype == 0)
         k_stage_add<double, double><<<int(n), 256, 0, st>>>(static_cast<double*>(stage), d, idx, int(n),
                                                             static_cast<const double*>(g), staged);
+    else if (stage_dtype == 1 && g_dtype == 1 && d % 4 == 0 && (reinterpret_cast<uintptr_t>(stage) | reinterpret_cast<uintptr_t>(g)) % 16 == 0)
+        k_stage_add_f32x4<<<int(n), 256, 0, st>>>(static_cast<float*>(stage), d, idx, int(n),
+                                                  static_cast<const float*>(g), staged);
     else if (stage_dtype == 1 && g_dtype == 1)
         k_stage_add<float, float><<<int(n), 256, 0, st>>>(static_cast<float*>(stage), d, idx, int(n),
                                                           static_cast<const float*>(g), staged);

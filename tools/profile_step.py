@@ -10,9 +10,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2406_04984_b200 import meft as G  # noqa: E402
 
 
-def main():
-    steps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
-    adam = sys.argv[2] if len(sys.argv) > 2 else "epilogue"
+def make_step(adam="epilogue"):
+    """A cfg2 store and inputs; returns step() running one fused layer step."""
     d, M, N, K, kk, T = 4096, 65536, 256, 128, 4, 8192
     ctx = G.Context(0)
     ctx.set_adam(adam)
@@ -25,11 +24,18 @@ def main():
     del w_b
     h = (torch.rand((T, d), generator=gen, device="cuda") * 2 - 1).to(torch.bfloat16)
     g = (torch.rand((T, d), generator=gen, device="cuda") * 2 - 1).to(torch.bfloat16)
+    return lambda: st.layer_step(0, h, g, kk, K, 1e-4)
+
+
+def main():
+    steps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+    adam = sys.argv[2] if len(sys.argv) > 2 else "epilogue"
+    step = make_step(adam)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for i in range(steps):
         if i == 1:
             e0.record(torch.cuda.current_stream())
-        st.layer_step(0, h, g, kk, K, 1e-4)
+        step()
     e1.record(torch.cuda.current_stream())
     torch.cuda.synchronize()
     if steps > 1:
