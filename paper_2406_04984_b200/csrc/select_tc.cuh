@@ -40,6 +40,16 @@ __device__ __forceinline__ double bfd(uint16_t b) { return double(bf16_bits_to_f
 // (an exact product has <= 16 significant bits; subnormals: 2^-149), sum|p| is accumulated in fp32 and inflated by
 // 2^-10 (its rounding error over <= 2^16 terms per lane and the warp sum is far smaller); the value in fp64.
 // ~6 instructions per product and loads 4 deep (the generic path below is ~15 and latency-bound).
+// Exponent of the lowest set bit of a finite nonzero double: x is a multiple of 2^lowbit_exp(x).
+__device__ __forceinline__ int lowbit_exp(double x) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x)) & 0x7FFFFFFFFFFFFFFFull;
+    const int e = int(b >> 52);
+    unsigned long long m = b & 0xFFFFFFFFFFFFFull;
+    if (e == 0) return -1074 + __ffsll(static_cast<long long>(m)) - 1;  // subnormal: m * 2^-1074
+    m |= 1ull << 52;
+    return e - 1075 + __ffsll(static_cast<long long>(m)) - 1;
+}
+
 __device__ __forceinline__ bool exact_dot_warp_f32(const uint4* __restrict__ a4, const uint4* __restrict__ b4, int d8,
                                                    int lane, double& value) {
     constexpr int U = 4;
@@ -135,18 +145,46 @@ __device__ double exact_dot_warp(const uint16_t* __restrict__ a, const uint16_t*
     }
     // every partial sum (in ANY order) is a multiple of 2^lsb bounded by sum|p|: representable iff < 2^(lsb+53)
     if (lsb == INT32_MAX || sa * (1.0 + 0x1p-30) < ldexp(1.0, lsb + 53)) return s;
+#ifdef MEFT_TIMING_PROBE_NO_SEQUENTIAL  // developer timing probe only: WRONG results for uncertified dots
+    return s;
+#endif
     // Certificate failed: the reference's sequential chain acc = fl(acc + a_k b_k), k ascending (products exact, so
-    // this equals its fma chain). The warp loads and multiplies 32 terms at a time; every lane then runs the same
-    // dependent add chain over the broadcast products -- only the fp64 adds are serial.
+    // this equals its fma chain), evaluated 128 terms at a time (lane l holds k = base + 4l .. 4l+3). A chunk whose
+    // every prefix sum acc + p_1 + ... + p_i is provably representable -- all are multiples of 2^L, L = the lowest
+    // set bit over acc and the chunk's products, and |acc| + sum|p| < 2^(L+53) -- adds no rounding, so the chain
+    // through it equals acc + (warp sum of the chunk), which is itself exact (every subset sum obeys the same
+    // bound). Only chunks that fail this local test run the dependent add chain over the broadcast products.
     double acc = 0.0;
-    for (int base = 0; base < d; base += 32) {
-        const int k = base + lane;
-        const double p = k < d ? bfd(a[k]) * bfd(b[k]) : 0.0;
-        const int n = min(32, d - base);
+    for (int base = 0; base < d; base += 128) {
+        double p[4];
+        double ls = 0.0, la = 0.0;
+        int lo = INT32_MAX;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            const double pj = __shfl_sync(0xffffffffu, p, j);
-            if (j < n) acc += pj;
+        for (int q = 0; q < 4; ++q) {
+            const int k = base + 4 * lane + q;
+            p[q] = k < d ? bfd(a[k]) * bfd(b[k]) : 0.0;
+            if (p[q] != 0.0) lo = min(lo, lowbit_exp(p[q]));
+            ls += p[q];
+            la += fabs(p[q]);
+        }
+        double cs = ls, ca = la;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            cs += __shfl_xor_sync(0xffffffffu, cs, o);
+            ca += __shfl_xor_sync(0xffffffffu, ca, o);
+            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        }
+        if (lo == INT32_MAX) continue;  // all 128 products are +-0: acc + (+-0) leaves acc unchanged
+        const int L = acc != 0.0 ? min(lo, lowbit_exp(acc)) : lo;
+        if ((fabs(acc) + ca) * (1.0 + 0x1p-40) < ldexp(1.0, L + 53)) {
+            acc += cs;
+            continue;
+        }
+        const int n = min(128, d - base);
+        for (int j = 0; j < n; ++j) {
+            const double pj = __shfl_sync(0xffffffffu, (j & 3) == 0 ? p[0] : (j & 3) == 1 ? p[1] : (j & 3) == 2 ? p[2] : p[3],
+                                          j >> 2);
+            acc += pj;
         }
     }
     if (lane == 0 && fallbacks) atomicAdd(fallbacks, 1);
@@ -197,7 +235,10 @@ __device__ __forceinline__ double exact_dot_rows(const uint16_t* __restrict__ a,
         // in fp32 too (a multiple of 2^-149 below 2^127 with <= 16 significant bits): one fp32 multiply and one
         // widening per product instead of two widenings and a DFMA.
         const bool f32_products = lsb >= -149 && lsb <= 74;
-        constexpr int U = 4;
+#ifndef MEFT_RESCORE_U
+#define MEFT_RESCORE_U 4
+#endif
+        constexpr int U = MEFT_RESCORE_U;
         double s0 = 0.0, s1 = 0.0;
         for (int v0 = lane; v0 < d / 8; v0 += 32 * U) {
             uint4 x[U], y[U];

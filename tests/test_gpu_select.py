@@ -205,3 +205,37 @@ def test_certified_at_extreme_magnitudes(ctx, scale_h, scale_k):
     np.testing.assert_array_equal(tau, want["tau"])
     np.testing.assert_array_equal(per, want["per_token"])
     np.testing.assert_array_equal(uni, want["unioned"])
+
+
+@pytest.mark.parametrize("d", [64, 1024, 4096])
+def test_exact_scores_uncertifiable_dots_match_reference_chain(ctx, d):
+    """Dots whose products span far more than 53 bits fail the whole-row exactness certificate and take the
+    chunked sequential fallback: 128-term chunks whose prefix sums are provably exact are added as one warp sum,
+    the rest replay the reference's dependent fp64 chain. Magnitude patterns put the tiny and huge products in the
+    same chunk, in different chunks, at chunk edges and at random; every score must equal the reference's dot()
+    (kernels.hpp:37-41, via the C restatement) bit for bit."""
+    from paper_2406_04984_b200 import sharded as SH
+    rs = np.random.RandomState(d)
+    M, N, R = 64, 8, 24
+    keys = rs.uniform(-1, 1, (M, d))
+    rows = rs.uniform(-1, 1, (R, d))
+    rows[0, d // 2:] *= 2.0 ** -70                    # tiny tail
+    rows[1, :d // 2] *= 2.0 ** -70                    # tiny head
+    rows[2, ::2] *= 2.0 ** -60                        # alternating inside every chunk
+    rows[3, (np.arange(d) // 128) % 2 == 1] *= 2.0 ** -80  # alternating chunks
+    rows[4, 127::128] *= 2.0 ** 40                    # chunk-edge spikes
+    rows[5, rs.rand(d) < 0.1] *= 2.0 ** -100           # sparse tiny entries
+    rows[6] *= 2.0 ** (rs.randint(-90, 30, d))         # random exponents per entry
+    rows[7, : d // 4] = 0.0                           # leading zeros, then a wide range
+    rows[7, d // 4:] *= 2.0 ** rs.randint(-70, 0, d - d // 4)
+    keys[1::3] *= 2.0 ** (rs.randint(-40, 40, (len(keys[1::3]), d)))
+    keys, rows = O.bf16_round(keys), O.bf16_round(rows)
+    st = G.Store(ctx, 1, d, M, N, G.STORE_MIXED)
+    st.upload(0, "w_a", keys.T.copy())
+    st.upload(0, "w_g", O.bf16_round(rs.uniform(-1, 1, (N, d))))
+    eng = SH.DeviceEngine(ctx, st, st.tensor(0, "w_g_compute"))
+    pr, pk = np.meshgrid(np.arange(R), np.arange(M), indexing="ij")
+    got = eng.exact(dev(rows, True), torch.from_numpy(pr.ravel().astype(np.int32)).cuda(),
+                    torch.from_numpy(pk.ravel().astype(np.int32)).cuda()).cpu().numpy().reshape(R, M)
+    want = np.stack([O.route_scores(rows[r], keys) for r in range(R)])
+    np.testing.assert_array_equal(got, want)
