@@ -42,6 +42,8 @@ struct KArgs {
     long long ldc;
     const uint16_t* mask;
     long long ldm;
+    uint32_t* bits;
+    long long ldbits;
     const int32_t* row_idx;
     // grouped mode: G groups; group g owns A rows [g_row_off[g], g_row_off[g+1]) and B rows
     // [g*g_brows, (g+1)*g_brows); g_tile_off = exclusive scan of its BM-tiles (device arrays).
@@ -238,6 +240,12 @@ __device__ __forceinline__ void epilogue_chunk(const KArgs& a, int m, int n, con
         }
         case EPI_RELU_BF16: {
             uint16_t* c = reinterpret_cast<uint16_t*>(a.c) + (long long)m * a.ldc + n;
+            if (a.bits) {
+                uint32_t w = 0;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) w |= (j < cnt && __uint_as_float(r[j]) > 0.0f) ? (1u << j) : 0u;
+                __stcs(a.bits + (long long)m * a.ldbits + (n >> 5), w);
+            }
             if (cnt == 32) {
                 uint4* c4 = reinterpret_cast<uint4*>(c);
 #pragma unroll
@@ -260,6 +268,27 @@ __device__ __forceinline__ void epilogue_chunk(const KArgs& a, int m, int n, con
         }
         case EPI_MASK_BF16: {
             uint16_t* c = reinterpret_cast<uint16_t*>(a.c) + (long long)m * a.ldc + n;
+            if (a.bits) {  // bitmask of act > 0 (written by the z GEMM's EPI_RELU_BF16)
+                const uint32_t w = __ldcs(a.bits + (long long)m * a.ldbits + (n >> 5));
+                if (cnt == 32) {
+                    uint4* c4 = reinterpret_cast<uint4*>(c);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        uint32_t o[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const int e = 8 * j + 2 * q;
+                            const uint16_t lo = (w >> e) & 1u ? f32_to_bf16_bits(__uint_as_float(r[e])) : 0;
+                            const uint16_t hi = (w >> (e + 1)) & 1u ? f32_to_bf16_bits(__uint_as_float(r[e + 1])) : 0;
+                            o[q] = pack_bf16x2(lo, hi);
+                        }
+                        __stcs(c4 + j, make_uint4(o[0], o[1], o[2], o[3]));
+                    }
+                } else {
+                    for (int j = 0; j < cnt; ++j) c[j] = (w >> j) & 1u ? f32_to_bf16_bits(__uint_as_float(r[j])) : 0;
+                }
+                break;
+            }
             const uint16_t* mk = a.mask + (long long)m * a.ldm + n;
             if (cnt == 32) {
                 uint4* c4 = reinterpret_cast<uint4*>(c);
@@ -997,7 +1026,7 @@ void check_epilogue(const GemmEpilogue& epi) {
     } else {
         if (!aligned16(epi.c) || (epi.ldc % 8)) throw MeftError(2, "gemm_bf16: bf16 output alignment");
     }
-    if (epi.kind == EPI_MASK_BF16 && (!aligned16(epi.mask) || (epi.ldm % 8)))
+    if (epi.kind == EPI_MASK_BF16 && !epi.bits && (!aligned16(epi.mask) || (epi.ldm % 8)))
         throw MeftError(2, "gemm_bf16: mask alignment");
     if ((epi.kind == EPI_ACT_BF16 || epi.kind == EPI_DACT_BF16) && (!epi.aux || epi.ldaux < 1 || epi.act < 0 ||
                                                                    epi.act > 1))
@@ -1018,6 +1047,8 @@ KArgs base_args(int64_t M, int64_t N, int64_t K, const GemmEpilogue& epi) {
     args.ldc = epi.ldc;
     args.mask = static_cast<const uint16_t*>(epi.mask);
     args.ldm = epi.ldm;
+    args.bits = epi.bits;
+    args.ldbits = epi.ldbits;
     args.row_idx = epi.row_idx;
     args.grouped = 0;
     args.b_idx = nullptr;
@@ -1250,6 +1281,7 @@ void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOpera
                     e.c = const_cast<void*>(advance(epi.c, m0 * epi.ldc + n0, ce));
                 }
                 if (epi.mask) e.mask = advance(epi.mask, m0 * epi.ldm + n0, 2);
+                if (epi.bits) e.bits = epi.bits + m0 * epi.ldbits + n0 / 32;
                 if (epi.aux) e.aux = const_cast<void*>(advance(epi.aux, m0 * epi.ldaux + n0, 2));
                 gemm_bf16_one(st, ml, nl, kl, a, b, e);
             }

@@ -23,8 +23,8 @@ struct GemmOperand {
 
 enum GemmEpi : int {
     EPI_STORE_F32 = 0,     // C f32 [M x ldc] = acc            (or += acc when accumulate)
-    EPI_RELU_BF16 = 1,     // C bf16 = relu(acc), positive never rounds to zero
-    EPI_MASK_BF16 = 2,     // C bf16 = mask(m,n) > 0 ? acc : 0 ; mask bf16 [M x ldm]
+    EPI_RELU_BF16 = 1,     // C bf16 = relu(acc), positive never rounds to zero; with `bits` also the bitmask acc > 0
+    EPI_MASK_BF16 = 2,     // C bf16 = mask(m,n) > 0 ? acc : 0 ; mask bf16 [M x ldm], or the bitmask `bits`
     EPI_ROWS_ADD_F32 = 3,  // C f32: C[row_idx[m]*ldc + n] += acc (row_idx unique -> no atomics)
     EPI_ROWS_STORE_F32 = 4,  // C f32: C[row_idx[m]*ldc + n] = acc
     // Push to peers: global row g = row0 + m belongs to home h = g / peer_rows; the f32 row is stored into that
@@ -51,6 +51,10 @@ struct GemmEpilogue {
     int64_t ldc = 0;
     const void* mask = nullptr;
     int64_t ldm = 0;
+    // EPI_RELU_BF16 (written) / EPI_MASK_BF16 (read instead of `mask`): bit (n % 32) of bits[m * ldbits + n / 32]
+    // is acc(m, n) > 0 -- 1/16 of the bytes of the bf16 activation as the backward's mask.
+    uint32_t* bits = nullptr;
+    int64_t ldbits = 0;
     const int32_t* row_idx = nullptr;
     bool accumulate = false;
     // K split (f32 store epilogues, 1-CTA kernel): split s of `ksplit` multiplies K-chunk s only and writes its

@@ -271,7 +271,8 @@ GemmEpilogue peer_epilogue(const meft_peer_out& po, bool grad_h, int64_t d) {
 
 void ffn_forward_impl(meft_ctx* ctx, meft_dtype dt, const void* h, const void* keys_s, const void* values_s,
                       int64_t T, int64_t d, int64_t s, int64_t ld_z, void* z, void* out, bool accumulate,
-                      const RowGather& rg = RowGather(), const meft_peer_out* peer = nullptr) {
+                      const RowGather& rg = RowGather(), const meft_peer_out* peer = nullptr,
+                      uint32_t* act_bits = nullptr) {
     cudaStream_t st = ctx->stream;
     if (dt == MEFT_F64) {
         double* outd = static_cast<double*>(out);
@@ -298,6 +299,8 @@ void ffn_forward_impl(meft_ctx* ctx, meft_dtype dt, const void* h, const void* k
     e1.kind = EPI_RELU_BF16;
     e1.c = z;
     e1.ldc = ld_z;
+    e1.bits = act_bits;  // [T x ceil(s / 32)] bitmask of z > 0 for the backward's mask
+    e1.ldbits = (s + 31) / 32;
     gemm_bf16(st, T, s, d, GemmOperand{h, d, false}, kv_operand(ctx, keys_s, d, false, rg, s), e1);
     GemmEpilogue e2;
     if (peer) {
@@ -318,7 +321,7 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
                        void* stage_keys, void* stage_values, const RowGather& rg = RowGather(),
                        cudaEvent_t grad_h_done = nullptr, const std::function<void()>* between = nullptr,
                        const meft_peer_out* peer = nullptr, const GemmEpilogue* epi_values = nullptr,
-                       const GemmEpilogue* epi_keys = nullptr) {
+                       const GemmEpilogue* epi_keys = nullptr, const uint32_t* act_bits = nullptr) {
     cudaStream_t st = ctx->stream;
     if (dt == MEFT_F64) {
         const double* gd = static_cast<const double*>(g);
@@ -360,6 +363,8 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
     e3.ldc = ld_z;
     e3.mask = z;
     e3.ldm = ld_z;
+    e3.bits = const_cast<uint32_t*>(act_bits);  // the forward's bitmask instead of re-reading act (1/16 the bytes)
+    e3.ldbits = (s + 31) / 32;
     gemm_bf16(st, T, s, d, GemmOperand{g, d, false}, kv_operand(ctx, values_s, d, false, rg, s), e3);
     if (grad_h || peer) {  // first after masked, so grad_h can stream back while the weight-gradient GEMMs run
         GemmEpilogue e6;  // grad_h (+)= masked * keys_s
@@ -1320,6 +1325,15 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
 
     uint16_t* act = static_cast<uint16_t*>(ctx->get("act", size_t(T * ld) * 2));
     uint16_t* masked = static_cast<uint16_t*>(ctx->get("masked", size_t(T * ld) * 2));
+    // the z GEMM also writes the bitmask z > 0; the masked GEMM reads it instead of the bf16 act (64 MB instead of
+    // 1 GB at cfg2). MEFT_ACT_BITS=0 reads act (A/B; bitwise identical).
+    static const bool use_bits = [] {
+        const char* v = std::getenv("MEFT_ACT_BITS");
+        return !(v && v[0] == '0');
+    }();
+    uint32_t* act_bits = use_bits ? static_cast<uint32_t*>(ctx->get(
+                                        "act_bits", size_t(std::max<int64_t>(T * ((su + 31) / 32), 1)) * 4))
+                                  : nullptr;
     float* outb = out ? out : static_cast<float*>(ctx->get("out", size_t(T * d) * 4));
     float* ghb = grad_h ? grad_h : static_cast<float*>(ctx->get("grad_h", size_t(T * d) * 4));
     // fetch (memtier.cpp:117-126): the selected key/value rows of the bf16 compute tables, either gathered inside
@@ -1367,7 +1381,7 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
             e2.ldc = d;
             gemm_bf16(st, T, d, base->n, GemmOperand{base_act, ldn, false}, GemmOperand{base->w_out, d, true}, e2);
         }
-        ffn_forward_impl(ctx, MEFT_BF16, h, ks, vs, T, d, su, ld, act, outb, base != nullptr, rg, peer);
+        ffn_forward_impl(ctx, MEFT_BF16, h, ks, vs, T, d, su, ld, act, outb, base != nullptr, rg, peer, act_bits);
     }
     if (fwd_done) MEFT_CUDA_CHECK(cudaEventRecord(fwd_done, st));
     if (g_ready) MEFT_CUDA_CHECK(cudaStreamWaitEvent(st, g_ready, 0));
@@ -1403,7 +1417,8 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
         {
             PhaseScope ps(ctx, 3);
             ffn_backward_impl(ctx, MEFT_BF16, g, h, act, ks, vs, T, d, su, ld, masked, nullptr, nullptr, ghb,
-                              base != nullptr, uni, L.st_a, L.st_b, rg, gh_done, nullptr, peer);
+                              base != nullptr, uni, L.st_a, L.st_b, rg, gh_done, nullptr, peer, nullptr, nullptr,
+                              act_bits);
         }
         train_router();
         PhaseScope ps(ctx, 4);
@@ -1444,7 +1459,8 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
         {
             PhaseScope ps(ctx, 3);
             ffn_backward_impl(ctx, MEFT_BF16, g, h, act, ks, vs, T, d, su, ld, masked, nullptr, nullptr, ghb,
-                              base != nullptr, nullptr, nullptr, nullptr, rg, gh_done, nullptr, peer, &ev, &ek);
+                              base != nullptr, nullptr, nullptr, nullptr, rg, gh_done, nullptr, peer, &ev, &ek,
+                              act_bits);
         }
         train_router();
         if (stats) {
@@ -1475,7 +1491,7 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
             p3.emplace(ctx, 3);
         };
         ffn_backward_impl(ctx, MEFT_BF16, g, h, act, ks, vs, T, d, su, ld, masked, gblk, gblk, ghb, base != nullptr,
-                          nullptr, nullptr, nullptr, rg, gh_done, &values_step, peer);
+                          nullptr, nullptr, nullptr, rg, gh_done, &values_step, peer, nullptr, nullptr, act_bits);
         p3.reset();
         train_router();
         if (su > 0) adam_table(1);
