@@ -145,9 +145,6 @@ __device__ double exact_dot_warp(const uint16_t* __restrict__ a, const uint16_t*
     }
     // every partial sum (in ANY order) is a multiple of 2^lsb bounded by sum|p|: representable iff < 2^(lsb+53)
     if (lsb == INT32_MAX || sa * (1.0 + 0x1p-30) < ldexp(1.0, lsb + 53)) return s;
-#ifdef MEFT_TIMING_PROBE_NO_SEQUENTIAL  // developer timing probe only: WRONG results for uncertified dots
-    return s;
-#endif
     // Certificate failed: the reference's sequential chain acc = fl(acc + a_k b_k), k ascending (products exact, so
     // this equals its fma chain), evaluated 128 terms at a time (lane l holds k = base + 4l .. 4l+3). A chunk whose
     // every prefix sum acc + p_1 + ... + p_i is provably representable -- all are multiples of 2^L, L = the lowest
@@ -235,10 +232,7 @@ __device__ __forceinline__ double exact_dot_rows(const uint16_t* __restrict__ a,
         // in fp32 too (a multiple of 2^-149 below 2^127 with <= 16 significant bits): one fp32 multiply and one
         // widening per product instead of two widenings and a DFMA.
         const bool f32_products = lsb >= -149 && lsb <= 74;
-#ifndef MEFT_RESCORE_U
-#define MEFT_RESCORE_U 4
-#endif
-        constexpr int U = MEFT_RESCORE_U;
+        constexpr int U = 4;  // 8 and 16 measured equal (the kernel's tail is the uncertifiable dots, not load depth)
         double s0 = 0.0, s1 = 0.0;
         for (int v0 = lane; v0 < d / 8; v0 += 32 * U) {
             uint4 x[U], y[U];
