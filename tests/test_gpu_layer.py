@@ -298,7 +298,8 @@ def test_check_finite_raises_reference_kind(ctx):
 
 
 @pytest.mark.parametrize("shape", [(512, 4096, 64, 32, 256),     # 1-CTA GEMMs (row-wise Adam epilogue)
-                                   (1024, 16384, 64, 64, 512)])  # CTA-pair GEMMs (transposed Adam epilogue)
+                                   (1024, 16384, 64, 64, 512),   # CTA-pair GEMMs (transposed Adam epilogue)
+                                   (1056, 8192, 32, 64, 384)])   # d % 256 != 0: partial column tile + stats part
 def test_adam_epilogue_matches_adam_pass_bitwise(ctx, shape):
     """Sparse Adam inside the weight-gradient GEMM epilogues (EPI_ADAM_F32) applies the same per-entry update to
     the same fp32 accumulator values as the separate Adam kernel over the gradient block: after three steps
