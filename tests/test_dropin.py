@@ -1,5 +1,7 @@
-"""The drop-in boundary: the reference's OWN unit tests (proj/tests/test_{numerics,adapter,experts,memtier}.cpp),
-compiled unmodified with tests/dropin/doctest.h against
+"""The drop-in boundary: the reference's OWN unit tests (proj/tests/test_{numerics,adapter,experts,memtier}.cpp, and
+test_{model,trainer}.cpp which drive the reference's trainer -- train(), eval_em, resume, micro-batch accumulation,
+full-model finite differences, meft(K=r, N=1) == dense trajectory -- end to end), compiled unmodified with
+tests/dropin/doctest.h against
 
   * the reference library itself (CPU; validates the harness — oracle/Makefile ref-tests), and
   * this repo's C++ shim libmeft_dropin.so over the C ABI (GPU; every numeric step on the B200).
@@ -14,7 +16,7 @@ import subprocess
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SUITES = ("test_numerics", "test_adapter", "test_experts", "test_memtier")
+SUITES = ("test_numerics", "test_adapter", "test_experts", "test_memtier", "test_model", "test_trainer")
 REF_BIN = os.path.join(ROOT, "oracle", "_ref", "tests")
 DROPIN_BIN = os.path.join(ROOT, "build", "dropin_tests")
 DROPIN_LIB = os.path.join(ROOT, "paper_2406_04984_b200", "libmeft_dropin.so")
