@@ -211,6 +211,33 @@ meft_status meft_base_ffn_backward(meft_ctx* ctx, const double* grad_out, const 
                                    const double* w_in, const double* w_out, int64_t T, int64_t d, int64_t n, int act,
                                    double* grad_h);
 
+/* ---- The reference's frozen toy trunk (model.cpp:50-218), fp64 on the device: what the drop-in's model.hpp
+ * functions call so that the reference trainer runs end to end on the B200. Arrays are device buffers (row-major,
+ * T = batch * seq rows); reductions follow the reference's order (deterministic). Ids must be in range: the drop-in
+ * validates them on the host with the reference's exceptions before calling. */
+/* embed (model.cpp:50-68): h[b*seq + i] = emb[tokens[.]] + pos[i] */
+meft_status meft_embed_f64(meft_ctx* ctx, const double* emb, int64_t vocab, const double* pos, int64_t max_seq,
+                           int64_t d, const int32_t* tokens, int64_t batch, int64_t seq, double* h);
+/* attention_forward (model.cpp:70-122): out = h + softmax(q k^T / sqrt(d), causal, same segment) v wo, q/k/v = h
+ * wq/wk/wv; the cache (q, k, v [T x d], probs [T x seq]) is returned for the backward. */
+meft_status meft_attention_forward_f64(meft_ctx* ctx, const double* h, const double* wq, const double* wk,
+                                       const double* wv, const double* wo, const int32_t* segments, int64_t batch,
+                                       int64_t seq, int64_t d, double* out, double* q, double* k, double* v,
+                                       double* probs);
+/* attention_backward (model.cpp:124-173): dh = dh_out + dq wq^T + dk wk^T + dv wv^T (weights frozen) */
+meft_status meft_attention_backward_f64(meft_ctx* ctx, const double* wq, const double* wk, const double* wv,
+                                        const double* wo, const int32_t* segments, int64_t batch, int64_t seq,
+                                        int64_t d, const double* q, const double* k, const double* v,
+                                        const double* probs, const double* dh_out, double* dh);
+/* lm_loss_and_grad (model.cpp:175-203): tied logits h emb^T, scaled cross-entropy at loss_mask positions;
+ * *loss_sum (host) and dh [T x d] (device). Synchronises. */
+meft_status meft_lm_loss_f64(meft_ctx* ctx, const double* emb, int64_t vocab, int64_t d, const double* h, int64_t T,
+                             const int32_t* targets, const uint8_t* loss_mask, double loss_scale, double* loss_sum,
+                             double* dh);
+/* argmax_logits (model.cpp:205-218): greedy token for one row, ties toward the lowest id; *token on the host. */
+meft_status meft_argmax_logits_f64(meft_ctx* ctx, const double* emb, int64_t vocab, int64_t d, const double* h_row,
+                                   int64_t* token);
+
 /* Dense fp64 product C[m x n] = A[m x k] * B[k x n] (row-major), the reference matmul (kernels.cpp:57-76):
  * ascending-k fma chains that skip zero a-entries, bitwise equal to the compiled reference. Non-finite
  * results return MEFT_E_NONFINITE like check_finite (kernels.cpp:7-13); synchronises. */

@@ -84,6 +84,12 @@ _SIGS = {
     "meft_base_ffn_forward": (INT, [P, P, P, P, I64, I64, I64, INT, P, P]),
     "meft_base_ffn_backward": (INT, [P, P, P, P, P, I64, I64, I64, INT, P]),
     "meft_matmul_f64": (INT, [P, P, P, I64, I64, I64, P]),
+    # toy trunk (model.cpp:50-218), fp64 device buffers
+    "meft_embed_f64": (INT, [P, P, I64, P, I64, I64, P, I64, I64, P]),
+    "meft_attention_forward_f64": (INT, [P, P, P, P, P, P, P, I64, I64, I64, P, P, P, P, P]),
+    "meft_attention_backward_f64": (INT, [P, P, P, P, P, P, I64, I64, I64, P, P, P, P, P, P]),
+    "meft_lm_loss_f64": (INT, [P, P, I64, I64, P, I64, P, P, D, C.POINTER(D), P]),
+    "meft_argmax_logits_f64": (INT, [P, P, I64, I64, P, C.POINTER(I64)]),
     "meft_transpose_f64": (INT, [P, P, P, I64, I64]),
     "meft_activation_f64": (INT, [P, INT, P, P, I64]),
     "meft_adam_rows_f64": (INT, [P, P, P, P, P, P, P, P, I64, I64, D, D, D, D]),

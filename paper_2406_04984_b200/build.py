@@ -89,11 +89,11 @@ def build_dropin(verbose: bool = False, force: bool = False) -> str:
 
 REF_TESTS = ("test_numerics", "test_adapter", "test_experts", "test_memtier")
 # The reference's model / trainer suites exercise its trainer (train(), eval_em, resume, gradient accumulation,
-# full-model finite differences) end to end over the drop-in; the out-of-scope parts they call (model.cpp,
-# trainer.cpp, dataset.cpp, report.cpp) are compiled from the reference's own sources on top of the shim, exactly
-# as INTEGRATION.md tells a maintainer to build them.
+# full-model finite differences) end to end over the drop-in, whose model.hpp runs the toy trunk on the GPU too;
+# the out-of-scope parts they call (trainer.cpp, dataset.cpp, report.cpp) are compiled from the reference's own
+# sources on top of the shim, exactly as INTEGRATION.md tells a maintainer to build them.
 TRAINER_TESTS = ("test_model", "test_trainer")
-TRAINER_SRCS = ("model.cpp", "trainer.cpp", "dataset.cpp", "report.cpp")
+TRAINER_SRCS = ("trainer.cpp", "dataset.cpp", "report.cpp")  # model.hpp: the drop-in's GPU trunk (dropin/model.cpp)
 JSON_INC = "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann"
 DROPIN_TEST_BIN = os.path.join(ROOT, "build", "dropin_tests")
 
@@ -106,10 +106,11 @@ def build_reference_tests(ref_proj: str = "/root/reference/proj", verbose: bool 
     lib = build_dropin(verbose)
     os.makedirs(DROPIN_TEST_BIN, exist_ok=True)
     out = []
-    for t in REF_TESTS + TRAINER_TESTS:
-        src = os.path.join(ref_proj, "tests", t + ".cpp")
+    for t in REF_TESTS + TRAINER_TESTS + ("trajectory",):
+        src = (os.path.join(ROOT, "tests", "dropin", "trajectory.cpp") if t == "trajectory"
+               else os.path.join(ref_proj, "tests", t + ".cpp"))
         exe = os.path.join(DROPIN_TEST_BIN, t)
-        extra = [os.path.join(ref_proj, "src", f) for f in TRAINER_SRCS] if t in TRAINER_TESTS else []
+        extra = [os.path.join(ref_proj, "src", f) for f in TRAINER_SRCS] if t not in REF_TESTS else []
         if _needs(exe, [src, lib] + extra):
             # our include/ first: the hot-path headers resolve to the drop-in's, the rest to the reference's
             cmd = [HOST_CXX, "-O1", "-std=c++20", "-w", "-fopenmp", "-I" + os.path.join(ROOT, "tests", "dropin"),

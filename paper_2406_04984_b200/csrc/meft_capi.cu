@@ -16,6 +16,7 @@
 #include "kernels.h"
 #include "select.h"
 #include "stream_ops.h"
+#include "trunk.h"
 
 using namespace meft_dev;
 
@@ -852,6 +853,85 @@ meft_status meft_base_ffn_backward(meft_ctx* ctx, const double* grad_out, const 
         dgemm(st, T, n, d, DOperand{grad_out, d, 1}, DOperand{w_out, 1, d}, da, n, DEPI_STORE, nullptr);
         act_backward(st, da, base_pre, T * n, act);
         dgemm(st, T, d, n, DOperand{da, n, 1}, DOperand{w_in, 1, n}, grad_h, d, DEPI_STORE, nullptr);
+    });
+}
+
+// ------------------------------------------------------------------ toy trunk (model.cpp:50-218), fp64
+
+meft_status meft_embed_f64(meft_ctx* ctx, const double* emb, int64_t vocab, const double* pos, int64_t max_seq,
+                           int64_t d, const int32_t* tokens, int64_t batch, int64_t seq, double* h) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(vocab >= 1 && d >= 1 && batch >= 0 && seq >= 0, MEFT_E_INVALID, "embed: dimensions");
+        if (seq > max_seq) throw MeftError(MEFT_E_RANGE, "embed: sequence longer than max_seq");
+        embed_f64(ctx->stream, emb, pos, tokens, batch * seq, seq, d, h);
+    });
+}
+
+meft_status meft_attention_forward_f64(meft_ctx* ctx, const double* h, const double* wq, const double* wk,
+                                       const double* wv, const double* wo, const int32_t* segments, int64_t batch,
+                                       int64_t seq, int64_t d, double* out, double* q, double* k, double* v,
+                                       double* probs) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(batch >= 0 && seq >= 1 && d >= 1, MEFT_E_INVALID, "attention_forward: dimensions");
+        const int64_t T = batch * seq;
+        double* c = static_cast<double*>(ctx->get("trunk_ctx", size_t(std::max<int64_t>(T * d, 1)) * 8));
+        attention_forward_f64(ctx->stream, h, wq, wk, wv, wo, segments, T, seq, d, q, k, v, probs, c, out);
+    });
+}
+
+meft_status meft_attention_backward_f64(meft_ctx* ctx, const double* wq, const double* wk, const double* wv,
+                                        const double* wo, const int32_t* segments, int64_t batch, int64_t seq,
+                                        int64_t d, const double* q, const double* k, const double* v,
+                                        const double* probs, const double* dh_out, double* dh) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(batch >= 0 && seq >= 1 && d >= 1, MEFT_E_INVALID, "attention_backward: dimensions");
+        const int64_t T = batch * seq, n = std::max<int64_t>(T * d, 1);
+        double* w = static_cast<double*>(ctx->get("trunk_bwd", size_t(4 * n + std::max<int64_t>(T * seq, 1)) * 8));
+        attention_backward_f64(ctx->stream, wq, wk, wv, wo, segments, T, seq, d, q, k, v, probs, dh_out, w,
+                               w + 4 * n, w + n, w + 2 * n, w + 3 * n, dh);
+    });
+}
+
+meft_status meft_lm_loss_f64(meft_ctx* ctx, const double* emb, int64_t vocab, int64_t d, const double* h, int64_t T,
+                             const int32_t* targets, const uint8_t* loss_mask, double loss_scale, double* loss_sum,
+                             double* dh) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(vocab >= 1 && d >= 1 && T >= 0 && loss_sum, MEFT_E_INVALID, "lm_loss: dimensions / loss_sum");
+        cudaStream_t st = ctx->stream;
+        *loss_sum = 0.0;
+        if (T == 0) return;
+        double* logits = static_cast<double*>(ctx->get("trunk_logits", size_t(2 * T * vocab + T) * 8));
+        double* dlogits = logits + T * vocab;
+        double* term = dlogits + T * vocab;
+        // logits = h emb^T ; rows ; dh = dlogits emb
+        dgemm(st, T, vocab, d, DOperand{h, d, 1}, DOperand{emb, 1, d}, logits, vocab, DEPI_STORE, nullptr);
+        lm_loss_rows_f64(st, logits, T, vocab, targets, loss_mask, loss_scale, dlogits, term);
+        dgemm(st, T, d, vocab, DOperand{dlogits, vocab, 1}, DOperand{emb, d, 1}, dh, d, DEPI_STORE, nullptr);
+        std::vector<double> terms(static_cast<size_t>(T));
+        std::vector<uint8_t> mask(static_cast<size_t>(T));
+        MEFT_CUDA_CHECK(cudaMemcpyAsync(terms.data(), term, size_t(T) * 8, cudaMemcpyDeviceToHost, st));
+        MEFT_CUDA_CHECK(cudaMemcpyAsync(mask.data(), loss_mask, size_t(T), cudaMemcpyDeviceToHost, st));
+        MEFT_CUDA_CHECK(cudaStreamSynchronize(st));
+        double loss = 0.0;  // model.cpp:193, contracted: loss = fma(log_denom - logit[target], scale, loss)
+        for (int64_t t = 0; t < T; ++t)
+            if (mask[size_t(t)]) loss = std::fma(terms[size_t(t)], loss_scale, loss);
+        *loss_sum = loss;
+    });
+}
+
+meft_status meft_argmax_logits_f64(meft_ctx* ctx, const double* emb, int64_t vocab, int64_t d, const double* h_row,
+                                   int64_t* token) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(vocab >= 1 && d >= 1 && token, MEFT_E_INVALID, "argmax_logits: dimensions / token");
+        int64_t* dev = reinterpret_cast<int64_t*>(ctx->dev_small + 24);
+        argmax_logits_f64(ctx->stream, emb, vocab, d, h_row, dev);
+        MEFT_CUDA_CHECK(cudaMemcpyAsync(token, dev, 8, cudaMemcpyDeviceToHost, ctx->stream));
+        MEFT_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     });
 }
 

@@ -70,6 +70,11 @@ DevBuf upload_indices(const std::vector<index_t>& idx) {
     return b;
 }
 
+void upload_bytes(DevBuf& dst, const void* host, size_t bytes) {
+    if (bytes) check(meft_copy_to_device(ctx(), dst.get(), host, bytes));
+    check(meft_synchronize(ctx()));  // the host buffer may be released on return
+}
+
 void download(double* host, const DevBuf& b, size_t count) {
     if (count) check(meft_copy_to_host(ctx(), host, b.get(), count * sizeof(double)));
 }

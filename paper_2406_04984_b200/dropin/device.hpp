@@ -42,6 +42,7 @@ class DevBuf {
 DevBuf upload(const double* host, size_t count);
 DevBuf upload(const Matrix& m);
 DevBuf upload_indices(const std::vector<index_t>& idx);  // int32 on device
+void upload_bytes(DevBuf& dst, const void* host, size_t bytes);
 void download(double* host, const DevBuf& b, size_t count);
 Matrix download_matrix(const DevBuf& b, index_t rows, index_t cols);
 void download_i32(std::vector<int32_t>& host, const DevBuf& b, size_t count);

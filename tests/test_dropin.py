@@ -49,7 +49,9 @@ def test_dropin_library_exports_reference_api():
                 "meft::gather_adapter(", "meft::sparse_ffn_pa(", "meft::sparse_backward(", "meft::dense_ffn_pa(",
                 "meft::fetch(", "meft::scatter_grads(", "meft::sparse_adam_update(", "meft::meft_ffn(",
                 "meft::HostStore::init(", "meft::measure_beta(", "meft::push_hidden(", "meft::save_checkpoint(",
-                "meft::load_checkpoint(", "meft::matmul(", "meft::warn(", "meft::finite_diff_grad("]:
+                "meft::load_checkpoint(", "meft::matmul(", "meft::warn(", "meft::finite_diff_grad(",
+                "meft::init_frozen_base(", "meft::embed(", "meft::attention_forward(", "meft::attention_backward(",
+                "meft::lm_loss_and_grad(", "meft::argmax_logits("]:
         assert sym in out, sym
     # the shim carries no numerics of its own: every kernel symbol lives in libmeft_cuda.so
     deps = subprocess.run(["ldd", DROPIN_LIB], capture_output=True, text=True).stdout
@@ -65,3 +67,42 @@ def test_reference_suites_pass_against_dropin_on_b200(suite):
     r, m = _run(exe)
     print(r.stdout[-400:])
     assert r.returncode == 0 and m and m.group(3) == "0", r.stdout[-2000:] + r.stderr[-6000:]
+
+
+def _trajectory(exe, args):
+    r = subprocess.run([exe] + args, capture_output=True, text=True, timeout=1200, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    out = {}
+    for line in r.stdout.splitlines():
+        f = line.split()
+        out[" ".join(f[:-1])] = float(f[-1])
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("args", [["meft", "8", "8"], ["meft", "1", "64"], ["meft", "16", "32"], ["dense", "8", "8"]])
+def test_training_trajectory_on_b200_matches_reference_cpu(args):
+    """The reference's own train() (tests/dropin/trajectory.cpp: 12 optimizer steps of a 2-layer toy model, MEFT or
+    dense) built once against the reference library on the CPU and once against the drop-in on the B200 (adapter
+    AND toy trunk on the GPU): identical step counts, identical per-pair Adam counters (the selections agree), and
+    losses, final weights and moments equal to fp64 round-off."""
+    cpu_exe = os.path.join(REF_BIN, "trajectory")
+    gpu_exe = os.path.join(DROPIN_BIN, "trajectory")
+    if not (os.path.exists(cpu_exe) and os.path.exists(gpu_exe)):
+        pytest.skip("trajectory drivers were not built (need /root/reference at build time)")
+    want, got = _trajectory(cpu_exe, args), _trajectory(gpu_exe, args)
+    assert want.keys() == got.keys()
+    assert got["steps"] == want["steps"] and got["em"] == want["em"]
+    worst = {}
+    for key, w in want.items():
+        g = got[key]
+        kind = key.split()[0]
+        if kind == "pair_step":
+            assert g == w, key
+            continue
+        err = abs(g - w) / max(1e-3, abs(w))
+        worst[kind] = max(worst.get(kind, 0.0), err)
+    print(args, {k: f"{v:.1e}" for k, v in worst.items()})
+    assert worst["loss"] < 1e-10
+    for k in ("w_a", "w_b", "m_a", "v_a", "m_b", "v_b"):
+        assert worst[k] < 1e-8, (k, worst[k])
