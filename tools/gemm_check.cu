@@ -343,6 +343,19 @@ int main(int argc, char** argv) {
         perf_case("gW=act^T.g (MN,MN)", S, D, T, true, true, EPI_STORE_F32);
         return 0;
     }
+    if (argc > 1 && std::strcmp(argv[1], "perfmaj") == 0) {  // the out / grad_h shape with every operand major
+        const int T = 8192, S = 65536, D = 4096;
+        for (int rep = 0; rep < 2; ++rep) {
+            perf_case("out-shape (K,K)", T, D, S, false, false, EPI_STORE_F32);
+            perf_case("out-shape (K,MN)", T, D, S, false, true, EPI_STORE_F32);
+            perf_case("out-shape (MN,K)", T, D, S, true, false, EPI_STORE_F32);
+            perf_case("out-shape (MN,MN)", T, D, S, true, true, EPI_STORE_F32);
+            perf_case("z-shape (K,K)", T, S, D, false, false, EPI_STORE_F32);
+            perf_case("gW-shape (MN,MN)", S, D, T, true, true, EPI_STORE_F32);
+            perf_case("gW-shape (K,K)", S, D, T, false, false, EPI_STORE_F32);
+        }
+        return 0;
+    }
     if (argc > 1 && std::strcmp(argv[1], "perfg") == 0) {
         const int T = 8192, S = 65536, D = 4096;
         perf_case("z dense", T, S, D, false, false, EPI_RELU_BF16);
