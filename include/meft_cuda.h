@@ -211,6 +211,28 @@ meft_status meft_base_ffn_backward(meft_ctx* ctx, const double* grad_out, const 
                                    const double* w_in, const double* w_out, int64_t T, int64_t d, int64_t n, int act,
                                    double* grad_h);
 
+/* ---- Bookkeeping of the expert-sharded selection protocol (paper_2406_04984_b200/sharded.py) on the
+ * device: deterministic stable bucketing instead of host-driven index manipulation between the exchanges.
+ * world <= 64. Host-side count arrays are written after a stream synchronisation. */
+/* Dispatch plan: row i = t*kk + s of tau goes to owner tau[i] / n_loc (experts per rank), rows bucketed by owner in
+ * ascending i. send_rows [T*kk x d] bf16 (= h[t]), send_exp (owner-local expert), order[p] = i, inv[i] = p,
+ * counts[world] (host): rows per owner. */
+meft_status meft_shard_dispatch(meft_ctx* ctx, const int32_t* tau, int64_t T, int64_t kk, int64_t n_loc, int world,
+                                const uint16_t* h, int64_t d, uint16_t* send_rows, int32_t* send_exp, int32_t* order,
+                                int32_t* inv, int64_t* counts);
+/* dst[order[p]] = src[p] for n rows of `cols` fp32 (candidate scores back into (token, slot) order) */
+meft_status meft_shard_unpermute_rows(meft_ctx* ctx, const float* src, const int32_t* order, int64_t n, int64_t cols,
+                                      float* dst);
+/* Exact re-scoring requests for the ambiguous candidates amb [T x C] (n_amb per token): key idx goes to owner
+ * idx / M_loc as (receive row inv[t*kk + slot(idx)] + row_base[owner], local key idx - owner*M_loc), bucketed by owner
+ * in (token, position) order; back[q] = t*C + a says where the answer goes. counts[world] and *total on the host. */
+meft_status meft_shard_requests(meft_ctx* ctx, const int32_t* amb, const int32_t* n_amb, const int32_t* tau,
+                                const int32_t* inv, int64_t T, int64_t C, int64_t kk, int64_t E, int64_t M_loc,
+                                int world, const int64_t* row_base, int32_t* row, int32_t* key, int32_t* back,
+                                int64_t* counts, int64_t* total);
+/* dst[back[i]] = x[i] */
+meft_status meft_shard_scatter_f64(meft_ctx* ctx, const double* x, const int32_t* back, int64_t n, double* dst);
+
 /* ---- The reference's frozen toy trunk (model.cpp:50-218), fp64 on the device: what the drop-in's model.hpp
  * functions call so that the reference trainer runs end to end on the B200. Arrays are device buffers (row-major,
  * T = batch * seq rows); reductions follow the reference's order (deterministic). Ids must be in range: the drop-in

@@ -16,6 +16,7 @@
 #include "kernels.h"
 #include "select.h"
 #include "stream_ops.h"
+#include "shard_plan.h"
 #include "trunk.h"
 
 using namespace meft_dev;
@@ -33,7 +34,7 @@ struct meft_ctx {
     cudaEvent_t ev_in = nullptr, ev_fwd = nullptr, ev_out = nullptr;
     std::string err;
     int64_t err_index = -1;
-    int32_t* dev_small = nullptr;   // 64 device ints (validation flags, counts)
+    int32_t* dev_small = nullptr;   // 128 device ints (validation flags, counts; [32, 96): sharded plan counts)
     int32_t* host_small = nullptr;  // 64 pinned ints
     struct Buf {
         void* p = nullptr;
@@ -580,7 +581,7 @@ meft_status meft_ctx_create(int device, void* stream, meft_ctx** out) {
         MEFT_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
         MEFT_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_fwd, cudaEventDisableTiming));
         MEFT_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
-        MEFT_CUDA_CHECK(cudaMalloc(&c->dev_small, 64 * sizeof(int32_t)));
+        MEFT_CUDA_CHECK(cudaMalloc(&c->dev_small, 128 * sizeof(int32_t)));
         MEFT_CUDA_CHECK(cudaMallocHost(&c->host_small, 64 * sizeof(int32_t)));
     });
     if (st != MEFT_OK) return st;
@@ -853,6 +854,71 @@ meft_status meft_base_ffn_backward(meft_ctx* ctx, const double* grad_out, const 
         dgemm(st, T, n, d, DOperand{grad_out, d, 1}, DOperand{w_out, 1, d}, da, n, DEPI_STORE, nullptr);
         act_backward(st, da, base_pre, T * n, act);
         dgemm(st, T, d, n, DOperand{da, n, 1}, DOperand{w_in, 1, n}, grad_h, d, DEPI_STORE, nullptr);
+    });
+}
+
+// ------------------------------------------------------------------ sharded-selection bookkeeping
+
+static void copy_counts(meft_ctx* ctx, const int32_t* dev, int world, int64_t* host) {
+    std::vector<int32_t> tmp(static_cast<size_t>(world));
+    MEFT_CUDA_CHECK(cudaMemcpyAsync(tmp.data(), dev, size_t(world) * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    MEFT_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    for (int r = 0; r < world; ++r) host[r] = tmp[size_t(r)];
+}
+
+meft_status meft_shard_dispatch(meft_ctx* ctx, const int32_t* tau, int64_t T, int64_t kk, int64_t n_loc, int world,
+                                const uint16_t* h, int64_t d, uint16_t* send_rows, int32_t* send_exp, int32_t* order,
+                                int32_t* inv, int64_t* counts) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(world >= 1 && world <= 64 && n_loc >= 1 && kk >= 1 && T >= 0 && d % 8 == 0 && counts, MEFT_E_INVALID,
+                "shard_dispatch: 1 <= world <= 64, n_loc >= 1, d % 8 == 0");
+        int32_t* pos = static_cast<int32_t*>(ctx->get("shard_pos", size_t(std::max<int64_t>(T * kk, 1)) * 4));
+        int32_t* cnt = ctx->dev_small + 32;
+        MEFT_CUDA_CHECK(cudaMemsetAsync(cnt, 0, size_t(world) * 4, ctx->stream));
+        shard_dispatch(ctx->stream, tau, T, kk, n_loc, world, h, d, pos, send_rows, send_exp, order, inv, cnt);
+        copy_counts(ctx, cnt, world, counts);
+    });
+}
+
+meft_status meft_shard_unpermute_rows(meft_ctx* ctx, const float* src, const int32_t* order, int64_t n, int64_t cols,
+                                      float* dst) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        shard_unpermute_rows(ctx->stream, src, order, n, cols, dst);
+    });
+}
+
+meft_status meft_shard_requests(meft_ctx* ctx, const int32_t* amb, const int32_t* n_amb, const int32_t* tau,
+                                const int32_t* inv, int64_t T, int64_t C, int64_t kk, int64_t E, int64_t M_loc,
+                                int world, const int64_t* row_base, int32_t* row, int32_t* key, int32_t* back,
+                                int64_t* counts, int64_t* total) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(world >= 1 && world <= 64 && E >= 1 && M_loc >= 1 && counts && total && row_base, MEFT_E_INVALID,
+                "shard_requests: arguments");
+        cudaStream_t st = ctx->stream;
+        int32_t* ws = static_cast<int32_t*>(ctx->get("shard_req", shard_requests_ws_ints(T, C) * 4 + 256));
+        int32_t* rb = ctx->dev_small + 32;
+        std::vector<int32_t> base(static_cast<size_t>(world));
+        for (int r = 0; r < world; ++r) base[size_t(r)] = int32_t(row_base[r]);
+        MEFT_CUDA_CHECK(cudaMemcpyAsync(rb, base.data(), size_t(world) * 4, cudaMemcpyHostToDevice, st));
+        shard_requests_fill(st, amb, n_amb, tau, inv, T, C, kk, E, M_loc, rb, ws);
+        int32_t n = 0;
+        MEFT_CUDA_CHECK(cudaMemcpyAsync(&n, ws + T, 4, cudaMemcpyDeviceToHost, st));
+        MEFT_CUDA_CHECK(cudaStreamSynchronize(st));
+        *total = n;
+        int32_t* cnt = ctx->dev_small + 32;
+        MEFT_CUDA_CHECK(cudaMemsetAsync(cnt, 0, size_t(world) * 4, st));
+        shard_requests_sort(st, T, C, M_loc, world, n, ws, row, key, back, cnt);
+        copy_counts(ctx, cnt, world, counts);
+    });
+}
+
+meft_status meft_shard_scatter_f64(meft_ctx* ctx, const double* x, const int32_t* back, int64_t n, double* dst) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        shard_scatter_f64(ctx->stream, x, back, n, dst);
     });
 }
 

@@ -41,6 +41,54 @@ def _p(t):
     return None if t is None else C.c_void_p(t.data_ptr())
 
 
+class TorchGlue:
+    """The protocol's index bookkeeping as framework ops -- the reference semantics of the device plan kernels
+    (csrc/shard_plan.cu), used by engines without them (the CPU test engine). All orders are stable."""
+
+    def dispatch(self, tau, h, n_loc, P):
+        """(token, slot) rows bucketed by expert owner: send rows / owner-local experts in bucket order, order[p] =
+        flat (t*kk + s) index, inv = its inverse, rows per owner."""
+        kk = tau.shape[1]
+        flat = tau.reshape(-1).long()
+        owner = flat // n_loc
+        order = torch.argsort(owner, stable=True)
+        inv = torch.empty_like(order)
+        inv[order] = torch.arange(order.numel(), device=order.device)
+        counts = torch.bincount(owner, minlength=P).tolist()
+        send_exp = (flat[order] - owner[order] * n_loc).to(torch.int32)
+        return h[order // kk], send_exp, order.to(torch.int32), inv.to(torch.int32), counts
+
+    def unpermute(self, src, order):
+        out = torch.empty_like(src)
+        out[order.long()] = src
+        return out
+
+    def requests(self, amb, n_amb, tau, inv, E, M_loc, P, row_base):
+        """Exact re-scoring requests of the ambiguous candidates, bucketed by key owner in (token, position) order:
+        (owner receive row, owner-local key, back index t*C + a, requests per owner, total)."""
+        T, C = amb.shape
+        kk = tau.shape[1]
+        dev = amb.device
+        na = n_amb.long()
+        n = int(na.sum().item())
+        tok = torch.repeat_interleave(torch.arange(T, device=dev), na)
+        pos = torch.arange(n, device=dev) - torch.repeat_interleave(torch.cumsum(na, 0) - na, na)
+        gidx = amb[tok, pos].long()
+        slot = (tau[tok].long() == (gidx // E)[:, None]).int().argmax(1)
+        owner = gidx // M_loc
+        row = inv[tok * kk + slot].long() + torch.tensor(row_base, device=dev)[owner]
+        key = gidx - owner * M_loc
+        order = torch.argsort(owner, stable=True)
+        counts = torch.bincount(owner, minlength=P).tolist()
+        return (row[order].to(torch.int32), key[order].to(torch.int32), (tok * C + pos)[order].to(torch.int32),
+                counts, n)
+
+    def scatter_exact(self, x, back, T, C):
+        xs = torch.zeros(T * C, dtype=torch.float64, device=x.device)
+        xs[back.long()] = x
+        return xs.view(T, C)
+
+
 class DeviceEngine:
     """Per-rank compute on one B200 through the C ABI (the store holds this rank's expert shard)."""
 
@@ -50,6 +98,48 @@ class DeviceEngine:
 
     def _check(self, st):
         self.ctx.check(st)
+
+    # ---- protocol bookkeeping on the device (csrc/shard_plan.cu; semantics: TorchGlue)
+    def dispatch(self, tau, h, n_loc, P):
+        T, kk = tau.shape
+        d = h.shape[1]
+        n = T * kk
+        send_rows = torch.empty((n, d), dtype=h.dtype, device=self.dev)
+        send_exp = torch.empty(n, dtype=torch.int32, device=self.dev)
+        order = torch.empty(n, dtype=torch.int32, device=self.dev)
+        inv = torch.empty(n, dtype=torch.int32, device=self.dev)
+        counts = (C.c_int64 * P)()
+        self._check(lib().meft_shard_dispatch(self.ctx.h, _p(tau), T, kk, n_loc, P, _p(h), d, _p(send_rows),
+                                              _p(send_exp), _p(order), _p(inv), counts))
+        return send_rows, send_exp, order, inv, list(counts)
+
+    def unpermute(self, src, order):
+        out = torch.empty_like(src)
+        n = src.shape[0]
+        self._check(lib().meft_shard_unpermute_rows(self.ctx.h, _p(src), _p(order), n, src.numel() // max(n, 1),
+                                                    _p(out)))
+        return out
+
+    def requests(self, amb, n_amb, tau, inv, E, M_loc, P, row_base):
+        T, Cc = amb.shape
+        kk = tau.shape[1]
+        cap = max(1, T * Cc)
+        row = torch.empty(cap, dtype=torch.int32, device=self.dev)
+        key = torch.empty(cap, dtype=torch.int32, device=self.dev)
+        back = torch.empty(cap, dtype=torch.int32, device=self.dev)
+        counts = (C.c_int64 * P)()
+        total = C.c_int64()
+        base = (C.c_int64 * P)(*row_base)
+        self._check(lib().meft_shard_requests(self.ctx.h, _p(amb), _p(n_amb), _p(tau), _p(inv), T, Cc, kk, E, M_loc,
+                                              P, base, _p(row), _p(key), _p(back), counts, C.byref(total)))
+        n = total.value
+        return row[:n], key[:n], back[:n], list(counts), n
+
+    def scatter_exact(self, x, back, T, Cc):
+        xs = torch.zeros((T, Cc), dtype=torch.float64, device=self.dev)
+        if back.numel():
+            self._check(lib().meft_shard_scatter_f64(self.ctx.h, _p(x), _p(back), back.numel(), _p(xs)))
+        return xs
 
     def route(self, h, kk):
         T, d = h.shape
@@ -270,13 +360,23 @@ def _a2a(tensor, send_counts, recv_counts, group):
     return out
 
 
-def _exchange_counts(counts, group):
+def _gather_counts(counts, group, host_group=None):
+    """Every rank's per-destination counts: matrix[src][dst] (lists), one collective. The counts already live on
+    the host, so with `host_group` (a gloo group over the same ranks) they never touch the GPU."""
+    world = _world(group)
+    if host_group is not None:
+        send = torch.tensor(counts, dtype=torch.int64)
+        parts = [torch.empty_like(send) for _ in range(world)]
+        dist.all_gather(parts, send, group=host_group)
+        return torch.stack(parts).tolist()
     send = torch.tensor(counts, dtype=torch.int64, device=_comm_device(group))
     if isinstance(group, ThreadGroup):
-        return group.all_to_all(send, [1] * group.world, [1] * group.world).tolist()
-    recv = torch.empty_like(send)
-    dist.all_to_all_single(recv, send, group=group)
-    return recv.tolist()
+        full = group.all_gather(send.view(1, -1))
+    else:
+        parts = [torch.empty_like(send) for _ in range(world)]
+        dist.all_gather(parts, send, group=group)
+        full = torch.stack(parts)
+    return full.view(world, len(counts)).tolist()
 
 
 def _comm_device(group):
@@ -318,6 +418,11 @@ class ShardedLayer:
             raise ValueError("N must be divisible by the world size and M by N")
         self.E, self.N_loc, self.M_loc = M // N, N // self.world, M // self.world
         self.last = {}
+        # protocol metadata (per-destination counts) is exchanged host to host over gloo when the data plane is NCCL
+        self.host_group = None
+        if not isinstance(group, ThreadGroup) and dist.get_backend(group) == "nccl":
+            ranks = list(range(self.world)) if group is None else dist.get_process_group_ranks(group)
+            self.host_group = dist.new_group(ranks=ranks, backend="gloo")
         # Overlap (device engine over NCCL): the bulk all-gathers / reduce-scatters run on their own stream and
         # communicator, so they proceed while the selection exchanges and the FFN compute.
         self.overlap = (isinstance(engine, DeviceEngine) and not isinstance(group, ThreadGroup)
@@ -392,58 +497,34 @@ class ShardedLayer:
             g.record_stream(cs)
         # 1. route (exact tau, ascending per token)
         tau = eng.route(h, kk)
-        # 2. dispatch (token, slot) rows to their expert owners
-        flat_e = tau.reshape(-1).long()
-        owner = flat_e // self.N_loc
-        order = torch.argsort(owner, stable=True)
-        send_counts = torch.bincount(owner, minlength=P).tolist()
-        recv_counts = _exchange_counts(send_counts, grp)
-        send_rows = h[order // kk_eff]
-        send_exp = (flat_e[order] - owner[order] * self.N_loc).to(torch.int32)
+        # 2. dispatch (token, slot) rows to their expert owners (stable bucket plan on the device)
+        send_rows, send_exp, order, inv, send_counts = eng.dispatch(tau, h, self.N_loc, P)
+        cmat = _gather_counts(send_counts, grp, self.host_group)  # cmat[src][dst]: rows src dispatches to dst
+        recv_counts = [cmat[s][r] for s in range(P)]
         recv_rows = _a2a(send_rows, send_counts, recv_counts, grp)
         recv_exp = _a2a(send_exp, send_counts, recv_counts, grp)
         # 3-4. owners score; candidate blocks come back in dispatch order
         cand_recv = eng.score(recv_rows, recv_exp)
         cand_back = _a2a(cand_recv, recv_counts, send_counts, grp)
-        cand = torch.empty((T * kk_eff, E), dtype=torch.float32, device=h.device)
-        cand[order] = cand_back
-        cand = cand.view(T, kk_eff * E)
+        cand = eng.unpermute(cand_back, order).view(T, kk_eff * E)
         hn, _ = eng.row_stats(h)
         kn_loc, _ = eng.key_stats()
         kn = _all_gather_rows(kn_loc, grp, P)
         # 5. certified classification at the token home
         sure, n_sure, amb, n_amb = eng.classify(cand, tau, hn, kn, take, d)
-        # 6. exact re-scoring of the ambiguous candidates by their owners
+        # 6. exact re-scoring of the ambiguous candidates by their owners: a request names the owner's receive row
+        # of the token's dispatched row (our block starts after the rows of lower source ranks) and the local key
         Ccand = kk_eff * E
-        na = n_amb.long()
-        tok = torch.repeat_interleave(torch.arange(T, device=h.device), na)
-        n_resc = int(na.sum().item())  # (host sync of the selection phase; never after the FFN is enqueued)
-        pos = torch.arange(n_resc, device=h.device) - torch.repeat_interleave(torch.cumsum(na, 0) - na, na)
-        gidx = amb[tok, pos].long()
-        e_glob = gidx // E
-        slot = (tau[tok].long() == e_glob[:, None]).int().argmax(1)  # position of the expert in tau
-        q = torch.empty_like(order)
-        q[order] = torch.arange(order.numel(), device=h.device)
-        dispatch_pos = q[tok * kk_eff + slot]                      # position in the send order
-        a_owner = gidx // self.M_loc
-        send_off = torch.cumsum(torch.tensor([0] + send_counts[:-1], device=h.device), 0)
-        req_row = (dispatch_pos - send_off[a_owner]).to(torch.int32)  # row index in the owner's recv buffer
-        req_key = (gidx - a_owner * self.M_loc).to(torch.int32)
-        rorder = torch.argsort(a_owner, stable=True)
-        rsend = torch.bincount(a_owner, minlength=P).tolist()
-        rrecv = _exchange_counts(rsend, grp)
-        in_row = _a2a(req_row[rorder], rsend, rrecv, grp)
-        in_key = _a2a(req_key[rorder], rsend, rrecv, grp)
-        # requests arrive grouped by source rank; their rows sit after the rows the earlier sources dispatched
-        src = torch.repeat_interleave(torch.arange(P, device=h.device), torch.tensor(rrecv, device=h.device))
-        recv_off = torch.cumsum(torch.tensor([0] + recv_counts[:-1], device=h.device), 0)
-        in_row = (in_row.long() + recv_off[src]).to(torch.int32)
+        send_off = [sum(send_counts[:o]) for o in range(P)]
+        row_base = [sum(cmat[s][o] for s in range(r)) - send_off[o] for o in range(P)]
+        req_row, req_key, back, rsend, n_resc = eng.requests(amb, n_amb, tau, inv, E, self.M_loc, P, row_base)
+        rmat = _gather_counts(rsend, grp, self.host_group)
+        rrecv = [rmat[s][r] for s in range(P)]
+        reqs = _a2a(torch.stack([req_row, req_key], 1), rsend, rrecv, grp)  # (receive row, local key) pairs
+        in_row, in_key = reqs[:, 0].contiguous(), reqs[:, 1].contiguous()
         x_out = eng.exact(recv_rows, in_row, in_key)
         x_back = _a2a(x_out, rrecv, rsend, grp)
-        xs = torch.zeros((T, Ccand), dtype=torch.float64, device=h.device)
-        x_sorted = torch.empty_like(x_back)
-        x_sorted[rorder] = x_back
-        xs[tok, pos] = x_sorted
+        xs = eng.scatter_exact(x_back, back, T, Ccand)
         # 7. final per-token selection and the global union
         per_token, flags = eng.finalize(sure, n_sure, amb, n_amb, xs, take, self.M)
         union = flags.to(torch.int32)

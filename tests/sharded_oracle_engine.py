@@ -6,10 +6,10 @@ import numpy as np
 import torch
 
 from oracle import oracle as O
-from paper_2406_04984_b200.sharded import cert_bound_coeff
+from paper_2406_04984_b200.sharded import TorchGlue, cert_bound_coeff
 
 
-class OracleEngine:
+class OracleEngine(TorchGlue):
     def __init__(self, w_a, w_b, w_g, rank, world):
         d, M = w_a.shape
         self.d, self.M, self.N = d, M, w_g.shape[0]

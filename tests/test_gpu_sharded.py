@@ -150,3 +150,41 @@ def test_sharded_device_path_multirank_emulated(ctx, P):
         assert float((res["grad_h"] - gh[rows]).norm() / gh[rows].norm()) < 1e-5
         for n_, t_ in tabs.items():
             assert torch.equal(t_, ref.tensor(0, n_)[r * M_loc:(r + 1) * M_loc]), (r, n_)
+
+
+@pytest.mark.parametrize("P", [1, 2, 8])
+def test_device_protocol_plans_equal_reference_glue(ctx, P):
+    """The device bookkeeping kernels of the sharded protocol (csrc/shard_plan.cu) produce exactly the arrays of
+    the framework-op statement (sharded.TorchGlue): dispatch bucket order / inverse / counts / rows, the request
+    plan (receive rows, local keys, back indices, counts) and both scatters."""
+    from paper_2406_04984_b200 import meft as G
+    T, kk, N, E, d = 300, 4, 32, 16, 64
+    M = N * E
+    gen = torch.Generator(device="cuda").manual_seed(P)
+    tau = torch.stack([torch.randperm(N, generator=gen, device="cuda")[:kk] for _ in range(T)]).sort(1).values
+    tau = tau.to(torch.int32).contiguous()
+    h = torch.randn((T, d), generator=gen, device="cuda").to(torch.bfloat16)
+    st = G.Store(ctx, 1, d, M // P, N // P, G.STORE_MIXED)
+    eng = SH.DeviceEngine(ctx, st, torch.zeros((N, d), dtype=torch.bfloat16, device="cuda"))
+    ref = SH.TorchGlue()
+    a = eng.dispatch(tau, h, N // P, P)
+    b = ref.dispatch(tau, h, N // P, P)
+    for x, y in zip(a[:4], b[:4]):
+        assert torch.equal(x, y)
+    assert a[4] == b[4]
+    src = torch.randn((T * kk, E), generator=gen, device="cuda")
+    assert torch.equal(eng.unpermute(src, a[2]), ref.unpermute(src, b[2]))
+    C = kk * E
+    n_amb = torch.randint(0, 9, (T,), generator=gen, device="cuda", dtype=torch.int32)
+    amb = torch.zeros((T, C), dtype=torch.int32, device="cuda")
+    for t in range(T):  # ambiguous keys drawn from the token's own experts
+        e = tau[t, torch.randint(0, kk, (C,), generator=gen, device="cuda")].long()
+        amb[t] = (e * E + torch.randint(0, E, (C,), generator=gen, device="cuda")).to(torch.int32)
+    row_base = [int(v) for v in torch.randint(0, 50, (P,), generator=torch.Generator().manual_seed(P)).tolist()]
+    ra = eng.requests(amb, n_amb, tau, a[3], E, M // P, P, row_base)
+    rb = ref.requests(amb, n_amb, tau, b[3], E, M // P, P, row_base)
+    for x, y in zip(ra[:3], rb[:3]):
+        assert torch.equal(x, y)
+    assert ra[3] == rb[3] and ra[4] == rb[4]
+    x = torch.randn(ra[4], generator=gen, device="cuda", dtype=torch.float64)
+    assert torch.equal(eng.scatter_exact(x, ra[2], T, C), ref.scatter_exact(x, rb[2], T, C))
