@@ -162,6 +162,8 @@ def lib():
             raise ImportError(f"{LIB_PATH} is not built; run __graft_entry__.build() (no CPU fallback exists)")
         L = C.CDLL(LIB_PATH)
         for name, (res, args) in _SIGS.items():
+            if os.environ.get("MEFT_LIB") and not hasattr(L, name):
+                continue  # an older A/B build (MEFT_LIB) may predate some entry points
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args

@@ -255,24 +255,6 @@ __device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const CUtensorM
 // land as 4 consecutive 128-B smem rows; the 128B swizzle follows the smem address, so four-row pieces compose
 // into the usual SW128 operand tile. Out-of-range rows are zero-filled and still count their bytes.
 // (Semantics measured by tools/gather4_probe.cu.)
-// L2 eviction-priority policies for TMA loads (hint: 1 evict_first, 2 evict_last; 0 = none).
-__device__ __forceinline__ uint64_t l2_policy(int hint) {
-    uint64_t p = 0;
-    if (hint == 1)
-        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    else if (hint == 2)
-        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ void tma_load_2d_pair_hint(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
-                                                      int32_t c1, uint64_t policy) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "l"(policy)
-        : "memory");
-}
-
 __device__ __forceinline__ void tma_gather4(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
                                             int32_t r0, int32_t r1, int32_t r2, int32_t r3) {
     asm volatile(

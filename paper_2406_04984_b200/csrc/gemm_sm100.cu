@@ -53,8 +53,6 @@ struct KArgs {
     const int32_t* g_tile_off;
     // pair-kernel raster: m-tiles per group (tiles_m = sweep all of M first); n_fast = sweep N first
     int raster_group, raster_n_fast;
-    // pair kernel: L2 eviction priority of the A / B operand loads (l2_policy: 0 none, 1 first, 2 last)
-    int hint_a, hint_b;
     // K split: tile index = split * base_tiles + base tile; split s runs k-blocks [s*kb_split, (s+1)*kb_split)
     int ksplit, kb_split;
     long long split_stride;
@@ -244,7 +242,7 @@ __device__ __forceinline__ void epilogue_chunk(const KArgs& a, int m, int n, con
                 uint32_t w = 0;
 #pragma unroll
                 for (int j = 0; j < 32; ++j) w |= (j < cnt && __uint_as_float(r[j]) > 0.0f) ? (1u << j) : 0u;
-                __stcs(a.bits + (long long)m * a.ldbits + (n >> 5), w);
+                a.bits[(long long)m * a.ldbits + (n >> 5)] = w;
             }
             if (cnt == 32) {
                 uint4* c4 = reinterpret_cast<uint4*>(c);
@@ -259,7 +257,7 @@ __device__ __forceinline__ void epilogue_chunk(const KArgs& a, int m, int n, con
                                       relu_bf16_bits(__uint_as_float(r[8 * j + 5])));
                     v.w = pack_bf16x2(relu_bf16_bits(__uint_as_float(r[8 * j + 6])),
                                       relu_bf16_bits(__uint_as_float(r[8 * j + 7])));
-                    __stcs(c4 + j, v);  // streamed: read back by the next GEMM long after L2 has turned over
+                    c4[j] = v;
                 }
             } else {
                 for (int j = 0; j < cnt; ++j) c[j] = relu_bf16_bits(__uint_as_float(r[j]));
@@ -269,7 +267,7 @@ __device__ __forceinline__ void epilogue_chunk(const KArgs& a, int m, int n, con
         case EPI_MASK_BF16: {
             uint16_t* c = reinterpret_cast<uint16_t*>(a.c) + (long long)m * a.ldc + n;
             if (a.bits) {  // bitmask of act > 0 (written by the z GEMM's EPI_RELU_BF16)
-                const uint32_t w = __ldcs(a.bits + (long long)m * a.ldbits + (n >> 5));
+                const uint32_t w = a.bits[(long long)m * a.ldbits + (n >> 5)];
                 if (cnt == 32) {
                     uint4* c4 = reinterpret_cast<uint4*>(c);
 #pragma unroll
@@ -282,7 +280,7 @@ __device__ __forceinline__ void epilogue_chunk(const KArgs& a, int m, int n, con
                             const uint16_t hi = (w >> (e + 1)) & 1u ? f32_to_bf16_bits(__uint_as_float(r[e + 1])) : 0;
                             o[q] = pack_bf16x2(lo, hi);
                         }
-                        __stcs(c4 + j, make_uint4(o[0], o[1], o[2], o[3]));
+                        c4[j] = make_uint4(o[0], o[1], o[2], o[3]);
                     }
                 } else {
                     for (int j = 0; j < cnt; ++j) c[j] = (w >> j) & 1u ? f32_to_bf16_bits(__uint_as_float(r[j])) : 0;
@@ -295,7 +293,7 @@ __device__ __forceinline__ void epilogue_chunk(const KArgs& a, int m, int n, con
                 const uint4* m4 = reinterpret_cast<const uint4*>(mk);
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    const uint4 mm = __ldcs(m4 + j);
+                    const uint4 mm = m4[j];
                     const uint32_t mw[4] = {mm.x, mm.y, mm.z, mm.w};
                     uint32_t o[4];
 #pragma unroll
@@ -304,7 +302,7 @@ __device__ __forceinline__ void epilogue_chunk(const KArgs& a, int m, int n, con
                         const uint16_t hi = (mw[q] >> 16) ? f32_to_bf16_bits(__uint_as_float(r[8 * j + 2 * q + 1])) : 0;
                         o[q] = pack_bf16x2(lo, hi);
                     }
-                    __stcs(c4 + j, make_uint4(o[0], o[1], o[2], o[3]));
+                    c4[j] = make_uint4(o[0], o[1], o[2], o[3]);
                 }
             } else {
                 for (int j = 0; j < cnt; ++j) c[j] = mk[j] ? f32_to_bf16_bits(__uint_as_float(r[j])) : 0;
@@ -813,15 +811,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             return nb_ * BN + int(rank) * 128;
         };
         if (gather && !B_MN && pair < num_tiles) load_nrows<1>(args, tile_n0(pair), lane, gn);
-        const uint64_t pol_a = l2_policy(args.hint_a), pol_b = l2_policy(args.hint_b);
-        auto load_a = [&](void* dst, uint64_t* bar, int c0, int c1) {
-            if (args.hint_a) tma_load_2d_pair_hint(dst, &tmA, bar, c0, c1, pol_a);
-            else tma_load_2d_pair(dst, &tmA, bar, c0, c1);
-        };
-        auto load_b = [&](void* dst, uint64_t* bar, int c0, int c1) {
-            if (args.hint_b) tma_load_2d_pair_hint(dst, &tmB, bar, c0, c1, pol_b);
-            else tma_load_2d_pair(dst, &tmB, bar, c0, c1);
-        };
         for (int tile = pair; tile < num_tiles; tile += npairs) {
             int mb, nb;
             tile_coords_pair(tile, args, mb, nb);
@@ -845,18 +834,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                     mbar_wait(empty + stage, phase ^ 1);
                     if (leader) mbar_arrive_expect_tx(full + stage, 2 * P_STAGE_BYTES);
                     if (!A_MN) {
-                        load_a(sa, full + stage, k0, m0);
+                        tma_load_2d_pair(sa, &tmA, full + stage, k0, m0);
                     } else {
 #pragma unroll
-                        for (int j = 0; j < 2; ++j) load_a(sa + j * 8192, full + stage, m0 + 64 * j, k0);
+                        for (int j = 0; j < 2; ++j)
+                            tma_load_2d_pair(sa + j * 8192, &tmA, full + stage, m0 + 64 * j, k0);
                     }
                     if (!gather || run >= 0) {  // plain box (gathered B: at the run's table row)
                         const int brow = gather ? run : (B_MN ? k0 : n0);
                         if (!B_MN) {
-                            load_b(sb, full + stage, k0, brow);
+                            tma_load_2d_pair(sb, &tmB, full + stage, k0, brow);
                         } else {
 #pragma unroll
-                            for (int j = 0; j < 2; ++j) load_b(sb + j * 8192, full + stage, n0 + 64 * j, brow);
+                            for (int j = 0; j < 2; ++j)
+                                tma_load_2d_pair(sb + j * 8192, &tmB, full + stage, n0 + 64 * j, brow);
                         }
                     }
                 }
@@ -1184,27 +1175,6 @@ void gemm_bf16_one(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmO
         }();
         args.raster_group = forced ? forced : (!A.mn_major && !B.mn_major ? 16 : 8);
         if (A.mn_major && forced_amn) args.raster_group = forced_amn;
-        // L2 residency (K-major x K-major, i.e. z / masked: h against the key or value table): the small operand
-        // every output tile re-reads is loaded evict_last, the streamed table evict_first (measured: masked GEMM
-        // 3.33 -> 3.18 ms, DRAM reads 6.3 -> 5.4 GB; step -1.5%). Hinting the MN-major grad-W GEMMs the same way
-        // made them re-read more (their big operand's panels are shared by the wave's concurrent N-tiles), so they
-        // stay unhinted (MEFT_GEMM_L2HINT=2 hints their small operand evict_last; 0 disables all hints).
-        static const int hints = [] {
-            const char* v = std::getenv("MEFT_GEMM_L2HINT");
-            return v ? std::atoi(v) : 1;
-        }();
-        const int64_t a_bytes = M * K * 2, b_bytes = (B.rows ? std::min<int64_t>(B.table_rows, N) : N) * K * 2;
-        constexpr int64_t kResident = 72ll << 20;
-        args.hint_a = args.hint_b = 0;
-        if (hints && std::min(a_bytes, b_bytes) <= kResident && std::max(a_bytes, b_bytes) > 4 * kResident) {
-            const bool a_small = a_bytes <= b_bytes;
-            if (!A.mn_major && !B.mn_major) {
-                args.hint_a = a_small ? 2 : 1;
-                args.hint_b = a_small ? 1 : 2;
-            } else if (hints >= 2) {
-                (a_small ? args.hint_a : args.hint_b) = 2;
-            }
-        }
         launch_pair_dispatch(st, A.mn_major, B.mn_major, ta, tb, B.rows ? tg : tb, args, int(pair_tiles));
         return;
     }
