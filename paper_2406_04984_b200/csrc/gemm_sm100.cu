@@ -402,6 +402,16 @@ __device__ __forceinline__ float4 ld_shared_f4(uint32_t addr) {
                  : "memory");
     return v;
 }
+#ifndef MEFT_ADAM_STREAMING
+#define MEFT_ADAM_STREAMING 1
+#endif
+#if MEFT_ADAM_STREAMING  // the tables are touched once per step: evict-first loads and stores
+#define ADAM_LD(p) __ldcs(p)
+#define ADAM_ST(p, v) __stcs(p, v)
+#else
+#define ADAM_LD(p) (*(p))
+#define ADAM_ST(p, v) (*(p) = (v))
+#endif
 constexpr int ADAM_SCRATCH_LD = 36;  // floats per scratch row (16-byte aligned, conflict-free quarter-warp phases)
 constexpr int ADAM_SCRATCH_BYTES = 4 * 32 * ADAM_SCRATCH_LD * 4;
 
@@ -437,9 +447,9 @@ __device__ __forceinline__ void adam_tile_transposed(const KArgs& a, uint32_t ta
 #pragma unroll
         for (int it = 0; it < 8; ++it) {  // invalid rows (past M: j < 0) read row 0 and never store
             const long long off = (long long)max(j[it], 0) * a.ldc + n + c4;
-            w[it] = __ldcs(reinterpret_cast<const float4*>(a.adam_w + off));
-            m[it] = __ldcs(reinterpret_cast<const float4*>(a.adam_m + off));
-            v[it] = __ldcs(reinterpret_cast<const float4*>(a.adam_v + off));
+            w[it] = ADAM_LD(reinterpret_cast<const float4*>(a.adam_w + off));
+            m[it] = ADAM_LD(reinterpret_cast<const float4*>(a.adam_m + off));
+            v[it] = ADAM_LD(reinterpret_cast<const float4*>(a.adam_v + off));
         }
         tmem_ld_wait();
         const uint32_t sbase = smem_u32(sw);
@@ -455,9 +465,9 @@ __device__ __forceinline__ void adam_tile_transposed(const KArgs& a, uint32_t ta
             const uint2 cb = adam4<STATS>(w[it], m[it], v[it], g, a, k[it], ss[it], lsb[it]);
             if (j[it] >= 0) {
                 const long long off = (long long)j[it] * a.ldc + n + c4;
-                __stcs(reinterpret_cast<float4*>(a.adam_w + off), w[it]);
-                __stcs(reinterpret_cast<float4*>(a.adam_m + off), m[it]);
-                __stcs(reinterpret_cast<float4*>(a.adam_v + off), v[it]);
+                ADAM_ST(reinterpret_cast<float4*>(a.adam_w + off), w[it]);
+                ADAM_ST(reinterpret_cast<float4*>(a.adam_m + off), m[it]);
+                ADAM_ST(reinterpret_cast<float4*>(a.adam_v + off), v[it]);
                 *reinterpret_cast<uint2*>(a.adam_c + off) = cb;
             }
         }
@@ -1173,8 +1183,13 @@ void gemm_bf16_one(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmO
             const char* v = std::getenv("MEFT_PAIR_GROUP_AMN");  // A/B experiments (grad-W GEMMs)
             return v ? std::max(1, std::atoi(v)) : 0;
         }();
+        static const int forced_bmn = [] {
+            const char* v = std::getenv("MEFT_PAIR_GROUP_BMN");  // A/B experiments (out / grad_h GEMMs)
+            return v ? std::max(1, std::atoi(v)) : 0;
+        }();
         args.raster_group = forced ? forced : (!A.mn_major && !B.mn_major ? 16 : 8);
         if (A.mn_major && forced_amn) args.raster_group = forced_amn;
+        if (!A.mn_major && B.mn_major && forced_bmn) args.raster_group = forced_bmn;
         launch_pair_dispatch(st, A.mn_major, B.mn_major, ta, tb, B.rows ? tg : tb, args, int(pair_tiles));
         return;
     }
