@@ -2,6 +2,8 @@
 // and thin inline-PTX wrappers for mbarrier, TMA (cp.async.bulk.tensor) and tcgen05/TMEM.
 #pragma once
 
+#include <atomic>
+
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -47,6 +49,18 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 
 int num_sms();  // cached cudaDevAttrMultiProcessorCount of the current device
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device attribute: set it once per (call site, device
+// ordinal < 64). `done` is the call site's own flag word.
+inline void set_max_smem_once(std::atomic<unsigned long long>& done, const void* kernel, int bytes) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return;
+    const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) throw MeftError(6, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    done.fetch_or(bit, std::memory_order_acq_rel);
+}
 
 // Blocks of `kernel` that are co-resident on the whole GPU (SMs x occupancy): the grid for grid-stride loops, so
 // there is never a partial second wave (it doubled the tail of the exact re-scoring kernel: 1.33 waves).

@@ -993,12 +993,8 @@ int gemm_sms() { return std::max(2, num_sms() - g_reserved_sms.load(std::memory_
 template <bool A_MN, bool B_MN>
 void launch(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tg, const KArgs& args,
             int tiles_bound) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        MEFT_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_bf16<A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             SMEM_BYTES));
-        attr_set = true;
-    }
+    static std::atomic<unsigned long long> attr_done{0};
+    set_max_smem_once(attr_done, reinterpret_cast<const void*>(k_gemm_bf16<A_MN, B_MN>), SMEM_BYTES);
     const int grid = std::max(1, std::min(tiles_bound, gemm_sms()));
     k_gemm_bf16<A_MN, B_MN><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ta, tb, tg, args);
     check_launch("k_gemm_bf16");
@@ -1104,12 +1100,9 @@ void dispatch(cudaStream_t st, bool a_mn, bool b_mn, const CUtensorMap& ta, cons
 template <bool A_MN, bool B_MN>
 void launch_pair(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tg, const KArgs& args,
                  int pair_tiles) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        MEFT_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_bf16_pair<A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             P_SMEM_BYTES + ADAM_SCRATCH_BYTES));
-        attr_set = true;
-    }
+    static std::atomic<unsigned long long> attr_done{0};
+    set_max_smem_once(attr_done, reinterpret_cast<const void*>(k_gemm_bf16_pair<A_MN, B_MN>),
+                      P_SMEM_BYTES + ADAM_SCRATCH_BYTES);
     const int pairs = std::max(1, std::min(pair_tiles, gemm_sms() / 2));
     const int smem = P_SMEM_BYTES + (args.epi == EPI_ADAM_F32 ? ADAM_SCRATCH_BYTES : 0);
     k_gemm_bf16_pair<A_MN, B_MN><<<2 * pairs, NUM_THREADS, smem, st>>>(ta, tb, tg, args);

@@ -587,12 +587,8 @@ static void ke_select_certified(cudaStream_t st, const void* h_, const void* w_g
         MEFT_CUDA_CHECK(cudaMemsetAsync(counts, 0, N * 4, st));
         const int wpb = 4;
         const size_t rsm = size_t(wpb) * (kk_eff + 2 * N) * 4 + size_t(wpb) * N * 8;
-        static bool rattr = false;
-        if (!rattr) {
-            MEFT_CUDA_CHECK(cudaFuncSetAttribute(k_router_certified, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 200 * 1024));
-            rattr = true;
-        }
+        static std::atomic<unsigned long long> rattr{0};
+        set_max_smem_once(rattr, reinterpret_cast<const void*>(k_router_certified), 200 * 1024);
         k_router_certified<<<int((T + wpb - 1) / wpb), wpb * 32, rsm, st>>>(P, int(ldp), hn, gn, hl, gl, cbr, h, wg,
                                                                           int(d),
                                                                           int(T), int(N), int(kk_eff), tau, counts,
@@ -635,11 +631,8 @@ static void ke_select_certified(cudaStream_t st, const void* h_, const void* w_g
     const CertSplit cs = cert_split(d, ksplit > 1);
     const int ks_eff = cs.ks;
     const double cbk = cs.cb;
-    static bool cattr = false;
-    if (!cattr) {
-        MEFT_CUDA_CHECK(cudaFuncSetAttribute(k_topk_classify, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        cattr = true;
-    }
+    static std::atomic<unsigned long long> cattr{0};
+    set_max_smem_once(cattr, reinterpret_cast<const void*>(k_topk_classify), 200 * 1024);
     MEFT_CUDA_CHECK(cudaMemsetAsync(acount, 0, N * 4, st));
     k_topk_classify<<<int(T), 256, csm, st>>>(cand, tau, int(kk_eff), int(E), int(C), P2, int(take), hn, kn, cbk,
                                               sure, n_sure, amb, n_amb, acount, ks_eff, (long long)(T * C));
@@ -722,11 +715,8 @@ void ke_select_exact(cudaStream_t st, int dtype, const void* h, const void* w_g,
         score_dispatch(st, dtype, h, int(d), keys, int(E), entries, off, tile_off, int(N), grid_x, int(T * kk_eff),
                        int(kk_eff), cand);
     }
-    static bool attr = false;
-    if (!attr) {
-        MEFT_CUDA_CHECK(cudaFuncSetAttribute(k_topk_neurons, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr = true;
-    }
+    static std::atomic<unsigned long long> attr{0};
+    set_max_smem_once(attr, reinterpret_cast<const void*>(k_topk_neurons), 200 * 1024);
     k_topk_neurons<<<int(T), 512, topk_smem, st>>>(cand, tau, int(kk_eff), int(E), int(C), P2, int(take), TP2,
                                                    per_token, flags);
     check_launch("k_topk_neurons");
@@ -823,11 +813,8 @@ void route_certified(cudaStream_t st, const uint16_t* h, const uint16_t* w_g, in
     MEFT_CUDA_CHECK(cudaMemsetAsync(counts, 0, N * 4, st));
     const int wpb = 4;
     const size_t rsm = size_t(wpb) * (kk_eff + 2 * N) * 4 + size_t(wpb) * N * 8;
-    static bool rattr = false;
-    if (!rattr) {
-        MEFT_CUDA_CHECK(cudaFuncSetAttribute(k_router_certified, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        rattr = true;
-    }
+    static std::atomic<unsigned long long> rattr{0};
+    set_max_smem_once(rattr, reinterpret_cast<const void*>(k_router_certified), 200 * 1024);
     k_router_certified<<<int((T + wpb - 1) / wpb), wpb * 32, rsm, st>>>(P, int(ldp), hn, gn, hl, gl,
                                                                       cbr, h, w_g, int(d), int(T),
                                                                       int(N), int(kk_eff), tau, counts, stats);
@@ -906,11 +893,8 @@ void topk_classify(cudaStream_t st, const float* cand, const int32_t* tau, int64
     if (T <= 0) return;
     const int64_t C = kk * E;
     const size_t csm = size_t(C) * 9 + 16;
-    static bool cattr = false;
-    if (!cattr) {
-        MEFT_CUDA_CHECK(cudaFuncSetAttribute(k_topk_classify, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        cattr = true;
-    }
+    static std::atomic<unsigned long long> cattr{0};
+    set_max_smem_once(cattr, reinterpret_cast<const void*>(k_topk_classify), 200 * 1024);
     k_topk_classify<<<int(T), 256, csm, st>>>(cand, tau, int(kk), int(E), int(C), next_pow2(int(C)), int(take), hn, kn,
                                               cert_split(d, true).cb, sure, n_sure, amb, n_amb, amb_count_per_expert,
                                               1, 0);
