@@ -1301,14 +1301,11 @@ meft_status meft_scatter_grads(meft_ctx* ctx, meft_store* s, int64_t layer, cons
         if (code == 0) {  // strictly ascending => unique rows => one CTA per row, no atomics
             stage_add(ctx->stream, sdt, L.st_a, s->d, S, n, dcode(gdt), gk, L.staged);
             stage_add(ctx->stream, sdt, L.st_b, s->d, S, n, dcode(gdt), gv, nullptr);
-        } else {  // repeated indices: apply entries in order (memtier.cpp:139-149 sums them in sequence)
-            const int ge = esize(gdt);
-            for (int64_t j = 0; j < n; ++j) {
-                stage_add(ctx->stream, sdt, L.st_a, s->d, S + j, 1, dcode(gdt),
-                          static_cast<const uint8_t*>(gk) + j * s->d * ge, L.staged);
-                stage_add(ctx->stream, sdt, L.st_b, s->d, S + j, 1, dcode(gdt),
-                          static_cast<const uint8_t*>(gv) + j * s->d * ge, nullptr);
-            }
+        } else {  // repeated indices (memtier.cpp:139-149 sums them in entry order): segmented by neuron id
+            const size_t wb = stage_add_segmented_ws(n);
+            void* ws = ctx->get("scatter_seg", wb);
+            stage_add_segmented(ctx->stream, sdt, L.st_a, s->d, S, n, dcode(gdt), gk, L.staged, ws, wb);
+            stage_add_segmented(ctx->stream, sdt, L.st_b, s->d, S, n, dcode(gdt), gv, nullptr, ws, wb);
         }
     });
 }

@@ -10,6 +10,11 @@ void gather_rows2(cudaStream_t st, const void* a, const void* b, int64_t row_byt
 void check_sorted_unique(cudaStream_t st, const int32_t* idx, int64_t n, int64_t limit, int32_t* err_dev);
 void stage_add(cudaStream_t st, int stage_dtype, void* stage, int64_t d, const int32_t* idx, int64_t n, int g_dtype,
                const void* g, uint8_t* staged);
+// scatter_grads with repeated ids (scatter_seg.cu): stable sort by id, one CTA per run of equal ids adding its rows
+// in position order -- atomic-free and bit-identical to the sequential per-entry loop.
+size_t stage_add_segmented_ws(int64_t n);
+void stage_add_segmented(cudaStream_t st, int stage_dtype, void* stage, int64_t d, const int32_t* idx, int64_t n,
+                         int g_dtype, const void* g, uint8_t* staged, void* ws, size_t ws_bytes);
 void mark_rows(cudaStream_t st, uint8_t* staged, const int32_t* idx, const int32_t* count_dev, int64_t count);
 void union_holes(cudaStream_t st, const int32_t* idx, const int32_t* n_dev, int32_t* out);
 void slot_sum(cudaStream_t st, const float* recv, int world, int64_t n, float* out);  // sum of `world` slots of n
