@@ -204,10 +204,12 @@ def our_arm(args, rank, world, local_rank):
         store.init_reference(seed=1)  # HostStore::init tables (reference RNG streams 0x5000/0x5001)
         wgen = torch.Generator(device=dev).manual_seed(0x7001)
         b = 1.0 / math.sqrt(d)
-        w_b = (torch.rand((M, d), generator=wgen, device=dev) * 2 - 1) * b  # W_B ~ U(+-1/sqrt d)
-        store.tensor(0, "w_b").copy_(w_b)
-        store.tensor(0, "w_b_compute").copy_(w_b.to(torch.bfloat16))
-        del w_b
+        w_b, w_bc = store.tensor(0, "w_b"), store.tensor(0, "w_b_compute")
+        for r0 in range(0, M, 65536):  # W_B ~ U(+-1/sqrt d), in place, chunked (no full temporary)
+            blk = (torch.rand((min(65536, M - r0), d), generator=wgen, device=dev) * 2 - 1) * b
+            w_b[r0:r0 + blk.shape[0]].copy_(blk)
+            w_bc[r0:r0 + blk.shape[0]].copy_(blk.to(torch.bfloat16))
+        del blk
 
         base = None
         if args.base_ffn:  # the frozen base FFN of the layer too (optional n = 11008 run)
@@ -350,9 +352,9 @@ def our_arm(args, rank, world, local_rank):
     roof_ms = (ffn_roof + key_bytes / (hbm * 1e9) + 2 * T * N * d / (tc_peak * 1e12)) * 1e3
 
     # DRAM traffic per GEMM launch from the committed ncu --set full capture of one step's six GEMMs
-    traffic = None
+    traffic = None  # the committed capture is of the cfg2 step only
     tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "gemm_traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and CFG["workload"] == "llama7b_meft_layer":
         with open(tpath) as f:
             traffic = json.load(f).get("mean_dram_bytes_per_launch")
 
@@ -378,7 +380,7 @@ def our_arm(args, rank, world, local_rank):
                        parallelism="single GPU" if not sharded else f"expert-sharded ep{world} (NCCL all-to-all)",
                        base_ffn=args.base_ffn,
                        precision="bf16 compute, fp32 "
-                       "master/Adam state", l2="inputs larger than L2 (7.5 GB of tables per layer)",
+                       "master/Adam state", l2=f"inputs larger than L2 ({M * d * 28 / 1e9:.1f} GB of tables per layer)",
                        union_size=S),
         "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": 2 * T * d * 2,
                 "d2h_bytes_per_step": 2 * T * d * 4, "ms_per_step": e2e_s * 1e3,
@@ -441,7 +443,12 @@ def main():
     ap.add_argument("--sharded", action="store_true", help="run the expert-sharded layer even on one GPU")
     ap.add_argument("--base-ffn", type=int, default=0,
                     help="also run the frozen base FFN of width n (SiLU), e.g. 11008 for LLaMA-7B (single GPU)")
+    ap.add_argument("--workload", choices=["cfg2", "cfg4"], default="cfg2",
+                    help="cfg2: the LLaMA-7B-shape layer (default, BASELINE configs[1]); cfg4: the Mistral-7B shape "
+                         "with M = 1,048,576 neurons and 1,024 experts (BASELINE configs[3], meant for --gpus 8)")
     args = ap.parse_args()
+    if args.workload == "cfg4":
+        CFG.update(workload="mistral7b_meft_layer_1m", pairs=1048576, experts=1024)
     args.warmup = max(args.warmup, 0)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -443,31 +443,50 @@ void* tensor_ptr(const meft_store* s, const LayerBufs& L, meft_tensor t, meft_dt
 
 // Uploads a float64 host matrix in the reference layout into the device tensor (converting layout/precision),
 // refreshing the bf16 compute copy when a MIXED master weight changes.
+// Host <-> store transfers in reference layouts, converted on the device through two fixed 64 MB fp64 scratch
+// buffers (chunks of whole columns of a d x r table, or of whole rows), so an M = 1M table (34 GB in fp64) never
+// needs a table-sized staging copy in HBM.
+constexpr int64_t kXferElems = int64_t(8) << 20;
+
+void* elem_offset(void* base, meft_dtype dt, int64_t elems) {
+    return static_cast<uint8_t*>(base) + elems * esize(dt);
+}
+
 void upload_f64(meft_ctx* ctx, meft_store* s, const LayerBufs& L, meft_tensor t, const double* host) {
     cudaStream_t st = ctx->stream;
     meft_dtype dt;
     int64_t rows, cols;
     void* dst = tensor_ptr(s, L, t, &dt, &rows, &cols);
-    const int64_t n = rows * cols;
-    double* tmp = static_cast<double*>(ctx->get("upload_a", size_t(n) * 8));
-    MEFT_CUDA_CHECK(cudaMemcpyAsync(tmp, host, size_t(n) * 8, cudaMemcpyHostToDevice, st));
-    const double* src = tmp;
-    if (is_a_family(t)) {  // host d x r -> device r x d
-        double* tr = static_cast<double*>(ctx->get("upload_b", size_t(n) * 8));
-        transpose8(st, tmp, tr, s->d, s->pairs);
-        src = tr;
+    void* comp = nullptr;  // the bf16 compute copy that follows the master (mixed stores)
+    if (s->prec == MEFT_STORE_MIXED)
+        comp = t == MEFT_T_W_A ? L.c_a : t == MEFT_T_W_B ? L.c_b : t == MEFT_T_W_G ? L.c_g : nullptr;
+    double* tmp = static_cast<double*>(ctx->get("xfer_a", size_t(kXferElems) * 8));
+    if (is_a_family(t)) {  // host d x r -> device r x d, a block of whole columns at a time
+        double* tr = static_cast<double*>(ctx->get("xfer_b", size_t(kXferElems) * 8));
+        const int64_t d = s->d, r = s->pairs, cw = std::max<int64_t>(1, kXferElems / d);
+        for (int64_t c0 = 0; c0 < r; c0 += cw) {
+            const int64_t w = std::min(cw, r - c0);
+            MEFT_CUDA_CHECK(cudaMemcpy2DAsync(tmp, size_t(w) * 8, host + c0, size_t(r) * 8, size_t(w) * 8, size_t(d),
+                                              cudaMemcpyHostToDevice, st));
+            transpose8(st, tmp, tr, d, w);  // d x w -> w x d
+            convert(st, dcode(dt), elem_offset(dst, dt, c0 * d), 0, tr, w * d);
+            if (comp) convert(st, 2, elem_offset(comp, MEFT_BF16, c0 * d), 0, tr, w * d);
+            MEFT_CUDA_CHECK(cudaStreamSynchronize(st));  // the scratch is reused by the next block
+        }
+    } else {
+        const int64_t rc = std::max<int64_t>(1, kXferElems / std::max<int64_t>(cols, 1));
+        for (int64_t r0 = 0; r0 < rows; r0 += rc) {
+            const int64_t nr = std::min(rc, rows - r0), n = nr * cols;
+            MEFT_CUDA_CHECK(cudaMemcpyAsync(tmp, host + r0 * cols, size_t(n) * 8, cudaMemcpyHostToDevice, st));
+            convert(st, dcode(dt), elem_offset(dst, dt, r0 * cols), 0, tmp, n);
+            if (comp) convert(st, 2, elem_offset(comp, MEFT_BF16, r0 * cols), 0, tmp, n);
+            MEFT_CUDA_CHECK(cudaStreamSynchronize(st));
+        }
     }
-    convert(st, dcode(dt), dst, 0, src, n);
     if (t == MEFT_T_W_A) {
         for (size_t l = 0; l < s->L.size(); ++l)
             if (&s->L[l] == &L) s->key_stats_valid[l] = 0;
     }
-    if (s->prec == MEFT_STORE_MIXED) {
-        if (t == MEFT_T_W_A) convert(st, 2, L.c_a, 0, src, n);
-        if (t == MEFT_T_W_B) convert(st, 2, L.c_b, 0, src, n);
-        if (t == MEFT_T_W_G) convert(st, 2, L.c_g, 0, src, n);
-    }
-    MEFT_CUDA_CHECK(cudaStreamSynchronize(st));  // the host buffer may be pageable and is released on return
 }
 
 void download_f64(meft_ctx* ctx, meft_store* s, const LayerBufs& L, meft_tensor t, double* host) {
@@ -475,17 +494,27 @@ void download_f64(meft_ctx* ctx, meft_store* s, const LayerBufs& L, meft_tensor 
     meft_dtype dt;
     int64_t rows, cols;
     const void* srcp = tensor_ptr(s, L, t, &dt, &rows, &cols);
-    const int64_t n = rows * cols;
-    double* tmp = static_cast<double*>(ctx->get("upload_a", size_t(n) * 8));
-    convert(st, 0, tmp, dcode(dt), srcp, n);
-    const double* out = tmp;
-    if (is_a_family(t)) {  // device r x d -> host d x r
-        double* tr = static_cast<double*>(ctx->get("upload_b", size_t(n) * 8));
-        transpose8(st, tmp, tr, s->pairs, s->d);
-        out = tr;
+    double* tmp = static_cast<double*>(ctx->get("xfer_a", size_t(kXferElems) * 8));
+    if (is_a_family(t)) {  // device r x d -> host d x r, a block of whole columns at a time
+        double* tr = static_cast<double*>(ctx->get("xfer_b", size_t(kXferElems) * 8));
+        const int64_t d = s->d, r = s->pairs, cw = std::max<int64_t>(1, kXferElems / d);
+        for (int64_t c0 = 0; c0 < r; c0 += cw) {
+            const int64_t w = std::min(cw, r - c0);
+            convert(st, 0, tmp, dcode(dt), elem_offset(const_cast<void*>(srcp), dt, c0 * d), w * d);
+            transpose8(st, tmp, tr, w, d);  // w x d -> d x w
+            MEFT_CUDA_CHECK(cudaMemcpy2DAsync(host + c0, size_t(r) * 8, tr, size_t(w) * 8, size_t(w) * 8, size_t(d),
+                                              cudaMemcpyDeviceToHost, st));
+            MEFT_CUDA_CHECK(cudaStreamSynchronize(st));
+        }
+    } else {
+        const int64_t rc = std::max<int64_t>(1, kXferElems / std::max<int64_t>(cols, 1));
+        for (int64_t r0 = 0; r0 < rows; r0 += rc) {
+            const int64_t nr = std::min(rc, rows - r0), n = nr * cols;
+            convert(st, 0, tmp, dcode(dt), elem_offset(const_cast<void*>(srcp), dt, r0 * cols), n);
+            MEFT_CUDA_CHECK(cudaMemcpyAsync(host + r0 * cols, tmp, size_t(n) * 8, cudaMemcpyDeviceToHost, st));
+            MEFT_CUDA_CHECK(cudaStreamSynchronize(st));
+        }
     }
-    MEFT_CUDA_CHECK(cudaMemcpyAsync(host, out, size_t(n) * 8, cudaMemcpyDeviceToHost, st));
-    MEFT_CUDA_CHECK(cudaStreamSynchronize(st));
 }
 
 // HostStore::init streams (memtier.cpp:67-77) with the reference RNG (rng.hpp:13-36, 62-66).
