@@ -92,7 +92,7 @@ def test_sharded_world1_peer_path_equals_layer_step(ctx, nccl_world1, monkeypatc
     layer.peer.close()
 
 
-@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("P", [2, 4, 8])
 def test_sharded_device_path_multirank_emulated(ctx, P):
     """The expert-sharded step with the DEVICE engine at P ranks, emulated in one process (ThreadGroup: one thread
     and one context per rank, collectives as host-side exchanges of finished tensors -- no kernel waits on another
