@@ -1,6 +1,8 @@
 """Whole-layer parity: meft_layer_step (ke_select -> fetch -> sparse_ffn_pa -> sparse_backward ->
 scatter_grads -> sparse_adam_update) on B200 against the reference layer step at the cfg1 shape, and
 size-independent properties at the BASELINE cfg2 shape."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -368,3 +370,66 @@ def test_layer_step_odd_dims_vs_live_reference(ctx, d, M, N, T, kk, K):
         err = np.abs((got - w0) - (exp - w0))
         assert np.all(err <= 2 * lr + 1e-6)
         assert (err <= 1e-2 * lr + 1e-6 * np.abs(exp)).mean() > 0.99
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("MEFT_RANDOM_GEOMETRIES", "8"))))
+def test_layer_step_random_geometries_vs_oracle(ctx, seed):
+    """Randomised geometries of the fused step (d a multiple of 8, expert sizes a multiple of 4, T from 1, K from 1
+    up to the clamp, kk up to N): indices bit-exact against the C restatement, out / grad_h within the bf16
+    tolerance, and Adam touching exactly the union."""
+    rs = np.random.RandomState(1000 + seed)
+    d = int(rs.choice([8, 64, 136, 256, 520]))
+    N = int(rs.choice([1, 2, 5, 16]))
+    E = int(rs.choice([4, 12, 64]))
+    M = N * E
+    kk = int(rs.randint(1, N + 1))
+    K = int(rs.randint(1, kk * E + 3))  # may exceed the visible candidates: clamped with a warning
+    T = int(rs.choice([1, 3, 77, 256]))
+    w_a, w_g, w_b, h, gr = cfg1_inputs(d, M, N, T)
+    st = make_store(ctx, w_a, w_g, w_b, N)
+    out = torch.empty((T, d), dtype=torch.float32, device="cuda")
+    gh = torch.empty_like(out)
+    res = st.layer_step(0, bf16_dev(h), bf16_dev(gr), kk, K, 1e-3, out=out, grad_h=gh, want_selection=True)
+    torch.cuda.synchronize()
+    sel = O.ke_select(h, w_g, w_a, kk, K)
+    np.testing.assert_array_equal(res["per_token"].cpu().numpy(), sel["per_token"])
+    np.testing.assert_array_equal(res["unioned"].cpu().numpy(), sel["unioned"])
+    wak, wbk = O.gather_adapter(w_a, w_b, sel["unioned"])
+    ref_out, z, _ = O.ffn_forward(h, wak, wbk)
+    _, _, ref_gh = O.ffn_backward(gr, h, z, None, wak, wbk)
+    if np.linalg.norm(ref_out) > 0:
+        assert rel(out.cpu().numpy(), ref_out) < BF16_TOL
+    if np.linalg.norm(ref_gh) > 0:
+        assert rel(gh.cpu().numpy(), ref_gh) < BF16_TOL
+    steps = st.download(0, "pair_step")
+    assert set(np.nonzero(steps)[0].tolist()) == set(sel["unioned"].tolist())
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("MEFT_RANDOM_GEOMETRIES_LARGE", "3"))))
+def test_layer_step_random_large_geometries_vs_oracle(ctx, seed):
+    """Randomised geometries large enough for the CTA-pair GEMMs, the transposed Adam epilogue and the TMA row
+    gather: indices bit-exact against the C restatement, values within the bf16 tolerance."""
+    rs = np.random.RandomState(2000 + seed)
+    d = int(rs.choice([768, 1024, 1056]))
+    N = int(rs.choice([8, 16, 32]))
+    E = int(rs.choice([128, 256]))
+    M = N * E
+    kk = int(rs.randint(1, min(N, 6) + 1))
+    K = int(rs.choice([16, 64, 128]))
+    T = int(rs.choice([384, 1000]))
+    w_a, w_g, w_b, h, gr = cfg1_inputs(d, M, N, T)
+    st = make_store(ctx, w_a, w_g, w_b, N)
+    out = torch.empty((T, d), dtype=torch.float32, device="cuda")
+    gh = torch.empty_like(out)
+    res = st.layer_step(0, bf16_dev(h), bf16_dev(gr), kk, K, 1e-3, out=out, grad_h=gh, want_selection=True)
+    torch.cuda.synchronize()
+    sel = O.ke_select(h, w_g, w_a, kk, K)
+    np.testing.assert_array_equal(res["per_token"].cpu().numpy(), sel["per_token"])
+    np.testing.assert_array_equal(res["unioned"].cpu().numpy(), sel["unioned"])
+    wak, wbk = O.gather_adapter(w_a, w_b, sel["unioned"])
+    ref_out, z, _ = O.ffn_forward(h, wak, wbk)
+    _, _, ref_gh = O.ffn_backward(gr, h, z, None, wak, wbk)
+    assert rel(out.cpu().numpy(), ref_out) < BF16_TOL
+    assert rel(gh.cpu().numpy(), ref_gh) < BF16_TOL
+    steps = st.download(0, "pair_step")
+    assert set(np.nonzero(steps)[0].tolist()) == set(sel["unioned"].tolist())
