@@ -3,10 +3,13 @@ count M and per-token budget K. Tables are initialised on the device (uniform +-
 inputs uniform(-1, 1); each point prints one JSON line. Points that do not fit HBM report the error.
 
   python tools/scale_sweep.py [T] M:N:K [M:N:K ...]      e.g.  8192 65536:256:128 1048576:1024:128
+With MEFT_SWEEP_CPU=1 every point whose fp64 reference store fits host RAM (M <= 65536 here) is also timed on the
+unmodified reference CPU implementation (oracle/_ref, all host cores) on a bounded 32-token sample of the step.
 """
 import json
 import os
 import sys
+import time
 
 import torch
 
@@ -58,6 +61,27 @@ def run_point(ctx, T, M, N, K, kk=4, steps=5, warmup=2):
     return line
 
 
+def cpu_point(T, M, N, K, kk=4, tokens=32):
+    """The reference's ref_layer_step (meft_ffn -> sparse_backward -> scatter_grads -> sparse_adam_update) on the
+    point's geometry for a bounded token sample; returns tokens/s and the thread count."""
+    import numpy as np
+
+    from oracle import oracle as O
+
+    R = O.ref()
+    cores = os.cpu_count()
+    R.ref_set_threads(cores)
+    st = O.RefStore(1, D, M, N, seed=1)
+    rng = np.random.default_rng(7)
+    st.set(0, "w_b", rng.uniform(-1, 1, size=(M, D)) / D ** 0.5)
+    h = rng.uniform(-1, 1, size=(tokens, D))
+    g = rng.uniform(-1, 1, size=(tokens, D))
+    st.layer_step(0, h[:2], g[:2], kk, K, 1e-4, want_outputs=False)  # warm-up
+    t0 = time.perf_counter()
+    st.layer_step(0, h, g, kk, K, 1e-4, want_outputs=False)
+    return tokens / (time.perf_counter() - t0), cores
+
+
 def main():
     args = sys.argv[1:]
     T = 8192
@@ -68,7 +92,12 @@ def main():
     for spec in args or ["65536:256:128"]:
         M, N, K = (int(x) for x in spec.split(":"))
         try:
-            print(json.dumps(run_point(ctx, T, M, N, K)), flush=True)
+            line = run_point(ctx, T, M, N, K)
+            if os.environ.get("MEFT_SWEEP_CPU") == "1" and M <= 65536:
+                tps, cores = cpu_point(T, M, N, K)
+                line["cpu_reference"] = {"tokens_per_s": tps, "cores": cores, "sample_tokens": 32,
+                                         "gpu_over_cpu": line["tokens_per_s"] / tps}
+            print(json.dumps(line), flush=True)
         except Exception as e:  # e.g. a point that does not fit HBM
             print(json.dumps({"T": T, "M": M, "experts": N, "K": K, "error": str(e)[:300]}), flush=True)
             torch.cuda.empty_cache()
