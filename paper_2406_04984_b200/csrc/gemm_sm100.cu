@@ -743,7 +743,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 //   warp 0 (both CTAs): TMA into the local ring, completion counted on the leader's full barrier
 //   warp 1 (leader)   : MMA issue; commits multicast to both CTAs' empty / tmem-full barriers
 //   warps 2-5 (both)  : epilogue of the local 128 rows; release the accumulator on the leader's tmem-empty
-constexpr int P_STAGES = 6;
+#ifndef MEFT_P_STAGES
+#define MEFT_P_STAGES 6
+#endif
+constexpr int P_STAGES = MEFT_P_STAGES;  // 6 x 32 KB stages (A/B knob for tuning)
 constexpr int P_A_BYTES = 128 * BK * 2;
 constexpr int P_B_BYTES = 128 * BK * 2;
 constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
