@@ -1218,9 +1218,13 @@ void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOpera
     // policy: 65536 per dimension (measured on |S| = 640k GEMMs: z 37.5 -> 33.8 ms, out 46.7 -> 38.5,
     // gW 45.2 -> 39.2; 32768 is equivalent, cfg2's |S| = 65536 stays one launch)
     constexpr int64_t kChunk = 65536;
-    const int64_t mc = round_up(mc_env ? mc_env : kChunk, P_TILE_M);
-    const int64_t nc = round_up(nc_env ? nc_env : kChunk, BN);
-    const int64_t kc = f32_out ? round_up(kc_env ? kc_env : kChunk, BK) : K;
+    // panelled operands fix the chunk width to the panel width
+    const bool panels = A.panel_stride || epi.panel_stride;
+    if (panels && (epi.mask && !epi.bits)) throw MeftError(2, "gemm_bf16: a panelled C needs the bitmask, not a mask");
+    const int64_t mc = panels ? kGemmPanel : round_up(mc_env ? mc_env : kChunk, P_TILE_M);
+    const int64_t nc = panels ? kGemmPanel : round_up(nc_env ? nc_env : kChunk, BN);
+    const int64_t kc = f32_out ? (panels ? kGemmPanel : round_up(kc_env ? kc_env : kChunk, BK)) : K;
+    static_assert(kChunk == kGemmPanel, "panel width = chunk width");
     if (epi.kind == EPI_ADAM_F32 && (N > nc || N != epi.ldc))
         throw MeftError(2, "gemm_bf16: the Adam epilogue covers whole table rows of at most 65536 columns");
     if ((mc >= M && nc >= N && kc >= K) || epi.ksplit > 1) return gemm_bf16_one(st, M, N, K, A, B, epi);
@@ -1232,7 +1236,13 @@ void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOpera
             for (int64_t k0 = 0; k0 < K; k0 += kc) {
                 const int64_t ml = std::min(mc, M - m0), nl = std::min(nc, N - n0), kl = std::min(kc, K - k0);
                 GemmOperand a = A;
-                a.ptr = advance(A.ptr, A.mn_major ? k0 * A.ld + m0 : m0 * A.ld + k0, 2);
+                if (A.panel_stride) {  // the chunked dimension steps through whole panels
+                    a.ptr = advance(A.ptr, A.mn_major ? (m0 / kGemmPanel) * A.panel_stride + k0 * A.ld
+                                                      : (k0 / kGemmPanel) * A.panel_stride + m0 * A.ld, 2);
+                    a.panel_stride = 0;
+                } else {
+                    a.ptr = advance(A.ptr, A.mn_major ? k0 * A.ld + m0 : m0 * A.ld + k0, 2);
+                }
                 GemmOperand b = B;
                 if (!B.rows) {
                     b.ptr = advance(B.ptr, B.mn_major ? k0 * B.ld + n0 : n0 * B.ld + k0, 2);
@@ -1258,6 +1268,9 @@ void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOpera
                 } else if (rows_epi) {
                     e.row_idx = epi.row_idx + m0;
                     e.c = const_cast<void*>(advance(epi.c, n0, ce));
+                } else if (epi.panel_stride) {
+                    e.c = const_cast<void*>(advance(epi.c, (n0 / kGemmPanel) * epi.panel_stride + m0 * epi.ldc, ce));
+                    e.panel_stride = 0;
                 } else {
                     e.c = const_cast<void*>(advance(epi.c, m0 * epi.ldc + n0, ce));
                 }

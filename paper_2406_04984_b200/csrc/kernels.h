@@ -19,7 +19,12 @@ struct GemmOperand {
     const int32_t* rows = nullptr;
     int64_t table_rows = 0;
     int32_t* run_ws = nullptr;  // MN-major gathered B: scratch of ceil(K / 64) ints (per-k-block run table)
+    // Panelled A (gemm_bf16 only): the dimension gemm_bf16 chunks (K of a K-major A, M of an MN-major A) is stored
+    // as consecutive panels of kGemmPanel columns, panel p at ptr + p * panel_stride, each with leading dimension
+    // ld, so every sub-GEMM reads one dense [rows x kGemmPanel] panel. 0 = one plain matrix.
+    int64_t panel_stride = 0;
 };
+constexpr int64_t kGemmPanel = 65536;  // = gemm_bf16's chunk width
 
 enum GemmEpi : int {
     EPI_STORE_F32 = 0,     // C f32 [M x ldc] = acc            (or += acc when accumulate)
@@ -81,6 +86,9 @@ struct GemmEpilogue {
     double* stat_ss = nullptr;
     int32_t* stat_lsb = nullptr;
     int64_t stat_ld = 0;  // >= ceil(N / 256)
+    // Panelled C of the bf16 epilogues (EPI_RELU_BF16 / EPI_MASK_BF16 with bits): N stored as kGemmPanel-wide panels
+    // at c + p * panel_stride, leading dimension ldc (see GemmOperand::panel_stride).
+    int64_t panel_stride = 0;
 };
 constexpr int kAdamStatTile = 256;  // columns per EPI_ADAM_F32 statistics partial
 

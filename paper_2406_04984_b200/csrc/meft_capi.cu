@@ -274,7 +274,7 @@ GemmEpilogue peer_epilogue(const meft_peer_out& po, bool grad_h, int64_t d) {
 void ffn_forward_impl(meft_ctx* ctx, meft_dtype dt, const void* h, const void* keys_s, const void* values_s,
                       int64_t T, int64_t d, int64_t s, int64_t ld_z, void* z, void* out, bool accumulate,
                       const RowGather& rg = RowGather(), const meft_peer_out* peer = nullptr,
-                      uint32_t* act_bits = nullptr) {
+                      uint32_t* act_bits = nullptr, int64_t panel = 0) {
     cudaStream_t st = ctx->stream;
     if (dt == MEFT_F64) {
         double* outd = static_cast<double*>(out);
@@ -292,7 +292,8 @@ void ffn_forward_impl(meft_ctx* ctx, meft_dtype dt, const void* h, const void* k
         return;
     }
     require(dt == MEFT_BF16, MEFT_E_INVALID, "ffn_forward: dtype must be F64 or BF16");
-    require(d % 8 == 0 && ld_z % 8 == 0 && ld_z >= s, MEFT_E_INVALID, "ffn_forward(bf16): d and ld_z must be multiples of 8");
+    require(d % 8 == 0 && ld_z % 8 == 0 && (panel ? ld_z == kGemmPanel : ld_z >= s), MEFT_E_INVALID,
+            "ffn_forward(bf16): d and ld_z must be multiples of 8");
     if (s == 0) {
         if (!accumulate) MEFT_CUDA_CHECK(cudaMemsetAsync(out, 0, size_t(T * d) * 4, st));
         return;
@@ -303,6 +304,7 @@ void ffn_forward_impl(meft_ctx* ctx, meft_dtype dt, const void* h, const void* k
     e1.ldc = ld_z;
     e1.bits = act_bits;  // [T x ceil(s / 32)] bitmask of z > 0 for the backward's mask
     e1.ldbits = (s + 31) / 32;
+    e1.panel_stride = panel;  // act in kGemmPanel-wide panels (|S| > 65536)
     gemm_bf16(st, T, s, d, GemmOperand{h, d, false}, kv_operand(ctx, keys_s, d, false, rg, s), e1);
     GemmEpilogue e2;
     if (peer) {
@@ -313,7 +315,9 @@ void ffn_forward_impl(meft_ctx* ctx, meft_dtype dt, const void* h, const void* k
         e2.ldc = d;
         e2.accumulate = accumulate;
     }
-    gemm_bf16(st, T, d, s, GemmOperand{z, ld_z, false}, kv_operand(ctx, values_s, d, true, rg, s), e2);
+    GemmOperand za{z, ld_z, false};
+    za.panel_stride = panel;
+    gemm_bf16(st, T, d, s, za, kv_operand(ctx, values_s, d, true, rg, s), e2);
 }
 
 // stage_keys/stage_values non-null => weight grads are row-added into the store staging at S (fused scatter).
@@ -323,7 +327,8 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
                        void* stage_keys, void* stage_values, const RowGather& rg = RowGather(),
                        cudaEvent_t grad_h_done = nullptr, const std::function<void()>* between = nullptr,
                        const meft_peer_out* peer = nullptr, const GemmEpilogue* epi_values = nullptr,
-                       const GemmEpilogue* epi_keys = nullptr, const uint32_t* act_bits = nullptr) {
+                       const GemmEpilogue* epi_keys = nullptr, const uint32_t* act_bits = nullptr,
+                       int64_t panel = 0) {
     cudaStream_t st = ctx->stream;
     if (dt == MEFT_F64) {
         const double* gd = static_cast<const double*>(g);
@@ -354,7 +359,13 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
         return;
     }
     require(dt == MEFT_BF16, MEFT_E_INVALID, "ffn_backward: dtype must be F64 or BF16");
-    require(d % 8 == 0 && ld_z % 8 == 0 && ld_z >= s, MEFT_E_INVALID, "ffn_backward(bf16): alignment");
+    require(d % 8 == 0 && ld_z % 8 == 0 && (panel ? ld_z == kGemmPanel && act_bits : ld_z >= s), MEFT_E_INVALID,
+            "ffn_backward(bf16): alignment");
+    auto op = [panel](const void* p, int64_t ld, bool mn) {  // act / masked operands, panelled when |S| > 65536
+        GemmOperand o{p, ld, mn};
+        o.panel_stride = panel;
+        return o;
+    };
     if (s == 0) {
         if (!acc_h && grad_h) MEFT_CUDA_CHECK(cudaMemsetAsync(grad_h, 0, size_t(T * d) * 4, st));
         return;
@@ -367,6 +378,7 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
     e3.ldm = ld_z;
     e3.bits = const_cast<uint32_t*>(act_bits);  // the forward's bitmask instead of re-reading act (1/16 the bytes)
     e3.ldbits = (s + 31) / 32;
+    e3.panel_stride = panel;
     gemm_bf16(st, T, s, d, GemmOperand{g, d, false}, kv_operand(ctx, values_s, d, false, rg, s), e3);
     if (grad_h || peer) {  // first after masked, so grad_h can stream back while the weight-gradient GEMMs run
         GemmEpilogue e6;  // grad_h (+)= masked * keys_s
@@ -378,7 +390,7 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
             e6.ldc = d;
             e6.accumulate = acc_h;
         }
-        gemm_bf16(st, T, d, s, GemmOperand{masked, ld_z, false}, kv_operand(ctx, keys_s, d, true, rg, s), e6);
+        gemm_bf16(st, T, d, s, op(masked, ld_z, false), kv_operand(ctx, keys_s, d, true, rg, s), e6);
     }
     if (grad_h_done) MEFT_CUDA_CHECK(cudaEventRecord(grad_h_done, st));
     GemmEpilogue e4;  // grad_values = act^T G   (M = s, N = d, K = T)
@@ -391,11 +403,11 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
         e4.c = grad_values_s;
     }
     e4.ldc = d;
-    gemm_bf16(st, s, d, T, GemmOperand{z, ld_z, true}, GemmOperand{g, d, true}, epi_values ? *epi_values : e4);
+    gemm_bf16(st, s, d, T, op(z, ld_z, true), GemmOperand{g, d, true}, epi_values ? *epi_values : e4);
     if (between) (*between)();  // e.g. consume grad_values before grad_keys reuses its buffer
     GemmEpilogue e5 = e4;  // grad_keys = masked^T h
     e5.c = S_rows ? stage_keys : grad_keys_s;
-    gemm_bf16(st, s, d, T, GemmOperand{masked, ld_z, true}, GemmOperand{h, d, true}, epi_keys ? *epi_keys : e5);
+    gemm_bf16(st, s, d, T, op(masked, ld_z, true), GemmOperand{h, d, true}, epi_keys ? *epi_keys : e5);
 }
 
 // ---- store helpers
@@ -1487,7 +1499,22 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
     const LayerBufs& L = layer_of(s, layer);
     const int64_t d = s->d;
     cudaStream_t st = ctx->stream;
-    const int64_t ld = round_up(std::max<int64_t>(su, 1), 64);
+    // the z GEMM also writes the bitmask z > 0; the masked GEMM reads it instead of the bf16 act (64 MB instead of
+    // 1 GB at cfg2). MEFT_ACT_BITS=0 reads act (A/B; bitwise identical).
+    static const bool use_bits = [] {
+        const char* v = std::getenv("MEFT_ACT_BITS");
+        return !(v && v[0] == '0');
+    }();
+    // |S| > 65536: act and masked are stored as 65536-column panels ([T x 65536] each), so every chunked sub-GEMM
+    // streams one dense panel instead of a strided window of a T x |S| matrix (MEFT_ACT_PANELS=0: one matrix)
+    static const bool panels_on = [] {
+        const char* v = std::getenv("MEFT_ACT_PANELS");
+        return !(v && v[0] == '0');
+    }();
+    const bool panels = panels_on && use_bits && su > kGemmPanel && !s->train_router && !base;
+    const int64_t ld = panels ? kGemmPanel : round_up(std::max<int64_t>(su, 1), 64);
+    const int64_t panel = panels ? T * kGemmPanel : 0;
+    const int64_t z_elems = panels ? ceil_div(su, kGemmPanel) * panel : T * ld;
     if (holes < 0 && su > 0 && use_tma_gather(ctx, su, 0)) {  // caller does not know: measure (one read-back)
         union_holes_n(st, uni, su, ctx->dev_small + 12);
         MEFT_CUDA_CHECK(cudaMemcpyAsync(ctx->host_small + 12, ctx->dev_small + 12, 4, cudaMemcpyDeviceToHost, st));
@@ -1495,14 +1522,8 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
         holes = ctx->host_small[12];
     }
 
-    uint16_t* act = static_cast<uint16_t*>(ctx->get("act", size_t(T * ld) * 2));
-    uint16_t* masked = static_cast<uint16_t*>(ctx->get("masked", size_t(T * ld) * 2));
-    // the z GEMM also writes the bitmask z > 0; the masked GEMM reads it instead of the bf16 act (64 MB instead of
-    // 1 GB at cfg2). MEFT_ACT_BITS=0 reads act (A/B; bitwise identical).
-    static const bool use_bits = [] {
-        const char* v = std::getenv("MEFT_ACT_BITS");
-        return !(v && v[0] == '0');
-    }();
+    uint16_t* act = static_cast<uint16_t*>(ctx->get("act", size_t(z_elems) * 2));
+    uint16_t* masked = static_cast<uint16_t*>(ctx->get("masked", size_t(z_elems) * 2));
     uint32_t* act_bits = use_bits ? static_cast<uint32_t*>(ctx->get(
                                         "act_bits", size_t(std::max<int64_t>(T * ((su + 31) / 32), 1)) * 4))
                                   : nullptr;
@@ -1553,7 +1574,8 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
             e2.ldc = d;
             gemm_bf16(st, T, d, base->n, GemmOperand{base_act, ldn, false}, GemmOperand{base->w_out, d, true}, e2);
         }
-        ffn_forward_impl(ctx, MEFT_BF16, h, ks, vs, T, d, su, ld, act, outb, base != nullptr, rg, peer, act_bits);
+        ffn_forward_impl(ctx, MEFT_BF16, h, ks, vs, T, d, su, ld, act, outb, base != nullptr, rg, peer, act_bits,
+                         panel);
     }
     if (fwd_done) MEFT_CUDA_CHECK(cudaEventRecord(fwd_done, st));
     if (g_ready) MEFT_CUDA_CHECK(cudaStreamWaitEvent(st, g_ready, 0));
@@ -1590,7 +1612,7 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
             PhaseScope ps(ctx, 3);
             ffn_backward_impl(ctx, MEFT_BF16, g, h, act, ks, vs, T, d, su, ld, masked, nullptr, nullptr, ghb,
                               base != nullptr, uni, L.st_a, L.st_b, rg, gh_done, nullptr, peer, nullptr, nullptr,
-                              act_bits);
+                              act_bits, panel);
         }
         train_router();
         PhaseScope ps(ctx, 4);
@@ -1632,7 +1654,7 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
             PhaseScope ps(ctx, 3);
             ffn_backward_impl(ctx, MEFT_BF16, g, h, act, ks, vs, T, d, su, ld, masked, nullptr, nullptr, ghb,
                               base != nullptr, nullptr, nullptr, nullptr, rg, gh_done, nullptr, peer, &ev, &ek,
-                              act_bits);
+                              act_bits, panel);
         }
         train_router();
         if (stats) {
@@ -1663,7 +1685,8 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
             p3.emplace(ctx, 3);
         };
         ffn_backward_impl(ctx, MEFT_BF16, g, h, act, ks, vs, T, d, su, ld, masked, gblk, gblk, ghb, base != nullptr,
-                          nullptr, nullptr, nullptr, rg, gh_done, &values_step, peer, nullptr, nullptr, act_bits);
+                          nullptr, nullptr, nullptr, rg, gh_done, &values_step, peer, nullptr, nullptr, act_bits,
+                          panel);
         p3.reset();
         train_router();
         if (su > 0) adam_table(1);

@@ -433,3 +433,28 @@ def test_layer_step_random_large_geometries_vs_oracle(ctx, seed):
     assert rel(gh.cpu().numpy(), ref_gh) < BF16_TOL
     steps = st.download(0, "pair_step")
     assert set(np.nonzero(steps)[0].tolist()) == set(sel["unioned"].tolist())
+
+
+def test_layer_step_union_beyond_one_panel_vs_oracle(ctx):
+    """|S| > 65,536: act / masked live as 65,536-column panels and every FFN GEMM runs as chunked sub-GEMMs over
+    them (z, masked by N; out, grad_h by K; both grad-W GEMMs with the Adam epilogue by M). Indices bit-exact,
+    values within the bf16 tolerance, Adam touching exactly the union."""
+    d, N, E, T, kk, K = 64, 1024, 256, 512, 4, 256
+    M = N * E
+    w_a, w_g, w_b, h, gr = cfg1_inputs(d, M, N, T)
+    st = make_store(ctx, w_a, w_g, w_b, N)
+    out = torch.empty((T, d), dtype=torch.float32, device="cuda")
+    gh = torch.empty_like(out)
+    res = st.layer_step(0, bf16_dev(h), bf16_dev(gr), kk, K, 1e-3, out=out, grad_h=gh, want_selection=True)
+    torch.cuda.synchronize()
+    sel = O.ke_select(h, w_g, w_a, kk, K)
+    assert len(sel["unioned"]) > 65536
+    np.testing.assert_array_equal(res["per_token"].cpu().numpy(), sel["per_token"])
+    np.testing.assert_array_equal(res["unioned"].cpu().numpy(), sel["unioned"])
+    wak, wbk = O.gather_adapter(w_a, w_b, sel["unioned"])
+    ref_out, z, _ = O.ffn_forward(h, wak, wbk)
+    _, gwa, ref_gh = O.ffn_backward(gr, h, z, None, wak, wbk)
+    assert rel(out.cpu().numpy(), ref_out) < BF16_TOL
+    assert rel(gh.cpu().numpy(), ref_gh) < BF16_TOL
+    steps = st.download(0, "pair_step")
+    assert set(np.nonzero(steps)[0].tolist()) == set(sel["unioned"].tolist())
