@@ -422,6 +422,8 @@ class ShardedLayer:
         self.host_group = None
         if not isinstance(group, ThreadGroup) and dist.get_backend(group) == "nccl":
             ranks = list(range(self.world)) if group is None else dist.get_process_group_ranks(group)
+            # one node: gloo over loopback (its default interface lookup resolves the hostname, which may not)
+            os.environ.setdefault("GLOO_SOCKET_IFNAME", "lo")
             self.host_group = dist.new_group(ranks=ranks, backend="gloo")
         # Overlap (device engine over NCCL): the bulk all-gathers / reduce-scatters run on their own stream and
         # communicator, so they proceed while the selection exchanges and the FFN compute.
