@@ -529,7 +529,7 @@ class ShardedLayer:
         xs = eng.scatter_exact(x_back, back, T, Ccand)
         # 7. final per-token selection and the global union
         per_token, flags = eng.finalize(sure, n_sure, amb, n_amb, xs, take, self.M)
-        union = flags.to(torch.int32)
+        union = flags.to(torch.uint8).contiguous()  # the M-entry union bitmap, OR-reduced as a byte max
         _all_reduce(union, grp, "max")
         S = torch.nonzero(union).flatten()
         S_loc = S[(S >= r * self.M_loc) & (S < (r + 1) * self.M_loc)] - r * self.M_loc
