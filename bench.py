@@ -6,14 +6,27 @@ experts, K=128 neurons/token, kk=4 experts/token, T=8192 tokens per step, bf16 c
 state resident in HBM. One step = meft_ffn (ke_select -> fetch -> sparse FFN) -> sparse_backward ->
 scatter_grads -> sparse_adam_update (the reference trainer's per-layer sequence).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload cfg2|cfg1|cfg4]
 
-N>1 (torchrun, one rank per GPU): the expert-sharded layer (paper_2406_04984_b200/sharded.py) —
-each rank owns N/P experts and M/P pairs and brings T tokens, so the step covers N*T tokens ("scaling": "weak");
-tokens, candidate scores and partial outputs move over NCCL. --sharded runs that path on one GPU too.
+N>1: one rank per GPU. Launched without torchrun (no WORLD_SIZE in the environment), `--gpus N` re-executes itself
+under `torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1` and fails loudly when fewer than N GPUs
+are visible. Each rank runs the expert-sharded layer (paper_2406_04984_b200/sharded.py): it owns
+N/P experts and M/P pairs and brings T tokens, so the step covers N*T tokens ("scaling": "weak"); tokens,
+candidate scores and partial outputs move over NCCL. --sharded runs that path on one GPU too.
 Rank 0 prints one JSON line.
-The reference arm times the UNMODIFIED reference CPU implementation (oracle/_ref, built from
-/root/reference by oracle/Makefile) on the host cores, same config/metric, bounded per-step sample.
+
+Inputs (both arms, BASELINE.md §3): HostStore::init(seed 1) tables, W_B ~ U(+-1/sqrt d) from the reference RNG
+stream mix_seed(1, 0x7001), h ~ U(-1, 1) from 0x7002, grad_out from 0x7003, all bf16-rounded (the GPU computes in
+bf16; the CPU reference gets the same values as doubles).
+
+The reference arm times the UNMODIFIED reference CPU implementation (oracle/_ref, built from /root/reference by
+oracle/Makefile) through its public API on all host cores, at the SAME configuration: ke_select + fetch of the
+whole T-token batch, scatter_grads + sparse_adam_update of its union (|S| = 65,536 at cfg2) are timed once at full
+size, and each timed step runs sparse_ffn_pa + sparse_backward -- the T x |S| part, ~99% of the reference's time
+-- on a slice of the batch's token rows against that same union (every row of both is independent of the others,
+so the slice costs exactly its share of the full step). A step's time is its slice's FFN time plus the slice's
+token share of the once-per-step phases; `cpu_baseline.sample` spells this out. `--ref-full-step` instead times
+one unsliced T-token ref_layer_step (cfg2: ~15 min on 16 cores) to validate the composite.
 """
 from __future__ import annotations
 
@@ -28,7 +41,24 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CFG = dict(workload="llama7b_meft_layer", d=4096, pairs=65536, experts=256, k=128, kk=4, tokens=8192, lr=1e-4)
+CFG = dict(lr=1e-4)  # + the chosen WORKLOADS entry (main)
+WORKLOADS = {  # BASELINE.json configs[1] (default), [0] (the reference's own CPU workload), [3]
+    "cfg2": dict(workload="llama7b_meft_layer", d=4096, pairs=65536, experts=256, k=128, kk=4, tokens=8192),
+    "cfg1": dict(workload="reference_cpu_workload", d=512, pairs=4096, experts=64, k=32, kk=4, tokens=256),
+    "cfg4": dict(workload="mistral7b_meft_layer_1m", d=4096, pairs=1048576, experts=1024, k=128, kk=4, tokens=8192),
+}
+METRIC = "MEFT adapter layer tokens/sec (fwd+bwd+sparse update)"
+SEED, W_B_STREAM, H_STREAM, G_STREAM = 1, 0x7001, 0x7002, 0x7003
+
+
+def config_dict(world):
+    """The workload as both arms report it (identical dicts: the driver compares the arms on the same config)."""
+    return dict(workload=CFG["workload"], d=CFG["d"], pairs=CFG["pairs"], experts=CFG["experts"], k=CFG["k"],
+                kk=CFG["kk"], tokens_per_gpu=CFG["tokens"], global_tokens=CFG["tokens"] * world,
+                parallelism="single GPU" if world == 1 else f"expert-sharded ep{world} (NCCL all-to-all)",
+                inputs="reference RNG streams 0x7001-0x7003 (BASELINE.md §3), bf16-rounded",
+                l2=(f"inputs larger than L2 ({CFG['pairs'] * CFG['d'] * 28 / 1e9:.1f} GB of tables per layer)"
+                    if CFG["pairs"] * CFG["d"] * 28 > 126e6 else "tables fit in L2 (not flushed; a parity size)"))
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
@@ -102,45 +132,75 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------------------------- reference arm
 
-def ref_sample_step_tokens(steps=1):
-    """Tokens per timed reference step: 64 (~13 s of 16-core fp64 work at cfg2), 32 for runs of more than 10
-    steps, so `--steps K --warmup W` stays within a few minutes. MEFT_REF_SAMPLE_TOKENS overrides."""
+def ref_slice_tokens(steps):
+    """Token rows per timed reference step at this workload: about 3-4 s of 16-core fp64 work per step at cfg2
+    (32 rows; 16 for runs of more than 20 steps), the whole batch at cfg1. MEFT_REF_SAMPLE_TOKENS overrides."""
     env = os.environ.get("MEFT_REF_SAMPLE_TOKENS")
     if env:
-        return int(env)
-    return 64 if steps <= 10 else 32
+        return max(1, min(int(env), CFG["tokens"]))
+    if CFG["tokens"] * CFG["pairs"] * CFG["d"] <= 1 << 34:  # small workloads: every step is the whole batch
+        return CFG["tokens"]
+    return 32 if steps <= 20 else 16
 
 
-def run_reference_sample(steps, warmup, tokens, threads=None):
-    """Times ref_layer_step of the unmodified reference (oracle/_ref) at the cfg2 table shapes on `tokens`
-    tokens per step; returns (tokens/s, seconds per step, phase split, cores)."""
-    import numpy as np
-
+def reference_inputs():
+    """(store, h, grad_out) of the workload on the reference (oracle/_ref): HostStore::init(seed 1) plus the
+    BASELINE.md §3 streams, bf16-rounded -- the values the GPU arm uploads."""
     from oracle import oracle as O
+    from paper_2406_04984_b200 import meft as G
 
     if not O.ref_available():
         O.build()
+    d, M, N, T = CFG["d"], CFG["pairs"], CFG["experts"], CFG["tokens"]
+    st = O.RefStore(1, d, M, N, seed=SEED)
+    b = 1.0 / math.sqrt(d)
+    st.set(0, "w_b", G.reference_uniform(SEED, W_B_STREAM, (M, d), -b, b, bf16=True))
+    h = G.reference_uniform(SEED, H_STREAM, (T, d), -1.0, 1.0, bf16=True)
+    g = G.reference_uniform(SEED, G_STREAM, (T, d), -1.0, 1.0, bf16=True)
+    return st, h, g
+
+
+def run_reference_phased(steps, warmup, rows, threads=None):
+    """The reference layer step of the full workload through its public API (oracle/ref_capi.cpp ref_step_*):
+    ke_select + fetch of the whole batch and scatter_grads + sparse_adam_update of its union timed once, the T x |S|
+    FFN forward + backward timed on `steps` slices of `rows` token rows (after `warmup` untimed slices).
+    Returns a dict: tokens/s, seconds per full step, per-slice step seconds, phase seconds of one full step, |S|."""
+    from oracle import oracle as O
+
     R = O.ref()
     cores = threads or os.cpu_count()
     R.ref_set_threads(cores)
-    d, M, N = CFG["d"], CFG["pairs"], CFG["experts"]
-    st = O.RefStore(1, d, M, N, seed=1)
-    rng = np.random.default_rng(0x7001)
-    b = 1.0 / math.sqrt(d)
-    st.set(0, "w_b", rng.uniform(-b, b, size=(M, d)))
-    h = rng.uniform(-1, 1, size=(tokens, d))
-    g = rng.uniform(-1, 1, size=(tokens, d))
-    times, phases = [], np.zeros(6)
-    for i in range(warmup + steps):
-        t0 = time.perf_counter()
-        hw, gw = (h, g) if i >= warmup else (h[:8], g[:8])  # warm-up steps: small samples, untimed
-        r = st.layer_step(0, hw, gw, CFG["kk"], CFG["k"], CFG["lr"], want_outputs=False)
-        dt = time.perf_counter() - t0
-        if i >= warmup:
-            times.append(dt)
-            phases += r["phases"]
-    sec = sum(times) / len(times)
-    return tokens / sec, sec, (phases / max(1, len(times))).tolist(), cores
+    st, h, g = reference_inputs()
+    T = CFG["tokens"]
+    slices = [((i * rows) % T, (i * rows) % T + rows) for i in range(warmup + steps)]
+    slices = [(lo, hi) if hi <= T else (T - rows, T) for lo, hi in slices]
+    t0 = time.perf_counter()
+    r = st.step_phases(0, h, g, CFG["kk"], CFG["k"], CFG["lr"], slices)
+    wall = time.perf_counter() - t0
+    fwd, bwd = r["forward"][warmup:], r["backward"][warmup:]
+    fixed = r["select"] + r["fetch"] + r["scatter"] + r["adam"]  # once per T-token step
+    per_row = (sum(fwd) + sum(bwd)) / (rows * len(fwd))
+    step_s = fixed + T * per_row
+    slice_steps = [f + b + fixed * rows / T for f, b in zip(fwd, bwd)]  # a slice + its token share of the rest
+    phases = dict(select=r["select"], fetch=r["fetch"], forward=T * sum(fwd) / (rows * len(fwd)),
+                  backward=T * sum(bwd) / (rows * len(bwd)), scatter=r["scatter"], adam=r["adam"])
+    return dict(tps=T / step_s, step_s=step_s, slice_steps=slice_steps, phases=phases, union_size=r["union_size"],
+                cores=cores, wall_s=wall, rows=rows)
+
+
+def run_reference_full(threads=None):
+    """One unsliced ref_layer_step of the whole T-token batch (validation of the phased composite)."""
+    from oracle import oracle as O
+
+    R = O.ref()
+    cores = threads or os.cpu_count()
+    R.ref_set_threads(cores)
+    st, h, g = reference_inputs()
+    t0 = time.perf_counter()
+    r = st.layer_step(0, h, g, CFG["kk"], CFG["k"], CFG["lr"], want_outputs=False)
+    sec = time.perf_counter() - t0
+    phases = dict(zip(["select", "fetch", "forward", "backward", "scatter", "adam"], r["phases"].tolist()))
+    return dict(tps=CFG["tokens"] / sec, step_s=sec, phases=phases, union_size=r["union_size"], cores=cores)
 
 
 def cpu_model():
@@ -153,30 +213,59 @@ def cpu_model():
     return "unknown"
 
 
+def phased_sample_text(r):
+    return (f"unmodified reference (oracle/_ref) through its public API, fp64, OpenMP {r['cores']} threads on "
+            f"{cpu_model()}, at the full workload (d={CFG['d']} M={CFG['pairs']} N={CFG['experts']} K={CFG['k']} "
+            f"kk={CFG['kk']} T={CFG['tokens']}, |S|={r['union_size']} of {CFG['pairs']}): ke_select + fetch of all "
+            f"{CFG['tokens']} tokens and scatter_grads + sparse_adam_update of the union timed once "
+            f"({r['phases']['select']:.1f} + {r['phases']['fetch']:.1f} + {r['phases']['scatter']:.1f} + "
+            f"{r['phases']['adam']:.1f} s); sparse_ffn_pa + sparse_backward timed on {len(r['slice_steps'])} slices "
+            f"of {r['rows']} token rows against that union and scaled by T/rows (rows are independent): "
+            f"{r['step_s']:.1f} s per {CFG['tokens']}-token step")
+
+
 def reference_arm(args, rank, world):
-    if rank != 0:
-        return  # rank 0 alone runs the CPU reference; other ranks exit 0 without work
-    tokens = ref_sample_step_tokens(args.steps)
-    try:
-        tps, sec, phases, cores = run_reference_sample(args.steps, args.warmup, tokens)
-    except Exception as e:  # pragma: no cover - surfaced as unavailable, never as a fake number
-        emit({"impl": "reference", "unavailable": f"reference CPU run failed: {e}"})
-        return
-    sample = (f"reference ref_layer_step (meft_ffn->sparse_backward->scatter_grads->sparse_adam_update) on the "
-              f"cfg2 tables d={CFG['d']} M={CFG['pairs']} N={CFG['experts']} K={CFG['k']} kk={CFG['kk']}, "
-              f"{tokens} tokens per step (bounded sample of the T={CFG['tokens']} step), fp64, OpenMP "
-              f"{cores} threads on {cpu_model()}")
+    if world > 1:  # every rank joins one rendezvous (proves the launch); rank 0 alone runs the CPU reference
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo")
+        seen = dist.get_world_size()
+        dist.barrier()
+        if rank != 0:
+            dist.destroy_process_group()
+            return
+    if args.ref_full_step:
+        try:
+            r = run_reference_full()
+        except Exception as e:  # pragma: no cover - surfaced as unavailable, never as a fake number
+            emit({"impl": "reference", "unavailable": f"reference CPU run failed: {e}"})
+            return
+        sample = (f"one unsliced ref_layer_step of all {CFG['tokens']} tokens (|S|={r['union_size']}), fp64, "
+                  f"OpenMP {r['cores']} threads on {cpu_model()}")
+        value, ms, steps_done = r["tps"], r["step_s"] * 1e3, 1
+    else:
+        rows = ref_slice_tokens(args.steps)
+        try:
+            r = run_reference_phased(args.steps, args.warmup, rows)
+        except Exception as e:  # pragma: no cover
+            emit({"impl": "reference", "unavailable": f"reference CPU run failed: {e}"})
+            return
+        sample = phased_sample_text(r)
+        value, ms, steps_done = r["tps"], r["step_s"] * 1e3, args.steps
     line = {
-        "impl": "reference", "metric": "MEFT adapter layer tokens/sec (fwd+bwd+sparse update)", "value": tps,
-        "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic",
-        "config": dict(workload=CFG["workload"], d=CFG["d"], pairs=CFG["pairs"], experts=CFG["experts"],
-                       k=CFG["k"], kk=CFG["kk"], tokens_per_step=tokens, global_tokens=CFG["tokens"]),
-        "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "reference", "sample": sample},
-        "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "phase_seconds": dict(zip(["select", "fetch", "forward", "backward", "scatter", "adam"], phases)),
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": steps_done, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_dict(world),
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": r["cores"], "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "phase_seconds": r["phases"], "union_size": r["union_size"],
     }
+    if world > 1:
+        line["ranks_joined"] = seen
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
     emit(line)
 
 
@@ -192,24 +281,32 @@ def our_arm(args, rank, world, local_rank):
     torch.cuda.set_device(dev)
     d, M, N, K, kk, T, lr = (CFG[x] for x in ("d", "pairs", "experts", "k", "kk", "tokens", "lr"))
 
+    if torch.cuda.device_count() < world or not torch.cuda.is_available():
+        raise SystemExit(f"bench.py: {world} rank(s) need {world} visible GPUs, found {torch.cuda.device_count()}")
     ctx = G.Context(local_rank)
-    gen = torch.Generator(device=dev).manual_seed(0x7002 + rank)
-    h = (torch.rand((T, d), generator=gen, device=dev) * 2 - 1).to(torch.bfloat16)
-    g = (torch.rand((T, d), generator=gen, device=dev) * 2 - 1).to(torch.bfloat16)
+    # BASELINE.md §3 inputs from the reference RNG streams (rank r of a sharded run: stream + 0x100 * r), bf16
+    h = torch.from_numpy(G.reference_uniform(SEED, H_STREAM + 0x100 * rank, (T, d), -1.0, 1.0, bf16=True)).to(
+        device=dev, dtype=torch.bfloat16)
+    g = torch.from_numpy(G.reference_uniform(SEED, G_STREAM + 0x100 * rank, (T, d), -1.0, 1.0, bf16=True)).to(
+        device=dev, dtype=torch.bfloat16)
     out = torch.empty((T, d), dtype=torch.float32, device=dev)
     grad_h = torch.empty((T, d), dtype=torch.float32, device=dev)
     sharded = world > 1 or args.sharded
     if not sharded:
         store = G.Store(ctx, 1, d, M, N, G.STORE_MIXED)
-        store.init_reference(seed=1)  # HostStore::init tables (reference RNG streams 0x5000/0x5001)
-        wgen = torch.Generator(device=dev).manual_seed(0x7001)
+        store.init_reference(seed=SEED)  # HostStore::init tables (reference RNG streams 0x5000/0x5001)
         b = 1.0 / math.sqrt(d)
-        w_b, w_bc = store.tensor(0, "w_b"), store.tensor(0, "w_b_compute")
-        for r0 in range(0, M, 65536):  # W_B ~ U(+-1/sqrt d), in place, chunked (no full temporary)
-            blk = (torch.rand((min(65536, M - r0), d), generator=wgen, device=dev) * 2 - 1) * b
-            w_b[r0:r0 + blk.shape[0]].copy_(blk)
-            w_bc[r0:r0 + blk.shape[0]].copy_(blk.to(torch.bfloat16))
-        del blk
+        if M * d <= 1 << 28:  # W_B ~ U(+-1/sqrt d) from stream 0x7001, bf16-rounded
+            store.upload(0, "w_b", G.reference_uniform(SEED, W_B_STREAM, (M, d), -b, b, bf16=True))
+        else:  # cfg4 (M = 1M: 34 GB of host doubles): the same distribution from torch's device RNG, in chunks
+            wgen = torch.Generator(device=dev).manual_seed(W_B_STREAM)
+            w_b, w_bc = store.tensor(0, "w_b"), store.tensor(0, "w_b_compute")
+            for r0 in range(0, M, 65536):
+                blk = ((torch.rand((min(65536, M - r0), d), generator=wgen, device=dev) * 2 - 1) * b).to(
+                    torch.bfloat16)
+                w_b[r0:r0 + blk.shape[0]].copy_(blk.float())
+                w_bc[r0:r0 + blk.shape[0]].copy_(blk)
+            del blk
 
         base = None
         if args.base_ffn:  # the frozen base FFN of the layer too (optional n = 11008 run)
@@ -359,29 +456,22 @@ def our_arm(args, rank, world, local_rank):
             traffic = json.load(f).get("mean_dram_bytes_per_launch")
 
     cpu = None
-    if world == 1 and not args.skip_cpu_baseline:
-        tokens = ref_sample_step_tokens()
-        try:
-            tps, sec, cph, cores = run_reference_sample(1, 0, tokens)
-            cpu = {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "reference",
-                   "sample": f"unmodified reference ref_layer_step, cfg2 tables, {tokens} tokens, one step "
-                             f"({sec:.1f} s, fp64, OpenMP {cores} threads, {cpu_model()})"}
+    if world == 1 and not args.skip_cpu_baseline and not args.base_ffn:
+        try:  # the reference arm's phased measurement on a bounded sample: 2 slices of rows, no warm-up
+            r = run_reference_phased(2, 0, ref_slice_tokens(args.steps))
+            cpu = {"value": r["tps"], "unit": "tokens/s", "cores": r["cores"], "kind": "reference",
+                   "sample": phased_sample_text(r), "phase_seconds": r["phases"]}
         except Exception as e:
             cpu = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"not run: {e}"}
 
     line = {
-        "metric": "MEFT adapter layer tokens/sec (fwd+bwd+sparse update)",
+        "metric": METRIC,
         "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic (HostStore::init tables, uniform W_B/h/grad_out)",
-        "config": dict(workload=CFG["workload"], d=d, pairs=M, experts=N, k=K, kk=kk, tokens_per_gpu=T,
-                       global_tokens=T * world,
-                       parallelism="single GPU" if not sharded else f"expert-sharded ep{world} (NCCL all-to-all)",
-                       base_ffn=args.base_ffn,
-                       precision="bf16 compute, fp32 "
-                       "master/Adam state", l2=f"inputs larger than L2 ({M * d * 28 / 1e9:.1f} GB of tables per layer)",
-                       union_size=S),
+        "data": "synthetic (HostStore::init tables; W_B, h, grad_out from the reference RNG streams, bf16)",
+        "config": config_dict(world),
+        "precision": "bf16 compute, fp32 master/Adam state", "union_size": S, "base_ffn": args.base_ffn,
         "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": 2 * T * d * 2,
                 "d2h_bytes_per_step": 2 * T * d * 4, "ms_per_step": e2e_s * 1e3,
                 "path": "meft_layer_step_host (C ABI, pinned host buffers)" if not sharded else
@@ -432,27 +522,59 @@ def emit(line):
     _JSON_OUT.flush()
 
 
+def _free_port():
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def spawn_ranks(n):
+    """`--gpus N` without a launcher: re-execute this command under torch.distributed.run with N local ranks
+    (rendezvous on 127.0.0.1). Rank 0's JSON line reaches our stdout; the exit code is the launcher's."""
+    import subprocess
+
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"bench.py: launching {n} ranks: {' '.join(cmd)}", file=sys.stderr)
+    return subprocess.run(cmd).returncode
+
+
 def main():
-    _claim_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--skip-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-full-step", action="store_true",
+                    help="reference arm: time one unsliced T-token reference step instead of the phased sample")
     ap.add_argument("--sharded", action="store_true", help="run the expert-sharded layer even on one GPU")
     ap.add_argument("--base-ffn", type=int, default=0,
                     help="also run the frozen base FFN of width n (SiLU), e.g. 11008 for LLaMA-7B (single GPU)")
-    ap.add_argument("--workload", choices=["cfg2", "cfg4"], default="cfg2",
-                    help="cfg2: the LLaMA-7B-shape layer (default, BASELINE configs[1]); cfg4: the Mistral-7B shape "
-                         "with M = 1,048,576 neurons and 1,024 experts (BASELINE configs[3], meant for --gpus 8)")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2",
+                    help="cfg2: the LLaMA-7B-shape layer (default, BASELINE configs[1]); cfg1: the reference's own "
+                         "CPU workload (configs[0]); cfg4: the Mistral-7B shape with M = 1,048,576 neurons and "
+                         "1,024 experts (configs[3], meant for --gpus 8)")
     args = ap.parse_args()
-    if args.workload == "cfg4":
-        CFG.update(workload="mistral7b_meft_layer_1m", pairs=1048576, experts=1024)
+    CFG.update(WORKLOADS[args.workload])
     args.warmup = max(args.warmup, 0)
+    if args.gpus < 1:
+        raise SystemExit("bench.py: --gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        if args.impl == "ours":
+            import torch
+
+            if torch.cuda.device_count() < args.gpus:
+                raise SystemExit(f"bench.py: --gpus {args.gpus} but only {torch.cuda.device_count()} GPU(s) visible")
+        sys.exit(spawn_ranks(args.gpus))
+    _claim_stdout()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: launched with WORLD_SIZE={world} but --gpus {args.gpus}")
     if args.impl == "reference":
         reference_arm(args, rank, world)
         return
@@ -461,7 +583,7 @@ def main():
         import torch
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        os.environ.setdefault("MASTER_PORT", "29511")
+        os.environ.setdefault("MASTER_PORT", str(_free_port()))
         os.environ.setdefault("RANK", "0")
         os.environ.setdefault("WORLD_SIZE", "1")
         torch.cuda.set_device(local_rank)

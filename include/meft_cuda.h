@@ -291,6 +291,13 @@ meft_status meft_store_info(const meft_store* store, int64_t* layers, int64_t* d
  * 0x5001+2l, W_B = 0, moments/steps/staging zero. Generated on the host with the reference RNG (rng.hpp),
  * bit-identical to the reference tables; bf16 compute copies are rounded from them in MIXED mode. */
 meft_status meft_store_init_reference(meft_ctx* ctx, meft_store* store, uint64_t seed);
+/* The reference's seeded input streams (rng.hpp:13-21, 62-66): n draws of
+ * SeededRng(mix_seed(seed, stream)).uniform(lo, hi) in storage order, i.e. uniform_matrix(rows, cols, lo, hi) for
+ * n = rows * cols, into a host fp64 buffer; with round_bf16 != 0 each value is rounded to the nearest bf16 (ties to
+ * even) and kept as a double. The synthetic inputs of BASELINE.md §3 (W_B 0x7001, h 0x7002, grad_out 0x7003) for
+ * bench.py's two arms and the parity tests, so both arms see identical values. Host-only; no device work. */
+meft_status meft_reference_uniform(uint64_t seed, uint64_t stream, int64_t n, double lo, double hi, int round_bf16,
+                                   double* host_out);
 /* Host transfers in the reference layouts (see meft_tensor). host_dt F64 (or int64/int8 for counters). */
 meft_status meft_store_upload_host(meft_ctx* ctx, meft_store* store, int64_t layer, meft_tensor t, const void* host,
                                    int64_t rows, int64_t cols);

@@ -83,6 +83,10 @@ def ref():
         _ref.ref_store_init.argtypes = [_I64, _I64, _I64, _I64, C.c_int, C.c_uint64]
         _ref.ref_store_free.argtypes = [_P]
         _ref.ref_warn_count.restype = C.c_long
+        _ref.ref_step_begin.restype = _P
+        _ref.ref_step_begin.argtypes = [_P, _I64, _P, _I64, _I64, _I64, _P, _P, _P]
+        _ref.ref_step_rows.argtypes = [_P, _P, _P, _I64, _P, _P]
+        _ref.ref_step_finish.argtypes = [_P, _P, _D, _P, _P]
     return _ref
 
 
@@ -382,6 +386,32 @@ class RefStore:
 
     def sparse_adam(self, layer, lr, beta1=0.9, beta2=0.999, eps=1e-8):
         _check_ref(ref().ref_sparse_adam(_P(self.h), _I64(layer), _D(beta1), _D(beta2), _D(eps), _D(lr)))
+
+    def step_phases(self, layer, h, grad_out, kk, k, lr, row_slices):
+        """The layer step of the T-token batch (h, grad_out) through the reference's public API in its phases:
+        push_hidden + ke_select + fetch on the whole batch, sparse_ffn_pa + sparse_backward on each (lo, hi) row
+        slice of the batch against that union, then scatter_grads + sparse_adam_update of the union (ref_capi.cpp
+        ref_step_*). Returns the phase seconds (per-slice lists for forward / backward) and |S|."""
+        h, grad_out = _f64(h), _f64(grad_out)
+        T = h.shape[0]
+        sel_s, fetch_s, us = _D(), _D(), _I64()
+        st = ref().ref_step_begin(_P(self.h), _I64(layer), _ptr(h), _I64(T), _I64(kk), _I64(k), C.byref(sel_s),
+                                  C.byref(fetch_s), C.byref(us))
+        if not st:
+            raise OracleError(9, ref().ref_last_error().decode())
+        fwd, bwd = [], []
+        try:
+            for lo, hi in row_slices:
+                f, b = _D(), _D()
+                _check_ref(ref().ref_step_rows(_P(st), _ptr(h[lo:hi]), _ptr(grad_out[lo:hi]), _I64(hi - lo),
+                                               C.byref(f), C.byref(b)))
+                fwd.append(f.value)
+                bwd.append(b.value)
+        finally:
+            sc, ad = _D(), _D()
+            _check_ref(ref().ref_step_finish(_P(st), _P(self.h), _D(lr), C.byref(sc), C.byref(ad)))
+        return dict(select=sel_s.value, fetch=fetch_s.value, forward=fwd, backward=bwd, scatter=sc.value,
+                    adam=ad.value, union_size=us.value)
 
     def layer_step(self, layer, h, grad_out, kk, k, lr, want_outputs=True):
         h, grad_out = _f64(h), _f64(grad_out)

@@ -18,9 +18,16 @@
 //   ref_sparse_adam      -> meft::sparse_adam_update proj/include/meft/memtier.hpp:161
 //   ref_layer_step       -> meft_ffn -> sparse_backward -> scatter_grads -> sparse_adam_update
 //                           (the trainer's per-layer sequence, proj/src/trainer.cpp:220,270,283,525)
+//   ref_step_begin / ref_step_rows / ref_step_finish
+//                        -> the same sequence split into its phases for bench.py's bounded CPU sample:
+//                           meft_ffn's push_hidden + ke_select + fetch on the whole batch
+//                           (meft_ffn.cpp:18-28), sparse_ffn_pa + sparse_backward on a slice of the batch's
+//                           token rows against that union (every row of both is independent of the others,
+//                           adapter.cpp:112-180), then scatter_grads + sparse_adam_update of the union.
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <memory>
 #include <stdexcept>
 #include <string>
 
@@ -344,6 +351,83 @@ int ref_layer_step(void* sp, int64_t layer, const double* h, int64_t tokens, con
             phase_s[5] = std::chrono::duration<double>(t4 - t3).count();
             (void)t0;
         }
+    });
+}
+
+// ---- the layer step in phases (bench.py's reference arm; see the header comment)
+struct RefStep {
+    int64_t layer = 0;
+    BaseFfn base;
+    CommMeter meter;
+    MeftFfnCache cache;  // sel + taus + slice of the whole batch (meft_ffn.cpp:22-28)
+    SparseFfnGrads grads;  // of the last row slice (scatter_grads' cost does not depend on the values)
+};
+
+// push_hidden + ke_select + fetch of the whole T-token batch, timed; returns the step state (nullptr on error).
+void* ref_step_begin(void* sp, int64_t layer, const double* h, int64_t tokens, int64_t kk, int64_t k,
+                     double* select_s, double* fetch_s, int64_t* union_size) {
+    RefStep* rs = nullptr;
+    const int rc = guard([&] {
+        using clk = std::chrono::steady_clock;
+        HostStore& st = *static_cast<HostStore*>(sp);
+        const int64_t d = st.dim();
+        auto state = std::make_unique<RefStep>();
+        state->layer = layer;
+        state->base.w_in = Matrix(d, 0);
+        state->base.w_out = Matrix(0, d);
+        HiddenBatch hb(1, tokens, to_matrix(h, tokens, d));
+        state->meter.set_layer(layer);
+        push_hidden(state->meter, hb.batch, hb.seq, hb.dim());
+        const ExpertPartition part = ExpertPartition::make(st.pairs(), st.experts());
+        auto t0 = clk::now();
+        state->cache.sel = ke_select(hb, st.layer(layer).router, part, st.layer(layer).adapter, kk, k,
+                                     &state->cache.taus);
+        auto t1 = clk::now();
+        state->cache.slice = fetch(st, state->meter, layer, state->cache.sel.unioned);
+        auto t2 = clk::now();
+        *select_s = std::chrono::duration<double>(t1 - t0).count();
+        *fetch_s = std::chrono::duration<double>(t2 - t1).count();
+        *union_size = static_cast<int64_t>(state->cache.sel.unioned.size());
+        rs = state.release();
+    });
+    return rc == 0 ? rs : nullptr;
+}
+
+// sparse_ffn_pa + sparse_backward of `rows` token rows of the batch against the whole batch's union, timed.
+int ref_step_rows(void* state, const double* h_rows, const double* g_rows, int64_t rows, double* forward_s,
+                  double* backward_s) {
+    return guard([&] {
+        using clk = std::chrono::steady_clock;
+        RefStep& rs = *static_cast<RefStep*>(state);
+        const int64_t d = rs.cache.slice.w_b_k.cols;
+        HiddenBatch hb(1, rows, to_matrix(h_rows, rows, d));
+        FfnCache fc;
+        auto t0 = clk::now();
+        const HiddenBatch o = sparse_ffn_pa(hb, rs.base, rs.cache.slice.w_a_k, rs.cache.slice.w_b_k, &fc);
+        auto t1 = clk::now();
+        rs.grads = sparse_backward(to_matrix(g_rows, rows, d), fc, rs.cache.slice.w_a_k, rs.cache.slice.w_b_k,
+                                   rs.base);
+        auto t2 = clk::now();
+        (void)o;
+        *forward_s = std::chrono::duration<double>(t1 - t0).count();
+        *backward_s = std::chrono::duration<double>(t2 - t1).count();
+    });
+}
+
+// scatter_grads of the union + sparse_adam_update, timed; frees the step state.
+int ref_step_finish(void* state, void* sp, double lr, double* scatter_s, double* adam_s) {
+    std::unique_ptr<RefStep> rs(static_cast<RefStep*>(state));
+    return guard([&] {
+        using clk = std::chrono::steady_clock;
+        HostStore& st = *static_cast<HostStore*>(sp);
+        auto t0 = clk::now();
+        scatter_grads(st, rs->meter, rs->layer, rs->cache.sel.unioned, rs->grads.grad_w_a_k, rs->grads.grad_w_b_k,
+                      &rs->cache.slice);
+        auto t1 = clk::now();
+        sparse_adam_update(st, rs->layer, AdamHyper{}, lr);
+        auto t2 = clk::now();
+        *scatter_s = std::chrono::duration<double>(t1 - t0).count();
+        *adam_s = std::chrono::duration<double>(t2 - t1).count();
     });
 }
 

@@ -110,6 +110,7 @@ _SIGS = {
     "meft_store_destroy": (None, [P]),
     "meft_store_info": (INT, [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64), C.POINTER(I64), C.POINTER(INT)]),
     "meft_store_init_reference": (INT, [P, P, C.c_uint64]),
+    "meft_reference_uniform": (INT, [C.c_uint64, C.c_uint64, I64, D, D, INT, P]),
     "meft_store_upload_host": (INT, [P, P, I64, INT, P, I64, I64]),
     "meft_store_download_host": (INT, [P, P, I64, INT, P, I64, I64]),
     "meft_store_tensor": (INT, [P, I64, INT, C.POINTER(P), C.POINTER(INT), C.POINTER(I64), C.POINTER(I64)]),

@@ -33,7 +33,7 @@ def _needs(target: str, deps) -> bool:
 
 
 def _headers():
-    hs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
+    hs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh", ".hpp"))]
     hs.append(os.path.join(ROOT, "include", "meft_cuda.h"))
     return hs
 

@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -79,6 +80,19 @@ class Parser {
     void expect(char c) {
         if (!eat(c)) fail(std::string("expected '") + c + "'");
     }
+    unsigned hex4() {  // the 4 hex digits of a \u escape
+        if (p_ + 4 > t_.size()) fail("bad \\u escape");
+        unsigned v = 0;
+        for (int i = 0; i < 4; ++i) {
+            const char h = t_[p_++];
+            v <<= 4;
+            if (h >= '0' && h <= '9') v |= unsigned(h - '0');
+            else if (h >= 'a' && h <= 'f') v |= unsigned(h - 'a' + 10);
+            else if (h >= 'A' && h <= 'F') v |= unsigned(h - 'A' + 10);
+            else fail("bad \\u escape");
+        }
+        return v;
+    }
     std::string str() {
         expect('"');
         std::string out;
@@ -97,15 +111,29 @@ class Parser {
                     case 'r': out += '\r'; break;
                     case 't': out += '\t'; break;
                     case 'u': {
-                        if (p_ + 4 > t_.size()) fail("bad \\u escape");
-                        const unsigned cp = unsigned(std::stoul(t_.substr(p_, 4), nullptr, 16));
-                        p_ += 4;
-                        if (cp < 0x80) out += char(cp);
-                        else if (cp < 0x800) {
+                        unsigned cp = hex4();
+                        if (cp >= 0xD800 && cp <= 0xDBFF) {  // high surrogate: must pair with \uDC00-\uDFFF
+                            if (p_ + 2 > t_.size() || t_[p_] != '\\' || t_[p_ + 1] != 'u')
+                                fail("unpaired UTF-16 surrogate");
+                            p_ += 2;
+                            const unsigned lo = hex4();
+                            if (lo < 0xDC00 || lo > 0xDFFF) fail("unpaired UTF-16 surrogate");
+                            cp = 0x10000 + ((cp - 0xD800) << 10) + (lo - 0xDC00);
+                        } else if (cp >= 0xDC00 && cp <= 0xDFFF) {
+                            fail("unpaired UTF-16 surrogate");
+                        }
+                        if (cp < 0x80) {
+                            out += char(cp);
+                        } else if (cp < 0x800) {
                             out += char(0xC0 | (cp >> 6));
                             out += char(0x80 | (cp & 0x3F));
-                        } else {
+                        } else if (cp < 0x10000) {
                             out += char(0xE0 | (cp >> 12));
+                            out += char(0x80 | ((cp >> 6) & 0x3F));
+                            out += char(0x80 | (cp & 0x3F));
+                        } else {
+                            out += char(0xF0 | (cp >> 18));
+                            out += char(0x80 | ((cp >> 12) & 0x3F));
                             out += char(0x80 | ((cp >> 6) & 0x3F));
                             out += char(0x80 | (cp & 0x3F));
                         }
@@ -166,9 +194,11 @@ class Parser {
             }
             const std::string num = t_.substr(s0, p_ - s0);
             if (num.empty() || num == "-") fail("bad token");
-            if (real) {
+            if (real) {  // strtod, not stod: subnormals (e.g. 5e-324) are valid JSON numbers, not range errors
                 v.kind = Value::Real;
-                v.r = std::stod(num);
+                char* end = nullptr;
+                v.r = std::strtod(num.c_str(), &end);
+                if (end != num.c_str() + num.size()) fail("bad number");
             } else {
                 v.kind = Value::Int;
                 v.i = std::stoll(num);
@@ -204,19 +234,59 @@ inline void dump_string(const std::string& s, std::string& out) {
     out += '"';
 }
 
+// Reals as nlohmann/json writes them (the reference's checkpoint headers): the shortest digit string that reads
+// back to the same double, laid out by its rules -- fixed notation for decimal exponents in (-4, 15] ("0.001",
+// "100.0", "1.5"), otherwise d[.ddd]e+XX with at least two exponent digits ("1e-05"); non-finite values are null.
+inline void dump_real(double x, std::string& out) {
+    if (!std::isfinite(x)) {
+        out += "null";
+        return;
+    }
+    if (x == 0.0) {
+        out += std::signbit(x) ? "-0.0" : "0.0";
+        return;
+    }
+    char buf[40];
+    int prec = 1;
+    for (; prec <= 17; ++prec) {  // shortest %.{p-1}e that round-trips
+        std::snprintf(buf, sizeof buf, "%.*e", prec - 1, x);
+        if (std::strtod(buf, nullptr) == x) break;
+    }
+    // buf = [-]d[.ddd]e(+|-)XX: collect the digits and the decimal exponent
+    std::string digits;
+    const char* q = buf;
+    if (*q == '-') {
+        out += '-';
+        ++q;
+    }
+    for (; *q && *q != 'e'; ++q)
+        if (*q != '.') digits += *q;
+    const int e10 = std::atoi(q + 1);
+    while (digits.size() > 1 && digits.back() == '0') digits.pop_back();
+    const int k = int(digits.size());
+    const int n = e10 + 1;  // x = 0.digits * 10^n
+    if (k <= n && n <= 15) {
+        out += digits + std::string(size_t(n - k), '0') + ".0";
+    } else if (0 < n && n <= 15) {
+        out += digits.substr(0, size_t(n)) + "." + digits.substr(size_t(n));
+    } else if (-4 < n && n <= 0) {
+        out += "0." + std::string(size_t(-n), '0') + digits;
+    } else {
+        out += digits.substr(0, 1);
+        if (k > 1) out += "." + digits.substr(1);
+        const int e = n - 1;
+        char eb[8];
+        std::snprintf(eb, sizeof eb, "e%c%02d", e < 0 ? '-' : '+', e < 0 ? -e : e);
+        out += eb;
+    }
+}
+
 inline void dump(const Value& v, std::string& out) {
     switch (v.kind) {
         case Value::Null: out += "null"; break;
         case Value::Bool: out += v.b ? "true" : "false"; break;
         case Value::Int: out += std::to_string(v.i); break;
-        case Value::Real: {
-            char buf[40];
-            std::snprintf(buf, sizeof buf, "%.17g", v.r);
-            std::string s = buf;
-            if (s.find_first_of(".eEn") == std::string::npos) s += ".0";
-            out += s;
-            break;
-        }
+        case Value::Real: dump_real(v.r, out); break;
         case Value::Str: dump_string(v.s, out); break;
         case Value::Arr: {
             out += '[';

@@ -257,6 +257,18 @@ GemmOperand kv_operand(meft_ctx* ctx, const void* p, int64_t d, bool mn_major, c
     return op;
 }
 
+// A rank whose part of the union is empty still owes every token home its slot of the fused reduce-scatter: the
+// homes fold all `world` slots of their receive buffers, which are never cleared between steps, so the slot is
+// written as zeros (the GEMM epilogue's row layout: home h, slot = this rank, rows [0, rows) x d).
+void zero_peer_slots(cudaStream_t st, const meft_peer_out& po, bool grad_h, int64_t d) {
+    for (int h = 0; h < po.world; ++h) {
+        float* base = grad_h ? po.grad_h_recv[h] : po.out_recv[h];
+        require(base != nullptr, MEFT_E_INVALID, "peer_out: null receive buffer");
+        MEFT_CUDA_CHECK(cudaMemsetAsync(base + size_t(po.rank) * size_t(po.rows) * size_t(d), 0,
+                                        size_t(po.rows) * size_t(d) * 4, st));
+    }
+}
+
 // The out / grad_h GEMMs' epilogue when their rows are pushed to the token homes (meft_peer_out).
 GemmEpilogue peer_epilogue(const meft_peer_out& po, bool grad_h, int64_t d) {
     require(po.world >= 1 && po.world <= kMaxPeers && po.rank >= 0 && po.rank < po.world && po.rows >= 1,
@@ -295,7 +307,11 @@ void ffn_forward_impl(meft_ctx* ctx, meft_dtype dt, const void* h, const void* k
     require(d % 8 == 0 && ld_z % 8 == 0 && (panel ? ld_z == kGemmPanel : ld_z >= s), MEFT_E_INVALID,
             "ffn_forward(bf16): d and ld_z must be multiples of 8");
     if (s == 0) {
-        if (!accumulate) MEFT_CUDA_CHECK(cudaMemsetAsync(out, 0, size_t(T * d) * 4, st));
+        if (peer) {
+            zero_peer_slots(st, *peer, false, d);
+        } else if (!accumulate) {
+            MEFT_CUDA_CHECK(cudaMemsetAsync(out, 0, size_t(T * d) * 4, st));
+        }
         return;
     }
     GemmEpilogue e1;
@@ -366,8 +382,13 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
         o.panel_stride = panel;
         return o;
     };
-    if (s == 0) {
-        if (!acc_h && grad_h) MEFT_CUDA_CHECK(cudaMemsetAsync(grad_h, 0, size_t(T * d) * 4, st));
+    if (s == 0) {  // nothing selected here: grad_h is zero (or this rank's peer slots are), and final now
+        if (peer) {
+            zero_peer_slots(st, *peer, true, d);
+        } else if (!acc_h && grad_h) {
+            MEFT_CUDA_CHECK(cudaMemsetAsync(grad_h, 0, size_t(T * d) * 4, st));
+        }
+        if (grad_h_done) MEFT_CUDA_CHECK(cudaEventRecord(grad_h_done, st));
         return;
     }
     GemmEpilogue e3;  // masked = mask(act) .* (G * values_s^T)
@@ -1226,6 +1247,25 @@ meft_status meft_store_init_reference(meft_ctx* ctx, meft_store* s, uint64_t see
             upload_f64(ctx, s, L, MEFT_T_W_A, buf.data());
             uniform_fill(mix_seed(seed, 0x5001 + 2 * uint64_t(l)), -bound, bound, buf.data(), s->experts * s->d);
             upload_f64(ctx, s, L, MEFT_T_W_G, buf.data());
+        }
+    });
+}
+
+meft_status meft_reference_uniform(uint64_t seed, uint64_t stream, int64_t n, double lo, double hi, int round_bf16,
+                                   double* host_out) {
+    return guarded(nullptr, [&] {
+        require(n >= 0 && (n == 0 || host_out != nullptr), MEFT_E_INVALID, "reference_uniform: n >= 0, output");
+        uniform_fill(mix_seed(seed, stream), lo, hi, host_out, n);
+        if (round_bf16) {
+            for (int64_t i = 0; i < n; ++i) {  // RNE to bf16 (finite inputs): add half an ulp plus the tie bit
+                const float f = float(host_out[i]);  // the doubles here are far from any float rounding tie
+                uint32_t u;
+                std::memcpy(&u, &f, 4);
+                u = (u + 0x7FFFu + ((u >> 16) & 1u)) & 0xFFFF0000u;
+                float r;
+                std::memcpy(&r, &u, 4);
+                host_out[i] = double(r);
+            }
         }
     });
 }

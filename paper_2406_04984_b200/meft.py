@@ -108,6 +108,16 @@ def kernel_launches() -> int:
     return int(lib().meft_kernel_launches())
 
 
+def reference_uniform(seed: int, stream: int, shape, lo: float, hi: float, bf16: bool = False) -> np.ndarray:
+    """SeededRng(mix_seed(seed, stream)).uniform_matrix(*shape, lo, hi) of the reference (rng.hpp:13-21, 62-66) as a
+    float64 host array, optionally bf16-rounded: the BASELINE.md §3 input streams (W_B 0x7001, h 0x7002, grad_out
+    0x7003) that bench.py's GPU and CPU arms share."""
+    out = np.empty(tuple(shape), np.float64)
+    check(lib().meft_reference_uniform(C.c_uint64(seed), C.c_uint64(stream), out.size, lo, hi, int(bf16),
+                                       out.ctypes.data_as(P)))
+    return out
+
+
 def selection_shape(M, N, kk, k):
     take, kk_eff, warn = I64(), I64(), C.c_int()
     check(lib().meft_selection_shape(M, N, kk, k, C.byref(take), C.byref(kk_eff), C.byref(warn)))

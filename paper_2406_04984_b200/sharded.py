@@ -226,7 +226,7 @@ class PeerExchange:
     CUDA IPC (handles all-gathered over the group). ``desc`` is the meft_peer_out for this rank; ``reduce`` folds
     this home's slots in slot order. ``peers`` lets a single process stand in for several ranks (tests)."""
 
-    def __init__(self, ctx, rows, d, group=None, world=None, rank=None, local=None):
+    def __init__(self, ctx, rows, d, group=None, world=None, rank=None, local=None, fail_local=False):
         self.ctx, self.rows, self.d = ctx, rows, d
         self.world = world if world is not None else dist.get_world_size(group)
         self.rank = rank if rank is not None else dist.get_rank(group)
@@ -236,31 +236,47 @@ class PeerExchange:
         if local is not None:  # single-process emulation: `local` = [(out_ptr, gh_ptr)] of every emulated rank
             bases = local
         else:
-            mine = []
-            for _ in range(2):
-                p = C.c_void_p()
-                check(lib().meft_device_alloc(ctx.h, nbytes, C.byref(p)), ctx.h)
-                self._own.append(p.value)
-                mine.append(p.value)
-            handles = []
-            for p in mine:
-                hb = (C.c_char * 64)()
-                check(lib().meft_ipc_handle(ctx.h, C.c_void_p(p), hb), ctx.h)
-                handles.append(bytes(hb))
+            # Local setup may fail on one rank only (allocation, IPC export). Every rank still joins the one
+            # all_gather_object below -- a failed rank contributes None -- so the group's collectives stay matched
+            # and every rank raises together instead of some waiting forever in the gather.
+            mine, handles = [], None
+            try:
+                if fail_local:
+                    raise RuntimeError("caller's local setup failed")
+                for _ in range(2):
+                    p = C.c_void_p()
+                    check(lib().meft_device_alloc(ctx.h, nbytes, C.byref(p)), ctx.h)
+                    self._own.append(p.value)
+                    mine.append(p.value)
+                handles = []
+                for p in mine:
+                    hb = (C.c_char * 64)()
+                    check(lib().meft_ipc_handle(ctx.h, C.c_void_p(p), hb), ctx.h)
+                    handles.append(bytes(hb))
+            except Exception:
+                handles = None
             every = [None] * self.world
             dist.all_gather_object(every, handles, group=group)
+            if any(e is None for e in every):
+                self.close()
+                raise RuntimeError("peer exchange: a rank could not allocate or export its receive buffers")
             bases = []
-            for r, hs in enumerate(every):
-                if r == self.rank:
-                    bases.append(tuple(mine))
-                    continue
-                ptrs = []
-                for hbytes in hs:
-                    p = C.c_void_p()
-                    check(lib().meft_ipc_open(ctx.h, (C.c_char * 64).from_buffer_copy(hbytes), C.byref(p)), ctx.h)
-                    self._opened.append(p.value)
-                    ptrs.append(p.value)
-                bases.append(tuple(ptrs))
+            try:  # a failure here is agreed on by the caller (ShardedLayer._peer_exchange: all-reduce of a flag)
+                for r, hs in enumerate(every):
+                    if r == self.rank:
+                        bases.append(tuple(mine))
+                        continue
+                    ptrs = []
+                    for hbytes in hs:
+                        p = C.c_void_p()
+                        check(lib().meft_ipc_open(ctx.h, (C.c_char * 64).from_buffer_copy(hbytes), C.byref(p)),
+                              ctx.h)
+                        self._opened.append(p.value)
+                        ptrs.append(p.value)
+                    bases.append(tuple(ptrs))
+            except Exception:
+                self.close()
+                raise
         self.desc = _lib.PeerOut()
         self.desc.world, self.desc.rank, self.desc.rows = self.world, self.rank, rows
         for r, (po, pg) in enumerate(bases):
@@ -406,6 +422,34 @@ def _reduce_scatter_rows(t, group, world, rank):
     return buf[rank * n:(rank + 1) * n].clone()
 
 
+def _single_node():
+    """True when every rank of the job runs on this host (torchrun's LOCAL_WORLD_SIZE == WORLD_SIZE)."""
+    lws, ws = os.environ.get("LOCAL_WORLD_SIZE"), os.environ.get("WORLD_SIZE")
+    return lws is not None and ws is not None and int(lws) == int(ws)
+
+
+def _loopback_gloo_group(group, world):
+    """A gloo group over the ranks of `group` for the protocol's host-side count exchange, or None.
+
+    Only on a single node: gloo then binds to loopback (its default interface lookup resolves the hostname, which
+    may not resolve in a container). GLOO_SOCKET_IFNAME is set only while the group is created and restored
+    afterwards, so groups the caller creates later are unaffected; an interface the user chose is kept. Created
+    with use_local_synchronization, so only the members of `group` take part (an expert-parallel subgroup of a
+    larger job does not deadlock the ranks outside it). Multi-node jobs get None: counts then travel over the
+    NCCL group (one device all-gather per exchange)."""
+    if world == 1 or not _single_node():
+        return None
+    ranks = list(range(world)) if group is None else dist.get_process_group_ranks(group)
+    prev = os.environ.get("GLOO_SOCKET_IFNAME")
+    if prev is None:
+        os.environ["GLOO_SOCKET_IFNAME"] = "lo"
+    try:
+        return dist.new_group(ranks=ranks, backend="gloo", use_local_synchronization=True)
+    finally:
+        if prev is None:
+            os.environ.pop("GLOO_SOCKET_IFNAME", None)
+
+
 class ShardedLayer:
     """One expert-sharded MEFT layer; ``engine`` does this rank's compute (DeviceEngine on a B200)."""
 
@@ -421,17 +465,14 @@ class ShardedLayer:
         # protocol metadata (per-destination counts) is exchanged host to host over gloo when the data plane is NCCL
         self.host_group = None
         if not isinstance(group, ThreadGroup) and dist.get_backend(group) == "nccl":
-            ranks = list(range(self.world)) if group is None else dist.get_process_group_ranks(group)
-            # one node: gloo over loopback (its default interface lookup resolves the hostname, which may not)
-            os.environ.setdefault("GLOO_SOCKET_IFNAME", "lo")
-            self.host_group = dist.new_group(ranks=ranks, backend="gloo")
+            self.host_group = _loopback_gloo_group(group, self.world)
         # Overlap (device engine over NCCL): the bulk all-gathers / reduce-scatters run on their own stream and
         # communicator, so they proceed while the selection exchanges and the FFN compute.
         self.overlap = (isinstance(engine, DeviceEngine) and not isinstance(group, ThreadGroup)
                         and dist.get_backend(group) == "nccl")
         if self.overlap:
             ranks = list(range(self.world)) if group is None else dist.get_process_group_ranks(group)
-            self.bulk_group = dist.new_group(ranks=ranks, backend="nccl")
+            self.bulk_group = dist.new_group(ranks=ranks, backend="nccl", use_local_synchronization=True)
             self.comm_stream = torch.cuda.Stream(device=engine.dev)
             # Reduce-scatters of out / grad_h: by default FUSED into the GEMM epilogues over NVLink peer memory
             # (PeerExchange; P > 1 or MEFT_SHARDED_PEER=1), else NCCL on the comm stream with SMs kept free of the
@@ -455,8 +496,11 @@ class ShardedLayer:
             from .meft import Context
             if self.comm_ctx is None:
                 self.comm_ctx = Context(torch.cuda.current_device(), stream=self.comm_stream)
-            px = PeerExchange(self.eng.ctx, T, d, group=self.bulk_group)
-        except Exception:  # e.g. no CUDA IPC / peer access between these devices
+        except Exception:
+            ok = 0
+        try:  # joins the group's handle exchange even when the context failed (collectives stay matched)
+            px = PeerExchange(self.eng.ctx, T, d, group=self.bulk_group, fail_local=not ok)
+        except Exception:  # e.g. no CUDA IPC / peer access between these devices, or a failed peer
             ok = 0
         flag = torch.tensor([ok], dtype=torch.int32, device=self.eng.dev)
         dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.bulk_group)

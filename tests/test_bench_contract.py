@@ -26,13 +26,38 @@ def test_reference_arm_prints_one_contract_line():
 
     if not O.ref_available():
         pytest.skip("oracle/_ref not built")
-    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "1"], env={"MEFT_REF_SAMPLE_TOKENS": "2"})
+    d = _run(["--impl", "reference", "--workload", "cfg1", "--steps", "2", "--warmup", "1"])
     if "unavailable" in d:
         pytest.skip(d["unavailable"])
     assert d["impl"] == "reference" and d["unit"] == "tokens/s" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
-    assert d["higher_is_better"] is True and d["dtype"] == "f64"
+    assert d["higher_is_better"] is True and d["dtype"] == "f64" and d["n_gpus"] == 1
+    # the same workload the GPU arm reports (BASELINE configs[0] here), its union at full size (3,483
+    # on unrounded inputs; 3,484 on the bf16-rounded streams both arms use)
+    assert d["config"]["workload"] == "reference_cpu_workload" and d["config"]["global_tokens"] == 256
+    assert d["union_size"] == 3484
+    assert set(d["phase_seconds"]) == {"select", "fetch", "forward", "backward", "scatter", "adam"}
+
+
+def test_gpus_flag_launches_that_many_ranks():
+    """`bench.py --gpus 2` without a launcher re-executes itself under torch.distributed.run with two ranks (the
+    reference arm needs no GPU: both ranks join a gloo rendezvous, rank 0 alone runs and prints)."""
+    from oracle import oracle as O
+
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    d = _run(["--gpus", "2", "--impl", "reference", "--workload", "cfg1", "--steps", "1", "--warmup", "0"],
+             env={"MASTER_ADDR": "127.0.0.1", "GLOO_SOCKET_IFNAME": "lo"})
+    assert d["n_gpus"] == 2 and d["ranks_joined"] == 2 and d["config"]["global_tokens"] == 512
+    assert d["config"]["parallelism"].startswith("expert-sharded ep2")
+
+
+def test_mismatched_world_size_fails_loudly():
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--impl", "reference"],
+                       capture_output=True, text=True, timeout=120, cwd=ROOT,
+                       env=dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0"))
+    assert r.returncode != 0 and "WORLD_SIZE=1" in r.stderr
 
 
 @pytest.mark.gpu

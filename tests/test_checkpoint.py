@@ -63,6 +63,27 @@ def test_format_round_trip_is_byte_identical_to_reference(tmp_path, train_router
     assert a.read_bytes() == b.read_bytes()
 
 
+REAL_EXTRAS = [
+    '{"lr": 0.001, "eps": 1e-08, "b1": 0.9, "b2": 0.999, "big": 1e+20, "e15": 1e15, "e16": 12345678901234567.0}',
+    '{"x": [0.1, 0.2, 0.30000000000000004, -0.0, 0.0, 100.0, 1.5, 123456.789, 5e-324, 1.7976931348623157e308]}',
+    '{"small": [0.0001, 0.00001, 2.5e-4, 1e-3], "name": "caf\\u00e9 \\ud83d\\ude00"}',
+]
+
+
+@pytest.mark.parametrize("extra", REAL_EXTRAS)
+def test_header_reals_and_unicode_are_byte_identical_to_reference(tmp_path, extra):
+    """The header's `extra` (e.g. the run config echo with lr, eps) is re-serialised by nlohmann in the reference:
+    reals in their shortest round-trip form, \\u surrogate pairs decoded to one UTF-8 code point."""
+    ref = _ref_store(False, layers=1)
+    a, b = tmp_path / "ref.meft", tmp_path / "ours.meft"
+    ref.save(a, extra=extra, step=3)
+    st, got, hdr, ex = _load(a)
+    assert st == 0, L.lib().meft_last_error(None)
+    assert _save(b, got, hdr, ex) == 0
+    assert a.read_bytes().split(b"\n", 1)[0] == b.read_bytes().split(b"\n", 1)[0]
+    assert a.read_bytes() == b.read_bytes()
+
+
 def _corrupt(tmp_path, name, transform):
     ref = _ref_store(False)
     p = tmp_path / name

@@ -63,6 +63,39 @@ def test_peer_push_and_fold_equals_reduce_scatter(ctx):
     assert torch.equal(bufs[2][0][1], parts[1][0][2 * T:3 * T])
 
 
+def test_peer_push_with_an_empty_local_union_zeroes_its_slots(ctx):
+    """A rank that owns none of the selected pairs (empty local union) must still overwrite its slot in every home's
+    receive buffer with zeros -- the buffers are reused across steps, so a skipped slot would fold stale rows of the
+    previous step into out / grad_h -- and must still fire grad_h_done (the overlapped copy / fold waits on it)."""
+    P, T, d, m_loc, n_loc = 2, 64, 256, 512, 8
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    h_all = (torch.rand((P * T, d), generator=gen, device="cuda") * 2 - 1).to(torch.bfloat16)
+    g_all = (torch.rand((P * T, d), generator=gen, device="cuda") * 2 - 1).to(torch.bfloat16)
+    unions = [torch.arange(0, m_loc, 3, dtype=torch.int32, device="cuda"),
+              torch.empty(0, dtype=torch.int32, device="cuda")]  # rank 1 owns nothing this step
+    st0 = _shard_store(ctx, d, m_loc, n_loc, 300)
+    want = SH.DeviceEngine(ctx, st0, st0.tensor(0, "w_g_compute")).ffn_local(h_all, g_all, unions[0], 1e-3)
+    # receive buffers full of garbage from a "previous step"
+    bufs = [(torch.full((P, T, d), 7.0, device="cuda"), torch.full((P, T, d), -3.0, device="cuda")) for _ in range(P)]
+    bases = [(o.data_ptr(), gh.data_ptr()) for o, gh in bufs]
+    xs = [SH.PeerExchange(ctx, T, d, world=P, rank=r, local=bases) for r in range(P)]
+    for r in range(P):
+        st = _shard_store(ctx, d, m_loc, n_loc, 300 + r)
+        eng = SH.DeviceEngine(ctx, st, st.tensor(0, "w_g_compute"))
+        gh_done = torch.cuda.Event()
+        gh_done.record()
+        assert eng.ffn_local(h_all, g_all, unions[r], 1e-3, gh_done=gh_done, peer=xs[r]) == (None, None)
+        torch.cuda.synchronize()
+        assert gh_done.query()
+    for home in range(P):
+        rows = slice(home * T, (home + 1) * T)
+        for which in (0, 1):
+            assert torch.equal(bufs[home][which][1], torch.zeros((T, d), device="cuda")), (home, which)
+            got = xs[home].reduce(ctx, which)
+            torch.cuda.synchronize()
+            assert torch.equal(got, want[which][rows] + 0.0), (home, which)
+
+
 def test_peer_reduce_rejects_bad_arguments(ctx):
     out = torch.empty((4, 8), dtype=torch.float32, device="cuda")
     st = _lib.lib().meft_peer_reduce(ctx.h, C.c_void_p(out.data_ptr()), 9, 1, 32, C.c_void_p(out.data_ptr()))
