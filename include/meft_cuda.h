@@ -49,8 +49,11 @@ typedef enum meft_status {
 typedef enum meft_dtype { MEFT_F64 = 0, MEFT_F32 = 1, MEFT_BF16 = 2 } meft_dtype;
 
 /* Store precision. F64 mirrors the reference HostStore bit for bit (API-fidelity mode); MIXED keeps fp32
- * master weights / Adam moments / staging plus bf16 compute copies (the performance mode). */
-typedef enum meft_precision { MEFT_STORE_F64 = 0, MEFT_STORE_MIXED = 1 } meft_precision;
+ * master weights / Adam moments / staging plus bf16 compute copies (the performance mode). COMPACT is MIXED with
+ * the Adam moments m, v stored in bf16 (round to nearest even after every update; the update itself runs in fp32):
+ * 20 bytes of tables per (pair, dim) instead of 28, so BASELINE config 3 (32 LLaMA-7B-width layers) fits one
+ * B200. Opt-in; its Adam tolerance is stated in DESIGN.md §5 and pinned by tests/test_gpu_compact.py. */
+typedef enum meft_precision { MEFT_STORE_F64 = 0, MEFT_STORE_MIXED = 1, MEFT_STORE_COMPACT = 2 } meft_precision;
 
 /* Per-layer store tensors (HostLayer, memtier.hpp:90-106). Reference layouts for _host transfers:
  * W_A, M_A, V_A, STAGE_A are d x r; W_B, M_B, V_B, STAGE_B are r x d; W_G is N x d; PAIR_STEP is int64[r];

@@ -123,7 +123,7 @@ _SIGS = {
 }
 
 F64, F32, BF16 = 0, 1, 2
-STORE_F64, STORE_MIXED = 0, 1
+STORE_F64, STORE_MIXED, STORE_COMPACT = 0, 1, 2
 
 TENSORS = {"w_a": 0, "w_b": 1, "w_g": 2, "m_a": 3, "v_a": 4, "m_b": 5, "v_b": 6, "stage_a": 7, "stage_b": 8,
            "pair_step": 9, "staged": 10, "w_a_compute": 11, "w_b_compute": 12, "w_g_compute": 13, "m_g": 14,

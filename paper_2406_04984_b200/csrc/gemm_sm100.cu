@@ -70,14 +70,17 @@ struct KArgs {
     int peer_slot;
     // EPI_ADAM_F32 (see kernels.h)
     float* adam_w;
-    float* adam_m;
-    float* adam_v;
+    void* adam_m;  // fp32, or bf16 when mom16
+    void* adam_v;
+    int mom16;
     uint16_t* adam_c;
     const float2* adam_coef;
     float b1, b2, eps;
     double* stat_ss;
     int32_t* stat_lsb;
     long long stat_ld;
+    // L2 eviction priority of the A / B TMA loads (GemmOperand::l2_hint)
+    int hint_a, hint_b;
 };
 
 __device__ __forceinline__ int gather_row(const KArgs& a, int p) {
@@ -412,10 +415,31 @@ __device__ __forceinline__ float4 ld_shared_f4(uint32_t addr) {
 #define ADAM_LD(p) (*(p))
 #define ADAM_ST(p, v) (*(p) = (v))
 #endif
+// Adam moments of 4 consecutive entries at element offset `off`: fp32 tables, or bf16 ones (COMPACT stores; rounded
+// to nearest even on store).
+template <bool MOM16>
+__device__ __forceinline__ float4 adam_ld_mom(const void* base, long long off) {
+    if (MOM16) {
+        const uint2 u = ADAM_LD(reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(base) + off));
+        return make_float4(bf16_bits_to_f32(uint16_t(u.x)), bf16_bits_to_f32(uint16_t(u.x >> 16)),
+                           bf16_bits_to_f32(uint16_t(u.y)), bf16_bits_to_f32(uint16_t(u.y >> 16)));
+    }
+    return ADAM_LD(reinterpret_cast<const float4*>(static_cast<const float*>(base) + off));
+}
+template <bool MOM16>
+__device__ __forceinline__ void adam_st_mom(void* base, long long off, float4 v) {
+    if (MOM16) {
+        ADAM_ST(reinterpret_cast<uint2*>(static_cast<uint16_t*>(base) + off),
+                make_uint2(pack_bf16x2(f32_to_bf16_bits(v.x), f32_to_bf16_bits(v.y)),
+                           pack_bf16x2(f32_to_bf16_bits(v.z), f32_to_bf16_bits(v.w))));
+    } else {
+        ADAM_ST(reinterpret_cast<float4*>(static_cast<float*>(base) + off), v);
+    }
+}
 constexpr int ADAM_SCRATCH_LD = 36;  // floats per scratch row (16-byte aligned, conflict-free quarter-warp phases)
 constexpr int ADAM_SCRATCH_BYTES = 4 * 32 * ADAM_SCRATCH_LD * 4;
 
-template <bool STATS>
+template <bool STATS, bool MOM16>
 __device__ __forceinline__ void adam_tile_transposed(const KArgs& a, uint32_t taddr, int m0, int n_col0, float* sw,
                                                      int lane) {
     const int mrow = m0 + lane;
@@ -448,8 +472,8 @@ __device__ __forceinline__ void adam_tile_transposed(const KArgs& a, uint32_t ta
         for (int it = 0; it < 8; ++it) {  // invalid rows (past M: j < 0) read row 0 and never store
             const long long off = (long long)max(j[it], 0) * a.ldc + n + c4;
             w[it] = ADAM_LD(reinterpret_cast<const float4*>(a.adam_w + off));
-            m[it] = ADAM_LD(reinterpret_cast<const float4*>(a.adam_m + off));
-            v[it] = ADAM_LD(reinterpret_cast<const float4*>(a.adam_v + off));
+            m[it] = adam_ld_mom<MOM16>(a.adam_m, off);
+            v[it] = adam_ld_mom<MOM16>(a.adam_v, off);
         }
         tmem_ld_wait();
         const uint32_t sbase = smem_u32(sw);
@@ -466,8 +490,8 @@ __device__ __forceinline__ void adam_tile_transposed(const KArgs& a, uint32_t ta
             if (j[it] >= 0) {
                 const long long off = (long long)j[it] * a.ldc + n + c4;
                 ADAM_ST(reinterpret_cast<float4*>(a.adam_w + off), w[it]);
-                ADAM_ST(reinterpret_cast<float4*>(a.adam_m + off), m[it]);
-                ADAM_ST(reinterpret_cast<float4*>(a.adam_v + off), v[it]);
+                adam_st_mom<MOM16>(a.adam_m, off, m[it]);
+                adam_st_mom<MOM16>(a.adam_v, off, v[it]);
                 *reinterpret_cast<uint2*>(a.adam_c + off) = cb;
             }
         }
@@ -494,6 +518,7 @@ __device__ __forceinline__ void adam_tile_transposed(const KArgs& a, uint32_t ta
 }
 
 // 1-CTA kernel (small problems): thread = accumulator row, same arithmetic without the transpose.
+template <bool MOM16>
 __device__ __forceinline__ void adam_tile_rows(const KArgs& a, uint32_t taddr, int m, int n_col0) {
     const bool ok = m < a.M;
     const int j = ok ? __ldg(a.row_idx + m) : 0;
@@ -513,14 +538,14 @@ __device__ __forceinline__ void adam_tile_rows(const KArgs& a, uint32_t taddr, i
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             float4 w = reinterpret_cast<const float4*>(a.adam_w + off)[q];
-            float4 mm = reinterpret_cast<const float4*>(a.adam_m + off)[q];
-            float4 v = reinterpret_cast<const float4*>(a.adam_v + off)[q];
+            float4 mm = adam_ld_mom<MOM16>(a.adam_m, off + 4 * q);
+            float4 v = adam_ld_mom<MOM16>(a.adam_v, off + 4 * q);
             const float4 g = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
                                          __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
             const uint2 cb = adam4<true>(w, mm, v, g, a, k, ss, lsb);
             reinterpret_cast<float4*>(a.adam_w + off)[q] = w;
-            reinterpret_cast<float4*>(a.adam_m + off)[q] = mm;
-            reinterpret_cast<float4*>(a.adam_v + off)[q] = v;
+            adam_st_mom<MOM16>(a.adam_m, off + 4 * q, mm);
+            adam_st_mom<MOM16>(a.adam_v, off + 4 * q, v);
             reinterpret_cast<uint2*>(a.adam_c + off)[q] = cb;
         }
     }
@@ -585,6 +610,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (warp == 0) {
         // ------------------------------------------------ TMA producer (lane 0; all lanes for gathered B rows)
         const bool gather = args.b_idx != nullptr;
+        const uint64_t pol_a = l2_policy(args.hint_a), pol_b = l2_policy(args.hint_b);
         int stage = 0;
         uint32_t phase = 0;
         int gn[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // K-major gathered B: the NEXT tile's rows (prefetched)
@@ -617,21 +643,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 if (lane == 0) {
                     mbar_wait(empty + stage, phase ^ 1);
                     mbar_arrive_expect_tx(full + stage, STAGE_BYTES);
+                    auto ld_a = [&](void* dst, int c0, int c1) {
+                        if (args.hint_a) tma_load_2d_hint(dst, &tmA, full + stage, c0, c1, pol_a);
+                        else tma_load_2d(dst, &tmA, full + stage, c0, c1);
+                    };
+                    auto ld_b = [&](void* dst, int c0, int c1) {
+                        if (args.hint_b) tma_load_2d_hint(dst, &tmB, full + stage, c0, c1, pol_b);
+                        else tma_load_2d(dst, &tmB, full + stage, c0, c1);
+                    };
                     if (!A_MN) {
-                        tma_load_2d(sa, &tmA, full + stage, k0, m0);
+                        ld_a(sa, k0, m0);
                     } else {
 #pragma unroll
-                        for (int j = 0; j < BM / 64; ++j)
-                            tma_load_2d(sa + j * 8192, &tmA, full + stage, m0 + 64 * j, k0);
+                        for (int j = 0; j < BM / 64; ++j) ld_a(sa + j * 8192, m0 + 64 * j, k0);
                     }
                     if (!gather || run >= 0) {  // plain box (gathered B: at the run's table row)
                         const int brow = gather ? run : (B_MN ? k0 : n0);
                         if (!B_MN) {
-                            tma_load_2d(sb, &tmB, full + stage, k0, brow);
+                            ld_b(sb, k0, brow);
                         } else {
 #pragma unroll
-                            for (int j = 0; j < BN / 64; ++j)
-                                tma_load_2d(sb + j * 8192, &tmB, full + stage, n0 + 64 * j, brow);
+                            for (int j = 0; j < BN / 64; ++j) ld_b(sb + j * 8192, n0 + 64 * j, brow);
                         }
                     }
                 }
@@ -711,7 +743,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             tc_fence_after();
             const int m = ti.a_row0 + q * 32 + lane;
             if (args.epi == EPI_ADAM_F32) {
-                adam_tile_rows(args, tmem_base + (uint32_t(q * 32) << 16) + acc * BN, m, ti.n_col0);
+                const uint32_t ta = tmem_base + (uint32_t(q * 32) << 16) + acc * BN;
+                if (args.mom16)
+                    adam_tile_rows<true>(args, ta, m, ti.n_col0);
+                else
+                    adam_tile_rows<false>(args, ta, m, ti.n_col0);
             } else {
 #pragma unroll 1
                 for (int c = 0; c < BN / 32; ++c) {
@@ -814,6 +850,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     if (warp == 0) {
         // ------------------------------------------------ TMA producer (both CTAs; all lanes for gathered B rows)
         const bool gather = args.b_idx != nullptr;
+        const uint64_t pol_a = l2_policy(args.hint_a), pol_b = l2_policy(args.hint_b);
         int stage = 0;
         uint32_t phase = 0;
         int gn[4] = {0, 0, 0, 0};  // K-major gathered B: the NEXT tile's rows of this CTA's half (prefetched)
@@ -846,21 +883,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 if (lane == 0) {
                     mbar_wait(empty + stage, phase ^ 1);
                     if (leader) mbar_arrive_expect_tx(full + stage, 2 * P_STAGE_BYTES);
+                    auto ld_a = [&](void* dst, int c0, int c1) {
+                        if (args.hint_a) tma_load_2d_pair_hint(dst, &tmA, full + stage, c0, c1, pol_a);
+                        else tma_load_2d_pair(dst, &tmA, full + stage, c0, c1);
+                    };
+                    auto ld_b = [&](void* dst, int c0, int c1) {
+                        if (args.hint_b) tma_load_2d_pair_hint(dst, &tmB, full + stage, c0, c1, pol_b);
+                        else tma_load_2d_pair(dst, &tmB, full + stage, c0, c1);
+                    };
                     if (!A_MN) {
-                        tma_load_2d_pair(sa, &tmA, full + stage, k0, m0);
+                        ld_a(sa, k0, m0);
                     } else {
 #pragma unroll
-                        for (int j = 0; j < 2; ++j)
-                            tma_load_2d_pair(sa + j * 8192, &tmA, full + stage, m0 + 64 * j, k0);
+                        for (int j = 0; j < 2; ++j) ld_a(sa + j * 8192, m0 + 64 * j, k0);
                     }
                     if (!gather || run >= 0) {  // plain box (gathered B: at the run's table row)
                         const int brow = gather ? run : (B_MN ? k0 : n0);
                         if (!B_MN) {
-                            tma_load_2d_pair(sb, &tmB, full + stage, k0, brow);
+                            ld_b(sb, k0, brow);
                         } else {
 #pragma unroll
-                            for (int j = 0; j < 2; ++j)
-                                tma_load_2d_pair(sb + j * 8192, &tmB, full + stage, n0 + 64 * j, brow);
+                            for (int j = 0; j < 2; ++j) ld_b(sb + j * 8192, n0 + 64 * j, brow);
                         }
                     }
                 }
@@ -931,10 +974,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             if (args.epi == EPI_ADAM_F32) {
                 float* sw = reinterpret_cast<float*>(smem + P_STAGES * P_STAGE_BYTES + 256) + q * 32 * ADAM_SCRATCH_LD;
                 const uint32_t ta = tmem_base + (uint32_t(q * 32) << 16) + acc * BN;
-                if (args.stat_ss)
-                    adam_tile_transposed<true>(args, ta, m - lane, nb * BN, sw, lane);
-                else
-                    adam_tile_transposed<false>(args, ta, m - lane, nb * BN, sw, lane);
+                if (args.mom16) {
+                    if (args.stat_ss)
+                        adam_tile_transposed<true, true>(args, ta, m - lane, nb * BN, sw, lane);
+                    else
+                        adam_tile_transposed<false, true>(args, ta, m - lane, nb * BN, sw, lane);
+                } else {
+                    if (args.stat_ss)
+                        adam_tile_transposed<true, false>(args, ta, m - lane, nb * BN, sw, lane);
+                    else
+                        adam_tile_transposed<false, false>(args, ta, m - lane, nb * BN, sw, lane);
+                }
             } else {
 #pragma unroll 1
                 for (int c = 0; c < BN / 32; ++c) {
@@ -1064,6 +1114,7 @@ KArgs base_args(int64_t M, int64_t N, int64_t K, const GemmEpilogue& epi) {
     args.adam_w = epi.adam_w;
     args.adam_m = epi.adam_m;
     args.adam_v = epi.adam_v;
+    args.mom16 = epi.adam_mom16 ? 1 : 0;
     args.adam_c = epi.adam_c;
     args.adam_coef = epi.adam_coef;
     args.b1 = epi.b1;
@@ -1147,6 +1198,8 @@ void gemm_bf16_one(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmO
         throw MeftError(2, "gemm_bf16: operands need 16-byte aligned base and leading dimension % 8 == 0");
     check_epilogue(epi);
     KArgs args = base_args(M, N, K, epi);
+    args.hint_a = A.l2_hint;
+    args.hint_b = B.l2_hint;
     const CUtensorMap ta = A.mn_major ? make_map(A.ptr, M, K, A.ld, 64, 64) : make_map(A.ptr, K, M, A.ld, 64, BM);
     CUtensorMap tg;
     if (B.rows) {  // gathered B rows: a {64 x 1} box over the whole table, rows fetched by tile::gather4
@@ -1186,6 +1239,8 @@ void gemm_bf16_one(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmO
         args.raster_group = forced ? forced : (!A.mn_major && !B.mn_major ? 16 : 8);
         if (A.mn_major && forced_amn) args.raster_group = forced_amn;
         if (!A.mn_major && B.mn_major && forced_bmn) args.raster_group = forced_bmn;
+        if (epi.raster > 0) args.raster_group = epi.raster;
+        args.raster_n_fast = epi.raster < 0 ? 1 : 0;
         launch_pair_dispatch(st, A.mn_major, B.mn_major, ta, tb, B.rows ? tg : tb, args, int(pair_tiles));
         return;
     }

@@ -23,6 +23,8 @@ struct GemmOperand {
     // as consecutive panels of kGemmPanel columns, panel p at ptr + p * panel_stride, each with leading dimension
     // ld, so every sub-GEMM reads one dense [rows x kGemmPanel] panel. 0 = one plain matrix.
     int64_t panel_stride = 0;
+    // L2 eviction priority of this operand's TMA loads: 0 default, 1 evict_first, 2 evict_last (plain boxes only).
+    int l2_hint = 0;
 };
 constexpr int64_t kGemmPanel = 65536;  // = gemm_bf16's chunk width
 
@@ -78,8 +80,9 @@ struct GemmEpilogue {
     int64_t row0 = 0, col0 = 0;
     // EPI_ADAM_F32 (ldc = table row pitch in elements)
     float* adam_w = nullptr;
-    float* adam_m = nullptr;
-    float* adam_v = nullptr;
+    void* adam_m = nullptr;  // fp32, or bf16 with adam_mom16 (COMPACT store)
+    void* adam_v = nullptr;
+    bool adam_mom16 = false;
     uint16_t* adam_c = nullptr;
     const float2* adam_coef = nullptr;
     float b1 = 0.9f, b2 = 0.999f, eps = 1e-8f;
@@ -89,6 +92,9 @@ struct GemmEpilogue {
     // Panelled C of the bf16 epilogues (EPI_RELU_BF16 / EPI_MASK_BF16 with bits): N stored as kGemmPanel-wide panels
     // at c + p * panel_stride, leading dimension ldc (see GemmOperand::panel_stride).
     int64_t panel_stride = 0;
+    // Launch option, CTA-pair kernel tile order: 0 = the default policy, -1 = sweep N first (the co-running tiles
+    // share their A panels; B is re-read every wave), g > 0 = groups of g 256-row M tiles per streamed B panel.
+    int raster = 0;
 };
 constexpr int kAdamStatTile = 256;  // columns per EPI_ADAM_F32 statistics partial
 

@@ -1,7 +1,9 @@
 // libmeft_cuda.so — C ABI of the B200 MEFT layer (declarations and reference citations: include/meft_cuda.h).
 // Host orchestration only: every numeric step is a kernel in gemm_sm100.cu / select.cu / stream_ops.cu /
 // dgemm.cu. There is no CPU compute path.
+#include <array>
 #include <cmath>
+#include <cstdio>
 #include <functional>
 #include <optional>
 #include <cstring>
@@ -119,7 +121,8 @@ struct LayerBufs {
 
 struct meft_store {
     int64_t layers = 0, d = 0, pairs = 0, experts = 0;
-    meft_precision prec = MEFT_STORE_MIXED;
+    meft_precision prec = MEFT_STORE_MIXED;  // F64 or MIXED (COMPACT stores are MIXED with bf16 moments)
+    bool mom16 = false;                      // COMPACT: Adam moments m_a, v_a, m_b, v_b in bf16
     int device = 0;
     std::vector<LayerBufs> L;
     std::vector<char> key_stats_valid;  // per layer: kn/kl match the current compute keys
@@ -237,6 +240,39 @@ int64_t selection_take(int64_t M, int64_t N, int64_t kk, int64_t k, int64_t* kk_
     return std::min(k, visible);
 }
 
+// Per-GEMM launch knobs of the six FFN GEMMs: CTA-pair tile order (GemmEpilogue::raster) and the L2 eviction
+// priority of each operand's TMA stream (GemmOperand::l2_hint). The defaults are the measured choices (DESIGN.md
+// §4); MEFT_GEMM_<Z|OUT|DA|GH|GWB|GWA>="raster,hint_a,hint_b" overrides one GEMM for A/B experiments.
+struct GemmKnob {
+    int raster = 0, hint_a = 0, hint_b = 0;
+};
+enum FfnGemm { G_Z = 0, G_OUT, G_DA, G_GH, G_GWB, G_GWA, G_COUNT };
+GemmKnob gemm_knob(int which) {
+    static const std::array<GemmKnob, G_COUNT> knobs = [] {
+        static const char* names[G_COUNT] = {"MEFT_GEMM_Z", "MEFT_GEMM_OUT", "MEFT_GEMM_DA",
+                                             "MEFT_GEMM_GH", "MEFT_GEMM_GWB", "MEFT_GEMM_GWA"};
+        std::array<GemmKnob, G_COUNT> k{};
+        for (int i = 0; i < G_COUNT; ++i) {
+            const char* v = std::getenv(names[i]);
+            if (v) std::sscanf(v, "%d,%d,%d", &k[i].raster, &k[i].hint_a, &k[i].hint_b);
+        }
+        return k;
+    }();
+    return knobs[which];
+}
+GemmOperand knob_a(GemmOperand op, int which) {
+    op.l2_hint = gemm_knob(which).hint_a;
+    return op;
+}
+GemmOperand knob_b(GemmOperand op, int which) {
+    op.l2_hint = gemm_knob(which).hint_b;
+    return op;
+}
+GemmEpilogue knob_e(GemmEpilogue e, int which) {
+    e.raster = gemm_knob(which).raster;
+    return e;
+}
+
 // ---- FFN building blocks (adapter.cpp:122-126, 166-175)
 
 // Selected key/value rows either materialised ([s x d], rows == nullptr) or gathered by the GEMMs themselves:
@@ -321,7 +357,8 @@ void ffn_forward_impl(meft_ctx* ctx, meft_dtype dt, const void* h, const void* k
     e1.bits = act_bits;  // [T x ceil(s / 32)] bitmask of z > 0 for the backward's mask
     e1.ldbits = (s + 31) / 32;
     e1.panel_stride = panel;  // act in kGemmPanel-wide panels (|S| > 65536)
-    gemm_bf16(st, T, s, d, GemmOperand{h, d, false}, kv_operand(ctx, keys_s, d, false, rg, s), e1);
+    gemm_bf16(st, T, s, d, knob_a(GemmOperand{h, d, false}, G_Z), knob_b(kv_operand(ctx, keys_s, d, false, rg, s), G_Z),
+              knob_e(e1, G_Z));
     GemmEpilogue e2;
     if (peer) {
         e2 = peer_epilogue(*peer, false, d);
@@ -333,7 +370,8 @@ void ffn_forward_impl(meft_ctx* ctx, meft_dtype dt, const void* h, const void* k
     }
     GemmOperand za{z, ld_z, false};
     za.panel_stride = panel;
-    gemm_bf16(st, T, d, s, za, kv_operand(ctx, values_s, d, true, rg, s), e2);
+    gemm_bf16(st, T, d, s, knob_a(za, G_OUT), knob_b(kv_operand(ctx, values_s, d, true, rg, s), G_OUT),
+              knob_e(e2, G_OUT));
 }
 
 // stage_keys/stage_values non-null => weight grads are row-added into the store staging at S (fused scatter).
@@ -400,7 +438,8 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
     e3.bits = const_cast<uint32_t*>(act_bits);  // the forward's bitmask instead of re-reading act (1/16 the bytes)
     e3.ldbits = (s + 31) / 32;
     e3.panel_stride = panel;
-    gemm_bf16(st, T, s, d, GemmOperand{g, d, false}, kv_operand(ctx, values_s, d, false, rg, s), e3);
+    gemm_bf16(st, T, s, d, knob_a(GemmOperand{g, d, false}, G_DA),
+              knob_b(kv_operand(ctx, values_s, d, false, rg, s), G_DA), knob_e(e3, G_DA));
     if (grad_h || peer) {  // first after masked, so grad_h can stream back while the weight-gradient GEMMs run
         GemmEpilogue e6;  // grad_h (+)= masked * keys_s
         if (peer) {
@@ -411,7 +450,8 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
             e6.ldc = d;
             e6.accumulate = acc_h;
         }
-        gemm_bf16(st, T, d, s, op(masked, ld_z, false), kv_operand(ctx, keys_s, d, true, rg, s), e6);
+        gemm_bf16(st, T, d, s, knob_a(op(masked, ld_z, false), G_GH),
+                  knob_b(kv_operand(ctx, keys_s, d, true, rg, s), G_GH), knob_e(e6, G_GH));
     }
     if (grad_h_done) MEFT_CUDA_CHECK(cudaEventRecord(grad_h_done, st));
     GemmEpilogue e4;  // grad_values = act^T G   (M = s, N = d, K = T)
@@ -424,11 +464,13 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
         e4.c = grad_values_s;
     }
     e4.ldc = d;
-    gemm_bf16(st, s, d, T, op(z, ld_z, true), GemmOperand{g, d, true}, epi_values ? *epi_values : e4);
+    gemm_bf16(st, s, d, T, knob_a(op(z, ld_z, true), G_GWB), knob_b(GemmOperand{g, d, true}, G_GWB),
+              knob_e(epi_values ? *epi_values : e4, G_GWB));
     if (between) (*between)();  // e.g. consume grad_values before grad_keys reuses its buffer
     GemmEpilogue e5 = e4;  // grad_keys = masked^T h
     e5.c = S_rows ? stage_keys : grad_keys_s;
-    gemm_bf16(st, s, d, T, op(masked, ld_z, true), GemmOperand{h, d, true}, epi_keys ? *epi_keys : e5);
+    gemm_bf16(st, s, d, T, knob_a(op(masked, ld_z, true), G_GWA), knob_b(GemmOperand{h, d, true}, G_GWA),
+              knob_e(epi_keys ? *epi_keys : e5, G_GWA));
 }
 
 // ---- store helpers
@@ -447,10 +489,10 @@ void* tensor_ptr(const meft_store* s, const LayerBufs& L, meft_tensor t, meft_dt
         case MEFT_T_W_A: *dt = master; return L.w_a;
         case MEFT_T_W_B: *dt = master; return L.w_b;
         case MEFT_T_W_G: *dt = master; *rows = s->experts; return L.w_g;
-        case MEFT_T_M_A: *dt = master; return L.m_a;
-        case MEFT_T_V_A: *dt = master; return L.v_a;
-        case MEFT_T_M_B: *dt = master; return L.m_b;
-        case MEFT_T_V_B: *dt = master; return L.v_b;
+        case MEFT_T_M_A: *dt = s->mom16 ? MEFT_BF16 : master; return L.m_a;
+        case MEFT_T_V_A: *dt = s->mom16 ? MEFT_BF16 : master; return L.v_a;
+        case MEFT_T_M_B: *dt = s->mom16 ? MEFT_BF16 : master; return L.m_b;
+        case MEFT_T_V_B: *dt = s->mom16 ? MEFT_BF16 : master; return L.v_b;
         case MEFT_T_STAGE_A: *dt = master; return L.st_a;
         case MEFT_T_STAGE_B: *dt = master; return L.st_b;
         case MEFT_T_W_A_COMPUTE: *dt = comp; return L.c_a;
@@ -607,10 +649,10 @@ void adam_impl(meft_ctx* ctx, meft_store* s, int64_t layer, double b1, double b2
     int32_t* cnt = ctx->dev_small + 8;
     compact_flags(st, L.staged, s->pairs, rows, cnt, bws);
     if (s->prec == MEFT_STORE_MIXED)
-        adam_mixed(st, rows, cnt, 0, s->d, static_cast<float*>(L.w_a), static_cast<float*>(L.m_a),
-                   static_cast<float*>(L.v_a), static_cast<float*>(L.st_a), static_cast<uint16_t*>(L.c_a),
-                   static_cast<float*>(L.w_b), static_cast<float*>(L.m_b), static_cast<float*>(L.v_b),
-                   static_cast<float*>(L.st_b), static_cast<uint16_t*>(L.c_b), L.step, L.staged, b1, b2, eps, lr);
+        adam_mixed(st, rows, cnt, 0, s->d, static_cast<float*>(L.w_a), L.m_a, L.v_a, static_cast<float*>(L.st_a),
+                   static_cast<uint16_t*>(L.c_a), static_cast<float*>(L.w_b), L.m_b, L.v_b,
+                   static_cast<float*>(L.st_b), static_cast<uint16_t*>(L.c_b), L.step, L.staged, b1, b2, eps, lr, 3,
+                   true, false, nullptr, nullptr, s->mom16);
     else
         adam_f64(st, rows, cnt, 0, s->d, static_cast<double*>(L.w_a), static_cast<double*>(L.m_a),
                  static_cast<double*>(L.v_a), static_cast<double*>(L.st_a), static_cast<double*>(L.w_b),
@@ -1109,17 +1151,22 @@ meft_status meft_store_create(meft_ctx* ctx, int64_t layers, int64_t d, int64_t 
         require_ctx(ctx);
         require(out != nullptr, MEFT_E_INVALID, "null output pointer");
         require(layers >= 1 && d >= 1 && pairs >= 1 && experts >= 1, MEFT_E_SHAPE, "store_create: non-positive shape");
+        require(precision == MEFT_STORE_F64 || precision == MEFT_STORE_MIXED || precision == MEFT_STORE_COMPACT,
+                MEFT_E_INVALID, "store_create: unknown precision");
         std::unique_ptr<meft_store> s(new meft_store());
         s->layers = layers;
         s->d = d;
         s->pairs = pairs;
         s->experts = experts;
-        s->prec = precision;
+        s->mom16 = precision == MEFT_STORE_COMPACT;
+        s->prec = s->mom16 ? MEFT_STORE_MIXED : precision;
+        precision = s->prec;
         s->device = ctx->device;
         const int mb = precision == MEFT_STORE_F64 ? 8 : 4;
+        const int momb = s->mom16 ? 2 : mb;  // Adam moment element size
         const size_t pd = size_t(pairs) * size_t(d), nd = size_t(experts) * size_t(d);
         auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-        size_t bytes = 6 * al(pd * mb) + al(nd * mb) + al(size_t(pairs) * 4) + al(size_t(pairs));
+        size_t bytes = 2 * al(pd * mb) + 4 * al(pd * momb) + al(nd * mb) + al(size_t(pairs) * 4) + al(size_t(pairs));
         if (precision == MEFT_STORE_MIXED) bytes += 2 * al(pd * 2) + al(nd * 2) + 2 * al(size_t(pairs) * 4);
         bytes += al(size_t(experts) * 8);
         for (int64_t l = 0; l < layers; ++l) {
@@ -1140,10 +1187,10 @@ meft_status meft_store_create(meft_ctx* ctx, int64_t layers, int64_t d, int64_t 
             };
             L.w_a = take(pd * mb);
             L.w_b = take(pd * mb);
-            L.m_a = take(pd * mb);
-            L.v_a = take(pd * mb);
-            L.m_b = take(pd * mb);
-            L.v_b = take(pd * mb);
+            L.m_a = take(pd * momb);
+            L.v_a = take(pd * momb);
+            L.m_b = take(pd * momb);
+            L.v_b = take(pd * momb);
             L.w_g = take(nd * mb);
             L.step = static_cast<int32_t*>(take(size_t(pairs) * 4));
             L.staged = static_cast<uint8_t*>(take(size_t(pairs)));
@@ -1231,7 +1278,7 @@ meft_status meft_store_info(const meft_store* s, int64_t* layers, int64_t* d, in
         if (d) *d = s->d;
         if (pairs) *pairs = s->pairs;
         if (experts) *experts = s->experts;
-        if (precision) *precision = s->prec;
+        if (precision) *precision = s->mom16 ? MEFT_STORE_COMPACT : s->prec;
     });
 }
 
@@ -1675,8 +1722,9 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
             e.ldc = d;
             e.row_idx = uni;
             e.adam_w = static_cast<float*>(keys ? L.w_a : L.w_b);
-            e.adam_m = static_cast<float*>(keys ? L.m_a : L.m_b);
-            e.adam_v = static_cast<float*>(keys ? L.v_a : L.v_b);
+            e.adam_m = keys ? L.m_a : L.m_b;
+            e.adam_v = keys ? L.v_a : L.v_b;
+            e.adam_mom16 = s->mom16;
             e.adam_c = static_cast<uint16_t*>(keys ? L.c_a : L.c_b);
             e.adam_coef = coef;
             e.b1 = float(b1);
@@ -1711,11 +1759,10 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
         auto adam_table = [&](int table) {
             PhaseScope p4(ctx, 4);
             const bool keys = table == 1;
-            adam_mixed(st, uni, nullptr, su, d, static_cast<float*>(L.w_a), static_cast<float*>(L.m_a),
-                       static_cast<float*>(L.v_a), gblk, static_cast<uint16_t*>(L.c_a), static_cast<float*>(L.w_b),
-                       static_cast<float*>(L.m_b), static_cast<float*>(L.v_b), gblk, static_cast<uint16_t*>(L.c_b),
-                       L.step, nullptr, b1, b2, eps, lr, table, keys, true, keys && stats_valid ? L.kn : nullptr,
-                       keys && stats_valid ? L.kl : nullptr);
+            adam_mixed(st, uni, nullptr, su, d, static_cast<float*>(L.w_a), L.m_a, L.v_a, gblk,
+                       static_cast<uint16_t*>(L.c_a), static_cast<float*>(L.w_b), L.m_b, L.v_b, gblk,
+                       static_cast<uint16_t*>(L.c_b), L.step, nullptr, b1, b2, eps, lr, table, keys, true,
+                       keys && stats_valid ? L.kn : nullptr, keys && stats_valid ? L.kl : nullptr, s->mom16);
         };
         std::optional<PhaseScope> p3;
         p3.emplace(ctx, 3);

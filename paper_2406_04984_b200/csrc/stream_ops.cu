@@ -114,11 +114,32 @@ __global__ void k_mark(uint8_t* __restrict__ staged, const int32_t* __restrict__
 // (the layer step updates the value rows first without bump, the key rows afterwards with it).
 // With `gpos` the gradients are not staging rows but a dense [count x d] block in `rows` order (the fused layer
 // step's weight-grad GEMM output): read once, never zeroed -- 30 B per entry instead of 34.
+// Four Adam moments of a row at vector index i: fp32 (float4) or, for COMPACT stores, bf16 (uint2), as floats.
+template <bool MOM16>
+__device__ __forceinline__ float4 load_mom4(const void* base, int64_t i) {
+    if (MOM16) {
+        const uint2 u = reinterpret_cast<const uint2*>(base)[i];
+        return make_float4(bf16_bits_to_f32(uint16_t(u.x)), bf16_bits_to_f32(uint16_t(u.x >> 16)),
+                           bf16_bits_to_f32(uint16_t(u.y)), bf16_bits_to_f32(uint16_t(u.y >> 16)));
+    }
+    return reinterpret_cast<const float4*>(base)[i];
+}
+template <bool MOM16>
+__device__ __forceinline__ void store_mom4(void* base, int64_t i, float4 v) {
+    if (MOM16) {
+        reinterpret_cast<uint2*>(base)[i] = make_uint2(pack_bf16x2(f32_to_bf16_bits(v.x), f32_to_bf16_bits(v.y)),
+                                                       pack_bf16x2(f32_to_bf16_bits(v.z), f32_to_bf16_bits(v.w)));
+    } else {
+        reinterpret_cast<float4*>(base)[i] = v;
+    }
+}
+
+template <bool MOM16>
 __global__ void __launch_bounds__(256) k_adam_mixed(const int32_t* __restrict__ rows, const int32_t* count_dev,
-                                                    int count, int64_t d, float* __restrict__ wa, float* __restrict__ ma,
-                                                    float* __restrict__ va, float* __restrict__ sa,
+                                                    int count, int64_t d, float* __restrict__ wa, void* __restrict__ ma,
+                                                    void* __restrict__ va, float* __restrict__ sa,
                                                     uint16_t* __restrict__ ca, float* __restrict__ wb,
-                                                    float* __restrict__ mb, float* __restrict__ vb,
+                                                    void* __restrict__ mb, void* __restrict__ vb,
                                                     float* __restrict__ sb, uint16_t* __restrict__ cb,
                                                     int32_t* __restrict__ step, uint8_t* __restrict__ staged, float b1,
                                                     float b2, float eps, float lr, int tables, int bump, int gpos,
@@ -144,8 +165,9 @@ __global__ void __launch_bounds__(256) k_adam_mixed(const int32_t* __restrict__ 
         for (int tab = 0; tab < 2; ++tab) {
             if (!(tables & (1 << tab))) continue;
             float4* w4 = reinterpret_cast<float4*>((tab ? wb : wa) + j * d);
-            float4* m4 = reinterpret_cast<float4*>((tab ? mb : ma) + j * d);
-            float4* v4 = reinterpret_cast<float4*>((tab ? vb : va) + j * d);
+            const int64_t esz = MOM16 ? 2 : 4;
+            void* m4 = static_cast<uint8_t*>(tab ? mb : ma) + j * d * esz;
+            void* v4 = static_cast<uint8_t*>(tab ? vb : va) + j * d * esz;
             float4* g4 = reinterpret_cast<float4*>((tab ? sb : sa) + (gpos ? int64_t(r) : j) * d);
             uint2* c4 = reinterpret_cast<uint2*>((tab ? cb : ca) + j * d);
             const bool stats = tab == 0 && kn != nullptr;  // refresh the key row's selection statistics
@@ -153,15 +175,15 @@ __global__ void __launch_bounds__(256) k_adam_mixed(const int32_t* __restrict__ 
             int lsb = INT32_MAX;
             for (int64_t i = threadIdx.x; i < d / 4; i += blockDim.x) {
                 const float4 g = g4[i];
-                float4 m = m4[i], v = v4[i], w = w4[i];
+                float4 m = load_mom4<MOM16>(m4, i), v = load_mom4<MOM16>(v4, i), w = w4[i];
                 float* mp = &m.x;
                 float* vp = &v.x;
                 float* wp = &w.x;
                 const float* gp = &g.x;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) adam_update(wp[q], mp[q], vp[q], gp[q], b1, b2, eps, k);
-                m4[i] = m;
-                v4[i] = v;
+                store_mom4<MOM16>(m4, i, m);
+                store_mom4<MOM16>(v4, i, v);
                 w4[i] = w;
                 if (!gpos) g4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
                 const uint16_t cb4[4] = {f32_to_bf16_bits(w.x), f32_to_bf16_bits(w.y), f32_to_bf16_bits(w.z),
@@ -473,14 +495,15 @@ void mark_rows(cudaStream_t st, uint8_t* staged, const int32_t* idx, const int32
 }
 
 void adam_mixed(cudaStream_t st, const int32_t* rows, const int32_t* count_dev, int64_t count, int64_t d, float* wa,
-                float* ma, float* va, float* sa, uint16_t* ca, float* wb, float* mb, float* vb, float* sb,
+                void* ma, void* va, float* sa, uint16_t* ca, float* wb, void* mb, void* vb, float* sb,
                 uint16_t* cb, int32_t* step, uint8_t* staged, double b1, double b2, double eps, double lr, int tables,
-                bool bump, bool grads_by_position, float* key_norms, int32_t* key_lsb) {
+                bool bump, bool grads_by_position, float* key_norms, int32_t* key_lsb, bool moments_bf16) {
     if (d % 4) throw MeftError(2, "adam: d must be a multiple of 4 in mixed precision");
     const int grid = std::max(1, std::min<int>(int(count > 0 ? count : num_sms() * 8), num_sms() * 8));
-    k_adam_mixed<<<grid, 256, 0, st>>>(rows, count_dev, int(count), d, wa, ma, va, sa, ca, wb, mb, vb, sb, cb, step,
-                                       staged, float(b1), float(b2), float(eps), float(lr), tables, bump ? 1 : 0,
-                                       grads_by_position ? 1 : 0, key_norms, key_lsb);
+    auto kern = moments_bf16 ? k_adam_mixed<true> : k_adam_mixed<false>;
+    kern<<<grid, 256, 0, st>>>(rows, count_dev, int(count), d, wa, ma, va, sa, ca, wb, mb, vb, sb, cb, step, staged,
+                               float(b1), float(b2), float(eps), float(lr), tables, bump ? 1 : 0,
+                               grads_by_position ? 1 : 0, key_norms, key_lsb);
     check_launch("k_adam_mixed");
 }
 

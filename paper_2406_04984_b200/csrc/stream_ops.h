@@ -27,11 +27,12 @@ void router_ste_grads(cudaStream_t st, const int32_t* uni, int64_t su, int64_t E
                       uint8_t* touched);
 void union_holes_n(cudaStream_t st, const int32_t* idx, int64_t n, int32_t* out);
 void adam_mixed(cudaStream_t st, const int32_t* rows, const int32_t* count_dev, int64_t count, int64_t d, float* wa,
-                float* ma, float* va, float* sa, uint16_t* ca, float* wb, float* mb, float* vb, float* sb,
+                void* ma, void* va, float* sa, uint16_t* ca, float* wb, void* mb, void* vb, float* sb,
                 uint16_t* cb, int32_t* step, uint8_t* staged, double b1, double b2, double eps, double lr,
                 int tables = 3, bool bump = true,  // tables: bit 0 keys, bit 1 values
                 bool grads_by_position = false,    // sa/sb = [count x d] gradients of rows[0..count), kept as is
-                float* key_norms = nullptr, int32_t* key_lsb = nullptr);  // refresh updated keys' select stats
+                float* key_norms = nullptr, int32_t* key_lsb = nullptr,  // refresh updated keys' select stats
+                bool moments_bf16 = false);  // m/v tables are bf16 (COMPACT store), else fp32
 // Adam fused into the weight-gradient GEMMs (EPI_ADAM_F32): advance step[rows[r]] and tabulate its
 // (lr / (1 - b1^t), 1 / (1 - b2^t)) by position; then fold the epilogue's key statistics partials.
 void adam_coef_bump(cudaStream_t st, const int32_t* rows, int64_t n, int32_t* step, float2* coef, double b1,

@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import BF16, F32, F64, STORE_F64, STORE_MIXED, TENSORS, CkptHeader, MeftError, check, lib
+from ._lib import BF16, F32, F64, STORE_COMPACT, STORE_F64, STORE_MIXED, TENSORS, CkptHeader, MeftError, check, lib
 
 P = C.c_void_p
 I64 = C.c_int64
@@ -243,7 +243,8 @@ def matmul_f64(ctx: Context, a, b):
 
 
 class Store:
-    """HBM-resident HostStore (memtier.hpp:108-133). precision: STORE_F64 (API fidelity) or STORE_MIXED."""
+    """HBM-resident HostStore (memtier.hpp:108-133). precision: STORE_F64 (API fidelity), STORE_MIXED, or
+    STORE_COMPACT (MIXED with bf16 Adam moments)."""
 
     def __init__(self, ctx: Context, layers, d, pairs, experts, precision=STORE_MIXED):
         self.ctx = ctx

@@ -1,9 +1,9 @@
 """BASELINE config 3 on ONE B200: a stack of L MEFT adapter layers (d=4096, M=65,536, 256 experts, K=128) with
 all tables and Adam state resident in HBM, T tokens per step (16,384 in the config). One step = the fused layer
-step of every layer in turn. 32 layers need ~240 GB of tables (two or more GPUs, expert-sharded); this measures
-the L that fit one GPU and reports the per-layer time and the projected 32-layer step.
+step of every layer in turn. With fp32 Adam moments (MIXED, 7.5 GB per layer) 32 layers need ~240 GB, so 22 fit
+one GPU; with bf16 moments (COMPACT, 5.4 GB per layer) all 32 do.
 
-  python tools/stack_bench.py [layers=20] [tokens=16384] [steps=3]
+  python tools/stack_bench.py [layers=20] [tokens=16384] [steps=3] [mixed|compact]
 """
 import json
 import os
@@ -19,9 +19,10 @@ def main():
     L = int(sys.argv[1]) if len(sys.argv) > 1 else 20
     T = int(sys.argv[2]) if len(sys.argv) > 2 else 16384
     steps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+    prec = sys.argv[4] if len(sys.argv) > 4 else "mixed"
     d, M, N, K, kk = 4096, 65536, 256, 128, 4
     ctx = G.Context(0)
-    st = G.Store(ctx, L, d, M, N, G.STORE_MIXED)
+    st = G.Store(ctx, L, d, M, N, G.STORE_COMPACT if prec == "compact" else G.STORE_MIXED)
     b = 1.0 / d ** 0.5
     gen = torch.Generator(device="cuda").manual_seed(1)
     with torch.no_grad():
@@ -45,7 +46,7 @@ def main():
     ms = e0.elapsed_time(e1) / steps
     per_layer = ms / L
     free, total = torch.cuda.mem_get_info()
-    print(json.dumps({"layers_resident": L, "tokens_per_step": T, "ms_per_step": ms, "ms_per_layer": per_layer,
+    print(json.dumps({"layers_resident": L, "precision": prec, "tokens_per_step": T, "ms_per_step": ms, "ms_per_layer": per_layer,
                       "tokens_per_s": T / ms * 1e3, "layer_tokens_per_s": T * L / ms * 1e3,
                       "projected_32_layer_ms": 32 * per_layer, "projected_32_layer_tokens_per_s": T / (32 * per_layer) * 1e3,
                       "hbm_used_gb": (total - free) / 1e9}))
