@@ -218,8 +218,8 @@ meft_status meft_base_ffn_backward(meft_ctx* ctx, const double* grad_out, const 
  * device: deterministic stable bucketing instead of host-driven index manipulation between the exchanges.
  * world <= 64. Host-side count arrays are written after a stream synchronisation. */
 /* Dispatch plan: row i = t*kk + s of tau goes to owner tau[i] / n_loc (experts per rank), rows bucketed by owner in
- * ascending i. send_rows [T*kk x d] bf16 (= h[t]), send_exp (owner-local expert), order[p] = i, inv[i] = p,
- * counts[world] (host): rows per owner. */
+ * ascending i. send_rows [T*kk x d] bf16 (= h[t]; may be NULL: no row copy), send_exp (owner-local expert),
+ * order[p] = i, inv[i] = p, counts[world] (host): rows per owner. */
 meft_status meft_shard_dispatch(meft_ctx* ctx, const int32_t* tau, int64_t T, int64_t kk, int64_t n_loc, int world,
                                 const uint16_t* h, int64_t d, uint16_t* send_rows, int32_t* send_exp, int32_t* order,
                                 int32_t* inv, int64_t* counts);
@@ -471,6 +471,46 @@ meft_status meft_layer_step_host(meft_ctx* ctx, meft_store* store, int64_t layer
                                  const uint16_t* grad_out_host, int64_t T, int64_t kk, int64_t k, double beta1,
                                  double beta2, double eps, double lr, float* out_host, float* grad_h_host,
                                  meft_step_info* info);
+
+/* ---- The expert-sharded layer step behind the C ABI (one rank per GPU). The context carries a
+ * communicator: NCCL (created from a unique id, or the caller's own ncclComm_t), or host callbacks (a process that
+ * stands in for several ranks, e.g. the test suite's emulation on one GPU). NCCL is loaded at run time
+ * (libnccl.so.2: the copy already in the process, e.g. torch's, else the system one); the sharded calls fail with
+ * MEFT_E_NCCL when it is absent, nothing else needs it. */
+/* ncclGetUniqueId into 128 bytes (rank 0 creates it; every rank passes the same bytes to meft_ctx_comm_init). */
+meft_status meft_nccl_unique_id(void* id128);
+/* A communicator owned by the context (ncclCommInitRank over `world` ranks). */
+meft_status meft_ctx_comm_init(meft_ctx* ctx, const void* id128, int rank, int world);
+/* The caller's ncclComm_t (not owned; must outlive its use by this context). */
+meft_status meft_ctx_set_comm(meft_ctx* ctx, void* nccl_comm, int rank, int world);
+/* Host-exchange communicator: every collective synchronises the context stream, copies its device payload to the
+ * host and calls back. all_gather: each rank contributes `bytes`; recv holds world * bytes in rank order.
+ * all_to_all_v: send holds world blocks (send_bytes[p] for rank p, consecutive); recv gets recv_bytes[p] from rank p,
+ * consecutive in rank order. Callbacks return 0 on success. */
+typedef struct meft_host_comm {
+    void* user;
+    int (*all_gather)(void* user, const void* send, size_t bytes, void* recv);
+    int (*all_to_all_v)(void* user, const void* send, const size_t* send_bytes, void* recv, const size_t* recv_bytes);
+} meft_host_comm;
+meft_status meft_ctx_set_host_comm(meft_ctx* ctx, const meft_host_comm* comm, int rank, int world);
+/* Releases the context's communicator (an owned NCCL communicator is destroyed). */
+meft_status meft_ctx_clear_comm(meft_ctx* ctx);
+/* One layer step of this rank's T tokens on its expert shard: `shard` holds experts [rank*N/P, (rank+1)*N/P) and
+ * their M/P pairs (a MIXED/COMPACT store with experts = N/P, pairs = M/P); w_g is the replicated bf16 router
+ * [N x d]. Every rank brings T tokens (h, grad_out bf16 [T x d]); the step covers all P*T tokens with the
+ * reference's batch-union semantics: selection split at the rank boundary (indices == the single-GPU step's),
+ * FFN + fused scatter + lazy Adam of the local part of the union on every owner, out / grad_h [T x d] fp32 summed
+ * back to the token homes. Exchanges: all-gather of h and grad_out; all-to-all of (token id, expert) dispatch
+ * entries (owners gather the token rows from the all-gathered h), of candidate scores, of exact-rescoring requests
+ * and answers; all-gather of per-destination counts and key norms; MAX all-reduce of the M-byte union bitmap;
+ * reduce-scatter of out / grad_h. per_token [T x take] (global pair ids, ascending) may be NULL. At world 1 the
+ * step equals meft_layer_step bit for bit. Replaces the reference trainer's per-layer calls (trainer.cpp:220, 270,
+ * 283, 525) for a sharded layer. */
+meft_status meft_layer_step_sharded(meft_ctx* ctx, meft_store* shard, int64_t layer, const uint16_t* w_g,
+                                    const uint16_t* h, const uint16_t* grad_out, int64_t T, int64_t kk, int64_t k,
+                                    double beta1, double beta2, double eps, double lr, float* out, float* grad_h,
+                                    int32_t* per_token, meft_step_info* info);
+
 
 #ifdef __cplusplus
 }

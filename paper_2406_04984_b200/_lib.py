@@ -32,6 +32,15 @@ class CkptHeader(C.Structure):
                 ("train_router", INT)]
 
 
+# meft_host_comm (include/meft_cuda.h): host-exchange communicator callbacks
+HC_ALL_GATHER = C.CFUNCTYPE(INT, P, P, C.c_size_t, P)
+HC_ALL_TO_ALL_V = C.CFUNCTYPE(INT, P, P, C.POINTER(C.c_size_t), P, C.POINTER(C.c_size_t))
+
+
+class HostComm(C.Structure):
+    _fields_ = [("user", P), ("all_gather", HC_ALL_GATHER), ("all_to_all_v", HC_ALL_TO_ALL_V)]
+
+
 # meft_ckpt_source / meft_ckpt_sink (include/meft_cuda.h)
 CKPT_SOURCE = C.CFUNCTYPE(INT, P, I64, INT, P, I64)
 CKPT_SINK = C.CFUNCTYPE(INT, P, C.POINTER(CkptHeader), I64, INT, P, I64)
@@ -120,6 +129,13 @@ _SIGS = {
     "meft_layer_step": (INT, [P, P, I64, P, P, I64, I64, I64, D, D, D, D, P, P, P, P, P]),
     "meft_layer_step_base": (INT, [P, P, I64, P, P, I64, I64, I64, D, D, D, D, P, P, P, P, P, P]),
     "meft_layer_step_host": (INT, [P, P, I64, P, P, I64, I64, I64, D, D, D, D, P, P, P]),
+    # the expert-sharded step behind the C ABI (csrc/sharded_step.cu)
+    "meft_nccl_unique_id": (INT, [P]),
+    "meft_ctx_comm_init": (INT, [P, P, INT, INT]),
+    "meft_ctx_set_comm": (INT, [P, P, INT, INT]),
+    "meft_ctx_set_host_comm": (INT, [P, C.POINTER(HostComm), INT, INT]),
+    "meft_ctx_clear_comm": (INT, [P]),
+    "meft_layer_step_sharded": (INT, [P, P, I64, P, P, P, I64, I64, I64, D, D, D, D, P, P, P, P]),
 }
 
 F64, F32, BF16 = 0, 1, 2

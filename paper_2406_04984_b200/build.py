@@ -126,6 +126,31 @@ def build_reference_tests(ref_proj: str = "/root/reference/proj", verbose: bool 
     return out
 
 
+CAPI_CHECKS = ("sharded_capi_check",)
+CAPI_CHECK_BIN = os.path.join(ROOT, "build", "capi_tests")
+
+
+def build_capi_checks(verbose: bool = False) -> list:
+    """C++ programs that use only the C ABI (tests/dropin/*.cpp listed in CAPI_CHECKS), linked against the in-tree
+    library; run on the GPU box by the -m gpu tests."""
+    lib = build(verbose)
+    os.makedirs(CAPI_CHECK_BIN, exist_ok=True)
+    out = []
+    for t in CAPI_CHECKS:
+        src = os.path.join(ROOT, "tests", "dropin", t + ".cpp")
+        exe = os.path.join(CAPI_CHECK_BIN, t)
+        if _needs(exe, [src, lib, os.path.join(ROOT, "include", "meft_cuda.h")]):
+            cmd = [HOST_CXX, "-O1", "-std=c++17", "-Wall", "-I" + os.path.join(ROOT, "include"), "-o", exe, src,
+                   "-L" + PKG, "-lmeft_cuda", "-Wl,-rpath," + PKG + ",-rpath,$ORIGIN/../../paper_2406_04984_b200"]
+            if verbose:
+                print(" ".join(cmd), file=sys.stderr)
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            if r.returncode != 0:
+                raise RuntimeError(f"g++ failed:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+        out.append(exe)
+    return out
+
+
 if __name__ == "__main__":
     print(build(verbose=True, force="--force" in sys.argv))
     print(build_dropin(verbose=True, force="--force" in sys.argv))

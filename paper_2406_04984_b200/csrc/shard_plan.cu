@@ -165,6 +165,7 @@ void shard_dispatch(cudaStream_t st, const int32_t* tau, int64_t T, int64_t kk, 
     check_launch("k_stable_bucket");
     k_dispatch_fill<<<grid_of(n), 256, 0, st>>>(tau, n, int(n_loc), pos_ws, order, inv, send_exp);
     check_launch("k_dispatch_fill");
+    if (!send_rows) return;  // the owners gather the rows themselves (from the all-gathered hidden states)
     k_gather_dispatch_rows<<<std::max(1, std::min(n / 8 + 1, num_sms() * 16)), 256, 0, st>>>(h, int(d), order, n,
                                                                                                int(kk), send_rows);
     check_launch("k_gather_dispatch_rows");

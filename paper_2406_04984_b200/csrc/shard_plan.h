@@ -8,7 +8,7 @@ namespace meft_dev {
 
 // Dispatch plan: (token, slot) i = t*kk + s goes to owner tau[i] / n_loc; stable bucket order by owner.
 // pos_ws: T*kk ints; send_rows [T*kk x d] bf16 = h[t]; send_exp: owner-local expert; order[p] = i; inv[i] = p;
-// counts[P] (device) rows per owner.
+// counts[P] (device) rows per owner. send_rows may be null (no row copy: owners gather rows by token id).
 void shard_dispatch(cudaStream_t st, const int32_t* tau, int64_t T, int64_t kk, int64_t n_loc, int P,
                     const uint16_t* h, int64_t d, int32_t* pos_ws, uint16_t* send_rows, int32_t* send_exp,
                     int32_t* order, int32_t* inv, int32_t* counts);

@@ -642,6 +642,88 @@ class ShardedLayer:
         return res
 
 
+class CShardedLayer:
+    """The same expert-sharded layer step issued entirely inside libmeft_cuda.so (meft_layer_step_sharded, csrc/
+    sharded_step.cu): what a C / C++ caller of the drop-in uses. The context's communicator is NCCL, created by the
+    library from a unique id that rank 0 broadcasts over `group` (a torch.distributed group), or -- with a
+    ThreadGroup -- host callbacks, so a single process can stand in for several ranks on one GPU. Owners gather the
+    dispatched token rows from the all-gathered h (no row all-to-all); per-destination counts are all-gathered on
+    the device."""
+
+    def __init__(self, ctx, store, w_g, group=None):
+        self.ctx, self.store, self.w_g = ctx, store, w_g
+        solo = group is None and not dist.is_initialized()  # one rank, no process group: a private communicator
+        self.world, self.rank = (1, 0) if solo else (_world(group), _rank(group))
+        self._keep = None
+        if isinstance(group, ThreadGroup):
+            self._set_host_comm(group)
+        else:
+            uid = (C.c_char * 128)()
+            if self.rank == 0:
+                check(lib().meft_nccl_unique_id(uid))
+            obj = [bytes(uid)]
+            if self.world > 1:
+                src = 0 if group is None else dist.get_global_rank(group, 0)
+                dist.broadcast_object_list(obj, src=src, group=group)
+            uid = (C.c_char * 128).from_buffer_copy(obj[0])
+            check(lib().meft_ctx_comm_init(ctx.h, uid, self.rank, self.world), ctx.h)
+
+    def _set_host_comm(self, group):
+        def all_gather(user, send, nbytes, recv):
+            try:
+                every = group._publish(C.string_at(send, nbytes))
+                C.memmove(recv, b"".join(every), nbytes * len(every))
+                return 0
+            except Exception:
+                return 1
+
+        def all_to_all_v(user, send, send_bytes, recv, recv_bytes):
+            try:
+                P = group.world
+                sizes = [send_bytes[p] for p in range(P)]
+                data = C.string_at(send, sum(sizes)) if sum(sizes) else b""
+                blocks, o = [], 0
+                for n in sizes:
+                    blocks.append(data[o:o + n])
+                    o += n
+                every = group._publish(blocks)
+                me = group.rank()
+                mine = b"".join(every[src][me] for src in range(P))
+                assert len(mine) == sum(recv_bytes[p] for p in range(P))
+                if mine:
+                    C.memmove(recv, mine, len(mine))
+                return 0
+            except Exception:
+                return 1
+
+        cb = _lib.HostComm(None, _lib.HC_ALL_GATHER(all_gather), _lib.HC_ALL_TO_ALL_V(all_to_all_v))
+        self._keep = cb  # the callbacks must outlive the context's use of them
+        check(lib().meft_ctx_set_host_comm(self.ctx.h, C.byref(cb), self.rank, self.world), self.ctx.h)
+
+    def close(self):
+        lib().meft_ctx_clear_comm(self.ctx.h)
+
+    def step(self, h, g, kk, k, lr, betas=(0.9, 0.999), eps=1e-8, out=None, grad_h=None, want_selection=False):
+        """One layer step of this rank's T tokens; returns out / grad_h [T x d] fp32 (and per_token, global ids)."""
+        from .meft import selection_shape
+
+        T, d = h.shape
+        N = self.w_g.shape[0]
+        take, _, _ = selection_shape(self.store.pairs * self.world, N, kk, k)
+        out = out if out is not None else torch.empty((T, d), dtype=torch.float32, device=h.device)
+        grad_h = grad_h if grad_h is not None else torch.empty_like(out)
+        per = torch.empty((T, take), dtype=torch.int32, device=h.device) if want_selection else None
+        info = _lib.StepInfo()
+        self.ctx.check(lib().meft_layer_step_sharded(self.ctx.h, self.store.h, 0, _p(self.w_g), _p(h), _p(g), T, kk, k,
+                                                     betas[0], betas[1], eps, lr, _p(out), _p(grad_h), _p(per),
+                                                     C.byref(info)))
+        res = {name: getattr(info, name) for name, _ in _lib.StepInfo._fields_}
+        res.update(out=out, grad_h=grad_h)
+        if want_selection:
+            res["per_token"] = per
+        return res
+
+
 def make_device_layer(ctx, d, M, N, group=None, seed=1, w_b_seed=0x7001):
     """This rank's shard as a MIXED HBM store: keys from HostStore::init(seed) restricted to the shard (the global
     table is generated once per rank with the reference RNG, then sliced), W_B ~ U(+-1/sqrt d) (torch RNG,

@@ -3,14 +3,14 @@ N=256, K=128, kk=4, T=8,192, bf16, one fused layer step on the B200 against the 
 on the same inputs -- HostStore::init(seed 1) tables and the BASELINE.md §3 streams (W_B 0x7001, h 0x7002,
 grad_out 0x7003), all bf16-rounded, so both sides score identical values.
 
-  * indices: tau, per-token top-K and the union of ALL 8,192 tokens == the reference's ke_select (experts.cpp:47-117)
+  * indices: the per-token top-K and the union of ALL 8,192 tokens == the reference's ke_select (experts.cpp:47-117)
   * out / grad_h of 32 tokens spread over the batch == sparse_ffn_pa / sparse_backward of those rows against the
     whole union (adapter.cpp:112-180; rows are independent), normwise within the bf16 tolerance below
   * the Adam-updated rows of 64 pairs spread over the union (w, m, v of the key column and value row) == the
     reference's scatter_grads + sparse_adam_update (memtier.cpp:128-228) of those pairs' full-batch gradients
 
-Tolerances are per tensor, about 3x the error observed on B200 (printed by the test), so an
-accuracy regression of a few x fails. The reference work is sized to run in well under a minute on 16 cores."""
+Tolerances are per tensor, about 2.5x the error observed on B200 (out 1.65e-3, grad_h 1.76e-3, gradients 1.65-1.72e-3,
+v 1.9-2.0e-3; printed by the test), so an accuracy regression of 3x fails. The reference work is sized to run in well under a minute on 16 cores."""
 import math
 
 import numpy as np
@@ -23,8 +23,8 @@ from paper_2406_04984_b200 import meft as G
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 D, M, N, K, KK, T, LR = 4096, 65536, 256, 128, 4, 8192, 1e-4
-# normwise relative error bounds vs the fp64 reference (observed on B200 x ~3)
-TOL = {"out": 6e-3, "grad_h": 6e-3, "grad_w_a": 6e-3, "grad_w_b": 6e-3, "v_a": 1.2e-2, "v_b": 1.2e-2}
+# normwise relative error bounds vs the fp64 reference (observed on B200 x ~2.5)
+TOL = {"out": 4.5e-3, "grad_h": 4.5e-3, "grad_w_a": 4.5e-3, "grad_w_b": 4.5e-3, "v_a": 5.5e-3, "v_b": 5.5e-3}
 N_TOKENS, N_PAIRS = 32, 64
 
 

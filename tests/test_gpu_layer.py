@@ -12,7 +12,17 @@ from paper_2406_04984_b200 import meft as G
 
 pytestmark = pytest.mark.gpu
 
-BF16_TOL = 1e-2
+# normwise relative error of the bf16 tcgen05 path vs the fp64 reference; observed 1.1e-3 .. 2.0e-3 on B200 at every
+# shape here and at cfg2 (tests/test_gpu_cfg2_parity.py) -- the bound is ~2.5x the worst observed
+BF16_TOL = 5e-3
+OBSERVED = []
+
+
+def check_rel(what, a, r, tol=None):
+    e = rel(a, r)
+    OBSERVED.append((what, e))
+    print(f"[bf16 parity] {what}: normwise rel err {e:.3e}")
+    assert e < (tol if tol is not None else BF16_TOL), (what, e)
 
 
 def bf16_dev(x):
@@ -58,8 +68,8 @@ def test_layer_step_cfg1_vs_reference_fixture(ctx, golden):
     assert res["union_size"] == int(g["union_size"])
     # values: stated bf16 tolerance
     toks = g["toks"]
-    assert rel(out.cpu().numpy()[toks], g["out"]) < BF16_TOL
-    assert rel(gh.cpu().numpy()[toks], g["grad_h"]) < BF16_TOL
+    check_rel("out", out.cpu().numpy()[toks], g["out"])
+    check_rel("grad_h", gh.cpu().numpy()[toks], g["grad_h"])
     assert abs(np.linalg.norm(out.cpu().numpy().astype(np.float64)) / float(g["out_fro"]) - 1) < BF16_TOL
     # Adam: per-pair counters exact; weights within |dw_gpu - dw_ref| <= 1e-2*lr + 1e-6|w|, except entries whose
     # gradient sign is ambiguous at bf16 precision (allowed 2*lr, since Adam's first step is ~ lr*sign(g)).
@@ -248,8 +258,8 @@ def test_layer_step_ragged_vs_live_reference(ctx, T, kk, K):
     torch.cuda.synchronize()
     np.testing.assert_array_equal(res["per_token"].cpu().numpy(), sel["per_token"])
     assert res["union_size"] == want["union_size"] == len(sel["unioned"])
-    assert rel(out.cpu().numpy(), want["out"]) < BF16_TOL
-    assert rel(gh.cpu().numpy(), want["grad_h"]) < BF16_TOL
+    check_rel("out", out.cpu().numpy(), want["out"])
+    check_rel("grad_h", gh.cpu().numpy(), want["grad_h"])
     np.testing.assert_array_equal(st.download(0, "pair_step"), ref.pair_step(0))
     for name, w0 in (("w_a", w_a), ("w_b", w_b)):
         got, exp = st.download(0, name), ref.get(0, name)
@@ -278,8 +288,8 @@ def test_layer_step_with_frozen_base_ffn(ctx, act):
                         base=(bf16_dev(w_in), bf16_dev(w_out), act))
     torch.cuda.synchronize()
     np.testing.assert_array_equal(res["per_token"].cpu().numpy(), sel["per_token"])
-    assert rel(out.cpu().numpy(), want_out) < BF16_TOL
-    assert rel(gh.cpu().numpy(), want_gh) < BF16_TOL
+    check_rel("out", out.cpu().numpy(), want_out)
+    check_rel("grad_h", gh.cpu().numpy(), want_gh)
 
 
 def test_check_finite_raises_reference_kind(ctx):
@@ -362,8 +372,8 @@ def test_layer_step_odd_dims_vs_live_reference(ctx, d, M, N, T, kk, K):
     np.testing.assert_array_equal(res["per_token"].cpu().numpy(), sel["per_token"])
     np.testing.assert_array_equal(res["unioned"].cpu().numpy(), sel["unioned"])
     assert res["union_size"] == want["union_size"]
-    assert rel(out.cpu().numpy(), want["out"]) < BF16_TOL
-    assert rel(gh.cpu().numpy(), want["grad_h"]) < BF16_TOL
+    check_rel("out", out.cpu().numpy(), want["out"])
+    check_rel("grad_h", gh.cpu().numpy(), want["grad_h"])
     np.testing.assert_array_equal(st.download(0, "pair_step"), ref.pair_step(0))
     for name, w0 in (("w_a", w_a), ("w_b", w_b)):
         got, exp = st.download(0, name), ref.get(0, name)
@@ -398,9 +408,9 @@ def test_layer_step_random_geometries_vs_oracle(ctx, seed):
     ref_out, z, _ = O.ffn_forward(h, wak, wbk)
     _, _, ref_gh = O.ffn_backward(gr, h, z, None, wak, wbk)
     if np.linalg.norm(ref_out) > 0:
-        assert rel(out.cpu().numpy(), ref_out) < BF16_TOL
+        check_rel("out", out.cpu().numpy(), ref_out)
     if np.linalg.norm(ref_gh) > 0:
-        assert rel(gh.cpu().numpy(), ref_gh) < BF16_TOL
+        check_rel("grad_h", gh.cpu().numpy(), ref_gh)
     steps = st.download(0, "pair_step")
     assert set(np.nonzero(steps)[0].tolist()) == set(sel["unioned"].tolist())
 
@@ -429,8 +439,8 @@ def test_layer_step_random_large_geometries_vs_oracle(ctx, seed):
     wak, wbk = O.gather_adapter(w_a, w_b, sel["unioned"])
     ref_out, z, _ = O.ffn_forward(h, wak, wbk)
     _, _, ref_gh = O.ffn_backward(gr, h, z, None, wak, wbk)
-    assert rel(out.cpu().numpy(), ref_out) < BF16_TOL
-    assert rel(gh.cpu().numpy(), ref_gh) < BF16_TOL
+    check_rel("out", out.cpu().numpy(), ref_out)
+    check_rel("grad_h", gh.cpu().numpy(), ref_gh)
     steps = st.download(0, "pair_step")
     assert set(np.nonzero(steps)[0].tolist()) == set(sel["unioned"].tolist())
 
@@ -454,7 +464,7 @@ def test_layer_step_union_beyond_one_panel_vs_oracle(ctx):
     wak, wbk = O.gather_adapter(w_a, w_b, sel["unioned"])
     ref_out, z, _ = O.ffn_forward(h, wak, wbk)
     _, gwa, ref_gh = O.ffn_backward(gr, h, z, None, wak, wbk)
-    assert rel(out.cpu().numpy(), ref_out) < BF16_TOL
-    assert rel(gh.cpu().numpy(), ref_gh) < BF16_TOL
+    check_rel("out", out.cpu().numpy(), ref_out)
+    check_rel("grad_h", gh.cpu().numpy(), ref_gh)
     steps = st.download(0, "pair_step")
     assert set(np.nonzero(steps)[0].tolist()) == set(sel["unioned"].tolist())
