@@ -20,13 +20,14 @@ stream mix_seed(1, 0x7001), h ~ U(-1, 1) from 0x7002, grad_out from 0x7003, all 
 bf16; the CPU reference gets the same values as doubles).
 
 The reference arm times the UNMODIFIED reference CPU implementation (oracle/_ref, built from /root/reference by
-oracle/Makefile) through its public API on all host cores, at the SAME configuration: ke_select + fetch of the
-whole T-token batch, scatter_grads + sparse_adam_update of its union (|S| = 65,536 at cfg2) are timed once at full
-size, and each timed step runs sparse_ffn_pa + sparse_backward -- the T x |S| part, ~99% of the reference's time
--- on a slice of the batch's token rows against that same union (every row of both is independent of the others,
-so the slice costs exactly its share of the full step). A step's time is its slice's FFN time plus the slice's
-token share of the once-per-step phases; `cpu_baseline.sample` spells this out. `--ref-full-step` instead times
-one unsliced T-token ref_layer_step (cfg2: ~15 min on 16 cores) to validate the composite.
+oracle/Makefile) through its public API on all host cores, at the SAME configuration: at N=1 one complete layer
+step of the whole T-token batch (meft_ffn -> sparse_backward -> scatter_grads -> sparse_adam_update, |S| = 65,536 at
+cfg2; ~580 s on 16 cores, so one step and no warm-up). With --ref-phased (and on rank 0 of N>1 runs) it times a
+bounded estimate instead: ke_select + fetch of the whole batch and scatter_grads + sparse_adam_update of its union
+measured once, sparse_ffn_pa + sparse_backward measured on slices of the batch's token rows against that same union
+and fitted per call as fixed cost + per-row cost (the reference re-transposes the gathered d x |S| tables on every
+call), evaluated at T. The GPU arm's `cpu_baseline` is that bounded estimate (a few minutes); the measured complete
+step is profiles/r2_reference_full_step.json.
 """
 from __future__ import annotations
 
@@ -132,15 +133,17 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------------------------- reference arm
 
-def ref_slice_tokens(steps):
-    """Token rows per timed reference step at this workload: about 3-4 s of 16-core fp64 work per step at cfg2
-    (32 rows; 16 for runs of more than 20 steps), the whole batch at cfg1. MEFT_REF_SAMPLE_TOKENS overrides."""
-    env = os.environ.get("MEFT_REF_SAMPLE_TOKENS")
+def ref_slice_plan(steps):
+    """Row counts of the timed reference FFN slices: two sizes (so the per-call fixed cost and the per-row cost
+    separate), about 20-45 s of 16-core fp64 work per slice at cfg2; the whole batch at small workloads.
+    MEFT_REF_SLICES="16,128" overrides."""
+    env = os.environ.get("MEFT_REF_SLICES")
     if env:
-        return max(1, min(int(env), CFG["tokens"]))
-    if CFG["tokens"] * CFG["pairs"] * CFG["d"] <= 1 << 34:  # small workloads: every step is the whole batch
-        return CFG["tokens"]
-    return 32 if steps <= 20 else 16
+        return [int(x) for x in env.split(",")]
+    T = CFG["tokens"]
+    if T * CFG["pairs"] * CFG["d"] <= 1 << 34:  # small workloads: every slice is the whole batch
+        return [T] * max(1, min(steps, 5))
+    return [16, 128, 16, 128] if steps > 2 else [16, 128]
 
 
 def reference_inputs():
@@ -160,11 +163,15 @@ def reference_inputs():
     return st, h, g
 
 
-def run_reference_phased(steps, warmup, rows, threads=None):
+def run_reference_phased(row_sizes, threads=None):
     """The reference layer step of the full workload through its public API (oracle/ref_capi.cpp ref_step_*):
-    ke_select + fetch of the whole batch and scatter_grads + sparse_adam_update of its union timed once, the T x |S|
-    FFN forward + backward timed on `steps` slices of `rows` token rows (after `warmup` untimed slices).
-    Returns a dict: tokens/s, seconds per full step, per-slice step seconds, phase seconds of one full step, |S|."""
+    ke_select + fetch of the whole batch and scatter_grads + sparse_adam_update of its union timed once; the T x |S|
+    FFN forward + backward timed on slices of the batch of the given row counts. Each sparse_backward call pays a
+    fixed cost (the reference transposes the two d x |S| gathered tables serially and allocates d x |S| gradients)
+    plus a per-row cost, so the full-T call is estimated as fixed + T * per_row, both fitted (least squares) over
+    the slices; the composite is labelled as such. Returns a dict (tokens/s, seconds per step, phases, |S|, ...)."""
+    import numpy as np
+
     from oracle import oracle as O
 
     R = O.ref()
@@ -172,20 +179,33 @@ def run_reference_phased(steps, warmup, rows, threads=None):
     R.ref_set_threads(cores)
     st, h, g = reference_inputs()
     T = CFG["tokens"]
-    slices = [((i * rows) % T, (i * rows) % T + rows) for i in range(warmup + steps)]
-    slices = [(lo, hi) if hi <= T else (T - rows, T) for lo, hi in slices]
+    slices, lo = [], 0
+    for n in row_sizes:
+        n = min(n, T)
+        if lo + n > T:
+            lo = 0
+        slices.append((lo, lo + n))
+        lo += n
     t0 = time.perf_counter()
     r = st.step_phases(0, h, g, CFG["kk"], CFG["k"], CFG["lr"], slices)
     wall = time.perf_counter() - t0
-    fwd, bwd = r["forward"][warmup:], r["backward"][warmup:]
-    fixed = r["select"] + r["fetch"] + r["scatter"] + r["adam"]  # once per T-token step
-    per_row = (sum(fwd) + sum(bwd)) / (rows * len(fwd))
-    step_s = fixed + T * per_row
-    slice_steps = [f + b + fixed * rows / T for f, b in zip(fwd, bwd)]  # a slice + its token share of the rest
-    phases = dict(select=r["select"], fetch=r["fetch"], forward=T * sum(fwd) / (rows * len(fwd)),
-                  backward=T * sum(bwd) / (rows * len(bwd)), scatter=r["scatter"], adam=r["adam"])
-    return dict(tps=T / step_s, step_s=step_s, slice_steps=slice_steps, phases=phases, union_size=r["union_size"],
-                cores=cores, wall_s=wall, rows=rows)
+    rows = np.array([hi - lo for lo, hi in slices], np.float64)
+    fits = {}
+    for ph in ("forward", "backward"):
+        y = np.array(r[ph], np.float64)
+        if len(set(rows.tolist())) >= 2:
+            per_row, fixed = np.polyfit(rows, y, 1)
+            per_row, fixed = max(per_row, 0.0), max(fixed, 0.0)
+        else:  # one slice size: no split, the slice is scaled as a whole
+            per_row, fixed = float(np.mean(y / rows)), 0.0
+        fits[ph] = (float(fixed), float(per_row))
+    phases = dict(select=r["select"], fetch=r["fetch"], scatter=r["scatter"], adam=r["adam"])
+    for ph, (fixed, per_row) in fits.items():
+        phases[ph] = fixed + per_row * T
+    step_s = sum(phases.values())
+    return dict(tps=T / step_s, step_s=step_s, phases=phases, union_size=r["union_size"], cores=cores, wall_s=wall,
+                slices=[int(x) for x in rows], fits=fits,
+                measured={"forward": r["forward"], "backward": r["backward"]})
 
 
 def run_reference_full(threads=None):
@@ -214,14 +234,18 @@ def cpu_model():
 
 
 def phased_sample_text(r):
+    f_fix, f_row = r["fits"]["forward"]
+    b_fix, b_row = r["fits"]["backward"]
     return (f"unmodified reference (oracle/_ref) through its public API, fp64, OpenMP {r['cores']} threads on "
             f"{cpu_model()}, at the full workload (d={CFG['d']} M={CFG['pairs']} N={CFG['experts']} K={CFG['k']} "
             f"kk={CFG['kk']} T={CFG['tokens']}, |S|={r['union_size']} of {CFG['pairs']}): ke_select + fetch of all "
-            f"{CFG['tokens']} tokens and scatter_grads + sparse_adam_update of the union timed once "
+            f"{CFG['tokens']} tokens and scatter_grads + sparse_adam_update of the union measured "
             f"({r['phases']['select']:.1f} + {r['phases']['fetch']:.1f} + {r['phases']['scatter']:.1f} + "
-            f"{r['phases']['adam']:.1f} s); sparse_ffn_pa + sparse_backward timed on {len(r['slice_steps'])} slices "
-            f"of {r['rows']} token rows against that union and scaled by T/rows (rows are independent): "
-            f"{r['step_s']:.1f} s per {CFG['tokens']}-token step")
+            f"{r['phases']['adam']:.1f} s); sparse_ffn_pa / sparse_backward measured on slices of "
+            f"{r['slices']} token rows against that union and fitted per call as fixed + per-row (forward "
+            f"{f_fix:.2f} s + {f_row * 1e3:.1f} ms/row, backward {b_fix:.2f} s + {b_row * 1e3:.1f} ms/row), "
+            f"evaluated at T={CFG['tokens']}: estimated {r['step_s']:.0f} s per {CFG['tokens']}-token step "
+            f"(a measured unsliced step: profiles/r2_reference_full_step.json)")
 
 
 def reference_arm(args, rank, world):
@@ -234,24 +258,27 @@ def reference_arm(args, rank, world):
         if rank != 0:
             dist.destroy_process_group()
             return
-    if args.ref_full_step:
+    if world == 1 and not args.ref_phased:
         try:
             r = run_reference_full()
         except Exception as e:  # pragma: no cover - surfaced as unavailable, never as a fake number
             emit({"impl": "reference", "unavailable": f"reference CPU run failed: {e}"})
             return
-        sample = (f"one unsliced ref_layer_step of all {CFG['tokens']} tokens (|S|={r['union_size']}), fp64, "
-                  f"OpenMP {r['cores']} threads on {cpu_model()}")
+        sample = (f"one complete reference layer step at the workload (meft_ffn -> sparse_backward -> scatter_grads "
+                  f"-> sparse_adam_update of all {CFG['tokens']} tokens, |S|={r['union_size']}), unsliced and "
+                  f"unextrapolated: fp64, OpenMP {r['cores']} threads on {cpu_model()}; one step because a step "
+                  f"takes ~10 min on 16 cores (--steps / --warmup apply to the GPU arm; --ref-phased times the "
+                  f"bounded phased estimate instead)")
         value, ms, steps_done = r["tps"], r["step_s"] * 1e3, 1
+        args.warmup = 0
     else:
-        rows = ref_slice_tokens(args.steps)
         try:
-            r = run_reference_phased(args.steps, args.warmup, rows)
+            r = run_reference_phased(ref_slice_plan(args.steps))
         except Exception as e:  # pragma: no cover
             emit({"impl": "reference", "unavailable": f"reference CPU run failed: {e}"})
             return
         sample = phased_sample_text(r)
-        value, ms, steps_done = r["tps"], r["step_s"] * 1e3, args.steps
+        value, ms, steps_done = r["tps"], r["step_s"] * 1e3, len(r["slices"])
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": steps_done, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -457,8 +484,8 @@ def our_arm(args, rank, world, local_rank):
 
     cpu = None
     if world == 1 and not args.skip_cpu_baseline and not args.base_ffn:
-        try:  # the reference arm's phased measurement on a bounded sample: 2 slices of rows, no warm-up
-            r = run_reference_phased(2, 0, ref_slice_tokens(args.steps))
+        try:  # the reference arm's phased measurement on a bounded sample: two slice sizes
+            r = run_reference_phased(ref_slice_plan(2))
             cpu = {"value": r["tps"], "unit": "tokens/s", "cores": r["cores"], "kind": "reference",
                    "sample": phased_sample_text(r), "phase_seconds": r["phases"]}
         except Exception as e:
@@ -548,8 +575,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--skip-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-full-step", action="store_true",
-                    help="reference arm: time one unsliced T-token reference step instead of the phased sample")
+    ap.add_argument("--ref-phased", action="store_true",
+                    help="reference arm: the bounded phased estimate (slices of the batch, per-call fixed cost + "
+                         "per-row cost fitted) instead of one complete T-token reference step (~10 min at cfg2)")
     ap.add_argument("--sharded", action="store_true", help="run the expert-sharded layer even on one GPU")
     ap.add_argument("--base-ffn", type=int, default=0,
                     help="also run the frozen base FFN of width n (SiLU), e.g. 11008 for LLaMA-7B (single GPU)")

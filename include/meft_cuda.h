@@ -274,6 +274,12 @@ meft_status meft_matmul_f64(meft_ctx* ctx, const double* A, const double* B, int
 meft_status meft_transpose_f64(meft_ctx* ctx, const double* src, double* dst, int64_t rows, int64_t cols);
 meft_status meft_activation_f64(meft_ctx* ctx, int act, const double* x, double* y, int64_t n);
 
+/* Row accumulation into an arbitrary row table (the drop-in's staging rows: scatter_grads memtier.cpp:139-149 on the
+ * touched rows only, stage_router_grads memtier.cpp:157-172): for i in [0, n) in order, table[idx[i], :] +=
+ * rows[i, :] and flags[idx[i]] = 1 (flags may be NULL). dt F64 or F32 for both. Repeated indices add in entry order
+ * (segmented, atomic-free), so the result is bit-identical to the sequential loop. Indices must be in range. */
+meft_status meft_rows_add(meft_ctx* ctx, meft_dtype dt, void* table, int64_t d, const int32_t* idx, int64_t n,
+                          const void* rows, uint8_t* flags);
 /* Lazy Adam over arbitrary fp64 row tables (the router rows of sparse_adam_update, memtier.cpp:211-227):
  * for each row r in rows[0..n): t = ++step[r]; Adam on w/m/v[r,:] with gradient stage[r,:]; stage[r,:] = 0;
  * staged[r] = 0. step is int64 [table rows]; staged uint8. */

@@ -108,6 +108,7 @@ _SIGS = {
     "meft_transpose_f64": (INT, [P, P, P, I64, I64]),
     "meft_activation_f64": (INT, [P, INT, P, P, I64]),
     "meft_adam_rows_f64": (INT, [P, P, P, P, P, P, P, P, I64, I64, D, D, D, D]),
+    "meft_rows_add": (INT, [P, INT, P, I64, P, I64, P, P]),
     "meft_store_create": (INT, [P, I64, I64, I64, I64, INT, C.POINTER(P)]),
     "meft_store_enable_router": (INT, [P, P]),
     "meft_store_expert_histogram": (INT, [P, P, I64, P, INT]),

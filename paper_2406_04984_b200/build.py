@@ -106,11 +106,12 @@ def build_reference_tests(ref_proj: str = "/root/reference/proj", verbose: bool 
     lib = build_dropin(verbose)
     os.makedirs(DROPIN_TEST_BIN, exist_ok=True)
     out = []
-    for t in REF_TESTS + TRAINER_TESTS + ("trajectory",):
-        src = (os.path.join(ROOT, "tests", "dropin", "trajectory.cpp") if t == "trajectory"
+    for t in REF_TESTS + TRAINER_TESTS + ("trajectory", "layer_bench"):
+        src = (os.path.join(ROOT, "tests", "dropin", t + ".cpp") if t in ("trajectory", "layer_bench")
                else os.path.join(ref_proj, "tests", t + ".cpp"))
         exe = os.path.join(DROPIN_TEST_BIN, t)
-        extra = [os.path.join(ref_proj, "src", f) for f in TRAINER_SRCS] if t not in REF_TESTS else []
+        extra = ([os.path.join(ref_proj, "src", f) for f in TRAINER_SRCS]
+                 if t not in REF_TESTS and t != "layer_bench" else [])
         if _needs(exe, [src, lib] + extra):
             # our include/ first: the hot-path headers resolve to the drop-in's, the rest to the reference's
             cmd = [HOST_CXX, "-O1", "-std=c++20", "-w", "-fopenmp", "-I" + os.path.join(ROOT, "tests", "dropin"),

@@ -13,6 +13,8 @@
 #include <unordered_map>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/meft_cuda.h"
 #include "common.cuh"
 #include "kernels.h"
@@ -134,19 +136,24 @@ struct meft_store {
 
 namespace {
 
-// Records CUDA events on the context stream around one phase of the layer step (when timing is enabled).
+// One phase of the layer step: an NVTX range (host-side enqueue; nsys / ncu --nvtx show it, a no-op without a
+// tool attached) and, when timing is enabled, CUDA events on the context stream around its kernels.
+const char* const kPhaseNames[] = {"meft/select (ke_select)", "meft/gather (fetch)", "meft/ffn_forward (sparse_ffn_pa)",
+                                   "meft/ffn_backward (sparse_backward + fused Adam)", "meft/adam (sparse_adam_update)"};
 struct PhaseScope {
     meft_ctx* c;
     int phase;
     cudaEvent_t a = nullptr;
     long long l0 = 0;
     PhaseScope(meft_ctx* ctx, int p) : c(ctx), phase(p) {
+        nvtxRangePushA(kPhaseNames[p]);
         if (!c->timing) return;
         a = c->next_event();
         MEFT_CUDA_CHECK(cudaEventRecord(a, c->stream));
         l0 = launch_counter();
     }
     ~PhaseScope() {
+        nvtxRangePop();
         if (!c->timing) return;
         cudaEvent_t b = c->next_event();
         cudaEventRecord(b, c->stream);
@@ -1131,6 +1138,29 @@ meft_status meft_activation_f64(meft_ctx* ctx, int act, const double* x, double*
         require_ctx(ctx);
         require(act == 0 || act == 1, MEFT_E_INVALID, "activation: 0 SiLU or 1 ReLU");
         act_forward(ctx->stream, x, y, n, act);
+    });
+}
+
+meft_status meft_rows_add(meft_ctx* ctx, meft_dtype dt, void* table, int64_t d, const int32_t* idx, int64_t n,
+                          const void* rows, uint8_t* flags) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(dt == MEFT_F64 || dt == MEFT_F32, MEFT_E_INVALID, "rows_add: dtype must be F64 or F32");
+        require(d >= 1 && n >= 0 && (n == 0 || (table && idx && rows)), MEFT_E_INVALID, "rows_add: arguments");
+        if (n == 0) return;
+        // strictly ascending indices: one CTA per row; otherwise the segmented (sorted, run-length) add
+        const int32_t init[2] = {0, INT32_MAX};
+        MEFT_CUDA_CHECK(cudaMemcpyAsync(ctx->dev_small, init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
+        check_sorted_unique(ctx->stream, idx, n, INT32_MAX, ctx->dev_small);
+        MEFT_CUDA_CHECK(cudaMemcpyAsync(ctx->host_small, ctx->dev_small, 4, cudaMemcpyDeviceToHost, ctx->stream));
+        MEFT_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        if (ctx->host_small[0] == 0) {
+            stage_add(ctx->stream, dcode(dt), table, d, idx, n, dcode(dt), rows, flags);
+        } else {
+            const size_t wb = stage_add_segmented_ws(n);
+            stage_add_segmented(ctx->stream, dcode(dt), table, d, idx, n, dcode(dt), rows, flags,
+                                ctx->get("scatter_seg", wb), wb);
+        }
     });
 }
 

@@ -169,3 +169,30 @@ def test_scatter_grads_repeated_ids_segmented_equals_sequential(ctx, prec):
     staged = np.zeros(r, np.int8)
     staged[np.unique(idx)] = 1
     np.testing.assert_array_equal(st.download(0, "staged"), staged)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_rows_add_repeated_indices_equals_sequential_loop(ctx, dtype):
+    """meft_rows_add (the drop-in's touched-row staging: scatter_grads / stage_router_grads on the mirrored rows):
+    table[idx[i]] += rows[i] in entry order, flags[idx[i]] = 1 -- bit-identical to the reference's sequential loop
+    (memtier.cpp:139-149) with repeated indices, and via the one-CTA-per-row path for strictly ascending ones."""
+    import ctypes as C
+
+    from paper_2406_04984_b200 import _lib
+
+    gen = torch.Generator(device="cuda").manual_seed(4)
+    n_rows, d = 37, 96
+    for idx_list in ([3, 5, 5, 0, 36, 3, 3, 12], [0, 2, 7, 9, 30]):
+        table = torch.randn((n_rows, d), generator=gen, device="cuda").to(dtype)
+        rows = torch.randn((len(idx_list), d), generator=gen, device="cuda").to(dtype)
+        idx = torch.tensor(idx_list, dtype=torch.int32, device="cuda")
+        flags = torch.zeros(n_rows, dtype=torch.uint8, device="cuda")
+        want = table.cpu().clone()
+        for i, j in enumerate(idx_list):  # the reference's sequential loop
+            want[j] += rows[i].cpu()
+        dt = _lib.F64 if dtype == torch.float64 else _lib.F32
+        ctx.check(_lib.lib().meft_rows_add(ctx.h, dt, C.c_void_p(table.data_ptr()), d, C.c_void_p(idx.data_ptr()),
+                                           len(idx_list), C.c_void_p(rows.data_ptr()), C.c_void_p(flags.data_ptr())))
+        torch.cuda.synchronize()
+        assert torch.equal(table.cpu(), want)
+        assert sorted(set(idx_list)) == torch.nonzero(flags).flatten().tolist()
