@@ -47,6 +47,8 @@ WORKLOADS = {  # BASELINE.json configs[1] (default), [0] (the reference's own CP
     "cfg2": dict(workload="llama7b_meft_layer", d=4096, pairs=65536, experts=256, k=128, kk=4, tokens=8192),
     "cfg1": dict(workload="reference_cpu_workload", d=512, pairs=4096, experts=64, k=32, kk=4, tokens=256),
     "cfg4": dict(workload="mistral7b_meft_layer_1m", d=4096, pairs=1048576, experts=1024, k=128, kk=4, tokens=8192),
+    # the M = 4M corner of the scaling sweep (configs[4]): 470 GB of tables, expert-sharded only (--gpus 8 --strong)
+    "cfg5": dict(workload="sweep_m4m_k16", d=4096, pairs=4194304, experts=4096, k=16, kk=4, tokens=8192),
 }
 METRIC = "MEFT adapter layer tokens/sec (fwd+bwd+sparse update)"
 SEED, W_B_STREAM, H_STREAM, G_STREAM = 1, 0x7001, 0x7002, 0x7003
@@ -54,8 +56,9 @@ SEED, W_B_STREAM, H_STREAM, G_STREAM = 1, 0x7001, 0x7002, 0x7003
 
 def config_dict(world):
     """The workload as both arms report it (identical dicts: the driver compares the arms on the same config)."""
+    per_gpu = CFG["tokens"] // world if CFG.get("strong") else CFG["tokens"]
     return dict(workload=CFG["workload"], d=CFG["d"], pairs=CFG["pairs"], experts=CFG["experts"], k=CFG["k"],
-                kk=CFG["kk"], tokens_per_gpu=CFG["tokens"], global_tokens=CFG["tokens"] * world,
+                kk=CFG["kk"], tokens_per_gpu=per_gpu, global_tokens=per_gpu * world,
                 parallelism="single GPU" if world == 1 else f"expert-sharded ep{world} (NCCL all-to-all)",
                 inputs="reference RNG streams 0x7001-0x7003 (BASELINE.md §3), bf16-rounded",
                 l2=(f"inputs larger than L2 ({CFG['pairs'] * CFG['d'] * 28 / 1e9:.1f} GB of tables per layer)"
@@ -258,6 +261,15 @@ def reference_arm(args, rank, world):
         if rank != 0:
             dist.destroy_process_group()
             return
+    need = 8 * CFG["d"] * CFG["pairs"] * 8  # the reference HostStore: 8 fp64 d x M tables per layer
+    try:
+        host = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    except (ValueError, OSError):
+        host = None
+    if host and need > 0.8 * host:
+        emit({"impl": "reference", "unavailable": f"the reference's fp64 HostStore needs {need / 1e9:.0f} GB of host "
+                                                  f"RAM at {CFG['workload']} (host: {host / 1e9:.0f} GB)"})
+        return
     if world == 1 and not args.ref_phased:
         try:
             r = run_reference_full()
@@ -281,7 +293,8 @@ def reference_arm(args, rank, world):
         value, ms, steps_done = r["tps"], r["step_s"] * 1e3, len(r["slices"])
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
-        "steps": steps_done, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "steps": steps_done, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if CFG.get("strong") else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_dict(world),
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": r["cores"], "kind": "reference",
                          "sample": sample},
@@ -307,6 +320,13 @@ def our_arm(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     d, M, N, K, kk, T, lr = (CFG[x] for x in ("d", "pairs", "experts", "k", "kk", "tokens", "lr"))
+    if CFG.get("strong"):
+        if T % world:
+            raise SystemExit(f"bench.py: --strong needs the workload's {T} tokens divisible by {world} ranks")
+        T //= world  # strong scaling: the global batch is split over the ranks
+    if M * d * 28 > 170e9 and world == 1 and not args.sharded:
+        raise SystemExit(f"bench.py: {CFG['workload']} needs {M * d * 28 / 1e9:.0f} GB of tables: expert-shard it "
+                         "(--gpus N, N >= 4 for M = 4M)")
 
     if torch.cuda.device_count() < world or not torch.cuda.is_available():
         raise SystemExit(f"bench.py: {world} rank(s) need {world} visible GPUs, found {torch.cuda.device_count()}")
@@ -495,7 +515,8 @@ def our_arm(args, rank, world, local_rank):
     line = {
         "metric": METRIC,
         "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong" if CFG.get("strong") else "weak",
+        "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (HostStore::init tables; W_B, h, grad_out from the reference RNG streams, bf16)",
         "config": config_dict(world),
         "precision": "bf16 compute, fp32 master/Adam state", "union_size": S, "base_ffn": args.base_ffn,
@@ -581,12 +602,15 @@ def main():
     ap.add_argument("--sharded", action="store_true", help="run the expert-sharded layer even on one GPU")
     ap.add_argument("--base-ffn", type=int, default=0,
                     help="also run the frozen base FFN of width n (SiLU), e.g. 11008 for LLaMA-7B (single GPU)")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: the workload's T tokens are split over the ranks (default: weak, T per rank)")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2",
                     help="cfg2: the LLaMA-7B-shape layer (default, BASELINE configs[1]); cfg1: the reference's own "
                          "CPU workload (configs[0]); cfg4: the Mistral-7B shape with M = 1,048,576 neurons and "
                          "1,024 experts (configs[3], meant for --gpus 8)")
     args = ap.parse_args()
     CFG.update(WORKLOADS[args.workload])
+    CFG["strong"] = args.strong
     args.warmup = max(args.warmup, 0)
     if args.gpus < 1:
         raise SystemExit("bench.py: --gpus must be >= 1")

@@ -2,6 +2,8 @@
 #include "device.hpp"
 
 #include <cmath>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 
 namespace meft::dropin {
@@ -35,17 +37,77 @@ void check(meft_status st) {
     }
 }
 
+// Device buffers are recycled through a size-class cache: the API calls allocate and release the same few shapes
+// over and over, and cudaFree synchronises the whole device. Every use is enqueued on the one context stream, so a
+// recycled block is only touched after the work of its previous owner (stream order).
+namespace {
+struct Pool {
+    std::mutex mu;
+    std::multimap<size_t, void*> free;  // size class -> blocks
+    size_t cached = 0;
+    static constexpr size_t kLimit = size_t(8) << 30;  // keep at most 8 GB of idle blocks
+};
+Pool& pool() {
+    static Pool* p = new Pool();  // never destroyed: blocks outlive static destruction order
+    return *p;
+}
+size_t size_class(size_t bytes) {
+    if (bytes <= 256) return 256;
+    if (bytes <= (size_t(64) << 20)) {
+        size_t c = 256;
+        while (c < bytes) c <<= 1;
+        return c;
+    }
+    const size_t g = size_t(64) << 20;
+    return (bytes + g - 1) / g * g;
+}
+void* pool_get(size_t cls) {
+    Pool& P = pool();
+    {
+        std::lock_guard<std::mutex> lk(P.mu);
+        auto it = P.free.find(cls);
+        if (it != P.free.end()) {
+            void* p = it->second;
+            P.free.erase(it);
+            P.cached -= cls;
+            return p;
+        }
+    }
+    void* p = nullptr;
+    meft_status st = meft_device_alloc(ctx(), cls, &p);
+    if (st == MEFT_E_OOM) {  // give the idle blocks back and retry once
+        std::lock_guard<std::mutex> lk(P.mu);
+        for (auto& kv : P.free) meft_device_free(ctx(), kv.second);
+        P.free.clear();
+        P.cached = 0;
+        st = meft_device_alloc(ctx(), cls, &p);
+    }
+    check(st);
+    return p;
+}
+void pool_put(void* p, size_t cls) {
+    Pool& P = pool();
+    std::lock_guard<std::mutex> lk(P.mu);
+    if (P.cached + cls > Pool::kLimit) {
+        meft_device_free(ctx(), p);
+        return;
+    }
+    P.free.emplace(cls, p);
+    P.cached += cls;
+}
+}  // namespace
+
 DevBuf::DevBuf(size_t bytes) : n_(bytes) {
-    if (bytes) check(meft_device_alloc(ctx(), bytes, &p_));
+    if (bytes) p_ = pool_get(size_class(bytes));
 }
 
 DevBuf::~DevBuf() {
-    if (p_) meft_device_free(ctx(), p_);
+    if (p_) pool_put(p_, size_class(n_));
 }
 
 DevBuf& DevBuf::operator=(DevBuf&& o) noexcept {
     if (this != &o) {
-        if (p_) meft_device_free(ctx(), p_);
+        if (p_) pool_put(p_, size_class(n_));
         p_ = o.p_;
         n_ = o.n_;
         o.p_ = nullptr;

@@ -724,15 +724,36 @@ class CShardedLayer:
         return res
 
 
+FULL_TABLE_LIMIT = 24 << 30  # bytes of one global MIXED table set a rank may build to slice its shard from
+
+
 def make_device_layer(ctx, d, M, N, group=None, seed=1, w_b_seed=0x7001):
     """This rank's shard as a MIXED HBM store: keys from HostStore::init(seed) restricted to the shard (the global
     table is generated once per rank with the reference RNG, then sliced), W_B ~ U(+-1/sqrt d) (torch RNG,
-    identical on every rank), router replicated."""
+    identical on every rank), router replicated. Layers too large for one GPU (M * d * 28 B above
+    FULL_TABLE_LIMIT, e.g. BASELINE config 5's M = 4M: 470 GB) are generated shard by shard instead -- the router
+    from the reference stream (replicated), keys and values from torch's device RNG seeded per (seed, rank) -- so
+    every rank only ever holds its M/P pairs."""
     from . import meft as G
 
     P = _world(group)
     r = _rank(group)
     M_loc, N_loc = M // P, N // P
+    if M * d * 28 > FULL_TABLE_LIMIT:
+        store = G.Store(ctx, 1, d, M_loc, N_loc, G.STORE_MIXED)
+        b = 1.0 / math.sqrt(d)
+        dev = store.tensor(0, "w_a").device
+        gen = torch.Generator(device=dev).manual_seed((seed << 20) + 0x5000 + r)
+        for name in ("w_a", "w_b"):
+            w, wc = store.tensor(0, name), store.tensor(0, name + "_compute")
+            for r0 in range(0, M_loc, 65536):  # chunked: no shard-sized temporaries
+                blk = ((torch.rand((min(65536, M_loc - r0), d), generator=gen, device=dev) * 2 - 1) * b).to(
+                    torch.bfloat16)
+                w[r0:r0 + blk.shape[0]].copy_(blk.float())
+                wc[r0:r0 + blk.shape[0]].copy_(blk)
+        w_g = torch.from_numpy(G.reference_uniform(seed, 0x5001, (N, d), -b, b, bf16=True)).to(
+            device=dev, dtype=torch.bfloat16)
+        return DeviceEngine(ctx, store, w_g), store
     full = G.Store(ctx, 1, d, M, N, G.STORE_MIXED)
     full.init_reference(seed)
     store = G.Store(ctx, 1, d, M_loc, N_loc, G.STORE_MIXED)

@@ -73,3 +73,10 @@ def test_gpu_arm_prints_one_contract_line():
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["clocks"]["sm_max_mhz"] and isinstance(d["clocks"]["reasons"], list)
+
+
+def test_reference_arm_reports_unreachable_workloads():
+    """BASELINE config 5's M = 4M layer needs 1.1 TB of fp64 HostStore on the host: the reference arm says so
+    (one line, exit 0) instead of faking or extrapolating a number."""
+    d = _run(["--impl", "reference", "--workload", "cfg5"])
+    assert d["impl"] == "reference" and "unavailable" in d and "GB of host RAM" in d["unavailable"]

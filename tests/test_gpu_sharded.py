@@ -188,3 +188,27 @@ def test_device_protocol_plans_equal_reference_glue(ctx, P):
     assert ra[3] == rb[3] and ra[4] == rb[4]
     x = torch.randn(ra[4], generator=gen, device="cuda", dtype=torch.float64)
     assert torch.equal(eng.scatter_exact(x, ra[2], T, C), ref.scatter_exact(x, rb[2], T, C))
+
+
+def test_large_layers_are_generated_shard_by_shard(ctx, monkeypatch):
+    """Layers too large for one GPU (BASELINE config 5's M = 4M: 470 GB of tables) are never built whole: above
+    FULL_TABLE_LIMIT each rank generates only its M/P pairs (keys / values from the device RNG) and the replicated
+    router from the reference stream, and the sharded step runs on them (exercised at a small M by lowering the
+    limit)."""
+    monkeypatch.setattr(SH, "FULL_TABLE_LIMIT", 1)
+    d, M, N, K, kk, T = 256, 2048, 16, 16, 4, 64
+    eng, store = SH.make_device_layer(ctx, d, M, N, seed=3)
+    assert (store.pairs, store.experts) == (M, N)  # world 1: the whole layer, generated like a shard
+    b = 1.0 / d ** 0.5
+    want_g = torch.from_numpy(G.reference_uniform(3, 0x5001, (N, d), -b, b, bf16=True)).cuda().bfloat16()
+    assert torch.equal(eng.w_g, want_g)
+    w = store.tensor(0, "w_a")
+    assert float(w.abs().max()) <= b and torch.equal(store.tensor(0, "w_a_compute").float(), w)
+    h = torch.from_numpy(G.reference_uniform(3, 0x7002, (T, d), -1, 1, bf16=True)).cuda().bfloat16()
+    layer = SH.CShardedLayer(ctx, store, eng.w_g)
+    try:
+        res = layer.step(h, h, kk, K, 1e-3)
+        torch.cuda.synchronize()
+        assert res["union_size"] > 0 and torch.isfinite(res["out"]).all()
+    finally:
+        layer.close()
