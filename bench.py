@@ -340,7 +340,7 @@ def our_arm(args, rank, world, local_rank):
     grad_h = torch.empty((T, d), dtype=torch.float32, device=dev)
     sharded = world > 1 or args.sharded
     if not sharded:
-        store = G.Store(ctx, 1, d, M, N, G.STORE_MIXED)
+        store = G.Store(ctx, 1, d, M, N, G.STORE_COMPACT if args.precision == "compact" else G.STORE_MIXED)
         store.init_reference(seed=SEED)  # HostStore::init tables (reference RNG streams 0x5000/0x5001)
         b = 1.0 / math.sqrt(d)
         if M * d <= 1 << 28:  # W_B ~ U(+-1/sqrt d) from stream 0x7001, bf16-rounded
@@ -478,7 +478,8 @@ def our_arm(args, rank, world, local_rank):
     # + write w,m,v fp32 + bf16 copy = 26 B/entry); MEFT_ADAM_EPILOGUE=0 runs the separate pass over a gradient
     # block (+ the gradient read: 30 B/entry)
     adam_fused = os.environ.get("MEFT_ADAM_EPILOGUE", "1") != "0"
-    adam_bytes = 2 * S * d * (26.0 if adam_fused else 30.0)  # key and value rows
+    per_entry = (26.0 if adam_fused else 30.0) - (8.0 if args.precision == "compact" else 0.0)  # bf16 m, v: -8 B
+    adam_bytes = 2 * S * d * per_entry  # key and value rows
     gather_bytes = 2 * S * d * 2 * 2.0
     adam_ms = phases["adam"][0] / args.steps
     gather_ms = phases["gather"][0] / args.steps
@@ -519,7 +520,9 @@ def our_arm(args, rank, world, local_rank):
         "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (HostStore::init tables; W_B, h, grad_out from the reference RNG streams, bf16)",
         "config": config_dict(world),
-        "precision": "bf16 compute, fp32 master/Adam state", "union_size": S, "base_ffn": args.base_ffn,
+        "precision": "bf16 compute, fp32 master weights, " + ("bf16 Adam moments (COMPACT)" if args.precision ==
+                                                                  "compact" else "fp32 Adam moments"),
+        "union_size": S, "base_ffn": args.base_ffn,
         "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": 2 * T * d * 2,
                 "d2h_bytes_per_step": 2 * T * d * 4, "ms_per_step": e2e_s * 1e3,
                 "path": "meft_layer_step_host (C ABI, pinned host buffers)" if not sharded else
@@ -602,6 +605,8 @@ def main():
     ap.add_argument("--sharded", action="store_true", help="run the expert-sharded layer even on one GPU")
     ap.add_argument("--base-ffn", type=int, default=0,
                     help="also run the frozen base FFN of width n (SiLU), e.g. 11008 for LLaMA-7B (single GPU)")
+    ap.add_argument("--precision", choices=["mixed", "compact"], default="mixed",
+                    help="store precision: fp32 Adam moments (default) or bf16 moments (COMPACT, opt-in)")
     ap.add_argument("--strong", action="store_true",
                     help="strong scaling: the workload's T tokens are split over the ranks (default: weak, T per rank)")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2",
