@@ -389,7 +389,7 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
                        cudaEvent_t grad_h_done = nullptr, const std::function<void()>* between = nullptr,
                        const meft_peer_out* peer = nullptr, const GemmEpilogue* epi_values = nullptr,
                        const GemmEpilogue* epi_keys = nullptr, const uint32_t* act_bits = nullptr,
-                       int64_t panel = 0) {
+                       int64_t panel = 0, const void* gT = nullptr, const void* hT = nullptr) {
     cudaStream_t st = ctx->stream;
     if (dt == MEFT_F64) {
         const double* gd = static_cast<const double*>(g);
@@ -471,12 +471,15 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
         e4.c = grad_values_s;
     }
     e4.ldc = d;
-    gemm_bf16(st, s, d, T, knob_a(op(z, ld_z, true), G_GWB), knob_b(GemmOperand{g, d, true}, G_GWB),
+    // grad-W B operands: g / h as stored ([T x d], MN-major) or their [d x T] transposes (K-major) when given
+    const GemmOperand gB = gT ? GemmOperand{gT, T, false} : GemmOperand{g, d, true};
+    const GemmOperand hB = hT ? GemmOperand{hT, T, false} : GemmOperand{h, d, true};
+    gemm_bf16(st, s, d, T, knob_a(op(z, ld_z, true), G_GWB), knob_b(gB, G_GWB),
               knob_e(epi_values ? *epi_values : e4, G_GWB));
     if (between) (*between)();  // e.g. consume grad_values before grad_keys reuses its buffer
     GemmEpilogue e5 = e4;  // grad_keys = masked^T h
     e5.c = S_rows ? stage_keys : grad_keys_s;
-    gemm_bf16(st, s, d, T, knob_a(op(masked, ld_z, true), G_GWA), knob_b(GemmOperand{h, d, true}, G_GWA),
+    gemm_bf16(st, s, d, T, knob_a(op(masked, ld_z, true), G_GWA), knob_b(hB, G_GWA),
               knob_e(epi_keys ? *epi_keys : e5, G_GWA));
 }
 
@@ -1770,9 +1773,22 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
         const GemmEpilogue ev = adam_epi(false), ek = adam_epi(true);
         {
             PhaseScope ps(ctx, 3);
+            // MEFT_GW_KMAJOR=1: the grad-W GEMMs read [d x T] transposes of g and h (K-major B) -- an A/B knob
+            static const bool kmajor = [] {
+                const char* v = std::getenv("MEFT_GW_KMAJOR");
+                return v && v[0] == '1';
+            }();
+            void* gT = nullptr;
+            void* hT = nullptr;
+            if (kmajor && su > 0) {
+                gT = ctx->get("gT", size_t(T * d) * 2);
+                hT = ctx->get("hT", size_t(T * d) * 2);
+                transpose2(st, g, gT, T, d);
+                transpose2(st, h, hT, T, d);
+            }
             ffn_backward_impl(ctx, MEFT_BF16, g, h, act, ks, vs, T, d, su, ld, masked, nullptr, nullptr, ghb,
                               base != nullptr, nullptr, nullptr, nullptr, rg, gh_done, nullptr, peer, &ev, &ek,
-                              act_bits, panel);
+                              act_bits, panel, gT, hT);
         }
         train_router();
         if (stats) {

@@ -374,6 +374,21 @@ __global__ void k_transpose8(const uint64_t* __restrict__ s, uint64_t* __restric
     }
 }
 
+// 32x32 tiled transpose of a rows x cols matrix of 2-byte (bf16) elements.
+__global__ void k_transpose2(const uint16_t* __restrict__ s, uint16_t* __restrict__ d, int64_t rows, int64_t cols) {
+    __shared__ uint16_t tile[32][34];
+    const int64_t c0 = int64_t(blockIdx.x) * 32, r0 = int64_t(blockIdx.y) * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int64_t r = r0 + i, c = c0 + threadIdx.x;
+        if (r < rows && c < cols) tile[i][threadIdx.x] = s[r * cols + c];
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int64_t c = c0 + i, r = r0 + threadIdx.x;
+        if (r < rows && c < cols) d[c * rows + r] = tile[threadIdx.x][i];
+    }
+}
+
 int grid_for(int64_t n, int per = 256) {
     int64_t g = (n + per - 1) / per;
     const int64_t cap = int64_t(num_sms()) * 16;
@@ -566,6 +581,14 @@ void convert_index(cudaStream_t st, bool to64, void* dst, const void* src, int64
     else
         k_i64_to_i32<<<g, 256, 0, st>>>(static_cast<const int64_t*>(src), static_cast<int32_t*>(dst), n);
     check_launch("convert_index");
+}
+
+void transpose2(cudaStream_t st, const void* src, void* dst, int64_t rows, int64_t cols) {
+    if (rows <= 0 || cols <= 0) return;
+    dim3 grid(unsigned((cols + 31) / 32), unsigned((rows + 31) / 32));
+    k_transpose2<<<grid, dim3(32, 8), 0, st>>>(static_cast<const uint16_t*>(src), static_cast<uint16_t*>(dst), rows,
+                                                cols);
+    check_launch("k_transpose2");
 }
 
 void transpose8(cudaStream_t st, const void* src, void* dst, int64_t rows, int64_t cols) {

@@ -52,5 +52,6 @@ void flag_nonfinite(cudaStream_t st, const double* x, int64_t n, int32_t* flag_d
 void flag_nonfinite_f32(cudaStream_t st, const float* x, int64_t n, int32_t* flag_dev);
 void add_f64(cudaStream_t st, double* a, const double* b, int64_t n);                  // a += b (add_inplace)
 void transpose8(cudaStream_t st, const void* src, void* dst, int64_t rows, int64_t cols);
+void transpose2(cudaStream_t st, const void* src, void* dst, int64_t rows, int64_t cols);  // bf16 rows x cols
 
 }  // namespace meft_dev
