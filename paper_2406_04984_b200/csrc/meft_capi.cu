@@ -1,7 +1,9 @@
 // libmeft_cuda.so — C ABI of the B200 MEFT layer (declarations and reference citations: include/meft_cuda.h).
 // Host orchestration only: every numeric step is a kernel in gemm_sm100.cu / select.cu / stream_ops.cu /
 // dgemm.cu. There is no CPU compute path.
+#include <algorithm>
 #include <array>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <functional>
@@ -30,6 +32,47 @@ thread_local std::string t_err;
 thread_local int64_t t_err_index = -1;
 }  // namespace
 
+// ---- guard zones (MEFT_GUARD_ZONES=1): the out-of-bounds-write check that stands in for compute-sanitizer, which
+// this pool does not allow. Every context scratch buffer is followed by a 4 KB guard region and every store table by
+// a 4 KB gap, all filled with 0xA5; after each C-ABI call the regions are verified on the device and a damaged one
+// fails the call (MEFT_E_CUDA, naming the buffer) -- so a test suite run with the variable set proves no kernel wrote
+// past a buffer it was given.
+namespace {
+constexpr size_t kGuard = 4096;
+constexpr int kGuardByte = 0xA5;
+bool guard_mode() {
+    static const bool on = [] {
+        const char* v = std::getenv("MEFT_GUARD_ZONES");
+        return v && v[0] == '1';
+    }();
+    return on;
+}
+struct GuardRegion {
+    const void* p;
+    size_t n;
+    std::string label;
+};
+std::mutex g_guard_mu;
+std::vector<GuardRegion>& guard_regions() {  // store tables' guard gaps (global: stores outlive contexts)
+    static std::vector<GuardRegion>* v = new std::vector<GuardRegion>();
+    return *v;
+}
+void forget_guards(const void* store) {  // drop a store's table guards (destroyed, or creation failed)
+    const std::string prefix = "store " + std::to_string(reinterpret_cast<uintptr_t>(store)) + " ";
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    auto& v = guard_regions();
+    v.erase(std::remove_if(v.begin(), v.end(),
+                           [&](const GuardRegion& g) { return g.label.compare(0, prefix.size(), prefix) == 0; }),
+            v.end());
+}
+__global__ void k_guard_check(const uint8_t* __restrict__ p, size_t n, int* __restrict__ bad) {
+    int c = 0;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+        c += p[i] != kGuardByte;
+    if (c) atomicAdd(bad, c);
+}
+}  // namespace
+
 struct meft_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -43,7 +86,9 @@ struct meft_ctx {
     struct Buf {
         void* p = nullptr;
         size_t n = 0;
+        size_t req = 0;  // bytes last requested (guard mode: [req, n + kGuard) is the guard region)
     };
+    int* guard_bad = nullptr;  // guard mode: per-region damage counts
     std::unordered_map<std::string, Buf> scratch;
 
     int selection_mode = MEFT_SELECT_AUTO;
@@ -73,12 +118,13 @@ struct meft_ctx {
 
     void* get(const std::string& name, size_t bytes) {
         Buf& b = scratch[name];
+        const size_t extra = guard_mode() ? kGuard : 0;
         if (b.n < bytes) {
             if (b.p) MEFT_CUDA_CHECK(cudaFree(b.p));
             b.p = nullptr;
             b.n = 0;
             const size_t want = std::max<size_t>(bytes, 256);
-            cudaError_t e = cudaMalloc(&b.p, want);
+            cudaError_t e = cudaMalloc(&b.p, want + extra);
             if (e != cudaSuccess) {
                 cudaGetLastError();
                 throw MeftError(MEFT_E_OOM, "device allocation of " + std::to_string(want) + " bytes for '" + name +
@@ -86,7 +132,46 @@ struct meft_ctx {
             }
             b.n = want;
         }
+        if (extra) {  // everything past the requested bytes is guard
+            b.req = bytes;
+            MEFT_CUDA_CHECK(cudaMemsetAsync(static_cast<uint8_t*>(b.p) + bytes, kGuardByte, b.n + extra - bytes, stream));
+        }
         return b.p;
+    }
+
+    // guard mode: verify every scratch guard region and the stores' table gaps; throws naming the damaged buffer
+    void check_guards() {
+        if (!guard_mode()) return;
+        if (!guard_bad) MEFT_CUDA_CHECK(cudaMalloc(&guard_bad, 64 * sizeof(int)));
+        int* bad = guard_bad;
+        std::vector<std::string> labels;
+        std::vector<std::pair<const void*, size_t>> regions;
+        for (auto& kv : scratch)
+            if (kv.second.p) {
+                labels.push_back("scratch '" + kv.first + "'");
+                regions.push_back({static_cast<uint8_t*>(kv.second.p) + kv.second.req, kv.second.n + kGuard - kv.second.req});
+            }
+        {
+            std::lock_guard<std::mutex> lk(g_guard_mu);
+            for (auto& g : guard_regions()) {
+                labels.push_back(g.label);
+                regions.push_back({g.p, g.n});
+            }
+        }
+        MEFT_CUDA_CHECK(cudaMemsetAsync(bad, 0, std::min<size_t>(regions.size(), 64) * 4, stream));
+        for (size_t i = 0; i < regions.size(); ++i) {
+            k_guard_check<<<8, 256, 0, stream>>>(static_cast<const uint8_t*>(regions[i].first), regions[i].second,
+                                                  bad + std::min<size_t>(i, 63));
+        }
+        std::vector<int> h(std::min<size_t>(regions.size(), 64));
+        MEFT_CUDA_CHECK(cudaMemcpyAsync(h.data(), bad, h.size() * 4, cudaMemcpyDeviceToHost, stream));
+        MEFT_CUDA_CHECK(cudaStreamSynchronize(stream));
+        for (size_t i = 0; i < h.size(); ++i)
+            if (h[i]) {
+                const std::string who = i < 63 ? labels[i] : std::string("one of the later regions");
+                throw MeftError(MEFT_E_CUDA, "guard zone after " + who + " overwritten (" + std::to_string(h[i]) +
+                                                 " bytes): an out-of-bounds write");
+            }
     }
 };
 
@@ -183,6 +268,7 @@ meft_status guarded(meft_ctx* ctx, F&& f) {
     try {
         if (ctx) MEFT_CUDA_CHECK(cudaSetDevice(ctx->device));
         f();
+        if (ctx && guard_mode()) ctx->check_guards();
         return MEFT_OK;
     } catch (const MeftError& e) {
         return fail(ctx, e.code, e.what(), e.index);
@@ -711,6 +797,7 @@ void meft_ctx_destroy(meft_ctx* ctx) {
         if (kv.second.p) cudaFree(kv.second.p);
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->dev_small) cudaFree(ctx->dev_small);
+    if (ctx->guard_bad) cudaFree(ctx->guard_bad);
     if (ctx->host_small) cudaFreeHost(ctx->host_small);
     if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
     if (ctx->ev_fwd) cudaEventDestroy(ctx->ev_fwd);
@@ -1199,23 +1286,36 @@ meft_status meft_store_create(meft_ctx* ctx, int64_t layers, int64_t d, int64_t 
         const int momb = s->mom16 ? 2 : mb;  // Adam moment element size
         const size_t pd = size_t(pairs) * size_t(d), nd = size_t(experts) * size_t(d);
         auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+        const size_t gap = guard_mode() ? kGuard : 0;  // guard mode: a 4 KB guard after every table
         size_t bytes = 2 * al(pd * mb) + 4 * al(pd * momb) + al(nd * mb) + al(size_t(pairs) * 4) + al(size_t(pairs));
         if (precision == MEFT_STORE_MIXED) bytes += 2 * al(pd * 2) + al(nd * 2) + 2 * al(size_t(pairs) * 4);
         bytes += al(size_t(experts) * 8);
+        bytes += 16 * gap;
         for (int64_t l = 0; l < layers; ++l) {
             LayerBufs L;
             cudaError_t e = cudaMalloc(&L.base, bytes);
             if (e != cudaSuccess) {
                 cudaGetLastError();
                 for (auto& p : s->L) cudaFree(p.base);
+                if (guard_mode()) forget_guards(s.get());
                 throw MeftError(MEFT_E_OOM, "store_create: cannot allocate " + std::to_string(bytes) +
                                                 " bytes for layer " + std::to_string(l));
             }
             MEFT_CUDA_CHECK(cudaMemsetAsync(L.base, 0, bytes, ctx->stream));
             uint8_t* p = static_cast<uint8_t*>(L.base);
+            int table = 0;
             auto take = [&](size_t n) {
                 void* r = p;
                 p += al(n);
+                if (gap) {  // the guard after this table
+                    MEFT_CUDA_CHECK(cudaMemsetAsync(p, kGuardByte, gap, ctx->stream));
+                    std::lock_guard<std::mutex> lk(g_guard_mu);
+                    guard_regions().push_back({p, gap, "store " + std::to_string(reinterpret_cast<uintptr_t>(s.get())) +
+                                                           " layer " + std::to_string(l) + " table " +
+                                                           std::to_string(table)});
+                    p += gap;
+                }
+                ++table;
                 return r;
             };
             L.w_a = take(pd * mb);
@@ -1250,6 +1350,7 @@ meft_status meft_store_create(meft_ctx* ctx, int64_t layers, int64_t d, int64_t 
 
 void meft_store_destroy(meft_store* store) {
     if (!store) return;
+    if (guard_mode()) forget_guards(store);
     cudaSetDevice(store->device);
     for (auto& L : store->L) {
         cudaFree(L.base);
