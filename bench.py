@@ -370,17 +370,26 @@ def our_arm(args, rank, world, local_rank):
         from paper_2406_04984_b200 import sharded as SH
 
         eng, store = SH.make_device_layer(ctx, d, M, N, seed=1)
-        layer = SH.ShardedLayer(eng, d, M, N)
+        if args.sharded_impl == "capi":  # the whole protocol inside libmeft_cuda.so (meft_layer_step_sharded)
+            layer = SH.CShardedLayer(ctx, store, eng.w_g, group=torch.distributed.group.WORLD)
 
-        def step():
-            l0 = G.kernel_launches()
-            res = layer.step(h, g, kk, K, lr)
-            out.copy_(res["out"])
-            grad_h.copy_(res["grad_h"])
-            info = dict(layer.last)
-            info["gpu_launches"] = G.kernel_launches() - l0
-            info["fallbacks"] = 0
-            return info
+            def step():
+                l0 = G.kernel_launches()
+                res = layer.step(h, g, kk, K, lr, out=out, grad_h=grad_h)
+                return dict(union_size=res["union_size"], rescored=res["rescored"], fallbacks=0,
+                            gpu_launches=G.kernel_launches() - l0)
+        else:  # the Python orchestration over the C ABI's blocks (comm-stream overlap, fused peer reduce-scatter)
+            layer = SH.ShardedLayer(eng, d, M, N)
+
+            def step():
+                l0 = G.kernel_launches()
+                res = layer.step(h, g, kk, K, lr)
+                out.copy_(res["out"])
+                grad_h.copy_(res["grad_h"])
+                info = dict(layer.last)
+                info["gpu_launches"] = G.kernel_launches() - l0
+                info["fallbacks"] = 0
+                return info
 
     for _ in range(args.warmup):
         info = step()
@@ -430,6 +439,13 @@ def our_arm(args, rank, world, local_rank):
     def e2e_step():
         if not sharded:  # one C-ABI call: copies overlapped with the step inside meft_layer_step_host
             store.layer_step_host(0, h_host, g_host, kk, K, lr, out_host, gh_host)
+        elif args.sharded_impl == "capi":  # copies in, one C-ABI call, copies out
+            h.copy_(h_host, non_blocking=True)
+            g.copy_(g_host, non_blocking=True)
+            layer.step(h, g, kk, K, lr, out=out, grad_h=grad_h)
+            out_host.copy_(out, non_blocking=True)
+            gh_host.copy_(grad_h, non_blocking=True)
+            torch.cuda.synchronize()
         else:  # h first; g, out and grad_h move on a copy stream while the step computes
             h.copy_(h_host, non_blocking=True)
             with torch.cuda.stream(copy_stream):
@@ -603,6 +619,9 @@ def main():
                     help="reference arm: the bounded phased estimate (slices of the batch, per-call fixed cost + "
                          "per-row cost fitted) instead of one complete T-token reference step (~10 min at cfg2)")
     ap.add_argument("--sharded", action="store_true", help="run the expert-sharded layer even on one GPU")
+    ap.add_argument("--sharded-impl", choices=["python", "capi"], default="python",
+                    help="expert-sharded step: Python orchestration (overlapped, fused peer reduce-scatter) or the "
+                         "C-ABI meft_layer_step_sharded")
     ap.add_argument("--base-ffn", type=int, default=0,
                     help="also run the frozen base FFN of width n (SiLU), e.g. 11008 for LLaMA-7B (single GPU)")
     ap.add_argument("--precision", choices=["mixed", "compact"], default="mixed",

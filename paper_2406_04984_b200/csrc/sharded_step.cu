@@ -349,6 +349,15 @@ void sharded_step(meft_ctx* ctx, ShardCtx& sc, meft_store* store, int64_t layer,
     cudaStream_t st = static_cast<cudaStream_t>(meft_ctx_stream(ctx));
     const long long launches0 = meft_kernel_launches();
 
+    {  // every rank must bring the same number of tokens (the homes' row blocks of the P*T-row products)
+        std::vector<int64_t> ts(static_cast<size_t>(P));
+        cm.all_gather_host(&T, 8, ts.data(), st);
+        for (int p = 0; p < P; ++p)
+            if (ts[size_t(p)] != T)
+                throw MeftError(MEFT_E_SHAPE, "layer_step_sharded: rank " + std::to_string(p) + " brings " +
+                                                  std::to_string(ts[size_t(p)]) + " tokens, this rank " +
+                                                  std::to_string(T) + " (all ranks need the same T)");
+    }
     // all-gather the hidden states and the incoming gradient (rank order: rank p's tokens are rows [p*T, (p+1)*T))
     uint16_t* h_all = S.get<uint16_t>("h_all", size_t(TT * d));
     uint16_t* g_all = S.get<uint16_t>("g_all", size_t(TT * d));

@@ -12,6 +12,7 @@ import os
 import subprocess
 import threading
 
+import numpy as np
 import pytest
 import torch
 
@@ -123,3 +124,60 @@ def test_cpp_program_runs_the_sharded_step_over_nccl(ctx):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "sharded_capi_check: OK" in r.stdout
+
+
+def test_capi_sharded_rank_with_empty_local_union(ctx):
+    """Every token routes to rank 0's experts (rank 1 owns nothing that is selected: its local union is empty). Rank
+    1 must still return the home rows of out / grad_h (rank 0's contributions only) and leave its tables untouched;
+    everything equals the single-GPU step on the same 2*T tokens."""
+    P, d, M, N, K, kk, T, lr = 2, 256, 1024, 16, 16, 2, 64, 1e-3
+    full = G.Store(ctx, 1, d, M, N, G.STORE_MIXED)
+    b = 1.0 / d ** 0.5
+    w_g = np.full((N, d), -b)
+    w_g[: N // P] = b  # positive hidden states score rank 0's experts above every expert of rank 1
+    full.upload(0, "w_g", w_g)
+    full.upload(0, "w_a", G.reference_uniform(2, 0x5000, (d, M), -b, b, bf16=True))
+    full.upload(0, "w_b", G.reference_uniform(2, 0x7001, (M, d), -b, b, bf16=True))
+    h = torch.from_numpy(G.reference_uniform(2, 0x7002, (P * T, d), 0.0, 1.0, bf16=True)).cuda().bfloat16()
+    g = torch.from_numpy(G.reference_uniform(2, 0x7003, (P * T, d), -1, 1, bf16=True)).cuda().bfloat16()
+    shards = [_shard_of(ctx, full, r, P) for r in range(P)]
+    before = {n: shards[1].tensor(0, n).clone() for n in ("w_a", "w_b", "m_a", "pair_step")}
+    wg_dev = full.tensor(0, "w_g_compute").clone()
+    out = torch.empty((P * T, d), dtype=torch.float32, device="cuda")
+    gh = torch.empty_like(out)
+    want = full.layer_step(0, h, g, kk, K, lr, out=out, grad_h=gh, want_selection=True)
+    torch.cuda.synchronize()
+    assert int(want["unioned"].max()) < M // P  # the premise: nothing of rank 1 is selected
+
+    tg = SH.ThreadGroup(P)
+    results, errors = [None] * P, []
+
+    def rank_main(r):
+        try:
+            tg.bind(r)
+            rctx = G.Context(0)
+            layer = SH.CShardedLayer(rctx, shards[r], wg_dev, group=tg)
+            res = layer.step(h[r * T:(r + 1) * T].contiguous(), g[r * T:(r + 1) * T].contiguous(), kk, K, lr,
+                             want_selection=True)
+            torch.cuda.synchronize()
+            results[r] = (res, rctx, layer)
+        except Exception as e:  # surfaced below
+            errors.append((r, repr(e)))
+            tg._barrier.abort()
+
+    threads = [threading.Thread(target=rank_main, args=(r,)) for r in range(P)]
+    for t_ in threads:
+        t_.start()
+    for t_ in threads:
+        t_.join(timeout=300)
+    assert not errors, errors
+    for r in range(P):
+        res = results[r][0]
+        rows = slice(r * T, (r + 1) * T)
+        assert torch.equal(res["per_token"], want["per_token"][rows])
+        assert float((res["out"] - out[rows]).norm() / out[rows].norm()) < 1e-5
+        assert float((res["grad_h"] - gh[rows]).norm() / gh[rows].norm()) < 1e-5
+    for n, t in before.items():
+        assert torch.equal(shards[1].tensor(0, n), t), n
+    for r in range(P):
+        results[r][2].close()
