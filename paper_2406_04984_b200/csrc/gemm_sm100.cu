@@ -439,6 +439,12 @@ __device__ __forceinline__ void adam_st_mom(void* base, long long off, float4 v)
 constexpr int ADAM_SCRATCH_LD = 36;  // floats per scratch row (16-byte aligned, conflict-free quarter-warp phases)
 constexpr int ADAM_SCRATCH_BYTES = 4 * 32 * ADAM_SCRATCH_LD * 4;
 
+// MEFT_ADAM_EXP (developer A/B builds only, tools/ab_variants.sh; results are NOT an Adam update): 1 = no w/m/v
+// loads and only the bf16 copy stored (the epilogue's compute and shared-memory transpose without its HBM traffic),
+// 2 = no shared-memory transpose (the accumulator registers used in place: same traffic, no scratch).
+#ifndef MEFT_ADAM_EXP
+#define MEFT_ADAM_EXP 0
+#endif
 template <bool STATS, bool MOM16>
 __device__ __forceinline__ void adam_tile_transposed(const KArgs& a, uint32_t taddr, int m0, int n_col0, float* sw,
                                                      int lane) {
@@ -471,27 +477,41 @@ __device__ __forceinline__ void adam_tile_transposed(const KArgs& a, uint32_t ta
 #pragma unroll
         for (int it = 0; it < 8; ++it) {  // invalid rows (past M: j < 0) read row 0 and never store
             const long long off = (long long)max(j[it], 0) * a.ldc + n + c4;
+#if MEFT_ADAM_EXP == 1
+            w[it] = m[it] = v[it] = make_float4(1e-3f, 0.f, 0.f, 0.f);
+            (void)off;
+#else
             w[it] = ADAM_LD(reinterpret_cast<const float4*>(a.adam_w + off));
             m[it] = adam_ld_mom<MOM16>(a.adam_m, off);
             v[it] = adam_ld_mom<MOM16>(a.adam_v, off);
+#endif
         }
         tmem_ld_wait();
         const uint32_t sbase = smem_u32(sw);
+#if MEFT_ADAM_EXP != 2
 #pragma unroll
         for (int q = 0; q < 8; ++q)
             st_shared_f4(sbase + (lane * ADAM_SCRATCH_LD + 4 * q) * 4,
                          make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
                                      __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3])));
         __syncwarp();
+#endif
 #pragma unroll
         for (int it = 0; it < 8; ++it) {
+#if MEFT_ADAM_EXP == 2
+            const float4 g = make_float4(__uint_as_float(r[4 * it]), __uint_as_float(r[4 * it + 1]),
+                                         __uint_as_float(r[4 * it + 2]), __uint_as_float(r[4 * it + 3]));
+#else
             const float4 g = ld_shared_f4(sbase + ((it * 4 + sub) * ADAM_SCRATCH_LD + c4) * 4);
+#endif
             const uint2 cb = adam4<STATS>(w[it], m[it], v[it], g, a, k[it], ss[it], lsb[it]);
             if (j[it] >= 0) {
                 const long long off = (long long)j[it] * a.ldc + n + c4;
+#if MEFT_ADAM_EXP != 1
                 ADAM_ST(reinterpret_cast<float4*>(a.adam_w + off), w[it]);
                 adam_st_mom<MOM16>(a.adam_m, off, m[it]);
                 adam_st_mom<MOM16>(a.adam_v, off, v[it]);
+#endif
                 *reinterpret_cast<uint2*>(a.adam_c + off) = cb;
             }
         }

@@ -57,9 +57,8 @@ std::vector<GuardRegion>& guard_regions() {  // store tables' guard gaps (global
     static std::vector<GuardRegion>* v = new std::vector<GuardRegion>();
     return *v;
 }
-void forget_guards(const void* store) {  // drop a store's table guards (destroyed, or creation failed)
+void forget_guards(const void* store) {  // drop a store's table guards (caller holds g_guard_mu)
     const std::string prefix = "store " + std::to_string(reinterpret_cast<uintptr_t>(store)) + " ";
-    std::lock_guard<std::mutex> lk(g_guard_mu);
     auto& v = guard_regions();
     v.erase(std::remove_if(v.begin(), v.end(),
                            [&](const GuardRegion& g) { return g.label.compare(0, prefix.size(), prefix) == 0; }),
@@ -151,12 +150,12 @@ struct meft_ctx {
                 labels.push_back("scratch '" + kv.first + "'");
                 regions.push_back({static_cast<uint8_t*>(kv.second.p) + kv.second.req, kv.second.n + kGuard - kv.second.req});
             }
-        {
-            std::lock_guard<std::mutex> lk(g_guard_mu);
-            for (auto& g : guard_regions()) {
-                labels.push_back(g.label);
-                regions.push_back({g.p, g.n});
-            }
+        // held until the check has run: another thread's meft_store_destroy frees its tables under the same lock, so
+        // no store guard region is read after its memory is gone
+        std::lock_guard<std::mutex> lk(g_guard_mu);
+        for (auto& g : guard_regions()) {
+            labels.push_back(g.label);
+            regions.push_back({g.p, g.n});
         }
         MEFT_CUDA_CHECK(cudaMemsetAsync(bad, 0, std::min<size_t>(regions.size(), 64) * 4, stream));
         for (size_t i = 0; i < regions.size(); ++i) {
@@ -1287,6 +1286,7 @@ meft_status meft_store_create(meft_ctx* ctx, int64_t layers, int64_t d, int64_t 
         const size_t pd = size_t(pairs) * size_t(d), nd = size_t(experts) * size_t(d);
         auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
         const size_t gap = guard_mode() ? kGuard : 0;  // guard mode: a 4 KB guard after every table
+        std::vector<GuardRegion> new_guards;
         size_t bytes = 2 * al(pd * mb) + 4 * al(pd * momb) + al(nd * mb) + al(size_t(pairs) * 4) + al(size_t(pairs));
         if (precision == MEFT_STORE_MIXED) bytes += 2 * al(pd * 2) + al(nd * 2) + 2 * al(size_t(pairs) * 4);
         bytes += al(size_t(experts) * 8);
@@ -1297,7 +1297,6 @@ meft_status meft_store_create(meft_ctx* ctx, int64_t layers, int64_t d, int64_t 
             if (e != cudaSuccess) {
                 cudaGetLastError();
                 for (auto& p : s->L) cudaFree(p.base);
-                if (guard_mode()) forget_guards(s.get());
                 throw MeftError(MEFT_E_OOM, "store_create: cannot allocate " + std::to_string(bytes) +
                                                 " bytes for layer " + std::to_string(l));
             }
@@ -1307,12 +1306,10 @@ meft_status meft_store_create(meft_ctx* ctx, int64_t layers, int64_t d, int64_t 
             auto take = [&](size_t n) {
                 void* r = p;
                 p += al(n);
-                if (gap) {  // the guard after this table
+                if (gap) {  // the guard after this table (registered once the fill has run, below)
                     MEFT_CUDA_CHECK(cudaMemsetAsync(p, kGuardByte, gap, ctx->stream));
-                    std::lock_guard<std::mutex> lk(g_guard_mu);
-                    guard_regions().push_back({p, gap, "store " + std::to_string(reinterpret_cast<uintptr_t>(s.get())) +
-                                                           " layer " + std::to_string(l) + " table " +
-                                                           std::to_string(table)});
+                    new_guards.push_back({p, gap, "store " + std::to_string(reinterpret_cast<uintptr_t>(s.get())) +
+                                                      " layer " + std::to_string(l) + " table " + std::to_string(table)});
                     p += gap;
                 }
                 ++table;
@@ -1344,13 +1341,21 @@ meft_status meft_store_create(meft_ctx* ctx, int64_t layers, int64_t d, int64_t 
             s->pending.push_back(0);
         }
         MEFT_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        if (!new_guards.empty()) {  // the gaps are filled now: other threads' checks may read them
+            std::lock_guard<std::mutex> lk(g_guard_mu);
+            for (auto& g : new_guards) guard_regions().push_back(g);
+        }
         *out = s.release();
     });
 }
 
 void meft_store_destroy(meft_store* store) {
     if (!store) return;
-    if (guard_mode()) forget_guards(store);
+    std::unique_lock<std::mutex> lk(g_guard_mu, std::defer_lock);
+    if (guard_mode()) {  // no guard check may be reading this store's gaps while they are freed
+        lk.lock();
+        forget_guards(store);
+    }
     cudaSetDevice(store->device);
     for (auto& L : store->L) {
         cudaFree(L.base);
