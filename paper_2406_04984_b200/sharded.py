@@ -402,11 +402,15 @@ def _comm_device(group):
 
 
 def _all_gather_rows(t, group, world):
+    """Rows of every rank's `t`, rank-major, gathered straight into one tensor (no per-rank parts + cat copy)."""
     if isinstance(group, ThreadGroup):
         return group.all_gather(t)
-    parts = [torch.empty_like(t) for _ in range(world)]
-    dist.all_gather(parts, t.contiguous(), group=group)
-    return torch.cat(parts, 0)
+    out = torch.empty((world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    if world == 1:
+        out.copy_(t)
+        return out
+    dist.all_gather_into_tensor(out, t.contiguous(), group=group)
+    return out
 
 
 def _reduce_scatter_rows(t, group, world, rank):
