@@ -174,16 +174,39 @@ SparseFfnGrads sparse_backward(const Matrix& grad_out, const FfnCache& cache, co
 }
 
 ActivationProfile activation_profile(const AdapterWeights& adapter, const std::vector<Matrix>& corpus) {
-    const index_t r = adapter.pairs();
-    std::vector<double> sums(size_t(r), 0.0);
+    const index_t r = adapter.pairs(), d = adapter.dim();
     index_t tokens = 0;
-    for (const Matrix& h : corpus) {
-        if (h.rows == 0) continue;
-        if (h.cols != adapter.dim()) throw ShapeError("activation_profile: dim mismatch");
-        const Matrix act = relu(matmul(h, adapter.w_a));  // device
-        for (index_t t = 0; t < act.rows; ++t)
-            for (index_t j = 0; j < r; ++j) sums[size_t(j)] += act.at(t, j);
-        tokens += h.rows;
+    std::vector<double> sums(size_t(r), 0.0);
+    {
+        // On the device: per batch, act = ReLU(h w_a) (meft_matmul_f64 + meft_activation_f64), then the running
+        // column sums as ONE ascending fp64 chain over [sums; act] (a 1 x (rows+1) ones vector times that stack):
+        // acc = sums[j], then acc + act[0][j], acc + act[1][j], ... -- the reference's sequential loop
+        // (adapter.cpp:190-193) bit for bit, fma(1, x, acc) being the exact add.
+        std::lock_guard<std::recursive_mutex> lk(dropin::api_mutex());
+        dropin::DevBuf dsums(size_t(std::max<index_t>(r, 1)) * sizeof(double));
+        dropin::DevBuf wa = r > 0 ? dropin::upload(adapter.w_a) : dropin::DevBuf();
+        for (const Matrix& h : corpus) {
+            if (h.rows == 0) continue;
+            if (h.cols != d) throw ShapeError("activation_profile: dim mismatch");
+            if (r == 0) {
+                tokens += h.rows;
+                continue;
+            }
+            const index_t T = h.rows;
+            dropin::DevBuf dh = dropin::upload(h);
+            dropin::DevBuf stack(size_t((T + 1) * r) * sizeof(double));  // row 0: the running sums, rows 1..T: act
+            dropin::check(meft_copy_to_device(dropin::ctx(), stack.get(), sums.data(), size_t(r) * sizeof(double)));
+            dropin::check(meft_matmul_f64(dropin::ctx(), dh.as<double>(), wa.as<double>(), T, d, r,
+                                          stack.as<double>() + r));
+            dropin::check(meft_activation_f64(dropin::ctx(), 1, stack.as<double>() + r, stack.as<double>() + r,
+                                              T * r));
+            std::vector<double> ones(size_t(T + 1), 1.0);
+            dropin::DevBuf dones = dropin::upload(ones.data(), ones.size());
+            dropin::check(meft_matmul_f64(dropin::ctx(), dones.as<double>(), stack.as<double>(), 1, T + 1, r,
+                                          dsums.as<double>()));
+            dropin::download(sums.data(), dsums, sums.size());  // synchronous: `ones` may go on return
+            tokens += T;
+        }
     }
     if (tokens == 0) throw std::invalid_argument("activation_profile: empty corpus");
     std::vector<double> means(sums);

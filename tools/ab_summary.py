@@ -8,7 +8,7 @@ for path in sys.argv[1:]:
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hi]
     mi, vi, ii, ui = h.index("Metric Name"), h.index("Metric Value"), h.index("ID"), h.index("Metric Unit")
-    scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "byte": 1e-9, "Kbyte": 1e-6, "Mbyte": 1e-3,
+    scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "ns": 1e-6, "us": 1e-3, "ms": 1.0, "byte": 1e-9, "Kbyte": 1e-6, "Mbyte": 1e-3,
              "Gbyte": 1.0, "hz": 1e-9, "Khz": 1e-6, "Mhz": 1e-3, "Ghz": 1.0, "cycle/second": 1e-9,
              "cycle/nsecond": 1.0, "cycle/usecond": 1e-3}
     d = collections.defaultdict(dict)
