@@ -235,6 +235,10 @@ meft_status meft_shard_requests(meft_ctx* ctx, const int32_t* amb, const int32_t
                                 int64_t* counts, int64_t* total);
 /* dst[back[i]] = x[i] */
 meft_status meft_shard_scatter_f64(meft_ctx* ctx, const double* x, const int32_t* back, int64_t n, double* dst);
+/* dst[r] = src[idx[r]] for n rows of row_bytes (a multiple of 16, 16-byte aligned buffers): the owners of the
+ * sharded selection gather their dispatched token rows from the all-gathered hidden states. */
+meft_status meft_gather_rows(meft_ctx* ctx, const void* src, int64_t row_bytes, const int32_t* idx, int64_t n,
+                             void* dst);
 
 /* ---- The reference's frozen toy trunk (model.cpp:50-218), fp64 on the device: what the drop-in's model.hpp
  * functions call so that the reference trainer runs end to end on the B200. Arrays are device buffers (row-major,

@@ -99,6 +99,7 @@ _SIGS = {
     "meft_shard_requests": (INT, [P, P, P, P, P, I64, I64, I64, I64, I64, INT, C.POINTER(I64), P, P, P,
                                   C.POINTER(I64), C.POINTER(I64)]),
     "meft_shard_scatter_f64": (INT, [P, P, P, I64, P]),
+    "meft_gather_rows": (INT, [P, P, I64, P, I64, P]),
     # toy trunk (model.cpp:50-218), fp64 device buffers
     "meft_embed_f64": (INT, [P, P, I64, P, I64, I64, P, I64, I64, P]),
     "meft_attention_forward_f64": (INT, [P, P, P, P, P, P, P, I64, I64, I64, P, P, P, P, P]),

@@ -1115,6 +1115,15 @@ meft_status meft_shard_requests(meft_ctx* ctx, const int32_t* amb, const int32_t
     });
 }
 
+meft_status meft_gather_rows(meft_ctx* ctx, const void* src, int64_t row_bytes, const int32_t* idx, int64_t n,
+                             void* dst) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(n >= 0 && row_bytes >= 0, MEFT_E_INVALID, "gather_rows: n, row_bytes >= 0");
+        gather_rows1(ctx->stream, src, row_bytes, idx, n, dst);
+    });
+}
+
 meft_status meft_shard_scatter_f64(meft_ctx* ctx, const double* x, const int32_t* back, int64_t n, double* dst) {
     return guarded(ctx, [&] {
         require_ctx(ctx);

@@ -397,6 +397,27 @@ int grid_for(int64_t n, int per = 256) {
 
 }  // namespace
 
+// dst[r] = src[idx[r]] for rows of row_bytes (a multiple of 16, 16-byte aligned): warp per row
+__global__ void k_gather1(const uint4* __restrict__ src, int64_t row_words, const int32_t* __restrict__ idx, int n,
+                          uint4* __restrict__ dst) {
+    const int lane = threadIdx.x & 31;
+    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += (gridDim.x * blockDim.x) >> 5) {
+        const uint4* s = src + int64_t(idx[r]) * row_words;
+        uint4* d = dst + int64_t(r) * row_words;
+        for (int64_t v = lane; v < row_words; v += 32) d[v] = __ldg(s + v);
+    }
+}
+
+void gather_rows1(cudaStream_t st, const void* src, int64_t row_bytes, const int32_t* idx, int64_t n, void* dst) {
+    if (n <= 0) return;
+    if (row_bytes % 16 || (reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) % 16)
+        throw MeftError(2, "gather_rows: rows must be 16-byte multiples, 16-byte aligned");
+    const int grid = std::max(1, std::min<int>(int((n * 32 + 255) / 256), num_sms() * 16));
+    k_gather1<<<grid, 256, 0, st>>>(static_cast<const uint4*>(src), row_bytes / 16, idx, int(n),
+                                    static_cast<uint4*>(dst));
+    check_launch("k_gather1");
+}
+
 void gather_rows2(cudaStream_t st, const void* a, const void* b, int64_t row_bytes, const int32_t* idx,
                   const int32_t* count_dev, int64_t count, void* oa, void* ob) {
     if (count <= 0 && !count_dev) return;

@@ -5,6 +5,7 @@
 
 namespace meft_dev {
 
+void gather_rows1(cudaStream_t st, const void* src, int64_t row_bytes, const int32_t* idx, int64_t n, void* dst);
 void gather_rows2(cudaStream_t st, const void* a, const void* b, int64_t row_bytes, const int32_t* idx,
                   const int32_t* count_dev, int64_t count, void* oa, void* ob);
 void check_sorted_unique(cudaStream_t st, const int32_t* idx, int64_t n, int64_t limit, int32_t* err_dev);

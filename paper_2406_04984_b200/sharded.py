@@ -5,7 +5,8 @@ replicated. Each rank brings its own T tokens (weak scaling: the layer step is o
 reference's batch-union semantics). Per step:
 
   1. route the local tokens (certified, exact tau) ............................ home rank
-  2. all-to-all: dispatch each (token, expert) row to the expert's owner ........ NCCL
+  2. all-to-all: dispatch (token id, expert) entries to the expert's owner, who gathers the token rows from the
+     all-gathered h (step 8a, started first) ..................................... NCCL
   3. approximate candidate scores against the owner's keys (tcgen05) ............ owner rank
   4. all-to-all: candidate scores back; all-gather key norms .................... NCCL
   5. certified top-K classification (sure / ambiguous) .......................... home rank
@@ -45,7 +46,7 @@ class TorchGlue:
     """The protocol's index bookkeeping as framework ops -- the reference semantics of the device plan kernels
     (csrc/shard_plan.cu), used by engines without them (the CPU test engine). All orders are stable."""
 
-    def dispatch(self, tau, h, n_loc, P):
+    def dispatch(self, tau, h, n_loc, P, rows=True):
         """(token, slot) rows bucketed by expert owner: send rows / owner-local experts in bucket order, order[p] =
         flat (t*kk + s) index, inv = its inverse, rows per owner."""
         kk = tau.shape[1]
@@ -62,6 +63,9 @@ class TorchGlue:
         out = torch.empty_like(src)
         out[order.long()] = src
         return out
+
+    def gather_rows(self, src, idx):
+        return src[idx.long()]
 
     def requests(self, amb, n_amb, tau, inv, E, M_loc, P, row_base):
         """Exact re-scoring requests of the ambiguous candidates, bucketed by key owner in (token, position) order:
@@ -100,11 +104,11 @@ class DeviceEngine:
         self.ctx.check(st)
 
     # ---- protocol bookkeeping on the device (csrc/shard_plan.cu; semantics: TorchGlue)
-    def dispatch(self, tau, h, n_loc, P):
+    def dispatch(self, tau, h, n_loc, P, rows=True):
         T, kk = tau.shape
         d = h.shape[1]
         n = T * kk
-        send_rows = torch.empty((n, d), dtype=h.dtype, device=self.dev)
+        send_rows = torch.empty((n, d), dtype=h.dtype, device=self.dev) if rows else None
         send_exp = torch.empty(n, dtype=torch.int32, device=self.dev)
         order = torch.empty(n, dtype=torch.int32, device=self.dev)
         inv = torch.empty(n, dtype=torch.int32, device=self.dev)
@@ -112,6 +116,15 @@ class DeviceEngine:
         self._check(lib().meft_shard_dispatch(self.ctx.h, _p(tau), T, kk, n_loc, P, _p(h), d, _p(send_rows),
                                               _p(send_exp), _p(order), _p(inv), counts))
         return send_rows, send_exp, order, inv, list(counts)
+
+    def gather_rows(self, src, idx):
+        """src[idx] (rows of a contiguous device tensor) by meft_gather_rows."""
+        n = idx.numel()
+        out = torch.empty((n,) + tuple(src.shape[1:]), dtype=src.dtype, device=self.dev)
+        if n:
+            row_bytes = src[0].numel() * src.element_size()
+            self._check(lib().meft_gather_rows(self.ctx.h, _p(src), row_bytes, _p(idx), n, _p(out)))
+        return out
 
     def unpermute(self, src, order):
         out = torch.empty_like(src)
@@ -545,14 +558,23 @@ class ShardedLayer:
                 ev_g.record(cs)
             h.record_stream(cs)
             g.record_stream(cs)
+        if not self.overlap:  # h_all is needed by the owners' row gather below
+            h_all = _all_gather_rows(h, grp, P)
         # 1. route (exact tau, ascending per token)
         tau = eng.route(h, kk)
-        # 2. dispatch (token, slot) rows to their expert owners (stable bucket plan on the device)
-        send_rows, send_exp, order, inv, send_counts = eng.dispatch(tau, h, self.N_loc, P)
+        # 2. dispatch (token id, owner-local expert) entries to the expert owners (stable bucket plan on the device);
+        # the owners gather the token rows from the all-gathered h they hold anyway -- 8 bytes per entry cross the
+        # wire instead of a d-wide bf16 row
+        _, send_exp, order, inv, send_counts = eng.dispatch(tau, h, self.N_loc, P, rows=False)
         cmat = _gather_counts(send_counts, grp, self.host_group)  # cmat[src][dst]: rows src dispatches to dst
         recv_counts = [cmat[s][r] for s in range(P)]
-        recv_rows = _a2a(send_rows, send_counts, recv_counts, grp)
-        recv_exp = _a2a(send_exp, send_counts, recv_counts, grp)
+        send_ids = (order.long() // kk_eff + r * T).to(torch.int32)
+        recv = _a2a(torch.stack([send_ids, send_exp], 1), send_counts, recv_counts, grp)
+        recv_ids, recv_exp = recv[:, 0].contiguous(), recv[:, 1].contiguous()
+        if self.overlap:
+            cur.wait_event(ev_h)  # h_all (the comm stream's all-gather) before the owners read it
+            h_all.record_stream(cur)
+        recv_rows = eng.gather_rows(h_all, recv_ids)
         # 3-4. owners score; candidate blocks come back in dispatch order
         cand_recv = eng.score(recv_rows, recv_exp)
         cand_back = _a2a(cand_recv, recv_counts, send_counts, grp)
@@ -633,7 +655,6 @@ class ShardedLayer:
         else:
             if g_ready is not None:
                 torch.cuda.current_stream().wait_event(g_ready)
-            h_all = _all_gather_rows(h, grp, P)
             g_all = _all_gather_rows(g, grp, P)
             out_p, gh_p = eng.ffn_local(h_all, g_all, S_loc, lr)
             out = _reduce_scatter_rows(out_p, grp, P, r)
