@@ -54,12 +54,13 @@ METRIC = "MEFT adapter layer tokens/sec (fwd+bwd+sparse update)"
 SEED, W_B_STREAM, H_STREAM, G_STREAM = 1, 0x7001, 0x7002, 0x7003
 
 
-def config_dict(world):
+def config_dict(world, sharded=False):
     """The workload as both arms report it (identical dicts: the driver compares the arms on the same config)."""
     per_gpu = CFG["tokens"] // world if CFG.get("strong") else CFG["tokens"]
     return dict(workload=CFG["workload"], d=CFG["d"], pairs=CFG["pairs"], experts=CFG["experts"], k=CFG["k"],
                 kk=CFG["kk"], tokens_per_gpu=per_gpu, global_tokens=per_gpu * world,
-                parallelism="single GPU" if world == 1 else f"expert-sharded ep{world} (NCCL all-to-all)",
+                parallelism=("single GPU" if world == 1 and not sharded else
+                             f"expert-sharded ep{world} (NCCL all-to-all)"),
                 inputs="reference RNG streams 0x7001-0x7003 (BASELINE.md §3), bf16-rounded",
                 l2=(f"inputs larger than L2 ({CFG['pairs'] * CFG['d'] * 28 / 1e9:.1f} GB of tables per layer)"
                     if CFG["pairs"] * CFG["d"] * 28 > 126e6 else "tables fit in L2 (not flushed; a parity size)"))
@@ -535,7 +536,7 @@ def our_arm(args, rank, world, local_rank):
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong" if CFG.get("strong") else "weak",
         "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (HostStore::init tables; W_B, h, grad_out from the reference RNG streams, bf16)",
-        "config": config_dict(world),
+        "config": config_dict(world, sharded),
         "precision": "bf16 compute, fp32 master weights, " + ("bf16 Adam moments (COMPACT)" if args.precision ==
                                                                   "compact" else "fp32 Adam moments"),
         "union_size": S, "base_ffn": args.base_ffn,
