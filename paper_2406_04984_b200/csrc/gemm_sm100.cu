@@ -441,7 +441,9 @@ constexpr int ADAM_SCRATCH_BYTES = 4 * 32 * ADAM_SCRATCH_LD * 4;
 
 // MEFT_ADAM_EXP (developer A/B builds only, tools/ab_variants.sh; results are NOT an Adam update): 1 = no w/m/v
 // loads and only the bf16 copy stored (the epilogue's compute and shared-memory transpose without its HBM traffic),
-// 2 = no shared-memory transpose (the accumulator registers used in place: same traffic, no scratch).
+// 2 = no shared-memory transpose (the accumulator registers used in place: same traffic, no scratch), 3 = no Adam
+// arithmetic (loads, transpose, stores of the raw gradient), 4 = neither traffic nor arithmetic (TMEM loads, the
+// transpose and the 8-byte copy store only).
 #ifndef MEFT_ADAM_EXP
 #define MEFT_ADAM_EXP 0
 #endif
@@ -477,7 +479,7 @@ __device__ __forceinline__ void adam_tile_transposed(const KArgs& a, uint32_t ta
 #pragma unroll
         for (int it = 0; it < 8; ++it) {  // invalid rows (past M: j < 0) read row 0 and never store
             const long long off = (long long)max(j[it], 0) * a.ldc + n + c4;
-#if MEFT_ADAM_EXP == 1
+#if MEFT_ADAM_EXP == 1 || MEFT_ADAM_EXP == 4
             w[it] = m[it] = v[it] = make_float4(1e-3f, 0.f, 0.f, 0.f);
             (void)off;
 #else
@@ -504,10 +506,15 @@ __device__ __forceinline__ void adam_tile_transposed(const KArgs& a, uint32_t ta
 #else
             const float4 g = ld_shared_f4(sbase + ((it * 4 + sub) * ADAM_SCRATCH_LD + c4) * 4);
 #endif
+#if MEFT_ADAM_EXP == 3 || MEFT_ADAM_EXP == 4  // no Adam arithmetic: the gradient stored as is
+            w[it] = m[it] = v[it] = g;
+            const uint2 cb = make_uint2(__float_as_uint(g.x), __float_as_uint(g.y));
+#else
             const uint2 cb = adam4<STATS>(w[it], m[it], v[it], g, a, k[it], ss[it], lsb[it]);
+#endif
             if (j[it] >= 0) {
                 const long long off = (long long)j[it] * a.ldc + n + c4;
-#if MEFT_ADAM_EXP != 1
+#if MEFT_ADAM_EXP != 1 && MEFT_ADAM_EXP != 4
                 ADAM_ST(reinterpret_cast<float4*>(a.adam_w + off), w[it]);
                 adam_st_mom<MOM16>(a.adam_m, off, m[it]);
                 adam_st_mom<MOM16>(a.adam_v, off, v[it]);
