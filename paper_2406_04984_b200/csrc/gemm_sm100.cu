@@ -439,13 +439,22 @@ __device__ __forceinline__ void adam_st_mom(void* base, long long off, float4 v)
 constexpr int ADAM_SCRATCH_LD = 36;  // floats per scratch row (16-byte aligned, conflict-free quarter-warp phases)
 constexpr int ADAM_SCRATCH_BYTES = 4 * 32 * ADAM_SCRATCH_LD * 4;
 
-// MEFT_ADAM_EXP (developer A/B builds only, tools/ab_variants.sh; results are NOT an Adam update): 1 = no w/m/v
-// loads and only the bf16 copy stored (the epilogue's compute and shared-memory transpose without its HBM traffic),
-// 2 = no shared-memory transpose (the accumulator registers used in place: same traffic, no scratch), 3 = no Adam
-// arithmetic (loads, transpose, stores of the raw gradient), 4 = neither traffic nor arithmetic (TMEM loads, the
-// transpose and the 8-byte copy store only).
-#ifndef MEFT_ADAM_EXP
-#define MEFT_ADAM_EXP 0
+// MEFT_ADAM_EXP_* (developer A/B builds only, tools/ab_variants.sh; results are NOT an Adam update):
+//   NOTRAFFIC: no w/m/v loads or stores (constants in their place); NOMATH: no Adam arithmetic (the gradient passed
+//   through); NOTRANSPOSE: no shared-memory transpose (the accumulator registers used in place); NOSTORE: nothing
+//   written at all (the stores sit behind a condition that is never true at run time, so the tables -- and hence the
+//   next step's union -- stay as they are while the code stays in the kernel).
+#ifndef MEFT_ADAM_EXP_NOTRAFFIC
+#define MEFT_ADAM_EXP_NOTRAFFIC 0
+#endif
+#ifndef MEFT_ADAM_EXP_NOMATH
+#define MEFT_ADAM_EXP_NOMATH 0
+#endif
+#ifndef MEFT_ADAM_EXP_NOTRANSPOSE
+#define MEFT_ADAM_EXP_NOTRANSPOSE 0
+#endif
+#ifndef MEFT_ADAM_EXP_NOSTORE
+#define MEFT_ADAM_EXP_NOSTORE 0
 #endif
 template <bool STATS, bool MOM16>
 __device__ __forceinline__ void adam_tile_transposed(const KArgs& a, uint32_t taddr, int m0, int n_col0, float* sw,
@@ -479,7 +488,7 @@ __device__ __forceinline__ void adam_tile_transposed(const KArgs& a, uint32_t ta
 #pragma unroll
         for (int it = 0; it < 8; ++it) {  // invalid rows (past M: j < 0) read row 0 and never store
             const long long off = (long long)max(j[it], 0) * a.ldc + n + c4;
-#if MEFT_ADAM_EXP == 1 || MEFT_ADAM_EXP == 4
+#if MEFT_ADAM_EXP_NOTRAFFIC
             w[it] = m[it] = v[it] = make_float4(1e-3f, 0.f, 0.f, 0.f);
             (void)off;
 #else
@@ -490,7 +499,7 @@ __device__ __forceinline__ void adam_tile_transposed(const KArgs& a, uint32_t ta
         }
         tmem_ld_wait();
         const uint32_t sbase = smem_u32(sw);
-#if MEFT_ADAM_EXP != 2
+#if !MEFT_ADAM_EXP_NOTRANSPOSE
 #pragma unroll
         for (int q = 0; q < 8; ++q)
             st_shared_f4(sbase + (lane * ADAM_SCRATCH_LD + 4 * q) * 4,
@@ -500,21 +509,21 @@ __device__ __forceinline__ void adam_tile_transposed(const KArgs& a, uint32_t ta
 #endif
 #pragma unroll
         for (int it = 0; it < 8; ++it) {
-#if MEFT_ADAM_EXP == 2
+#if MEFT_ADAM_EXP_NOTRANSPOSE
             const float4 g = make_float4(__uint_as_float(r[4 * it]), __uint_as_float(r[4 * it + 1]),
                                          __uint_as_float(r[4 * it + 2]), __uint_as_float(r[4 * it + 3]));
 #else
             const float4 g = ld_shared_f4(sbase + ((it * 4 + sub) * ADAM_SCRATCH_LD + c4) * 4);
 #endif
-#if MEFT_ADAM_EXP == 3 || MEFT_ADAM_EXP == 4  // no Adam arithmetic: the gradient stored as is
+#if MEFT_ADAM_EXP_NOMATH  // no Adam arithmetic: the gradient passed through
             w[it] = m[it] = v[it] = g;
             const uint2 cb = make_uint2(__float_as_uint(g.x), __float_as_uint(g.y));
 #else
             const uint2 cb = adam4<STATS>(w[it], m[it], v[it], g, a, k[it], ss[it], lsb[it]);
 #endif
-            if (j[it] >= 0) {
-                const long long off = (long long)j[it] * a.ldc + n + c4;
-#if MEFT_ADAM_EXP != 1 && MEFT_ADAM_EXP != 4
+            if (MEFT_ADAM_EXP_NOSTORE ? j[it] < -1 : j[it] >= 0) {
+                const long long off = (long long)max(j[it], 0) * a.ldc + n + c4;
+#if !MEFT_ADAM_EXP_NOTRAFFIC
                 ADAM_ST(reinterpret_cast<float4*>(a.adam_w + off), w[it]);
                 adam_st_mom<MOM16>(a.adam_m, off, m[it]);
                 adam_st_mom<MOM16>(a.adam_v, off, v[it]);
@@ -536,7 +545,7 @@ __device__ __forceinline__ void adam_tile_transposed(const KArgs& a, uint32_t ta
                 l = min(l, __shfl_xor_sync(0xffffffffu, l, o));
             }
             const int mr = m0 + it * 4 + sub;
-            if ((lane & 7) == 0 && mr < a.M) {
+            if ((lane & 7) == 0 && mr < a.M && (!MEFT_ADAM_EXP_NOSTORE || j[it] < -1)) {
                 a.stat_ss[mr * a.stat_ld + nb] = t;
                 a.stat_lsb[mr * a.stat_ld + nb] = l;
             }

@@ -1,4 +1,5 @@
-"""Per-launch (ms, DRAM GB read, GHz) of the last step's six FFN GEMMs from tools/ab_*.sh ncu csv files."""
+"""Per-launch (ms, DRAM GB read, GHz[, tensor-active %, active tensor Gcycles/s]) of the last step's six FFN GEMMs
+from tools/ab_*.sh ncu csv files."""
 import collections
 import csv
 import sys
@@ -16,6 +17,9 @@ for path in sys.argv[1:]:
         d[int(r[ii])][r[mi]] = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
     ids = sorted(d)[-6:]
     tot = sum(d[i]["gpu__time_duration.sum"] for i in ids)
+    tensor = "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"
     print(path.split("/")[-1], f"sum {tot:.3f} ms",
           [(round(d[i]["gpu__time_duration.sum"], 3), round(d[i]["dram__bytes_read.sum"], 1),
-            round(d[i]["sm__cycles_elapsed.avg.per_second"], 2)) for i in ids])
+            round(d[i]["sm__cycles_elapsed.avg.per_second"], 2))
+           + ((round(d[i][tensor], 1), round(d[i][tensor] * d[i]["sm__cycles_elapsed.avg.per_second"] / 100, 3))
+              if tensor in d[i] else ()) for i in ids])
