@@ -134,6 +134,25 @@ meft_status meft_ctx_set_adam(meft_ctx* ctx, int mode);
  * grad_h once the step is done (one extra sync) and return MEFT_E_NONFINITE ("... non-finite ...") on NaN / Inf.
  * Default off: the scan costs a sync per step. */
 meft_status meft_ctx_set_check_finite(meft_ctx* ctx, int enable);
+/* Host synchronisation of the fused layer step. enable = 1 (default): meft_layer_step reads the union size back
+ * once, mid-step, and sizes the FFN GEMMs to it. enable = 0: the step never waits for the device -- the six FFN
+ * GEMMs are launched for the capacity (M pairs) and read |S| from device memory before their first tile
+ * (GemmEpilogue::extent), so consecutive layer steps enqueue back to back and a step can be captured into a CUDA
+ * graph (meft_graph_*). Bit-identical results. It applies to the fused-Adam step (no pending scatter_grads, no base
+ * FFN, no router training, check_finite off, M <= 65536, d % 32 == 0); any other step takes the synchronising
+ * path (an error while capturing). A non-NULL info then costs one synchronisation at the END of the step. */
+meft_status meft_ctx_set_host_sync(meft_ctx* ctx, int enable);
+
+/* CUDA graphs over the context stream. meft_graph_begin starts capturing the context stream; the calls that follow
+ * must only enqueue work (e.g. meft_layer_step with host sync off, after one eager warm-up step so every scratch
+ * buffer already exists -- an allocation while capturing fails the capture); meft_graph_end instantiates the
+ * graph; meft_graph_launch replays it on the context stream (inputs and outputs are the captured buffers). */
+typedef struct meft_graph meft_graph;
+meft_status meft_graph_begin(meft_ctx* ctx);
+meft_status meft_graph_end(meft_ctx* ctx, meft_graph** graph);
+meft_status meft_graph_launch(meft_ctx* ctx, meft_graph* graph);
+void meft_graph_destroy(meft_graph* graph);
+
 /* Keep `sms` SMs free of the persistent tcgen05 GEMMs (process-wide; 0 = all SMs). The expert-sharded step sets it
  * while collectives are meant to overlap its FFN: NCCL's kernels need SMs of their own to make progress. */
 meft_status meft_set_gemm_sm_reserve(int sms);
@@ -462,7 +481,7 @@ typedef struct meft_base_ffn {
  * (trainer.cpp:220,270,283,525): meft_ffn (ke_select -> fetch -> sparse_ffn_pa) -> sparse_backward ->
  * scatter_grads -> sparse_adam_update. h and grad_out are bf16 [T x d] on device; out and grad_h are f32
  * [T x d] (either may be NULL). Optional outputs per_token [T x take] / union_idx [M] (device int32) may be
- * NULL. Synchronises once (to size the union).
+ * NULL. Synchronises once (to size the union) unless host sync is off (meft_ctx_set_host_sync).
  */
 meft_status meft_layer_step(meft_ctx* ctx, meft_store* store, int64_t layer, const void* h, const void* grad_out,
                             int64_t T, int64_t kk, int64_t k, double beta1, double beta2, double eps, double lr,

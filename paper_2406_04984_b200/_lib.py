@@ -72,6 +72,11 @@ _SIGS = {
     "meft_ctx_set_gather": (INT, [P, INT]),
     "meft_ctx_set_adam": (INT, [P, INT]),
     "meft_ctx_set_check_finite": (INT, [P, INT]),
+    "meft_ctx_set_host_sync": (INT, [P, INT]),
+    "meft_graph_begin": (INT, [P]),
+    "meft_graph_end": (INT, [P, C.POINTER(P)]),
+    "meft_graph_launch": (INT, [P, P]),
+    "meft_graph_destroy": (None, [P]),
     "meft_set_gemm_sm_reserve": (INT, [INT]),
     "meft_ctx_read_timing": (INT, [P, P, P]),
     "meft_device_alloc": (INT, [P, C.c_size_t, C.POINTER(P)]),

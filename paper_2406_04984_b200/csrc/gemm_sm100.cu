@@ -81,7 +81,35 @@ struct KArgs {
     long long stat_ld;
     // L2 eviction priority of the A / B TMA loads (GemmOperand::l2_hint)
     int hint_a, hint_b;
+    // device-sized extent (GemmEpilogue::extent): the launch is sized for the static M / N / K (a capacity); the
+    // kernel reads the real size of dimension extent_dim (1 = M, 2 = N, 3 = K) from *extent before its first tile
+    const int32_t* extent;
+    int extent_dim, extent_tile_m;
 };
+
+// Shrink the capacity-sized problem to the device-resident extent (every thread, before any tile is resolved).
+// N: tiles past the extent do not run, and the output columns up to the next multiple of 64 are stored -- exact
+// zeros, because B's rows there read as zeros (a gathered B: out-of-bounds rows; a materialised B: the caller pads
+// it, gather_rows2 pad64), so a K-extent consumer of this output reads zeros there just as TMA's out-of-bounds
+// fill gives a host-sized launch. K: k-blocks past the extent are not issued. M: tiles past it do not run.
+__device__ __forceinline__ void apply_extent(KArgs& a) {
+    if (a.extent_dim == 0) return;
+    const int v = max(0, __ldg(a.extent));
+    if (a.extent_dim == 1) {
+        a.M = min(v, a.M);
+        a.tiles_m = (a.M + a.extent_tile_m - 1) / a.extent_tile_m;
+    } else if (a.extent_dim == 2) {
+        const int n = min(v, a.N);
+        a.tiles_n = (n + BN - 1) / BN;
+        if (a.b_idx) a.b_idx_n = n;
+        a.N = min((n + 63) & ~63, a.N);
+    } else {
+        a.K = min(v, a.K);
+        a.num_kb = (a.K + BK - 1) / BK;
+        a.kb_split = a.num_kb;
+        if (a.b_idx) a.b_idx_n = a.K;
+    }
+}
 
 __device__ __forceinline__ int gather_row(const KArgs& a, int p) {
     return p < a.b_idx_n ? __ldg(a.b_idx + p) : a.b_oob_row;
@@ -131,9 +159,11 @@ struct RunBatch {
     }
 };
 
-__global__ void k_kb_runs(const int32_t* __restrict__ idx, int n, int num_kb, int32_t* __restrict__ out) {
+__global__ void k_kb_runs(const int32_t* __restrict__ idx, int n, int num_kb, int32_t* __restrict__ out,
+                          const int32_t* __restrict__ n_dev) {
     const int kb = blockIdx.x * blockDim.x + threadIdx.x;
     if (kb >= num_kb) return;
+    if (n_dev) n = min(n, max(0, *n_dev));
     const int p = kb * BK;
     out[kb] = (p + BK <= n && idx[p + BK - 1] - idx[p] == BK - 1) ? idx[p] : -1;
 }
@@ -593,9 +623,8 @@ __device__ __forceinline__ void adam_tile_rows(const KArgs& a, uint32_t taddr, i
 }
 
 template <bool A_MN, bool B_MN>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
-    k_gemm_bf16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const __grid_constant__ CUtensorMap tmG, const KArgs args) {
+__device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmG,
+                                          const KArgs& args) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -790,6 +819,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     uint32_t r[32];
                     tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c * 32, r);
                     tmem_ld_wait();
+                    if (args.num_kb == 0)  // empty K (a zero extent): nothing was accumulated
+                        for (int j = 0; j < 32; ++j) r[j] = 0u;
                     const int n = ti.n_col0 + c * 32;
                     if (m < ti.m_lim && n < args.N) epilogue_chunk(args, m, n, r, c_off);
                 }
@@ -843,9 +874,8 @@ __device__ __forceinline__ void tile_coords_pair(int tile, const KArgs& args, in
 }
 
 template <bool A_MN, bool B_MN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
-    k_gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ CUtensorMap tmG, const KArgs args) {
+__device__ __forceinline__ void pair_body(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmG,
+                                          const KArgs& args) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + P_STAGES * P_STAGE_BYTES);
@@ -1027,6 +1057,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                     uint32_t r[32];
                     tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c * 32, r);
                     tmem_ld_wait();
+                    if (args.num_kb == 0)  // empty K (a zero extent): nothing was accumulated
+                        for (int j = 0; j < 32; ++j) r[j] = 0u;
                     const int n = nb * BN + c * 32;
                     if (m < args.M && n < args.N) epilogue_chunk(args, m, n, r);
                 }
@@ -1043,6 +1075,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         tc_fence_after();
         tmem_dealloc_pair(tmem_base, TMEM_COLS);
     }
+}
+
+// The kernels. The *_ext variants first shrink a capacity-sized launch to its device-resident extent
+// (apply_extent; a private copy of the arguments); the plain ones read the arguments straight from parameter space.
+template <bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    k_gemm_bf16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmG, const KArgs args) {
+    gemm_body<A_MN, B_MN>(tmA, tmB, tmG, args);
+}
+template <bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    k_gemm_bf16_ext(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ CUtensorMap tmG, const KArgs args_in) {
+    KArgs args = args_in;
+    apply_extent(args);
+    gemm_body<A_MN, B_MN>(tmA, tmB, tmG, args);
+}
+template <bool A_MN, bool B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    k_gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmG, const KArgs args) {
+    pair_body<A_MN, B_MN>(tmA, tmB, tmG, args);
+}
+template <bool A_MN, bool B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    k_gemm_bf16_pair_ext(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                         const __grid_constant__ CUtensorMap tmG, const KArgs args_in) {
+    KArgs args = args_in;
+    apply_extent(args);
+    pair_body<A_MN, B_MN>(tmA, tmB, tmG, args);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -1082,10 +1145,15 @@ int gemm_sms() { return std::max(2, num_sms() - g_reserved_sms.load(std::memory_
 template <bool A_MN, bool B_MN>
 void launch(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tg, const KArgs& args,
             int tiles_bound) {
-    static std::atomic<unsigned long long> attr_done{0};
-    set_max_smem_once(attr_done, reinterpret_cast<const void*>(k_gemm_bf16<A_MN, B_MN>), SMEM_BYTES);
+    static std::atomic<unsigned long long> attr_done{0}, attr_done_ext{0};
     const int grid = std::max(1, std::min(tiles_bound, gemm_sms()));
-    k_gemm_bf16<A_MN, B_MN><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ta, tb, tg, args);
+    if (args.extent_dim) {
+        set_max_smem_once(attr_done_ext, reinterpret_cast<const void*>(k_gemm_bf16_ext<A_MN, B_MN>), SMEM_BYTES);
+        k_gemm_bf16_ext<A_MN, B_MN><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ta, tb, tg, args);
+    } else {
+        set_max_smem_once(attr_done, reinterpret_cast<const void*>(k_gemm_bf16<A_MN, B_MN>), SMEM_BYTES);
+        k_gemm_bf16<A_MN, B_MN><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ta, tb, tg, args);
+    }
     check_launch("k_gemm_bf16");
 }
 
@@ -1161,6 +1229,11 @@ KArgs base_args(int64_t M, int64_t N, int64_t K, const GemmEpilogue& epi) {
     args.stat_ld = epi.stat_ld;
     args.b_idx_n = 0;
     args.b_oob_row = 0;
+    args.extent = epi.extent;
+    args.extent_dim = epi.extent ? epi.extent_dim : 0;
+    args.extent_tile_m = BM;
+    if (args.extent_dim && (args.extent_dim < 1 || args.extent_dim > 3 || epi.ksplit > 1))
+        throw MeftError(2, "gemm_bf16: extent_dim must be 1 (M), 2 (N) or 3 (K), without a K split");
     args.ksplit = 1;
     args.kb_split = args.num_kb;
     args.split_stride = 0;
@@ -1190,12 +1263,18 @@ void dispatch(cudaStream_t st, bool a_mn, bool b_mn, const CUtensorMap& ta, cons
 template <bool A_MN, bool B_MN>
 void launch_pair(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tg, const KArgs& args,
                  int pair_tiles) {
-    static std::atomic<unsigned long long> attr_done{0};
-    set_max_smem_once(attr_done, reinterpret_cast<const void*>(k_gemm_bf16_pair<A_MN, B_MN>),
-                      P_SMEM_BYTES + ADAM_SCRATCH_BYTES);
+    static std::atomic<unsigned long long> attr_done{0}, attr_done_ext{0};
     const int pairs = std::max(1, std::min(pair_tiles, gemm_sms() / 2));
     const int smem = P_SMEM_BYTES + (args.epi == EPI_ADAM_F32 ? ADAM_SCRATCH_BYTES : 0);
-    k_gemm_bf16_pair<A_MN, B_MN><<<2 * pairs, NUM_THREADS, smem, st>>>(ta, tb, tg, args);
+    if (args.extent_dim) {
+        set_max_smem_once(attr_done_ext, reinterpret_cast<const void*>(k_gemm_bf16_pair_ext<A_MN, B_MN>),
+                          P_SMEM_BYTES + ADAM_SCRATCH_BYTES);
+        k_gemm_bf16_pair_ext<A_MN, B_MN><<<2 * pairs, NUM_THREADS, smem, st>>>(ta, tb, tg, args);
+    } else {
+        set_max_smem_once(attr_done, reinterpret_cast<const void*>(k_gemm_bf16_pair<A_MN, B_MN>),
+                          P_SMEM_BYTES + ADAM_SCRATCH_BYTES);
+        k_gemm_bf16_pair<A_MN, B_MN><<<2 * pairs, NUM_THREADS, smem, st>>>(ta, tb, tg, args);
+    }
     check_launch("k_gemm_bf16_pair");
 }
 
@@ -1246,7 +1325,8 @@ void gemm_bf16_one(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmO
         args.b_oob_row = int(B.table_rows);
         if (B.mn_major) {
             if (!B.run_ws) throw MeftError(2, "gemm_bf16: MN-major gathered B needs run_ws");
-            k_kb_runs<<<int((args.num_kb + 255) / 256), 256, 0, st>>>(B.rows, args.b_idx_n, args.num_kb, B.run_ws);
+            k_kb_runs<<<int((args.num_kb + 255) / 256), 256, 0, st>>>(B.rows, args.b_idx_n, args.num_kb, B.run_ws,
+                                                                     args.extent_dim == 3 ? args.extent : nullptr);
             check_launch("k_kb_runs");
             args.kb_run = B.run_ws;
         }
@@ -1257,6 +1337,7 @@ void gemm_bf16_one(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmO
         const CUtensorMap tb = B.mn_major ? make_map(B.ptr, N, B.rows ? B.table_rows : K, B.ld, 64, 64)
                                           : make_map(B.ptr, K, B.rows ? B.table_rows : N, B.ld, 64, 128);
         args.tiles_m = int(ceil_div(M, P_TILE_M));
+        args.extent_tile_m = P_TILE_M;
         // G pair-tiles of M share each streamed B panel.  Measured (ncu dram bytes + time, tools/gemm_check):
         // K-major x K-major (z, dA: K = d) likes 16 (dA 3.31 -> 3.08 ms); the long-K / MN-major GEMMs 8.
         // Sweeping all of M first doubles DRAM reads: a 64 MB 'resident' operand does not survive per-die L2.
@@ -1318,6 +1399,9 @@ void gemm_bf16(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmOpera
     static_assert(kChunk == kGemmPanel, "panel width = chunk width");
     if (epi.kind == EPI_ADAM_F32 && (N > nc || N != epi.ldc))
         throw MeftError(2, "gemm_bf16: the Adam epilogue covers whole table rows of at most 65536 columns");
+    if (epi.extent && ((epi.extent_dim == 1 && M > mc) || (epi.extent_dim == 2 && N > nc) ||
+                       (epi.extent_dim == 3 && K > kc)))
+        throw MeftError(2, "gemm_bf16: a device-sized dimension must fit one launch (at most 65536)");
     if ((mc >= M && nc >= N && kc >= K) || epi.ksplit > 1) return gemm_bf16_one(st, M, N, K, A, B, epi);
     const int64_t ce = (epi.kind == EPI_STORE_F32 || epi.kind == EPI_ROWS_ADD_F32 || epi.kind == EPI_ROWS_STORE_F32)
                            ? 4 : 2;
@@ -1380,6 +1464,7 @@ void gemm_bf16_grouped(cudaStream_t st, int G, int64_t N, int64_t K, const GemmO
     if (G <= 0 || N <= 0 || a_rows <= 0) return;
     if (A.mn_major || B.mn_major) throw MeftError(2, "gemm_bf16_grouped: K-major operands only");
     if (B.rows) throw MeftError(2, "gemm_bf16_grouped: gathered B is not supported");
+    if (epi.extent) throw MeftError(2, "gemm_bf16_grouped: no device-sized extent");
     if (!aligned16(A.ptr) || !aligned16(B.ptr) || (A.ld % 8) || (B.ld % 8))
         throw MeftError(2, "gemm_bf16_grouped: operand alignment");
     check_epilogue(epi);

@@ -95,6 +95,10 @@ struct GemmEpilogue {
     // Launch option, CTA-pair kernel tile order: 0 = the default policy, -1 = sweep N first (the co-running tiles
     // share their A panels; B is re-read every wave), g > 0 = groups of g 256-row M tiles per streamed B panel.
     int raster = 0;
+    // Device-sized extent: M / N / K as passed is a capacity; the kernels read the real size of dimension
+    // extent_dim (1 = M, 2 = N, 3 = K) from device memory, so the launch needs no host read-back (see apply_extent).
+    const int32_t* extent = nullptr;
+    int extent_dim = 0;
 };
 constexpr int kAdamStatTile = 256;  // columns per EPI_ADAM_F32 statistics partial
 

@@ -72,6 +72,10 @@ __global__ void k_guard_check(const uint8_t* __restrict__ p, size_t n, int* __re
 }
 }  // namespace
 
+struct meft_graph {
+    cudaGraphExec_t exec = nullptr;
+};
+
 struct meft_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -94,6 +98,13 @@ struct meft_ctx {
     int adam_mode = -1;  // MEFT_ADAM_*; -1 = not set (environment MEFT_ADAM_EPILOGUE, else EPILOGUE)
     int gather_mode = -1;  // MEFT_GATHER_*; -1 = not set (environment MEFT_GATHER, else AUTO)
     bool check_finite = false;  // fused step: raise MEFT_E_NONFINITE like check_finite (kernels.cpp:7-13)
+    bool host_sync = true;      // meft_ctx_set_host_sync: false = device-sized FFN GEMMs, no mid-step read-back
+
+    bool capturing() const {  // the context stream is being captured into a CUDA graph
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        MEFT_CUDA_CHECK(cudaStreamIsCapturing(stream, &cs));
+        return cs != cudaStreamCaptureStatusNone;
+    }
 
     // phase timing (meft_ctx_set_timing)
     bool timing = false;
@@ -119,6 +130,9 @@ struct meft_ctx {
         Buf& b = scratch[name];
         const size_t extra = guard_mode() ? kGuard : 0;
         if (b.n < bytes) {
+            if (capturing())
+                throw MeftError(MEFT_E_INVALID, "scratch '" + name + "' would grow while capturing a graph: run the "
+                                                "same calls once eagerly before meft_graph_begin");
             if (b.p) MEFT_CUDA_CHECK(cudaFree(b.p));
             b.p = nullptr;
             b.n = 0;
@@ -140,7 +154,7 @@ struct meft_ctx {
 
     // guard mode: verify every scratch guard region and the stores' table gaps; throws naming the damaged buffer
     void check_guards() {
-        if (!guard_mode()) return;
+        if (!guard_mode() || capturing()) return;
         if (!guard_bad) MEFT_CUDA_CHECK(cudaMalloc(&guard_bad, 64 * sizeof(int)));
         int* bad = guard_bad;
         std::vector<std::string> labels;
@@ -414,7 +428,7 @@ GemmEpilogue peer_epilogue(const meft_peer_out& po, bool grad_h, int64_t d) {
 void ffn_forward_impl(meft_ctx* ctx, meft_dtype dt, const void* h, const void* keys_s, const void* values_s,
                       int64_t T, int64_t d, int64_t s, int64_t ld_z, void* z, void* out, bool accumulate,
                       const RowGather& rg = RowGather(), const meft_peer_out* peer = nullptr,
-                      uint32_t* act_bits = nullptr, int64_t panel = 0) {
+                      uint32_t* act_bits = nullptr, int64_t panel = 0, const int32_t* s_dev = nullptr) {
     cudaStream_t st = ctx->stream;
     if (dt == MEFT_F64) {
         double* outd = static_cast<double*>(out);
@@ -449,6 +463,9 @@ void ffn_forward_impl(meft_ctx* ctx, meft_dtype dt, const void* h, const void* k
     e1.bits = act_bits;  // [T x ceil(s / 32)] bitmask of z > 0 for the backward's mask
     e1.ldbits = (s + 31) / 32;
     e1.panel_stride = panel;  // act in kGemmPanel-wide panels (|S| > 65536)
+    // s_dev: s is a capacity, the union size is read on the device (z: N, out: K)
+    e1.extent = s_dev;
+    e1.extent_dim = 2;
     gemm_bf16(st, T, s, d, knob_a(GemmOperand{h, d, false}, G_Z), knob_b(kv_operand(ctx, keys_s, d, false, rg, s), G_Z),
               knob_e(e1, G_Z));
     GemmEpilogue e2;
@@ -460,6 +477,8 @@ void ffn_forward_impl(meft_ctx* ctx, meft_dtype dt, const void* h, const void* k
         e2.ldc = d;
         e2.accumulate = accumulate;
     }
+    e2.extent = s_dev;
+    e2.extent_dim = 3;
     GemmOperand za{z, ld_z, false};
     za.panel_stride = panel;
     gemm_bf16(st, T, d, s, knob_a(za, G_OUT), knob_b(kv_operand(ctx, values_s, d, true, rg, s), G_OUT),
@@ -474,7 +493,8 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
                        cudaEvent_t grad_h_done = nullptr, const std::function<void()>* between = nullptr,
                        const meft_peer_out* peer = nullptr, const GemmEpilogue* epi_values = nullptr,
                        const GemmEpilogue* epi_keys = nullptr, const uint32_t* act_bits = nullptr,
-                       int64_t panel = 0, const void* gT = nullptr, const void* hT = nullptr) {
+                       int64_t panel = 0, const void* gT = nullptr, const void* hT = nullptr,
+                       const int32_t* s_dev = nullptr) {
     cudaStream_t st = ctx->stream;
     if (dt == MEFT_F64) {
         const double* gd = static_cast<const double*>(g);
@@ -530,6 +550,8 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
     e3.bits = const_cast<uint32_t*>(act_bits);  // the forward's bitmask instead of re-reading act (1/16 the bytes)
     e3.ldbits = (s + 31) / 32;
     e3.panel_stride = panel;
+    e3.extent = s_dev;  // s_dev: s is a capacity (dA: N, grad_h: K, grad-W: M)
+    e3.extent_dim = 2;
     gemm_bf16(st, T, s, d, knob_a(GemmOperand{g, d, false}, G_DA),
               knob_b(kv_operand(ctx, values_s, d, false, rg, s), G_DA), knob_e(e3, G_DA));
     if (grad_h || peer) {  // first after masked, so grad_h can stream back while the weight-gradient GEMMs run
@@ -542,6 +564,8 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
             e6.ldc = d;
             e6.accumulate = acc_h;
         }
+        e6.extent = s_dev;
+        e6.extent_dim = 3;
         gemm_bf16(st, T, d, s, knob_a(op(masked, ld_z, false), G_GH),
                   knob_b(kv_operand(ctx, keys_s, d, true, rg, s), G_GH), knob_e(e6, G_GH));
     }
@@ -559,13 +583,18 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
     // grad-W B operands: g / h as stored ([T x d], MN-major) or their [d x T] transposes (K-major) when given
     const GemmOperand gB = gT ? GemmOperand{gT, T, false} : GemmOperand{g, d, true};
     const GemmOperand hB = hT ? GemmOperand{hT, T, false} : GemmOperand{h, d, true};
+    auto rows_extent = [s_dev](GemmEpilogue e) {
+        e.extent = s_dev;
+        e.extent_dim = 1;
+        return e;
+    };
     gemm_bf16(st, s, d, T, knob_a(op(z, ld_z, true), G_GWB), knob_b(gB, G_GWB),
-              knob_e(epi_values ? *epi_values : e4, G_GWB));
+              knob_e(rows_extent(epi_values ? *epi_values : e4), G_GWB));
     if (between) (*between)();  // e.g. consume grad_values before grad_keys reuses its buffer
     GemmEpilogue e5 = e4;  // grad_keys = masked^T h
     e5.c = S_rows ? stage_keys : grad_keys_s;
     gemm_bf16(st, s, d, T, knob_a(op(masked, ld_z, true), G_GWA), knob_b(hB, G_GWA),
-              knob_e(epi_keys ? *epi_keys : e5, G_GWA));
+              knob_e(rows_extent(epi_keys ? *epi_keys : e5), G_GWA));
 }
 
 // ---- store helpers
@@ -839,6 +868,58 @@ meft_status meft_ctx_set_check_finite(meft_ctx* ctx, int enable) {
         require_ctx(ctx);
         ctx->check_finite = enable != 0;
     });
+}
+
+meft_status meft_ctx_set_host_sync(meft_ctx* ctx, int enable) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        ctx->host_sync = enable != 0;
+    });
+}
+
+meft_status meft_graph_begin(meft_ctx* ctx) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(!ctx->capturing(), MEFT_E_INVALID, "graph_begin: the context stream is already being captured");
+        require(!ctx->timing, MEFT_E_INVALID, "graph_begin: phase timing (meft_ctx_set_timing) cannot be captured");
+        // thread-local: an unsafe call (allocation, synchronisation) from this thread fails the capture loudly
+        MEFT_CUDA_CHECK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    });
+}
+
+meft_status meft_graph_end(meft_ctx* ctx, meft_graph** graph) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(graph != nullptr, MEFT_E_INVALID, "graph_end: null output");
+        *graph = nullptr;
+        cudaGraph_t g = nullptr;
+        const cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+        if (e != cudaSuccess || !g) {
+            cudaGetLastError();
+            if (g) cudaGraphDestroy(g);
+            throw MeftError(MEFT_E_CUDA, std::string("graph_end: the capture failed (") + cudaGetErrorString(e) +
+                                             "): a call synchronised or allocated while capturing");
+        }
+        cudaGraphExec_t x = nullptr;
+        const cudaError_t ei = cudaGraphInstantiate(&x, g, 0);
+        cudaGraphDestroy(g);
+        if (ei != cudaSuccess) throw MeftError(MEFT_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei));
+        *graph = new meft_graph{x};
+    });
+}
+
+meft_status meft_graph_launch(meft_ctx* ctx, meft_graph* graph) {
+    return guarded(ctx, [&] {
+        require_ctx(ctx);
+        require(graph != nullptr && graph->exec != nullptr, MEFT_E_INVALID, "graph_launch: null graph");
+        MEFT_CUDA_CHECK(cudaGraphLaunch(graph->exec, ctx->stream));
+    });
+}
+
+void meft_graph_destroy(meft_graph* graph) {
+    if (!graph) return;
+    if (graph->exec) cudaGraphExecDestroy(graph->exec);
+    delete graph;
 }
 
 meft_status meft_set_gemm_sm_reserve(int sms) {
@@ -1602,15 +1683,19 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
                             const int32_t* uni, int64_t su, int64_t holes, double b1, double b2, double eps,
                             double lr, float* out, float* grad_h, cudaEvent_t g_ready, cudaEvent_t fwd_done,
                             cudaEvent_t gh_done = nullptr, const int32_t* tau = nullptr, int64_t kk_eff = 0,
-                            const meft_peer_out* peer = nullptr, const meft_base_ffn* base = nullptr);
+                            const meft_peer_out* peer = nullptr, const meft_base_ffn* base = nullptr,
+                            const int32_t* su_dev = nullptr);
 
 static void ensure_key_stats(meft_ctx* ctx, meft_store* s, int64_t layer);
+static bool adam_epilogue_enabled(const meft_ctx* ctx);
+static void finish_info(meft_ctx* ctx, const meft_store* s, int64_t T, int64_t k, meft_step_info* info);
 
 static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const void* h, const void* g, int64_t T,
                             int64_t kk, int64_t k, double b1, double b2, double eps, double lr, float* out,
                             float* grad_h, int32_t* per_token_user, int32_t* union_user, meft_step_info* info,
                             cudaEvent_t g_ready, cudaEvent_t fwd_done, cudaEvent_t gh_done = nullptr,
-                            const meft_base_ffn* base = nullptr) {
+                            const meft_base_ffn* base = nullptr, bool defer_info = false) {
+    // defer_info (enqueue-only step): the caller synchronises the stream later and then calls finish_info
     const long long launches0 = launch_counter();
     const LayerBufs& L = layer_of(s, layer);
     require(s->prec == MEFT_STORE_MIXED, MEFT_E_INVALID, "layer_step: requires a MIXED precision store");
@@ -1638,12 +1723,36 @@ static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
                          ctx->dev_small + 5, ctx->selection_mode == MEFT_SELECT_AUTO, L.kn, L.kl);
     }
     histogram_add(st, tau, T * kk_eff, L.ehist);
-    union_holes(st, uni, usize, usize + 3);
-    MEFT_CUDA_CHECK(cudaMemcpyAsync(ctx->host_small + 4, usize, 16, cudaMemcpyDeviceToHost, st));
-    MEFT_CUDA_CHECK(cudaStreamSynchronize(st));
-    const int64_t su = ctx->host_small[4];
-    ffn_update_impl(ctx, s, layer, h, g, T, uni, su, ctx->host_small[7], b1, b2, eps, lr, out, grad_h, g_ready,
-                    fwd_done, gh_done, s->train_router ? tau : nullptr, kk_eff, nullptr, base);
+    // Enqueue-only step (host sync off): the FFN GEMMs are launched for the capacity M and read |S| from usize on
+    // the device, so nothing here waits for the selection; otherwise |S| (and the union's hole count, which picks
+    // the gather) is read back once and the GEMMs are sized exactly. Bit-identical either way.
+    const bool device_sized = !ctx->host_sync && !s->pending[size_t(layer)] && !s->train_router &&
+                              !(base && base->n > 0) && !ctx->check_finite && adam_epilogue_enabled(ctx) &&
+                              d % 32 == 0 && M <= kGemmPanel;
+    int64_t su = -1;
+    if (device_sized) {
+        // The gather (TMA from the tables vs a gather kernel, bit-identical) is chosen without the union: from the
+        // hole count a union of T * take uniform draws over M pairs would have, M p (1 - p) with p = exp(-T take / M)
+        // (AUTO's rule then takes TMA from T take / M >= ~9.5: cfg2, 16; cfg1, 2 -> the kernel)
+        const double p = std::exp(-double(T) * double(take) / double(M));
+        const int64_t holes_est = int64_t(std::ceil(double(M) * p * (1.0 - p)));
+        ffn_update_impl(ctx, s, layer, h, g, T, uni, M, holes_est, b1, b2, eps, lr, out, grad_h, g_ready, fwd_done,
+                        gh_done, nullptr, kk_eff, nullptr, nullptr, usize);
+        if (info) {  // the step is fully enqueued: read |S| and the selection counters at its end
+            MEFT_CUDA_CHECK(cudaMemcpyAsync(ctx->host_small + 4, usize, 16, cudaMemcpyDeviceToHost, st));
+            if (!defer_info) MEFT_CUDA_CHECK(cudaStreamSynchronize(st));
+        }
+    } else {
+        require(!ctx->capturing(), MEFT_E_INVALID,
+                "layer_step: this step reads the union size back (host sync on, or a step outside the enqueue-only "
+                "conditions of meft_ctx_set_host_sync) and cannot be captured");
+        union_holes(st, uni, usize, usize + 3);
+        MEFT_CUDA_CHECK(cudaMemcpyAsync(ctx->host_small + 4, usize, 16, cudaMemcpyDeviceToHost, st));
+        MEFT_CUDA_CHECK(cudaStreamSynchronize(st));
+        su = ctx->host_small[4];
+        ffn_update_impl(ctx, s, layer, h, g, T, uni, su, ctx->host_small[7], b1, b2, eps, lr, out, grad_h, g_ready,
+                        fwd_done, gh_done, s->train_router ? tau : nullptr, kk_eff, nullptr, base);
+    }
     if (ctx->check_finite) {  // the reference's check_finite on its matmul outputs (kernels.cpp:7-13)
         int32_t* flag = ctx->dev_small + 20;
         MEFT_CUDA_CHECK(cudaMemsetAsync(flag, 0, 4, st));
@@ -1655,22 +1764,30 @@ static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
     }
 
     if (info) {
-        info->union_size = su;
         info->take = take;
         info->kk_eff = kk_eff;
         info->warned = warned;
         info->gpu_launches = int(launch_counter() - launches0);
-        info->rescored = ctx->host_small[5];
-        info->fallbacks = ctx->host_small[6];
-        info->meter_h2d = 2 * d * su;
-        info->meter_d2h = 2 * d * su;
         info->meter_hidden = T * d;
-        info->beta_paper = double(su) / double(k);
-        info->dedup_ratio = double(su) / double(T * k);
-        info->activated_fraction = double(su) / double(M);
         info->router_flops = T * N * d;
         info->expert_scoring_flops = T * kk * (M / N) * d;
+        if (!(device_sized && defer_info)) finish_info(ctx, s, T, k, info);
     }
+    (void)su;
+}
+
+// The union-dependent fields of meft_step_info from the read-back |S| and selection counters (host_small[4..6]),
+// once the stream has passed the step's read-back copy.
+static void finish_info(meft_ctx* ctx, const meft_store* s, int64_t T, int64_t k, meft_step_info* info) {
+    const int64_t su = ctx->host_small[4], d = s->d;
+    info->union_size = su;
+    info->rescored = ctx->host_small[5];
+    info->fallbacks = ctx->host_small[6];
+    info->meter_h2d = 2 * d * su;
+    info->meter_d2h = 2 * d * su;
+    info->beta_paper = double(su) / double(k);
+    info->dedup_ratio = double(su) / double(T * k);
+    info->activated_fraction = double(su) / double(s->pairs);
 }
 
 // fetch -> sparse_ffn_pa -> sparse_backward -> scatter_grads -> sparse_adam_update for T tokens against the union S
@@ -1730,7 +1847,9 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
                             const int32_t* uni, int64_t su, int64_t holes, double b1, double b2, double eps,
                             double lr, float* out, float* grad_h, cudaEvent_t g_ready, cudaEvent_t fwd_done,
                             cudaEvent_t gh_done, const int32_t* tau, int64_t kk_eff, const meft_peer_out* peer,
-                            const meft_base_ffn* base) {
+                            const meft_base_ffn* base, const int32_t* su_dev) {
+    // su_dev != nullptr: su is the capacity (the store's M) and the union size lives on the device (the
+    // enqueue-only step of layer_step_impl): every union-sized launch reads it there
     const LayerBufs& L = layer_of(s, layer);
     const int64_t d = s->d;
     cudaStream_t st = ctx->stream;
@@ -1769,7 +1888,7 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
     RowGather rg;
     const void* ks = L.c_a;
     const void* vs = L.c_b;
-    if (use_tma_gather(ctx, su, holes)) {
+    if (use_tma_gather(ctx, su, holes)) {  // device-sized: `holes` is layer_step_impl's estimate
         rg.rows = uni;
         rg.table_rows = s->pairs;
     } else {
@@ -1777,7 +1896,8 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
         uint16_t* vsb = static_cast<uint16_t*>(ctx->get("values_s", size_t(std::max<int64_t>(su, 1) * d) * 2));
         if (su > 0) {
             PhaseScope ps(ctx, 1);
-            gather_rows2(st, L.c_a, L.c_b, d * 2, uni, nullptr, su, ksb, vsb);
+            // device-sized: the union's rows plus zero rows up to the next multiple of 64 (apply_extent)
+            gather_rows2(st, L.c_a, L.c_b, d * 2, uni, su_dev, su, ksb, vsb, su_dev != nullptr);
         }
         ks = ksb;
         vs = vsb;
@@ -1810,7 +1930,7 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
             gemm_bf16(st, T, d, base->n, GemmOperand{base_act, ldn, false}, GemmOperand{base->w_out, d, true}, e2);
         }
         ffn_forward_impl(ctx, MEFT_BF16, h, ks, vs, T, d, su, ld, act, outb, base != nullptr, rg, peer, act_bits,
-                         panel);
+                         panel, su_dev);
     }
     if (fwd_done) MEFT_CUDA_CHECK(cudaEventRecord(fwd_done, st));
     if (g_ready) MEFT_CUDA_CHECK(cudaStreamWaitEvent(st, g_ready, 0));
@@ -1839,6 +1959,9 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
             router_update_impl(ctx, s, layer, static_cast<const uint16_t*>(h), act, masked, ld, uni, su, tau, T,
                                kk_eff, b1, b2, eps, lr);
     };
+    require(!su_dev || (!s->pending[size_t(layer)] && !s->train_router && !base && !peer && !panels &&
+                        adam_epilogue_enabled(ctx) && d % 32 == 0),
+            MEFT_E_LOGIC, "device-sized layer step outside the fused-Adam path");
     if (s->pending[size_t(layer)]) {
         // earlier scatter_grads are pending: sparse_backward + scatter_grads fused, the weight-grad GEMM epilogues
         // add straight into the stage rows at S, then Adam consumes every staged pair (memtier.cpp:187-210)
@@ -1863,7 +1986,7 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
         const bool stats = stats_valid && su > 0;
         double* kss = stats ? static_cast<double*>(ctx->get("adam_kss", size_t(su * parts) * 8)) : nullptr;
         int32_t* klsb = stats ? static_cast<int32_t*>(ctx->get("adam_klsb", size_t(su * parts) * 4)) : nullptr;
-        if (su > 0) adam_coef_bump(st, uni, su, L.step, coef, b1, b2, lr);
+        if (su > 0) adam_coef_bump(st, uni, su, L.step, coef, b1, b2, lr, su_dev);
         auto adam_epi = [&](bool keys) {
             GemmEpilogue e;
             e.kind = EPI_ADAM_F32;
@@ -1903,12 +2026,12 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
             }
             ffn_backward_impl(ctx, MEFT_BF16, g, h, act, ks, vs, T, d, su, ld, masked, nullptr, nullptr, ghb,
                               base != nullptr, nullptr, nullptr, nullptr, rg, gh_done, nullptr, peer, &ev, &ek,
-                              act_bits, panel, gT, hT);
+                              act_bits, panel, gT, hT, su_dev);
         }
         train_router();
         if (stats) {
             PhaseScope p4(ctx, 4);
-            adam_stats_finalize(st, uni, su, kss, klsb, parts, L.kn, L.kl);
+            adam_stats_finalize(st, uni, su, kss, klsb, parts, L.kn, L.kl, su_dev);
         }
         return;  // key statistics stay valid (refreshed for exactly the rows that changed)
     } else {
@@ -2125,7 +2248,7 @@ meft_status meft_layer_step_host(meft_ctx* ctx, meft_store* s, int64_t layer, co
         // as its GEMM (scheduled right after `masked`) is done -- overlapping the weight-gradient GEMMs and Adam.
         // The copies are enqueued after the step is (the events are recorded inside it).
         layer_step_impl(ctx, s, layer, hd, gd, T, kk, k, beta1, beta2, eps, lr, od, ghd, nullptr, nullptr, info,
-                        ctx->ev_in, ctx->ev_fwd, ctx->ev_out);
+                        ctx->ev_in, ctx->ev_fwd, ctx->ev_out, nullptr, /*defer_info=*/true);
         if (out_host) {
             MEFT_CUDA_CHECK(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_fwd, 0));
             MEFT_CUDA_CHECK(cudaMemcpyAsync(out_host, od, out_bytes, cudaMemcpyDeviceToHost, ctx->copy_stream));
@@ -2136,6 +2259,7 @@ meft_status meft_layer_step_host(meft_ctx* ctx, meft_store* s, int64_t layer, co
         }
         MEFT_CUDA_CHECK(cudaStreamSynchronize(ctx->copy_stream));
         MEFT_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        if (info) finish_info(ctx, s, T, k, info);  // idempotent when the step already synchronised
     });
 }
 

@@ -16,10 +16,22 @@ namespace {
 template <typename W>
 __global__ void k_gather2(const W* __restrict__ a, const W* __restrict__ b, int64_t row_words,
                           const int32_t* __restrict__ idx, const int32_t* __restrict__ count_dev, int count,
-                          W* __restrict__ oa, W* __restrict__ ob) {
-    const int n = count_dev ? *count_dev : count;
+                          W* __restrict__ oa, W* __restrict__ ob, int pad64) {
+    const int n = count_dev ? min(*count_dev, count > 0 ? count : INT32_MAX) : count;
     const int lane = threadIdx.x & 31;
-    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += (gridDim.x * blockDim.x) >> 5) {
+    // pad64: rows [n, next multiple of 64) (capped at count) are written as zeros -- the padding a device-sized
+    // GEMM reads past the union (gemm_sm100.cu apply_extent)
+    const int n_pad = pad64 ? min((n + 63) & ~63, count) : n;
+    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n_pad; r += (gridDim.x * blockDim.x) >> 5) {
+        if (r >= n) {
+            W* da = oa + int64_t(r) * row_words;
+            W* db = ob + int64_t(r) * row_words;
+            for (int64_t v = lane; v < row_words; v += 32) {
+                da[v] = W{};
+                db[v] = W{};
+            }
+            continue;
+        }
         const W* sa = a + int64_t(idx[r]) * row_words;
         const W* sb = b + int64_t(idx[r]) * row_words;
         W* da = oa + int64_t(r) * row_words;
@@ -228,7 +240,9 @@ __global__ void __launch_bounds__(256) k_adam_mixed(const int32_t* __restrict__ 
 // once (memtier.cpp:192-195, the key column and value row share it) and its bias-correction coefficients are
 // tabulated by position, before either GEMM runs. Same coefficients as k_adam_mixed (adam_coef).
 __global__ void k_adam_coef_bump(const int32_t* __restrict__ rows, int n, int32_t* __restrict__ step,
-                                 float2* __restrict__ coef, float b1, float b2, float lr) {
+                                 float2* __restrict__ coef, float b1, float b2, float lr,
+                                 const int32_t* __restrict__ n_dev) {
+    if (n_dev) n = min(n, max(0, *n_dev));
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
         const int32_t j = rows[r];
         const int t = step[j] + 1;
@@ -243,7 +257,8 @@ __global__ void k_adam_coef_bump(const int32_t* __restrict__ rows, int n, int32_
 // margin (which also covers the fp64 rounding of this 16-term sum).
 __global__ void k_adam_stats_finalize(const int32_t* __restrict__ rows, int n, const double* __restrict__ ss,
                                       const int32_t* __restrict__ lsb, int parts, float* __restrict__ kn,
-                                      int32_t* __restrict__ kl) {
+                                      int32_t* __restrict__ kl, const int32_t* __restrict__ n_dev) {
+    if (n_dev) n = min(n, max(0, *n_dev));
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
         double t = 0.0;
         int l = INT32_MAX;
@@ -419,7 +434,7 @@ void gather_rows1(cudaStream_t st, const void* src, int64_t row_bytes, const int
 }
 
 void gather_rows2(cudaStream_t st, const void* a, const void* b, int64_t row_bytes, const int32_t* idx,
-                  const int32_t* count_dev, int64_t count, void* oa, void* ob) {
+                  const int32_t* count_dev, int64_t count, void* oa, void* ob, bool pad64) {
     if (count <= 0 && !count_dev) return;
     const int64_t warps = count > 0 ? count : int64_t(num_sms()) * 64;
     const int grid = std::max(1, std::min<int>(int((warps * 32 + 255) / 256), num_sms() * 8));
@@ -427,15 +442,15 @@ void gather_rows2(cudaStream_t st, const void* a, const void* b, int64_t row_byt
     if (row_bytes % 16 == 0 && al(a, 16) && al(b, 16) && al(oa, 16) && al(ob, 16))
         k_gather2<uint4><<<grid, 256, 0, st>>>(static_cast<const uint4*>(a), static_cast<const uint4*>(b),
                                                row_bytes / 16, idx, count_dev, int(count), static_cast<uint4*>(oa),
-                                               static_cast<uint4*>(ob));
+                                               static_cast<uint4*>(ob), pad64 ? 1 : 0);
     else if (row_bytes % 8 == 0)
         k_gather2<uint2><<<grid, 256, 0, st>>>(static_cast<const uint2*>(a), static_cast<const uint2*>(b),
                                                row_bytes / 8, idx, count_dev, int(count), static_cast<uint2*>(oa),
-                                               static_cast<uint2*>(ob));
+                                               static_cast<uint2*>(ob), pad64 ? 1 : 0);
     else
         k_gather2<uint16_t><<<grid, 256, 0, st>>>(static_cast<const uint16_t*>(a), static_cast<const uint16_t*>(b),
                                                   row_bytes / 2, idx, count_dev, int(count),
-                                                  static_cast<uint16_t*>(oa), static_cast<uint16_t*>(ob));
+                                                  static_cast<uint16_t*>(oa), static_cast<uint16_t*>(ob), pad64 ? 1 : 0);
     check_launch("k_gather2");
 }
 
@@ -544,16 +559,16 @@ void adam_mixed(cudaStream_t st, const int32_t* rows, const int32_t* count_dev, 
 }
 
 void adam_coef_bump(cudaStream_t st, const int32_t* rows, int64_t n, int32_t* step, float2* coef, double b1,
-                    double b2, double lr) {
+                    double b2, double lr, const int32_t* n_dev) {
     if (n <= 0) return;
-    k_adam_coef_bump<<<grid_for(n), 256, 0, st>>>(rows, int(n), step, coef, float(b1), float(b2), float(lr));
+    k_adam_coef_bump<<<grid_for(n), 256, 0, st>>>(rows, int(n), step, coef, float(b1), float(b2), float(lr), n_dev);
     check_launch("k_adam_coef_bump");
 }
 
 void adam_stats_finalize(cudaStream_t st, const int32_t* rows, int64_t n, const double* ss, const int32_t* lsb,
-                         int64_t parts, float* kn, int32_t* kl) {
+                         int64_t parts, float* kn, int32_t* kl, const int32_t* n_dev) {
     if (n <= 0) return;
-    k_adam_stats_finalize<<<grid_for(n), 256, 0, st>>>(rows, int(n), ss, lsb, int(parts), kn, kl);
+    k_adam_stats_finalize<<<grid_for(n), 256, 0, st>>>(rows, int(n), ss, lsb, int(parts), kn, kl, n_dev);
     check_launch("k_adam_stats_finalize");
 }
 

@@ -6,8 +6,10 @@
 namespace meft_dev {
 
 void gather_rows1(cudaStream_t st, const void* src, int64_t row_bytes, const int32_t* idx, int64_t n, void* dst);
+// count_dev (optional): the row count is *count_dev (at most count when count > 0); pad64 (with count_dev and the
+// capacity as count): rows up to the next multiple of 64 after the count are written as zeros
 void gather_rows2(cudaStream_t st, const void* a, const void* b, int64_t row_bytes, const int32_t* idx,
-                  const int32_t* count_dev, int64_t count, void* oa, void* ob);
+                  const int32_t* count_dev, int64_t count, void* oa, void* ob, bool pad64 = false);
 void check_sorted_unique(cudaStream_t st, const int32_t* idx, int64_t n, int64_t limit, int32_t* err_dev);
 void stage_add(cudaStream_t st, int stage_dtype, void* stage, int64_t d, const int32_t* idx, int64_t n, int g_dtype,
                const void* g, uint8_t* staged);
@@ -36,10 +38,11 @@ void adam_mixed(cudaStream_t st, const int32_t* rows, const int32_t* count_dev, 
                 bool moments_bf16 = false);  // m/v tables are bf16 (COMPACT store), else fp32
 // Adam fused into the weight-gradient GEMMs (EPI_ADAM_F32): advance step[rows[r]] and tabulate its
 // (lr / (1 - b1^t), 1 / (1 - b2^t)) by position; then fold the epilogue's key statistics partials.
+// n_dev (optional): the row count is min(n, *n_dev) -- a device-resident union size with n its capacity
 void adam_coef_bump(cudaStream_t st, const int32_t* rows, int64_t n, int32_t* step, float2* coef, double b1,
-                    double b2, double lr);
+                    double b2, double lr, const int32_t* n_dev = nullptr);
 void adam_stats_finalize(cudaStream_t st, const int32_t* rows, int64_t n, const double* ss, const int32_t* lsb,
-                         int64_t parts, float* kn, int32_t* kl);
+                         int64_t parts, float* kn, int32_t* kl, const int32_t* n_dev = nullptr);
 void adam_f64(cudaStream_t st, const int32_t* rows, const int32_t* count_dev, int64_t count, int64_t d, double* wa,
               double* ma, double* va, double* sa, double* wb, double* mb, double* vb, double* sb, int32_t* step,
               uint8_t* staged, double b1, double b2, double eps, double lr);

@@ -92,6 +92,16 @@ class Context:
         """Fused layer steps raise the reference's 'non-finite' error on NaN / Inf in out or grad_h."""
         self.check(lib().meft_ctx_set_check_finite(self.h, int(on)))
 
+    def set_host_sync(self, on: bool):
+        """on=False: fused layer steps never wait for the device (the FFN GEMMs read |S| on the device), so steps
+        enqueue back to back and can be captured (graph()); bit-identical results (meft_ctx_set_host_sync)."""
+        self.check(lib().meft_ctx_set_host_sync(self.h, int(on)))
+
+    def graph(self):
+        """Capture the enqueue-only calls made inside `with ctx.graph() as g:` into a CUDA graph; g.replay()
+        re-runs them on the context stream. Run the same calls once eagerly first (scratch buffers must exist)."""
+        return Graph(self)
+
     def set_timing(self, on: bool):
         self.check(lib().meft_ctx_set_timing(self.h, int(on)))
 
@@ -101,6 +111,42 @@ class Context:
         ln = (C.c_int64 * 5)()
         self.check(lib().meft_ctx_read_timing(self.h, ms, ln))
         return {p: (ms[i], ln[i]) for i, p in enumerate(self.PHASES)}
+
+
+class Graph:
+    """A CUDA graph of context-stream work (meft_graph_begin / end / launch)."""
+
+    def __init__(self, ctx: Context):
+        self.ctx = ctx
+        self.h = None
+
+    def __enter__(self):
+        self.ctx.check(lib().meft_graph_begin(self.ctx.h))
+        return self
+
+    def __exit__(self, exc_type, exc, tb):
+        h = P()
+        st = lib().meft_graph_end(self.ctx.h, C.byref(h))
+        if exc_type is None:
+            self.ctx.check(st)
+            self.h = h
+        elif h:
+            lib().meft_graph_destroy(h)
+        return False
+
+    def replay(self):
+        self.ctx.check(lib().meft_graph_launch(self.ctx.h, self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().meft_graph_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def kernel_launches() -> int:
@@ -357,26 +403,32 @@ class Store:
         self.ctx.check(lib().meft_sparse_adam_update(self.ctx.h, self.h, layer, beta1, beta2, eps, lr))
 
     def layer_step(self, layer, h, grad_out, kk, k, lr, beta1=0.9, beta2=0.999, eps=1e-8, out=None, grad_h=None,
-                   want_selection=False, base=None):
+                   want_selection=False, base=None, want_info=True, per_token=None, union=None):
         """meft_ffn -> sparse_backward -> scatter_grads -> sparse_adam_update on device buffers (bf16 in).
-        base = (w_in bf16 [d x n], w_out bf16 [n x d], act 0 SiLU / 1 ReLU): the frozen base FFN as well."""
+        base = (w_in bf16 [d x n], w_out bf16 [n x d], act 0 SiLU / 1 ReLU): the frozen base FFN as well.
+        want_info=False passes no meft_step_info (with host sync off the step then never synchronises; returns
+        None); per_token / union: caller-owned int32 outputs ([T x take], [M]) instead of fresh ones."""
         _contig(h, grad_out)
         T, d = h.shape
         take, _, _ = selection_shape(self.pairs, self.experts, kk, k)
-        per = torch.empty((T, take), dtype=torch.int32, device=h.device) if want_selection else None
-        uni = torch.empty(self.pairs, dtype=torch.int32, device=h.device) if want_selection else None
+        per = per_token if per_token is not None else (
+            torch.empty((T, take), dtype=torch.int32, device=h.device) if want_selection else None)
+        uni = union if union is not None else (
+            torch.empty(self.pairs, dtype=torch.int32, device=h.device) if want_selection else None)
         info = _lib.StepInfo()
+        info_p = C.byref(info) if want_info else None
         if base is None:
             self.ctx.check(lib().meft_layer_step(self.ctx.h, self.h, layer, _p(h), _p(grad_out), T, kk, k, beta1,
-                                                 beta2, eps, lr, _p(out), _p(grad_h), _p(per), _p(uni),
-                                                 C.byref(info)))
+                                                 beta2, eps, lr, _p(out), _p(grad_h), _p(per), _p(uni), info_p))
         else:
             w_in, w_out, act = base
             _contig(w_in, w_out)
             bf = _lib.BaseFfn(w_in.data_ptr(), w_out.data_ptr(), w_in.shape[1], act)
             self.ctx.check(lib().meft_layer_step_base(self.ctx.h, self.h, layer, _p(h), _p(grad_out), T, kk, k, beta1,
                                                       beta2, eps, lr, _p(out), _p(grad_h), _p(per), _p(uni),
-                                                      C.byref(info), C.byref(bf)))
+                                                      info_p, C.byref(bf)))
+        if not want_info:
+            return None
         res = {name: getattr(info, name) for name, _ in _lib.StepInfo._fields_}
         res["warned"] = bool(info.warned)
         if want_selection:
