@@ -1,10 +1,13 @@
 // Drop-in shim plumbing (see device.hpp).
 #include "device.hpp"
 
+#include <algorithm>
 #include <cmath>
 #include <map>
 #include <mutex>
+#include <cstring>
 #include <stdexcept>
+#include <thread>
 
 namespace meft::dropin {
 
@@ -122,7 +125,32 @@ DevBuf upload(const double* host, size_t count) {
     return b;
 }
 
-DevBuf upload(const Matrix& m) { return upload(m.data.data(), m.data.size()); }
+// Large pageable sources (whole host tables: ke_select's keys, gather_adapter's tables) go through two page-locked
+// chunks: the host's threads copy chunk i into one while the DMA of chunk i-1 drains the other (the driver's own
+// pageable path copies on one thread).
+DevBuf upload(const Matrix& m) {
+    const size_t count = m.data.size();
+    constexpr size_t kChunk = size_t(4) << 20;  // doubles (32 MB)
+    if (count < 2 * kChunk) return upload(m.data.data(), count);
+    DevBuf b(count * sizeof(double));
+    double* buf[2] = {staging(kStagingSlots - 2, kChunk), staging(kStagingSlots - 1, kChunk)};
+    const unsigned workers = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    size_t i = 0;
+    for (size_t off = 0; off < count; off += kChunk, ++i) {
+        const size_t n = std::min(kChunk, count - off);
+        double* dst = buf[i & 1];
+        const double* src = m.data.data() + off;
+        std::vector<std::thread> pool;
+        const size_t per = (n + workers - 1) / workers;
+        for (size_t lo = 0; lo < n; lo += per)
+            pool.emplace_back([=] { std::memcpy(dst + lo, src + lo, std::min(per, n - lo) * sizeof(double)); });
+        for (auto& t : pool) t.join();
+        check(meft_synchronize(ctx()));  // chunk i-1's DMA is done: its buffer is free for chunk i+1
+        check(meft_copy_to_device(ctx(), static_cast<double*>(b.get()) + off, dst, n * sizeof(double)));
+    }
+    check(meft_synchronize(ctx()));  // the chunks are reused by the next call
+    return b;
+}
 
 DevBuf upload_indices(const std::vector<index_t>& idx) {
     std::vector<int32_t> tmp(idx.begin(), idx.end());
@@ -156,6 +184,25 @@ DevBuf transposed(const DevBuf& src, index_t rows, index_t cols) {
     DevBuf out(size_t(rows * cols) * sizeof(double));
     if (rows * cols > 0) check(meft_transpose_f64(ctx(), src.as<double>(), out.as<double>(), rows, cols));
     return out;
+}
+
+double* staging(int slot, size_t count) {
+    struct Slot {
+        void* p = nullptr;
+        size_t bytes = 0;
+    };
+    static Slot slots[kStagingSlots];
+    if (slot < 0 || slot >= kStagingSlots) throw std::logic_error("staging: slot out of range");
+    Slot& s = slots[slot];
+    const size_t want = std::max<size_t>(count, 1) * sizeof(double);
+    if (s.bytes < want) {
+        if (s.p) check(meft_host_free(ctx(), s.p));
+        s.p = nullptr;
+        s.bytes = 0;
+        check(meft_host_alloc(ctx(), want, &s.p));
+        s.bytes = want;
+    }
+    return static_cast<double*>(s.p);
 }
 
 void require_finite(const Matrix& m, const char* where) {

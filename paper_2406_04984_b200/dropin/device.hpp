@@ -50,6 +50,12 @@ void download_i32(std::vector<int32_t>& host, const DevBuf& b, size_t count);
 // Device transpose of a row-major [rows x cols] float64 buffer.
 DevBuf transposed(const DevBuf& src, index_t rows, index_t cols);
 
+// Reusable page-locked host staging for the row-mirroring transfers: slot `slot` holds at least `count` doubles
+// (grown on demand, never shrunk), so repeated calls neither re-fault fresh pages nor copy through the driver's
+// pageable bounce buffers. Callers hold api_mutex.
+double* staging(int slot, size_t count);
+constexpr int kStagingSlots = 10;  // 0-7: callers' transfer blocks; 8-9: upload(const Matrix&) chunks
+
 // Throws runtime_error("<where>: non-finite entry") like check_finite (kernels.cpp:7-13).
 void require_finite(const Matrix& m, const char* where);
 
