@@ -66,3 +66,19 @@ def test_error_taxonomy_without_gpu(libpath):
     st = L.meft_synchronize(None)
     assert st == 2
     assert "context" in L.meft_last_error(None).decode()
+
+
+def test_enqueue_only_and_graph_entry_points_reject_null_arguments(libpath):
+    """meft_ctx_set_host_sync / meft_graph_* (the enqueue-only step and CUDA graphs) validate before touching CUDA."""
+    import ctypes as C
+
+    from paper_2406_04984_b200 import _lib
+
+    L = _lib.lib()
+    assert L.meft_ctx_set_host_sync(None, 0) == 2
+    assert L.meft_graph_begin(None) == 2
+    out = C.c_void_p()
+    assert L.meft_graph_end(None, C.byref(out)) == 2
+    assert L.meft_graph_launch(None, None) == 2
+    assert "context" in L.meft_last_error(None).decode()
+    L.meft_graph_destroy(None)  # a no-op, like free(NULL)
