@@ -127,7 +127,7 @@ def build_reference_tests(ref_proj: str = "/root/reference/proj", verbose: bool 
     return out
 
 
-CAPI_CHECKS = ("sharded_capi_check",)
+CAPI_CHECKS = ("sharded_capi_check", "graph_capi_check")
 CAPI_CHECK_BIN = os.path.join(ROOT, "build", "capi_tests")
 
 

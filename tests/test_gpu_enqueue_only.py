@@ -229,3 +229,18 @@ def test_enqueue_only_falls_back_outside_the_fused_adam_path(ctxs):
     a.close()
     b.close()
     assert np.isfinite(res[1][1].cpu().numpy()).all()
+
+
+def test_graph_from_a_cpp_program_linked_only_against_the_c_abi():
+    """tests/dropin/graph_capi_check.cpp: the same capture / replay from C++ (no Python), bit for bit."""
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "build", "capi_tests",
+                       "graph_capi_check")
+    if not os.path.exists(exe):
+        pytest.skip("tests/dropin/graph_capi_check.cpp not built (build.build_capi_checks)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "graph_capi_check: OK" in r.stdout
