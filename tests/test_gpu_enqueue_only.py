@@ -76,11 +76,14 @@ SHAPES = [
     (512, 8192, 32, 16, 333, G.STORE_MIXED, "tma"),
     (512, 16384, 64, 128, 2048, G.STORE_MIXED, "auto"),
     (512, 16384, 64, 128, 2048, G.STORE_MIXED, "kernel"),
+    (1056, 3300, 33, 40, 200, G.STORE_MIXED, "auto"),   # M not a multiple of 64, d % 256 != 0, 33 experts
+    (1056, 3300, 33, 40, 200, G.STORE_MIXED, "tma"),
+    (1056, 8192, 32, 64, 384, G.STORE_MIXED, "tma"),   # partial 256-column Adam tiles on the pair kernel
 ]
 
 
 @pytest.mark.parametrize("shape", SHAPES, ids=["cfg1", "pair", "odd", "compact", "pair-tma", "odd-tma", "dense",
-                                                "dense-kernel"])
+                                                "dense-kernel", "m3300", "m3300-tma", "d1056-tma"])
 def test_enqueue_only_step_is_bit_identical_to_the_synchronising_step(ctxs, shape):
     d, M, N, K, T, prec, gather = shape
     kk, lr = 4, 1e-3
