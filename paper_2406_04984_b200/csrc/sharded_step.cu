@@ -8,12 +8,14 @@
 //   (token id, owner-local expert) entries -> owners gather the token rows from the all-gathered h and score them ->
 //   candidate scores all-to-all back -> key norms all-gather -> certified classification -> exact re-scoring
 //   requests all-to-all -> exact scores back -> finalize -> MAX all-reduce of the union bitmap -> FFN + Adam of the
-//   local union over all P*T tokens -> reduce-scatter of out / grad_h.
+//   local union over all P*T tokens, its out / grad_h GEMMs storing every row straight into the row's home over peer
+//   memory (the reduce-scatter fused into the epilogue) -> barrier -> each home folds its slots.
 // Every host-visible count is read once per exchange (the all-to-all sizes), exactly where sharded.py reads them.
 #include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -99,6 +101,10 @@ struct Comm {
     virtual void reduce_scatter_sum_f32(const float* send, float* recv, size_t n_per_rank, cudaStream_t st) = 0;
     // host metadata: every rank's `bytes` in rank order (synchronous)
     virtual void all_gather_host(const void* send, size_t bytes, void* recv, cudaStream_t st) = 0;
+    // every rank's work enqueued on `st` before the barrier is complete before any rank's work after it
+    virtual void barrier(cudaStream_t st) = 0;
+    // the ranks share one process (device pointers are valid across them; no IPC)
+    virtual bool same_process() const = 0;
 };
 
 std::vector<size_t> offsets(const std::vector<size_t>& n) {
@@ -112,9 +118,16 @@ struct NcclComm final : Comm {
     bool owned = false;
     void* meta = nullptr;  // device scratch for host metadata all-gathers
     size_t meta_bytes = 0;
+    int32_t* word = nullptr;  // the barrier's one-word all-reduce
     ~NcclComm() override {
         if (meta) cudaFree(meta);
+        if (word) cudaFree(word);
         if (owned && comm) nccl().CommDestroy(comm);
+    }
+    bool same_process() const override { return false; }
+    void barrier(cudaStream_t st) override {
+        if (!word) MEFT_CUDA_CHECK(cudaMalloc(&word, 4));
+        nck(nccl().AllReduce(word, word, 1, ncclInt32, ncclSum, comm, st), "ncclAllReduce (barrier)");
     }
     void all_gather(const void* send, void* recv, size_t bytes, cudaStream_t st) override {
         nck(nccl().AllGather(send, recv, bytes, ncclInt8, comm, st), "ncclAllGather");
@@ -159,6 +172,12 @@ struct HostComm final : Comm {
     meft_host_comm cb{};
     void call(int rc, const char* what) {
         if (rc != 0) throw MeftError(MEFT_E_NCCL, std::string("host communicator: ") + what + " failed");
+    }
+    bool same_process() const override { return true; }
+    void barrier(cudaStream_t st) override {
+        const uint8_t b = 1;
+        std::vector<uint8_t> all(static_cast<size_t>(world));
+        all_gather_host(&b, 1, all.data(), st);  // synchronises this rank's stream first
     }
     void all_gather_host(const void* send, size_t bytes, void* recv, cudaStream_t st) override {
         MEFT_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -236,10 +255,116 @@ struct Scratch {
     }
 };
 
+// Receive buffers of the reduce-scatter fused into the out / grad_h GEMM epilogues (EPI_PEER_F32, meft_peer_out):
+// each home owns [world x rows x d] fp32 for out and for grad_h; every rank maps every home's pair (CUDA IPC across
+// processes, plain pointers when the ranks share a process) and its GEMMs store each output row straight into the
+// row's home at slot = its rank; the home folds the slots in slot order (meft_peer_reduce) after a barrier.
+struct PeerSet {
+    int world = 0;
+    int64_t rows = 0, d = 0;
+    bool ready = false, failed = false;
+    void* own[2] = {nullptr, nullptr};
+    std::vector<void*> opened;
+    meft_peer_out desc{};
+    void release() {
+        for (void* p : opened) cudaIpcCloseMemHandle(p);
+        opened.clear();
+        for (void*& p : own) {
+            if (p) cudaFree(p);
+            p = nullptr;
+        }
+        ready = false;
+    }
+    ~PeerSet() { release(); }
+};
+
 struct ShardCtx {
     std::unique_ptr<Comm> comm;
     Scratch scratch;
+    PeerSet peers;
+    int last_peer = 0;  // meft_ctx_sharded_peer_path
 };
+
+// Map every home's receive buffers on every rank; all ranks agree (twice: after allocation / export and after
+// opening) so that either all use the fused path or all fall back to the reduce-scatter collectives.
+bool setup_peers(Comm& cm, PeerSet& ps, int64_t rows, int64_t d, cudaStream_t st) {
+    if (ps.world == cm.world && ps.rows == rows && ps.d == d && (ps.ready || ps.failed)) return ps.ready;
+    ps.release();
+    ps.failed = false;
+    ps.world = cm.world;
+    ps.rows = rows;
+    ps.d = d;
+    const size_t bytes = size_t(cm.world) * size_t(rows) * size_t(d) * 4;
+    struct Rec {
+        int32_t ok, pad;
+        uint64_t ptr[2];
+        unsigned char handle[2][64];
+    };
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    Rec mine{};
+    mine.ok = 1;
+    for (int i = 0; i < 2 && mine.ok; ++i) {
+        if (cudaMalloc(&ps.own[i], bytes) != cudaSuccess) {
+            cudaGetLastError();
+            ps.own[i] = nullptr;
+            mine.ok = 0;
+            break;
+        }
+        mine.ptr[i] = reinterpret_cast<uint64_t>(ps.own[i]);
+        if (!cm.same_process()) {
+            cudaIpcMemHandle_t h;
+            if (cudaIpcGetMemHandle(&h, ps.own[i]) != cudaSuccess) {
+                cudaGetLastError();
+                mine.ok = 0;
+            } else {
+                std::memcpy(mine.handle[i], &h, 64);
+            }
+        }
+    }
+    std::vector<Rec> all(static_cast<size_t>(cm.world));
+    cm.all_gather_host(&mine, sizeof(Rec), all.data(), st);
+    int32_t mapped = 1;
+    for (const Rec& r : all) mapped &= r.ok;
+    if (mapped) {
+        ps.desc = meft_peer_out{};
+        ps.desc.world = cm.world;
+        ps.desc.rank = cm.rank;
+        ps.desc.rows = rows;
+        for (int p = 0; p < cm.world && mapped; ++p) {
+            float* base[2];
+            for (int i = 0; i < 2; ++i) {
+                if (p == cm.rank || cm.same_process()) {
+                    base[i] = reinterpret_cast<float*>(all[size_t(p)].ptr[i]);
+                    continue;
+                }
+                cudaIpcMemHandle_t h;
+                std::memcpy(&h, all[size_t(p)].handle[i], 64);
+                void* q = nullptr;
+                if (cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                    cudaGetLastError();
+                    mapped = 0;
+                    break;
+                }
+                ps.opened.push_back(q);
+                base[i] = static_cast<float*>(q);
+            }
+            if (mapped) {
+                ps.desc.out_recv[p] = base[0];
+                ps.desc.grad_h_recv[p] = base[1];
+            }
+        }
+    }
+    std::vector<int32_t> every(static_cast<size_t>(cm.world));
+    cm.all_gather_host(&mapped, 4, every.data(), st);
+    for (int32_t m : every) mapped &= m;
+    if (!mapped) {
+        ps.release();
+        ps.failed = true;
+        return false;
+    }
+    ps.ready = true;
+    return true;
+}
 
 std::mutex g_mu;
 std::unordered_map<const meft_ctx*, std::unique_ptr<ShardCtx>> g_shard;
@@ -490,14 +615,30 @@ void sharded_step(meft_ctx* ctx, ShardCtx& sc, meft_store* store, int64_t layer,
     const int64_t su = host_cnt[0];
     unsigned long long union_size = 0;
     std::memcpy(&union_size, host_cnt + 2, 8);
-    // 8-9. FFN over all P*T tokens on the local part of the union (fused scatter + lazy Adam), partial sums home
-    float* out_p = S.get<float>("out_p", size_t(TT * d));
-    float* gh_p = S.get<float>("gh_p", size_t(TT * d));
-    ok(meft_layer_ffn_local(ctx, store, layer, h_all, g_all, TT, S_loc, su, b1, b2, eps, lr, out_p, gh_p, nullptr,
-                            nullptr, nullptr, nullptr),
-       ctx);
-    cm.reduce_scatter_sum_f32(out_p, out, size_t(T * d), st);
-    cm.reduce_scatter_sum_f32(gh_p, grad_h, size_t(T * d), st);
+    // 8-9. FFN over all P*T tokens on the local part of the union (fused scatter + lazy Adam), partial sums home:
+    // pushed by the out / grad_h GEMM epilogues straight into the homes' receive buffers over peer memory and
+    // folded there in slot order (MEFT_SHARDED_PEER=0, or a rank that cannot map the buffers: reduce-scatters)
+    static const bool peer_env = [] {
+        const char* v = std::getenv("MEFT_SHARDED_PEER");
+        return !(v && v[0] == '0');
+    }();
+    sc.last_peer = peer_env && setup_peers(cm, sc.peers, T, d, st) ? 1 : 0;
+    if (sc.last_peer) {
+        ok(meft_layer_ffn_local(ctx, store, layer, h_all, g_all, TT, S_loc, su, b1, b2, eps, lr, nullptr, nullptr,
+                                nullptr, nullptr, nullptr, &sc.peers.desc),
+           ctx);
+        cm.barrier(st);  // every rank's rows are in this home's slots
+        ok(meft_peer_reduce(ctx, static_cast<const float*>(sc.peers.own[0]), P, T, d, out), ctx);
+        ok(meft_peer_reduce(ctx, static_cast<const float*>(sc.peers.own[1]), P, T, d, grad_h), ctx);
+    } else {
+        float* out_p = S.get<float>("out_p", size_t(TT * d));
+        float* gh_p = S.get<float>("gh_p", size_t(TT * d));
+        ok(meft_layer_ffn_local(ctx, store, layer, h_all, g_all, TT, S_loc, su, b1, b2, eps, lr, out_p, gh_p, nullptr,
+                                nullptr, nullptr, nullptr),
+           ctx);
+        cm.reduce_scatter_sum_f32(out_p, out, size_t(T * d), st);
+        cm.reduce_scatter_sum_f32(gh_p, grad_h, size_t(T * d), st);
+    }
     if (info) {
         std::memset(info, 0, sizeof(*info));
         info->union_size = int64_t(union_size);
@@ -588,6 +729,13 @@ meft_status meft_layer_step_sharded(meft_ctx* ctx, meft_store* shard, int64_t la
         if (!sc.comm) throw MeftError(MEFT_E_LOGIC, "layer_step_sharded: the context has no communicator");
         sharded_step(ctx, sc, shard, layer, w_g, h, grad_out, T, kk, k, beta1, beta2, eps, lr, out, grad_h, per_token,
                      info);
+    });
+}
+
+meft_status meft_ctx_sharded_peer_path(meft_ctx* ctx, int* peer) {
+    return guard(ctx, [&] {
+        if (!ctx || !peer) throw MeftError(MEFT_E_INVALID, "sharded_peer_path: null argument");
+        *peer = shard_of(ctx).last_peer;
     });
 }
 

@@ -743,7 +743,9 @@ class CShardedLayer:
                                                      betas[0], betas[1], eps, lr, _p(out), _p(grad_h), _p(per),
                                                      C.byref(info)))
         res = {name: getattr(info, name) for name, _ in _lib.StepInfo._fields_}
-        res.update(out=out, grad_h=grad_h)
+        peer = C.c_int()
+        self.ctx.check(lib().meft_ctx_sharded_peer_path(self.ctx.h, C.byref(peer)))
+        res.update(out=out, grad_h=grad_h, peer_path=bool(peer.value))  # partial sums pushed over peer memory
         if want_selection:
             res["per_token"] = per
         return res

@@ -62,6 +62,7 @@ def test_capi_sharded_world1_over_nccl_equals_layer_step(ctx):
             assert torch.equal(res["per_token"], want["per_token"])
             assert res["union_size"] == want["union_size"]
             assert torch.equal(res["out"], out) and torch.equal(res["grad_h"], gh)
+            assert res["peer_path"]  # partial sums stored by the GEMM epilogues into the home's buffers
             for n in TABLES:
                 assert torch.equal(shard.tensor(0, n), ref.tensor(0, n)), (step, n)
     finally:
@@ -109,6 +110,7 @@ def test_capi_sharded_multirank_emulated_equals_single_gpu(ctx, P):
         rows = slice(r * T, (r + 1) * T)
         assert torch.equal(res["per_token"], want["per_token"][rows])
         assert res["union_size"] == want["union_size"]
+        assert res["peer_path"]  # every emulated rank pushed into every home's buffers
         assert float((res["out"] - out[rows]).norm() / out[rows].norm()) < 1e-5
         assert float((res["grad_h"] - gh[rows]).norm() / gh[rows].norm()) < 1e-5
         for n in TABLES:
@@ -121,9 +123,12 @@ def test_cpp_program_runs_the_sharded_step_over_nccl(ctx):
     exe = os.path.join(ROOT, "build", "capi_tests", "sharded_capi_check")
     if not os.path.exists(exe):
         pytest.skip("tests/dropin/sharded_capi_check.cpp not built (build.build_capi_checks)")
-    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-    assert "sharded_capi_check: OK" in r.stdout
+    for peer in ("1", "0"):  # the reduce-scatter fused into the GEMM epilogues, and the NCCL reduce-scatter fallback
+        env = dict(os.environ, MEFT_SHARDED_PEER=peer)
+        r = subprocess.run([exe], capture_output=True, text=True, timeout=600, env=env)
+        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+        assert "sharded_capi_check: OK" in r.stdout
+        assert f"peer path {peer}" in r.stdout, r.stdout
 
 
 def test_capi_sharded_rank_with_empty_local_union(ctx):
