@@ -247,3 +247,25 @@ def test_graph_from_a_cpp_program_linked_only_against_the_c_abi():
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "graph_capi_check: OK" in r.stdout
+
+
+def test_host_buffer_step_with_host_sync_off(ctxs):
+    """meft_layer_step_host (pinned host buffers in and out, copies overlapped with the step) on the enqueue-only
+    step: the union read-back is deferred to the call's final synchronisation, results equal the default step."""
+    d, M, N, K, T = 1024, 16384, 64, 32, 300
+    sync, free = ctxs
+    a, b = _store(sync, d, M, N, 17), _store(free, d, M, N, 17)
+    for step in range(2):
+        h, g = _inputs(T, d, 60 + step)
+        hh, gg = h.cpu().pin_memory(), g.cpu().pin_memory()
+        res = []
+        for st in (a, b):
+            out = torch.empty((T, d), dtype=torch.float32).pin_memory()
+            gh = torch.empty_like(out).pin_memory()
+            info = st.layer_step_host(0, hh, gg, 4, K, 1e-3, out_host=out, grad_h_host=gh)
+            res.append((info, out, gh))
+        assert res[0][0]["union_size"] == res[1][0]["union_size"] > 0
+        assert torch.equal(res[0][1], res[1][1]) and torch.equal(res[0][2], res[1][2])
+    _assert_tables_equal(a, b)
+    a.close()
+    b.close()
