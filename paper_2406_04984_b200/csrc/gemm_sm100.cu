@@ -85,6 +85,7 @@ struct KArgs {
     // kernel reads the real size of dimension extent_dim (1 = M, 2 = N, 3 = K) from *extent before its first tile
     const int32_t* extent;
     int extent_dim, extent_tile_m;
+    int b_gather_k;  // gathered B rows index K (MN-major B) rather than N
 };
 
 // Shrink the capacity-sized problem to the device-resident extent (every thread, before any tile is resolved).
@@ -101,13 +102,13 @@ __device__ __forceinline__ void apply_extent(KArgs& a) {
     } else if (a.extent_dim == 2) {
         const int n = min(v, a.N);
         a.tiles_n = (n + BN - 1) / BN;
-        if (a.b_idx) a.b_idx_n = n;
+        if (a.b_idx && !a.b_gather_k) a.b_idx_n = n;
         a.N = min((n + 63) & ~63, a.N);
     } else {
         a.K = min(v, a.K);
         a.num_kb = (a.K + BK - 1) / BK;
         a.kb_split = a.num_kb;
-        if (a.b_idx) a.b_idx_n = a.K;
+        if (a.b_idx && a.b_gather_k) a.b_idx_n = a.K;
     }
 }
 
@@ -1321,6 +1322,7 @@ void gemm_bf16_one(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmO
         if (B.table_rows <= 0 || B.table_rows >= INT32_MAX) throw MeftError(2, "gemm_bf16: gather table rows");
         tg = make_map(B.ptr, B.mn_major ? N : K, B.table_rows, B.ld, 64, 1);
         args.b_idx = B.rows;
+        args.b_gather_k = B.mn_major ? 1 : 0;
         args.b_idx_n = int(B.mn_major ? K : N);
         args.b_oob_row = int(B.table_rows);
         if (B.mn_major) {
