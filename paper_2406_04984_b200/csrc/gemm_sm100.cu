@@ -584,7 +584,8 @@ __device__ __forceinline__ void adam_tile_transposed(const KArgs& a, uint32_t ta
     }
 }
 
-// 1-CTA kernel (small problems): thread = accumulator row, same arithmetic without the transpose.
+// 1-CTA kernel (MEFT_GEMM_PAIR=0 only; the Adam GEMMs otherwise always run on CTA pairs): thread = accumulator row,
+// same arithmetic without the transpose.
 template <bool MOM16>
 __device__ __forceinline__ void adam_tile_rows(const KArgs& a, uint32_t taddr, int m, int n_col0) {
     const bool ok = m < a.M;
@@ -1333,9 +1334,11 @@ void gemm_bf16_one(cudaStream_t st, int64_t M, int64_t N, int64_t K, const GemmO
             args.kb_run = B.run_ws;
         }
     }
-    // large problems: 256x256 tiles on CTA pairs (enough pair-tiles to fill the machine at least once)
+    // large problems: 256x256 tiles on CTA pairs (enough pair-tiles to fill the machine at least once); the Adam
+    // epilogue always (its transposed, coalesced table stream lives in the pair kernel: at cfg1 the two grad-W
+    // GEMMs took 85 us each with the 1-CTA kernel's row-per-thread epilogue)
     const int64_t pair_tiles = ceil_div(M, P_TILE_M) * ceil_div(N, BN);
-    if (pair_tiles >= num_sms() / 2 && pair_mode_enabled() && args.ksplit == 1) {
+    if ((pair_tiles >= num_sms() / 2 || epi.kind == EPI_ADAM_F32) && pair_mode_enabled() && args.ksplit == 1) {
         const CUtensorMap tb = B.mn_major ? make_map(B.ptr, N, B.rows ? B.table_rows : K, B.ld, 64, 64)
                                           : make_map(B.ptr, K, B.rows ? B.table_rows : N, B.ld, 64, 128);
         args.tiles_m = int(ceil_div(M, P_TILE_M));

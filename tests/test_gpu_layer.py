@@ -309,7 +309,7 @@ def test_check_finite_raises_reference_kind(ctx):
         ctx.set_check_finite(False)
 
 
-@pytest.mark.parametrize("shape", [(512, 4096, 64, 32, 256),     # 1-CTA GEMMs (row-wise Adam epilogue)
+@pytest.mark.parametrize("shape", [(512, 4096, 64, 32, 256),     # small: 1-CTA plain GEMMs, 28-pair grad-W GEMMs
                                    (1024, 16384, 64, 64, 512),   # CTA-pair GEMMs (transposed Adam epilogue)
                                    (1056, 8192, 32, 64, 384)])   # d % 256 != 0: partial column tile + stats part
 def test_adam_epilogue_matches_adam_pass_bitwise(ctx, shape):
