@@ -169,9 +169,33 @@ void download(double* host, const DevBuf& b, size_t count) {
     if (count) check(meft_copy_to_host(ctx(), host, b.get(), count * sizeof(double)));
 }
 
+// Large results come back through the same two page-locked chunks: the DMA of chunk i+1 runs while the host's
+// threads copy chunk i out (the driver's pageable path copies on one thread).
 Matrix download_matrix(const DevBuf& b, index_t rows, index_t cols) {
     Matrix m(rows, cols);
-    download(m.data.data(), b, m.data.size());
+    const size_t count = m.data.size();
+    constexpr size_t kChunk = size_t(4) << 20;  // doubles (32 MB)
+    if (count < 2 * kChunk) {
+        download(m.data.data(), b, count);
+        return m;
+    }
+    double* buf[2] = {staging(kStagingSlots - 2, kChunk), staging(kStagingSlots - 1, kChunk)};
+    const unsigned workers = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    size_t i = 0;
+    for (size_t off = 0; off < count; off += kChunk, ++i) {
+        const size_t n = std::min(kChunk, count - off);
+        double* src = buf[i & 1];
+        // chunk i-1's copy-out still reads the other buffer; this DMA fills `src` (synchronous)
+        check(meft_copy_to_host(ctx(), src, static_cast<const double*>(b.get()) + off, n * sizeof(double)));
+        for (auto& t : pool) t.join();  // chunk i-1 copied out: its buffer is free for chunk i+1
+        pool.clear();
+        double* dst = m.data.data() + off;
+        const size_t per = (n + workers - 1) / workers;
+        for (size_t lo = 0; lo < n; lo += per)
+            pool.emplace_back([=] { std::memcpy(dst + lo, src + lo, std::min(per, n - lo) * sizeof(double)); });
+    }
+    for (auto& t : pool) t.join();
     return m;
 }
 
