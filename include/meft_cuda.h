@@ -533,19 +533,21 @@ meft_status meft_ctx_clear_comm(meft_ctx* ctx);
  * entries (owners gather the token rows from the all-gathered h), of candidate scores, of exact-rescoring requests
  * and answers; all-gather of per-destination counts and key norms; MAX all-reduce of the M-byte union bitmap;
  * out / grad_h rows stored by the GEMM epilogues straight into their homes over peer memory and folded there
- * (meft_ctx_sharded_peer_path; else a reduce-scatter of out / grad_h). per_token [T x take] (global pair ids, ascending) may be NULL. At world 1 the
+ * (meft_ctx_sharded_paths; else a reduce-scatter of out / grad_h). per_token [T x take] (global pair ids, ascending) may be NULL. At world 1 the
  * step equals meft_layer_step bit for bit. Replaces the reference trainer's per-layer calls (trainer.cpp:220, 270,
  * 283, 525) for a sharded layer. */
 meft_status meft_layer_step_sharded(meft_ctx* ctx, meft_store* shard, int64_t layer, const uint16_t* w_g,
                                     const uint16_t* h, const uint16_t* grad_out, int64_t T, int64_t kk, int64_t k,
                                     double beta1, double beta2, double eps, double lr, float* out, float* grad_h,
                                     int32_t* per_token, meft_step_info* info);
-/* How the last meft_layer_step_sharded on this context returned the out / grad_h partial sums to the token homes:
- * *peer = 1 when its out / grad_h GEMM epilogues stored them straight into the homes' receive buffers over peer
- * memory (the reduce-scatter fused into the GEMMs; the default whenever every rank can map every home's buffers --
- * CUDA IPC across processes), 0 when it fell back to the communicator's reduce-scatters (MEFT_SHARDED_PEER=0, or a
- * rank could not allocate / map them). */
-meft_status meft_ctx_sharded_peer_path(meft_ctx* ctx, int* peer);
+/* Which data paths the last meft_layer_step_sharded on this context took. *peer = 1 when its out / grad_h GEMM
+ * epilogues stored the partial sums straight into the token homes' receive buffers over peer memory (the
+ * reduce-scatter fused into the GEMMs; the default whenever every rank can map every home's buffers -- CUDA IPC
+ * across processes), 0 when it fell back to the communicator's reduce-scatters (MEFT_SHARDED_PEER=0, or a rank
+ * could not allocate / map them). *overlap = 1 when grad_out's all-gather ran on a second NCCL communicator
+ * (ncclCommSplit) and stream behind the selection and forward, 0 when it ran in stream order (host-callback
+ * communicators, or no ncclCommSplit). Either pointer may be NULL. */
+meft_status meft_ctx_sharded_paths(meft_ctx* ctx, int* peer, int* overlap);
 
 
 #ifdef __cplusplus

@@ -143,7 +143,7 @@ _SIGS = {
     "meft_ctx_set_host_comm": (INT, [P, C.POINTER(HostComm), INT, INT]),
     "meft_ctx_clear_comm": (INT, [P]),
     "meft_layer_step_sharded": (INT, [P, P, I64, P, P, P, I64, I64, I64, D, D, D, D, P, P, P, P]),
-    "meft_ctx_sharded_peer_path": (INT, [P, P]),
+    "meft_ctx_sharded_paths": (INT, [P, P, P]),
 }
 
 F64, F32, BF16 = 0, 1, 2

@@ -51,6 +51,7 @@ struct NcclApi {
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;  // optional (>= 2.18)
 };
 
 const NcclApi& nccl() {
@@ -76,6 +77,7 @@ const NcclApi& nccl() {
         api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
         api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
         api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+        api.CommSplit = reinterpret_cast<decltype(api.CommSplit)>(sym("ncclCommSplit"));
         api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllGather && api.AllReduce &&
                  api.ReduceScatter && api.Send && api.Recv && api.GroupStart && api.GroupEnd && api.GetErrorString;
         if (!api.ok) api.why = "libnccl.so.2 lacks a required symbol";
@@ -105,6 +107,10 @@ struct Comm {
     virtual void barrier(cudaStream_t st) = 0;
     // the ranks share one process (device pointers are valid across them; no IPC)
     virtual bool same_process() const = 0;
+    // All-gather on a second communicator and stream, started once `ready` (recorded on the caller's stream) has
+    // fired; returns the event that fires when it is done, or nullptr when this communicator cannot overlap (the
+    // caller then all-gathers in stream order).
+    virtual cudaEvent_t all_gather_behind(const void*, void*, size_t, cudaEvent_t) { return nullptr; }
 };
 
 std::vector<size_t> offsets(const std::vector<size_t>& n) {
@@ -119,10 +125,35 @@ struct NcclComm final : Comm {
     void* meta = nullptr;  // device scratch for host metadata all-gathers
     size_t meta_bytes = 0;
     int32_t* word = nullptr;  // the barrier's one-word all-reduce
+    // bulk exchanges that overlap the step: a communicator split off `comm` (collective: every rank creates it in its
+    // first step) with its own stream, so its kernels never queue behind the selection's collectives
+    ncclComm_t bulk = nullptr;
+    cudaStream_t bulk_stream = nullptr;
+    cudaEvent_t bulk_done = nullptr;
+    bool bulk_tried = false;
     ~NcclComm() override {
         if (meta) cudaFree(meta);
         if (word) cudaFree(word);
+        if (bulk) nccl().CommDestroy(bulk);
+        if (bulk_done) cudaEventDestroy(bulk_done);
+        if (bulk_stream) cudaStreamDestroy(bulk_stream);
         if (owned && comm) nccl().CommDestroy(comm);
+    }
+    cudaEvent_t all_gather_behind(const void* send, void* recv, size_t bytes, cudaEvent_t ready) override {
+        if (!bulk_tried) {  // every rank takes this branch in the same (first) step
+            bulk_tried = true;
+            if (nccl().CommSplit && nccl().CommSplit(comm, 0, rank, &bulk, nullptr) == ncclSuccess) {
+                MEFT_CUDA_CHECK(cudaStreamCreateWithFlags(&bulk_stream, cudaStreamNonBlocking));
+                MEFT_CUDA_CHECK(cudaEventCreateWithFlags(&bulk_done, cudaEventDisableTiming));
+            } else {
+                bulk = nullptr;
+            }
+        }
+        if (!bulk) return nullptr;
+        MEFT_CUDA_CHECK(cudaStreamWaitEvent(bulk_stream, ready, 0));
+        nck(nccl().AllGather(send, recv, bytes, ncclInt8, bulk, bulk_stream), "ncclAllGather (bulk)");
+        MEFT_CUDA_CHECK(cudaEventRecord(bulk_done, bulk_stream));
+        return bulk_done;
     }
     bool same_process() const override { return false; }
     void barrier(cudaStream_t st) override {
@@ -282,7 +313,11 @@ struct ShardCtx {
     std::unique_ptr<Comm> comm;
     Scratch scratch;
     PeerSet peers;
-    int last_peer = 0;  // meft_ctx_sharded_peer_path
+    int last_peer = 0, last_overlap = 0;  // meft_ctx_sharded_paths
+    cudaEvent_t in_ready = nullptr;  // the step's inputs are ready (start of the overlapped grad_out all-gather)
+    ~ShardCtx() {
+        if (in_ready) cudaEventDestroy(in_ready);
+    }
 };
 
 // Map every home's receive buffers on every rank; all ranks agree (twice: after allocation / export and after
@@ -483,11 +518,18 @@ void sharded_step(meft_ctx* ctx, ShardCtx& sc, meft_store* store, int64_t layer,
                                                   std::to_string(ts[size_t(p)]) + " tokens, this rank " +
                                                   std::to_string(T) + " (all ranks need the same T)");
     }
-    // all-gather the hidden states and the incoming gradient (rank order: rank p's tokens are rows [p*T, (p+1)*T))
+    // all-gather the hidden states and the incoming gradient (rank order: rank p's tokens are rows [p*T, (p+1)*T)).
+    // grad_out is needed only by the backward: over NCCL it travels on the bulk communicator behind the selection
+    // and the forward, and the FFN waits for it (g_ready) just before its backward GEMMs. Its buffer's previous
+    // readers (the last step's backward) precede `in_ready` on this stream.
     uint16_t* h_all = S.get<uint16_t>("h_all", size_t(TT * d));
     uint16_t* g_all = S.get<uint16_t>("g_all", size_t(TT * d));
+    if (!sc.in_ready) MEFT_CUDA_CHECK(cudaEventCreateWithFlags(&sc.in_ready, cudaEventDisableTiming));
+    MEFT_CUDA_CHECK(cudaEventRecord(sc.in_ready, st));
+    cudaEvent_t g_ready = cm.all_gather_behind(g, g_all, size_t(T * d) * 2, sc.in_ready);
     cm.all_gather(h, h_all, size_t(T * d) * 2, st);
-    cm.all_gather(g, g_all, size_t(T * d) * 2, st);
+    if (!g_ready) cm.all_gather(g, g_all, size_t(T * d) * 2, st);
+    sc.last_overlap = g_ready ? 1 : 0;
 
     // 1. route this rank's tokens (certified, exact tau)
     int32_t* tau = S.get<int32_t>("tau", size_t(n));
@@ -625,7 +667,7 @@ void sharded_step(meft_ctx* ctx, ShardCtx& sc, meft_store* store, int64_t layer,
     sc.last_peer = peer_env && setup_peers(cm, sc.peers, T, d, st) ? 1 : 0;
     if (sc.last_peer) {
         ok(meft_layer_ffn_local(ctx, store, layer, h_all, g_all, TT, S_loc, su, b1, b2, eps, lr, nullptr, nullptr,
-                                nullptr, nullptr, nullptr, &sc.peers.desc),
+                                g_ready, nullptr, nullptr, &sc.peers.desc),
            ctx);
         cm.barrier(st);  // every rank's rows are in this home's slots
         ok(meft_peer_reduce(ctx, static_cast<const float*>(sc.peers.own[0]), P, T, d, out), ctx);
@@ -633,7 +675,7 @@ void sharded_step(meft_ctx* ctx, ShardCtx& sc, meft_store* store, int64_t layer,
     } else {
         float* out_p = S.get<float>("out_p", size_t(TT * d));
         float* gh_p = S.get<float>("gh_p", size_t(TT * d));
-        ok(meft_layer_ffn_local(ctx, store, layer, h_all, g_all, TT, S_loc, su, b1, b2, eps, lr, out_p, gh_p, nullptr,
+        ok(meft_layer_ffn_local(ctx, store, layer, h_all, g_all, TT, S_loc, su, b1, b2, eps, lr, out_p, gh_p, g_ready,
                                 nullptr, nullptr, nullptr),
            ctx);
         cm.reduce_scatter_sum_f32(out_p, out, size_t(T * d), st);
@@ -732,10 +774,12 @@ meft_status meft_layer_step_sharded(meft_ctx* ctx, meft_store* shard, int64_t la
     });
 }
 
-meft_status meft_ctx_sharded_peer_path(meft_ctx* ctx, int* peer) {
+meft_status meft_ctx_sharded_paths(meft_ctx* ctx, int* peer, int* overlap) {
     return guard(ctx, [&] {
-        if (!ctx || !peer) throw MeftError(MEFT_E_INVALID, "sharded_peer_path: null argument");
-        *peer = shard_of(ctx).last_peer;
+        if (!ctx) throw MeftError(MEFT_E_INVALID, "sharded_paths: null context");
+        const ShardCtx& sc = shard_of(ctx);
+        if (peer) *peer = sc.last_peer;
+        if (overlap) *overlap = sc.last_overlap;
     });
 }
 

@@ -743,9 +743,10 @@ class CShardedLayer:
                                                      betas[0], betas[1], eps, lr, _p(out), _p(grad_h), _p(per),
                                                      C.byref(info)))
         res = {name: getattr(info, name) for name, _ in _lib.StepInfo._fields_}
-        peer = C.c_int()
-        self.ctx.check(lib().meft_ctx_sharded_peer_path(self.ctx.h, C.byref(peer)))
-        res.update(out=out, grad_h=grad_h, peer_path=bool(peer.value))  # partial sums pushed over peer memory
+        peer, overlap = C.c_int(), C.c_int()
+        self.ctx.check(lib().meft_ctx_sharded_paths(self.ctx.h, C.byref(peer), C.byref(overlap)))
+        # peer_path: partial sums pushed over peer memory; overlap: grad_out all-gathered behind the selection
+        res.update(out=out, grad_h=grad_h, peer_path=bool(peer.value), overlap=bool(overlap.value))
         if want_selection:
             res["per_token"] = per
         return res

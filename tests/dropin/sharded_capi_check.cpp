@@ -101,11 +101,11 @@ int main() {
             same_tables = same_tables && host_copy<uint32_t>(ctx, p[0], size_t(r_ * c_)) ==
                                              host_copy<uint32_t>(ctx, p[1], size_t(r_ * c_));
         }
-        int peer = -1;
-        ck(meft_ctx_sharded_peer_path(ctx, &peer), ctx, "sharded_peer_path");
-        std::printf("step %d: |S| %lld, selection %s, out %s, grad_h %s, tables %s, peer path %d\n", step,
+        int peer = -1, overlap = -1;
+        ck(meft_ctx_sharded_paths(ctx, &peer, &overlap), ctx, "sharded_paths");
+        std::printf("step %d: |S| %lld, selection %s, out %s, grad_h %s, tables %s, peer path %d, overlap %d\n", step,
                     (long long)info[1].union_size, same_sel ? "equal" : "DIFFER", same_out ? "equal" : "DIFFER",
-                    same_gh ? "equal" : "DIFFER", same_tables ? "equal" : "DIFFER", peer);
+                    same_gh ? "equal" : "DIFFER", same_tables ? "equal" : "DIFFER", peer, overlap);
         failures += !(same_out && same_gh && same_sel && same_s && same_tables);
         meft_device_free(ctx, const_cast<uint16_t*>(h));
         meft_device_free(ctx, const_cast<uint16_t*>(g));

@@ -63,6 +63,7 @@ def test_capi_sharded_world1_over_nccl_equals_layer_step(ctx):
             assert res["union_size"] == want["union_size"]
             assert torch.equal(res["out"], out) and torch.equal(res["grad_h"], gh)
             assert res["peer_path"]  # partial sums stored by the GEMM epilogues into the home's buffers
+            assert res["overlap"]  # grad_out all-gathered on a second (split) NCCL communicator and stream
             for n in TABLES:
                 assert torch.equal(shard.tensor(0, n), ref.tensor(0, n)), (step, n)
     finally:
@@ -129,6 +130,7 @@ def test_cpp_program_runs_the_sharded_step_over_nccl(ctx):
         assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
         assert "sharded_capi_check: OK" in r.stdout
         assert f"peer path {peer}" in r.stdout, r.stdout
+        assert "overlap 1" in r.stdout, r.stdout  # grad_out all-gathered on the split communicator's stream
 
 
 def test_capi_sharded_rank_with_empty_local_union(ctx):
