@@ -88,6 +88,7 @@ class ClockSampler:
     def __init__(self, device_index=0, period=0.01):
         self.samples, self.reasons, self.period, self.ok = [], set(), period, False
         self.max_mhz = None
+        self.power_mw, self.power_limit_mw = [], None  # board power draw under load vs the enforced cap
         try:
             import pynvml
 
@@ -95,6 +96,10 @@ class ClockSampler:
             self.nv = pynvml
             self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            try:
+                self.power_limit_mw = pynvml.nvmlDeviceGetEnforcedPowerLimit(self.h)
+            except Exception:
+                self.power_limit_mw = None
             self.ok = True
         except Exception:
             self.ok = False
@@ -113,6 +118,10 @@ class ClockSampler:
                 for bit, name in self.REASONS.items():
                     if r & bit and name != "gpu_idle":
                         self.reasons.add(name)
+                try:
+                    self.power_mw.append(nv.nvmlDeviceGetPowerUsage(self.h))
+                except Exception:
+                    pass
             except Exception:
                 pass
             time.sleep(self.period)
@@ -132,7 +141,13 @@ class ClockSampler:
     def summary(self):
         s = sorted(self.samples)
         med = s[len(s) // 2] if s else None
-        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(s)}
+        p = sorted(self.power_mw)
+        out = {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(s)}
+        if p:  # median board power under load next to the enforced limit (the power cap the GEMMs run into)
+            out["power_w"] = round(p[len(p) // 2] / 1e3, 1)
+        if self.power_limit_mw:
+            out["power_limit_w"] = round(self.power_limit_mw / 1e3, 1)
+        return out
 
 
 # ----------------------------------------------------------------------------------------------- reference arm
