@@ -118,8 +118,10 @@ class ClockSampler:
                 for bit, name in self.REASONS.items():
                     if r & bit and name != "gpu_idle":
                         self.reasons.add(name)
-                try:
-                    self.power_mw.append(nv.nvmlDeviceGetPowerUsage(self.h))
+                try:  # the instantaneous reading (nvmlDeviceGetPowerUsage averages over ~1 s, longer than the
+                    # timed region of a short run)
+                    fv = nv.nvmlDeviceGetFieldValues(self.h, [nv.NVML_FI_DEV_POWER_INSTANT])[0]
+                    self.power_mw.append(fv.value.uiVal if fv.nvmlReturn == 0 else nv.nvmlDeviceGetPowerUsage(self.h))
                 except Exception:
                     pass
             except Exception:
