@@ -110,7 +110,7 @@ struct Comm {
     // All-gather on a second communicator and stream, started once `ready` (recorded on the caller's stream) has
     // fired; returns the event that fires when it is done, or nullptr when this communicator cannot overlap (the
     // caller then all-gathers in stream order).
-    virtual cudaEvent_t all_gather_behind(const void*, void*, size_t, cudaEvent_t) { return nullptr; }
+    virtual cudaEvent_t all_gather_behind(const void*, void*, size_t, cudaEvent_t, cudaStream_t) { return nullptr; }
 };
 
 std::vector<size_t> offsets(const std::vector<size_t>& n) {
@@ -139,13 +139,24 @@ struct NcclComm final : Comm {
         if (bulk_stream) cudaStreamDestroy(bulk_stream);
         if (owned && comm) nccl().CommDestroy(comm);
     }
-    cudaEvent_t all_gather_behind(const void* send, void* recv, size_t bytes, cudaEvent_t ready) override {
+    cudaEvent_t all_gather_behind(const void* send, void* recv, size_t bytes, cudaEvent_t ready,
+                                  cudaStream_t st) override {
         if (!bulk_tried) {  // every rank takes this branch in the same (first) step
             bulk_tried = true;
+            int32_t ok = 0;
             if (nccl().CommSplit && nccl().CommSplit(comm, 0, rank, &bulk, nullptr) == ncclSuccess) {
-                MEFT_CUDA_CHECK(cudaStreamCreateWithFlags(&bulk_stream, cudaStreamNonBlocking));
-                MEFT_CUDA_CHECK(cudaEventCreateWithFlags(&bulk_done, cudaEventDisableTiming));
+                ok = cudaStreamCreateWithFlags(&bulk_stream, cudaStreamNonBlocking) == cudaSuccess &&
+                     cudaEventCreateWithFlags(&bulk_done, cudaEventDisableTiming) == cudaSuccess;
+                if (!ok) cudaGetLastError();
             } else {
+                bulk = nullptr;
+            }
+            // all ranks use the split communicator, or none does (a rank without it would never join its collectives)
+            std::vector<int32_t> every(static_cast<size_t>(world));
+            all_gather_host(&ok, 4, every.data(), st);
+            for (int32_t e : every) ok &= e;
+            if (!ok && bulk) {
+                nccl().CommDestroy(bulk);
                 bulk = nullptr;
             }
         }
@@ -322,7 +333,7 @@ struct ShardCtx {
 
 // Map every home's receive buffers on every rank; all ranks agree (twice: after allocation / export and after
 // opening) so that either all use the fused path or all fall back to the reduce-scatter collectives.
-bool setup_peers(Comm& cm, PeerSet& ps, int64_t rows, int64_t d, cudaStream_t st) {
+bool setup_peers(Comm& cm, PeerSet& ps, int64_t rows, int64_t d, cudaStream_t st, bool wanted) {
     if (ps.world == cm.world && ps.rows == rows && ps.d == d && (ps.ready || ps.failed)) return ps.ready;
     ps.release();
     ps.failed = false;
@@ -337,7 +348,7 @@ bool setup_peers(Comm& cm, PeerSet& ps, int64_t rows, int64_t d, cudaStream_t st
     };
     static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");
     Rec mine{};
-    mine.ok = 1;
+    mine.ok = wanted ? 1 : 0;  // a rank that opts out (MEFT_SHARDED_PEER=0) takes every rank to the fallback
     for (int i = 0; i < 2 && mine.ok; ++i) {
         if (cudaMalloc(&ps.own[i], bytes) != cudaSuccess) {
             cudaGetLastError();
@@ -526,7 +537,7 @@ void sharded_step(meft_ctx* ctx, ShardCtx& sc, meft_store* store, int64_t layer,
     uint16_t* g_all = S.get<uint16_t>("g_all", size_t(TT * d));
     if (!sc.in_ready) MEFT_CUDA_CHECK(cudaEventCreateWithFlags(&sc.in_ready, cudaEventDisableTiming));
     MEFT_CUDA_CHECK(cudaEventRecord(sc.in_ready, st));
-    cudaEvent_t g_ready = cm.all_gather_behind(g, g_all, size_t(T * d) * 2, sc.in_ready);
+    cudaEvent_t g_ready = cm.all_gather_behind(g, g_all, size_t(T * d) * 2, sc.in_ready, st);
     cm.all_gather(h, h_all, size_t(T * d) * 2, st);
     if (!g_ready) cm.all_gather(g, g_all, size_t(T * d) * 2, st);
     sc.last_overlap = g_ready ? 1 : 0;
@@ -664,7 +675,7 @@ void sharded_step(meft_ctx* ctx, ShardCtx& sc, meft_store* store, int64_t layer,
         const char* v = std::getenv("MEFT_SHARDED_PEER");
         return !(v && v[0] == '0');
     }();
-    sc.last_peer = peer_env && setup_peers(cm, sc.peers, T, d, st) ? 1 : 0;
+    sc.last_peer = setup_peers(cm, sc.peers, T, d, st, peer_env) ? 1 : 0;
     if (sc.last_peer) {
         ok(meft_layer_ffn_local(ctx, store, layer, h_all, g_all, TT, S_loc, su, b1, b2, eps, lr, nullptr, nullptr,
                                 g_ready, nullptr, nullptr, &sc.peers.desc),
