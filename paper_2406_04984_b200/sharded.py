@@ -496,6 +496,12 @@ class ShardedLayer:
             # persistent FFN GEMMs so its kernels can run beside them (~5% of GEMM throughput).
             env = os.environ.get("MEFT_SHARDED_PEER")
             self.peer_mode = (env == "1") or (env is None and self.world > 1)
+            if self.world > 1:  # every rank takes the same path (the peer exchange is collective): MIN over ranks
+                flag = torch.tensor([int(self.peer_mode)], dtype=torch.int32,
+                                    device="cpu" if self.host_group is not None else engine.dev)
+                dist.all_reduce(flag, op=dist.ReduceOp.MIN,
+                                group=self.host_group if self.host_group is not None else group)
+                self.peer_mode = bool(flag.item())
             self.peer = None
             self.comm_ctx = None
             self.reserve_sms = 0 if (self.peer_mode or self.world == 1) else int(
