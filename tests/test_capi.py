@@ -82,3 +82,29 @@ def test_enqueue_only_and_graph_entry_points_reject_null_arguments(libpath):
     assert L.meft_graph_launch(None, None) == 2
     assert "context" in L.meft_last_error(None).decode()
     L.meft_graph_destroy(None)  # a no-op, like free(NULL)
+
+
+def test_header_is_plain_c_and_links(libpath, tmp_path):
+    """include/meft_cuda.h is a C header (the FFI boundary): a C11 translation unit compiles against it with
+    -pedantic -Werror, links against libmeft_cuda.so and calls into it (argument validation, no GPU needed)."""
+    import shutil
+    import subprocess
+
+    if not shutil.which("gcc"):
+        pytest.skip("gcc not available")
+    src = tmp_path / "caller.c"
+    src.write_text('#include "meft_cuda.h"\n'
+                   "int main(void) {\n"
+                   "    int peer = 0, overlap = 0;\n"
+                   "    meft_graph_destroy((meft_graph*)0);\n"
+                   "    if (meft_ctx_sharded_paths((meft_ctx*)0, &peer, &overlap) != MEFT_E_INVALID) return 10;\n"
+                   "    return meft_ctx_set_host_sync((meft_ctx*)0, 0) == MEFT_E_INVALID ? 0 : 11;\n"
+                   "}\n")
+    exe = tmp_path / "caller"
+    libdir = os.path.dirname(libpath)
+    r = subprocess.run(["gcc", "-std=c11", "-Wall", "-Wextra", "-pedantic", "-Werror", "-I",
+                        os.path.join(ROOT, "include"), str(src), "-o", str(exe), "-L", libdir, "-lmeft_cuda",
+                        "-Wl,-rpath," + libdir], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
