@@ -1730,6 +1730,9 @@ static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
                               !(base && base->n > 0) && !ctx->check_finite && adam_epilogue_enabled(ctx) &&
                               d % 32 == 0 && M <= kGemmPanel;
     int64_t su = -1;
+    if (device_sized && info && !defer_info)
+        require(!ctx->capturing(), MEFT_E_INVALID,
+                "layer_step: pass a NULL meft_step_info while capturing a graph (it is read back at the step's end)");
     if (device_sized) {
         // The gather (TMA from the tables vs a gather kernel, bit-identical) is chosen without the union: from the
         // hole count a union of T * take uniform draws over M pairs would have, M p (1 - p) with p = exp(-T take / M)

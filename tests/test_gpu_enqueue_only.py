@@ -212,6 +212,22 @@ def test_a_synchronising_step_cannot_be_captured(side):
     st.close()
 
 
+def test_capturing_a_step_that_asks_for_its_info_is_refused(side):
+    """meft_step_info is read back at the end of an enqueue-only step: while capturing, the step asks for NULL."""
+    _, free = side
+    d, M, N, K, T = 512, 4096, 64, 32, 256
+    st = _store(free, d, M, N, 4)
+    h, g = _inputs(T, d, 70)
+    torch.cuda.synchronize()
+    st.layer_step(0, h, g, 4, K, 1e-3, want_info=False)  # warm-up
+    torch.cuda.synchronize()
+    with pytest.raises(G.MeftError, match="NULL meft_step_info"):
+        with free.graph():
+            st.layer_step(0, h, g, 4, K, 1e-3)  # want_info=True
+    torch.cuda.synchronize()
+    st.close()
+
+
 def test_enqueue_only_falls_back_outside_the_fused_adam_path(ctxs):
     """Pending scatter_grads take the synchronising path even with host sync off (same results as host sync on)."""
     sync, free = ctxs
