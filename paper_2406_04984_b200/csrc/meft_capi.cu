@@ -80,6 +80,9 @@ struct meft_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;  // overlaps host transfers with compute in the _host step
+    // small FFNs: out and grad_h run on a side stream beside dA / the grad-W GEMMs (SmallFfnStreams)
+    cudaStream_t side_stream = nullptr;
+    cudaEvent_t ev_z = nullptr, ev_side_out = nullptr, ev_da = nullptr, ev_side_gh = nullptr;
     bool own_stream = false;
     cudaEvent_t ev_in = nullptr, ev_fwd = nullptr, ev_out = nullptr;
     std::string err;
@@ -425,10 +428,21 @@ GemmEpilogue peer_epilogue(const meft_peer_out& po, bool grad_h, int64_t d) {
     return e;
 }
 
+// Small FFNs (the GEMMs cannot fill the machine, e.g. BASELINE config 1): the out GEMM runs on the context's side
+// stream beside dA, and grad_h beside the value-table grad-W GEMM. Dependencies: out and dA need z; grad_h needs
+// dA; the value grad-W GEMM's Adam epilogue rewrites the bf16 values out and dA read, so it waits for out; the
+// key grad-W GEMM rewrites the keys grad_h reads, so it waits for grad_h (the main stream then also covers all
+// side work). Same kernels on the same inputs: bit-identical to the serial order.
+struct SmallFfnStreams {
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_z = nullptr, ev_out = nullptr, ev_da = nullptr, ev_gh = nullptr;
+};
+
 void ffn_forward_impl(meft_ctx* ctx, meft_dtype dt, const void* h, const void* keys_s, const void* values_s,
                       int64_t T, int64_t d, int64_t s, int64_t ld_z, void* z, void* out, bool accumulate,
                       const RowGather& rg = RowGather(), const meft_peer_out* peer = nullptr,
-                      uint32_t* act_bits = nullptr, int64_t panel = 0, const int32_t* s_dev = nullptr) {
+                      uint32_t* act_bits = nullptr, int64_t panel = 0, const int32_t* s_dev = nullptr,
+                      const SmallFfnStreams* cc = nullptr) {
     cudaStream_t st = ctx->stream;
     if (dt == MEFT_F64) {
         double* outd = static_cast<double*>(out);
@@ -481,8 +495,15 @@ void ffn_forward_impl(meft_ctx* ctx, meft_dtype dt, const void* h, const void* k
     e2.extent_dim = 3;
     GemmOperand za{z, ld_z, false};
     za.panel_stride = panel;
-    gemm_bf16(st, T, d, s, knob_a(za, G_OUT), knob_b(kv_operand(ctx, values_s, d, true, rg, s), G_OUT),
+    cudaStream_t so = st;
+    if (cc) {  // out beside dA (SmallFfnStreams)
+        MEFT_CUDA_CHECK(cudaEventRecord(cc->ev_z, st));
+        MEFT_CUDA_CHECK(cudaStreamWaitEvent(cc->side, cc->ev_z, 0));
+        so = cc->side;
+    }
+    gemm_bf16(so, T, d, s, knob_a(za, G_OUT), knob_b(kv_operand(ctx, values_s, d, true, rg, s), G_OUT),
               knob_e(e2, G_OUT));
+    if (cc) MEFT_CUDA_CHECK(cudaEventRecord(cc->ev_out, so));
 }
 
 // stage_keys/stage_values non-null => weight grads are row-added into the store staging at S (fused scatter).
@@ -494,7 +515,7 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
                        const meft_peer_out* peer = nullptr, const GemmEpilogue* epi_values = nullptr,
                        const GemmEpilogue* epi_keys = nullptr, const uint32_t* act_bits = nullptr,
                        int64_t panel = 0, const void* gT = nullptr, const void* hT = nullptr,
-                       const int32_t* s_dev = nullptr) {
+                       const int32_t* s_dev = nullptr, const SmallFfnStreams* cc = nullptr) {
     cudaStream_t st = ctx->stream;
     if (dt == MEFT_F64) {
         const double* gd = static_cast<const double*>(g);
@@ -566,10 +587,17 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
         }
         e6.extent = s_dev;
         e6.extent_dim = 3;
-        gemm_bf16(st, T, d, s, knob_a(op(masked, ld_z, false), G_GH),
+        cudaStream_t sg = st;
+        if (cc) {  // grad_h beside the value grad-W GEMM (SmallFfnStreams)
+            MEFT_CUDA_CHECK(cudaEventRecord(cc->ev_da, st));
+            MEFT_CUDA_CHECK(cudaStreamWaitEvent(cc->side, cc->ev_da, 0));
+            sg = cc->side;
+        }
+        gemm_bf16(sg, T, d, s, knob_a(op(masked, ld_z, false), G_GH),
                   knob_b(kv_operand(ctx, keys_s, d, true, rg, s), G_GH), knob_e(e6, G_GH));
+        if (cc) MEFT_CUDA_CHECK(cudaEventRecord(cc->ev_gh, sg));
     }
-    if (grad_h_done) MEFT_CUDA_CHECK(cudaEventRecord(grad_h_done, st));
+    if (grad_h_done) MEFT_CUDA_CHECK(cudaEventRecord(grad_h_done, cc ? cc->side : st));
     GemmEpilogue e4;  // grad_values = act^T G   (M = s, N = d, K = T)
     if (S_rows) {
         e4.kind = EPI_ROWS_ADD_F32;
@@ -588,11 +616,13 @@ void ffn_backward_impl(meft_ctx* ctx, meft_dtype dt, const void* g, const void* 
         e.extent_dim = 1;
         return e;
     };
+    if (cc) MEFT_CUDA_CHECK(cudaStreamWaitEvent(st, cc->ev_out, 0));  // out has read the values this rewrites
     gemm_bf16(st, s, d, T, knob_a(op(z, ld_z, true), G_GWB), knob_b(gB, G_GWB),
               knob_e(rows_extent(epi_values ? *epi_values : e4), G_GWB));
     if (between) (*between)();  // e.g. consume grad_values before grad_keys reuses its buffer
     GemmEpilogue e5 = e4;  // grad_keys = masked^T h
     e5.c = S_rows ? stage_keys : grad_keys_s;
+    if (cc) MEFT_CUDA_CHECK(cudaStreamWaitEvent(st, cc->ev_gh, 0));  // grad_h has read the keys this rewrites
     gemm_bf16(st, s, d, T, knob_a(op(masked, ld_z, true), G_GWA), knob_b(hB, G_GWA),
               knob_e(rows_extent(epi_keys ? *epi_keys : e5), G_GWA));
 }
@@ -809,6 +839,9 @@ meft_status meft_ctx_create(int device, void* stream, meft_ctx** out) {
         MEFT_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
         MEFT_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_fwd, cudaEventDisableTiming));
         MEFT_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
+        MEFT_CUDA_CHECK(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
+        for (cudaEvent_t* e : {&c->ev_z, &c->ev_side_out, &c->ev_da, &c->ev_side_gh})
+            MEFT_CUDA_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
         MEFT_CUDA_CHECK(cudaMalloc(&c->dev_small, 128 * sizeof(int32_t)));
         MEFT_CUDA_CHECK(cudaMallocHost(&c->host_small, 64 * sizeof(int32_t)));
     });
@@ -830,6 +863,12 @@ void meft_ctx_destroy(meft_ctx* ctx) {
     if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
     if (ctx->ev_fwd) cudaEventDestroy(ctx->ev_fwd);
     if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
+    for (cudaEvent_t e : {ctx->ev_z, ctx->ev_side_out, ctx->ev_da, ctx->ev_side_gh})
+        if (e) cudaEventDestroy(e);
+    if (ctx->side_stream) {
+        cudaStreamSynchronize(ctx->side_stream);
+        cudaStreamDestroy(ctx->side_stream);
+    }
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -1909,6 +1948,17 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
     // sparse_ffn_pa: the frozen base FFN first (adapter.cpp:118-120), then the adapter term (122-126) added onto
     // it; every token against the whole union
     if (base && base->n == 0) base = nullptr;
+    // small fused-Adam steps: out / grad_h beside dA / the grad-W GEMMs (SmallFfnStreams; MEFT_SMALL_STREAMS=0 off)
+    static const bool small_streams_env = [] {
+        const char* v = std::getenv("MEFT_SMALL_STREAMS");
+        return !(v && v[0] == '0');
+    }();
+    const bool fused_adam = !s->pending[size_t(layer)] && adam_epilogue_enabled(ctx) && d % 32 == 0 && d <= 65536;
+    const bool small = ceil_div(T, int64_t(256)) * ceil_div(std::max<int64_t>(su, 1), int64_t(256)) < num_sms() / 2;
+    const SmallFfnStreams ccs{ctx->side_stream, ctx->ev_z, ctx->ev_side_out, ctx->ev_da, ctx->ev_side_gh};
+    const SmallFfnStreams* cc =
+        small_streams_env && fused_adam && small && !base && !peer && !s->train_router && ctx->side_stream ? &ccs
+                                                                                                          : nullptr;
     require(!(base && peer), MEFT_E_INVALID, "layer step: the base FFN runs on the token home, not with peer outputs");
     const int64_t ldn = base ? round_up(base->n, 8) : 0;
     uint16_t* base_pre = base ? static_cast<uint16_t*>(ctx->get("base_pre", size_t(T * ldn) * 2)) : nullptr;
@@ -1933,9 +1983,9 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
             gemm_bf16(st, T, d, base->n, GemmOperand{base_act, ldn, false}, GemmOperand{base->w_out, d, true}, e2);
         }
         ffn_forward_impl(ctx, MEFT_BF16, h, ks, vs, T, d, su, ld, act, outb, base != nullptr, rg, peer, act_bits,
-                         panel, su_dev);
+                         panel, su_dev, cc);
     }
-    if (fwd_done) MEFT_CUDA_CHECK(cudaEventRecord(fwd_done, st));
+    if (fwd_done) MEFT_CUDA_CHECK(cudaEventRecord(fwd_done, cc ? cc->side : st));  // out is done
     if (g_ready) MEFT_CUDA_CHECK(cudaStreamWaitEvent(st, g_ready, 0));
 
     const bool stats_valid = s->key_stats_valid[size_t(layer)] != 0;
@@ -2029,7 +2079,7 @@ static void ffn_update_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
             }
             ffn_backward_impl(ctx, MEFT_BF16, g, h, act, ks, vs, T, d, su, ld, masked, nullptr, nullptr, ghb,
                               base != nullptr, nullptr, nullptr, nullptr, rg, gh_done, nullptr, peer, &ev, &ek,
-                              act_bits, panel, gT, hT, su_dev);
+                              act_bits, panel, gT, hT, su_dev, cc);
         }
         train_router();
         if (stats) {
