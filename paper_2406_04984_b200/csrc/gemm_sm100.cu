@@ -848,10 +848,14 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
 //   warp 0 (both CTAs): TMA into the local ring, completion counted on the leader's full barrier
 //   warp 1 (leader)   : MMA issue; commits multicast to both CTAs' empty / tmem-full barriers
 //   warps 2-5 (both)  : epilogue of the local 128 rows; release the accumulator on the leader's tmem-empty
+// 4 x 32 KB stages. Measured against 6 (round 2, tools/r2_call45.sh / r2_call46.sh, alternating on one box): the
+// step 23.83-23.91 -> 23.47-23.48 ms, the co-running tiles' operand streams stay closer together (ncu: z / dA DRAM
+// 2.8-3.5 -> 1.6 GB, grad-W 14.1-14.5 -> 8.3-8.4 GB per launch) and the power-capped clock rises (1.28 -> 1.41 GHz
+// on the grad-W GEMMs); 3 stages starve the MMA (24.79 ms), 5 sit between.
 #ifndef MEFT_P_STAGES
-#define MEFT_P_STAGES 6
+#define MEFT_P_STAGES 4
 #endif
-constexpr int P_STAGES = MEFT_P_STAGES;  // 6 x 32 KB stages (A/B knob for tuning)
+constexpr int P_STAGES = MEFT_P_STAGES;
 constexpr int P_A_BYTES = 128 * BK * 2;
 constexpr int P_B_BYTES = 128 * BK * 2;
 constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
