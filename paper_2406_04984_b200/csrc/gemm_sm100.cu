@@ -1129,6 +1129,9 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 // 2-D bf16 tensor map: `inner` contiguous elements per row, `outer` rows of pitch ld elements.
+#ifndef MEFT_L2_PROMOTION  // A/B knob (tools/ab_variants.sh)
+#define MEFT_L2_PROMOTION CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
 CUtensorMap make_map(const void* base, int64_t inner, int64_t outer, int64_t ld, uint32_t box_inner,
                      uint32_t box_outer) {
     CUtensorMap m;
@@ -1137,8 +1140,8 @@ CUtensorMap make_map(const void* base, int64_t inner, int64_t outer, int64_t ld,
     cuuint32_t box[2] = {box_inner, box_outer};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
-                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, MEFT_L2_PROMOTION,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw MeftError(6, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
     return m;
 }
@@ -1146,7 +1149,13 @@ CUtensorMap make_map(const void* base, int64_t inner, int64_t outer, int64_t ld,
 // SMs the persistent GEMMs may occupy. A communication-overlapped caller reserves a few for concurrently running
 // NCCL kernels, which otherwise only get an SM once a whole chain of persistent GEMMs has drained.
 std::atomic<int> g_reserved_sms{0};
-int gemm_sms() { return std::max(2, num_sms() - g_reserved_sms.load(std::memory_order_relaxed)); }
+int gemm_sms() {
+    static const int env_reserve = [] {  // MEFT_GEMM_SM_RESERVE: A/B knob (SMs left idle by every persistent GEMM)
+        const char* v = std::getenv("MEFT_GEMM_SM_RESERVE");
+        return v ? std::max(0, std::atoi(v)) : 0;
+    }();
+    return std::max(2, num_sms() - std::max(env_reserve, g_reserved_sms.load(std::memory_order_relaxed)));
+}
 
 template <bool A_MN, bool B_MN>
 void launch(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tg, const KArgs& args,
