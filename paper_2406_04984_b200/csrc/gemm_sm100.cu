@@ -21,7 +21,10 @@ namespace {
 constexpr int BM = 128;
 constexpr int BN = 256;
 constexpr int BK = 64;  // one 128-byte swizzle atom of bf16
-constexpr int STAGES = 4;
+#ifndef MEFT_STAGES  // 1-CTA kernel ring depth (A/B knob)
+#define MEFT_STAGES 4
+#endif
+constexpr int STAGES = MEFT_STAGES;
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int B_BYTES = BN * BK * 2;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
