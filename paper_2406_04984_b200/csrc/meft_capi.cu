@@ -84,7 +84,7 @@ struct meft_ctx {
     cudaStream_t side_stream = nullptr;
     cudaEvent_t ev_z = nullptr, ev_side_out = nullptr, ev_da = nullptr, ev_side_gh = nullptr;
     bool own_stream = false;
-    cudaEvent_t ev_in = nullptr, ev_fwd = nullptr, ev_out = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_fwd = nullptr, ev_out = nullptr, ev_h_in = nullptr;
     std::string err;
     int64_t err_index = -1;
     int32_t* dev_small = nullptr;   // 128 device ints (validation flags, counts; [32, 96): sharded plan counts)
@@ -839,6 +839,7 @@ meft_status meft_ctx_create(int device, void* stream, meft_ctx** out) {
         MEFT_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
         MEFT_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_fwd, cudaEventDisableTiming));
         MEFT_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
+        MEFT_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_h_in, cudaEventDisableTiming));
         MEFT_CUDA_CHECK(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
         for (cudaEvent_t* e : {&c->ev_z, &c->ev_side_out, &c->ev_da, &c->ev_side_gh})
             MEFT_CUDA_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
@@ -863,6 +864,7 @@ void meft_ctx_destroy(meft_ctx* ctx) {
     if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
     if (ctx->ev_fwd) cudaEventDestroy(ctx->ev_fwd);
     if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
+    if (ctx->ev_h_in) cudaEventDestroy(ctx->ev_h_in);
     for (cudaEvent_t e : {ctx->ev_z, ctx->ev_side_out, ctx->ev_da, ctx->ev_side_gh})
         if (e) cudaEventDestroy(e);
     if (ctx->side_stream) {
@@ -2293,8 +2295,18 @@ meft_status meft_layer_step_host(meft_ctx* ctx, meft_store* s, int64_t layer, co
         void* gd = ctx->get("g_in", in_bytes);
         float* od = static_cast<float*>(ctx->get("out_dev", out_bytes));
         float* ghd = static_cast<float*>(ctx->get("gh_dev", out_bytes));
-        // h on the compute stream; grad_out on the copy stream, overlapping selection + forward
+        // h on the compute stream; grad_out on the copy stream, overlapping selection + forward. grad_out starts
+        // after h has arrived (MEFT_H2D_SERIAL=0: at once), so h -- on the critical path of the selection -- gets
+        // the whole host link instead of sharing it with a transfer needed only by the backward.
+        static const bool h_first = [] {
+            const char* v = std::getenv("MEFT_H2D_SERIAL");
+            return !(v && v[0] == '0');
+        }();
         MEFT_CUDA_CHECK(cudaMemcpyAsync(hd, h_host, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+        if (h_first) {
+            MEFT_CUDA_CHECK(cudaEventRecord(ctx->ev_h_in, ctx->stream));
+            MEFT_CUDA_CHECK(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_h_in, 0));
+        }
         MEFT_CUDA_CHECK(cudaMemcpyAsync(gd, g_host, in_bytes, cudaMemcpyHostToDevice, ctx->copy_stream));
         MEFT_CUDA_CHECK(cudaEventRecord(ctx->ev_in, ctx->copy_stream));
         // The copy stream carries both results back while compute continues: out after the forward, grad_h as soon
