@@ -134,13 +134,17 @@ meft_status meft_ctx_set_adam(meft_ctx* ctx, int mode);
  * grad_h once the step is done (one extra sync) and return MEFT_E_NONFINITE ("... non-finite ...") on NaN / Inf.
  * Default off: the scan costs a sync per step. */
 meft_status meft_ctx_set_check_finite(meft_ctx* ctx, int enable);
-/* Host synchronisation of the fused layer step. enable = 1 (default): meft_layer_step reads the union size back
- * once, mid-step, and sizes the FFN GEMMs to it. enable = 0: the step never waits for the device -- the six FFN
+/* Host synchronisation of the fused layer step. enable = 1: meft_layer_step reads the union size back once,
+ * mid-step, and sizes the FFN GEMMs to it. enable = 0: the step never waits for the device -- the six FFN
  * GEMMs are launched for the capacity (M pairs) and read |S| from device memory before their first tile
  * (GemmEpilogue::extent), so consecutive layer steps enqueue back to back and a step can be captured into a CUDA
  * graph (meft_graph_*). Bit-identical results. It applies to the fused-Adam step (no pending scatter_grads, no base
  * FFN, no router training, check_finite off, M <= 65536, d % 32 == 0); any other step takes the synchronising
- * path (an error while capturing). A non-NULL info then costs one synchronisation at the END of the step. */
+ * path (an error while capturing). A non-NULL info then costs one synchronisation at the END of the step.
+ * MEFT_HOST_SYNC_AUTO (the default; environment MEFT_HOST_SYNC=0|1|auto for new contexts): the enqueue-only step
+ * when the union is expected dense (T * take / M >= ~9.5, capacity ~ |S|; the LLaMA-shape layer), the read-back
+ * otherwise (a sparse union would launch for far more than it selects). Capture needs 0. */
+#define MEFT_HOST_SYNC_AUTO (-1)
 meft_status meft_ctx_set_host_sync(meft_ctx* ctx, int enable);
 
 /* CUDA graphs over the context stream. meft_graph_begin starts capturing the context stream; the calls that follow
@@ -481,7 +485,9 @@ typedef struct meft_base_ffn {
  * (trainer.cpp:220,270,283,525): meft_ffn (ke_select -> fetch -> sparse_ffn_pa) -> sparse_backward ->
  * scatter_grads -> sparse_adam_update. h and grad_out are bf16 [T x d] on device; out and grad_h are f32
  * [T x d] (either may be NULL). Optional outputs per_token [T x take] / union_idx [M] (device int32) may be
- * NULL. Synchronises once (to size the union) unless host sync is off (meft_ctx_set_host_sync).
+ * NULL. With host sync on (meft_ctx_set_host_sync) it synchronises once, mid-step, to size the union; off, it does
+ * not (the FFN GEMMs read the union size on the device) and a non-NULL info costs one sync at the end; the default
+ * (MEFT_HOST_SYNC_AUTO) takes the second for dense unions.
  */
 meft_status meft_layer_step(meft_ctx* ctx, meft_store* store, int64_t layer, const void* h, const void* grad_out,
                             int64_t T, int64_t kk, int64_t k, double beta1, double beta2, double eps, double lr,

@@ -101,7 +101,9 @@ struct meft_ctx {
     int adam_mode = -1;  // MEFT_ADAM_*; -1 = not set (environment MEFT_ADAM_EPILOGUE, else EPILOGUE)
     int gather_mode = -1;  // MEFT_GATHER_*; -1 = not set (environment MEFT_GATHER, else AUTO)
     bool check_finite = false;  // fused step: raise MEFT_E_NONFINITE like check_finite (kernels.cpp:7-13)
-    bool host_sync = true;      // meft_ctx_set_host_sync: false = device-sized FFN GEMMs, no mid-step read-back
+    // meft_ctx_set_host_sync: 1 = read |S| back mid-step, 0 = device-sized FFN GEMMs (no read-back), -1 = AUTO (the
+    // default; environment MEFT_HOST_SYNC=0|1|auto for new contexts): device-sized when the union is expected dense
+    int host_sync = MEFT_HOST_SYNC_AUTO;
 
     bool capturing() const {  // the context stream is being captured into a CUDA graph
         cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -845,6 +847,8 @@ meft_status meft_ctx_create(int device, void* stream, meft_ctx** out) {
             MEFT_CUDA_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
         MEFT_CUDA_CHECK(cudaMalloc(&c->dev_small, 128 * sizeof(int32_t)));
         MEFT_CUDA_CHECK(cudaMallocHost(&c->host_small, 64 * sizeof(int32_t)));
+        if (const char* v = std::getenv("MEFT_HOST_SYNC"))  // the default of new contexts
+            c->host_sync = v[0] == '0' ? 0 : v[0] == '1' ? 1 : MEFT_HOST_SYNC_AUTO;
     });
     if (st != MEFT_OK) return st;
     *out = c.release();
@@ -914,7 +918,9 @@ meft_status meft_ctx_set_check_finite(meft_ctx* ctx, int enable) {
 meft_status meft_ctx_set_host_sync(meft_ctx* ctx, int enable) {
     return guarded(ctx, [&] {
         require_ctx(ctx);
-        ctx->host_sync = enable != 0;
+        require(enable == 0 || enable == 1 || enable == MEFT_HOST_SYNC_AUTO, MEFT_E_INVALID,
+                "set_host_sync: 0, 1 or MEFT_HOST_SYNC_AUTO");
+        ctx->host_sync = enable;
     });
 }
 
@@ -1767,19 +1773,22 @@ static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
     // Enqueue-only step (host sync off): the FFN GEMMs are launched for the capacity M and read |S| from usize on
     // the device, so nothing here waits for the selection; otherwise |S| (and the union's hole count, which picks
     // the gather) is read back once and the GEMMs are sized exactly. Bit-identical either way.
-    const bool device_sized = !ctx->host_sync && !s->pending[size_t(layer)] && !s->train_router &&
-                              !(base && base->n > 0) && !ctx->check_finite && adam_epilogue_enabled(ctx) &&
-                              d % 32 == 0 && M <= kGemmPanel;
+    // The gather of a device-sized step is chosen without the union, from the hole count a union of T * take
+    // uniform draws over M pairs would have, M p (1 - p) with p = exp(-T take / M) (AUTO's rule then takes TMA from
+    // T take / M >= ~9.5: cfg2, 16; cfg1, 2 -> the kernel). AUTO host sync takes the device-sized step exactly when
+    // that estimate calls the union dense (capacity ~ |S|: cfg2 +1% measured); a sparse union keeps the read-back
+    // (cfg1: capacity-sized launches and the padded gather cost ~10% there).
+    const double p_miss = std::exp(-double(T) * double(take) / double(M));
+    const int64_t holes_est = int64_t(std::ceil(double(M) * p_miss * (1.0 - p_miss)));
+    const bool dense_expected = holes_est * 12800 <= M;
+    const bool device_sized = (ctx->host_sync == 0 || (ctx->host_sync == MEFT_HOST_SYNC_AUTO && dense_expected)) &&
+                              !s->pending[size_t(layer)] && !s->train_router && !(base && base->n > 0) &&
+                              !ctx->check_finite && adam_epilogue_enabled(ctx) && d % 32 == 0 && M <= kGemmPanel;
     int64_t su = -1;
     if (device_sized && info && !defer_info)
         require(!ctx->capturing(), MEFT_E_INVALID,
                 "layer_step: pass a NULL meft_step_info while capturing a graph (it is read back at the step's end)");
     if (device_sized) {
-        // The gather (TMA from the tables vs a gather kernel, bit-identical) is chosen without the union: from the
-        // hole count a union of T * take uniform draws over M pairs would have, M p (1 - p) with p = exp(-T take / M)
-        // (AUTO's rule then takes TMA from T take / M >= ~9.5: cfg2, 16; cfg1, 2 -> the kernel)
-        const double p = std::exp(-double(T) * double(take) / double(M));
-        const int64_t holes_est = int64_t(std::ceil(double(M) * p * (1.0 - p)));
         ffn_update_impl(ctx, s, layer, h, g, T, uni, M, holes_est, b1, b2, eps, lr, out, grad_h, g_ready, fwd_done,
                         gh_done, nullptr, kk_eff, nullptr, nullptr, usize);
         if (info) {  // the step is fully enqueued: read |S| and the selection counters at its end

@@ -92,10 +92,12 @@ class Context:
         """Fused layer steps raise the reference's 'non-finite' error on NaN / Inf in out or grad_h."""
         self.check(lib().meft_ctx_set_check_finite(self.h, int(on)))
 
-    def set_host_sync(self, on: bool):
+    def set_host_sync(self, on):
         """on=False: fused layer steps never wait for the device (the FFN GEMMs read |S| on the device), so steps
-        enqueue back to back and can be captured (graph()); bit-identical results (meft_ctx_set_host_sync)."""
-        self.check(lib().meft_ctx_set_host_sync(self.h, int(on)))
+        enqueue back to back and can be captured (graph()); on=True reads |S| back mid-step and sizes the GEMMs on
+        the host; on=None (the default, MEFT_HOST_SYNC_AUTO): the first for dense unions, the second otherwise.
+        Bit-identical results (meft_ctx_set_host_sync)."""
+        self.check(lib().meft_ctx_set_host_sync(self.h, -1 if on is None else int(bool(on))))
 
     def graph(self):
         """Capture the enqueue-only calls made inside `with ctx.graph() as g:` into a CUDA graph; g.replay()

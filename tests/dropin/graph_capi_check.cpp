@@ -1,5 +1,5 @@
 // A C++ caller of the C ABI alone (no Python, no torch): the enqueue-only layer step (meft_ctx_set_host_sync(ctx,
-// 0)) of a two-layer store captured into a CUDA graph (meft_graph_*) and replayed, against the default synchronising
+// 0)) of a two-layer store captured into a CUDA graph (meft_graph_*) and replayed, against the synchronising (host sync on)
 // meft_layer_step on a twin store, bit for bit -- out, grad_h, the selection and every table -- over three
 // iterations with fresh inputs copied into the captured buffers. The sequence INTEGRATION.md §2 shows for a trainer
 // that launches a whole iteration's adapter layers as one graph (trainer.cpp:523-526's per-layer loop). Built by
@@ -49,10 +49,11 @@ void* dev_alloc(meft_ctx* ctx, size_t bytes) {
 int main() {
     const int64_t d = 1024, M = 16384, N = 64, K = 32, kk = 4, T = 300, L = 2;  // a sparse union: kernel gather
     const double lr = 1e-3, b1 = 0.9, b2 = 0.999, eps = 1e-8;
-    meft_ctx* ref = nullptr;  // host sync on (the default), legacy default stream
+    meft_ctx* ref = nullptr;  // host sync on, legacy default stream
     meft_ctx* ctx = nullptr;  // host sync off, its own (capturable) stream
     ck(meft_ctx_create(0, nullptr, &ref), nullptr, "ctx_create");
     ck(meft_ctx_create(0, MEFT_OWN_STREAM, &ctx), nullptr, "ctx_create");
+    ck(meft_ctx_set_host_sync(ref, 1), ref, "set_host_sync");  // the synchronising reference step
     ck(meft_ctx_set_host_sync(ctx, 0), ctx, "set_host_sync");
     meft_store* st[2] = {nullptr, nullptr};  // [0] reference steps on `ref`, [1] the graph's store on `ctx`
     meft_ctx* owner[2] = {ref, ctx};

@@ -46,6 +46,7 @@ def _assert_tables_equal(a, b, layers=1):
 @pytest.fixture(scope="module")
 def ctxs():
     sync, free = G.Context(0), G.Context(0)
+    sync.set_host_sync(True)
     free.set_host_sync(False)
     yield sync, free
     free.close()
@@ -57,6 +58,7 @@ def side():
     """Contexts on a non-default stream (the legacy default stream cannot be captured): (host sync on, off)."""
     s = torch.cuda.Stream()
     sync, free = G.Context(0, stream=s), G.Context(0, stream=s)
+    sync.set_host_sync(True)
     free.set_host_sync(False)
     yield sync, free
     free.close()
