@@ -142,8 +142,9 @@ meft_status meft_ctx_set_check_finite(meft_ctx* ctx, int enable);
  * FFN, no router training, check_finite off, M <= 65536, d % 32 == 0); any other step takes the synchronising
  * path (an error while capturing). A non-NULL info then costs one synchronisation at the END of the step.
  * MEFT_HOST_SYNC_AUTO (the default; environment MEFT_HOST_SYNC=0|1|auto for new contexts): the enqueue-only step
- * when the union is expected dense (T * take / M >= ~9.5, capacity ~ |S|; the LLaMA-shape layer), the read-back
- * otherwise (a sparse union would launch for far more than it selects). Capture needs 0. */
+ * for a layer whose last read-back union was dense (one TMA run up to a hole per 12,800 rows and >= 3/4 of M: the
+ * capacity launch is ~|S|; the LLaMA-shape layer), re-read every 64 steps; the read-back otherwise (a sparse union
+ * would launch for far more than it selects). Capture needs 0 (or an AUTO layer already known dense). */
 #define MEFT_HOST_SYNC_AUTO (-1)
 meft_status meft_ctx_set_host_sync(meft_ctx* ctx, int enable);
 

@@ -234,6 +234,10 @@ struct meft_store {
     // per layer: staging may hold gradients (scatter_grads / caller access) that the next Adam must consume.
     // While clear, staging is all zero and the fused layer step bypasses it entirely.
     std::vector<char> pending;
+    // host-sync AUTO: per layer, whether the last read-back union was dense (1) or not (0), -1 before the first;
+    // and the steps since (AUTO re-reads |S| every kUnionRecheck steps, so a drifting union is noticed)
+    std::vector<signed char> union_dense;
+    std::vector<int> since_check;
     bool train_router = false;
 };
 
@@ -1476,6 +1480,8 @@ meft_status meft_store_create(meft_ctx* ctx, int64_t layers, int64_t d, int64_t 
             s->L.push_back(L);
             s->key_stats_valid.push_back(0);
             s->pending.push_back(0);
+            s->union_dense.push_back(-1);
+            s->since_check.push_back(0);
         }
         MEFT_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
         if (!new_guards.empty()) {  // the gaps are filled now: other threads' checks may read them
@@ -1773,22 +1779,28 @@ static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
     // Enqueue-only step (host sync off): the FFN GEMMs are launched for the capacity M and read |S| from usize on
     // the device, so nothing here waits for the selection; otherwise |S| (and the union's hole count, which picks
     // the gather) is read back once and the GEMMs are sized exactly. Bit-identical either way.
-    // The gather of a device-sized step is chosen without the union, from the hole count a union of T * take
-    // uniform draws over M pairs would have, M p (1 - p) with p = exp(-T take / M) (AUTO's rule then takes TMA from
-    // T take / M >= ~9.5: cfg2, 16; cfg1, 2 -> the kernel). AUTO host sync takes the device-sized step exactly when
-    // that estimate calls the union dense (capacity ~ |S|: cfg2 +1% measured); a sparse union keeps the read-back
-    // (cfg1: capacity-sized launches and the padded gather cost ~10% there).
+    // AUTO host sync takes the device-sized step for a layer whose last read-back union was dense (one TMA run up to
+    // a hole per 12,800 rows and at least 3/4 of M, so the capacity launch is ~|S|: cfg2, cfg3), re-reading |S| every
+    // kUnionRecheck steps; any other union keeps the read-back (cfg1: capacity-sized launches and the padded gather
+    // cost ~10% there). A forced device-sized step (host sync 0) with no dense read-back yet picks its gather from
+    // the hole count of T * take uniform draws over M, M p (1 - p) with p = exp(-T take / M) (TMA from T take / M
+    // >= ~9.5).
+    constexpr int kUnionRecheck = 64;
+    const size_t li = size_t(layer);
+    const bool known_dense = s->union_dense[li] == 1;
+    const bool recheck = !ctx->capturing() && (s->union_dense[li] < 0 || s->since_check[li] >= kUnionRecheck);
     const double p_miss = std::exp(-double(T) * double(take) / double(M));
-    const int64_t holes_est = int64_t(std::ceil(double(M) * p_miss * (1.0 - p_miss)));
-    const bool dense_expected = holes_est * 12800 <= M;
-    const bool device_sized = (ctx->host_sync == 0 || (ctx->host_sync == MEFT_HOST_SYNC_AUTO && dense_expected)) &&
-                              !s->pending[size_t(layer)] && !s->train_router && !(base && base->n > 0) &&
-                              !ctx->check_finite && adam_epilogue_enabled(ctx) && d % 32 == 0 && M <= kGemmPanel;
+    const int64_t holes_est = known_dense ? 0 : int64_t(std::ceil(double(M) * p_miss * (1.0 - p_miss)));
+    const bool device_sized = (ctx->host_sync == 0 || (ctx->host_sync == MEFT_HOST_SYNC_AUTO && known_dense &&
+                                                       !recheck)) &&
+                              !s->pending[li] && !s->train_router && !(base && base->n > 0) && !ctx->check_finite &&
+                              adam_epilogue_enabled(ctx) && d % 32 == 0 && M <= kGemmPanel;
     int64_t su = -1;
     if (device_sized && info && !defer_info)
         require(!ctx->capturing(), MEFT_E_INVALID,
                 "layer_step: pass a NULL meft_step_info while capturing a graph (it is read back at the step's end)");
     if (device_sized) {
+        ++s->since_check[li];
         ffn_update_impl(ctx, s, layer, h, g, T, uni, M, holes_est, b1, b2, eps, lr, out, grad_h, g_ready, fwd_done,
                         gh_done, nullptr, kk_eff, nullptr, nullptr, usize);
         if (info) {  // the step is fully enqueued: read |S| and the selection counters at its end
@@ -1803,6 +1815,9 @@ static void layer_step_impl(meft_ctx* ctx, meft_store* s, int64_t layer, const v
         MEFT_CUDA_CHECK(cudaMemcpyAsync(ctx->host_small + 4, usize, 16, cudaMemcpyDeviceToHost, st));
         MEFT_CUDA_CHECK(cudaStreamSynchronize(st));
         su = ctx->host_small[4];
+        const int64_t holes = ctx->host_small[7];
+        s->union_dense[li] = (holes >= 0 && holes * 12800 <= su && 4 * su >= 3 * M) ? 1 : 0;
+        s->since_check[li] = 0;
         ffn_update_impl(ctx, s, layer, h, g, T, uni, su, ctx->host_small[7], b1, b2, eps, lr, out, grad_h, g_ready,
                         fwd_done, gh_done, s->train_router ? tau : nullptr, kk_eff, nullptr, base);
     }

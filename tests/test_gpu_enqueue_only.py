@@ -287,3 +287,39 @@ def test_host_buffer_step_with_host_sync_off(ctxs):
     _assert_tables_equal(a, b)
     a.close()
     b.close()
+
+
+def test_auto_host_sync_follows_the_read_back_union(ctx):
+    """MEFT_HOST_SYNC_AUTO (the default): the first step of a layer reads |S| back; a dense union (one run, >= 3/4
+    of M) makes the next steps device-sized -- a capture then succeeds -- while a sparse one keeps the read-back (a
+    capture is refused). Results equal the always-synchronising step either way."""
+    s = torch.cuda.Stream()
+    auto = G.Context(0, stream=s)  # default mode
+    sync = G.Context(0, stream=s)
+    sync.set_host_sync(True)
+    for shape, dense in (((512, 16384, 64, 128, 2048), True), ((512, 4096, 64, 32, 256), False)):
+        d, M, N, K, T = shape
+        a, b = _store(auto, d, M, N, 23), _store(sync, d, M, N, 23)
+        h, g = _inputs(T, d, 80)
+        torch.cuda.synchronize()
+        for st in (a, b):
+            for _ in range(2):
+                st.layer_step(0, h, g, 4, K, 1e-3, want_info=False)
+        torch.cuda.synchronize()
+        if dense:
+            with auto.graph() as graph:  # device-sized now: capturable
+                a.layer_step(0, h, g, 4, K, 1e-3, want_info=False)
+            torch.cuda.synchronize()
+            graph.replay()
+            b.layer_step(0, h, g, 4, K, 1e-3, want_info=False)
+            graph.close()
+        else:
+            with pytest.raises(G.MeftError, match="cannot be captured"):
+                with auto.graph():
+                    a.layer_step(0, h, g, 4, K, 1e-3, want_info=False)
+        torch.cuda.synchronize()
+        _assert_tables_equal(a, b)
+        a.close()
+        b.close()
+    auto.close()
+    sync.close()
