@@ -294,7 +294,8 @@ def test_auto_host_sync_follows_the_read_back_union(ctx):
     of M) makes the next steps device-sized -- a capture then succeeds -- while a sparse one keeps the read-back (a
     capture is refused). Results equal the always-synchronising step either way."""
     s = torch.cuda.Stream()
-    auto = G.Context(0, stream=s)  # default mode
+    auto = G.Context(0, stream=s)
+    auto.set_host_sync(None)  # MEFT_HOST_SYNC_AUTO (the default unless the environment overrides it)
     sync = G.Context(0, stream=s)
     sync.set_host_sync(True)
     for shape, dense in (((512, 16384, 64, 128, 2048), True), ((512, 4096, 64, 32, 256), False)):
